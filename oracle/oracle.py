@@ -1,0 +1,331 @@
+"""TEST INFRASTRUCTURE ONLY — ctypes access to the checkers.
+
+Two CPU checkers live here, both built by ``oracle/Makefile``:
+
+* ``Ref``    — the UNMODIFIED reference mini-app (``/root/reference/proj``)
+  compiled in place into ``oracle/_ref/libtmref.so`` with the extern "C"
+  shim ``oracle/ref_capi.cpp``. This is ground truth.
+* ``Oracle`` — our plain-C restatement ``oracle/tm_oracle.c``
+  (``oracle/_ref/liboracle.so``), pinned bitwise against ``Ref`` by
+  ``tests/test_oracle_pin.py``.
+
+Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s
+cpu_baseline / ``--impl reference`` legs may import this module. The
+product (``paper_2412_15518_b200``) never does.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+REF_DIR = os.path.join(HERE, "_ref")
+
+_dp = C.POINTER(C.c_double)
+_u64p = C.POINTER(C.c_uint64)
+_i64p = C.POINTER(C.c_int64)
+_ip = C.POINTER(C.c_int)
+
+
+def dptr(a: np.ndarray):
+    assert a.dtype == np.float64 and a.flags["C_CONTIGUOUS"]
+    return a.ctypes.data_as(_dp)
+
+
+def u64ptr(a: np.ndarray):
+    assert a.dtype == np.uint64 and a.flags["C_CONTIGUOUS"]
+    return a.ctypes.data_as(_u64p)
+
+
+def build(quiet: bool = True) -> None:
+    """Build the checkers (needs /root/reference for the Ref part)."""
+    import subprocess
+
+    targets = ["oracle"]
+    if os.path.isdir("/root/reference/proj"):
+        targets.append("ref")
+    subprocess.run(["make", "-s", "-C", HERE, *targets], check=True,
+                   stdout=subprocess.DEVNULL if quiet else None)
+
+
+def ref_available() -> bool:
+    return os.path.exists(os.path.join(REF_DIR, "libtmref.so"))
+
+
+def oracle_available() -> bool:
+    return os.path.exists(os.path.join(REF_DIR, "liboracle.so"))
+
+
+class _Lib:
+    def __init__(self, name: str):
+        path = os.path.join(REF_DIR, name)
+        if not os.path.exists(path):
+            raise FileNotFoundError(f"{path} not built (run make -C oracle)")
+        self.lib = C.CDLL(path)
+
+
+class Ref(_Lib):
+    """The reference's own code through oracle/ref_capi.cpp."""
+
+    def __init__(self):
+        super().__init__("libtmref.so")
+        L = self.lib
+        L.tmref_stage_fused.argtypes = [_dp, _dp, C.c_size_t, C.c_size_t, C.c_size_t,
+                                        C.c_int, C.c_int, C.c_int, C.c_uint, C.c_char_p,
+                                        C.c_size_t]
+        L.tmref_in_slice.restype = C.c_size_t
+        L.tmref_in_slice.argtypes = [C.c_int] * 3
+        L.tmref_out_slice.restype = C.c_size_t
+        L.tmref_out_slice.argtypes = [C.c_int] * 3
+        L.tmref_encode_header.argtypes = [C.c_int] + [C.c_double] * 6 + [_dp]
+        L.tmref_max_wavespeed.restype = C.c_double
+        L.tmref_max_wavespeed.argtypes = [_dp, C.c_int, C.c_int, C.c_int, _dp]
+        L.tmref_rk3_combine.restype = C.c_double
+        L.tmref_rk3_combine.argtypes = [C.c_int, C.c_double, C.c_double]
+        for f in ("tmref_minmod_scalar", "tmref_minmod_lane"):
+            getattr(L, f).restype = C.c_double
+            getattr(L, f).argtypes = [C.c_double, C.c_double]
+        L.tmref_reconstruct_face.argtypes = [C.c_double] * 4 + [_dp]
+        L.tmref_rusanov_euler.argtypes = [_dp, _dp, C.c_double, C.c_int, _dp]
+        L.tmref_rusanov_scalar.restype = C.c_double
+        L.tmref_rusanov_scalar.argtypes = [C.c_double] * 3
+        L.tmref_morton_encode.argtypes = [C.c_int, C.c_uint64, C.c_uint64, C.c_uint64, _u64p]
+        L.tmref_morton_decode.argtypes = [C.c_int, C.c_uint64, _u64p]
+        L.tmref_morton_dfs_rank.restype = C.c_uint64
+        L.tmref_morton_dfs_rank.argtypes = [C.c_int, C.c_uint64]
+        L.tmref_partition_leaves.argtypes = [_u64p, C.c_size_t, C.c_int, _ip]
+        L.tmref_prolong_cell.argtypes = [C.c_double] * 7 + [_dp]
+        L.tmref_tree_create.restype = C.c_void_p
+        L.tmref_tree_create.argtypes = [C.c_int] * 4 + [_ip, _ip]
+        L.tmref_tree_destroy.argtypes = [C.c_void_p]
+        L.tmref_tree_refine.argtypes = [C.c_void_p, C.c_uint64]
+        L.tmref_tree_coarsen.argtypes = [C.c_void_p, C.c_uint64]
+        L.tmref_tree_leaves.restype = C.c_size_t
+        L.tmref_tree_leaves.argtypes = [C.c_void_p, _u64p, C.c_size_t]
+        L.tmref_tree_grid.restype = _dp
+        L.tmref_tree_grid.argtypes = [C.c_void_p, C.c_uint64]
+        L.tmref_tree_fill_ghosts.argtypes = [C.c_void_p]
+        L.tmref_tree_flag.argtypes = [C.c_void_p, C.c_uint64, C.c_double]
+        L.tmref_tree_balanced.argtypes = [C.c_void_p]
+        L.tmref_tree_cell_size.restype = C.c_double
+        L.tmref_tree_cell_size.argtypes = [C.c_void_p, C.c_int]
+        L.tmref_tree_cell_center.argtypes = [C.c_void_p, C.c_uint64, C.c_int, C.c_int, C.c_int, _dp]
+        L.tmref_tree_face_neighbor.argtypes = [C.c_void_p, C.c_uint64, C.c_int, C.c_int, _u64p, _ip]
+        L.tmref_tree_plan.restype = C.c_size_t
+        L.tmref_tree_plan.argtypes = [C.c_void_p, C.c_int, _i64p, C.c_size_t]
+        L.tmref_hydro_step.argtypes = [C.c_void_p, C.c_double, C.c_double, C.c_uint, C.c_uint,
+                                       C.c_size_t, _dp, _dp, C.c_char_p, C.c_size_t]
+        L.tmref_stage_aggregated.restype = C.c_double
+        L.tmref_stage_aggregated.argtypes = [_dp, C.c_size_t, C.c_int, C.c_int, C.c_int,
+                                             C.c_uint, C.c_uint, C.c_size_t, _dp]
+
+    # -- hydro
+    def stage_fused(self, packed_in, count, edge=8, ghost=2, vars=5, lane_width=1):
+        L = self.lib
+        ins, outs = L.tmref_in_slice(edge, ghost, vars), L.tmref_out_slice(edge, ghost, vars)
+        out = np.zeros(count * outs)
+        err = C.create_string_buffer(256)
+        rc = L.tmref_stage_fused(dptr(packed_in), dptr(out), ins, outs, count, edge, ghost,
+                                 vars, lane_width, err, 256)
+        return rc, out, err.value.decode()
+
+    def encode_header(self, mode, dx, dt, gamma=1.4, advect=(1.0, 0.0, 0.0)):
+        h = np.zeros(8)
+        self.lib.tmref_encode_header(mode, dx, dt, gamma, *advect, dptr(h))
+        return h
+
+    def max_wavespeed(self, header, ghosted, edge=8, ghost=2, vars=5):
+        return self.lib.tmref_max_wavespeed(dptr(header), edge, ghost, vars,
+                                            dptr(ghosted) if ghosted is not None else None)
+
+    # -- tree
+    def tree(self, edge=8, ghost=2, vars=5, max_level=10, root_dims=(1, 1, 1), bc=(0, 0, 0)):
+        return RefTree(self, edge, ghost, vars, max_level, root_dims, bc)
+
+
+class RefTree:
+    def __init__(self, ref: Ref, edge, ghost, vars, max_level, root_dims, bc):
+        self.ref, self.L = ref, ref.lib
+        self.edge, self.ghost, self.vars = edge, ghost, vars
+        self.stride = edge + 2 * ghost
+        rd = (C.c_int * 3)(*root_dims)
+        b = (C.c_int * 3)(*bc)
+        self.h = self.L.tmref_tree_create(edge, ghost, vars, max_level, rd, b)
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            self.L.tmref_tree_destroy(self.h)
+            self.h = None
+
+    def refine(self, packed: int) -> None:
+        if self.L.tmref_tree_refine(self.h, packed) != 0:
+            raise RuntimeError("reference refine failed")
+
+    def leaves(self) -> np.ndarray:
+        n = self.L.tmref_tree_leaves(self.h, None, 0)
+        out = np.zeros(n, dtype=np.uint64)
+        self.L.tmref_tree_leaves(self.h, u64ptr(out), n)
+        return out
+
+    def grid(self, packed: int) -> np.ndarray:
+        p = self.L.tmref_tree_grid(self.h, packed)
+        S = self.stride
+        n = self.vars * S * S * S
+        return np.ctypeslib.as_array(p, shape=(n,))
+
+    def fill_ghosts(self) -> None:
+        self.L.tmref_tree_fill_ghosts(self.h)
+
+    def flag(self, packed: int, theta: float) -> bool:
+        return bool(self.L.tmref_tree_flag(self.h, packed, theta))
+
+    def balanced(self) -> bool:
+        return bool(self.L.tmref_tree_balanced(self.h))
+
+    def cell_size(self, level: int) -> float:
+        return self.L.tmref_tree_cell_size(self.h, level)
+
+    def face_neighbor(self, packed, axis, direction):
+        ids = np.zeros(4, dtype=np.uint64)
+        cnt = C.c_int(0)
+        kind = self.L.tmref_tree_face_neighbor(self.h, packed, axis, direction, u64ptr(ids),
+                                               C.byref(cnt))
+        return kind, [int(x) for x in ids[: cnt.value]]
+
+    def plan(self, axis) -> np.ndarray:
+        n = self.L.tmref_tree_plan(self.h, axis, None, 0)
+        rows = np.zeros((n, 7), dtype=np.int64)
+        self.L.tmref_tree_plan(self.h, axis, rows.ctypes.data_as(_i64p), n)
+        return rows
+
+    def hydro_step(self, dt, gamma=1.4, workers=1, lane_width=1, max_slices=8):
+        tex, tst = C.c_double(0), C.c_double(0)
+        err = C.create_string_buffer(256)
+        rc = self.L.tmref_hydro_step(self.h, dt, gamma, workers, lane_width, max_slices,
+                                     C.byref(tex), C.byref(tst), err, 256)
+        if rc != 0:
+            raise RuntimeError(f"reference hydro step failed: {err.value.decode()}")
+        return tex.value, tst.value
+
+
+class Oracle(_Lib):
+    """Our plain-C restatement (oracle/tm_oracle.c)."""
+
+    def __init__(self):
+        super().__init__("liboracle.so")
+        L = self.lib
+        for f in ("tmo_minmod_scalar", "tmo_minmod_lane"):
+            getattr(L, f).restype = C.c_double
+            getattr(L, f).argtypes = [C.c_double, C.c_double]
+        L.tmo_reconstruct_face.argtypes = [C.c_double] * 4 + [_dp]
+        L.tmo_rusanov_euler.argtypes = [_dp, _dp, C.c_double, C.c_int, _dp]
+        L.tmo_rusanov_scalar.restype = C.c_double
+        L.tmo_rusanov_scalar.argtypes = [C.c_double] * 3
+        L.tmo_stage_subgrid.argtypes = [_dp, C.c_int, C.c_int, C.c_int, _dp, _dp, _ip]
+        L.tmo_stage_fused.argtypes = [_dp, _dp, C.c_size_t, C.c_size_t, C.c_size_t, C.c_int,
+                                      C.c_int, C.c_int, C.POINTER(C.c_size_t), _ip]
+        L.tmo_max_wavespeed.restype = C.c_double
+        L.tmo_max_wavespeed.argtypes = [_dp, C.c_int, C.c_int, C.c_int, _dp]
+        L.tmo_rk3_combine.restype = C.c_double
+        L.tmo_rk3_combine.argtypes = [C.c_int, C.c_double, C.c_double]
+        L.tmo_morton_encode.argtypes = [C.c_int, C.c_uint64, C.c_uint64, C.c_uint64, _u64p]
+        L.tmo_morton_decode.argtypes = [C.c_int, C.c_uint64, _u64p]
+        L.tmo_morton_dfs_rank.restype = C.c_uint64
+        L.tmo_morton_dfs_rank.argtypes = [C.c_int, C.c_uint64]
+        L.tmo_partition_leaves.argtypes = [_u64p, C.c_size_t, C.c_int, _ip]
+        L.tmo_tree_create.restype = C.c_void_p
+        L.tmo_tree_create.argtypes = [C.c_int, C.c_int, C.c_int, _ip, _ip, _u64p, C.c_size_t]
+        L.tmo_tree_destroy.argtypes = [C.c_void_p]
+        L.tmo_tree_leaves.restype = C.c_size_t
+        L.tmo_tree_leaves.argtypes = [C.c_void_p, _u64p, C.c_size_t]
+        L.tmo_tree_face_neighbor.argtypes = [C.c_void_p, C.c_uint64, C.c_int, C.c_int, _u64p, _ip]
+        L.tmo_tree_plan.restype = C.c_size_t
+        L.tmo_tree_plan.argtypes = [C.c_void_p, C.c_int, _i64p, C.c_size_t]
+        L.tmo_fill_ghosts_sync.argtypes = [C.c_void_p, C.POINTER(_dp)]
+        L.tmo_flag_refinement.argtypes = [C.c_void_p, _dp, C.c_double, C.c_double]
+
+    def stage_fused(self, packed_in, count, edge=8, ghost=2, vars=5):
+        S = edge + 2 * ghost
+        ins = 8 + vars * S ** 3
+        outs = vars * edge ** 3 + 6 * vars * edge ** 2 + 1
+        out = np.zeros(count * outs)
+        bad_slice = C.c_size_t(0)
+        cell = (C.c_int * 3)()
+        rc = self.lib.tmo_stage_fused(dptr(packed_in), dptr(out), ins, outs, count, edge, ghost,
+                                      vars, C.byref(bad_slice), cell)
+        return rc, out, (bad_slice.value, tuple(cell))
+
+    def max_wavespeed(self, header, ghosted, edge=8, ghost=2, vars=5):
+        return self.lib.tmo_max_wavespeed(dptr(header), edge, ghost, vars, dptr(ghosted))
+
+    def tree(self, leaves, edge=8, ghost=2, vars=5, root_dims=(1, 1, 1), bc=(0, 0, 0)):
+        return OracleTree(self, leaves, edge, ghost, vars, root_dims, bc)
+
+
+class OracleTree:
+    def __init__(self, o: Oracle, leaves, edge, ghost, vars, root_dims, bc):
+        self.L = o.lib
+        self.edge, self.ghost, self.vars = edge, ghost, vars
+        lv = np.ascontiguousarray(np.asarray(leaves, dtype=np.uint64))
+        self.h = self.L.tmo_tree_create(edge, ghost, vars, (C.c_int * 3)(*root_dims),
+                                        (C.c_int * 3)(*bc), u64ptr(lv), len(lv))
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            self.L.tmo_tree_destroy(self.h)
+            self.h = None
+
+    def leaves(self):
+        n = self.L.tmo_tree_leaves(self.h, None, 0)
+        out = np.zeros(n, dtype=np.uint64)
+        self.L.tmo_tree_leaves(self.h, u64ptr(out), n)
+        return out
+
+    def face_neighbor(self, packed, axis, direction):
+        ids = np.zeros(4, dtype=np.uint64)
+        cnt = C.c_int(0)
+        kind = self.L.tmo_tree_face_neighbor(self.h, packed, axis, direction, u64ptr(ids),
+                                             C.byref(cnt))
+        return kind, [int(x) for x in ids[: cnt.value]]
+
+    def plan(self, axis):
+        n = self.L.tmo_tree_plan(self.h, axis, None, 0)
+        rows = np.zeros((n, 7), dtype=np.int64)
+        self.L.tmo_tree_plan(self.h, axis, rows.ctypes.data_as(_i64p), n)
+        return rows
+
+    def fill_ghosts(self, grids):
+        """grids: list of float64 arrays in canonical leaf order (modified in place)."""
+        arr = (_dp * len(grids))(*[dptr(g) for g in grids])
+        if self.L.tmo_fill_ghosts_sync(self.h, arr) != 0:
+            raise RuntimeError("oracle ghost fill failed")
+
+    def flag(self, grid, theta, rho_floor=1e-10):
+        return bool(self.L.tmo_flag_refinement(self.h, dptr(grid), theta, rho_floor))
+
+
+def pack(level, ci, cj, ck) -> int:
+    """NodeId::packed (reference octree.hpp:29-33)."""
+    return (level << 60) | (ci << 40) | (cj << 20) | ck
+
+
+def unpack(p: int):
+    p = int(p)
+    return p >> 60, (p >> 40) & 0xFFFFF, (p >> 20) & 0xFFFFF, p & 0xFFFFF
+
+
+def random_state(rng: np.random.Generator, edge=8, ghost=2, euler=True, gamma=1.4):
+    """Reference test_hydro.cpp:21-43 state distribution (rho,p ~ U(0.2,2),
+    velocities ~ U(-0.5,0.5)), drawn with numpy: identical buffers are fed to
+    every implementation, so the RNG itself need not match libstdc++."""
+    S = edge + 2 * ghost
+    n = S ** 3
+    if not euler:
+        return rng.uniform(0.2, 2.0, n)
+    rho = rng.uniform(0.2, 2.0, n)
+    u, v, w = (rng.uniform(-0.5, 0.5, n) for _ in range(3))
+    p = rng.uniform(0.2, 2.0, n)
+    e = p / (gamma - 1.0) + 0.5 * rho * (u * u + v * v + w * w)
+    return np.concatenate([rho, rho * u, rho * v, rho * w, e])
