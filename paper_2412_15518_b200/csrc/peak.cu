@@ -1,0 +1,50 @@
+// FP64 pipe peak microbenchmark (roofline denominator: MEASURED_PEAKS.json has
+// no FP64 entry). Each thread runs 8 independent DFMA chains; FLOP = 2 per FMA.
+#include "tmgpu_internal.h"
+
+namespace tmgpu {
+namespace {
+__global__ void __launch_bounds__(256) dfma_kernel(double* out, int iters, double a, double b) {
+  double x[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) x[k] = threadIdx.x * 1e-3 + k;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) x[k] = fma(x[k], a, b);
+  }
+  double s = 0;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) s += x[k];
+  if (s == 12345.678) out[0] = s;  // never true; keeps the chains live
+}
+}  // namespace
+}  // namespace tmgpu
+
+extern "C" int tmgpu_fp64_peak(int iters, double* tflops, double* ms, tmgpu_error* err) {
+  using namespace tmgpu;
+  double* d = nullptr;
+  cudaError_t e = cudaMalloc(&d, sizeof(double));
+  if (e != cudaSuccess) return cuda_err(err, e, "tmgpu_fp64_peak");
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  const int blocks = sms * 8, threads = 256;
+  cudaEvent_t t0, t1;
+  cudaEventCreate(&t0);
+  cudaEventCreate(&t1);
+  dfma_kernel<<<blocks, threads>>>(d, iters / 10 + 1, 0.999999, 1e-7);  // warm-up
+  cudaEventRecord(t0);
+  dfma_kernel<<<blocks, threads>>>(d, iters, 0.999999, 1e-7);
+  cudaEventRecord(t1);
+  e = cudaEventSynchronize(t1);
+  float msf = 0;
+  cudaEventElapsedTime(&msf, t0, t1);
+  g_launches.fetch_add(2);
+  cudaEventDestroy(t0);
+  cudaEventDestroy(t1);
+  cudaFree(d);
+  if (e != cudaSuccess) return cuda_err(err, e, "tmgpu_fp64_peak");
+  const double flops = 2.0 * 8.0 * (double)iters * blocks * threads;
+  *ms = msf;
+  *tflops = flops / (msf * 1e-3) / 1e12;
+  return TMGPU_OK;
+}

@@ -1,0 +1,508 @@
+// Aggregated hydro stage kernel for sm_100a, FP64.
+//
+// Restates reference proj/src/hydro/stage.cpp:93-218 (stage_impl) with
+// euler.hpp:27-137 (MUSCL-minmod "PPM slot" + Rusanov/KT flux) for
+// E=8, G=2 (S=12) sub-grids; one CTA = one sub-grid, any number of
+// sub-grids (slices) per launch (the paper's kernel aggregation).
+//
+// Data flow per CTA
+//   1. TMA (cp.async.bulk.tensor, 5-D map over [slice][var][z][y][x]) stages
+//      exactly the cells the stage reads: the 12x8x8 x-pencil box plus four
+//      8x2x8 / 8x8x2 face-ghost slabs = 1280 cells x V vars (51.2 KB at V=5).
+//      Edge/corner ghosts are never read by the reference stage (its
+//      pencils are tangential-interior, stage.cpp:131-140), so never loaded.
+//   2. cons -> prim in place, once per staged cell (the reference converts
+//      every pencil cell per axis, stage.cpp:141-153; each cell's primitive
+//      is a pure function of its own conserved values, so converting once is
+//      bitwise identical). Interior conserved values seed the accumulator.
+//   3. per axis x,y,z: 64 pencils x 9 faces; each of 192 lanes evaluates 3
+//      consecutive faces of one pencil; the 9th-face neighbour flux comes
+//      from the next lane by warp shuffle; the lane applies
+//      acc -= cdt*(F[c0+1]-F[c0]) to its cells after a block barrier, so per
+//      cell the update order is x, then y, then z exactly as stage.cpp:166-183.
+//   4. epilogue per cell: floors (stage.cpp:187-208), non-finite check
+//      (stage.cpp:209-216), optional SSP-RK3 combine (rk3.hpp:18-27), store.
+//
+// BITWISE (compiled with -fmad=false): every + - * / sqrt is one IEEE
+// round-to-nearest op in the reference's association order; fmax/fmin are not
+// used (vmax is `x > f ? x : f`, std::max is `(a < b) ? b : a`).
+// FAST: reciprocal reuse + FMA; parity within 1e-10 of the per-variable scale.
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "tmgpu_internal.h"
+
+namespace tmgpu {
+
+constexpr int kE = 8, kG = 2, kS = 12;
+constexpr int kE2 = 64, kE3 = 512;
+constexpr int kStageThreads = 224;  // 7 warps x 30 face lanes >= 64 pencils x 3 segments
+constexpr double kRhoFloor = 1e-10;       // euler.hpp:15
+constexpr double kPressureFloor = 1e-12;  // euler.hpp:16
+
+// Staged smem layout (doubles), var-major inside each TMA box:
+//   B0 [V][8 z][8 y][12 x]  (y,z interior, x full)       var stride 768
+//   B1 [V][8 z][2 y][8 x]   y in {0,1}                     var stride 128
+//   B2 [V][8 z][2 y][8 x]   y in {10,11}
+//   B3 [V][2 z][8 y][8 x]   z in {0,1}
+//   B4 [V][2 z][8 y][8 x]   z in {10,11}
+template <int V>
+struct Lay {
+  static constexpr int B0 = 0;
+  static constexpr int B1 = V * 768;
+  static constexpr int B2 = B1 + V * 128;
+  static constexpr int B3 = B2 + V * 128;
+  static constexpr int B4 = B3 + V * 128;
+  static constexpr int kStaged = B4 + V * 128;  // = V*1280 doubles
+  static constexpr int kAcc = kStaged;          // accumulator [V][E^3]
+  static constexpr int kDoubles = kAcc + V * kE3;
+  static constexpr int kBytes = kDoubles * 8 + 64;  // + mbarrier/scratch
+  static constexpr uint32_t kTxBytes = (uint32_t)(V * 1280 * 8);
+};
+
+// StageLaunch is declared in tmgpu_internal.h
+
+
+// ------------------------------------------------------------------ PTX helpers
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+  uint32_t addr = smem_u32(bar);
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@!P1 bra WAIT_%=;\n\t}" ::"r"(addr),
+      "r"(phase)
+      : "memory");
+}
+
+__device__ __forceinline__ void tma_load_5d(void* dst, const CUtensorMap* map, uint64_t* bar,
+                                            int c0, int c1, int c2, int c3, int c4) {
+  asm volatile(
+      "cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5, %6, %7}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2),
+      "r"(c3), "r"(c4)
+      : "memory");
+}
+
+// ------------------------------------------------------------------ arithmetic
+// lanes.hpp:109-113 vmax and std::max, exactly (NaN / signed-zero behaviour).
+__device__ __forceinline__ double vmax_(double x, double f) { return x > f ? x : f; }
+__device__ __forceinline__ double stdmax_(double a, double b) { return (a < b) ? b : a; }
+
+// limiter.hpp:18-26 lane minmod: select(a*b > 0, select(|a|<|b|, a, b), 0)
+__device__ __forceinline__ double minmod_lane(double a, double b) {
+  double sm = fabs(a) < fabs(b) ? a : b;
+  return (a * b) > 0.0 ? sm : 0.0;
+}
+
+// euler.hpp:27-35
+__device__ __forceinline__ void recon(double um1, double u0, double up1, double up2, double& l,
+                                      double& r) {
+  l = u0 + 0.5 * minmod_lane(u0 - um1, up1 - u0);
+  r = up1 - 0.5 * minmod_lane(up1 - u0, up2 - up1);
+}
+
+// Rusanov / KT central flux between primitive face states (euler.hpp:116-137
+// with euler_flux :96-114, prim_to_cons :78-89, sound_speed :91-94).
+// prim_to_cons is evaluated once per side: the reference evaluates it twice
+// (inside euler_flux and again for U) with identical operands, so sharing the
+// value is bitwise neutral.
+template <int AXIS, bool FAST>
+__device__ __forceinline__ void rusanov(const double (&ql)[5], const double (&qr)[5], double gamma,
+                                        double gm1, double inv_gm1, double (&f)[5]) {
+  double cl, cr, el, er;
+  if constexpr (!FAST) {
+    cl = sqrt(gamma * ql[4] / ql[0]);
+    cr = sqrt(gamma * qr[4] / qr[0]);
+    el = ql[4] / gm1 + 0.5 * ql[0] * (ql[1] * ql[1] + ql[2] * ql[2] + ql[3] * ql[3]);
+    er = qr[4] / gm1 + 0.5 * qr[0] * (qr[1] * qr[1] + qr[2] * qr[2] + qr[3] * qr[3]);
+  } else {
+    cl = sqrt(gamma * ql[4] * __drcp_rn(ql[0]));
+    cr = sqrt(gamma * qr[4] * __drcp_rn(qr[0]));
+    el = fma(ql[4], inv_gm1,
+             0.5 * ql[0] * fma(ql[1], ql[1], fma(ql[2], ql[2], ql[3] * ql[3])));
+    er = fma(qr[4], inv_gm1,
+             0.5 * qr[0] * fma(qr[1], qr[1], fma(qr[2], qr[2], qr[3] * qr[3])));
+  }
+  const double unl = ql[1 + AXIS], unr = qr[1 + AXIS];
+  const double smax = vmax_(fabs(unl) + cl, fabs(unr) + cr);
+  const double hs = 0.5 * smax;
+  // conserved states
+  const double ul[5] = {ql[0], ql[0] * ql[1], ql[0] * ql[2], ql[0] * ql[3], el};
+  const double ur[5] = {qr[0], qr[0] * qr[1], qr[0] * qr[2], qr[0] * qr[3], er};
+  double fl[5], fr[5];
+#pragma unroll
+  for (int v = 0; v < 4; ++v) {
+    fl[v] = ul[v] * unl;
+    fr[v] = ur[v] * unr;
+  }
+  fl[1 + AXIS] = fl[1 + AXIS] + ql[4];
+  fr[1 + AXIS] = fr[1 + AXIS] + qr[4];
+  fl[4] = (el + ql[4]) * unl;
+  fr[4] = (er + qr[4]) * unr;
+#pragma unroll
+  for (int v = 0; v < 5; ++v) {
+    if constexpr (!FAST)
+      f[v] = 0.5 * (fl[v] + fr[v]) - hs * (ur[v] - ul[v]);
+    else
+      f[v] = fma(-hs, ur[v] - ul[v], 0.5 * (fl[v] + fr[v]));
+  }
+}
+
+// Address (var 0) and var stride of storage position `pos` along AXIS for the
+// pencil with tangential interior indices (c1 on axis AXIS+1, c2 on AXIS+2).
+template <int V, int AXIS>
+__device__ __forceinline__ void pos_addr(int pos, int c1, int c2, int& a, int& vs) {
+  using L = Lay<V>;
+  if constexpr (AXIS == 0) {  // y = c1, z = c2 interior
+    a = L::B0 + c2 * 96 + c1 * 12 + pos;
+    vs = 768;
+  } else if constexpr (AXIS == 1) {  // z = c1, x = c2 interior
+    if (pos < 2) {
+      a = L::B1 + c1 * 16 + pos * 8 + c2;
+      vs = 128;
+    } else if (pos >= 10) {
+      a = L::B2 + c1 * 16 + (pos - 10) * 8 + c2;
+      vs = 128;
+    } else {
+      a = L::B0 + c1 * 96 + (pos - 2) * 12 + (c2 + 2);
+      vs = 768;
+    }
+  } else {  // x = c1, y = c2 interior
+    if (pos < 2) {
+      a = L::B3 + pos * 64 + c2 * 8 + c1;
+      vs = 128;
+    } else if (pos >= 10) {
+      a = L::B4 + (pos - 10) * 64 + c2 * 8 + c1;
+      vs = 128;
+    } else {
+      a = L::B0 + (pos - 2) * 96 + c2 * 12 + (c1 + 2);
+      vs = 768;
+    }
+  }
+}
+
+// Lane -> (pencil, segment) map for the face phase. Returns false for idle
+// lanes. nb = lane holding segment r+1 of the same pencil.
+template <int AXIS>
+__device__ __forceinline__ bool face_map(int tid, int& c1, int& c2, int& r, int& nb) {
+  const int warp = tid >> 5, lane = tid & 31;
+  int j;
+  if constexpr (AXIS == 2) {  // segments 10 lanes apart: x-fast lanes, distinct banks
+    j = lane % 10;
+    r = lane / 10;
+    nb = lane + 10;
+  } else {
+    j = lane / 3;
+    r = lane % 3;
+    nb = lane + 1;
+  }
+  const int p = warp * 10 + j;
+  if constexpr (AXIS == 1) {
+    c2 = p & 7;
+    c1 = p >> 3;
+  } else {
+    c1 = p & 7;
+    c2 = p >> 3;
+  }
+  return lane < 30 && p < 64;
+}
+
+__device__ __forceinline__ int interior_index(int axis, int c0, int c1, int c2) {
+  int cc[3];
+  cc[axis] = c0;
+  cc[(axis + 1) % 3] = c1;
+  cc[(axis + 2) % 3] = c2;
+  return (cc[2] * kE + cc[1]) * kE + cc[0];
+}
+
+// One axis of the stage: fluxes of 3 faces per lane, boundary-face record,
+// then (after the barrier) the divergence update of the lane's cells.
+template <int V, int AXIS, bool FAST, bool EULER>
+__device__ __forceinline__ void axis_pass(const double* __restrict__ sm, double* __restrict__ acc,
+                                          int tid, double gamma, double gm1, double inv_gm1,
+                                          double a_vel, double cdt, double* faces_out) {
+  int c1, c2, r, nb;
+  const bool active = face_map<AXIS>(tid, c1, c2, r, nb);
+  double F[3][V];
+#pragma unroll
+  for (int k = 0; k < 3; ++k)
+#pragma unroll
+    for (int v = 0; v < V; ++v) F[k][v] = 0.0;
+  if (active) {
+    const int base = 3 * r;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      const int f0 = base + k;  // face f0: stencil positions f0..f0+3
+      int a[4], vs[4];
+#pragma unroll
+      for (int s = 0; s < 4; ++s) pos_addr<V, AXIS>(f0 + s, c1, c2, a[s], vs[s]);
+      if constexpr (EULER) {
+        double ql[5], qr[5];
+#pragma unroll
+        for (int v = 0; v < 5; ++v)
+          recon(sm[a[0] + v * vs[0]], sm[a[1] + v * vs[1]], sm[a[2] + v * vs[2]],
+                sm[a[3] + v * vs[3]], ql[v], qr[v]);
+        // stage.cpp:80-83 face floors
+        ql[0] = vmax_(ql[0], kRhoFloor);
+        qr[0] = vmax_(qr[0], kRhoFloor);
+        ql[4] = vmax_(ql[4], kPressureFloor);
+        qr[4] = vmax_(qr[4], kPressureFloor);
+        double f[5];
+        rusanov<AXIS, FAST>(ql, qr, gamma, gm1, inv_gm1, f);
+#pragma unroll
+        for (int v = 0; v < 5; ++v) F[k][v] = f[v];
+      } else {
+        // stage.cpp:44-55 scalar advection on var 0; other vars keep zero flux
+        double l, rr;
+        recon(sm[a[0]], sm[a[1]], sm[a[2]], sm[a[3]], l, rr);
+        F[k][0] = 0.5 * (a_vel * l + a_vel * rr) - 0.5 * fabs(a_vel) * (rr - l);
+      }
+    }
+    // boundary-face record (stage.cpp:180-182): F[0] -> side 0, F[E] -> side 1
+    if (faces_out) {
+      const int fo = c2 * kE + c1;
+      if (r == 0) {
+#pragma unroll
+        for (int v = 0; v < V; ++v) faces_out[(2 * AXIS) * V * kE2 + v * kE2 + fo] = F[0][v];
+      } else if (r == 2) {
+#pragma unroll
+        for (int v = 0; v < V; ++v) faces_out[(2 * AXIS + 1) * V * kE2 + v * kE2 + fo] = F[2][v];
+      }
+    }
+  }
+  // F[3] = first face of the next segment (warp shuffle; all lanes take part)
+  double D[3][V];
+#pragma unroll
+  for (int v = 0; v < V; ++v) {
+    const double nxt = __shfl_sync(0xffffffffu, F[0][v], nb & 31);
+    D[0][v] = F[1][v] - F[0][v];
+    D[1][v] = F[2][v] - F[1][v];
+    D[2][v] = nxt - F[2][v];
+  }
+  __syncthreads();  // previous axis' updates of every cell are complete
+  if (active) {
+    const int ncell = r == 2 ? 2 : 3;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      if (k < ncell) {
+        const int ci = interior_index(AXIS, 3 * r + k, c1, c2);
+#pragma unroll
+        for (int v = 0; v < V; ++v) {
+          double& o = acc[v * kE3 + ci];
+          if constexpr (FAST)
+            o = fma(-cdt, D[k][v], o);
+          else
+            o -= cdt * D[k][v];
+        }
+      }
+    }
+  }
+}
+
+template <int V, bool FAST>
+__global__ void __launch_bounds__(kStageThreads, 2)
+    stage_kernel(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CUtensorMap tm_y,
+                 const __grid_constant__ CUtensorMap tm_z, const StageLaunch p) {
+  using L = Lay<V>;
+  extern __shared__ __align__(128) double smem[];
+  double* sm = smem;
+  double* acc = smem + L::kAcc;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + L::kDoubles);
+  unsigned int& s_hits = *reinterpret_cast<unsigned int*>(smem + L::kDoubles + 1);
+  unsigned int& s_bad = *(reinterpret_cast<unsigned int*>(smem + L::kDoubles + 1) + 1);
+
+  const int tid = threadIdx.x;
+  const int s = blockIdx.x;
+  const int slot = p.index ? p.index[s] : s;  // per-slice outputs are indexed by slot
+
+  if (tid == 0) {
+    s_hits = 0;
+    s_bad = 0xffffffffu;
+    mbar_init(bar, 1);
+    mbar_expect_tx(bar, L::kTxBytes);
+    tma_load_5d(sm + L::B0, &tm_x, bar, 0, 2, 2, 0, slot);
+    tma_load_5d(sm + L::B1, &tm_y, bar, 2, 0, 2, 0, slot);
+    tma_load_5d(sm + L::B2, &tm_y, bar, 2, 10, 2, 0, slot);
+    tma_load_5d(sm + L::B3, &tm_z, bar, 2, 2, 0, 0, slot);
+    tma_load_5d(sm + L::B4, &tm_z, bar, 2, 2, 10, 0, slot);
+  }
+
+  // header (decode_header stage.cpp:21-29)
+  double mode, dx, dt, gamma, ax, ay, az;
+  if (p.hdr) {
+    const double* h = p.hdr + (long long)slot * p.hdr_stride;
+    mode = h[0];
+    dx = h[1];
+    dt = h[2];
+    gamma = h[3];
+    ax = h[4];
+    ay = h[5];
+    az = h[6];
+  } else {
+    mode = p.g_mode;
+    dx = p.leaf_dx[slot];
+    dt = p.g_dt;
+    gamma = p.g_gamma;
+    ax = p.g_ax;
+    ay = p.g_ay;
+    az = p.g_az;
+  }
+  const bool euler = mode != 0.0;
+  const double cdt = dt / dx;
+  const double gm1 = gamma - 1.0;
+  const double inv_gm1 = 1.0 / gm1;
+
+  __syncthreads();  // barrier init visible
+  mbar_wait(bar, 0);
+
+  // ---- phase 2: accumulator seed + cons -> prim in place (stage.cpp:141-153)
+  for (int c = tid; c < 1280; c += kStageThreads) {
+    int a, vs, x, y, z;
+    if (c < 768) {
+      x = c % 12;
+      y = 2 + (c / 12) % 8;
+      z = 2 + c / 96;
+      a = L::B0 + c;
+      vs = 768;
+    } else {
+      const int q = c - 768, box = q >> 7, w = q & 127;
+      a = L::B1 + box * V * 128 + w;
+      vs = 128;
+      if (box < 2) {  // [z 8][y 2][x 8]
+        x = 2 + (w & 7);
+        y = (box == 0 ? 0 : 10) + ((w >> 3) & 1);
+        z = 2 + (w >> 4);
+      } else {  // [z 2][y 8][x 8]
+        x = 2 + (w & 7);
+        y = 2 + ((w >> 3) & 7);
+        z = (box == 2 ? 0 : 10) + (w >> 6);
+      }
+    }
+    double u[V];
+#pragma unroll
+    for (int v = 0; v < V; ++v) u[v] = sm[a + v * vs];
+    if (x >= 2 && x < 10 && y >= 2 && y < 10 && z >= 2 && z < 10) {
+      const int ci = ((z - 2) * kE + (y - 2)) * kE + (x - 2);
+#pragma unroll
+      for (int v = 0; v < V; ++v) acc[v * kE3 + ci] = u[v];
+    }
+    if constexpr (V == 5) {
+      if (euler) {
+        const double rho = stdmax_(u[0], kRhoFloor);
+        double iu, iv, iw, ke, pr;
+        if constexpr (!FAST) {
+          iu = u[1] / rho;
+          iv = u[2] / rho;
+          iw = u[3] / rho;
+          ke = 0.5 * rho * (iu * iu + iv * iv + iw * iw);
+          pr = stdmax_(gm1 * (u[4] - ke), kPressureFloor);
+        } else {
+          const double ir = __drcp_rn(rho);
+          iu = u[1] * ir;
+          iv = u[2] * ir;
+          iw = u[3] * ir;
+          ke = 0.5 * rho * fma(iu, iu, fma(iv, iv, iw * iw));
+          pr = stdmax_(gm1 * (u[4] - ke), kPressureFloor);
+        }
+        sm[a] = rho;
+        sm[a + vs] = iu;
+        sm[a + 2 * vs] = iv;
+        sm[a + 3 * vs] = iw;
+        sm[a + 4 * vs] = pr;
+      }
+    }
+  }
+  __syncthreads();
+
+  // ---- phase 3: x, y, z passes
+  double* faces_out = p.faces ? p.faces + (long long)slot * p.faces_stride : nullptr;
+  if (V == 5 && euler) {
+    axis_pass<V, 0, FAST, (V == 5)>(sm, acc, tid, gamma, gm1, inv_gm1, 0.0, cdt, faces_out);
+    axis_pass<V, 1, FAST, (V == 5)>(sm, acc, tid, gamma, gm1, inv_gm1, 0.0, cdt, faces_out);
+    axis_pass<V, 2, FAST, (V == 5)>(sm, acc, tid, gamma, gm1, inv_gm1, 0.0, cdt, faces_out);
+  } else {
+    axis_pass<V, 0, FAST, false>(sm, acc, tid, gamma, gm1, inv_gm1, ax, cdt, faces_out);
+    axis_pass<V, 1, FAST, false>(sm, acc, tid, gamma, gm1, inv_gm1, ay, cdt, faces_out);
+    axis_pass<V, 2, FAST, false>(sm, acc, tid, gamma, gm1, inv_gm1, az, cdt, faces_out);
+  }
+  __syncthreads();
+
+  // ---- phase 4: floors, finiteness, RK3 combine, store
+  unsigned int hits = 0, bad = 0xffffffffu;
+  double* outp = p.out + (long long)slot * p.out_stride;
+  const double* u0p = p.u0 ? p.u0 + (long long)slot * p.u0_stride : nullptr;
+  for (int c = tid; c < kE3; c += kStageThreads) {
+    double u[V];
+#pragma unroll
+    for (int v = 0; v < V; ++v) u[v] = acc[v * kE3 + c];
+    if constexpr (V == 5) {
+      if (euler) {  // stage.cpp:187-208
+        if (u[0] < kRhoFloor) {
+          u[0] = kRhoFloor;
+          ++hits;
+        }
+        double ke, pr;
+        if constexpr (!FAST) {
+          ke = 0.5 * (u[1] * u[1] + u[2] * u[2] + u[3] * u[3]) / u[0];
+        } else {
+          ke = 0.5 * fma(u[1], u[1], fma(u[2], u[2], u[3] * u[3])) * __drcp_rn(u[0]);
+        }
+        pr = gm1 * (u[4] - ke);
+        if (pr < kPressureFloor) {
+          u[4] = kPressureFloor / gm1 + ke;
+          ++hits;
+        }
+      }
+    }
+#pragma unroll
+    for (int v = 0; v < V; ++v)
+      if (!isfinite(u[v])) bad = min(bad, (unsigned)(v * kE3 + c));
+    const int z = c >> 6, y = (c >> 3) & 7, x = c & 7;
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      double o = u[v];
+      if (u0p) {  // rk3.hpp:18-27
+        const double a0 = u0p[v * kE3 + c];
+        if (p.rk_stage == 2)
+          o = a0 + 0.25 * (o - a0);
+        else if (p.rk_stage == 3)
+          o = a0 + (2.0 / 3.0) * (o - a0);
+      }
+      if (p.out_ghosted)
+        outp[((v * kS + z + 2) * kS + y + 2) * kS + x + 2] = o;
+      else
+        outp[v * kE3 + c] = o;
+    }
+  }
+  // block reductions (integer counts: order-free, exact as double)
+  if (hits) atomicAdd(&s_hits, hits);
+  if (bad != 0xffffffffu) atomicMin(&s_bad, bad);
+  __syncthreads();
+  if (tid == 0) {
+    if (p.diag) p.diag[(long long)slot * p.diag_stride] = (double)s_hits;
+    if (s_bad != 0xffffffffu && p.err)
+      atomicMin(p.err, ((unsigned long long)slot << 32) | s_bad);
+  }
+}
+
+}  // namespace tmgpu

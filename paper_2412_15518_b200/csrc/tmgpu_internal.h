@@ -1,0 +1,86 @@
+// Internal C++ interfaces shared by the CUDA translation units and the C ABI.
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstdint>
+#include <cstdio>
+#include <string>
+
+#include "../../include/tmgpu.h"
+
+namespace tmgpu {
+
+// Per-launch arguments of the aggregated stage kernel (stage_kernel.cuh).
+struct StageLaunch {
+  // headers: slice mode reads hdr + s*hdr_stride; arena mode (hdr == nullptr)
+  // uses leaf_dx[slot] and the launch-wide fields below.
+  const double* hdr;
+  long long hdr_stride;
+  const double* leaf_dx;
+  double g_mode, g_dt, g_gamma, g_ax, g_ay, g_az;
+  // interior destination
+  double* out;
+  long long out_stride;
+  int out_ghosted;  // 1: write interior positions of a ghosted S^3 block
+  // optional outputs
+  double* faces;  // [6][V][E^2] per slice
+  long long faces_stride;
+  double* diag;  // floor hits per slice
+  long long diag_stride;
+  // optional SSP-RK3 combine: out = rk3_combine(rk_stage, u0, v)
+  const double* u0;
+  long long u0_stride;
+  int rk_stage;
+  const int* index;  // optional: tensor slot of CTA b = index[b]
+  unsigned long long* err;  // atomicMin of (slice << 32 | var-major interior index)
+  int count;
+};
+
+// Number of kernels this library launched since load.
+extern std::atomic<uint64_t> g_launches;
+
+struct StageMaps {
+  CUtensorMap x, y, z;  // boxes 12x8x8, 8x2x8, 8x8x2 over [slot][var][z][y][x]
+};
+
+// Encode the three TMA maps for `count` ghosted 12^3 blocks of V vars whose
+// var-0 element of slot s sits at base + s*slot_stride (doubles). base must be
+// 16-byte aligned and slot_stride*8 a multiple of 16.
+int make_stage_maps(const double* base, int V, long long slot_stride, long long count,
+                    StageMaps* maps, std::string* why);
+
+cudaError_t launch_stage(int V, bool fast, const StageMaps& maps, const StageLaunch& p,
+                         cudaStream_t stream);
+
+cudaError_t launch_max_wavespeed(const double* in, long long slot_stride, const double* hdr,
+                                 long long hdr_stride, const double* leaf_dx, double g_gamma,
+                                 int V, long long count, double* result, cudaStream_t stream);
+
+cudaError_t launch_rk3_combine(int stage, const double* u0, const double* v, double* out,
+                               long long n, cudaStream_t stream);
+
+inline int set_err(tmgpu_error* err, int code, const char* msg) {
+  if (err) {
+    err->code = code;
+    std::snprintf(err->message, sizeof(err->message), "%s", msg);
+  }
+  return code;
+}
+
+inline int cuda_err(tmgpu_error* err, cudaError_t e, const char* where) {
+  if (e == cudaSuccess) return TMGPU_OK;
+  if (err) {
+    err->code = TMGPU_ERR_CUDA;
+    std::snprintf(err->message, sizeof(err->message), "%s: %s", where, cudaGetErrorString(e));
+  }
+  return TMGPU_ERR_CUDA;
+}
+
+inline cudaStream_t as_stream(void* s) {
+  return s ? static_cast<cudaStream_t>(s) : cudaStreamPerThread;
+}
+
+}  // namespace tmgpu
