@@ -40,6 +40,7 @@ typedef struct tmgpu_error {
 /* ---------------------------------------------------------------- flags */
 #define TMGPU_HOST_PTRS 0x1  /* in/out are host memory: H2D, kernel, D2H inside the call */
 #define TMGPU_FAST 0x2       /* FMA/reciprocal arithmetic: parity within 1e-10 (scaled), not bitwise */
+#define TMGPU_ASYNC 0x4      /* enqueue only; errors latched until tmgpu_forest_check */
 
 /* ---------------------------------------------------------------- hydro
  * Slice contract (reference stage.hpp:8-12, 39-66):
@@ -78,6 +79,69 @@ int tmgpu_max_wavespeed(const double* in, size_t in_slice, size_t count, int edg
 /* hydro::rk3_combine (reference include/taskmesh/hydro/rk3.hpp:18-34) on n values. */
 int tmgpu_rk3_combine(int stage, const double* u0, const double* v, double* out, size_t n,
                       int flags, void* stream, tmgpu_error* err);
+
+/* ---------------------------------------------------------------- indexing
+ * Bit-exact with the reference (tests/test_forest.py). */
+/* amr::morton_encode / morton_decode / morton_dfs_rank (amr/morton.hpp:32-66);
+ * out-of-range arguments return TMGPU_ERR_AMR (the reference throws AmrError). */
+int tmgpu_morton_encode(int level, uint64_t i, uint64_t j, uint64_t k, uint64_t* index,
+                        tmgpu_error* err);
+int tmgpu_morton_decode(int level, uint64_t index, uint64_t* ijk, tmgpu_error* err);
+uint64_t tmgpu_morton_dfs_rank(int level, uint64_t index);
+/* amr::partition_leaves (src/amr/octree.cpp:374-399) */
+int tmgpu_partition_leaves(const uint64_t* weights, size_t n, int localities, int* owner,
+                           tmgpu_error* err);
+
+/* ---------------------------------------------------------------- forest
+ * Octree topology (amr::Tree, amr/octree.hpp:241-314) with the leaf state
+ * held in a device arena [slot][vars][S^3] indexed by canonical leaf order.
+ * Node ids are NodeId::packed() (octree.hpp:29-33); bc[a]: 0 periodic,
+ * 1 reflective. */
+typedef struct tmgpu_forest tmgpu_forest;
+tmgpu_forest* tmgpu_forest_create(int edge, int ghost, int vars, int max_level,
+                                  const int* root_dims, const int* bc, tmgpu_error* err);
+void tmgpu_forest_destroy(tmgpu_forest* f);
+int tmgpu_forest_refine(tmgpu_forest* f, uint64_t packed, tmgpu_error* err);  /* Tree::refine octree.cpp:200-234 */
+size_t tmgpu_forest_leaves(tmgpu_forest* f, uint64_t* out, size_t cap);     /* Tree::leaves octree.cpp:52-77 */
+/* Tree::face_neighbor (octree.cpp:92-132): returns kind 0 same, 1 coarser, 2 finer, 3 boundary */
+int tmgpu_forest_face_neighbor(tmgpu_forest* f, uint64_t leaf, int axis, int dir, uint64_t* ids4,
+                               int* count);
+/* ghost::plan_axis_fills (ghost.cpp:168-210): rows of 7 int64 (dst, src|-1, kind, axis, dir, qt1, qt2) */
+size_t tmgpu_forest_plan(tmgpu_forest* f, int axis, int64_t* rows, size_t cap);
+int tmgpu_forest_balanced(tmgpu_forest* f);                                   /* Tree::is_balanced */
+double tmgpu_forest_cell_size(tmgpu_forest* f, int level);                    /* Tree::cell_size */
+uint64_t tmgpu_forest_topology_version(tmgpu_forest* f);
+uint64_t tmgpu_forest_exchanges(tmgpu_forest* f);
+/* synthetic scenarios: kind 0 rotating star, 1 double white dwarf, 2 Sod, 3 Sedov */
+int tmgpu_forest_scenario_refine(tmgpu_forest* f, int kind, int min_level, int max_level,
+                                 double theta, tmgpu_error* err);
+int tmgpu_forest_scenario_fill(tmgpu_forest* f, int kind, uint64_t seed, double* compact_host,
+                               tmgpu_error* err);
+/* (re)allocate the zeroed device arena + ghost plans for the current topology */
+int tmgpu_forest_alloc(tmgpu_forest* f, tmgpu_error* err);
+double* tmgpu_forest_arena(tmgpu_forest* f);
+/* compact interior [slot][vars][E^3] <-> arena (SubGrid::copy_interior_in/out, subgrid.hpp:63-76) */
+int tmgpu_forest_interior(tmgpu_forest* f, double* compact, int to_device, int flags, void* stream,
+                          tmgpu_error* err);
+/* whole ghosted arena <-> host [slot][vars][S^3] (SubGrid::raw, subgrid.hpp:59-60) */
+int tmgpu_forest_grids(tmgpu_forest* f, double* ghosted_host, int to_device, tmgpu_error* err);
+/* ghost::fill_ghosts_sync (ghost.cpp:282-296), bitwise on the full ghosted arrays */
+int tmgpu_forest_fill_ghosts(tmgpu_forest* f, void* stream, tmgpu_error* err);
+/* hydro::max_wavespeed per leaf (stage.cpp:248-272) */
+int tmgpu_forest_max_wavespeed(tmgpu_forest* f, double gamma, double* per_leaf_host, tmgpu_error* err);
+/* SSP-RK3 step (rk3.hpp): 3 x (fill_ghosts_sync -> aggregated
+ * stage over all leaves -> rk3_combine); cfl > 0 computes dt on the device */
+int tmgpu_forest_step(tmgpu_forest* f, double dt, double cfl, double gamma, int flags,
+                      void* stream, double* dt_used, tmgpu_error* err);
+int tmgpu_forest_check(tmgpu_forest* f, void* stream, tmgpu_error* err);
+/* per-phase device timing (CUDA events) of subsequent steps: accumulated ms */
+int tmgpu_forest_set_timing(tmgpu_forest* f, int on, tmgpu_error* err);
+int tmgpu_forest_timing(tmgpu_forest* f, double* ms_cfl, double* ms_exchange, double* ms_stage,
+                        long long* steps);
+int tmgpu_forest_floor_hits(tmgpu_forest* f, double* per_leaf_host, tmgpu_error* err);
+
+/* FP64 DFMA throughput microbenchmark (roofline denominator) */
+int tmgpu_fp64_peak(int iters, double* tflops, double* ms, tmgpu_error* err);
 
 /* ---------------------------------------------------------------- build info */
 const char* tmgpu_version(void);

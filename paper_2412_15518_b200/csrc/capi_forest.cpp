@@ -1,0 +1,506 @@
+// C ABI: octree forest, device leaf arena, reference-exact ghost exchange and
+// the SSP-RK3 hydro step (include/tmgpu.h, "forest" section).
+#include <cmath>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "forest.h"
+#include "ghost.h"
+#include "tmgpu_internal.h"
+
+using namespace tmgpu;
+
+struct tmgpu_forest {
+  explicit tmgpu_forest(const ForestConfig& c) : forest(c) {}
+  Forest forest;
+  // device state (valid for `dev_version`)
+  uint64_t dev_version = ~0ull;
+  long long nslots = 0;
+  double* arena = nullptr;    // [slot][V][S^3]
+  double* u0 = nullptr;       // [slot][V][E^3]
+  double* leaf_dx = nullptr;  // [slot]
+  double* speeds = nullptr;   // [slot]
+  double* diag = nullptr;     // [slot] floor hits of the last stage
+  double* dt_dev = nullptr;   // [1]
+  unsigned long long* err_dev = nullptr;
+  double* staged = nullptr;
+  GhostFill* fills[3] = {nullptr, nullptr, nullptr};
+  int* staged_of[3] = {nullptr, nullptr, nullptr};
+  int* prolong[3] = {nullptr, nullptr, nullptr};
+  GhostPassDev pass[3];
+  StageMaps maps{};
+  uint64_t exchanges = 0;  // ghost exchanges performed (structural counter)
+  // optional per-phase device timing: events [start, cfl, (exch, stage) x 3]
+  bool timing = false;
+  cudaEvent_t ev[8] = {};
+  double t_cfl = 0, t_exchange = 0, t_stage = 0;
+  long long timed_steps = 0, pending_timed = 0;
+};
+
+namespace {
+
+int fail(tmgpu_error* err, int code, const std::string& m) { return set_err(err, code, m.c_str()); }
+
+void collect_timing(tmgpu_forest* f) {
+  if (!f->pending_timed) return;
+  float ms = 0;
+  if (cudaEventSynchronize(f->ev[7]) != cudaSuccess) return;
+  cudaEventElapsedTime(&ms, f->ev[0], f->ev[1]);
+  f->t_cfl += ms;
+  for (int s = 0; s < 3; ++s) {
+    cudaEventElapsedTime(&ms, f->ev[1 + 2 * s], f->ev[2 + 2 * s]);
+    f->t_exchange += ms;
+    cudaEventElapsedTime(&ms, f->ev[2 + 2 * s], f->ev[3 + 2 * s]);
+    f->t_stage += ms;
+  }
+  f->timed_steps += 1;
+  f->pending_timed = 0;
+}
+
+void free_dev(tmgpu_forest* f) {
+  auto fr = [](void* p) {
+    if (p) cudaFree(p);
+  };
+  fr(f->arena);
+  fr(f->u0);
+  fr(f->leaf_dx);
+  fr(f->speeds);
+  fr(f->diag);
+  fr(f->dt_dev);
+  fr(f->err_dev);
+  fr(f->staged);
+  for (int a = 0; a < 3; ++a) {
+    fr(f->fills[a]);
+    fr(f->staged_of[a]);
+    fr(f->prolong[a]);
+    f->fills[a] = nullptr;
+    f->staged_of[a] = nullptr;
+    f->prolong[a] = nullptr;
+    f->pass[a] = GhostPassDev{};
+  }
+  f->arena = f->u0 = f->leaf_dx = f->speeds = f->diag = f->dt_dev = f->staged = nullptr;
+  f->err_dev = nullptr;
+  f->dev_version = ~0ull;
+  f->nslots = 0;
+}
+
+int ready(tmgpu_forest* f, tmgpu_error* err) {
+  if (!f) return fail(err, TMGPU_ERR_INVALID, "null forest");
+  if (f->dev_version != f->forest.topology_version() || !f->arena)
+    return fail(err, TMGPU_ERR_INVALID,
+                "device arena is stale: call tmgpu_forest_alloc after changing the topology");
+  return TMGPU_OK;
+}
+
+// (Re)build the device arena and the per-axis ghost plans for the current topology.
+int alloc_device(tmgpu_forest* f, tmgpu_error* err) {
+  free_dev(f);
+  const auto& cfg = f->forest.config();
+  if (cfg.edge != 8 || cfg.ghost != 2 || (cfg.vars != 5 && cfg.vars != 1))
+    return fail(err, TMGPU_ERR_INVALID, "device arena supports edge 8, ghost 2, vars 1|5");
+  const auto& lv = f->forest.leaves();
+  const long long n = (long long)lv.size();
+  const int V = cfg.vars;
+  const size_t S3 = 1728;
+  cudaError_t e = cudaSuccess;
+  auto M = [&](void** p, size_t bytes) {
+    if (e == cudaSuccess) e = cudaMalloc(p, bytes ? bytes : 8);
+  };
+  M((void**)&f->arena, n * V * S3 * sizeof(double));
+  M((void**)&f->u0, n * V * 512 * sizeof(double));
+  M((void**)&f->leaf_dx, n * sizeof(double));
+  M((void**)&f->speeds, n * sizeof(double));
+  M((void**)&f->diag, n * sizeof(double));
+  M((void**)&f->dt_dev, sizeof(double));
+  M((void**)&f->err_dev, sizeof(unsigned long long));
+  if (e == cudaSuccess) e = cudaMemset(f->arena, 0, n * V * S3 * sizeof(double));  // SubGrid() zeroes
+  std::vector<double> dx(n);
+  for (long long s = 0; s < n; ++s) dx[s] = f->forest.cell_size(lv[s].level);
+  if (e == cudaSuccess) e = cudaMemcpy(f->leaf_dx, dx.data(), n * sizeof(double), cudaMemcpyHostToDevice);
+  size_t max_prolong = 0;
+  for (int a = 0; a < 3 && e == cudaSuccess; ++a) {
+    const std::vector<Fill> plan = f->forest.plan_axis(a);
+    std::vector<GhostFill> gf(plan.size());
+    std::vector<int> sof(plan.size(), -1), pro;
+    for (size_t i = 0; i < plan.size(); ++i) {
+      const Fill& p = plan[i];
+      gf[i] = GhostFill{p.dst, p.src, p.kind, p.axis, p.dir, p.qt1, p.qt2, {0, 0, 0}};
+      if (p.kind == 1) {
+        sof[i] = (int)pro.size();
+        pro.push_back((int)i);
+      }
+    }
+    max_prolong = std::max(max_prolong, pro.size());
+    M((void**)&f->fills[a], gf.size() * sizeof(GhostFill));
+    M((void**)&f->staged_of[a], sof.size() * sizeof(int));
+    M((void**)&f->prolong[a], pro.size() * sizeof(int));
+    if (e == cudaSuccess && !gf.empty())
+      e = cudaMemcpy(f->fills[a], gf.data(), gf.size() * sizeof(GhostFill), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess && !sof.empty())
+      e = cudaMemcpy(f->staged_of[a], sof.data(), sof.size() * sizeof(int), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess && !pro.empty())
+      e = cudaMemcpy(f->prolong[a], pro.data(), pro.size() * sizeof(int), cudaMemcpyHostToDevice);
+    f->pass[a] = GhostPassDev{f->fills[a], f->staged_of[a], f->prolong[a], (int)gf.size(),
+                              (int)pro.size()};
+  }
+  M((void**)&f->staged, max_prolong * V * 8 * 8 * 2 * sizeof(double));
+  if (e != cudaSuccess) {
+    free_dev(f);
+    return cuda_err(err, e, "tmgpu_forest_alloc");
+  }
+  std::string why;
+  int rc = make_stage_maps(f->arena, V, (long long)V * S3, n, &f->maps, &why);
+  if (rc != TMGPU_OK) {
+    free_dev(f);
+    return fail(err, rc, why);
+  }
+  f->nslots = n;
+  f->dev_version = f->forest.topology_version();
+  return TMGPU_OK;
+}
+
+int exchange(tmgpu_forest* f, cudaStream_t st) {
+  const int V = f->forest.config().vars;
+  for (int a = 0; a < 3; ++a) {
+    cudaError_t e = ghost_pass(f->arena, V, f->pass[a], f->staged, st);
+    if (e != cudaSuccess) return (int)e;
+  }
+  f->exchanges += 1;
+  return 0;
+}
+
+int solver_err_from_word(tmgpu_error* err, unsigned long long w) {
+  const unsigned cell = (unsigned)(w & 0xffffffffu) % 512u;
+  const int i = (int)(cell % 8), j = (int)(cell / 8 % 8), k = (int)(cell / 64);
+  if (err) {
+    err->code = TMGPU_ERR_SOLVER;
+    err->slice = (int64_t)(w >> 32);
+    err->cell[0] = i;
+    err->cell[1] = j;
+    err->cell[2] = k;
+    std::snprintf(err->message, sizeof(err->message),
+                  "non-finite state after stage at cell (%d,%d,%d)", i, j, k);
+  }
+  return TMGPU_ERR_SOLVER;
+}
+
+}  // namespace
+
+extern "C" {
+
+tmgpu_forest* tmgpu_forest_create(int edge, int ghost, int vars, int max_level,
+                                  const int* root_dims, const int* bc, tmgpu_error* err) {
+  if (err) std::memset(err, 0, sizeof(*err));
+  ForestConfig c;
+  c.edge = edge;
+  c.ghost = ghost;
+  c.vars = vars;
+  c.max_level = max_level;
+  for (int a = 0; a < 3; ++a) {
+    c.root_dims[a] = root_dims ? root_dims[a] : 1;
+    c.bc[a] = bc ? bc[a] : 0;
+  }
+  try {
+    return new tmgpu_forest(c);
+  } catch (const std::exception& ex) {
+    set_err(err, TMGPU_ERR_AMR, ex.what());
+    return nullptr;
+  }
+}
+
+void tmgpu_forest_destroy(tmgpu_forest* f) {
+  if (!f) return;
+  free_dev(f);
+  for (auto& e : f->ev)
+    if (e) cudaEventDestroy(e);
+  delete f;
+}
+
+int tmgpu_forest_refine(tmgpu_forest* f, uint64_t packed, tmgpu_error* err) {
+  if (err) std::memset(err, 0, sizeof(*err));
+  try {
+    f->forest.refine(NodeId::unpack(packed));
+    return TMGPU_OK;
+  } catch (const std::exception& ex) {
+    return fail(err, TMGPU_ERR_AMR, ex.what());
+  }
+}
+
+size_t tmgpu_forest_leaves(tmgpu_forest* f, uint64_t* out, size_t cap) {
+  const auto& lv = f->forest.leaves();
+  for (size_t i = 0; i < lv.size() && i < cap; ++i) out[i] = lv[i].packed();
+  return lv.size();
+}
+
+int tmgpu_forest_face_neighbor(tmgpu_forest* f, uint64_t leaf, int axis, int dir, uint64_t* ids4,
+                               int* count) {
+  try {
+    FaceNeighbors nb = f->forest.face_neighbor(NodeId::unpack(leaf), axis, dir);
+    *count = nb.count;
+    for (int q = 0; q < nb.count; ++q) ids4[q] = nb.ids[q].packed();
+    return (int)nb.kind;
+  } catch (const std::exception&) {
+    *count = 0;
+    return -1;
+  }
+}
+
+size_t tmgpu_forest_plan(tmgpu_forest* f, int axis, int64_t* rows, size_t cap) {
+  const auto plan = f->forest.plan_axis(axis);
+  const auto& lv = f->forest.leaves();
+  for (size_t r = 0; r < plan.size() && r < cap; ++r) {
+    const Fill& p = plan[r];
+    int64_t* o = rows + 7 * r;
+    o[0] = (int64_t)lv[p.dst].packed();
+    o[1] = p.src < 0 ? -1 : (int64_t)lv[p.src].packed();
+    o[2] = p.kind;
+    o[3] = p.axis;
+    o[4] = p.dir;
+    o[5] = p.qt1;
+    o[6] = p.qt2;
+  }
+  return plan.size();
+}
+
+int tmgpu_forest_balanced(tmgpu_forest* f) { return f->forest.is_balanced() ? 1 : 0; }
+
+double tmgpu_forest_cell_size(tmgpu_forest* f, int level) { return f->forest.cell_size(level); }
+
+uint64_t tmgpu_forest_topology_version(tmgpu_forest* f) { return f->forest.topology_version(); }
+
+uint64_t tmgpu_forest_exchanges(tmgpu_forest* f) { return f->exchanges; }
+
+int tmgpu_forest_scenario_refine(tmgpu_forest* f, int kind, int min_level, int max_level,
+                                 double theta, tmgpu_error* err) {
+  if (err) std::memset(err, 0, sizeof(*err));
+  try {
+    scenario_refine(f->forest, kind, min_level, max_level, theta);
+    return TMGPU_OK;
+  } catch (const std::exception& ex) {
+    return fail(err, TMGPU_ERR_AMR, ex.what());
+  }
+}
+
+int tmgpu_forest_scenario_fill(tmgpu_forest* f, int kind, uint64_t seed, double* compact_host,
+                               tmgpu_error* err) {
+  if (err) std::memset(err, 0, sizeof(*err));
+  if (f->forest.config().vars != 5) return fail(err, TMGPU_ERR_INVALID, "scenarios are Euler (vars 5)");
+  scenario_fill(f->forest, kind, seed, compact_host);
+  return TMGPU_OK;
+}
+
+int tmgpu_forest_alloc(tmgpu_forest* f, tmgpu_error* err) {
+  if (err) std::memset(err, 0, sizeof(*err));
+  return alloc_device(f, err);
+}
+
+double* tmgpu_forest_arena(tmgpu_forest* f) { return f->arena; }
+
+int tmgpu_forest_interior(tmgpu_forest* f, double* compact, int to_device, int flags, void* stream,
+                          tmgpu_error* err) {
+  if (err) std::memset(err, 0, sizeof(*err));
+  if (int rc = ready(f, err)) return rc;
+  cudaStream_t st = as_stream(stream);
+  const int V = f->forest.config().vars;
+  const size_t bytes = (size_t)f->nslots * V * 512 * sizeof(double);
+  double* dev = compact;
+  cudaError_t e = cudaSuccess;
+  if (flags & TMGPU_HOST_PTRS) {
+    e = cudaMallocAsync(&dev, bytes ? bytes : 8, st);
+    if (e == cudaSuccess && to_device) e = cudaMemcpyAsync(dev, compact, bytes, cudaMemcpyHostToDevice, st);
+  }
+  if (e == cudaSuccess) e = interior_copy(f->arena, dev, V, f->nslots, to_device != 0, st);
+  if (e == cudaSuccess && (flags & TMGPU_HOST_PTRS) && !to_device)
+    e = cudaMemcpyAsync(compact, dev, bytes, cudaMemcpyDeviceToHost, st);
+  if (flags & TMGPU_HOST_PTRS) cudaFreeAsync(dev, st);
+  cudaError_t e2 = cudaStreamSynchronize(st);
+  return cuda_err(err, e != cudaSuccess ? e : e2, "tmgpu_forest_interior");
+}
+
+int tmgpu_forest_grids(tmgpu_forest* f, double* ghosted_host, int to_device, tmgpu_error* err) {
+  if (err) std::memset(err, 0, sizeof(*err));
+  if (int rc = ready(f, err)) return rc;
+  const size_t bytes = (size_t)f->nslots * f->forest.config().vars * 1728 * sizeof(double);
+  cudaError_t e = to_device ? cudaMemcpy(f->arena, ghosted_host, bytes, cudaMemcpyHostToDevice)
+                            : cudaMemcpy(ghosted_host, f->arena, bytes, cudaMemcpyDeviceToHost);
+  return cuda_err(err, e, "tmgpu_forest_grids");
+}
+
+int tmgpu_forest_fill_ghosts(tmgpu_forest* f, void* stream, tmgpu_error* err) {
+  if (err) std::memset(err, 0, sizeof(*err));
+  if (int rc = ready(f, err)) return rc;
+  cudaStream_t st = as_stream(stream);
+  int e = exchange(f, st);
+  if (e) return cuda_err(err, (cudaError_t)e, "tmgpu_forest_fill_ghosts");
+  return cuda_err(err, cudaStreamSynchronize(st), "tmgpu_forest_fill_ghosts");
+}
+
+int tmgpu_forest_max_wavespeed(tmgpu_forest* f, double gamma, double* per_leaf_host,
+                               tmgpu_error* err) {
+  if (err) std::memset(err, 0, sizeof(*err));
+  if (int rc = ready(f, err)) return rc;
+  const int V = f->forest.config().vars;
+  cudaStream_t st = cudaStreamPerThread;
+  cudaError_t e = launch_max_wavespeed(f->arena, (long long)V * 1728, nullptr, 0, nullptr, gamma, V,
+                                       f->nslots, f->speeds, st);
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(per_leaf_host, f->speeds, f->nslots * sizeof(double), cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  return cuda_err(err, e, "tmgpu_forest_max_wavespeed");
+}
+
+// One SSP-RK3 step (rk3.hpp:16-34): [cfl dt] then 3 x
+// (ghost exchange -> aggregated stage kernel over every leaf, in place, with
+// the rk3_combine epilogue). cfl > 0: dt = cfl * min(dx / max_wavespeed)
+// computed on the device; else `dt` is used. With TMGPU_ASYNC the call only
+// enqueues; tmgpu_forest_check reports errors later.
+int tmgpu_forest_step(tmgpu_forest* f, double dt, double cfl, double gamma, int flags, void* stream,
+                      double* dt_used, tmgpu_error* err) {
+  if (err) std::memset(err, 0, sizeof(*err));
+  if (int rc = ready(f, err)) return rc;
+  const int V = f->forest.config().vars;
+  if (V != 5) return fail(err, TMGPU_ERR_INVALID, "the hydro step is Euler (vars 5)");
+  cudaStream_t st = as_stream(stream);
+  cudaError_t e = cudaSuccess;
+  const bool timed = f->timing;
+  if (timed) {
+    collect_timing(f);  // events are reused: fold the previous step in first
+    cudaEventRecord(f->ev[0], st);
+  }
+  if (!(flags & TMGPU_ASYNC)) e = cudaMemsetAsync(f->err_dev, 0xff, sizeof(unsigned long long), st);
+  if (e == cudaSuccess && cfl > 0.0) {
+    e = launch_max_wavespeed(f->arena, (long long)V * 1728, nullptr, 0, nullptr, gamma, V, f->nslots,
+                             f->speeds, st);
+    if (e == cudaSuccess) e = launch_cfl_reduce(f->speeds, f->leaf_dx, f->nslots, cfl, f->dt_dev, st);
+  }
+  if (timed) cudaEventRecord(f->ev[1], st);
+  StageLaunch p{};
+  p.hdr = nullptr;
+  p.leaf_dx = f->leaf_dx;
+  p.g_mode = 1.0;
+  p.g_dt = dt;
+  p.g_gamma = gamma;
+  p.dt_ptr = cfl > 0.0 ? f->dt_dev : nullptr;
+  p.out = f->arena;
+  p.out_stride = (long long)V * 1728;
+  p.out_ghosted = 1;
+  p.faces = nullptr;
+  p.diag = f->diag;
+  p.diag_stride = 1;
+  p.u0 = f->u0;
+  p.u0_stride = (long long)V * 512;
+  p.err = f->err_dev;
+  p.count = (int)f->nslots;
+  for (int stage = 1; stage <= 3 && e == cudaSuccess; ++stage) {
+    int x = exchange(f, st);
+    if (x) {
+      e = (cudaError_t)x;
+      break;
+    }
+    if (timed) cudaEventRecord(f->ev[2 * stage], st);
+    p.rk_stage = stage;
+    p.u0_save = stage == 1 ? f->u0 : nullptr;
+    p.u0_save_stride = (long long)V * 512;
+    e = launch_stage(V, (flags & TMGPU_FAST) != 0, f->maps, p, st);
+    if (timed) cudaEventRecord(f->ev[2 * stage + 1], st);
+  }
+  if (timed && e == cudaSuccess) f->pending_timed = 1;
+  if (e != cudaSuccess) return cuda_err(err, e, "tmgpu_forest_step");
+  if (flags & TMGPU_ASYNC) return TMGPU_OK;
+  unsigned long long w = ~0ull;
+  double dtv = dt;
+  e = cudaMemcpyAsync(&w, f->err_dev, sizeof(w), cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess && cfl > 0.0)
+    e = cudaMemcpyAsync(&dtv, f->dt_dev, sizeof(double), cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) return cuda_err(err, e, "tmgpu_forest_step");
+  if (dt_used) *dt_used = dtv;
+  if (cfl > 0.0 && !std::isfinite(dtv))
+    return fail(err, TMGPU_ERR_SOLVER, "cfl_dt: no wave speed (s = 0 everywhere)");
+  if (w != ~0ull) return solver_err_from_word(err, w);
+  return TMGPU_OK;
+}
+
+// Per-phase device timing of subsequent steps (CUDA events on the step's
+// stream): accumulated milliseconds for the CFL reduction, the ghost
+// exchanges and the stage kernels.
+int tmgpu_forest_set_timing(tmgpu_forest* f, int on, tmgpu_error* err) {
+  if (err) std::memset(err, 0, sizeof(*err));
+  if (on && !f->ev[0])
+    for (auto& e : f->ev) cudaEventCreate(&e);
+  f->timing = on != 0;
+  f->t_cfl = f->t_exchange = f->t_stage = 0;
+  f->timed_steps = f->pending_timed = 0;
+  return TMGPU_OK;
+}
+
+int tmgpu_forest_timing(tmgpu_forest* f, double* ms_cfl, double* ms_exchange, double* ms_stage,
+                        long long* steps) {
+  collect_timing(f);
+  *ms_cfl = f->t_cfl;
+  *ms_exchange = f->t_exchange;
+  *ms_stage = f->t_stage;
+  *steps = f->timed_steps;
+  return TMGPU_OK;
+}
+
+// Errors latched by TMGPU_ASYNC steps since the last check (synchronises).
+int tmgpu_forest_check(tmgpu_forest* f, void* stream, tmgpu_error* err) {
+  if (err) std::memset(err, 0, sizeof(*err));
+  if (int rc = ready(f, err)) return rc;
+  cudaStream_t st = as_stream(stream);
+  unsigned long long w = ~0ull;
+  cudaError_t e = cudaMemcpyAsync(&w, f->err_dev, sizeof(w), cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaMemsetAsync(f->err_dev, 0xff, sizeof(w), st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) return cuda_err(err, e, "tmgpu_forest_check");
+  if (w != ~0ull) return solver_err_from_word(err, w);
+  return TMGPU_OK;
+}
+
+int tmgpu_forest_floor_hits(tmgpu_forest* f, double* per_leaf_host, tmgpu_error* err) {
+  if (err) std::memset(err, 0, sizeof(*err));
+  if (int rc = ready(f, err)) return rc;
+  return cuda_err(err, cudaMemcpy(per_leaf_host, f->diag, f->nslots * sizeof(double), cudaMemcpyDeviceToHost),
+                  "tmgpu_forest_floor_hits");
+}
+
+// ------------------------------------------------------------- indexing
+int tmgpu_morton_encode(int level, uint64_t i, uint64_t j, uint64_t k, uint64_t* index,
+                        tmgpu_error* err) {
+  if (err) std::memset(err, 0, sizeof(*err));
+  try {
+    *index = morton_encode(level, i, j, k);
+    return TMGPU_OK;
+  } catch (const std::exception& ex) {
+    return fail(err, TMGPU_ERR_AMR, ex.what());
+  }
+}
+
+int tmgpu_morton_decode(int level, uint64_t index, uint64_t* ijk, tmgpu_error* err) {
+  if (err) std::memset(err, 0, sizeof(*err));
+  try {
+    morton_decode(level, index, ijk[0], ijk[1], ijk[2]);
+    return TMGPU_OK;
+  } catch (const std::exception& ex) {
+    return fail(err, TMGPU_ERR_AMR, ex.what());
+  }
+}
+
+uint64_t tmgpu_morton_dfs_rank(int level, uint64_t index) { return morton_dfs_rank(level, index); }
+
+int tmgpu_partition_leaves(const uint64_t* weights, size_t n, int localities, int* owner,
+                           tmgpu_error* err) {
+  if (err) std::memset(err, 0, sizeof(*err));
+  try {
+    auto o = partition_leaves(std::vector<uint64_t>(weights, weights + n), localities);
+    std::memcpy(owner, o.data(), o.size() * sizeof(int));
+    return TMGPU_OK;
+  } catch (const std::exception& ex) {
+    return fail(err, TMGPU_ERR_AMR, ex.what());
+  }
+}
+
+}  // extern "C"

@@ -1,6 +1,7 @@
 // C ABI: hydro stage entry points (include/tmgpu.h). Host-side only; the
 // kernels live in stage.cu.
 #include <cstring>
+#include <mutex>
 #include <string>
 
 #include "tmgpu_internal.h"
@@ -33,6 +34,21 @@ int solver_error(tmgpu_error* err, unsigned long long word) {
   return TMGPU_ERR_SOLVER;
 }
 
+// Stream-ordered allocations are served from the device's default memory pool;
+// keep freed blocks cached in the pool (release threshold = max) so repeated
+// calls do not remap memory.
+void keep_pool_warm() {
+  static std::once_flag once;
+  std::call_once(once, [] {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return;
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) != cudaSuccess) return;
+    uint64_t thr = ~0ull;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  });
+}
+
 // Device-pointer fused stage over packed slices; synchronises `st`.
 int stage_fused_device(const double* in, double* out, size_t in_slice, size_t out_slice,
                        size_t count, int vars, bool fast, cudaStream_t st, tmgpu_error* err) {
@@ -41,6 +57,7 @@ int stage_fused_device(const double* in, double* out, size_t in_slice, size_t ou
   std::string why;
   int rc = make_stage_maps(in + kHeader, vars, (long long)in_slice, (long long)count, &maps, &why);
   if (rc != TMGPU_OK) return set_err(err, rc, why.c_str());
+  keep_pool_warm();
   unsigned long long* d_err = nullptr;
   cudaError_t e = cudaMallocAsync(&d_err, sizeof(unsigned long long), st);
   if (e != cudaSuccess) return cuda_err(err, e, "cudaMallocAsync");
@@ -100,6 +117,7 @@ int tmgpu_stage_fused(const double* in, double* out, size_t in_slice, size_t out
     return stage_fused_device(in, out, in_slice, out_slice, count, vars, fast, st, err);
 
   // Host buffers: stage through stream-ordered device allocations.
+  keep_pool_warm();
   const size_t in_bytes = count * in_slice * sizeof(double);
   const size_t out_bytes = count * out_slice * sizeof(double);
   double *d_in = nullptr, *d_out = nullptr;

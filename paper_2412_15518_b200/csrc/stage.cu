@@ -105,7 +105,41 @@ __global__ void rk3_combine_kernel(int stage, const double* __restrict__ u0,
   }
 }
 
+// dt = cfl * min_leaf(dx_leaf / smax_leaf) (min over cells
+// of dx/s equals dx / max s because IEEE division is monotone). One block.
+__global__ void __launch_bounds__(1024) cfl_reduce_kernel(const double* __restrict__ speeds,
+                                                          const double* __restrict__ leaf_dx,
+                                                          long long n, double cfl,
+                                                          double* __restrict__ dt) {
+  __shared__ double red[32];
+  double m = __longlong_as_double(0x7ff0000000000000ll);  // +inf
+  for (long long i = threadIdx.x; i < n; i += blockDim.x) {
+    const double s = speeds[i];
+    if (s > 0.0) {
+      const double q = leaf_dx[i] / s;
+      m = q < m ? q : m;
+    }
+  }
+  for (int off = 16; off > 0; off >>= 1) {
+    const double o = __shfl_xor_sync(0xffffffffu, m, off);
+    m = o < m ? o : m;
+  }
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) m = red[w] < m ? red[w] : m;
+    dt[0] = cfl * m;
+  }
+}
+
 }  // namespace
+
+cudaError_t launch_cfl_reduce(const double* speeds, const double* leaf_dx, long long n, double cfl,
+                              double* dt, cudaStream_t stream) {
+  cfl_reduce_kernel<<<1, 1024, 0, stream>>>(speeds, leaf_dx, n, cfl, dt);
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return cudaGetLastError();
+}
 
 int make_stage_maps(const double* base, int V, long long slot_stride, long long count,
                     StageMaps* maps, std::string* why) {

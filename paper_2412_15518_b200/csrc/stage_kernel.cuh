@@ -361,7 +361,7 @@ __global__ void __launch_bounds__(kStageThreads, 2)
   } else {
     mode = p.g_mode;
     dx = p.leaf_dx[slot];
-    dt = p.g_dt;
+    dt = p.dt_ptr ? *p.dt_ptr : p.g_dt;
     gamma = p.g_gamma;
     ax = p.g_ax;
     ay = p.g_ay;
@@ -405,6 +405,11 @@ __global__ void __launch_bounds__(kStageThreads, 2)
       const int ci = ((z - 2) * kE + (y - 2)) * kE + (x - 2);
 #pragma unroll
       for (int v = 0; v < V; ++v) acc[v * kE3 + ci] = u[v];
+      if (p.u0_save) {
+        double* u0s = p.u0_save + (long long)slot * p.u0_save_stride;
+#pragma unroll
+        for (int v = 0; v < V; ++v) u0s[v * kE3 + ci] = u[v];
+      }
     }
     if constexpr (V == 5) {
       if (euler) {

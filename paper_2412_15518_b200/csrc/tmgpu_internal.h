@@ -21,6 +21,7 @@ struct StageLaunch {
   long long hdr_stride;
   const double* leaf_dx;
   double g_mode, g_dt, g_gamma, g_ax, g_ay, g_az;
+  const double* dt_ptr;  // arena mode: dt read from device memory when non-null
   // interior destination
   double* out;
   long long out_stride;
@@ -34,6 +35,8 @@ struct StageLaunch {
   const double* u0;
   long long u0_stride;
   int rk_stage;
+  double* u0_save;  // optional: interior state before the update -> compact [V][E^3]
+  long long u0_save_stride;
   const int* index;  // optional: tensor slot of CTA b = index[b]
   unsigned long long* err;  // atomicMin of (slice << 32 | var-major interior index)
   int count;
@@ -58,6 +61,9 @@ cudaError_t launch_stage(int V, bool fast, const StageMaps& maps, const StageLau
 cudaError_t launch_max_wavespeed(const double* in, long long slot_stride, const double* hdr,
                                  long long hdr_stride, const double* leaf_dx, double g_gamma,
                                  int V, long long count, double* result, cudaStream_t stream);
+
+cudaError_t launch_cfl_reduce(const double* speeds, const double* leaf_dx, long long n, double cfl,
+                              double* dt, cudaStream_t stream);
 
 cudaError_t launch_rk3_combine(int stage, const double* u0, const double* v, double* out,
                                long long n, cudaStream_t stream);

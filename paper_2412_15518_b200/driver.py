@@ -1,0 +1,39 @@
+"""SSP-RK3 hydro step driver on the device (the reference specifies the
+step, but ships no driver: proj/tools/taskmesh_cli.cpp:1).
+
+One step = [CFL dt on device] + 3 x (reference-exact ghost exchange ->
+aggregated stage kernel over every leaf of the arena, in place, with the
+rk3_combine epilogue, rk3.hpp:18-27).
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+from . import _lib
+from ._lib import TmgpuError, lib
+from .amr import Forest
+from .hydro import SolverError
+
+
+class HydroDriver:
+    def __init__(self, forest: Forest, gamma: float = 1.4, cfl: float = 0.4, fast: bool = False):
+        self.forest, self.gamma, self.cfl, self.fast = forest, gamma, cfl, fast
+        self.steps = 0
+
+    def step(self, dt: float | None = None, stream=None, sync: bool = True) -> float | None:
+        """Advance one SSP-RK3 step. dt None: CFL dt on the device. Returns
+        the dt used (None when sync=False; errors are then latched until
+        ``check``)."""
+        flags = (_lib.TMGPU_FAST if self.fast else 0) | (0 if sync else _lib.TMGPU_ASYNC)
+        used = C.c_double(0.0)
+        err = TmgpuError()
+        rc = lib.tmgpu_forest_step(self.forest.h, float(dt or 0.0),
+                                   self.cfl if dt is None else 0.0, self.gamma, flags, stream,
+                                   C.byref(used), C.byref(err))
+        _lib.check(rc, err, SolverError)
+        self.steps += 1
+        return used.value if sync else None
+
+    def check(self, stream=None) -> None:
+        err = TmgpuError()
+        _lib.check(lib.tmgpu_forest_check(self.forest.h, stream, C.byref(err)), err, SolverError)

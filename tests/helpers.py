@@ -1,0 +1,29 @@
+"""Shared test helpers (test infrastructure)."""
+import numpy as np
+
+from paper_2412_15518_b200 import amr
+
+
+def replay_on_reference(ref, f, max_level, bc=(0, 0, 0), root_dims=(1, 1, 1)):
+    """Rebuild a forest topology inside the reference Tree by refining every
+    internal node in level order (cascades only touch nodes internal in ours)."""
+    internal = set()
+    for p in f.leaves():
+        lvl, ci, cj, ck = amr.unpack(int(p))
+        for l in range(lvl):
+            s = lvl - l
+            internal.add(amr.pack(l, ci >> s, cj >> s, ck >> s))
+    t = ref.tree(max_level=max_level, bc=bc, root_dims=root_dims)
+    for p in sorted(internal, key=lambda q: (q >> 60, q)):
+        if p in set(int(x) for x in t.leaves()):
+            t.refine(p)
+    return t
+
+
+def interior_to_ghosted(compact, edge=8, ghost=2):
+    """compact [n][V][E^3] -> ghosted [n][V*S^3] with zero ghosts."""
+    n, V, _ = compact.shape
+    S = edge + 2 * ghost
+    g = np.zeros((n, V, S, S, S))
+    g[:, :, ghost:ghost + edge, ghost:ghost + edge, ghost:ghost + edge] = compact.reshape(n, V, edge, edge, edge)
+    return g.reshape(n, -1)
