@@ -115,8 +115,8 @@ def build_workload(args):
 
 def workload_config(f, args, extra=None):
     n = f.leaf_count()
-    cfg = {"workload": f"rotating star, {args.max_level - args.min_level + 1}-level AMR octree "
-                       f"(levels {args.min_level}-{args.max_level}), {n} leaves x 8^3 cells, full "
+    cfg = {"workload": f"rotating star, {args.max_level}-level AMR octree "
+                       f"(leaf levels {args.min_level}-{args.max_level}), {n} leaves x 8^3 cells, full "
                        "SSP-RK3 hydro step: CFL dt + 3 x (ghost exchange + aggregated stage + rk3 combine)",
            "leaves": n, "cells": n * 512, "subgrid": "8^3 + 2 ghost layers, 5 vars (Euler)",
            "l2": "inputs larger than L2 (ghosted arena %.0f MB > 126 MB L2)" % (n * 69120 / 1e6),

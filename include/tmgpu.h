@@ -41,6 +41,7 @@ typedef struct tmgpu_error {
 #define TMGPU_HOST_PTRS 0x1  /* in/out are host memory: H2D, kernel, D2H inside the call */
 #define TMGPU_FAST 0x2       /* FMA/reciprocal arithmetic: parity within 1e-10 (scaled), not bitwise */
 #define TMGPU_ASYNC 0x4      /* enqueue only; errors latched until tmgpu_forest_check */
+#define TMGPU_EXACT_GHOSTS 0x8 /* step: reference 3-pass full-shell exchange instead of one-round faces */
 
 /* ---------------------------------------------------------------- hydro
  * Slice contract (reference stage.hpp:8-12, 39-66):
@@ -127,6 +128,9 @@ int tmgpu_forest_interior(tmgpu_forest* f, double* compact, int to_device, int f
 int tmgpu_forest_grids(tmgpu_forest* f, double* ghosted_host, int to_device, tmgpu_error* err);
 /* ghost::fill_ghosts_sync (ghost.cpp:282-296), bitwise on the full ghosted arrays */
 int tmgpu_forest_fill_ghosts(tmgpu_forest* f, void* stream, tmgpu_error* err);
+/* one-round face-only exchange: every ghost the stage reads, bitwise equal to
+ * fill_ghosts_sync; edge/corner ghosts are left untouched */
+int tmgpu_forest_fill_faces(tmgpu_forest* f, void* stream, tmgpu_error* err);
 /* hydro::max_wavespeed per leaf (stage.cpp:248-272) */
 int tmgpu_forest_max_wavespeed(tmgpu_forest* f, double gamma, double* per_leaf_host, tmgpu_error* err);
 /* SSP-RK3 step (rk3.hpp): 3 x (fill_ghosts_sync -> aggregated

@@ -22,6 +22,8 @@ TMGPU_ERR_AGG = 5
 
 TMGPU_HOST_PTRS = 0x1
 TMGPU_FAST = 0x2
+TMGPU_ASYNC = 0x4
+TMGPU_EXACT_GHOSTS = 0x8
 
 
 class TmgpuError(C.Structure):

@@ -53,6 +53,7 @@ _sig("tmgpu_forest_arena", _vp, [_vp])
 _sig("tmgpu_forest_interior", C.c_int, [_vp, _vp, C.c_int, C.c_int, _vp, _ep])
 _sig("tmgpu_forest_grids", C.c_int, [_vp, _vp, C.c_int, _ep])
 _sig("tmgpu_forest_fill_ghosts", C.c_int, [_vp, _vp, _ep])
+_sig("tmgpu_forest_fill_faces", C.c_int, [_vp, _vp, _ep])
 _sig("tmgpu_forest_max_wavespeed", C.c_int, [_vp, C.c_double, _vp, _ep])
 _sig("tmgpu_forest_step", C.c_int, [_vp, C.c_double, C.c_double, C.c_double, C.c_int, _vp, _dp,
                                     _ep])
@@ -248,6 +249,12 @@ class Forest:
         """ghost::fill_ghosts_sync (ghost.cpp:282-296) on the device."""
         err = TmgpuError()
         _lib.check(lib.tmgpu_forest_fill_ghosts(self.h, stream, C.byref(err)), err)
+
+    def fill_faces(self, stream=None) -> None:
+        """One-round face-only exchange (the step's default): every ghost the
+        stage reads, bitwise equal to fill_ghosts_sync; edges/corners untouched."""
+        err = TmgpuError()
+        _lib.check(lib.tmgpu_forest_fill_faces(self.h, stream, C.byref(err)), err)
 
     def max_wavespeed(self, gamma: float = 1.4) -> np.ndarray:
         out = np.zeros(self.leaf_count())

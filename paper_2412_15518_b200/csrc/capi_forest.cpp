@@ -20,6 +20,7 @@ struct tmgpu_forest {
   long long nslots = 0;
   double* arena = nullptr;    // [slot][V][S^3]
   double* u0 = nullptr;       // [slot][V][E^3]
+  double* xfer = nullptr;     // [slot][V][E^3] host-transfer staging (lazy)
   double* leaf_dx = nullptr;  // [slot]
   double* speeds = nullptr;   // [slot]
   double* diag = nullptr;     // [slot] floor hits of the last stage
@@ -30,6 +31,9 @@ struct tmgpu_forest {
   int* staged_of[3] = {nullptr, nullptr, nullptr};
   int* prolong[3] = {nullptr, nullptr, nullptr};
   GhostPassDev pass[3];
+  FaceSrc* faces = nullptr;          // [slot][6] one-round face sources
+  GhostFill* prolong_all = nullptr;  // coarser fills of all axes (one-round snapshot)
+  int n_prolong_all = 0;
   StageMaps maps{};
   uint64_t exchanges = 0;  // ghost exchanges performed (structural counter)
   // optional per-phase device timing: events [start, cfl, (exch, stage) x 3]
@@ -65,12 +69,19 @@ void free_dev(tmgpu_forest* f) {
   };
   fr(f->arena);
   fr(f->u0);
+  fr(f->xfer);
+  f->xfer = nullptr;
   fr(f->leaf_dx);
   fr(f->speeds);
   fr(f->diag);
   fr(f->dt_dev);
   fr(f->err_dev);
   fr(f->staged);
+  fr(f->faces);
+  fr(f->prolong_all);
+  f->faces = nullptr;
+  f->prolong_all = nullptr;
+  f->n_prolong_all = 0;
   for (int a = 0; a < 3; ++a) {
     fr(f->fills[a]);
     fr(f->staged_of[a]);
@@ -116,12 +127,31 @@ int alloc_device(tmgpu_forest* f, tmgpu_error* err) {
   M((void**)&f->dt_dev, sizeof(double));
   M((void**)&f->err_dev, sizeof(unsigned long long));
   if (e == cudaSuccess) e = cudaMemset(f->arena, 0, n * V * S3 * sizeof(double));  // SubGrid() zeroes
+  if (e == cudaSuccess) e = cudaMemset(f->err_dev, 0xff, sizeof(unsigned long long));  // no error
   std::vector<double> dx(n);
   for (long long s = 0; s < n; ++s) dx[s] = f->forest.cell_size(lv[s].level);
   if (e == cudaSuccess) e = cudaMemcpy(f->leaf_dx, dx.data(), n * sizeof(double), cudaMemcpyHostToDevice);
   size_t max_prolong = 0;
+  std::vector<FaceSrc> fsrc(n * 6);
+  for (auto& x : fsrc) {
+    std::memset(&x, 0, sizeof(x));
+    x.kind = 3;
+  }
+  std::vector<GhostFill> pall;
   for (int a = 0; a < 3 && e == cudaSuccess; ++a) {
     const std::vector<Fill> plan = f->forest.plan_axis(a);
+    for (const Fill& p : plan) {
+      FaceSrc& fs = fsrc[(size_t)p.dst * 6 + 2 * a + (p.dir > 0 ? 1 : 0)];
+      fs.kind = p.kind;
+      if (p.kind == 2)
+        fs.src[p.qt2 * 2 + p.qt1] = p.src;
+      else
+        fs.src[0] = p.src;
+      if (p.kind == 1) {
+        fs.staged = (int)pall.size();
+        pall.push_back(GhostFill{p.dst, p.src, p.kind, p.axis, p.dir, p.qt1, p.qt2, {0, 0, 0}});
+      }
+    }
     std::vector<GhostFill> gf(plan.size());
     std::vector<int> sof(plan.size(), -1), pro;
     for (size_t i = 0; i < plan.size(); ++i) {
@@ -145,7 +175,15 @@ int alloc_device(tmgpu_forest* f, tmgpu_error* err) {
     f->pass[a] = GhostPassDev{f->fills[a], f->staged_of[a], f->prolong[a], (int)gf.size(),
                               (int)pro.size()};
   }
+  max_prolong = std::max(max_prolong, pall.size());
   M((void**)&f->staged, max_prolong * V * 8 * 8 * 2 * sizeof(double));
+  M((void**)&f->faces, fsrc.size() * sizeof(FaceSrc));
+  M((void**)&f->prolong_all, pall.size() * sizeof(GhostFill));
+  if (e == cudaSuccess && !fsrc.empty())
+    e = cudaMemcpy(f->faces, fsrc.data(), fsrc.size() * sizeof(FaceSrc), cudaMemcpyHostToDevice);
+  if (e == cudaSuccess && !pall.empty())
+    e = cudaMemcpy(f->prolong_all, pall.data(), pall.size() * sizeof(GhostFill), cudaMemcpyHostToDevice);
+  f->n_prolong_all = (int)pall.size();
   if (e != cudaSuccess) {
     free_dev(f);
     return cuda_err(err, e, "tmgpu_forest_alloc");
@@ -161,10 +199,18 @@ int alloc_device(tmgpu_forest* f, tmgpu_error* err) {
   return TMGPU_OK;
 }
 
-int exchange(tmgpu_forest* f, cudaStream_t st) {
+// exact = reference-exact 3-pass fill of the full ghost shell (ghost.cpp:282-296);
+// otherwise the one-round face-only exchange (bitwise on every stage-visible ghost).
+int exchange(tmgpu_forest* f, cudaStream_t st, bool exact) {
   const int V = f->forest.config().vars;
-  for (int a = 0; a < 3; ++a) {
-    cudaError_t e = ghost_pass(f->arena, V, f->pass[a], f->staged, st);
+  if (exact) {
+    for (int a = 0; a < 3; ++a) {
+      cudaError_t e = ghost_pass(f->arena, V, f->pass[a], f->staged, st);
+      if (e != cudaSuccess) return (int)e;
+    }
+  } else {
+    cudaError_t e = ghost_exchange_faces(f->arena, V, f->nslots, f->faces, f->prolong_all,
+                                         f->n_prolong_all, f->staged, st);
     if (e != cudaSuccess) return (int)e;
   }
   f->exchanges += 1;
@@ -308,14 +354,14 @@ int tmgpu_forest_interior(tmgpu_forest* f, double* compact, int to_device, int f
   double* dev = compact;
   cudaError_t e = cudaSuccess;
   if (flags & TMGPU_HOST_PTRS) {
-    e = cudaMallocAsync(&dev, bytes ? bytes : 8, st);
+    if (!f->xfer) e = cudaMalloc(&f->xfer, bytes ? bytes : 8);
+    dev = f->xfer;
     if (e == cudaSuccess && to_device) e = cudaMemcpyAsync(dev, compact, bytes, cudaMemcpyHostToDevice, st);
   }
   if (e == cudaSuccess) e = interior_copy(f->arena, dev, V, f->nslots, to_device != 0, st);
   if (e == cudaSuccess && (flags & TMGPU_HOST_PTRS) && !to_device)
     e = cudaMemcpyAsync(compact, dev, bytes, cudaMemcpyDeviceToHost, st);
-  if (flags & TMGPU_HOST_PTRS) cudaFreeAsync(dev, st);
-  cudaError_t e2 = cudaStreamSynchronize(st);
+  cudaError_t e2 = (flags & TMGPU_ASYNC) ? cudaSuccess : cudaStreamSynchronize(st);
   return cuda_err(err, e != cudaSuccess ? e : e2, "tmgpu_forest_interior");
 }
 
@@ -332,9 +378,19 @@ int tmgpu_forest_fill_ghosts(tmgpu_forest* f, void* stream, tmgpu_error* err) {
   if (err) std::memset(err, 0, sizeof(*err));
   if (int rc = ready(f, err)) return rc;
   cudaStream_t st = as_stream(stream);
-  int e = exchange(f, st);
+  int e = exchange(f, st, true);
   if (e) return cuda_err(err, (cudaError_t)e, "tmgpu_forest_fill_ghosts");
   return cuda_err(err, cudaStreamSynchronize(st), "tmgpu_forest_fill_ghosts");
+}
+
+// One-round face-only exchange (the step's default).
+int tmgpu_forest_fill_faces(tmgpu_forest* f, void* stream, tmgpu_error* err) {
+  if (err) std::memset(err, 0, sizeof(*err));
+  if (int rc = ready(f, err)) return rc;
+  cudaStream_t st = as_stream(stream);
+  int e = exchange(f, st, false);
+  if (e) return cuda_err(err, (cudaError_t)e, "tmgpu_forest_fill_faces");
+  return cuda_err(err, cudaStreamSynchronize(st), "tmgpu_forest_fill_faces");
 }
 
 int tmgpu_forest_max_wavespeed(tmgpu_forest* f, double gamma, double* per_leaf_host,
@@ -394,7 +450,7 @@ int tmgpu_forest_step(tmgpu_forest* f, double dt, double cfl, double gamma, int 
   p.err = f->err_dev;
   p.count = (int)f->nslots;
   for (int stage = 1; stage <= 3 && e == cudaSuccess; ++stage) {
-    int x = exchange(f, st);
+    int x = exchange(f, st, (flags & TMGPU_EXACT_GHOSTS) != 0);
     if (x) {
       e = (cudaError_t)x;
       break;

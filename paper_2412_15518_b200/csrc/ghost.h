@@ -25,6 +25,23 @@ struct GhostPassDev {
   int n_prolong = 0;
 };
 
+// Per destination leaf and face (2*axis + (dir>0)): where its face ghosts come
+// from in the one-round exchange.
+struct alignas(16) FaceSrc {
+  int32_t src[4];  // same/coarser: src[0]; finer: quadrant (qt2*2+qt1); boundary: unused
+  int32_t staged;  // coarser: index of the snapshot slab
+  int8_t kind;     // 0 same, 1 coarser, 2 finer, 3 boundary
+  int8_t pad[11];
+};
+
+// One-round, face-only exchange (production): snapshot every prolonged slab
+// of all three axes from the pre-exchange state, then one CTA per leaf pulls
+// its six E x E x G face-ghost slabs. Bitwise identical to the reference on
+// every ghost the stage reads; edge/corner ghosts untouched.
+cudaError_t ghost_exchange_faces(double* arena, int V, long long nslots, const FaceSrc* faces,
+                                 const GhostFill* prolong_fills, int n_prolong, double* staged,
+                                 cudaStream_t st);
+
 // Phase 1 (prolonged snapshot) + phase 2 (apply) of one axis pass.
 cudaError_t ghost_pass(double* arena, int V, const GhostPassDev& pass, double* staged,
                        cudaStream_t st);

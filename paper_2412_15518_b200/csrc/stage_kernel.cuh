@@ -58,7 +58,8 @@ struct Lay {
   static constexpr int B4 = B3 + V * 128;
   static constexpr int kStaged = B4 + V * 128;  // = V*1280 doubles
   static constexpr int kAcc = kStaged;          // accumulator [V][E^3]
-  static constexpr int kDoubles = kAcc + V * kE3;
+  static constexpr int kU0 = kAcc + V * kE3;     // RK3 u0 block [V][E^3] (bulk-copied)
+  static constexpr int kDoubles = kU0 + V * kE3;
   static constexpr int kBytes = kDoubles * 8 + 64;  // + mbarrier/scratch
   static constexpr uint32_t kTxBytes = (uint32_t)(V * 1280 * 8);
 };
@@ -103,6 +104,15 @@ __device__ __forceinline__ void tma_load_5d(void* dst, const CUtensorMap* map, u
       : "memory");
 }
 
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes,
+                                          uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(src)), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
 // ------------------------------------------------------------------ arithmetic
 // lanes.hpp:109-113 vmax and std::max, exactly (NaN / signed-zero behaviour).
 __device__ __forceinline__ double vmax_(double x, double f) { return x > f ? x : f; }
@@ -112,6 +122,24 @@ __device__ __forceinline__ double stdmax_(double a, double b) { return (a < b) ?
 __device__ __forceinline__ double minmod_lane(double a, double b) {
   double sm = fabs(a) < fabs(b) ? a : b;
   return (a * b) > 0.0 ? sm : 0.0;
+}
+
+// Correctly rounded a / b from y = RN(1/b) (Markstein): q = RN(a*y),
+// r = a - b*q (exact via FMA), RN(q + r*y) == RN(a/b) when no operand or
+// result is near over/underflow; outside [2^-900, 2^901) (and for 0, inf,
+// NaN) it falls back to the IEEE division, so the result is bitwise the
+// reference's `a / b` for every input. Lets one reciprocal serve several
+// quotients with the same divisor (cons->prim) and a per-slice constant
+// divisor (gamma - 1) cost 3 FP64 ops instead of a full division sequence.
+__device__ __forceinline__ bool exp_ok(double x) {
+  const unsigned e = ((unsigned)__double2hiint(x) >> 20) & 0x7ffu;
+  return (e - 123u) < 1800u;
+}
+__device__ __forceinline__ double div_rn(double a, double b, double y, bool b_ok) {
+  const double q = a * y;
+  const double r = fma(-q, b, a);
+  const double q2 = fma(r, y, q);
+  return (b_ok && exp_ok(a) && exp_ok(q2)) ? q2 : a / b;
 }
 
 // euler.hpp:27-35
@@ -128,13 +156,15 @@ __device__ __forceinline__ void recon(double um1, double u0, double up1, double 
 // value is bitwise neutral.
 template <int AXIS, bool FAST>
 __device__ __forceinline__ void rusanov(const double (&ql)[5], const double (&qr)[5], double gamma,
-                                        double gm1, double inv_gm1, double (&f)[5]) {
+                                        double gm1, double inv_gm1, bool gm1_ok, double (&f)[5]) {
   double cl, cr, el, er;
   if constexpr (!FAST) {
     cl = sqrt(gamma * ql[4] / ql[0]);
     cr = sqrt(gamma * qr[4] / qr[0]);
-    el = ql[4] / gm1 + 0.5 * ql[0] * (ql[1] * ql[1] + ql[2] * ql[2] + ql[3] * ql[3]);
-    er = qr[4] / gm1 + 0.5 * qr[0] * (qr[1] * qr[1] + qr[2] * qr[2] + qr[3] * qr[3]);
+    el = div_rn(ql[4], gm1, inv_gm1, gm1_ok) +
+         0.5 * ql[0] * (ql[1] * ql[1] + ql[2] * ql[2] + ql[3] * ql[3]);
+    er = div_rn(qr[4], gm1, inv_gm1, gm1_ok) +
+         0.5 * qr[0] * (qr[1] * qr[1] + qr[2] * qr[2] + qr[3] * qr[3]);
   } else {
     cl = sqrt(gamma * ql[4] * __drcp_rn(ql[0]));
     cr = sqrt(gamma * qr[4] * __drcp_rn(qr[0]));
@@ -240,7 +270,8 @@ __device__ __forceinline__ int interior_index(int axis, int c0, int c1, int c2) 
 template <int V, int AXIS, bool FAST, bool EULER>
 __device__ __forceinline__ void axis_pass(const double* __restrict__ sm, double* __restrict__ acc,
                                           int tid, double gamma, double gm1, double inv_gm1,
-                                          double a_vel, double cdt, double* faces_out) {
+                                          bool gm1_ok, double a_vel, double cdt,
+                                          double* faces_out) {
   int c1, c2, r, nb;
   const bool active = face_map<AXIS>(tid, c1, c2, r, nb);
   double F[3][V];
@@ -249,32 +280,52 @@ __device__ __forceinline__ void axis_pass(const double* __restrict__ sm, double*
 #pragma unroll
     for (int v = 0; v < V; ++v) F[k][v] = 0.0;
   if (active) {
+    // Stencil window: positions 3r..3r+5 along the axis serve faces 3r..3r+2.
+    // Each cell's limited slope m[j] = minmod(d[j-1], d[j]) is computed once
+    // and shared by the right state of face j-2 and the left state of face
+    // j-1 (the reference evaluates the identical expression twice,
+    // euler.hpp:32-33).
     const int base = 3 * r;
+    int a[6], vs[6];
+#pragma unroll
+    for (int s = 0; s < 6; ++s) pos_addr<V, AXIS>(base + s, c1, c2, a[s], vs[s]);
+    constexpr int NV = EULER ? 5 : 1;
+    double ql[3][NV], qr[3][NV];
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+      double c[6], d[5], m[5];
+#pragma unroll
+      for (int s = 0; s < 6; ++s) c[s] = sm[a[s] + v * vs[s]];
+#pragma unroll
+      for (int i = 0; i < 5; ++i) d[i] = c[i + 1] - c[i];
+#pragma unroll
+      for (int j = 1; j < 5; ++j) m[j] = minmod_lane(d[j - 1], d[j]);
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        ql[k][v] = c[k + 1] + 0.5 * m[k + 1];
+        qr[k][v] = c[k + 2] - 0.5 * m[k + 2];
+      }
+    }
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
-      const int f0 = base + k;  // face f0: stencil positions f0..f0+3
-      int a[4], vs[4];
-#pragma unroll
-      for (int s = 0; s < 4; ++s) pos_addr<V, AXIS>(f0 + s, c1, c2, a[s], vs[s]);
       if constexpr (EULER) {
-        double ql[5], qr[5];
+        double l5[5], r5[5], f[5];
 #pragma unroll
-        for (int v = 0; v < 5; ++v)
-          recon(sm[a[0] + v * vs[0]], sm[a[1] + v * vs[1]], sm[a[2] + v * vs[2]],
-                sm[a[3] + v * vs[3]], ql[v], qr[v]);
+        for (int v = 0; v < 5; ++v) {
+          l5[v] = ql[k][v];
+          r5[v] = qr[k][v];
+        }
         // stage.cpp:80-83 face floors
-        ql[0] = vmax_(ql[0], kRhoFloor);
-        qr[0] = vmax_(qr[0], kRhoFloor);
-        ql[4] = vmax_(ql[4], kPressureFloor);
-        qr[4] = vmax_(qr[4], kPressureFloor);
-        double f[5];
-        rusanov<AXIS, FAST>(ql, qr, gamma, gm1, inv_gm1, f);
+        l5[0] = vmax_(l5[0], kRhoFloor);
+        r5[0] = vmax_(r5[0], kRhoFloor);
+        l5[4] = vmax_(l5[4], kPressureFloor);
+        r5[4] = vmax_(r5[4], kPressureFloor);
+        rusanov<AXIS, FAST>(l5, r5, gamma, gm1, inv_gm1, gm1_ok, f);
 #pragma unroll
         for (int v = 0; v < 5; ++v) F[k][v] = f[v];
       } else {
         // stage.cpp:44-55 scalar advection on var 0; other vars keep zero flux
-        double l, rr;
-        recon(sm[a[0]], sm[a[1]], sm[a[2]], sm[a[3]], l, rr);
+        const double l = ql[k][0], rr = qr[k][0];
         F[k][0] = 0.5 * (a_vel * l + a_vel * rr) - 0.5 * fabs(a_vel) * (rr - l);
       }
     }
@@ -339,7 +390,10 @@ __global__ void __launch_bounds__(kStageThreads, 2)
     s_hits = 0;
     s_bad = 0xffffffffu;
     mbar_init(bar, 1);
-    mbar_expect_tx(bar, L::kTxBytes);
+    const bool want_u0 = p.u0 && p.rk_stage >= 2;
+    mbar_expect_tx(bar, L::kTxBytes + (want_u0 ? (uint32_t)(V * kE3 * 8) : 0u));
+    if (want_u0)  // u0 block rides the same barrier; consumed in the epilogue
+      bulk_load(smem + L::kU0, p.u0 + (long long)slot * p.u0_stride, V * kE3 * 8, bar);
     tma_load_5d(sm + L::B0, &tm_x, bar, 0, 2, 2, 0, slot);
     tma_load_5d(sm + L::B1, &tm_y, bar, 2, 0, 2, 0, slot);
     tma_load_5d(sm + L::B2, &tm_y, bar, 2, 10, 2, 0, slot);
@@ -370,7 +424,8 @@ __global__ void __launch_bounds__(kStageThreads, 2)
   const bool euler = mode != 0.0;
   const double cdt = dt / dx;
   const double gm1 = gamma - 1.0;
-  const double inv_gm1 = 1.0 / gm1;
+  const double inv_gm1 = 1.0 / gm1;  // RN(1/(gamma-1)) for div_rn
+  const bool gm1_ok = exp_ok(gm1) && exp_ok(inv_gm1);
 
   __syncthreads();  // barrier init visible
   mbar_wait(bar, 0);
@@ -416,9 +471,11 @@ __global__ void __launch_bounds__(kStageThreads, 2)
         const double rho = stdmax_(u[0], kRhoFloor);
         double iu, iv, iw, ke, pr;
         if constexpr (!FAST) {
-          iu = u[1] / rho;
-          iv = u[2] / rho;
-          iw = u[3] / rho;
+          const double yr = __drcp_rn(rho);  // RN(1/rho)
+          const bool rok = exp_ok(rho) && exp_ok(yr);
+          iu = div_rn(u[1], rho, yr, rok);
+          iv = div_rn(u[2], rho, yr, rok);
+          iw = div_rn(u[3], rho, yr, rok);
           ke = 0.5 * rho * (iu * iu + iv * iv + iw * iw);
           pr = stdmax_(gm1 * (u[4] - ke), kPressureFloor);
         } else {
@@ -442,20 +499,20 @@ __global__ void __launch_bounds__(kStageThreads, 2)
   // ---- phase 3: x, y, z passes
   double* faces_out = p.faces ? p.faces + (long long)slot * p.faces_stride : nullptr;
   if (V == 5 && euler) {
-    axis_pass<V, 0, FAST, (V == 5)>(sm, acc, tid, gamma, gm1, inv_gm1, 0.0, cdt, faces_out);
-    axis_pass<V, 1, FAST, (V == 5)>(sm, acc, tid, gamma, gm1, inv_gm1, 0.0, cdt, faces_out);
-    axis_pass<V, 2, FAST, (V == 5)>(sm, acc, tid, gamma, gm1, inv_gm1, 0.0, cdt, faces_out);
+    axis_pass<V, 0, FAST, (V == 5)>(sm, acc, tid, gamma, gm1, inv_gm1, gm1_ok, 0.0, cdt, faces_out);
+    axis_pass<V, 1, FAST, (V == 5)>(sm, acc, tid, gamma, gm1, inv_gm1, gm1_ok, 0.0, cdt, faces_out);
+    axis_pass<V, 2, FAST, (V == 5)>(sm, acc, tid, gamma, gm1, inv_gm1, gm1_ok, 0.0, cdt, faces_out);
   } else {
-    axis_pass<V, 0, FAST, false>(sm, acc, tid, gamma, gm1, inv_gm1, ax, cdt, faces_out);
-    axis_pass<V, 1, FAST, false>(sm, acc, tid, gamma, gm1, inv_gm1, ay, cdt, faces_out);
-    axis_pass<V, 2, FAST, false>(sm, acc, tid, gamma, gm1, inv_gm1, az, cdt, faces_out);
+    axis_pass<V, 0, FAST, false>(sm, acc, tid, gamma, gm1, inv_gm1, gm1_ok, ax, cdt, faces_out);
+    axis_pass<V, 1, FAST, false>(sm, acc, tid, gamma, gm1, inv_gm1, gm1_ok, ay, cdt, faces_out);
+    axis_pass<V, 2, FAST, false>(sm, acc, tid, gamma, gm1, inv_gm1, gm1_ok, az, cdt, faces_out);
   }
   __syncthreads();
 
   // ---- phase 4: floors, finiteness, RK3 combine, store
   unsigned int hits = 0, bad = 0xffffffffu;
   double* outp = p.out + (long long)slot * p.out_stride;
-  const double* u0p = p.u0 ? p.u0 + (long long)slot * p.u0_stride : nullptr;
+  const double* u0p = (p.u0 && p.rk_stage >= 2) ? smem + L::kU0 : nullptr;
   for (int c = tid; c < kE3; c += kStageThreads) {
     double u[V];
 #pragma unroll

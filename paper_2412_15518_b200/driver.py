@@ -16,15 +16,21 @@ from .hydro import SolverError
 
 
 class HydroDriver:
-    def __init__(self, forest: Forest, gamma: float = 1.4, cfl: float = 0.4, fast: bool = False):
+    def __init__(self, forest: Forest, gamma: float = 1.4, cfl: float = 0.4, fast: bool = False,
+                 exact_ghosts: bool = False):
+        """exact_ghosts: reference 3-pass full-shell exchange (full ghosted arrays
+        bitwise equal to the reference); default one-round face-only exchange
+        (bitwise on every ghost the stage reads, hence on the state)."""
         self.forest, self.gamma, self.cfl, self.fast = forest, gamma, cfl, fast
+        self.exact_ghosts = exact_ghosts
         self.steps = 0
 
     def step(self, dt: float | None = None, stream=None, sync: bool = True) -> float | None:
         """Advance one SSP-RK3 step. dt None: CFL dt on the device. Returns
         the dt used (None when sync=False; errors are then latched until
         ``check``)."""
-        flags = (_lib.TMGPU_FAST if self.fast else 0) | (0 if sync else _lib.TMGPU_ASYNC)
+        flags = ((_lib.TMGPU_FAST if self.fast else 0) | (0 if sync else _lib.TMGPU_ASYNC) |
+                 (_lib.TMGPU_EXACT_GHOSTS if self.exact_ghosts else 0))
         used = C.c_double(0.0)
         err = TmgpuError()
         rc = lib.tmgpu_forest_step(self.forest.h, float(dt or 0.0),

@@ -27,3 +27,13 @@ def interior_to_ghosted(compact, edge=8, ghost=2):
     g = np.zeros((n, V, S, S, S))
     g[:, :, ghost:ghost + edge, ghost:ghost + edge, ghost:ghost + edge] = compact.reshape(n, V, edge, edge, edge)
     return g.reshape(n, -1)
+
+
+def stage_visible_mask(vars_=5, edge=8, ghost=2):
+    """Cells the stage reads: interior + face ghosts (at most one coordinate
+    outside the interior range), as a flat mask over [V][S][S][S]."""
+    S = edge + 2 * ghost
+    r = np.arange(S)
+    out = (r < ghost) | (r >= ghost + edge)
+    nout = out[:, None, None].astype(int) + out[None, :, None] + out[None, None, :]
+    return np.broadcast_to(nout <= 1, (vars_, S, S, S)).reshape(-1)
