@@ -32,6 +32,10 @@ struct tmgpu_forest {
   int* prolong[3] = {nullptr, nullptr, nullptr};
   GhostPassDev pass[3];
   FaceSrc* faces = nullptr;          // [slot][6] one-round face sources
+  int* face_src = nullptr;           // [slot][6] stage-kernel TMA sources (fused same-level)
+  int2* items_all = nullptr;         // every (slot, face)
+  int2* items_cf = nullptr;          // coarse-fine + boundary (slot, face) only
+  int n_items_all = 0, n_items_cf = 0;
   GhostFill* prolong_all = nullptr;  // coarser fills of all axes (one-round snapshot)
   int n_prolong_all = 0;
   StageMaps maps{};
@@ -79,6 +83,12 @@ void free_dev(tmgpu_forest* f) {
   fr(f->staged);
   fr(f->faces);
   fr(f->prolong_all);
+  fr(f->face_src);
+  fr(f->items_all);
+  fr(f->items_cf);
+  f->face_src = nullptr;
+  f->items_all = f->items_cf = nullptr;
+  f->n_items_all = f->n_items_cf = 0;
   f->faces = nullptr;
   f->prolong_all = nullptr;
   f->n_prolong_all = 0;
@@ -184,6 +194,30 @@ int alloc_device(tmgpu_forest* f, tmgpu_error* err) {
   if (e == cudaSuccess && !pall.empty())
     e = cudaMemcpy(f->prolong_all, pall.data(), pall.size() * sizeof(GhostFill), cudaMemcpyHostToDevice);
   f->n_prolong_all = (int)pall.size();
+  {
+    std::vector<int> fsrc_code(n * 6);
+    std::vector<int2> all, cf;
+    all.reserve(n * 6);
+    for (long long s = 0; s < n; ++s)
+      for (int face = 0; face < 6; ++face) {
+        const FaceSrc& x = fsrc[(size_t)s * 6 + face];
+        const bool same = x.kind == 0;
+        fsrc_code[(size_t)s * 6 + face] = same ? ((x.src[0] << 1) | 1) : (int)(s << 1);
+        all.push_back(make_int2((int)s, face));
+        if (!same) cf.push_back(make_int2((int)s, face));
+      }
+    M((void**)&f->face_src, fsrc_code.size() * sizeof(int));
+    M((void**)&f->items_all, all.size() * sizeof(int2));
+    M((void**)&f->items_cf, cf.size() * sizeof(int2));
+    if (e == cudaSuccess && !fsrc_code.empty())
+      e = cudaMemcpy(f->face_src, fsrc_code.data(), fsrc_code.size() * sizeof(int), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess && !all.empty())
+      e = cudaMemcpy(f->items_all, all.data(), all.size() * sizeof(int2), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess && !cf.empty())
+      e = cudaMemcpy(f->items_cf, cf.data(), cf.size() * sizeof(int2), cudaMemcpyHostToDevice);
+    f->n_items_all = (int)all.size();
+    f->n_items_cf = (int)cf.size();
+  }
   if (e != cudaSuccess) {
     free_dev(f);
     return cuda_err(err, e, "tmgpu_forest_alloc");
@@ -199,20 +233,25 @@ int alloc_device(tmgpu_forest* f, tmgpu_error* err) {
   return TMGPU_OK;
 }
 
-// exact = reference-exact 3-pass fill of the full ghost shell (ghost.cpp:282-296);
-// otherwise the one-round face-only exchange (bitwise on every stage-visible ghost).
-int exchange(tmgpu_forest* f, cudaStream_t st, bool exact) {
+// Exchange modes: kExact = reference 3-pass fill of the full ghost shell
+// (ghost.cpp:282-296); kFaces = one-round fill of every face ghost; kFused =
+// one-round fill of the coarse-fine and boundary faces only, the same-level
+// faces being read by the stage kernel straight from the neighbour.
+enum ExchangeMode { kExact, kFaces, kFused };
+
+int exchange(tmgpu_forest* f, cudaStream_t st, ExchangeMode mode) {
   const int V = f->forest.config().vars;
-  if (exact) {
-    for (int a = 0; a < 3; ++a) {
-      cudaError_t e = ghost_pass(f->arena, V, f->pass[a], f->staged, st);
-      if (e != cudaSuccess) return (int)e;
-    }
+  cudaError_t e = cudaSuccess;
+  if (mode == kExact) {
+    for (int a = 0; a < 3 && e == cudaSuccess; ++a)
+      e = ghost_pass(f->arena, V, f->pass[a], f->staged, st);
   } else {
-    cudaError_t e = ghost_exchange_faces(f->arena, V, f->nslots, f->faces, f->prolong_all,
-                                         f->n_prolong_all, f->staged, st);
-    if (e != cudaSuccess) return (int)e;
+    const bool all = mode == kFaces;
+    e = ghost_exchange_faces(f->arena, V, f->faces, all ? f->items_all : f->items_cf,
+                             all ? f->n_items_all : f->n_items_cf, f->prolong_all,
+                             f->n_prolong_all, f->staged, st);
   }
+  if (e != cudaSuccess) return (int)e;
   f->exchanges += 1;
   return 0;
 }
@@ -378,7 +417,7 @@ int tmgpu_forest_fill_ghosts(tmgpu_forest* f, void* stream, tmgpu_error* err) {
   if (err) std::memset(err, 0, sizeof(*err));
   if (int rc = ready(f, err)) return rc;
   cudaStream_t st = as_stream(stream);
-  int e = exchange(f, st, true);
+  int e = exchange(f, st, kExact);
   if (e) return cuda_err(err, (cudaError_t)e, "tmgpu_forest_fill_ghosts");
   return cuda_err(err, cudaStreamSynchronize(st), "tmgpu_forest_fill_ghosts");
 }
@@ -388,7 +427,7 @@ int tmgpu_forest_fill_faces(tmgpu_forest* f, void* stream, tmgpu_error* err) {
   if (err) std::memset(err, 0, sizeof(*err));
   if (int rc = ready(f, err)) return rc;
   cudaStream_t st = as_stream(stream);
-  int e = exchange(f, st, false);
+  int e = exchange(f, st, kFaces);
   if (e) return cuda_err(err, (cudaError_t)e, "tmgpu_forest_fill_faces");
   return cuda_err(err, cudaStreamSynchronize(st), "tmgpu_forest_fill_faces");
 }
@@ -449,8 +488,10 @@ int tmgpu_forest_step(tmgpu_forest* f, double dt, double cfl, double gamma, int 
   p.u0_stride = (long long)V * 512;
   p.err = f->err_dev;
   p.count = (int)f->nslots;
+  p.face_src = (flags & TMGPU_EXACT_GHOSTS) ? nullptr : f->face_src;
   for (int stage = 1; stage <= 3 && e == cudaSuccess; ++stage) {
-    int x = exchange(f, st, (flags & TMGPU_EXACT_GHOSTS) != 0);
+    const bool exact = (flags & TMGPU_EXACT_GHOSTS) != 0;
+    int x = exchange(f, st, exact ? kExact : kFused);
     if (x) {
       e = (cudaError_t)x;
       break;

@@ -166,39 +166,33 @@ __global__ void __launch_bounds__(128) prolong_snapshot_kernel(const double* __r
   }
 }
 
-// One CTA per destination leaf: its 6 face-ghost slabs (V x G x E x E each),
-// enumerated in destination storage order (x fastest) so a warp writes one
-// contiguous run; 640 = 20 warps per face, so a warp never spans two faces.
-__global__ void __launch_bounds__(256) pull_faces_kernel(double* __restrict__ arena, int V,
-                                                         const FaceSrc* __restrict__ faces,
-                                                         const double* __restrict__ staged) {
-  const int slot = blockIdx.x;
+// One CTA per (destination leaf, face) item: the face's V x G x E x E ghost
+// slab, enumerated in destination storage order (x fastest).
+template <int AXIS>
+__device__ __forceinline__ void pull_face(double* __restrict__ arena, int V, int slot, int dir,
+                                          const FaceSrc& fs, const double* __restrict__ staged) {
   double* dst = arena + (long long)slot * V * S3;
+  constexpr int t1 = (AXIS + 1) % 3, t2 = (AXIS + 2) % 3;
+  constexpr int ex = AXIS == 0 ? G : E, ey = AXIS == 1 ? G : E, ez = AXIS == 2 ? G : E;
   const int per_face = V * G * E * E;
-  for (int n = threadIdx.x; n < 6 * per_face; n += blockDim.x) {
-    const int face = n / per_face, m = n % per_face;
-    const int axis = face >> 1, dir = (face & 1) ? 1 : -1;
-    const FaceSrc fs = faces[(long long)slot * 6 + face];
-    int e[3] = {E, E, E};
-    e[axis] = G;
-    const int lx = m % e[0], ly = (m / e[0]) % e[1], lz = (m / (e[0] * e[1])) % e[2];
-    const int var = m / (e[0] * e[1] * e[2]);
+  for (int m = threadIdx.x; m < per_face; m += blockDim.x) {
+    const int lx = m % ex, ly = (m / ex) % ey, lz = (m / (ex * ey)) % ez, var = m / (ex * ey * ez);
     int p[3] = {G + lx, G + ly, G + lz};
-    p[axis] = (dir > 0 ? G + E : 0) + (axis == 0 ? lx : axis == 1 ? ly : lz);
-    const int t1 = (axis + 1) % 3, t2 = (axis + 2) % 3;
-    const int dd = dir > 0 ? p[axis] - (G + E) : G - 1 - p[axis];
+    const int la = AXIS == 0 ? lx : AXIS == 1 ? ly : lz;
+    p[AXIS] = (dir > 0 ? G + E : 0) + la;
+    const int dd = dir > 0 ? la : G - 1 - la;
     double v;
     switch (fs.kind) {
       case 0: {  // same level (ghost.cpp:40-68)
         int q[3] = {p[0], p[1], p[2]};
-        q[axis] = dir > 0 ? p[axis] - E : p[axis] + E;
+        q[AXIS] = dir > 0 ? p[AXIS] - E : p[AXIS] + E;
         v = arena[(long long)fs.src[0] * V * S3 + at(var, q[0], q[1], q[2])];
         break;
       }
       case 3: {  // reflective wall (ghost.cpp:151-166)
         int q[3] = {p[0], p[1], p[2]};
-        q[axis] = dir > 0 ? 2 * (G + E) - 1 - p[axis] : 2 * G - 1 - p[axis];
-        const double sgn = (V == 5 && var == 1 + axis) ? -1.0 : 1.0;
+        q[AXIS] = dir > 0 ? 2 * (G + E) - 1 - p[AXIS] : 2 * G - 1 - p[AXIS];
+        const double sgn = (V == 5 && var == 1 + AXIS) ? -1.0 : 1.0;
         v = sgn * dst[at(var, q[0], q[1], q[2])];
         break;
       }
@@ -208,17 +202,20 @@ __global__ void __launch_bounds__(256) pull_faces_kernel(double* __restrict__ ar
         break;
       }
       default: {  // finer: restricted quadrant (ghost.cpp:113-149)
-        const int h = E / 2;
+        constexpr int h = E / 2;
         const int a1 = p[t1] - G, a2 = p[t2] - G;
         const int qt1 = a1 / h, qt2 = a2 / h, c1 = a1 % h, c2 = a2 % h;
         const double* src = arena + (long long)fs.src[qt2 * 2 + qt1] * V * S3;
         double acc = 0.0;
+#pragma unroll
         for (int dn = 0; dn < 2; ++dn)
+#pragma unroll
           for (int d1 = 0; d1 < 2; ++d1)
+#pragma unroll
             for (int d2 = 0; d2 < 2; ++d2) {
               const int fn = dir > 0 ? G + 2 * dd + dn : G + E - 1 - (2 * dd + dn);
               int x, y, z;
-              compose(axis, fn, G + 2 * c1 + d1, G + 2 * c2 + d2, x, y, z);
+              compose(AXIS, fn, G + 2 * c1 + d1, G + 2 * c2 + d2, x, y, z);
               acc += src[at(var, x, y, z)];
             }
         v = acc * 0.125;
@@ -227,6 +224,21 @@ __global__ void __launch_bounds__(256) pull_faces_kernel(double* __restrict__ ar
     }
     dst[at(var, p[0], p[1], p[2])] = v;
   }
+}
+
+__global__ void __launch_bounds__(128) pull_faces_kernel(double* __restrict__ arena, int V,
+                                                         const FaceSrc* __restrict__ faces,
+                                                         const int2* __restrict__ items,
+                                                         const double* __restrict__ staged) {
+  const int2 it = items[blockIdx.x];  // (slot, face = 2*axis + (dir > 0))
+  const FaceSrc fs = faces[(long long)it.x * 6 + it.y];
+  const int axis = it.y >> 1, dir = (it.y & 1) ? 1 : -1;
+  if (axis == 0)
+    pull_face<0>(arena, V, it.x, dir, fs, staged);
+  else if (axis == 1)
+    pull_face<1>(arena, V, it.x, dir, fs, staged);
+  else
+    pull_face<2>(arena, V, it.x, dir, fs, staged);
 }
 
 // compact [slot][V][E^3] (k,j,i order) <-> arena interior
@@ -262,15 +274,15 @@ cudaError_t ghost_pass(double* arena, int V, const GhostPassDev& pass, double* s
   return cudaGetLastError();
 }
 
-cudaError_t ghost_exchange_faces(double* arena, int V, long long nslots, const FaceSrc* faces,
-                                 const GhostFill* prolong_fills, int n_prolong, double* staged,
-                                 cudaStream_t st) {
+cudaError_t ghost_exchange_faces(double* arena, int V, const FaceSrc* faces, const int2* items,
+                                 int n_items, const GhostFill* prolong_fills, int n_prolong,
+                                 double* staged, cudaStream_t st) {
   if (n_prolong > 0) {
     prolong_snapshot_kernel<<<n_prolong, 128, 0, st>>>(arena, prolong_fills, V, staged);
     g_launches.fetch_add(1, std::memory_order_relaxed);
   }
-  if (nslots > 0) {
-    pull_faces_kernel<<<(unsigned)nslots, 256, 0, st>>>(arena, V, faces, staged);
+  if (n_items > 0) {
+    pull_faces_kernel<<<(unsigned)n_items, 128, 0, st>>>(arena, V, faces, items, staged);
     g_launches.fetch_add(1, std::memory_order_relaxed);
   }
   return cudaGetLastError();

@@ -34,13 +34,16 @@ struct alignas(16) FaceSrc {
   int8_t pad[11];
 };
 
-// One-round, face-only exchange (production): snapshot every prolonged slab
-// of all three axes from the pre-exchange state, then one CTA per leaf pulls
-// its six E x E x G face-ghost slabs. Bitwise identical to the reference on
+// One-round, face-only exchange: snapshot every prolonged slab of all three
+// axes from the pre-exchange state, then one CTA per (leaf, face) item pulls
+// that face's E x E x G ghost slab. Bitwise identical to the reference on
 // every ghost the stage reads; edge/corner ghosts untouched.
-cudaError_t ghost_exchange_faces(double* arena, int V, long long nslots, const FaceSrc* faces,
-                                 const GhostFill* prolong_fills, int n_prolong, double* staged,
-                                 cudaStream_t st);
+// items = all 6 faces of every leaf (full face exchange) or only the
+// coarse-fine / boundary faces (the step: same-level faces are read by the
+// stage kernel straight from the neighbour, see StageLaunch::face_src).
+cudaError_t ghost_exchange_faces(double* arena, int V, const FaceSrc* faces, const int2* items,
+                                 int n_items, const GhostFill* prolong_fills, int n_prolong,
+                                 double* staged, cudaStream_t st);
 
 // Phase 1 (prolonged snapshot) + phase 2 (apply) of one axis pass.
 cudaError_t ghost_pass(double* arena, int V, const GhostPassDev& pass, double* staged,

@@ -40,7 +40,7 @@ cudaError_t launch_stage_t(const StageMaps& m, const StageLaunch& p, cudaStream_
   });
   if (attr_err != cudaSuccess) return attr_err;
   if (p.count <= 0) return cudaSuccess;
-  stage_kernel<V, FAST><<<p.count, kStageThreads, Lay<V>::kBytes, stream>>>(m.x, m.y, m.z, p);
+  stage_kernel<V, FAST><<<p.count, kStageThreads, Lay<V>::kBytes, stream>>>(m.i, m.x, m.y, m.z, p);
   g_launches.fetch_add(1, std::memory_order_relaxed);
   return cudaGetLastError();
 }
@@ -155,11 +155,12 @@ int make_stage_maps(const double* base, int V, long long slot_stride, long long 
   cuuint64_t dims[5] = {12, 12, 12, (cuuint64_t)V, (cuuint64_t)(count > 0 ? count : 1)};
   cuuint64_t strides[4] = {12 * 8, 144 * 8, 1728 * 8, (cuuint64_t)slot_stride * 8};
   cuuint32_t estr[5] = {1, 1, 1, 1, 1};
-  const cuuint32_t boxes[3][5] = {{12, 8, 8, (cuuint32_t)V, 1},
+  const cuuint32_t boxes[4][5] = {{10, 8, 8, (cuuint32_t)V, 1},
+                                  {2, 8, 8, (cuuint32_t)V, 1},
                                   {8, 2, 8, (cuuint32_t)V, 1},
                                   {8, 8, 2, (cuuint32_t)V, 1}};
-  CUtensorMap* out[3] = {&maps->x, &maps->y, &maps->z};
-  for (int b = 0; b < 3; ++b) {
+  CUtensorMap* out[4] = {&maps->i, &maps->x, &maps->y, &maps->z};
+  for (int b = 0; b < 4; ++b) {
     CUresult r = fn(out[b], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 5, const_cast<double*>(base), dims,
                     strides, boxes[b], estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                     CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,

@@ -44,24 +44,30 @@ constexpr double kRhoFloor = 1e-10;       // euler.hpp:15
 constexpr double kPressureFloor = 1e-12;  // euler.hpp:16
 
 // Staged smem layout (doubles), var-major inside each TMA box:
-//   B0 [V][8 z][8 y][12 x]  (y,z interior, x full)       var stride 768
-//   B1 [V][8 z][2 y][8 x]   y in {0,1}                     var stride 128
-//   B2 [V][8 z][2 y][8 x]   y in {10,11}
-//   B3 [V][2 z][8 y][8 x]   z in {0,1}
-//   B4 [V][2 z][8 y][8 x]   z in {10,11}
+//   B0 [V][8 z][8 y][10 x]  x in [1,11): interior plus one never-read column
+//                           per side, so the 80-byte row stride spreads the
+//                           pencil loads of neighbouring lanes over the banks
+//   XL [V][8 z][8 y][2 x]  x in {0,1}     XH  x in {10,11}
+//   YL [V][8 z][2 y][8 x]  y in {0,1}     YH  y in {10,11}
+//   ZL [V][2 z][8 y][8 x]  z in {0,1}     ZH  z in {10,11}
+// Each face slab is TMA-loaded either from the leaf's own ghost cells or,
+// for a same-level neighbour, straight from the neighbour's interior
+// (StageLaunch::face_src): the same-level ghost copy is fused into the load.
 template <int V>
 struct Lay {
   static constexpr int B0 = 0;
-  static constexpr int B1 = V * 768;
-  static constexpr int B2 = B1 + V * 128;
-  static constexpr int B3 = B2 + V * 128;
-  static constexpr int B4 = B3 + V * 128;
-  static constexpr int kStaged = B4 + V * 128;  // = V*1280 doubles
+  static constexpr int XL = V * 640;
+  static constexpr int XH = XL + V * 128;
+  static constexpr int YL = XH + V * 128;
+  static constexpr int YH = YL + V * 128;
+  static constexpr int ZL = YH + V * 128;
+  static constexpr int ZH = ZL + V * 128;
+  static constexpr int kStaged = ZH + V * 128;  // = V*1408 doubles
   static constexpr int kAcc = kStaged;          // accumulator [V][E^3]
   static constexpr int kU0 = kAcc + V * kE3;     // RK3 u0 block [V][E^3] (bulk-copied)
   static constexpr int kDoubles = kU0 + V * kE3;
   static constexpr int kBytes = kDoubles * 8 + 64;  // + mbarrier/scratch
-  static constexpr uint32_t kTxBytes = (uint32_t)(V * 1280 * 8);
+  static constexpr uint32_t kTxBytes = (uint32_t)(V * 1408 * 8);
 };
 
 // StageLaunch is declared in tmgpu_internal.h
@@ -204,29 +210,38 @@ template <int V, int AXIS>
 __device__ __forceinline__ void pos_addr(int pos, int c1, int c2, int& a, int& vs) {
   using L = Lay<V>;
   if constexpr (AXIS == 0) {  // y = c1, z = c2 interior
-    a = L::B0 + c2 * 96 + c1 * 12 + pos;
-    vs = 768;
-  } else if constexpr (AXIS == 1) {  // z = c1, x = c2 interior
+    const int row = c2 * 8 + c1;
     if (pos < 2) {
-      a = L::B1 + c1 * 16 + pos * 8 + c2;
+      a = L::XL + row * 2 + pos;
       vs = 128;
     } else if (pos >= 10) {
-      a = L::B2 + c1 * 16 + (pos - 10) * 8 + c2;
+      a = L::XH + row * 2 + (pos - 10);
       vs = 128;
     } else {
-      a = L::B0 + c1 * 96 + (pos - 2) * 12 + (c2 + 2);
-      vs = 768;
+      a = L::B0 + row * 10 + (pos - 1);
+      vs = 640;
+    }
+  } else if constexpr (AXIS == 1) {  // z = c1, x = c2 interior
+    if (pos < 2) {
+      a = L::YL + (c1 * 2 + pos) * 8 + c2;
+      vs = 128;
+    } else if (pos >= 10) {
+      a = L::YH + (c1 * 2 + pos - 10) * 8 + c2;
+      vs = 128;
+    } else {
+      a = L::B0 + (c1 * 8 + pos - 2) * 10 + (c2 + 1);
+      vs = 640;
     }
   } else {  // x = c1, y = c2 interior
     if (pos < 2) {
-      a = L::B3 + pos * 64 + c2 * 8 + c1;
+      a = L::ZL + (pos * 8 + c2) * 8 + c1;
       vs = 128;
     } else if (pos >= 10) {
-      a = L::B4 + (pos - 10) * 64 + c2 * 8 + c1;
+      a = L::ZH + ((pos - 10) * 8 + c2) * 8 + c1;
       vs = 128;
     } else {
-      a = L::B0 + (pos - 2) * 96 + c2 * 12 + (c1 + 2);
-      vs = 768;
+      a = L::B0 + ((pos - 2) * 8 + c2) * 10 + (c1 + 1);
+      vs = 640;
     }
   }
 }
@@ -235,17 +250,13 @@ __device__ __forceinline__ void pos_addr(int pos, int c1, int c2, int& a, int& v
 // lanes. nb = lane holding segment r+1 of the same pencil.
 template <int AXIS>
 __device__ __forceinline__ bool face_map(int tid, int& c1, int& c2, int& r, int& nb) {
+  (void)AXIS;
   const int warp = tid >> 5, lane = tid & 31;
-  int j;
-  if constexpr (AXIS == 2) {  // segments 10 lanes apart: x-fast lanes, distinct banks
-    j = lane % 10;
-    r = lane / 10;
-    nb = lane + 10;
-  } else {
-    j = lane / 3;
-    r = lane % 3;
-    nb = lane + 1;
-  }
+  // segments 10 lanes apart: the 10 lanes of one segment walk consecutive
+  // pencils, which the B0 row stride maps to distinct banks
+  const int j = lane % 10;
+  r = lane / 10;
+  nb = lane + 10;
   const int p = warp * 10 + j;
   if constexpr (AXIS == 1) {
     c2 = p & 7;
@@ -372,8 +383,9 @@ __device__ __forceinline__ void axis_pass(const double* __restrict__ sm, double*
 
 template <int V, bool FAST>
 __global__ void __launch_bounds__(kStageThreads, 2)
-    stage_kernel(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CUtensorMap tm_y,
-                 const __grid_constant__ CUtensorMap tm_z, const StageLaunch p) {
+    stage_kernel(const __grid_constant__ CUtensorMap tm_i, const __grid_constant__ CUtensorMap tm_x,
+                 const __grid_constant__ CUtensorMap tm_y, const __grid_constant__ CUtensorMap tm_z,
+                 const StageLaunch p) {
   using L = Lay<V>;
   extern __shared__ __align__(128) double smem[];
   double* sm = smem;
@@ -394,11 +406,26 @@ __global__ void __launch_bounds__(kStageThreads, 2)
     mbar_expect_tx(bar, L::kTxBytes + (want_u0 ? (uint32_t)(V * kE3 * 8) : 0u));
     if (want_u0)  // u0 block rides the same barrier; consumed in the epilogue
       bulk_load(smem + L::kU0, p.u0 + (long long)slot * p.u0_stride, V * kE3 * 8, bar);
-    tma_load_5d(sm + L::B0, &tm_x, bar, 0, 2, 2, 0, slot);
-    tma_load_5d(sm + L::B1, &tm_y, bar, 2, 0, 2, 0, slot);
-    tma_load_5d(sm + L::B2, &tm_y, bar, 2, 10, 2, 0, slot);
-    tma_load_5d(sm + L::B3, &tm_z, bar, 2, 2, 0, 0, slot);
-    tma_load_5d(sm + L::B4, &tm_z, bar, 2, 2, 10, 0, slot);
+    tma_load_5d(sm + L::B0, &tm_i, bar, 1, 2, 2, 0, slot);
+    // face f = 2*axis + side; own ghost layer or the same-level neighbour's
+    // adjacent interior layers (ghost.cpp:40-68 same-slab, fused)
+    const CUtensorMap* fm[3] = {&tm_x, &tm_y, &tm_z};
+    const int off[6] = {L::XL, L::XH, L::YL, L::YH, L::ZL, L::ZH};
+#pragma unroll
+    for (int f = 0; f < 6; ++f) {
+      const int axis = f >> 1, side = f & 1;
+      int src = slot, ca;
+      const int code = p.face_src ? p.face_src[(long long)slot * 6 + f] : (slot << 1);
+      if (code & 1) {
+        src = code >> 1;
+        ca = side ? kG : kE;  // neighbour interior layers next to the shared face
+      } else {
+        ca = side ? kG + kE : 0;  // own ghost layers
+      }
+      int c[3] = {kG, kG, kG};
+      c[axis] = ca;
+      tma_load_5d(sm + off[f], fm[axis], bar, c[0], c[1], c[2], 0, src);
+    }
   }
 
   // header (decode_header stage.cpp:21-29)
@@ -432,32 +459,21 @@ __global__ void __launch_bounds__(kStageThreads, 2)
 
   // ---- phase 2: accumulator seed + cons -> prim in place (stage.cpp:141-153)
   for (int c = tid; c < 1280; c += kStageThreads) {
-    int a, vs, x, y, z;
-    if (c < 768) {
-      x = c % 12;
-      y = 2 + (c / 12) % 8;
-      z = 2 + c / 96;
-      a = L::B0 + c;
-      vs = 768;
+    int a, vs;
+    const bool interior = c < kE3;
+    if (interior) {  // compact (k,j,i) == acc index
+      a = L::B0 + (c >> 3) * 10 + (c & 7) + 1;
+      vs = 640;
     } else {
-      const int q = c - 768, box = q >> 7, w = q & 127;
-      a = L::B1 + box * V * 128 + w;
+      const int q = c - kE3;
+      a = L::XL + (q >> 7) * V * 128 + (q & 127);
       vs = 128;
-      if (box < 2) {  // [z 8][y 2][x 8]
-        x = 2 + (w & 7);
-        y = (box == 0 ? 0 : 10) + ((w >> 3) & 1);
-        z = 2 + (w >> 4);
-      } else {  // [z 2][y 8][x 8]
-        x = 2 + (w & 7);
-        y = 2 + ((w >> 3) & 7);
-        z = (box == 2 ? 0 : 10) + (w >> 6);
-      }
     }
     double u[V];
 #pragma unroll
     for (int v = 0; v < V; ++v) u[v] = sm[a + v * vs];
-    if (x >= 2 && x < 10 && y >= 2 && y < 10 && z >= 2 && z < 10) {
-      const int ci = ((z - 2) * kE + (y - 2)) * kE + (x - 2);
+    if (interior) {
+      const int ci = c;
 #pragma unroll
       for (int v = 0; v < V; ++v) acc[v * kE3 + ci] = u[v];
       if (p.u0_save) {

@@ -38,6 +38,10 @@ struct StageLaunch {
   double* u0_save;  // optional: interior state before the update -> compact [V][E^3]
   long long u0_save_stride;
   const int* index;  // optional: tensor slot of CTA b = index[b]
+  // optional [slot][6] face sources (face = 2*axis + side): (slot << 1) loads
+  // the leaf's own ghost layers, (nbr << 1) | 1 the same-level neighbour's
+  // adjacent interior layers. nullptr: own ghosts everywhere.
+  const int* face_src;
   unsigned long long* err;  // atomicMin of (slice << 32 | var-major interior index)
   int count;
 };
@@ -46,7 +50,7 @@ struct StageLaunch {
 extern std::atomic<uint64_t> g_launches;
 
 struct StageMaps {
-  CUtensorMap x, y, z;  // boxes 12x8x8, 8x2x8, 8x8x2 over [slot][var][z][y][x]
+  CUtensorMap i, x, y, z;  // boxes 10x8x8, 2x8x8, 8x2x8, 8x8x2 over [slot][var][z][y][x]
 };
 
 // Encode the three TMA maps for `count` ghosted 12^3 blocks of V vars whose

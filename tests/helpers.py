@@ -37,3 +37,12 @@ def stage_visible_mask(vars_=5, edge=8, ghost=2):
     out = (r < ghost) | (r >= ghost + edge)
     nout = out[:, None, None].astype(int) + out[None, :, None] + out[None, None, :]
     return np.broadcast_to(nout <= 1, (vars_, S, S, S)).reshape(-1)
+
+
+def interior_mask(vars_=5, edge=8, ghost=2):
+    """Interior cells of a flat ghosted [V][S][S][S] block."""
+    S = edge + 2 * ghost
+    r = np.arange(S)
+    inn = (r >= ghost) & (r < ghost + edge)
+    m = inn[:, None, None] & inn[None, :, None] & inn[None, None, :]
+    return np.broadcast_to(m, (vars_, S, S, S)).reshape(-1)
