@@ -44,9 +44,10 @@ constexpr double kRhoFloor = 1e-10;       // euler.hpp:15
 constexpr double kPressureFloor = 1e-12;  // euler.hpp:16
 
 // Staged smem layout (doubles), var-major inside each TMA box:
-//   B0 [V][8 z][8 y][10 x]  x in [1,11): interior plus one never-read column
-//                           per side, so the 80-byte row stride spreads the
-//                           pencil loads of neighbouring lanes over the banks
+//   B0 [V][8 z][8 y][10 x]  x in [2,12): interior plus two never-read columns,
+//                           so the 80-byte row stride spreads the pencil loads
+//                           of neighbouring lanes over the banks (the box start
+//                           stays 16-byte aligned)
 //   XL [V][8 z][8 y][2 x]  x in {0,1}     XH  x in {10,11}
 //   YL [V][8 z][2 y][8 x]  y in {0,1}     YH  y in {10,11}
 //   ZL [V][2 z][8 y][8 x]  z in {0,1}     ZH  z in {10,11}
@@ -218,7 +219,7 @@ __device__ __forceinline__ void pos_addr(int pos, int c1, int c2, int& a, int& v
       a = L::XH + row * 2 + (pos - 10);
       vs = 128;
     } else {
-      a = L::B0 + row * 10 + (pos - 1);
+      a = L::B0 + row * 10 + (pos - 2);
       vs = 640;
     }
   } else if constexpr (AXIS == 1) {  // z = c1, x = c2 interior
@@ -229,7 +230,7 @@ __device__ __forceinline__ void pos_addr(int pos, int c1, int c2, int& a, int& v
       a = L::YH + (c1 * 2 + pos - 10) * 8 + c2;
       vs = 128;
     } else {
-      a = L::B0 + (c1 * 8 + pos - 2) * 10 + (c2 + 1);
+      a = L::B0 + (c1 * 8 + pos - 2) * 10 + c2;
       vs = 640;
     }
   } else {  // x = c1, y = c2 interior
@@ -240,7 +241,7 @@ __device__ __forceinline__ void pos_addr(int pos, int c1, int c2, int& a, int& v
       a = L::ZH + ((pos - 10) * 8 + c2) * 8 + c1;
       vs = 128;
     } else {
-      a = L::B0 + ((pos - 2) * 8 + c2) * 10 + (c1 + 1);
+      a = L::B0 + ((pos - 2) * 8 + c2) * 10 + c1;
       vs = 640;
     }
   }
@@ -406,7 +407,7 @@ __global__ void __launch_bounds__(kStageThreads, 2)
     mbar_expect_tx(bar, L::kTxBytes + (want_u0 ? (uint32_t)(V * kE3 * 8) : 0u));
     if (want_u0)  // u0 block rides the same barrier; consumed in the epilogue
       bulk_load(smem + L::kU0, p.u0 + (long long)slot * p.u0_stride, V * kE3 * 8, bar);
-    tma_load_5d(sm + L::B0, &tm_i, bar, 1, 2, 2, 0, slot);
+    tma_load_5d(sm + L::B0, &tm_i, bar, 2, 2, 2, 0, slot);
     // face f = 2*axis + side; own ghost layer or the same-level neighbour's
     // adjacent interior layers (ghost.cpp:40-68 same-slab, fused)
     const CUtensorMap* fm[3] = {&tm_x, &tm_y, &tm_z};
@@ -462,7 +463,7 @@ __global__ void __launch_bounds__(kStageThreads, 2)
     int a, vs;
     const bool interior = c < kE3;
     if (interior) {  // compact (k,j,i) == acc index
-      a = L::B0 + (c >> 3) * 10 + (c & 7) + 1;
+      a = L::B0 + (c >> 3) * 10 + (c & 7);
       vs = 640;
     } else {
       const int q = c - kE3;
