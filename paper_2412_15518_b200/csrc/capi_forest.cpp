@@ -18,7 +18,12 @@ struct tmgpu_forest {
   // device state (valid for `dev_version`)
   uint64_t dev_version = ~0ull;
   long long nslots = 0;
-  double* arena = nullptr;    // [slot][V][S^3]
+  // Two ghosted arenas [slot][V][S^3]: the fused step reads arenas[cur] and
+  // writes the updated interiors into arenas[cur ^ 1] (a CTA reads its
+  // same-level neighbours' interiors, so updating in place would race).
+  double* arenas[2] = {nullptr, nullptr};
+  int cur = 0;
+  double* arena() const { return arenas[cur]; }
   double* u0 = nullptr;       // [slot][V][E^3]
   double* xfer = nullptr;     // [slot][V][E^3] host-transfer staging (lazy)
   double* leaf_dx = nullptr;  // [slot]
@@ -38,7 +43,7 @@ struct tmgpu_forest {
   int n_items_all = 0, n_items_cf = 0;
   GhostFill* prolong_all = nullptr;  // coarser fills of all axes (one-round snapshot)
   int n_prolong_all = 0;
-  StageMaps maps{};
+  StageMaps maps[2]{};
   uint64_t exchanges = 0;  // ghost exchanges performed (structural counter)
   // optional per-phase device timing: events [start, cfl, (exch, stage) x 3]
   bool timing = false;
@@ -71,7 +76,10 @@ void free_dev(tmgpu_forest* f) {
   auto fr = [](void* p) {
     if (p) cudaFree(p);
   };
-  fr(f->arena);
+  fr(f->arenas[0]);
+  fr(f->arenas[1]);
+  f->arenas[0] = f->arenas[1] = nullptr;
+  f->cur = 0;
   fr(f->u0);
   fr(f->xfer);
   f->xfer = nullptr;
@@ -101,7 +109,7 @@ void free_dev(tmgpu_forest* f) {
     f->prolong[a] = nullptr;
     f->pass[a] = GhostPassDev{};
   }
-  f->arena = f->u0 = f->leaf_dx = f->speeds = f->diag = f->dt_dev = f->staged = nullptr;
+  f->u0 = f->leaf_dx = f->speeds = f->diag = f->dt_dev = f->staged = nullptr;
   f->err_dev = nullptr;
   f->dev_version = ~0ull;
   f->nslots = 0;
@@ -109,7 +117,7 @@ void free_dev(tmgpu_forest* f) {
 
 int ready(tmgpu_forest* f, tmgpu_error* err) {
   if (!f) return fail(err, TMGPU_ERR_INVALID, "null forest");
-  if (f->dev_version != f->forest.topology_version() || !f->arena)
+  if (f->dev_version != f->forest.topology_version() || !f->arenas[0])
     return fail(err, TMGPU_ERR_INVALID,
                 "device arena is stale: call tmgpu_forest_alloc after changing the topology");
   return TMGPU_OK;
@@ -129,14 +137,16 @@ int alloc_device(tmgpu_forest* f, tmgpu_error* err) {
   auto M = [&](void** p, size_t bytes) {
     if (e == cudaSuccess) e = cudaMalloc(p, bytes ? bytes : 8);
   };
-  M((void**)&f->arena, n * V * S3 * sizeof(double));
+  M((void**)&f->arenas[0], n * V * S3 * sizeof(double));
+  M((void**)&f->arenas[1], n * V * S3 * sizeof(double));
   M((void**)&f->u0, n * V * 512 * sizeof(double));
   M((void**)&f->leaf_dx, n * sizeof(double));
   M((void**)&f->speeds, n * sizeof(double));
   M((void**)&f->diag, n * sizeof(double));
   M((void**)&f->dt_dev, sizeof(double));
   M((void**)&f->err_dev, sizeof(unsigned long long));
-  if (e == cudaSuccess) e = cudaMemset(f->arena, 0, n * V * S3 * sizeof(double));  // SubGrid() zeroes
+  for (int b = 0; b < 2 && e == cudaSuccess; ++b)  // SubGrid() zeroes
+    e = cudaMemset(f->arenas[b], 0, n * V * S3 * sizeof(double));
   if (e == cudaSuccess) e = cudaMemset(f->err_dev, 0xff, sizeof(unsigned long long));  // no error
   std::vector<double> dx(n);
   for (long long s = 0; s < n; ++s) dx[s] = f->forest.cell_size(lv[s].level);
@@ -223,7 +233,8 @@ int alloc_device(tmgpu_forest* f, tmgpu_error* err) {
     return cuda_err(err, e, "tmgpu_forest_alloc");
   }
   std::string why;
-  int rc = make_stage_maps(f->arena, V, (long long)V * S3, n, &f->maps, &why);
+  int rc = make_stage_maps(f->arenas[0], V, (long long)V * S3, n, &f->maps[0], &why);
+  if (rc == TMGPU_OK) rc = make_stage_maps(f->arenas[1], V, (long long)V * S3, n, &f->maps[1], &why);
   if (rc != TMGPU_OK) {
     free_dev(f);
     return fail(err, rc, why);
@@ -244,10 +255,14 @@ int exchange(tmgpu_forest* f, cudaStream_t st, ExchangeMode mode) {
   cudaError_t e = cudaSuccess;
   if (mode == kExact) {
     for (int a = 0; a < 3 && e == cudaSuccess; ++a)
-      e = ghost_pass(f->arena, V, f->pass[a], f->staged, st);
+      e = ghost_pass(f->arena(), V, f->pass[a], f->staged, st);
   } else {
+    // kFused: the previous exchange wrote its ghosts into the other arena
+    // (the stage ping-pongs), so the prolongation stencil's ghost taps read
+    // there; kFaces works in place.
     const bool all = mode == kFaces;
-    e = ghost_exchange_faces(f->arena, V, f->faces, all ? f->items_all : f->items_cf,
+    const double* prev = all ? f->arena() : f->arenas[f->cur ^ 1];
+    e = ghost_exchange_faces(f->arena(), prev, V, f->faces, all ? f->items_all : f->items_cf,
                              all ? f->n_items_all : f->n_items_cf, f->prolong_all,
                              f->n_prolong_all, f->staged, st);
   }
@@ -381,7 +396,7 @@ int tmgpu_forest_alloc(tmgpu_forest* f, tmgpu_error* err) {
   return alloc_device(f, err);
 }
 
-double* tmgpu_forest_arena(tmgpu_forest* f) { return f->arena; }
+double* tmgpu_forest_arena(tmgpu_forest* f) { return f->arena(); }
 
 int tmgpu_forest_interior(tmgpu_forest* f, double* compact, int to_device, int flags, void* stream,
                           tmgpu_error* err) {
@@ -397,7 +412,7 @@ int tmgpu_forest_interior(tmgpu_forest* f, double* compact, int to_device, int f
     dev = f->xfer;
     if (e == cudaSuccess && to_device) e = cudaMemcpyAsync(dev, compact, bytes, cudaMemcpyHostToDevice, st);
   }
-  if (e == cudaSuccess) e = interior_copy(f->arena, dev, V, f->nslots, to_device != 0, st);
+  if (e == cudaSuccess) e = interior_copy(f->arena(), dev, V, f->nslots, to_device != 0, st);
   if (e == cudaSuccess && (flags & TMGPU_HOST_PTRS) && !to_device)
     e = cudaMemcpyAsync(compact, dev, bytes, cudaMemcpyDeviceToHost, st);
   cudaError_t e2 = (flags & TMGPU_ASYNC) ? cudaSuccess : cudaStreamSynchronize(st);
@@ -408,8 +423,8 @@ int tmgpu_forest_grids(tmgpu_forest* f, double* ghosted_host, int to_device, tmg
   if (err) std::memset(err, 0, sizeof(*err));
   if (int rc = ready(f, err)) return rc;
   const size_t bytes = (size_t)f->nslots * f->forest.config().vars * 1728 * sizeof(double);
-  cudaError_t e = to_device ? cudaMemcpy(f->arena, ghosted_host, bytes, cudaMemcpyHostToDevice)
-                            : cudaMemcpy(ghosted_host, f->arena, bytes, cudaMemcpyDeviceToHost);
+  cudaError_t e = to_device ? cudaMemcpy(f->arena(), ghosted_host, bytes, cudaMemcpyHostToDevice)
+                            : cudaMemcpy(ghosted_host, f->arena(), bytes, cudaMemcpyDeviceToHost);
   return cuda_err(err, e, "tmgpu_forest_grids");
 }
 
@@ -438,7 +453,7 @@ int tmgpu_forest_max_wavespeed(tmgpu_forest* f, double gamma, double* per_leaf_h
   if (int rc = ready(f, err)) return rc;
   const int V = f->forest.config().vars;
   cudaStream_t st = cudaStreamPerThread;
-  cudaError_t e = launch_max_wavespeed(f->arena, (long long)V * 1728, nullptr, 0, nullptr, gamma, V,
+  cudaError_t e = launch_max_wavespeed(f->arena(), (long long)V * 1728, nullptr, 0, nullptr, gamma, V,
                                        f->nslots, f->speeds, st);
   if (e == cudaSuccess)
     e = cudaMemcpyAsync(per_leaf_host, f->speeds, f->nslots * sizeof(double), cudaMemcpyDeviceToHost, st);
@@ -466,7 +481,7 @@ int tmgpu_forest_step(tmgpu_forest* f, double dt, double cfl, double gamma, int 
   }
   if (!(flags & TMGPU_ASYNC)) e = cudaMemsetAsync(f->err_dev, 0xff, sizeof(unsigned long long), st);
   if (e == cudaSuccess && cfl > 0.0) {
-    e = launch_max_wavespeed(f->arena, (long long)V * 1728, nullptr, 0, nullptr, gamma, V, f->nslots,
+    e = launch_max_wavespeed(f->arena(), (long long)V * 1728, nullptr, 0, nullptr, gamma, V, f->nslots,
                              f->speeds, st);
     if (e == cudaSuccess) e = launch_cfl_reduce(f->speeds, f->leaf_dx, f->nslots, cfl, f->dt_dev, st);
   }
@@ -478,7 +493,6 @@ int tmgpu_forest_step(tmgpu_forest* f, double dt, double cfl, double gamma, int 
   p.g_dt = dt;
   p.g_gamma = gamma;
   p.dt_ptr = cfl > 0.0 ? f->dt_dev : nullptr;
-  p.out = f->arena;
   p.out_stride = (long long)V * 1728;
   p.out_ghosted = 1;
   p.faces = nullptr;
@@ -488,9 +502,9 @@ int tmgpu_forest_step(tmgpu_forest* f, double dt, double cfl, double gamma, int 
   p.u0_stride = (long long)V * 512;
   p.err = f->err_dev;
   p.count = (int)f->nslots;
-  p.face_src = (flags & TMGPU_EXACT_GHOSTS) ? nullptr : f->face_src;
+  const bool exact = (flags & TMGPU_EXACT_GHOSTS) != 0;
+  p.face_src = exact ? nullptr : f->face_src;
   for (int stage = 1; stage <= 3 && e == cudaSuccess; ++stage) {
-    const bool exact = (flags & TMGPU_EXACT_GHOSTS) != 0;
     int x = exchange(f, st, exact ? kExact : kFused);
     if (x) {
       e = (cudaError_t)x;
@@ -500,7 +514,11 @@ int tmgpu_forest_step(tmgpu_forest* f, double dt, double cfl, double gamma, int 
     p.rk_stage = stage;
     p.u0_save = stage == 1 ? f->u0 : nullptr;
     p.u0_save_stride = (long long)V * 512;
-    e = launch_stage(V, (flags & TMGPU_FAST) != 0, f->maps, p, st);
+    // exact: in place (each CTA reads only its own block); fused: ping-pong
+    const int dst = exact ? f->cur : (f->cur ^ 1);
+    p.out = f->arenas[dst];
+    e = launch_stage(V, (flags & TMGPU_FAST) != 0, f->maps[f->cur], p, st);
+    f->cur = dst;
     if (timed) cudaEventRecord(f->ev[2 * stage + 1], st);
   }
   if (timed && e == cudaSuccess) f->pending_timed = 1;

@@ -140,11 +140,15 @@ __global__ void __launch_bounds__(128) apply_kernel(double* __restrict__ arena,
 }
 
 // One-round snapshot: one CTA per prolonged fill (any axis), fills listed directly.
+// Interior taps read `arena`; the ghost tap (the coarse source's restricted
+// face ghost, filled by the previous exchange) reads `prev`.
 __global__ void __launch_bounds__(128) prolong_snapshot_kernel(const double* __restrict__ arena,
+                                                               const double* __restrict__ prev,
                                                                const GhostFill* __restrict__ fills,
                                                                int V, double* __restrict__ staged) {
   const GhostFill f = fills[blockIdx.x];
   const double* src = arena + (long long)f.src * V * S3;
+  const double* gsrc = prev + (long long)f.src * V * S3;
   double* out = staged + (long long)blockIdx.x * V * E * E * G;
   const int axis = f.axis, dir = f.dir;
   const int n_el = V * E * E * G;
@@ -159,7 +163,10 @@ __global__ void __launch_bounds__(128) prolong_snapshot_kernel(const double* __r
     compose(axis, na - 1, ct1, ct2, xm, ym, zm);
     compose(axis, na + 1, ct1, ct2, xp, yp, zp);
     const double c = src[at(var, x, y, z)];
-    const double s = minmod_scalar(src[at(var, xp, yp, zp)] - c, c - src[at(var, xm, ym, zm)]);
+    // na-1 (dir > 0) / na+1 (dir < 0) is the ghost layer; the other tap is interior
+    const double cp = dir > 0 ? src[at(var, xp, yp, zp)] : gsrc[at(var, xp, yp, zp)];
+    const double cm = dir > 0 ? gsrc[at(var, xm, ym, zm)] : src[at(var, xm, ym, zm)];
+    const double s = minmod_scalar(cp - c, c - cm);
     const double off = 0.25 * s;
     const int sign = dir > 0 ? (sub == 0 ? -1 : +1) : (sub == 0 ? +1 : -1);
     out[n] = sign > 0 ? c + off : c - off;
@@ -274,11 +281,11 @@ cudaError_t ghost_pass(double* arena, int V, const GhostPassDev& pass, double* s
   return cudaGetLastError();
 }
 
-cudaError_t ghost_exchange_faces(double* arena, int V, const FaceSrc* faces, const int2* items,
-                                 int n_items, const GhostFill* prolong_fills, int n_prolong,
-                                 double* staged, cudaStream_t st) {
+cudaError_t ghost_exchange_faces(double* arena, const double* prev, int V, const FaceSrc* faces,
+                                 const int2* items, int n_items, const GhostFill* prolong_fills,
+                                 int n_prolong, double* staged, cudaStream_t st) {
   if (n_prolong > 0) {
-    prolong_snapshot_kernel<<<n_prolong, 128, 0, st>>>(arena, prolong_fills, V, staged);
+    prolong_snapshot_kernel<<<n_prolong, 128, 0, st>>>(arena, prev, prolong_fills, V, staged);
     g_launches.fetch_add(1, std::memory_order_relaxed);
   }
   if (n_items > 0) {

@@ -41,9 +41,10 @@ struct alignas(16) FaceSrc {
 // items = all 6 faces of every leaf (full face exchange) or only the
 // coarse-fine / boundary faces (the step: same-level faces are read by the
 // stage kernel straight from the neighbour, see StageLaunch::face_src).
-cudaError_t ghost_exchange_faces(double* arena, int V, const FaceSrc* faces, const int2* items,
-                                 int n_items, const GhostFill* prolong_fills, int n_prolong,
-                                 double* staged, cudaStream_t st);
+// `prev` holds the ghosts of the previous exchange (== arena when in place).
+cudaError_t ghost_exchange_faces(double* arena, const double* prev, int V, const FaceSrc* faces,
+                                 const int2* items, int n_items, const GhostFill* prolong_fills,
+                                 int n_prolong, double* staged, cudaStream_t st);
 
 // Phase 1 (prolonged snapshot) + phase 2 (apply) of one axis pass.
 cudaError_t ghost_pass(double* arena, int V, const GhostPassDev& pass, double* staged,
