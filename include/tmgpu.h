@@ -118,6 +118,19 @@ int tmgpu_forest_scenario_refine(tmgpu_forest* f, int kind, int min_level, int m
                                  double theta, tmgpu_error* err);
 int tmgpu_forest_scenario_fill(tmgpu_forest* f, int kind, uint64_t seed, double* compact_host,
                                tmgpu_error* err);
+/* ---- distribution over GPUs (one process per GPU, NCCL over NVLink) */
+typedef struct tmgpu_comm tmgpu_comm;
+int tmgpu_comm_unique_id(unsigned char* id128, tmgpu_error* err);      /* ncclGetUniqueId (rank 0) */
+tmgpu_comm* tmgpu_comm_create(int rank, int world, const unsigned char* id128, tmgpu_error* err);
+void tmgpu_comm_destroy(tmgpu_comm* c);
+/* owner[g] per canonical leaf (partition_leaves; Node::owner octree.hpp:74); call alloc after */
+int tmgpu_forest_distribute(tmgpu_forest* f, tmgpu_comm* comm, const int* owner, size_t n,
+                            tmgpu_error* err);
+/* owned leaves in canonical order (= local slot order of the arena and the compact arrays) */
+size_t tmgpu_forest_local_leaves(tmgpu_forest* f, uint64_t* out, size_t cap);
+/* host-only halo manifest of (owner, rank): rows (send 0|recv 1, peer, dst, src, kind, axis, dir) */
+size_t tmgpu_forest_halo_manifest(tmgpu_forest* f, const int* owner, int rank, int world,
+                                  int64_t* rows, size_t cap);
 /* (re)allocate the zeroed device arena + ghost plans for the current topology */
 int tmgpu_forest_alloc(tmgpu_forest* f, tmgpu_error* err);
 double* tmgpu_forest_arena(tmgpu_forest* f);
@@ -143,6 +156,35 @@ int tmgpu_forest_set_timing(tmgpu_forest* f, int on, tmgpu_error* err);
 int tmgpu_forest_timing(tmgpu_forest* f, double* ms_cfl, double* ms_exchange, double* ms_stage,
                         long long* steps);
 int tmgpu_forest_floor_hits(tmgpu_forest* f, double* per_leaf_host, tmgpu_error* err);
+
+/* ---------------------------------------------------------------- aggregation executor
+ * agg::ExecutorPool / agg::AggregationRegion (include/taskmesh/aggregator.hpp:57-172,
+ * src/aggregator.cpp) with CUDA streams as executors. Pool bookkeeping is host-only
+ * (no CUDA until the first launch). */
+typedef struct tmgpu_execpool tmgpu_execpool;
+typedef struct tmgpu_region tmgpu_region;
+tmgpu_execpool* tmgpu_execpool_create(size_t count, tmgpu_error* err);   /* ExecutorPool(count) */
+void tmgpu_execpool_destroy(tmgpu_execpool* p);
+size_t tmgpu_execpool_size(tmgpu_execpool* p);
+size_t tmgpu_execpool_acquire(tmgpu_execpool* p);                        /* acquire() -> lease index */
+size_t tmgpu_execpool_pick_index(tmgpu_execpool* p);                     /* pick_index() */
+int tmgpu_execpool_acquire_at(tmgpu_execpool* p, size_t index, tmgpu_error* err); /* acquire_at */
+void tmgpu_execpool_release(tmgpu_execpool* p, size_t index);            /* ExecutorLease::reset */
+uint64_t tmgpu_execpool_in_flight(tmgpu_execpool* p, size_t index);
+/* kind 0: y = 2x + 1 test kernel (test_aggregator.cpp:17-29); kind 1: the hydro
+ * stage (make_stage_kernel, stage.cpp:229-246; slice sizes from the geometry).
+ * counters: optional uint64[3] {launches, fused_slices, solo_launches}. */
+tmgpu_region* tmgpu_region_create(tmgpu_execpool* pool, int kind, size_t in_slice,
+                                  size_t out_slice, int edge, int ghost, int vars, int flags,
+                                  size_t max_slices, size_t capacity, uint64_t* counters,
+                                  tmgpu_error* err);
+long long tmgpu_region_submit(tmgpu_region* r, const double* input, size_t len,
+                              tmgpu_error* err);                          /* submit_slice */
+int tmgpu_region_flush(tmgpu_region* r, tmgpu_error* err);              /* flush */
+int tmgpu_region_wait(tmgpu_region* r, long long ticket, tmgpu_error* err); /* Future::get */
+const double* tmgpu_region_output(tmgpu_region* r, long long ticket);   /* SliceOutput::values */
+size_t tmgpu_region_submitted(tmgpu_region* r);                           /* submitted() */
+void tmgpu_region_destroy(tmgpu_region* r);
 
 /* FP64 DFMA throughput microbenchmark (roofline denominator) */
 int tmgpu_fp64_peak(int iters, double* tflops, double* ms, tmgpu_error* err);

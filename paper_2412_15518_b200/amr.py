@@ -58,6 +58,9 @@ _sig("tmgpu_forest_max_wavespeed", C.c_int, [_vp, C.c_double, _vp, _ep])
 _sig("tmgpu_forest_step", C.c_int, [_vp, C.c_double, C.c_double, C.c_double, C.c_int, _vp, _dp,
                                     _ep])
 _sig("tmgpu_forest_check", C.c_int, [_vp, _vp, _ep])
+_sig("tmgpu_forest_distribute", C.c_int, [_vp, _vp, _ip, C.c_size_t, _ep])
+_sig("tmgpu_forest_local_leaves", C.c_size_t, [_vp, _u64p, C.c_size_t])
+_sig("tmgpu_forest_halo_manifest", C.c_size_t, [_vp, _ip, C.c_int, C.c_int, _i64p, C.c_size_t])
 _sig("tmgpu_forest_floor_hits", C.c_int, [_vp, _vp, _ep])
 
 
@@ -205,6 +208,35 @@ class Forest:
                                                   C.byref(err)), err)
         return out
 
+    # -- distribution (one process per GPU)
+    def distribute(self, comm, owner) -> None:
+        """Own the leaves with owner[g] == comm.rank (partition_leaves over the
+        canonical order); the device arena then holds only local leaves."""
+        o = np.ascontiguousarray(np.asarray(owner, dtype=np.int32))
+        err = TmgpuError()
+        self._comm = comm  # keep the communicator alive as long as the forest
+        _lib.check(lib.tmgpu_forest_distribute(self.h, comm.h if comm else None,
+                                               o.ctypes.data_as(_ip), len(o), C.byref(err)), err)
+
+    def local_leaves(self) -> np.ndarray:
+        n = lib.tmgpu_forest_local_leaves(self.h, None, 0)
+        out = np.zeros(n, dtype=np.uint64)
+        lib.tmgpu_forest_local_leaves(self.h, out.ctypes.data_as(_u64p), n)
+        return out
+
+    def local_count(self) -> int:
+        return int(lib.tmgpu_forest_local_leaves(self.h, None, 0))
+
+    def halo_manifest(self, owner, rank: int, world: int) -> np.ndarray:
+        """Host-only: every slab rank `rank` sends/receives per exchange, rows
+        (send 0 | recv 1, peer, dst leaf, src leaf, kind, axis, dir)."""
+        o = np.ascontiguousarray(np.asarray(owner, dtype=np.int32))
+        n = lib.tmgpu_forest_halo_manifest(self.h, o.ctypes.data_as(_ip), rank, world, None, 0)
+        rows = np.zeros((n, 7), dtype=np.int64)
+        lib.tmgpu_forest_halo_manifest(self.h, o.ctypes.data_as(_ip), rank, world,
+                                       rows.ctypes.data_as(_i64p), n)
+        return rows
+
     # -- device state
     def alloc(self) -> None:
         """(Re)allocate the zeroed device arena for the current topology."""
@@ -219,7 +251,7 @@ class Forest:
 
     def get_interior(self, out=None):
         if out is None:
-            out = np.zeros((self.leaf_count(), self.vars, self.edge ** 3))
+            out = np.zeros((self.local_count(), self.vars, self.edge ** 3))
         self._interior(out, False)
         return out
 
@@ -227,7 +259,7 @@ class Forest:
         from .hydro import _addr
 
         ptr, host, st, n = _addr(buf)
-        if n != self.leaf_count() * self.vars * self.edge ** 3:
+        if n != self.local_count() * self.vars * self.edge ** 3:
             raise ValueError("compact interior has the wrong size")
         err = TmgpuError()
         _lib.check(lib.tmgpu_forest_interior(self.h, ptr, 1 if to_device else 0,
@@ -235,7 +267,7 @@ class Forest:
                                              C.byref(err)), err)
 
     def get_grids(self) -> np.ndarray:
-        out = np.zeros((self.leaf_count(), self.vars * self.stride ** 3))
+        out = np.zeros((self.local_count(), self.vars * self.stride ** 3))
         err = TmgpuError()
         _lib.check(lib.tmgpu_forest_grids(self.h, out.ctypes.data, 0, C.byref(err)), err)
         return out
@@ -257,14 +289,14 @@ class Forest:
         _lib.check(lib.tmgpu_forest_fill_faces(self.h, stream, C.byref(err)), err)
 
     def max_wavespeed(self, gamma: float = 1.4) -> np.ndarray:
-        out = np.zeros(self.leaf_count())
+        out = np.zeros(self.local_count())
         err = TmgpuError()
         _lib.check(lib.tmgpu_forest_max_wavespeed(self.h, gamma, out.ctypes.data, C.byref(err)),
                    err)
         return out
 
     def floor_hits(self) -> np.ndarray:
-        out = np.zeros(self.leaf_count())
+        out = np.zeros(self.local_count())
         err = TmgpuError()
         _lib.check(lib.tmgpu_forest_floor_hits(self.h, out.ctypes.data, C.byref(err)), err)
         return out

@@ -1,13 +1,16 @@
-// C ABI: octree forest, device leaf arena, reference-exact ghost exchange and
-// the SSP-RK3 hydro step (include/tmgpu.h, "forest" section).
+// C ABI: octree forest, device leaf arenas, ghost exchange (reference-exact
+// 3-pass, or the one-round face exchange with cross-GPU halos) and the
+// SSP-RK3 hydro step (include/tmgpu.h, "forest" section).
 #include <cmath>
 #include <cstring>
 #include <mutex>
 #include <string>
 #include <vector>
 
+#include "comm.h"
 #include "forest.h"
 #include "ghost.h"
+#include "halo_plan.h"
 #include "tmgpu_internal.h"
 
 using namespace tmgpu;
@@ -15,7 +18,12 @@ using namespace tmgpu;
 struct tmgpu_forest {
   explicit tmgpu_forest(const ForestConfig& c) : forest(c) {}
   Forest forest;
-  // device state (valid for `dev_version`)
+  // distribution: owner rank of every canonical leaf (empty = all on rank 0)
+  tmgpu_comm* comm = nullptr;
+  std::vector<int> owner;
+  HaloPlan plan;
+  // device state (valid for `dev_version`); slots are LOCAL leaves (owned,
+  // canonical order)
   uint64_t dev_version = ~0ull;
   long long nslots = 0;
   // Two ghosted arenas [slot][V][S^3]: the fused step reads arenas[cur] and
@@ -31,18 +39,20 @@ struct tmgpu_forest {
   double* diag = nullptr;     // [slot] floor hits of the last stage
   double* dt_dev = nullptr;   // [1]
   unsigned long long* err_dev = nullptr;
+  // reference-exact 3-pass exchange (single GPU only)
   double* staged = nullptr;
   GhostFill* fills[3] = {nullptr, nullptr, nullptr};
   int* staged_of[3] = {nullptr, nullptr, nullptr};
   int* prolong[3] = {nullptr, nullptr, nullptr};
   GhostPassDev pass[3];
-  FaceSrc* faces = nullptr;          // [slot][6] one-round face sources
-  int* face_src = nullptr;           // [slot][6] stage-kernel TMA sources (fused same-level)
-  int2* items_all = nullptr;         // every (slot, face)
-  int2* items_cf = nullptr;          // coarse-fine + boundary (slot, face) only
-  int n_items_all = 0, n_items_cf = 0;
-  GhostFill* prolong_all = nullptr;  // coarser fills of all axes (one-round snapshot)
-  int n_prolong_all = 0;
+  // one-round face exchange (halo.h)
+  PackItem* pack = nullptr;
+  FaceSrc* faces = nullptr;
+  int* face_src = nullptr;
+  int2* pull_all = nullptr;
+  int2* pull_fused = nullptr;
+  double* slabs = nullptr;
+  int n_pack = 0, n_pull_all = 0, n_pull_fused = 0;
   StageMaps maps[2]{};
   uint64_t exchanges = 0;  // ghost exchanges performed (structural counter)
   // optional per-phase device timing: events [start, cfl, (exch, stage) x 3]
@@ -50,6 +60,8 @@ struct tmgpu_forest {
   cudaEvent_t ev[8] = {};
   double t_cfl = 0, t_exchange = 0, t_stage = 0;
   long long timed_steps = 0, pending_timed = 0;
+  int world() const { return comm_world(comm); }
+  int rank() const { return comm_rank(comm); }
 };
 
 namespace {
@@ -76,30 +88,11 @@ void free_dev(tmgpu_forest* f) {
   auto fr = [](void* p) {
     if (p) cudaFree(p);
   };
-  fr(f->arenas[0]);
-  fr(f->arenas[1]);
-  f->arenas[0] = f->arenas[1] = nullptr;
-  f->cur = 0;
-  fr(f->u0);
-  fr(f->xfer);
-  f->xfer = nullptr;
-  fr(f->leaf_dx);
-  fr(f->speeds);
-  fr(f->diag);
-  fr(f->dt_dev);
-  fr(f->err_dev);
-  fr(f->staged);
-  fr(f->faces);
-  fr(f->prolong_all);
-  fr(f->face_src);
-  fr(f->items_all);
-  fr(f->items_cf);
-  f->face_src = nullptr;
-  f->items_all = f->items_cf = nullptr;
-  f->n_items_all = f->n_items_cf = 0;
-  f->faces = nullptr;
-  f->prolong_all = nullptr;
-  f->n_prolong_all = 0;
+  for (void* p : {(void*)f->arenas[0], (void*)f->arenas[1], (void*)f->u0, (void*)f->xfer,
+                  (void*)f->leaf_dx, (void*)f->speeds, (void*)f->diag, (void*)f->dt_dev,
+                  (void*)f->err_dev, (void*)f->staged, (void*)f->pack, (void*)f->faces,
+                  (void*)f->face_src, (void*)f->pull_all, (void*)f->pull_fused, (void*)f->slabs})
+    fr(p);
   for (int a = 0; a < 3; ++a) {
     fr(f->fills[a]);
     fr(f->staged_of[a]);
@@ -109,8 +102,15 @@ void free_dev(tmgpu_forest* f) {
     f->prolong[a] = nullptr;
     f->pass[a] = GhostPassDev{};
   }
-  f->u0 = f->leaf_dx = f->speeds = f->diag = f->dt_dev = f->staged = nullptr;
+  f->arenas[0] = f->arenas[1] = nullptr;
+  f->cur = 0;
+  f->u0 = f->xfer = f->leaf_dx = f->speeds = f->diag = f->dt_dev = f->staged = f->slabs = nullptr;
   f->err_dev = nullptr;
+  f->pack = nullptr;
+  f->faces = nullptr;
+  f->face_src = nullptr;
+  f->pull_all = f->pull_fused = nullptr;
+  f->n_pack = f->n_pull_all = f->n_pull_fused = 0;
   f->dev_version = ~0ull;
   f->nslots = 0;
 }
@@ -123,110 +123,86 @@ int ready(tmgpu_forest* f, tmgpu_error* err) {
   return TMGPU_OK;
 }
 
-// (Re)build the device arena and the per-axis ghost plans for the current topology.
+template <class T>
+cudaError_t upload(T** dst, const std::vector<T>& v, cudaError_t e) {
+  if (e != cudaSuccess) return e;
+  e = cudaMalloc((void**)dst, v.empty() ? 16 : v.size() * sizeof(T));
+  if (e == cudaSuccess && !v.empty())
+    e = cudaMemcpy(*dst, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice);
+  return e;
+}
+
+// (Re)build the device arenas, the exchange plans and the TMA maps for the
+// current topology and distribution.
 int alloc_device(tmgpu_forest* f, tmgpu_error* err) {
   free_dev(f);
   const auto& cfg = f->forest.config();
   if (cfg.edge != 8 || cfg.ghost != 2 || (cfg.vars != 5 && cfg.vars != 1))
     return fail(err, TMGPU_ERR_INVALID, "device arena supports edge 8, ghost 2, vars 1|5");
   const auto& lv = f->forest.leaves();
-  const long long n = (long long)lv.size();
+  const int world = f->world(), rank = f->rank();
+  std::vector<int> owner = f->owner;
+  if (owner.size() != lv.size()) {
+    if (world > 1) return fail(err, TMGPU_ERR_INVALID, "distribution does not match the topology");
+    owner.assign(lv.size(), 0);
+  }
+  try {
+    f->plan = build_halo_plan(f->forest, owner, rank, world);
+  } catch (const std::exception& ex) {
+    return fail(err, TMGPU_ERR_AMR, ex.what());
+  }
+  const HaloPlan& P = f->plan;
+  const long long n = (long long)P.loc2gl.size();
   const int V = cfg.vars;
   const size_t S3 = 1728;
   cudaError_t e = cudaSuccess;
   auto M = [&](void** p, size_t bytes) {
-    if (e == cudaSuccess) e = cudaMalloc(p, bytes ? bytes : 8);
+    if (e == cudaSuccess) e = cudaMalloc(p, bytes ? bytes : 16);
   };
   M((void**)&f->arenas[0], n * V * S3 * sizeof(double));
   M((void**)&f->arenas[1], n * V * S3 * sizeof(double));
   M((void**)&f->u0, n * V * 512 * sizeof(double));
-  M((void**)&f->leaf_dx, n * sizeof(double));
   M((void**)&f->speeds, n * sizeof(double));
   M((void**)&f->diag, n * sizeof(double));
   M((void**)&f->dt_dev, sizeof(double));
   M((void**)&f->err_dev, sizeof(unsigned long long));
+  M((void**)&f->slabs, P.total_doubles * sizeof(double));
   for (int b = 0; b < 2 && e == cudaSuccess; ++b)  // SubGrid() zeroes
     e = cudaMemset(f->arenas[b], 0, n * V * S3 * sizeof(double));
-  if (e == cudaSuccess) e = cudaMemset(f->err_dev, 0xff, sizeof(unsigned long long));  // no error
+  if (e == cudaSuccess) e = cudaMemset(f->err_dev, 0xff, sizeof(unsigned long long));
   std::vector<double> dx(n);
-  for (long long s = 0; s < n; ++s) dx[s] = f->forest.cell_size(lv[s].level);
-  if (e == cudaSuccess) e = cudaMemcpy(f->leaf_dx, dx.data(), n * sizeof(double), cudaMemcpyHostToDevice);
-  size_t max_prolong = 0;
-  std::vector<FaceSrc> fsrc(n * 6);
-  for (auto& x : fsrc) {
-    std::memset(&x, 0, sizeof(x));
-    x.kind = 3;
-  }
-  std::vector<GhostFill> pall;
-  for (int a = 0; a < 3 && e == cudaSuccess; ++a) {
-    const std::vector<Fill> plan = f->forest.plan_axis(a);
-    for (const Fill& p : plan) {
-      FaceSrc& fs = fsrc[(size_t)p.dst * 6 + 2 * a + (p.dir > 0 ? 1 : 0)];
-      fs.kind = p.kind;
-      if (p.kind == 2)
-        fs.src[p.qt2 * 2 + p.qt1] = p.src;
-      else
-        fs.src[0] = p.src;
-      if (p.kind == 1) {
-        fs.staged = (int)pall.size();
-        pall.push_back(GhostFill{p.dst, p.src, p.kind, p.axis, p.dir, p.qt1, p.qt2, {0, 0, 0}});
+  for (long long s = 0; s < n; ++s) dx[s] = f->forest.cell_size(lv[P.loc2gl[s]].level);
+  e = upload(&f->leaf_dx, dx, e);
+  e = upload(&f->pack, P.pack, e);
+  e = upload(&f->faces, P.faces, e);
+  e = upload(&f->face_src, P.face_src, e);
+  e = upload((int**)&f->pull_all, P.pull_all, e);
+  e = upload((int**)&f->pull_fused, P.pull_fused, e);
+  f->n_pack = (int)P.pack.size();
+  f->n_pull_all = (int)P.pull_all.size() / 2;
+  f->n_pull_fused = (int)P.pull_fused.size() / 2;
+  if (world == 1) {  // reference-exact 3-pass plans (global slot == local slot)
+    size_t max_prolong = 0;
+    for (int a = 0; a < 3 && e == cudaSuccess; ++a) {
+      const std::vector<Fill> plan = f->forest.plan_axis(a);
+      std::vector<GhostFill> gf(plan.size());
+      std::vector<int> sof(plan.size(), -1), pro;
+      for (size_t i = 0; i < plan.size(); ++i) {
+        const Fill& p = plan[i];
+        gf[i] = GhostFill{p.dst, p.src, p.kind, p.axis, p.dir, p.qt1, p.qt2, {0, 0, 0}};
+        if (p.kind == 1) {
+          sof[i] = (int)pro.size();
+          pro.push_back((int)i);
+        }
       }
+      max_prolong = std::max(max_prolong, pro.size());
+      e = upload(&f->fills[a], gf, e);
+      e = upload(&f->staged_of[a], sof, e);
+      e = upload(&f->prolong[a], pro, e);
+      f->pass[a] = GhostPassDev{f->fills[a], f->staged_of[a], f->prolong[a], (int)gf.size(),
+                                (int)pro.size()};
     }
-    std::vector<GhostFill> gf(plan.size());
-    std::vector<int> sof(plan.size(), -1), pro;
-    for (size_t i = 0; i < plan.size(); ++i) {
-      const Fill& p = plan[i];
-      gf[i] = GhostFill{p.dst, p.src, p.kind, p.axis, p.dir, p.qt1, p.qt2, {0, 0, 0}};
-      if (p.kind == 1) {
-        sof[i] = (int)pro.size();
-        pro.push_back((int)i);
-      }
-    }
-    max_prolong = std::max(max_prolong, pro.size());
-    M((void**)&f->fills[a], gf.size() * sizeof(GhostFill));
-    M((void**)&f->staged_of[a], sof.size() * sizeof(int));
-    M((void**)&f->prolong[a], pro.size() * sizeof(int));
-    if (e == cudaSuccess && !gf.empty())
-      e = cudaMemcpy(f->fills[a], gf.data(), gf.size() * sizeof(GhostFill), cudaMemcpyHostToDevice);
-    if (e == cudaSuccess && !sof.empty())
-      e = cudaMemcpy(f->staged_of[a], sof.data(), sof.size() * sizeof(int), cudaMemcpyHostToDevice);
-    if (e == cudaSuccess && !pro.empty())
-      e = cudaMemcpy(f->prolong[a], pro.data(), pro.size() * sizeof(int), cudaMemcpyHostToDevice);
-    f->pass[a] = GhostPassDev{f->fills[a], f->staged_of[a], f->prolong[a], (int)gf.size(),
-                              (int)pro.size()};
-  }
-  max_prolong = std::max(max_prolong, pall.size());
-  M((void**)&f->staged, max_prolong * V * 8 * 8 * 2 * sizeof(double));
-  M((void**)&f->faces, fsrc.size() * sizeof(FaceSrc));
-  M((void**)&f->prolong_all, pall.size() * sizeof(GhostFill));
-  if (e == cudaSuccess && !fsrc.empty())
-    e = cudaMemcpy(f->faces, fsrc.data(), fsrc.size() * sizeof(FaceSrc), cudaMemcpyHostToDevice);
-  if (e == cudaSuccess && !pall.empty())
-    e = cudaMemcpy(f->prolong_all, pall.data(), pall.size() * sizeof(GhostFill), cudaMemcpyHostToDevice);
-  f->n_prolong_all = (int)pall.size();
-  {
-    std::vector<int> fsrc_code(n * 6);
-    std::vector<int2> all, cf;
-    all.reserve(n * 6);
-    for (long long s = 0; s < n; ++s)
-      for (int face = 0; face < 6; ++face) {
-        const FaceSrc& x = fsrc[(size_t)s * 6 + face];
-        const bool same = x.kind == 0;
-        fsrc_code[(size_t)s * 6 + face] = same ? ((x.src[0] << 1) | 1) : (int)(s << 1);
-        all.push_back(make_int2((int)s, face));
-        if (!same) cf.push_back(make_int2((int)s, face));
-      }
-    M((void**)&f->face_src, fsrc_code.size() * sizeof(int));
-    M((void**)&f->items_all, all.size() * sizeof(int2));
-    M((void**)&f->items_cf, cf.size() * sizeof(int2));
-    if (e == cudaSuccess && !fsrc_code.empty())
-      e = cudaMemcpy(f->face_src, fsrc_code.data(), fsrc_code.size() * sizeof(int), cudaMemcpyHostToDevice);
-    if (e == cudaSuccess && !all.empty())
-      e = cudaMemcpy(f->items_all, all.data(), all.size() * sizeof(int2), cudaMemcpyHostToDevice);
-    if (e == cudaSuccess && !cf.empty())
-      e = cudaMemcpy(f->items_cf, cf.data(), cf.size() * sizeof(int2), cudaMemcpyHostToDevice);
-    f->n_items_all = (int)all.size();
-    f->n_items_cf = (int)cf.size();
+    M((void**)&f->staged, max_prolong * V * 8 * 8 * 2 * sizeof(double));
   }
   if (e != cudaSuccess) {
     free_dev(f);
@@ -245,38 +221,52 @@ int alloc_device(tmgpu_forest* f, tmgpu_error* err) {
 }
 
 // Exchange modes: kExact = reference 3-pass fill of the full ghost shell
-// (ghost.cpp:282-296); kFaces = one-round fill of every face ghost; kFused =
-// one-round fill of the coarse-fine and boundary faces only, the same-level
-// faces being read by the stage kernel straight from the neighbour.
+// (ghost.cpp:282-296, single GPU); kFaces = one-round fill of every face
+// ghost, in place; kFused = one-round fill of every face the stage kernel
+// does not read straight from a local same-level neighbour, with the
+// prolongation ghost taps read from the other arena (the previous exchange).
 enum ExchangeMode { kExact, kFaces, kFused };
 
-int exchange(tmgpu_forest* f, cudaStream_t st, ExchangeMode mode) {
+int exchange(tmgpu_forest* f, cudaStream_t st, ExchangeMode mode, std::string* why) {
   const int V = f->forest.config().vars;
   cudaError_t e = cudaSuccess;
   if (mode == kExact) {
+    if (f->world() > 1) {
+      if (why) *why = "the reference-exact 3-pass exchange is single-GPU only";
+      return TMGPU_ERR_INVALID;
+    }
     for (int a = 0; a < 3 && e == cudaSuccess; ++a)
       e = ghost_pass(f->arena(), V, f->pass[a], f->staged, st);
   } else {
-    // kFused: the previous exchange wrote its ghosts into the other arena
-    // (the stage ping-pongs), so the prolongation stencil's ghost taps read
-    // there; kFaces works in place.
     const bool all = mode == kFaces;
     const double* prev = all ? f->arena() : f->arenas[f->cur ^ 1];
-    e = ghost_exchange_faces(f->arena(), prev, V, f->faces, all ? f->items_all : f->items_cf,
-                             all ? f->n_items_all : f->n_items_cf, f->prolong_all,
-                             f->n_prolong_all, f->staged, st);
+    e = halo_pack(f->arena(), prev, V, f->pack, f->n_pack, f->slabs, st);
+    if (e == cudaSuccess && f->world() > 1) {
+      const HaloPlan& P = f->plan;
+      int rc = comm_exchange(f->comm, f->slabs + P.send_base, P.send_off, P.send_cnt,
+                             f->slabs + P.recv_base, P.recv_off, P.recv_cnt, st, why);
+      if (rc != TMGPU_OK) return rc;
+    }
+    if (e == cudaSuccess)
+      e = halo_pull(f->arena(), V, f->faces, all ? f->pull_all : f->pull_fused,
+                    all ? f->n_pull_all : f->n_pull_fused, f->slabs, st);
   }
-  if (e != cudaSuccess) return (int)e;
+  if (e != cudaSuccess) {
+    if (why) *why = std::string("ghost exchange: ") + cudaGetErrorString(e);
+    return TMGPU_ERR_CUDA;
+  }
   f->exchanges += 1;
-  return 0;
+  return TMGPU_OK;
 }
 
-int solver_err_from_word(tmgpu_error* err, unsigned long long w) {
+// slice = canonical leaf index of the first failing local leaf
+int solver_err_from_word(tmgpu_error* err, unsigned long long w, const std::vector<int>& loc2gl) {
   const unsigned cell = (unsigned)(w & 0xffffffffu) % 512u;
   const int i = (int)(cell % 8), j = (int)(cell / 8 % 8), k = (int)(cell / 64);
   if (err) {
+    const size_t slot = (size_t)(w >> 32);
     err->code = TMGPU_ERR_SOLVER;
-    err->slice = (int64_t)(w >> 32);
+    err->slice = slot < loc2gl.size() ? loc2gl[slot] : (int64_t)slot;
     err->cell[0] = i;
     err->cell[1] = j;
     err->cell[2] = k;
@@ -391,6 +381,52 @@ int tmgpu_forest_scenario_fill(tmgpu_forest* f, int kind, uint64_t seed, double*
   return TMGPU_OK;
 }
 
+// Distribute the canonical leaves over the ranks of `comm` (owner[g] per leaf,
+// normally partition_leaves); invalidates the device state (call alloc).
+int tmgpu_forest_distribute(tmgpu_forest* f, tmgpu_comm* comm, const int* owner, size_t n,
+                            tmgpu_error* err) {
+  if (err) std::memset(err, 0, sizeof(*err));
+  if (n != f->forest.leaves().size())
+    return fail(err, TMGPU_ERR_INVALID, "owner list does not match the leaf count");
+  const int world = comm_world(comm);
+  for (size_t i = 0; i < n; ++i)
+    if (owner[i] < 0 || owner[i] >= world) return fail(err, TMGPU_ERR_INVALID, "owner out of range");
+  free_dev(f);
+  f->comm = comm;
+  f->owner.assign(owner, owner + n);
+  return TMGPU_OK;
+}
+
+// Local (owned) leaves in canonical order = local slot order.
+size_t tmgpu_forest_local_leaves(tmgpu_forest* f, uint64_t* out, size_t cap) {
+  const auto& lv = f->forest.leaves();
+  std::vector<int> loc;
+  for (size_t g = 0; g < lv.size(); ++g)
+    if (f->owner.size() != lv.size() ? f->rank() == 0 : f->owner[g] == f->rank())
+      loc.push_back((int)g);
+  for (size_t i = 0; i < loc.size() && i < cap; ++i) out[i] = lv[loc[i]].packed();
+  return loc.size();
+}
+
+// Host halo plan of (rank, owner) without touching the device (tests):
+// rows of 7 int64 (direction 0 send / 1 recv, peer, dst, src, kind, axis, dir).
+size_t tmgpu_forest_halo_manifest(tmgpu_forest* f, const int* owner, int rank, int world,
+                                  int64_t* rows, size_t cap) {
+  std::vector<int> o(owner, owner + f->forest.leaves().size());
+  HaloPlan P = build_halo_plan(f->forest, o, rank, world);
+  size_t r = 0;
+  for (int d = 0; d < 2; ++d)
+    for (const auto& m : d == 0 ? P.send_manifest : P.recv_manifest) {
+      if (r < cap) {
+        int64_t* x = rows + 7 * r;
+        x[0] = d;
+        for (int k = 0; k < 6; ++k) x[1 + k] = m[k];
+      }
+      ++r;
+    }
+  return r;
+}
+
 int tmgpu_forest_alloc(tmgpu_forest* f, tmgpu_error* err) {
   if (err) std::memset(err, 0, sizeof(*err));
   return alloc_device(f, err);
@@ -432,8 +468,8 @@ int tmgpu_forest_fill_ghosts(tmgpu_forest* f, void* stream, tmgpu_error* err) {
   if (err) std::memset(err, 0, sizeof(*err));
   if (int rc = ready(f, err)) return rc;
   cudaStream_t st = as_stream(stream);
-  int e = exchange(f, st, kExact);
-  if (e) return cuda_err(err, (cudaError_t)e, "tmgpu_forest_fill_ghosts");
+  std::string why;
+  if (int rc = exchange(f, st, kExact, &why)) return fail(err, rc, why);
   return cuda_err(err, cudaStreamSynchronize(st), "tmgpu_forest_fill_ghosts");
 }
 
@@ -442,8 +478,8 @@ int tmgpu_forest_fill_faces(tmgpu_forest* f, void* stream, tmgpu_error* err) {
   if (err) std::memset(err, 0, sizeof(*err));
   if (int rc = ready(f, err)) return rc;
   cudaStream_t st = as_stream(stream);
-  int e = exchange(f, st, kFaces);
-  if (e) return cuda_err(err, (cudaError_t)e, "tmgpu_forest_fill_faces");
+  std::string why;
+  if (int rc = exchange(f, st, kFaces, &why)) return fail(err, rc, why);
   return cuda_err(err, cudaStreamSynchronize(st), "tmgpu_forest_fill_faces");
 }
 
@@ -484,6 +520,10 @@ int tmgpu_forest_step(tmgpu_forest* f, double dt, double cfl, double gamma, int 
     e = launch_max_wavespeed(f->arena(), (long long)V * 1728, nullptr, 0, nullptr, gamma, V, f->nslots,
                              f->speeds, st);
     if (e == cudaSuccess) e = launch_cfl_reduce(f->speeds, f->leaf_dx, f->nslots, cfl, f->dt_dev, st);
+    if (e == cudaSuccess && f->world() > 1) {  // global dt: min over ranks (exact)
+      std::string why;
+      if (int rc = comm_allreduce_min(f->comm, f->dt_dev, 1, st, &why)) return fail(err, rc, why);
+    }
   }
   if (timed) cudaEventRecord(f->ev[1], st);
   StageLaunch p{};
@@ -505,11 +545,8 @@ int tmgpu_forest_step(tmgpu_forest* f, double dt, double cfl, double gamma, int 
   const bool exact = (flags & TMGPU_EXACT_GHOSTS) != 0;
   p.face_src = exact ? nullptr : f->face_src;
   for (int stage = 1; stage <= 3 && e == cudaSuccess; ++stage) {
-    int x = exchange(f, st, exact ? kExact : kFused);
-    if (x) {
-      e = (cudaError_t)x;
-      break;
-    }
+    std::string why;
+    if (int rc = exchange(f, st, exact ? kExact : kFused, &why)) return fail(err, rc, why);
     if (timed) cudaEventRecord(f->ev[2 * stage], st);
     p.rk_stage = stage;
     p.u0_save = stage == 1 ? f->u0 : nullptr;
@@ -534,7 +571,7 @@ int tmgpu_forest_step(tmgpu_forest* f, double dt, double cfl, double gamma, int 
   if (dt_used) *dt_used = dtv;
   if (cfl > 0.0 && !std::isfinite(dtv))
     return fail(err, TMGPU_ERR_SOLVER, "cfl_dt: no wave speed (s = 0 everywhere)");
-  if (w != ~0ull) return solver_err_from_word(err, w);
+  if (w != ~0ull) return solver_err_from_word(err, w, f->plan.loc2gl);
   return TMGPU_OK;
 }
 
@@ -571,7 +608,7 @@ int tmgpu_forest_check(tmgpu_forest* f, void* stream, tmgpu_error* err) {
   if (e == cudaSuccess) e = cudaMemsetAsync(f->err_dev, 0xff, sizeof(w), st);
   if (e == cudaSuccess) e = cudaStreamSynchronize(st);
   if (e != cudaSuccess) return cuda_err(err, e, "tmgpu_forest_check");
-  if (w != ~0ull) return solver_err_from_word(err, w);
+  if (w != ~0ull) return solver_err_from_word(err, w, f->plan.loc2gl);
   return TMGPU_OK;
 }
 

@@ -1,0 +1,27 @@
+// NCCL communicator for the cross-GPU halo and the CFL reduction (comm.cpp).
+// NCCL is bound at run time (dlopen of libnccl.so.2: the copy torch already
+// loaded, else the system library), so the library has no link-time NCCL
+// dependency and single-GPU use never touches it.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <string>
+#include <vector>
+
+struct tmgpu_comm;
+
+namespace tmgpu {
+
+int comm_rank(const tmgpu_comm* c);
+int comm_world(const tmgpu_comm* c);
+// Grouped point-to-point: for every peer p with a nonzero count, send
+// send[send_off[p] .. +send_cnt[p]) and receive into recv[recv_off[p] ..).
+int comm_exchange(tmgpu_comm* c, const double* send, const std::vector<long long>& send_off,
+                  const std::vector<long long>& send_cnt, double* recv,
+                  const std::vector<long long>& recv_off, const std::vector<long long>& recv_cnt,
+                  cudaStream_t st, std::string* why);
+// In-place min-allreduce of n doubles (the global CFL dt).
+int comm_allreduce_min(tmgpu_comm* c, double* buf, size_t n, cudaStream_t st, std::string* why);
+
+}  // namespace tmgpu

@@ -139,115 +139,6 @@ __global__ void __launch_bounds__(128) apply_kernel(double* __restrict__ arena,
   }
 }
 
-// One-round snapshot: one CTA per prolonged fill (any axis), fills listed directly.
-// Interior taps read `arena`; the ghost tap (the coarse source's restricted
-// face ghost, filled by the previous exchange) reads `prev`.
-__global__ void __launch_bounds__(128) prolong_snapshot_kernel(const double* __restrict__ arena,
-                                                               const double* __restrict__ prev,
-                                                               const GhostFill* __restrict__ fills,
-                                                               int V, double* __restrict__ staged) {
-  const GhostFill f = fills[blockIdx.x];
-  const double* src = arena + (long long)f.src * V * S3;
-  const double* gsrc = prev + (long long)f.src * V * S3;
-  double* out = staged + (long long)blockIdx.x * V * E * E * G;
-  const int axis = f.axis, dir = f.dir;
-  const int n_el = V * E * E * G;
-  for (int n = threadIdx.x; n < n_el; n += blockDim.x) {
-    const int dd = n % G, f1 = (n / G) % E, f2 = (n / (G * E)) % E, var = n / (G * E * E);
-    const int cd = dd / 2, sub = dd - 2 * cd;
-    const int na = dir > 0 ? G + cd : G + E - 1 - cd;
-    const int ct1 = G + f.qt1 * (E / 2) + f1 / 2;
-    const int ct2 = G + f.qt2 * (E / 2) + f2 / 2;
-    int x, y, z, xm, ym, zm, xp, yp, zp;
-    compose(axis, na, ct1, ct2, x, y, z);
-    compose(axis, na - 1, ct1, ct2, xm, ym, zm);
-    compose(axis, na + 1, ct1, ct2, xp, yp, zp);
-    const double c = src[at(var, x, y, z)];
-    // na-1 (dir > 0) / na+1 (dir < 0) is the ghost layer; the other tap is interior
-    const double cp = dir > 0 ? src[at(var, xp, yp, zp)] : gsrc[at(var, xp, yp, zp)];
-    const double cm = dir > 0 ? gsrc[at(var, xm, ym, zm)] : src[at(var, xm, ym, zm)];
-    const double s = minmod_scalar(cp - c, c - cm);
-    const double off = 0.25 * s;
-    const int sign = dir > 0 ? (sub == 0 ? -1 : +1) : (sub == 0 ? +1 : -1);
-    out[n] = sign > 0 ? c + off : c - off;
-  }
-}
-
-// One CTA per (destination leaf, face) item: the face's V x G x E x E ghost
-// slab, enumerated in destination storage order (x fastest).
-template <int AXIS>
-__device__ __forceinline__ void pull_face(double* __restrict__ arena, int V, int slot, int dir,
-                                          const FaceSrc& fs, const double* __restrict__ staged) {
-  double* dst = arena + (long long)slot * V * S3;
-  constexpr int t1 = (AXIS + 1) % 3, t2 = (AXIS + 2) % 3;
-  constexpr int ex = AXIS == 0 ? G : E, ey = AXIS == 1 ? G : E, ez = AXIS == 2 ? G : E;
-  const int per_face = V * G * E * E;
-  for (int m = threadIdx.x; m < per_face; m += blockDim.x) {
-    const int lx = m % ex, ly = (m / ex) % ey, lz = (m / (ex * ey)) % ez, var = m / (ex * ey * ez);
-    int p[3] = {G + lx, G + ly, G + lz};
-    const int la = AXIS == 0 ? lx : AXIS == 1 ? ly : lz;
-    p[AXIS] = (dir > 0 ? G + E : 0) + la;
-    const int dd = dir > 0 ? la : G - 1 - la;
-    double v;
-    switch (fs.kind) {
-      case 0: {  // same level (ghost.cpp:40-68)
-        int q[3] = {p[0], p[1], p[2]};
-        q[AXIS] = dir > 0 ? p[AXIS] - E : p[AXIS] + E;
-        v = arena[(long long)fs.src[0] * V * S3 + at(var, q[0], q[1], q[2])];
-        break;
-      }
-      case 3: {  // reflective wall (ghost.cpp:151-166)
-        int q[3] = {p[0], p[1], p[2]};
-        q[AXIS] = dir > 0 ? 2 * (G + E) - 1 - p[AXIS] : 2 * G - 1 - p[AXIS];
-        const double sgn = (V == 5 && var == 1 + AXIS) ? -1.0 : 1.0;
-        v = sgn * dst[at(var, q[0], q[1], q[2])];
-        break;
-      }
-      case 1: {  // coarser: snapshot slab in ghost.cpp:161-186 order
-        const int f1 = p[t1] - G, f2 = p[t2] - G;
-        v = staged[(long long)fs.staged * per_face + ((var * E + f2) * E + f1) * G + dd];
-        break;
-      }
-      default: {  // finer: restricted quadrant (ghost.cpp:113-149)
-        constexpr int h = E / 2;
-        const int a1 = p[t1] - G, a2 = p[t2] - G;
-        const int qt1 = a1 / h, qt2 = a2 / h, c1 = a1 % h, c2 = a2 % h;
-        const double* src = arena + (long long)fs.src[qt2 * 2 + qt1] * V * S3;
-        double acc = 0.0;
-#pragma unroll
-        for (int dn = 0; dn < 2; ++dn)
-#pragma unroll
-          for (int d1 = 0; d1 < 2; ++d1)
-#pragma unroll
-            for (int d2 = 0; d2 < 2; ++d2) {
-              const int fn = dir > 0 ? G + 2 * dd + dn : G + E - 1 - (2 * dd + dn);
-              int x, y, z;
-              compose(AXIS, fn, G + 2 * c1 + d1, G + 2 * c2 + d2, x, y, z);
-              acc += src[at(var, x, y, z)];
-            }
-        v = acc * 0.125;
-        break;
-      }
-    }
-    dst[at(var, p[0], p[1], p[2])] = v;
-  }
-}
-
-__global__ void __launch_bounds__(128) pull_faces_kernel(double* __restrict__ arena, int V,
-                                                         const FaceSrc* __restrict__ faces,
-                                                         const int2* __restrict__ items,
-                                                         const double* __restrict__ staged) {
-  const int2 it = items[blockIdx.x];  // (slot, face = 2*axis + (dir > 0))
-  const FaceSrc fs = faces[(long long)it.x * 6 + it.y];
-  const int axis = it.y >> 1, dir = (it.y & 1) ? 1 : -1;
-  if (axis == 0)
-    pull_face<0>(arena, V, it.x, dir, fs, staged);
-  else if (axis == 1)
-    pull_face<1>(arena, V, it.x, dir, fs, staged);
-  else
-    pull_face<2>(arena, V, it.x, dir, fs, staged);
-}
-
 // compact [slot][V][E^3] (k,j,i order) <-> arena interior
 __global__ void interior_copy_kernel(double* __restrict__ arena, double* __restrict__ compact,
                                      int V, long long nslots, int to_arena) {
@@ -276,20 +167,6 @@ cudaError_t ghost_pass(double* arena, int V, const GhostPassDev& pass, double* s
   }
   if (pass.n_fills > 0) {
     apply_kernel<<<pass.n_fills, 128, 0, st>>>(arena, pass.fills, pass.staged_of, V, staged);
-    g_launches.fetch_add(1, std::memory_order_relaxed);
-  }
-  return cudaGetLastError();
-}
-
-cudaError_t ghost_exchange_faces(double* arena, const double* prev, int V, const FaceSrc* faces,
-                                 const int2* items, int n_items, const GhostFill* prolong_fills,
-                                 int n_prolong, double* staged, cudaStream_t st) {
-  if (n_prolong > 0) {
-    prolong_snapshot_kernel<<<n_prolong, 128, 0, st>>>(arena, prev, prolong_fills, V, staged);
-    g_launches.fetch_add(1, std::memory_order_relaxed);
-  }
-  if (n_items > 0) {
-    pull_faces_kernel<<<(unsigned)n_items, 128, 0, st>>>(arena, V, faces, items, staged);
     g_launches.fetch_add(1, std::memory_order_relaxed);
   }
   return cudaGetLastError();

@@ -25,27 +25,6 @@ struct GhostPassDev {
   int n_prolong = 0;
 };
 
-// Per destination leaf and face (2*axis + (dir>0)): where its face ghosts come
-// from in the one-round exchange.
-struct alignas(16) FaceSrc {
-  int32_t src[4];  // same/coarser: src[0]; finer: quadrant (qt2*2+qt1); boundary: unused
-  int32_t staged;  // coarser: index of the snapshot slab
-  int8_t kind;     // 0 same, 1 coarser, 2 finer, 3 boundary
-  int8_t pad[11];
-};
-
-// One-round, face-only exchange: snapshot every prolonged slab of all three
-// axes from the pre-exchange state, then one CTA per (leaf, face) item pulls
-// that face's E x E x G ghost slab. Bitwise identical to the reference on
-// every ghost the stage reads; edge/corner ghosts untouched.
-// items = all 6 faces of every leaf (full face exchange) or only the
-// coarse-fine / boundary faces (the step: same-level faces are read by the
-// stage kernel straight from the neighbour, see StageLaunch::face_src).
-// `prev` holds the ghosts of the previous exchange (== arena when in place).
-cudaError_t ghost_exchange_faces(double* arena, const double* prev, int V, const FaceSrc* faces,
-                                 const int2* items, int n_items, const GhostFill* prolong_fills,
-                                 int n_prolong, double* staged, cudaStream_t st);
-
 // Phase 1 (prolonged snapshot) + phase 2 (apply) of one axis pass.
 cudaError_t ghost_pass(double* arena, int V, const GhostPassDev& pass, double* staged,
                        cudaStream_t st);

@@ -1,0 +1,51 @@
+// One-round face exchange with cross-GPU halos (halo.cu).
+//
+// Every directed face fill of the reference plan (ghost.cpp:168-210) is
+// executed once per exchange as
+//   pack   — on the SOURCE leaf's GPU: the slab the destination needs
+//            (same-level: 2 interior layers; prolonged: ghost.cpp:70-96 with
+//            the coarse source's ghost tap read from the previous exchange;
+//            restricted: ghost.cpp:113-131 2x2x2 means), into a slab buffer;
+//   move   — when source and destination GPUs differ, the slab travels in
+//            one grouped NCCL send/recv per peer (comm.cpp);
+//   pull   — on the DESTINATION leaf's GPU: one CTA per (leaf, face) writes
+//            the E x E x G face-ghost slab from a local leaf, a slab, or the
+//            reflective mirror (ghost.cpp:151-166).
+// Same-level fills between leaves on the same GPU are neither packed nor
+// pulled: the stage kernel TMA-loads the neighbour's interior directly.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace tmgpu {
+
+// kind: 0 same, 1 coarser source (prolonged), 2 finer source (restricted)
+struct alignas(16) PackItem {
+  int32_t src;  // local slot of the source leaf
+  int32_t out;  // offset (doubles) into the slab buffer
+  int8_t kind, axis, dir, qt1, qt2;
+  int8_t pad[3];
+};
+
+// Where a destination face gets its ghosts. kind as NeighborKind (0 same,
+// 1 coarser, 2 finer, 3 boundary). Per source q (finer: quadrant qt2*2+qt1;
+// otherwise q = 0): src[q] >= 0 a local leaf slot, else off[q] is the slab
+// buffer offset of a packed slab (coarser fills always use a slab).
+struct alignas(16) FaceSrc {
+  int32_t src[4];
+  int32_t off[4];
+  int8_t kind;
+  int8_t pad[15];
+};
+
+// Slab sizes in doubles per kind (V vars).
+inline int slab_doubles(int kind, int V) { return kind == 2 ? V * 2 * 4 * 4 : V * 2 * 8 * 8; }
+
+cudaError_t halo_pack(const double* arena, const double* prev, int V, const PackItem* items,
+                      int n_items, double* slabs, cudaStream_t st);
+cudaError_t halo_pull(double* arena, int V, const FaceSrc* faces, const int2* items, int n_items,
+                      const double* slabs, cudaStream_t st);
+
+}  // namespace tmgpu
