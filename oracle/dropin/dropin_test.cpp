@@ -76,12 +76,14 @@ int main() {
     std::printf("max_slices=%zu gpu launches=%llu fused=%llu\n", max_slices,
                 (unsigned long long)cb.launches.load(), (unsigned long long)cb.fused_slices.load());
   }
-  {  // error path: NaN in one slice of a fused batch
+  // error path: NaN in one slice of a fused batch, GPU and CPU kernels
+  std::string msgs[2];
+  for (int which = 0; which < 2; ++which) {
     task::Scheduler sched(2);
     agg::ExecutorPool execs(1);
     mem::BufferPool pool;
     auto busy = execs.acquire();  // keep the executor busy so the 4 slices fuse
-    agg::AggregationRegion rb(sched, execs, pool, gpu, 4, 4);
+    agg::AggregationRegion rb(sched, execs, pool, which ? cpu : gpu, 4, 4);
     std::vector<task::Future<agg::SliceOutput>> fb;
     for (std::size_t s = 0; s < 4; ++s) {
       auto x = slices[s];
@@ -90,18 +92,19 @@ int main() {
     }
     busy.reset();
     int thrown = 0;
-    std::string msg;
     for (auto& f : fb) {
       try {
         sched.run_until(f);
       } catch (const hydro::SolverError& e) {
         ++thrown;
-        msg = e.what();
+        msgs[which] = e.what();
       }
     }
-    std::printf("error batch: %d/4 promises failed: %s\n", thrown, msg.c_str());
+    std::printf("%s error batch: %d/4 promises failed: %s\n", which ? "cpu" : "gpu", thrown,
+                msgs[which].c_str());
     if (thrown != 4) ++failures;
   }
+  if (msgs[0] != msgs[1]) ++failures;
   std::printf(failures ? "DROPIN_FAIL\n" : "DROPIN_OK\n");
   return failures ? 1 : 0;
 }

@@ -263,18 +263,18 @@ __device__ __forceinline__ int interior_index(int axis, int c0, int c1, int c2) 
   return (cc[2] * kE + cc[1]) * kE + cc[0];
 }
 
-// Fluxes of faces 3R..3R+2 of one pencil (R = segment, warp-uniform, so the
-// six stencil positions 3R..3R+5 and their smem boxes are compile-time).
+// Fluxes of faces 3r..3r+2 of one pencil (r = segment, warp-uniform; kept a
+// run-time value: one body per axis keeps the kernel inside the I-cache).
 // Each cell's limited slope m[j] = minmod(d[j-1], d[j]) is computed once and
 // shared by the right state of face j-2 and the left state of face j-1 (the
 // reference evaluates the identical expression twice, euler.hpp:32-33).
-template <int V, int AXIS, int R, bool FAST, bool EULER>
-__device__ __forceinline__ void face_segment(const double* __restrict__ sm, int c1, int c2,
+template <int V, int AXIS, bool FAST, bool EULER>
+__device__ __forceinline__ void face_segment(const double* __restrict__ sm, int r, int c1, int c2,
                                              double gamma, double gm1, double inv_gm1,
                                              bool gm1_ok, double a_vel, double (&F)[3][V]) {
   int a[6], vs[6];
 #pragma unroll
-  for (int s = 0; s < 6; ++s) pos_addr<V, AXIS>(3 * R + s, c1, c2, a[s], vs[s]);
+  for (int s = 0; s < 6; ++s) pos_addr<V, AXIS>(3 * r + s, c1, c2, a[s], vs[s]);
   constexpr int NV = EULER ? 5 : 1;
   double ql[3][NV], qr[3][NV];
 #pragma unroll
@@ -344,12 +344,7 @@ __device__ __forceinline__ void axis_pass(double* __restrict__ sm, double* __res
   for (int k = 0; k < 3; ++k)
 #pragma unroll
     for (int v = 0; v < V; ++v) F[k][v] = 0.0;
-  if (r == 0)
-    face_segment<V, AXIS, 0, FAST, EULER>(sm, c1, c2, gamma, gm1, inv_gm1, gm1_ok, a_vel, F);
-  else if (r == 1)
-    face_segment<V, AXIS, 1, FAST, EULER>(sm, c1, c2, gamma, gm1, inv_gm1, gm1_ok, a_vel, F);
-  else
-    face_segment<V, AXIS, 2, FAST, EULER>(sm, c1, c2, gamma, gm1, inv_gm1, gm1_ok, a_vel, F);
+  face_segment<V, AXIS, FAST, EULER>(sm, r, c1, c2, gamma, gm1, inv_gm1, gm1_ok, a_vel, F);
   // boundary-face record (stage.cpp:180-182): F[0] -> side 0, F[E] -> side 1
   if (faces_out) {
     const int fo = c2 * kE + c1;
