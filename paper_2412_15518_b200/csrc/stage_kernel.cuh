@@ -39,7 +39,7 @@ namespace tmgpu {
 
 constexpr int kE = 8, kG = 2, kS = 12;
 constexpr int kE2 = 64, kE3 = 512;
-constexpr int kStageThreads = 192;  // 6 warps: 3 face segments x 64 pencils, one pencil per lane
+constexpr int kStageThreads = 224;  // 7 warps x 30 face lanes >= 64 pencils x 3 segments
 constexpr double kRhoFloor = 1e-10;       // euler.hpp:15
 constexpr double kPressureFloor = 1e-12;  // euler.hpp:16
 
@@ -129,7 +129,7 @@ __device__ __forceinline__ double stdmax_(double a, double b) { return (a < b) ?
 // When a*b > 0 both arguments are non-zero with one sign, so the smaller
 // magnitude is min(a,b) for positives and max(a,b) for negatives (equal
 // arguments are the same value); NaN never reaches the min/max (a*b > 0 is
-// false), so one DMNMX replaces two compares and two 64-bit selects.
+// false).
 __device__ __forceinline__ double minmod_lane(double a, double b) {
   const double sm = a > 0.0 ? fmin(a, b) : fmax(a, b);
   return (a * b) > 0.0 ? sm : 0.0;
@@ -255,6 +255,28 @@ __device__ __forceinline__ void pos_addr(int pos, int c1, int c2, int& a, int& v
   }
 }
 
+// Lane -> (pencil, segment) map for the face phase. Returns false for idle
+// lanes. nb = lane holding segment r+1 of the same pencil.
+template <int AXIS>
+__device__ __forceinline__ bool face_map(int tid, int& c1, int& c2, int& r, int& nb) {
+  (void)AXIS;
+  const int warp = tid >> 5, lane = tid & 31;
+  // segments 10 lanes apart: the 10 lanes of one segment walk consecutive
+  // pencils, which the B0 row stride maps to distinct banks
+  const int j = lane % 10;
+  r = lane / 10;
+  nb = lane + 10;
+  const int p = warp * 10 + j;
+  if constexpr (AXIS == 1) {
+    c2 = p & 7;
+    c1 = p >> 3;
+  } else {
+    c1 = p & 7;
+    c2 = p >> 3;
+  }
+  return lane < 30 && p < 64;
+}
+
 __device__ __forceinline__ int interior_index(int axis, int c0, int c1, int c2) {
   int cc[3];
   cc[axis] = c0;
@@ -263,132 +285,106 @@ __device__ __forceinline__ int interior_index(int axis, int c0, int c1, int c2) 
   return (cc[2] * kE + cc[1]) * kE + cc[0];
 }
 
-// Fluxes of faces 3r..3r+2 of one pencil (r = segment, warp-uniform; kept a
-// run-time value: one body per axis keeps the kernel inside the I-cache).
-// Each cell's limited slope m[j] = minmod(d[j-1], d[j]) is computed once and
-// shared by the right state of face j-2 and the left state of face j-1 (the
-// reference evaluates the identical expression twice, euler.hpp:32-33).
+// One axis of the stage: fluxes of 3 faces per lane, boundary-face record,
+// then (after the barrier) the divergence update of the lane's cells.
 template <int V, int AXIS, bool FAST, bool EULER>
-__device__ __forceinline__ void face_segment(const double* __restrict__ sm, int r, int c1, int c2,
-                                             double gamma, double gm1, double inv_gm1,
-                                             bool gm1_ok, double a_vel, double (&F)[3][V]) {
-  int a[6], vs[6];
-#pragma unroll
-  for (int s = 0; s < 6; ++s) pos_addr<V, AXIS>(3 * r + s, c1, c2, a[s], vs[s]);
-  constexpr int NV = EULER ? 5 : 1;
-  double ql[3][NV], qr[3][NV];
-#pragma unroll
-  for (int v = 0; v < NV; ++v) {
-    double c[6], d[5], m[5];
-#pragma unroll
-    for (int s = 0; s < 6; ++s) c[s] = sm[a[s] + v * vs[s]];
-#pragma unroll
-    for (int i = 0; i < 5; ++i) d[i] = c[i + 1] - c[i];
-#pragma unroll
-    for (int j = 1; j < 5; ++j) m[j] = minmod_lane(d[j - 1], d[j]);
-#pragma unroll
-    for (int k = 0; k < 3; ++k) {
-      ql[k][v] = c[k + 1] + 0.5 * m[k + 1];
-      qr[k][v] = c[k + 2] - 0.5 * m[k + 2];
-    }
-  }
-#pragma unroll
-  for (int k = 0; k < 3; ++k) {
-    if constexpr (EULER) {
-      double l5[5], r5[5], f[5];
-#pragma unroll
-      for (int v = 0; v < 5; ++v) {
-        l5[v] = ql[k][v];
-        r5[v] = qr[k][v];
-      }
-      // stage.cpp:80-83 face floors
-      l5[0] = vmax_floor(l5[0], kRhoFloor);
-      r5[0] = vmax_floor(r5[0], kRhoFloor);
-      l5[4] = vmax_floor(l5[4], kPressureFloor);
-      r5[4] = vmax_floor(r5[4], kPressureFloor);
-      rusanov<AXIS, FAST>(l5, r5, gamma, gm1, inv_gm1, gm1_ok, f);
-#pragma unroll
-      for (int v = 0; v < 5; ++v) F[k][v] = f[v];
-    } else {
-      // stage.cpp:44-55 scalar advection on var 0; other vars keep zero flux
-      const double l = ql[k][0], rr = qr[k][0];
-      F[k][0] = 0.5 * (a_vel * l + a_vel * rr) - 0.5 * fabs(a_vel) * (rr - l);
-    }
-  }
-}
-
-// One axis of the stage. Warps 2R, 2R+1 own segment R (faces 3R..3R+2) of
-// the 64 pencils, one pencil per lane. The flux of the first face of segment
-// R+1 is handed to segment R through `xbuf` (dead smem: B0's two unused
-// columns, or the x face slabs once the x pass has read them); after the
-// barrier each lane applies acc -= cdt*(F[c0+1]-F[c0]) to its cells, so per
-// cell the update order is x, then y, then z (stage.cpp:166-183).
-template <int V, int AXIS, bool FAST, bool EULER>
-__device__ __forceinline__ void axis_pass(double* __restrict__ sm, double* __restrict__ acc,
+__device__ __forceinline__ void axis_pass(const double* __restrict__ sm, double* __restrict__ acc,
                                           int tid, double gamma, double gm1, double inv_gm1,
                                           bool gm1_ok, double a_vel, double cdt,
                                           double* faces_out) {
-  using L = Lay<V>;
-  const int warp = tid >> 5, lane = tid & 31;
-  const int r = warp >> 1, p = (warp & 1) * 32 + lane;
-  int c1, c2;
-  if constexpr (AXIS == 1) {  // x (= c2) fastest across lanes
-    c2 = p & 7;
-    c1 = p >> 3;
-  } else {
-    c1 = p & 7;
-    c2 = p >> 3;
-  }
+  int c1, c2, r, nb;
+  const bool active = face_map<AXIS>(tid, c1, c2, r, nb);
   double F[3][V];
 #pragma unroll
   for (int k = 0; k < 3; ++k)
 #pragma unroll
     for (int v = 0; v < V; ++v) F[k][v] = 0.0;
-  face_segment<V, AXIS, FAST, EULER>(sm, r, c1, c2, gamma, gm1, inv_gm1, gm1_ok, a_vel, F);
-  // boundary-face record (stage.cpp:180-182): F[0] -> side 0, F[E] -> side 1
-  if (faces_out) {
-    const int fo = c2 * kE + c1;
-    if (r == 0) {
+  if (active) {
+    // Stencil window: positions 3r..3r+5 along the axis serve faces 3r..3r+2.
+    // Each cell's limited slope m[j] = minmod(d[j-1], d[j]) is computed once
+    // and shared by the right state of face j-2 and the left state of face
+    // j-1 (the reference evaluates the identical expression twice,
+    // euler.hpp:32-33).
+    const int base = 3 * r;
+    int a[6], vs[6];
 #pragma unroll
-      for (int v = 0; v < V; ++v) faces_out[(2 * AXIS) * V * kE2 + v * kE2 + fo] = F[0][v];
-    } else if (r == 2) {
+    for (int s = 0; s < 6; ++s) pos_addr<V, AXIS>(base + s, c1, c2, a[s], vs[s]);
+    constexpr int NV = EULER ? 5 : 1;
+    double ql[3][NV], qr[3][NV];
 #pragma unroll
-      for (int v = 0; v < V; ++v) faces_out[(2 * AXIS + 1) * V * kE2 + v * kE2 + fo] = F[2][v];
+    for (int v = 0; v < NV; ++v) {
+      double c[6], d[5], m[5];
+#pragma unroll
+      for (int s = 0; s < 6; ++s) c[s] = sm[a[s] + v * vs[s]];
+#pragma unroll
+      for (int i = 0; i < 5; ++i) d[i] = c[i + 1] - c[i];
+#pragma unroll
+      for (int j = 1; j < 5; ++j) m[j] = minmod_lane(d[j - 1], d[j]);
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        ql[k][v] = c[k + 1] + 0.5 * m[k + 1];
+        qr[k][v] = c[k + 2] - 0.5 * m[k + 2];
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      if constexpr (EULER) {
+        double l5[5], r5[5], f[5];
+#pragma unroll
+        for (int v = 0; v < 5; ++v) {
+          l5[v] = ql[k][v];
+          r5[v] = qr[k][v];
+        }
+        // stage.cpp:80-83 face floors
+        l5[0] = vmax_floor(l5[0], kRhoFloor);
+        r5[0] = vmax_floor(r5[0], kRhoFloor);
+        l5[4] = vmax_floor(l5[4], kPressureFloor);
+        r5[4] = vmax_floor(r5[4], kPressureFloor);
+        rusanov<AXIS, FAST>(l5, r5, gamma, gm1, inv_gm1, gm1_ok, f);
+#pragma unroll
+        for (int v = 0; v < 5; ++v) F[k][v] = f[v];
+      } else {
+        // stage.cpp:44-55 scalar advection on var 0; other vars keep zero flux
+        const double l = ql[k][0], rr = qr[k][0];
+        F[k][0] = 0.5 * (a_vel * l + a_vel * rr) - 0.5 * fabs(a_vel) * (rr - l);
+      }
+    }
+    // boundary-face record (stage.cpp:180-182): F[0] -> side 0, F[E] -> side 1
+    if (faces_out) {
+      const int fo = c2 * kE + c1;
+      if (r == 0) {
+#pragma unroll
+        for (int v = 0; v < V; ++v) faces_out[(2 * AXIS) * V * kE2 + v * kE2 + fo] = F[0][v];
+      } else if (r == 2) {
+#pragma unroll
+        for (int v = 0; v < V; ++v) faces_out[(2 * AXIS + 1) * V * kE2 + v * kE2 + fo] = F[2][v];
+      }
     }
   }
-  // xbuf slot of (segment s in {1,2}, pencil, var): x and z passes use B0's
-  // unused columns 8, 9 (never read as state); the y pass uses XL (read only
-  // by the x pass, which every thread finished before the x-pass barrier)
-  auto xslot = [&](int s, int v) -> double& {
-    if constexpr (AXIS == 1)
-      return sm[L::XL + (s - 1) * V * 64 + v * 64 + p];
-    else
-      return sm[L::B0 + v * 640 + p * 10 + 8 + (s - 1)];
-  };
-  if (r > 0) {
-#pragma unroll
-    for (int v = 0; v < V; ++v) xslot(r, v) = F[0][v];
-  }
-  __syncthreads();  // xbuf written; previous axis' updates of every cell are complete
+  // F[3] = first face of the next segment (warp shuffle; all lanes take part)
   double D[3][V];
 #pragma unroll
   for (int v = 0; v < V; ++v) {
+    const double nxt = __shfl_sync(0xffffffffu, F[0][v], nb & 31);
     D[0][v] = F[1][v] - F[0][v];
     D[1][v] = F[2][v] - F[1][v];
-    if (r < 2) D[2][v] = xslot(r + 1, v) - F[2][v];
+    D[2][v] = nxt - F[2][v];
   }
-  const int ncell = r == 2 ? 2 : 3;
+  __syncthreads();  // previous axis' updates of every cell are complete
+  if (active) {
+    const int ncell = r == 2 ? 2 : 3;
 #pragma unroll
-  for (int k = 0; k < 3; ++k) {
-    if (k < ncell) {
-      const int ci = interior_index(AXIS, 3 * r + k, c1, c2);
+    for (int k = 0; k < 3; ++k) {
+      if (k < ncell) {
+        const int ci = interior_index(AXIS, 3 * r + k, c1, c2);
 #pragma unroll
-      for (int v = 0; v < V; ++v) {
-        double& o = acc[v * kE3 + ci];
-        if constexpr (FAST)
-          o = fma(-cdt, D[k][v], o);
-        else
-          o -= cdt * D[k][v];
+        for (int v = 0; v < V; ++v) {
+          double& o = acc[v * kE3 + ci];
+          if constexpr (FAST)
+            o = fma(-cdt, D[k][v], o);
+          else
+            o -= cdt * D[k][v];
+        }
       }
     }
   }
@@ -542,7 +538,6 @@ __global__ void __launch_bounds__(kStageThreads, 2)
   unsigned int hits = 0, bad = 0xffffffffu;
   double* outp = p.out + (long long)slot * p.out_stride;
   const double* u0p = (p.u0 && p.rk_stage >= 2) ? smem + L::kU0 : nullptr;
-  // (the x face slabs hold the y pass' xbuf by now; the epilogue reads acc and u0 only)
   for (int c = tid; c < kE3; c += kStageThreads) {
     double u[V];
 #pragma unroll
