@@ -33,7 +33,6 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
-#include "fastmath.cuh"
 #include "tmgpu_internal.h"
 
 namespace tmgpu {
@@ -126,19 +125,29 @@ __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t b
 __device__ __forceinline__ double vmax_(double x, double f) { return x > f ? x : f; }
 __device__ __forceinline__ double stdmax_(double a, double b) { return (a < b) ? b : a; }
 
-// limiter.hpp:18-26 lane minmod: select(a*b > 0, select(|a|<|b|, a, b), 0).
-// When a*b > 0 both arguments are non-zero with one sign, so the smaller
-// magnitude is min(a,b) for positives and max(a,b) for negatives (equal
-// arguments are the same value); NaN never reaches the min/max (a*b > 0 is
-// false).
+// limiter.hpp:18-26 lane minmod: select(a*b > 0, select(|a|<|b|, a, b), 0)
 __device__ __forceinline__ double minmod_lane(double a, double b) {
-  const double sm = a > 0.0 ? fmin(a, b) : fmax(a, b);
+  double sm = fabs(a) < fabs(b) ? a : b;
   return (a * b) > 0.0 ? sm : 0.0;
 }
 
-// vmax against a positive, non-NaN floor (lanes.hpp:109-113, x > f ? x : f):
-// identical to fmax for every x, NaN (-> f) and -0 (-> f) included.
-__device__ __forceinline__ double vmax_floor(double x, double f) { return fmax(x, f); }
+// Correctly rounded a / b from y = RN(1/b) (Markstein): q = RN(a*y),
+// r = a - b*q (exact via FMA), RN(q + r*y) == RN(a/b) when no operand or
+// result is near over/underflow; outside [2^-900, 2^901) (and for 0, inf,
+// NaN) it falls back to the IEEE division, so the result is bitwise the
+// reference's `a / b` for every input. Lets one reciprocal serve several
+// quotients with the same divisor (cons->prim) and a per-slice constant
+// divisor (gamma - 1) cost 3 FP64 ops instead of a full division sequence.
+__device__ __forceinline__ bool exp_ok(double x) {
+  const unsigned e = ((unsigned)__double2hiint(x) >> 20) & 0x7ffu;
+  return (e - 123u) < 1800u;
+}
+__device__ __forceinline__ double div_rn(double a, double b, double y, bool b_ok) {
+  const double q = a * y;
+  const double r = fma(-q, b, a);
+  const double q2 = fma(r, y, q);
+  return (b_ok && exp_ok(a) && exp_ok(q2)) ? q2 : a / b;
+}
 
 // euler.hpp:27-35
 __device__ __forceinline__ void recon(double um1, double u0, double up1, double up2, double& l,
@@ -152,34 +161,24 @@ __device__ __forceinline__ void recon(double um1, double u0, double up1, double 
 // prim_to_cons is evaluated once per side: the reference evaluates it twice
 // (inside euler_flux and again for U) with identical operands, so sharing the
 // value is bitwise neutral.
-// Math policies: kIeee = CUDA's IEEE operators (the exact reference);
-// kFastExact = branch-free fastmath.cuh operators, bitwise equal to kIeee
-// whenever `ok` stays true (callers re-run kIeee otherwise); kTol = the FAST
-// tolerance mode (reciprocal reuse + FMA contraction).
-enum Math { kIeee = 0, kFastExact = 1, kTol = 2 };
-
-template <int AXIS, int M>
+template <int AXIS, bool FAST>
 __device__ __forceinline__ void rusanov(const double (&ql)[5], const double (&qr)[5], double gamma,
-                                        double gm1, double ygm1, double (&f)[5], bool& ok) {
+                                        double gm1, double inv_gm1, bool gm1_ok, double (&f)[5]) {
   double cl, cr, el, er;
-  if constexpr (M == kIeee) {
+  if constexpr (!FAST) {
     cl = sqrt(gamma * ql[4] / ql[0]);
     cr = sqrt(gamma * qr[4] / qr[0]);
-    el = ql[4] / gm1 + 0.5 * ql[0] * (ql[1] * ql[1] + ql[2] * ql[2] + ql[3] * ql[3]);
-    er = qr[4] / gm1 + 0.5 * qr[0] * (qr[1] * qr[1] + qr[2] * qr[2] + qr[3] * qr[3]);
-  } else if constexpr (M == kFastExact) {
-    cl = fm_sqrt(fm_div(gamma * ql[4], ql[0], ok), ok);
-    cr = fm_sqrt(fm_div(gamma * qr[4], qr[0], ok), ok);
-    const double pl = fm_div_y(ql[4], gm1, ygm1), pr = fm_div_y(qr[4], gm1, ygm1);
-    ok = ok && fm_range_ok(ql[4]) && fm_range_ok(qr[4]) && fm_range_ok(pl) && fm_range_ok(pr);
-    el = pl + 0.5 * ql[0] * (ql[1] * ql[1] + ql[2] * ql[2] + ql[3] * ql[3]);
-    er = pr + 0.5 * qr[0] * (qr[1] * qr[1] + qr[2] * qr[2] + qr[3] * qr[3]);
+    el = div_rn(ql[4], gm1, inv_gm1, gm1_ok) +
+         0.5 * ql[0] * (ql[1] * ql[1] + ql[2] * ql[2] + ql[3] * ql[3]);
+    er = div_rn(qr[4], gm1, inv_gm1, gm1_ok) +
+         0.5 * qr[0] * (qr[1] * qr[1] + qr[2] * qr[2] + qr[3] * qr[3]);
   } else {
-    bool dummy = true;
-    cl = fm_sqrt(gamma * ql[4] * fm_rcp(ql[0]), dummy);
-    cr = fm_sqrt(gamma * qr[4] * fm_rcp(qr[0]), dummy);
-    el = fma(ql[4], ygm1, 0.5 * ql[0] * fma(ql[1], ql[1], fma(ql[2], ql[2], ql[3] * ql[3])));
-    er = fma(qr[4], ygm1, 0.5 * qr[0] * fma(qr[1], qr[1], fma(qr[2], qr[2], qr[3] * qr[3])));
+    cl = sqrt(gamma * ql[4] * __drcp_rn(ql[0]));
+    cr = sqrt(gamma * qr[4] * __drcp_rn(qr[0]));
+    el = fma(ql[4], inv_gm1,
+             0.5 * ql[0] * fma(ql[1], ql[1], fma(ql[2], ql[2], ql[3] * ql[3])));
+    er = fma(qr[4], inv_gm1,
+             0.5 * qr[0] * fma(qr[1], qr[1], fma(qr[2], qr[2], qr[3] * qr[3])));
   }
   const double unl = ql[1 + AXIS], unr = qr[1 + AXIS];
   const double smax = vmax_(fabs(unl) + cl, fabs(unr) + cr);
@@ -199,7 +198,7 @@ __device__ __forceinline__ void rusanov(const double (&ql)[5], const double (&qr
   fr[4] = (er + qr[4]) * unr;
 #pragma unroll
   for (int v = 0; v < 5; ++v) {
-    if constexpr (M != kTol)
+    if constexpr (!FAST)
       f[v] = 0.5 * (fl[v] + fr[v]) - hs * (ur[v] - ul[v]);
     else
       f[v] = fma(-hs, ur[v] - ul[v], 0.5 * (fl[v] + fr[v]));
@@ -278,66 +277,11 @@ __device__ __forceinline__ int interior_index(int axis, int c0, int c1, int c2) 
   return (cc[2] * kE + cc[1]) * kE + cc[0];
 }
 
-// Fluxes of faces 3r..3r+2 of one pencil. Stencil window: positions
-// 3r..3r+5 along the axis. Each cell's limited slope m[j] = minmod(d[j-1],
-// d[j]) is computed once and shared by the right state of face j-2 and the
-// left state of face j-1 (the reference evaluates the identical expression
-// twice, euler.hpp:32-33).
-template <int V, int AXIS, int M, bool EULER>
-__device__ __forceinline__ void face_compute(const double* __restrict__ sm, int r, int c1, int c2,
-                                             double gamma, double gm1, double ygm1, double a_vel,
-                                             double (&F)[3][V], bool& ok) {
-  const int base = 3 * r;
-  int a[6], vs[6];
-#pragma unroll
-  for (int s = 0; s < 6; ++s) pos_addr<V, AXIS>(base + s, c1, c2, a[s], vs[s]);
-  constexpr int NV = EULER ? 5 : 1;
-  double ql[3][NV], qr[3][NV];
-#pragma unroll
-  for (int v = 0; v < NV; ++v) {
-    double c[6], d[5], m[5];
-#pragma unroll
-    for (int s = 0; s < 6; ++s) c[s] = sm[a[s] + v * vs[s]];
-#pragma unroll
-    for (int i = 0; i < 5; ++i) d[i] = c[i + 1] - c[i];
-#pragma unroll
-    for (int j = 1; j < 5; ++j) m[j] = minmod_lane(d[j - 1], d[j]);
-#pragma unroll
-    for (int k = 0; k < 3; ++k) {
-      ql[k][v] = c[k + 1] + 0.5 * m[k + 1];
-      qr[k][v] = c[k + 2] - 0.5 * m[k + 2];
-    }
-  }
-#pragma unroll
-  for (int k = 0; k < 3; ++k) {
-    if constexpr (EULER) {
-      double l5[5], r5[5], f[5];
-#pragma unroll
-      for (int v = 0; v < 5; ++v) {
-        l5[v] = ql[k][v];
-        r5[v] = qr[k][v];
-      }
-      // stage.cpp:80-83 face floors
-      l5[0] = vmax_floor(l5[0], kRhoFloor);
-      r5[0] = vmax_floor(r5[0], kRhoFloor);
-      l5[4] = vmax_floor(l5[4], kPressureFloor);
-      r5[4] = vmax_floor(r5[4], kPressureFloor);
-      rusanov<AXIS, M>(l5, r5, gamma, gm1, ygm1, f, ok);
-#pragma unroll
-      for (int v = 0; v < 5; ++v) F[k][v] = f[v];
-    } else {
-      // stage.cpp:44-55 scalar advection on var 0; other vars keep zero flux
-      const double l = ql[k][0], rr = qr[k][0];
-      F[k][0] = 0.5 * (a_vel * l + a_vel * rr) - 0.5 * fabs(a_vel) * (rr - l);
-    }
-  }
-}
-
 // One axis of the stage: fluxes of 3 faces per lane, boundary-face record,
 // then (after the barrier) the divergence update of the lane's cells.
 template <int V, int AXIS, bool FAST, bool EULER>
 __device__ __forceinline__ void axis_pass(const double* __restrict__ sm, double* __restrict__ acc,
-                                          int tid, double gamma, double gm1, double ygm1,
+                                          int tid, double gamma, double gm1, double inv_gm1,
                                           bool gm1_ok, double a_vel, double cdt,
                                           double* faces_out) {
   int c1, c2, r, nb;
@@ -347,19 +291,56 @@ __device__ __forceinline__ void axis_pass(const double* __restrict__ sm, double*
   for (int k = 0; k < 3; ++k)
 #pragma unroll
     for (int v = 0; v < V; ++v) F[k][v] = 0.0;
-  bool ok = gm1_ok;
   if (active) {
-    if constexpr (FAST)
-      face_compute<V, AXIS, kTol, EULER>(sm, r, c1, c2, gamma, gm1, ygm1, a_vel, F, ok);
-    else
-      face_compute<V, AXIS, kFastExact, EULER>(sm, r, c1, c2, gamma, gm1, ygm1, a_vel, F, ok);
-  }
-  // exact fallback for lanes whose operands left the fast path's range
-  const bool redo = !FAST && active && !ok;
-  if (__any_sync(0xffffffffu, redo)) {
-    if (redo) face_compute<V, AXIS, kIeee, EULER>(sm, r, c1, c2, gamma, gm1, ygm1, a_vel, F, ok);
-  }
-  if (active) {
+    // Stencil window: positions 3r..3r+5 along the axis serve faces 3r..3r+2.
+    // Each cell's limited slope m[j] = minmod(d[j-1], d[j]) is computed once
+    // and shared by the right state of face j-2 and the left state of face
+    // j-1 (the reference evaluates the identical expression twice,
+    // euler.hpp:32-33).
+    const int base = 3 * r;
+    int a[6], vs[6];
+#pragma unroll
+    for (int s = 0; s < 6; ++s) pos_addr<V, AXIS>(base + s, c1, c2, a[s], vs[s]);
+    constexpr int NV = EULER ? 5 : 1;
+    double ql[3][NV], qr[3][NV];
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+      double c[6], d[5], m[5];
+#pragma unroll
+      for (int s = 0; s < 6; ++s) c[s] = sm[a[s] + v * vs[s]];
+#pragma unroll
+      for (int i = 0; i < 5; ++i) d[i] = c[i + 1] - c[i];
+#pragma unroll
+      for (int j = 1; j < 5; ++j) m[j] = minmod_lane(d[j - 1], d[j]);
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        ql[k][v] = c[k + 1] + 0.5 * m[k + 1];
+        qr[k][v] = c[k + 2] - 0.5 * m[k + 2];
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      if constexpr (EULER) {
+        double l5[5], r5[5], f[5];
+#pragma unroll
+        for (int v = 0; v < 5; ++v) {
+          l5[v] = ql[k][v];
+          r5[v] = qr[k][v];
+        }
+        // stage.cpp:80-83 face floors
+        l5[0] = vmax_(l5[0], kRhoFloor);
+        r5[0] = vmax_(r5[0], kRhoFloor);
+        l5[4] = vmax_(l5[4], kPressureFloor);
+        r5[4] = vmax_(r5[4], kPressureFloor);
+        rusanov<AXIS, FAST>(l5, r5, gamma, gm1, inv_gm1, gm1_ok, f);
+#pragma unroll
+        for (int v = 0; v < 5; ++v) F[k][v] = f[v];
+      } else {
+        // stage.cpp:44-55 scalar advection on var 0; other vars keep zero flux
+        const double l = ql[k][0], rr = qr[k][0];
+        F[k][0] = 0.5 * (a_vel * l + a_vel * rr) - 0.5 * fabs(a_vel) * (rr - l);
+      }
+    }
     // boundary-face record (stage.cpp:180-182): F[0] -> side 0, F[E] -> side 1
     if (faces_out) {
       const int fo = c2 * kE + c1;
@@ -471,8 +452,8 @@ __global__ void __launch_bounds__(kStageThreads, 2)
   const bool euler = mode != 0.0;
   const double cdt = dt / dx;
   const double gm1 = gamma - 1.0;
-  const double ygm1 = fm_rcp(gm1);  // reciprocal for the Markstein divisions by (gamma - 1)
-  const bool gm1_ok = fm_range_ok(gm1) && fm_range_ok(ygm1);
+  const double inv_gm1 = 1.0 / gm1;  // RN(1/(gamma-1)) for div_rn
+  const bool gm1_ok = exp_ok(gm1) && exp_ok(inv_gm1);
 
   __syncthreads();  // barrier init visible
   mbar_wait(bar, 0);
@@ -507,20 +488,15 @@ __global__ void __launch_bounds__(kStageThreads, 2)
         const double rho = stdmax_(u[0], kRhoFloor);
         double iu, iv, iw, ke, pr;
         if constexpr (!FAST) {
-          const double yr = fm_rcp(rho);  // one reciprocal, three exact quotients
-          iu = fm_div_y(u[1], rho, yr);
-          iv = fm_div_y(u[2], rho, yr);
-          iw = fm_div_y(u[3], rho, yr);
-          if (!(fm_range_ok(rho) && fm_range_ok(u[1]) && fm_range_ok(u[2]) && fm_range_ok(u[3]) &&
-                fm_range_ok(iu) && fm_range_ok(iv) && fm_range_ok(iw))) {
-            iu = u[1] / rho;  // exact fallback (zeros, extremes, inf, NaN)
-            iv = u[2] / rho;
-            iw = u[3] / rho;
-          }
+          const double yr = __drcp_rn(rho);  // RN(1/rho)
+          const bool rok = exp_ok(rho) && exp_ok(yr);
+          iu = div_rn(u[1], rho, yr, rok);
+          iv = div_rn(u[2], rho, yr, rok);
+          iw = div_rn(u[3], rho, yr, rok);
           ke = 0.5 * rho * (iu * iu + iv * iv + iw * iw);
           pr = stdmax_(gm1 * (u[4] - ke), kPressureFloor);
         } else {
-          const double ir = fm_rcp(rho);
+          const double ir = __drcp_rn(rho);
           iu = u[1] * ir;
           iv = u[2] * ir;
           iw = u[3] * ir;
@@ -540,13 +516,13 @@ __global__ void __launch_bounds__(kStageThreads, 2)
   // ---- phase 3: x, y, z passes
   double* faces_out = p.faces ? p.faces + (long long)slot * p.faces_stride : nullptr;
   if (V == 5 && euler) {
-    axis_pass<V, 0, FAST, (V == 5)>(sm, acc, tid, gamma, gm1, ygm1, gm1_ok, 0.0, cdt, faces_out);
-    axis_pass<V, 1, FAST, (V == 5)>(sm, acc, tid, gamma, gm1, ygm1, gm1_ok, 0.0, cdt, faces_out);
-    axis_pass<V, 2, FAST, (V == 5)>(sm, acc, tid, gamma, gm1, ygm1, gm1_ok, 0.0, cdt, faces_out);
+    axis_pass<V, 0, FAST, (V == 5)>(sm, acc, tid, gamma, gm1, inv_gm1, gm1_ok, 0.0, cdt, faces_out);
+    axis_pass<V, 1, FAST, (V == 5)>(sm, acc, tid, gamma, gm1, inv_gm1, gm1_ok, 0.0, cdt, faces_out);
+    axis_pass<V, 2, FAST, (V == 5)>(sm, acc, tid, gamma, gm1, inv_gm1, gm1_ok, 0.0, cdt, faces_out);
   } else {
-    axis_pass<V, 0, FAST, false>(sm, acc, tid, gamma, gm1, ygm1, gm1_ok, ax, cdt, faces_out);
-    axis_pass<V, 1, FAST, false>(sm, acc, tid, gamma, gm1, ygm1, gm1_ok, ay, cdt, faces_out);
-    axis_pass<V, 2, FAST, false>(sm, acc, tid, gamma, gm1, ygm1, gm1_ok, az, cdt, faces_out);
+    axis_pass<V, 0, FAST, false>(sm, acc, tid, gamma, gm1, inv_gm1, gm1_ok, ax, cdt, faces_out);
+    axis_pass<V, 1, FAST, false>(sm, acc, tid, gamma, gm1, inv_gm1, gm1_ok, ay, cdt, faces_out);
+    axis_pass<V, 2, FAST, false>(sm, acc, tid, gamma, gm1, inv_gm1, gm1_ok, az, cdt, faces_out);
   }
   __syncthreads();
 
@@ -566,12 +542,9 @@ __global__ void __launch_bounds__(kStageThreads, 2)
         }
         double ke, pr;
         if constexpr (!FAST) {
-          const double num = 0.5 * (u[1] * u[1] + u[2] * u[2] + u[3] * u[3]);
-          bool kok = true;
-          ke = fm_div(num, u[0], kok);
-          if (!kok) ke = num / u[0];
+          ke = 0.5 * (u[1] * u[1] + u[2] * u[2] + u[3] * u[3]) / u[0];
         } else {
-          ke = 0.5 * fma(u[1], u[1], fma(u[2], u[2], u[3] * u[3])) * fm_rcp(u[0]);
+          ke = 0.5 * fma(u[1], u[1], fma(u[2], u[2], u[3] * u[3])) * __drcp_rn(u[0]);
         }
         pr = gm1 * (u[4] - ke);
         if (pr < kPressureFloor) {
