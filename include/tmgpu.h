@@ -186,6 +186,22 @@ const double* tmgpu_region_output(tmgpu_region* r, long long ticket);   /* Slice
 size_t tmgpu_region_submitted(tmgpu_region* r);                           /* submitted() */
 void tmgpu_region_destroy(tmgpu_region* r);
 
+/* ---------------------------------------------------------------- gravity (FMM)
+ * No reference implementation exists: our cell-level FMM,
+ * restated bitwise in oracle/gravity_oracle.c. Uniform cell level D (N = 2^D per
+ * axis, unit box, isolated boundaries, G = 1); outputs phi[N^3], g[3][N^3] in
+ * (k,j,i) order. */
+typedef struct tmgpu_gravity tmgpu_gravity;
+tmgpu_gravity* tmgpu_gravity_create(int D, tmgpu_error* err);
+void tmgpu_gravity_destroy(tmgpu_gravity* g);
+int tmgpu_gravity_solve(tmgpu_gravity* G, const double* mass, double* phi, double* g, int flags,
+                        void* stream, tmgpu_error* err);
+int tmgpu_gravity_mass_from_arena(tmgpu_gravity* G, const double* arena, const int* leaf_ijk_dev,
+                                  long long nleaves, int vars, double dV, void* stream,
+                                  tmgpu_error* err);
+int tmgpu_selftest_fastmath(int mode, long long n, uint64_t seed, unsigned long long* mismatches,
+                            unsigned long long* checked, double* first_bad, tmgpu_error* err);
+
 /* FP64 DFMA throughput microbenchmark (roofline denominator) */
 int tmgpu_fp64_peak(int iters, double* tflops, double* ms, tmgpu_error* err);
 

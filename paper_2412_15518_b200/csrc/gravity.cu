@@ -1,0 +1,356 @@
+// Cell-level FMM gravity on a uniform octree level (rows a12/a13 of SURVEY.md §8).
+//
+// The reference has no gravity code (prose only, PAPER.md:120,
+// 233,238,241,347), so the specification is ours and is restated operation by
+// operation in oracle/gravity_oracle.c; these kernels follow
+// the same operation order and are bitwise equal to it (-fmad=false).
+//
+//   P2M   masses m = rho * h^3 of the finest cells (from the leaf arena)
+//   M2M   order-2 Cartesian moments (M, D_i, Q_ij) per cell of every level
+//   M2L   per level, each cell sums its 189-cell interaction list ("stencil
+//         approach"): children of the parent's 27 neighbours that
+//         are not its own neighbours; Dehnen truncation |alpha|+|beta| <= 2,
+//         which makes every mutual pair force exactly opposite (linear
+//         momentum conserved to round-off)
+//   L2L   local expansions shifted down the levels
+//   P2P   monopole near field over the 26 neighbours at the finest level,
+//         fused with L2P (phi = L0, g = -L_i at the cell centre)
+#include <cstring>
+#include <vector>
+
+#include "tmgpu_internal.h"
+
+namespace tmgpu {
+namespace {
+
+__device__ __forceinline__ int s2(int i, int j) {
+  return (i == 0) ? j : (i == 1) ? (j == 0 ? 1 : 2 + j) : (j == 0 ? 2 : 3 + j);
+}
+
+// identical arithmetic to oracle/gravity_oracle.c:tmo_grav_m2l (accumulates)
+__device__ __forceinline__ void m2l(const double* __restrict__ mom, const double R[3],
+                                    double out[10]) {
+  const double x = R[0], y = R[1], z = R[2];
+  const double r2 = x * x + y * y + z * z;
+  const double r = sqrt(r2);
+  const double ir = 1.0 / r;
+  const double ir2 = ir * ir;
+  const double ir3 = ir * ir2, ir5 = ir3 * ir2;
+  double d1[3], d2[3][3];
+#pragma unroll
+  for (int i = 0; i < 3; ++i) d1[i] = -R[i] * ir3;
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int j = 0; j < 3; ++j) d2[i][j] = 3.0 * R[i] * R[j] * ir5 - (i == j ? ir3 : 0.0);
+  const double M = mom[0];
+  const double Dp[3] = {mom[1], mom[2], mom[3]};
+  double Q[3][3];
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int j = 0; j < 3; ++j) Q[i][j] = mom[4 + s2(i, j)];
+  double a = M * ir, b = 0.0, c = 0.0;
+#pragma unroll
+  for (int i = 0; i < 3; ++i) b += Dp[i] * d1[i];
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int j = 0; j < 3; ++j) c += Q[i][j] * d2[i][j];
+  out[0] += -(a - b + 0.5 * c);
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    double bb = 0.0;
+#pragma unroll
+    for (int j = 0; j < 3; ++j) bb += Dp[j] * d2[i][j];
+    out[1 + i] += -(M * d1[i] - bb);
+  }
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int j = i; j < 3; ++j) out[4 + s2(i, j)] += -(M * d2[i][j]);
+}
+
+__device__ __forceinline__ long long cidx(long long n, long long i, long long j, long long k) {
+  return (k * n + j) * n + i;
+}
+
+__global__ void p2m_kernel(const double* __restrict__ mass, double* __restrict__ mom, long long n3) {
+  for (long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x; c < n3;
+       c += (long long)gridDim.x * blockDim.x) {
+    double* o = mom + c * 10;
+    o[0] = mass[c];
+#pragma unroll
+    for (int q = 1; q < 10; ++q) o[q] = 0.0;
+  }
+}
+
+// arena (uniform level, leaf slot = canonical Morton order) -> finest masses (k,j,i)
+__global__ void arena_mass_kernel(const double* __restrict__ arena, const int* __restrict__ leaf_ijk,
+                                  long long nleaves, int V, double dV, long long N,
+                                  double* __restrict__ mass) {
+  const long long total = nleaves * 512;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
+       t += (long long)gridDim.x * blockDim.x) {
+    const long long s = t >> 9;
+    const int c = (int)(t & 511);
+    const int i = c & 7, j = (c >> 3) & 7, k = c >> 6;
+    const double rho = arena[s * V * 1728 + ((k + 2) * 12 + (j + 2)) * 12 + (i + 2)];
+    const long long gi = leaf_ijk[3 * s] * 8LL + i, gj = leaf_ijk[3 * s + 1] * 8LL + j,
+                    gk = leaf_ijk[3 * s + 2] * 8LL + k;
+    mass[cidx(N, gi, gj, gk)] = rho * dV;
+  }
+}
+
+__global__ void m2m_kernel(const double* __restrict__ child, double* __restrict__ parent, long long n,
+                           double hc) {
+  const long long n3 = n * n * n;
+  for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < n3;
+       p += (long long)gridDim.x * blockDim.x) {
+    const long long I = p % n, J = (p / n) % n, K = p / (n * n);
+    double o[10];
+#pragma unroll
+    for (int q = 0; q < 10; ++q) o[q] = 0.0;
+    for (int c = 0; c < 2; ++c)
+      for (int b = 0; b < 2; ++b)
+        for (int a = 0; a < 2; ++a) {
+          const double s[3] = {(a - 0.5) * hc, (b - 0.5) * hc, (c - 0.5) * hc};
+          const double* ch = child + cidx(2 * n, 2 * I + a, 2 * J + b, 2 * K + c) * 10;
+          const double M = ch[0];
+          o[0] += M;
+#pragma unroll
+          for (int i = 0; i < 3; ++i) o[1 + i] += ch[1 + i] + M * s[i];
+#pragma unroll
+          for (int i = 0; i < 3; ++i)
+#pragma unroll
+            for (int j = i; j < 3; ++j)
+              o[4 + s2(i, j)] += ch[4 + s2(i, j)] + ch[1 + i] * s[j] + s[i] * ch[1 + j] + M * s[i] * s[j];
+        }
+    double* out = parent + p * 10;
+#pragma unroll
+    for (int q = 0; q < 10; ++q) out[q] = o[q];
+  }
+}
+
+__global__ void __launch_bounds__(128) m2l_kernel(const double* __restrict__ mom,
+                                                  double* __restrict__ loc, long long m, double h) {
+  const long long n3 = m * m * m;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < n3;
+       t += (long long)gridDim.x * blockDim.x) {
+    const long long i = t % m, j = (t / m) % m, k = t / (m * m);
+    double o[10];
+#pragma unroll
+    for (int q = 0; q < 10; ++q) o[q] = 0.0;
+    for (long long dz = -2 - (k & 1); dz <= 3 - (k & 1); ++dz)
+      for (long long dy = -2 - (j & 1); dy <= 3 - (j & 1); ++dy)
+        for (long long dx = -2 - (i & 1); dx <= 3 - (i & 1); ++dx) {
+          if (dx >= -1 && dx <= 1 && dy >= -1 && dy <= 1 && dz >= -1 && dz <= 1) continue;
+          const long long si = i + dx, sj = j + dy, sk = k + dz;
+          if (si < 0 || sj < 0 || sk < 0 || si >= m || sj >= m || sk >= m) continue;
+          const double R[3] = {-(double)dx * h, -(double)dy * h, -(double)dz * h};
+          m2l(mom + cidx(m, si, sj, sk) * 10, R, o);
+        }
+    double* out = loc + t * 10;
+#pragma unroll
+    for (int q = 0; q < 10; ++q) out[q] = o[q];
+  }
+}
+
+__global__ void l2l_kernel(const double* __restrict__ parent, double* __restrict__ loc, long long m,
+                           double h) {
+  const long long n3 = m * m * m;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < n3;
+       t += (long long)gridDim.x * blockDim.x) {
+    const long long i = t % m, j = (t / m) % m, k = t / (m * m);
+    const double s[3] = {((i & 1) - 0.5) * h, ((j & 1) - 0.5) * h, ((k & 1) - 0.5) * h};
+    const double* L = parent + cidx(m / 2, i >> 1, j >> 1, k >> 1) * 10;
+    double Lm[3][3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+      for (int b = 0; b < 3; ++b) Lm[a][b] = L[4 + s2(a, b)];
+    double t1 = 0.0, t2 = 0.0;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) t1 += L[1 + a] * s[a];
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+      for (int b = 0; b < 3; ++b) t2 += Lm[a][b] * s[a] * s[b];
+    double sh[10];
+    sh[0] = L[0] + t1 + 0.5 * t2;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      double u = 0.0;
+#pragma unroll
+      for (int b = 0; b < 3; ++b) u += Lm[a][b] * s[b];
+      sh[1 + a] = L[1 + a] + u;
+    }
+#pragma unroll
+    for (int q = 0; q < 6; ++q) sh[4 + q] = L[4 + q];
+    double* out = loc + t * 10;
+#pragma unroll
+    for (int q = 0; q < 10; ++q) out[q] = sh[q] + out[q];
+  }
+}
+
+__global__ void p2p_kernel(const double* __restrict__ mass, const double* __restrict__ loc,
+                           long long N, double h, double* __restrict__ phi, double* __restrict__ g) {
+  const long long n3 = N * N * N;
+  for (long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x; c < n3;
+       c += (long long)gridDim.x * blockDim.x) {
+    const long long i = c % N, j = (c / N) % N, k = c / (N * N);
+    const double* L = loc + c * 10;
+    double p = L[0], gx = -L[1], gy = -L[2], gz = -L[3];
+    for (int dz = -1; dz <= 1; ++dz)
+      for (int dy = -1; dy <= 1; ++dy)
+        for (int dx = -1; dx <= 1; ++dx) {
+          if (!dx && !dy && !dz) continue;
+          const long long si = i + dx, sj = j + dy, sk = k + dz;
+          if (si < 0 || sj < 0 || sk < 0 || si >= N || sj >= N || sk >= N) continue;
+          const double ms = mass[cidx(N, si, sj, sk)];
+          const double Rx = -(double)dx * h, Ry = -(double)dy * h, Rz = -(double)dz * h;
+          const double r2 = Rx * Rx + Ry * Ry + Rz * Rz;
+          const double ir = 1.0 / sqrt(r2);
+          const double ir3 = ir * ir * ir;
+          p -= ms * ir;
+          gx -= ms * Rx * ir3;
+          gy -= ms * Ry * ir3;
+          gz -= ms * Rz * ir3;
+        }
+    phi[c] = p;
+    g[c] = gx;
+    g[n3 + c] = gy;
+    g[2 * n3 + c] = gz;
+  }
+}
+
+unsigned grid_for(long long n) {
+  long long b = (n + 127) / 128;
+  if (b < 1) b = 1;
+  if (b > 148 * 64) b = 148 * 64;
+  return (unsigned)b;
+}
+
+}  // namespace
+
+struct GravityWork {
+  int D = 0;
+  std::vector<double*> mom, loc;
+  double* mass = nullptr;
+};
+
+}  // namespace tmgpu
+
+using namespace tmgpu;
+
+struct tmgpu_gravity {
+  GravityWork w;
+};
+
+extern "C" {
+
+// Workspace for a uniform cell level D (N = 2^D cells per axis).
+tmgpu_gravity* tmgpu_gravity_create(int D, tmgpu_error* err) {
+  if (err) std::memset(err, 0, sizeof(*err));
+  if (D < 2 || D > 11) {
+    set_err(err, TMGPU_ERR_INVALID, "gravity: cell level must be in [2, 11]");
+    return nullptr;
+  }
+  auto* g = new tmgpu_gravity;
+  g->w.D = D;
+  cudaError_t e = cudaSuccess;
+  for (int l = 0; l <= D && e == cudaSuccess; ++l) {
+    const size_t n3 = (size_t)1 << (3 * l);
+    double *m = nullptr, *L = nullptr;
+    e = cudaMalloc(&m, n3 * 10 * sizeof(double));
+    if (e == cudaSuccess) e = cudaMalloc(&L, n3 * 10 * sizeof(double));
+    g->w.mom.push_back(m);
+    g->w.loc.push_back(L);
+  }
+  if (e == cudaSuccess) e = cudaMalloc(&g->w.mass, ((size_t)1 << (3 * D)) * sizeof(double));
+  if (e != cudaSuccess) {
+    cuda_err(err, e, "tmgpu_gravity_create");
+    for (auto p : g->w.mom)
+      if (p) cudaFree(p);
+    for (auto p : g->w.loc)
+      if (p) cudaFree(p);
+    delete g;
+    return nullptr;
+  }
+  return g;
+}
+
+void tmgpu_gravity_destroy(tmgpu_gravity* g) {
+  if (!g) return;
+  for (auto p : g->w.mom) cudaFree(p);
+  for (auto p : g->w.loc) cudaFree(p);
+  if (g->w.mass) cudaFree(g->w.mass);
+  delete g;
+}
+
+// Solve from finest-level masses ((k,j,i), x fastest). mass == NULL: use the
+// workspace masses (filled by tmgpu_gravity_mass_from_forest). Device pointers
+// unless TMGPU_HOST_PTRS. phi: N^3, g: 3 x N^3.
+int tmgpu_gravity_solve(tmgpu_gravity* G, const double* mass, double* phi, double* g, int flags,
+                        void* stream, tmgpu_error* err) {
+  if (err) std::memset(err, 0, sizeof(*err));
+  cudaStream_t st = as_stream(stream);
+  GravityWork& w = G->w;
+  const int D = w.D;
+  const long long N = 1LL << D, n3 = N * N * N;
+  const bool host = (flags & TMGPU_HOST_PTRS) != 0;
+  cudaError_t e = cudaSuccess;
+  double *dphi = phi, *dg = g;
+  if (mass) {
+    e = cudaMemcpyAsync(w.mass, mass, n3 * sizeof(double),
+                        host ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice, st);
+  }
+  if (host && e == cudaSuccess) {
+    e = cudaMallocAsync(&dphi, n3 * sizeof(double), st);
+    if (e == cudaSuccess) e = cudaMallocAsync(&dg, 3 * n3 * sizeof(double), st);
+  }
+  if (e == cudaSuccess) {
+    p2m_kernel<<<grid_for(n3), 128, 0, st>>>(w.mass, w.mom[D], n3);
+    for (int l = D - 1; l >= 0; --l)
+      m2m_kernel<<<grid_for(1LL << (3 * l)), 128, 0, st>>>(w.mom[l + 1], w.mom[l], 1LL << l,
+                                                          1.0 / (double)(1LL << (l + 1)));
+    for (int l = 2; l <= D; ++l)
+      m2l_kernel<<<grid_for(1LL << (3 * l)), 128, 0, st>>>(w.mom[l], w.loc[l], 1LL << l,
+                                                          1.0 / (double)(1LL << l));
+    for (int l = 3; l <= D; ++l)
+      l2l_kernel<<<grid_for(1LL << (3 * l)), 128, 0, st>>>(w.loc[l - 1], w.loc[l], 1LL << l,
+                                                          1.0 / (double)(1LL << l));
+    p2p_kernel<<<grid_for(n3), 128, 0, st>>>(w.mass, w.loc[D], N, 1.0 / (double)N, dphi, dg);
+    g_launches.fetch_add(2 + D + 2 * (D - 1), std::memory_order_relaxed);
+    e = cudaGetLastError();
+  }
+  if (host) {
+    if (e == cudaSuccess) e = cudaMemcpyAsync(phi, dphi, n3 * sizeof(double), cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(g, dg, 3 * n3 * sizeof(double), cudaMemcpyDeviceToHost, st);
+    if (dphi && dphi != phi) cudaFreeAsync(dphi, st);
+    if (dg && dg != g) cudaFreeAsync(dg, st);
+    cudaError_t e2 = cudaStreamSynchronize(st);
+    if (e == cudaSuccess) e = e2;
+  } else if (!(flags & TMGPU_ASYNC)) {
+    cudaError_t e2 = cudaStreamSynchronize(st);
+    if (e == cudaSuccess) e = e2;
+  }
+  return cuda_err(err, e, "tmgpu_gravity_solve");
+}
+
+// Finest-level masses from a device leaf arena of a UNIFORM forest: leaf s
+// covers cells 8*leaf_ijk[3s..3s+2] + (i,j,k); mass = rho * dV.
+int tmgpu_gravity_mass_from_arena(tmgpu_gravity* G, const double* arena, const int* leaf_ijk_dev,
+                                  long long nleaves, int vars, double dV, void* stream,
+                                  tmgpu_error* err) {
+  if (err) std::memset(err, 0, sizeof(*err));
+  const long long N = 1LL << G->w.D;
+  if (nleaves * 512 != N * N * N) return set_err(err, TMGPU_ERR_INVALID, "gravity: leaves do not tile the level");
+  cudaStream_t st = as_stream(stream);
+  arena_mass_kernel<<<grid_for(nleaves * 512), 128, 0, st>>>(arena, leaf_ijk_dev, nleaves, vars, dV,
+                                                             N, G->w.mass);
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return cuda_err(err, cudaGetLastError(), "tmgpu_gravity_mass_from_arena");
+}
+
+}  // extern "C"

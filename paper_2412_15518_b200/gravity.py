@@ -1,0 +1,92 @@
+"""FMM gravity on a uniform cell level.
+
+The reference has no gravity code, so the algorithm is our own
+specification, restated in oracle/gravity_oracle.c and matched
+bitwise by the sm_100a kernels (csrc/gravity.cu): order-2 Cartesian
+multipoles, the 189-cell same-level interaction stencil (M2L, Dehnen
+truncation -> exact linear-momentum conservation), L2L, and the 26-neighbour
+monopole near field (P2P) fused with L2P.
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from . import _lib
+from ._lib import TmgpuError, lib
+
+_vp = C.c_void_p
+_ep = C.POINTER(TmgpuError)
+lib.tmgpu_gravity_create.restype = _vp
+lib.tmgpu_gravity_create.argtypes = [C.c_int, _ep]
+lib.tmgpu_gravity_destroy.restype = None
+lib.tmgpu_gravity_destroy.argtypes = [_vp]
+lib.tmgpu_gravity_solve.restype = C.c_int
+lib.tmgpu_gravity_solve.argtypes = [_vp, _vp, _vp, _vp, C.c_int, _vp, _ep]
+lib.tmgpu_gravity_mass_from_arena.restype = C.c_int
+lib.tmgpu_gravity_mass_from_arena.argtypes = [_vp, _vp, _vp, C.c_longlong, C.c_int, C.c_double,
+                                              _vp, _ep]
+
+
+class GravitySolver:
+    """FMM on a uniform level of N = 2^D cells per axis (unit box)."""
+
+    def __init__(self, D: int):
+        err = TmgpuError()
+        self.D, self.N = D, 1 << D
+        self.h = lib.tmgpu_gravity_create(D, C.byref(err))
+        if not self.h:
+            _lib.check(err.code or _lib.TMGPU_ERR_CUDA, err)
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            lib.tmgpu_gravity_destroy(self.h)
+            self.h = None
+
+    def solve(self, mass):
+        """mass: N^3 finest-level masses, (k,j,i) order (numpy: host path;
+        CUDA tensor: device path). Returns (phi[N^3], g[3, N^3])."""
+        n3 = self.N ** 3
+        err = TmgpuError()
+        if isinstance(mass, np.ndarray):
+            m = np.ascontiguousarray(mass, dtype=np.float64).reshape(-1)
+            if m.size != n3:
+                raise ValueError("mass must have N^3 entries")
+            phi, g = np.zeros(n3), np.zeros(3 * n3)
+            _lib.check(lib.tmgpu_gravity_solve(self.h, m.ctypes.data, phi.ctypes.data,
+                                               g.ctypes.data, _lib.TMGPU_HOST_PTRS, None,
+                                               C.byref(err)), err)
+            return phi, g.reshape(3, -1)
+        import torch
+
+        phi = torch.empty(n3, dtype=torch.float64, device=mass.device)
+        g = torch.empty(3 * n3, dtype=torch.float64, device=mass.device)
+        st = torch.cuda.current_stream(mass.device).cuda_stream
+        _lib.check(lib.tmgpu_gravity_solve(self.h, mass.data_ptr(), phi.data_ptr(), g.data_ptr(),
+                                           0, st, C.byref(err)), err)
+        return phi, g.view(3, -1)
+
+    def solve_forest(self, forest, phi, g, stream=None, sync=True):
+        """Gravity of a uniform forest's device state (rho -> masses -> FMM)
+        into device tensors phi[N^3], g[3*N^3]."""
+        import torch
+
+        if getattr(self, "_ijk_for", None) != id(forest):
+            from .amr import unpack
+
+            leaves = [unpack(int(p)) for p in forest.local_leaves()]
+            if {lv[0] for lv in leaves} != {self.D - 3}:
+                raise ValueError("gravity needs a uniform forest at level D - 3")
+            ijk = np.array([lv[1:] for lv in leaves], dtype=np.int32).reshape(-1)
+            self._ijk = torch.from_numpy(ijk).cuda()
+            self._ijk_for = id(forest)
+        hc = 1.0 / self.N
+        err = TmgpuError()
+        _lib.check(lib.tmgpu_gravity_mass_from_arena(self.h, forest.arena_ptr(),
+                                                     self._ijk.data_ptr(), forest.local_count(),
+                                                     forest.vars, hc * hc * hc, stream,
+                                                     C.byref(err)), err)
+        _lib.check(lib.tmgpu_gravity_solve(self.h, None, phi.data_ptr(), g.data_ptr(),
+                                           0 if sync else _lib.TMGPU_ASYNC, stream, C.byref(err)),
+                   err)
