@@ -47,6 +47,7 @@ def parse():
     ap.add_argument("--max-level", type=int, default=5)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-steps", type=int, default=2)
+    ap.add_argument("--no-gravity", action="store_true")
     return ap.parse_args()
 
 
@@ -164,6 +165,64 @@ def time_reference(f, state, steps, warmup=0):
         ex += tex
         st += tst
     return statistics.median(walls), cores, {"exchange_s": ex / steps, "stage_s": st / steps}
+
+
+M2L_FLOP = 68  # per interaction (oracle/gravity_oracle.c contraction, geometry tabulated)
+P2P_FLOP = 20  # per near-field pair (sqrt and division counted as 1)
+
+
+def fmm_work(D):
+    """(M2L interactions, P2P pairs) of the FMM on level D."""
+    def axis(n, lo, hi):
+        return sum(sum(1 for d in range(lo(i), hi(i) + 1) if 0 <= i + d < n) for i in range(n))
+
+    m2l = 0
+    for l in range(2, D + 1):
+        n = 1 << l
+        A = axis(n, lambda i: -2 - (i & 1), lambda i: 3 - (i & 1))
+        B = axis(n, lambda i: -1, lambda i: 1)
+        m2l += A ** 3 - B ** 3
+    n = 1 << D
+    B = axis(n, lambda i: -1, lambda i: 1)
+    return m2l, B ** 3 - n ** 3
+
+
+def bench_gravity(stream, peak_tf):
+    """configs[1]: uniform level-4 octree (4,096 leaves, 128^3 cells), one FMM
+    gravity solve from the device arena (rho -> masses -> P2M..P2P)."""
+    import torch
+
+    from paper_2412_15518_b200 import amr
+    from paper_2412_15518_b200.gravity import GravitySolver
+
+    f = amr.build_scenario(amr.Scenario.rotating_star, 4, 4)
+    f.alloc()
+    f.set_interior(f.scenario_state(amr.Scenario.rotating_star))
+    G = GravitySolver(7)
+    n3 = 128 ** 3
+    phi = torch.empty(n3, dtype=torch.float64, device="cuda")
+    g = torch.empty(3 * n3, dtype=torch.float64, device="cuda")
+    sp = stream.cuda_stream
+    for _ in range(3):
+        G.solve_forest(f, phi, g, stream=sp, sync=False)
+    torch.cuda.synchronize()
+    reps = 20
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(reps):
+        G.solve_forest(f, phi, g, stream=sp, sync=False)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / reps
+    m2l, p2p = fmm_work(7)
+    tf = (m2l * M2L_FLOP + p2p * P2P_FLOP) / (ms * 1e-3) / 1e12
+    return {"config": "configs[1]: rotating star, uniform level-4 octree (4,096 leaves, 128^3 "
+                      "cells), one FMM solve (our spec, DESIGN.md §7; no reference exists)",
+            "ms_per_solve": ms, "cells_per_s": n3 / (ms * 1e-3),
+            "m2l_interactions": m2l, "p2p_pairs": p2p,
+            "roofline": {"bound": "fp64", "achieved": tf, "peak": peak_tf, "unit": "TFLOP/s",
+                         "frac": tf / peak_tf if peak_tf else None,
+                         "alg_flop": f"{M2L_FLOP}/M2L interaction + {P2P_FLOP}/P2P pair"}}
 
 
 # ---------------------------------------------------------------- arms
@@ -344,6 +403,8 @@ def run_ours(args, rank, world):
             "gpu_launches": launches,
             "clocks": clk.summary()}
 
+    if rank == 0 and world == 1 and not args.no_gravity:
+        line["gravity"] = bench_gravity(stream, peak_tf.value)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
             sec, cores, detail = time_reference(f, state, args.cpu_steps)

@@ -27,22 +27,47 @@ __device__ __forceinline__ int s2(int i, int j) {
   return (i == 0) ? j : (i == 1) ? (j == 0 ? 1 : 2 + j) : (j == 0 ? 2 : 3 + j);
 }
 
-// identical arithmetic to oracle/gravity_oracle.c:tmo_grav_m2l (accumulates)
-__device__ __forceinline__ void m2l(const double* __restrict__ mom, const double R[3],
-                                    double out[10]) {
+// The stencil approach: on a uniform level R depends only on
+// the integer offset, so 1/r, D1 and D2 of each of the 7^3 offsets are
+// computed once per level (with m2l's exact operations) and the per-pair M2L
+// reduces to contractions. Table entry: [ir, d1[3], d2[3][3]] = 13 doubles.
+constexpr int kOff = 7, kOff3 = 343, kTab = 13;
+
+__global__ void stencil_table_kernel(double* __restrict__ tab, int D) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (D + 1) * kOff3) return;
+  const int l = t / kOff3, o = t % kOff3;
+  const int dx = o % kOff - 3, dy = (o / kOff) % kOff - 3, dz = o / (kOff * kOff) - 3;
+  double* e = tab + (long long)t * kTab;
+  if (dx == 0 && dy == 0 && dz == 0) {
+    for (int q = 0; q < kTab; ++q) e[q] = 0.0;
+    return;
+  }
+  const double h = 1.0 / (double)(1LL << l);
+  const double R[3] = {-(double)dx * h, -(double)dy * h, -(double)dz * h};
   const double x = R[0], y = R[1], z = R[2];
   const double r2 = x * x + y * y + z * z;
   const double r = sqrt(r2);
   const double ir = 1.0 / r;
   const double ir2 = ir * ir;
   const double ir3 = ir * ir2, ir5 = ir3 * ir2;
+  e[0] = ir;
+  for (int i = 0; i < 3; ++i) e[1 + i] = -R[i] * ir3;
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j) e[4 + 3 * i + j] = 3.0 * R[i] * R[j] * ir5 - (i == j ? ir3 : 0.0);
+}
+
+// m2l with the offset's precomputed geometry: identical arithmetic to m2l()
+__device__ __forceinline__ void m2l_tab(const double* __restrict__ mom,
+                                        const double* __restrict__ e, double out[10]) {
+  const double ir = e[0];
   double d1[3], d2[3][3];
 #pragma unroll
-  for (int i = 0; i < 3; ++i) d1[i] = -R[i] * ir3;
+  for (int i = 0; i < 3; ++i) d1[i] = e[1 + i];
 #pragma unroll
   for (int i = 0; i < 3; ++i)
 #pragma unroll
-    for (int j = 0; j < 3; ++j) d2[i][j] = 3.0 * R[i] * R[j] * ir5 - (i == j ? ir3 : 0.0);
+    for (int j = 0; j < 3; ++j) d2[i][j] = e[4 + 3 * i + j];
   const double M = mom[0];
   const double Dp[3] = {mom[1], mom[2], mom[3]};
   double Q[3][3];
@@ -133,7 +158,8 @@ __global__ void m2m_kernel(const double* __restrict__ child, double* __restrict_
 }
 
 __global__ void __launch_bounds__(128) m2l_kernel(const double* __restrict__ mom,
-                                                  double* __restrict__ loc, long long m, double h) {
+                                                  double* __restrict__ loc, long long m,
+                                                  const double* __restrict__ tab) {
   const long long n3 = m * m * m;
   for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < n3;
        t += (long long)gridDim.x * blockDim.x) {
@@ -147,8 +173,8 @@ __global__ void __launch_bounds__(128) m2l_kernel(const double* __restrict__ mom
           if (dx >= -1 && dx <= 1 && dy >= -1 && dy <= 1 && dz >= -1 && dz <= 1) continue;
           const long long si = i + dx, sj = j + dy, sk = k + dz;
           if (si < 0 || sj < 0 || sk < 0 || si >= m || sj >= m || sk >= m) continue;
-          const double R[3] = {-(double)dx * h, -(double)dy * h, -(double)dz * h};
-          m2l(mom + cidx(m, si, sj, sk) * 10, R, o);
+          m2l_tab(mom + cidx(m, si, sj, sk) * 10,
+                  tab + (((dz + 3) * kOff + (dy + 3)) * kOff + (dx + 3)) * kTab, o);
         }
     double* out = loc + t * 10;
 #pragma unroll
@@ -237,6 +263,7 @@ struct GravityWork {
   int D = 0;
   std::vector<double*> mom, loc;
   double* mass = nullptr;
+  double* tab = nullptr;  // [level][343][13] stencil geometry
 };
 
 }  // namespace tmgpu
@@ -268,6 +295,12 @@ tmgpu_gravity* tmgpu_gravity_create(int D, tmgpu_error* err) {
     g->w.loc.push_back(L);
   }
   if (e == cudaSuccess) e = cudaMalloc(&g->w.mass, ((size_t)1 << (3 * D)) * sizeof(double));
+  if (e == cudaSuccess) e = cudaMalloc(&g->w.tab, (size_t)(D + 1) * kOff3 * kTab * sizeof(double));
+  if (e == cudaSuccess) {
+    stencil_table_kernel<<<((D + 1) * kOff3 + 127) / 128, 128>>>(g->w.tab, D);
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    e = cudaDeviceSynchronize();
+  }
   if (e != cudaSuccess) {
     cuda_err(err, e, "tmgpu_gravity_create");
     for (auto p : g->w.mom)
@@ -285,6 +318,7 @@ void tmgpu_gravity_destroy(tmgpu_gravity* g) {
   for (auto p : g->w.mom) cudaFree(p);
   for (auto p : g->w.loc) cudaFree(p);
   if (g->w.mass) cudaFree(g->w.mass);
+  if (g->w.tab) cudaFree(g->w.tab);
   delete g;
 }
 
@@ -316,7 +350,7 @@ int tmgpu_gravity_solve(tmgpu_gravity* G, const double* mass, double* phi, doubl
                                                           1.0 / (double)(1LL << (l + 1)));
     for (int l = 2; l <= D; ++l)
       m2l_kernel<<<grid_for(1LL << (3 * l)), 128, 0, st>>>(w.mom[l], w.loc[l], 1LL << l,
-                                                          1.0 / (double)(1LL << l));
+                                                          w.tab + (long long)l * kOff3 * kTab);
     for (int l = 3; l <= D; ++l)
       l2l_kernel<<<grid_for(1LL << (3 * l)), 128, 0, st>>>(w.loc[l - 1], w.loc[l], 1LL << l,
                                                           1.0 / (double)(1LL << l));
