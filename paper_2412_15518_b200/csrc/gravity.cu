@@ -182,6 +182,51 @@ __global__ void __launch_bounds__(128) m2l_kernel(const double* __restrict__ mom
   }
 }
 
+// Tiled M2L for levels with m >= 8: a CTA owns an 8x4x4 block of targets
+// (128 threads, one target each); the union of their interaction lists is the
+// 12x8x8 source box [x0-2, x0+9] x [y0-2, y0+5] x [z0-2, z0+5], staged once in
+// shared memory (SoA by component) and reused by all 128 targets. Per-target
+// loop order and arithmetic are those of m2l_kernel (bitwise identical).
+constexpr int TBX = 8, TBY = 4, TBZ = 4;
+constexpr int SBX = TBX + 4, SBY = TBY + 4, SBZ = TBZ + 4, SB3 = SBX * SBY * SBZ;
+
+__global__ void __launch_bounds__(128) m2l_tiled_kernel(const double* __restrict__ mom,
+                                                        double* __restrict__ loc, long long m,
+                                                        const double* __restrict__ tab) {
+  __shared__ double sm[10 * SB3];  // 61,440 B
+  const long long nbx = m / TBX, nby = m / TBY;
+  const long long b = blockIdx.x;
+  const long long x0 = (b % nbx) * TBX, y0 = ((b / nbx) % nby) * TBY, z0 = (b / (nbx * nby)) * TBZ;
+  for (int q = threadIdx.x; q < SB3; q += blockDim.x) {
+    const long long sx = x0 - 2 + q % SBX, sy = y0 - 2 + (q / SBX) % SBY, sz = z0 - 2 + q / (SBX * SBY);
+    const bool in = sx >= 0 && sy >= 0 && sz >= 0 && sx < m && sy < m && sz < m;
+    const double* src = mom + cidx(m, in ? sx : 0, in ? sy : 0, in ? sz : 0) * 10;
+#pragma unroll
+    for (int c = 0; c < 10; ++c) sm[c * SB3 + q] = in ? src[c] : 0.0;
+  }
+  __syncthreads();
+  const int tx = threadIdx.x % TBX, ty = (threadIdx.x / TBX) % TBY, tz = threadIdx.x / (TBX * TBY);
+  const long long i = x0 + tx, j = y0 + ty, k = z0 + tz;
+  double o[10];
+#pragma unroll
+  for (int q = 0; q < 10; ++q) o[q] = 0.0;
+  for (long long dz = -2 - (k & 1); dz <= 3 - (k & 1); ++dz)
+    for (long long dy = -2 - (j & 1); dy <= 3 - (j & 1); ++dy)
+      for (long long dx = -2 - (i & 1); dx <= 3 - (i & 1); ++dx) {
+        if (dx >= -1 && dx <= 1 && dy >= -1 && dy <= 1 && dz >= -1 && dz <= 1) continue;
+        const long long si = i + dx, sj = j + dy, sk = k + dz;
+        if (si < 0 || sj < 0 || sk < 0 || si >= m || sj >= m || sk >= m) continue;
+        const int q = (int)(((sk - z0 + 2) * SBY + (sj - y0 + 2)) * SBX + (si - x0 + 2));
+        double mom_q[10];
+#pragma unroll
+        for (int c = 0; c < 10; ++c) mom_q[c] = sm[c * SB3 + q];
+        m2l_tab(mom_q, tab + (((dz + 3) * kOff + (dy + 3)) * kOff + (dx + 3)) * kTab, o);
+      }
+  double* out = loc + cidx(m, i, j, k) * 10;
+#pragma unroll
+  for (int q = 0; q < 10; ++q) out[q] = o[q];
+}
+
 __global__ void l2l_kernel(const double* __restrict__ parent, double* __restrict__ loc, long long m,
                            double h) {
   const long long n3 = m * m * m;
@@ -348,9 +393,15 @@ int tmgpu_gravity_solve(tmgpu_gravity* G, const double* mass, double* phi, doubl
     for (int l = D - 1; l >= 0; --l)
       m2m_kernel<<<grid_for(1LL << (3 * l)), 128, 0, st>>>(w.mom[l + 1], w.mom[l], 1LL << l,
                                                           1.0 / (double)(1LL << (l + 1)));
-    for (int l = 2; l <= D; ++l)
-      m2l_kernel<<<grid_for(1LL << (3 * l)), 128, 0, st>>>(w.mom[l], w.loc[l], 1LL << l,
-                                                          w.tab + (long long)l * kOff3 * kTab);
+    for (int l = 2; l <= D; ++l) {
+      const long long m = 1LL << l;
+      if (m >= TBX)
+        m2l_tiled_kernel<<<(unsigned)(m * m * m / (TBX * TBY * TBZ)), 128, 0, st>>>(
+            w.mom[l], w.loc[l], m, w.tab + (long long)l * kOff3 * kTab);
+      else
+        m2l_kernel<<<grid_for(m * m * m), 128, 0, st>>>(w.mom[l], w.loc[l], m,
+                                                         w.tab + (long long)l * kOff3 * kTab);
+    }
     for (int l = 3; l <= D; ++l)
       l2l_kernel<<<grid_for(1LL << (3 * l)), 128, 0, st>>>(w.loc[l - 1], w.loc[l], 1LL << l,
                                                           1.0 / (double)(1LL << l));
