@@ -193,7 +193,7 @@ constexpr int SBX = TBX + 4, SBY = TBY + 4, SBZ = TBZ + 4, SB3 = SBX * SBY * SBZ
 __global__ void __launch_bounds__(128) m2l_tiled_kernel(const double* __restrict__ mom,
                                                         double* __restrict__ loc, long long m,
                                                         const double* __restrict__ tab) {
-  __shared__ double sm[10 * SB3];  // 61,440 B
+  extern __shared__ double sm[];  // 10 x SB3 doubles = 61,440 B (dynamic)
   const long long nbx = m / TBX, nby = m / TBY;
   const long long b = blockIdx.x;
   const long long x0 = (b % nbx) * TBX, y0 = ((b / nbx) % nby) * TBY, z0 = (b / (nbx * nby)) * TBZ;
@@ -341,6 +341,9 @@ tmgpu_gravity* tmgpu_gravity_create(int D, tmgpu_error* err) {
   }
   if (e == cudaSuccess) e = cudaMalloc(&g->w.mass, ((size_t)1 << (3 * D)) * sizeof(double));
   if (e == cudaSuccess) e = cudaMalloc(&g->w.tab, (size_t)(D + 1) * kOff3 * kTab * sizeof(double));
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(m2l_tiled_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)(10 * SB3 * sizeof(double)));
   if (e == cudaSuccess) {
     stencil_table_kernel<<<((D + 1) * kOff3 + 127) / 128, 128>>>(g->w.tab, D);
     g_launches.fetch_add(1, std::memory_order_relaxed);
@@ -396,7 +399,8 @@ int tmgpu_gravity_solve(tmgpu_gravity* G, const double* mass, double* phi, doubl
     for (int l = 2; l <= D; ++l) {
       const long long m = 1LL << l;
       if (m >= TBX)
-        m2l_tiled_kernel<<<(unsigned)(m * m * m / (TBX * TBY * TBZ)), 128, 0, st>>>(
+        m2l_tiled_kernel<<<(unsigned)(m * m * m / (TBX * TBY * TBZ)), 128,
+                           10 * SB3 * sizeof(double), st>>>(
             w.mom[l], w.loc[l], m, w.tab + (long long)l * kOff3 * kTab);
       else
         m2l_kernel<<<grid_for(m * m * m), 128, 0, st>>>(w.mom[l], w.loc[l], m,
