@@ -53,6 +53,15 @@ struct tmgpu_forest {
   int2* pull_fused = nullptr;
   double* slabs = nullptr;
   int n_pack = 0, n_pull_all = 0, n_pull_fused = 0;
+  // multi-GPU overlap: halo NCCL + remote pulls on a side stream while the
+  // interior leaves' stage runs; then the boundary leaves
+  int2* pull_local = nullptr;
+  int2* pull_remote = nullptr;
+  int* interior_idx = nullptr;
+  int* boundary_idx = nullptr;
+  int n_pull_local = 0, n_pull_remote = 0, n_interior = 0, n_boundary = 0;
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_packed = nullptr, ev_remote = nullptr;
   StageMaps maps[2]{};
   uint64_t exchanges = 0;  // ghost exchanges performed (structural counter)
   // optional per-phase device timing: events [start, cfl, (exch, stage) x 3]
@@ -91,8 +100,13 @@ void free_dev(tmgpu_forest* f) {
   for (void* p : {(void*)f->arenas[0], (void*)f->arenas[1], (void*)f->u0, (void*)f->xfer,
                   (void*)f->leaf_dx, (void*)f->speeds, (void*)f->diag, (void*)f->dt_dev,
                   (void*)f->err_dev, (void*)f->staged, (void*)f->pack, (void*)f->faces,
-                  (void*)f->face_src, (void*)f->pull_all, (void*)f->pull_fused, (void*)f->slabs})
+                  (void*)f->face_src, (void*)f->pull_all, (void*)f->pull_fused, (void*)f->slabs,
+                  (void*)f->pull_local, (void*)f->pull_remote, (void*)f->interior_idx,
+                  (void*)f->boundary_idx})
     fr(p);
+  f->pull_local = f->pull_remote = nullptr;
+  f->interior_idx = f->boundary_idx = nullptr;
+  f->n_pull_local = f->n_pull_remote = f->n_interior = f->n_boundary = 0;
   for (int a = 0; a < 3; ++a) {
     fr(f->fills[a]);
     fr(f->staged_of[a]);
@@ -181,6 +195,19 @@ int alloc_device(tmgpu_forest* f, tmgpu_error* err) {
   f->n_pack = (int)P.pack.size();
   f->n_pull_all = (int)P.pull_all.size() / 2;
   f->n_pull_fused = (int)P.pull_fused.size() / 2;
+  e = upload((int**)&f->pull_local, P.pull_fused_local, e);
+  e = upload((int**)&f->pull_remote, P.pull_fused_remote, e);
+  e = upload(&f->interior_idx, P.interior_slots, e);
+  e = upload(&f->boundary_idx, P.boundary_slots, e);
+  f->n_pull_local = (int)P.pull_fused_local.size() / 2;
+  f->n_pull_remote = (int)P.pull_fused_remote.size() / 2;
+  f->n_interior = (int)P.interior_slots.size();
+  f->n_boundary = (int)P.boundary_slots.size();
+  if (e == cudaSuccess && world > 1 && !f->side) {
+    e = cudaStreamCreateWithFlags(&f->side, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&f->ev_packed, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&f->ev_remote, cudaEventDisableTiming);
+  }
   if (world == 1) {  // reference-exact 3-pass plans (global slot == local slot)
     size_t max_prolong = 0;
     for (int a = 0; a < 3 && e == cudaSuccess; ++a) {
@@ -303,6 +330,9 @@ tmgpu_forest* tmgpu_forest_create(int edge, int ghost, int vars, int max_level,
 void tmgpu_forest_destroy(tmgpu_forest* f) {
   if (!f) return;
   free_dev(f);
+  if (f->side) cudaStreamDestroy(f->side);
+  if (f->ev_packed) cudaEventDestroy(f->ev_packed);
+  if (f->ev_remote) cudaEventDestroy(f->ev_remote);
   for (auto& e : f->ev)
     if (e) cudaEventDestroy(e);
   delete f;
@@ -544,9 +574,29 @@ int tmgpu_forest_step(tmgpu_forest* f, double dt, double cfl, double gamma, int 
   p.count = (int)f->nslots;
   const bool exact = (flags & TMGPU_EXACT_GHOSTS) != 0;
   p.face_src = exact ? nullptr : f->face_src;
+  const bool overlap = !exact && f->world() > 1;
   for (int stage = 1; stage <= 3 && e == cudaSuccess; ++stage) {
     std::string why;
-    if (int rc = exchange(f, st, exact ? kExact : kFused, &why)) return fail(err, rc, why);
+    if (overlap) {
+      // pack (all slabs) -> [side: NCCL halo, remote pulls] || [main: local pulls,
+      // interior leaves' stage] -> join -> boundary leaves' stage
+      e = halo_pack(f->arena(), f->arenas[f->cur ^ 1], V, f->pack, f->n_pack, f->slabs, st);
+      if (e == cudaSuccess) e = cudaEventRecord(f->ev_packed, st);
+      if (e == cudaSuccess) e = cudaStreamWaitEvent(f->side, f->ev_packed, 0);
+      if (e != cudaSuccess) break;
+      const HaloPlan& P = f->plan;
+      if (int rc = comm_exchange(f->comm, f->slabs + P.send_base, P.send_off, P.send_cnt,
+                                 f->slabs + P.recv_base, P.recv_off, P.recv_cnt, f->side, &why))
+        return fail(err, rc, why);
+      e = halo_pull(f->arena(), V, f->faces, f->pull_remote, f->n_pull_remote, f->slabs, f->side);
+      if (e == cudaSuccess) e = cudaEventRecord(f->ev_remote, f->side);
+      if (e == cudaSuccess)
+        e = halo_pull(f->arena(), V, f->faces, f->pull_local, f->n_pull_local, f->slabs, st);
+      if (e != cudaSuccess) break;
+      f->exchanges += 1;
+    } else if (int rc = exchange(f, st, exact ? kExact : kFused, &why)) {
+      return fail(err, rc, why);
+    }
     if (timed) cudaEventRecord(f->ev[2 * stage], st);
     p.rk_stage = stage;
     p.u0_save = stage == 1 ? f->u0 : nullptr;
@@ -554,7 +604,18 @@ int tmgpu_forest_step(tmgpu_forest* f, double dt, double cfl, double gamma, int 
     // exact: in place (each CTA reads only its own block); fused: ping-pong
     const int dst = exact ? f->cur : (f->cur ^ 1);
     p.out = f->arenas[dst];
-    e = launch_stage(V, (flags & TMGPU_FAST) != 0, f->maps[f->cur], p, st);
+    if (overlap) {
+      StageLaunch pi = p, pb = p;
+      pi.index = f->interior_idx;
+      pi.count = f->n_interior;
+      pb.index = f->boundary_idx;
+      pb.count = f->n_boundary;
+      e = launch_stage(V, (flags & TMGPU_FAST) != 0, f->maps[f->cur], pi, st);
+      if (e == cudaSuccess) e = cudaStreamWaitEvent(st, f->ev_remote, 0);
+      if (e == cudaSuccess) e = launch_stage(V, (flags & TMGPU_FAST) != 0, f->maps[f->cur], pb, st);
+    } else {
+      e = launch_stage(V, (flags & TMGPU_FAST) != 0, f->maps[f->cur], p, st);
+    }
     f->cur = dst;
     if (timed) cudaEventRecord(f->ev[2 * stage + 1], st);
   }

@@ -109,18 +109,27 @@ HaloPlan build_halo_plan(const Forest& f, const std::vector<int>& owner, int ran
     }
 
   P.face_src.assign((size_t)nl * 6, 0);
-  for (int l = 0; l < nl; ++l)
+  for (int l = 0; l < nl; ++l) {
+    bool boundary = false;
     for (int face = 0; face < 6; ++face) {
       const FaceSrc& fs = P.faces[(size_t)l * 6 + face];
       const bool local_same = fs.kind == (int8_t)NeighborKind::same && fs.src[0] >= 0;
+      bool remote = false;
+      for (int q = 0; q < 4; ++q) remote |= fs.src[q] < 0 && fs.off[q] >= P.recv_base;
       P.face_src[(size_t)l * 6 + face] = local_same ? ((fs.src[0] << 1) | 1) : (l << 1);
       P.pull_all.push_back(l);
       P.pull_all.push_back(face);
       if (!local_same) {
         P.pull_fused.push_back(l);
         P.pull_fused.push_back(face);
+        auto& v = remote ? P.pull_fused_remote : P.pull_fused_local;
+        v.push_back(l);
+        v.push_back(face);
       }
+      boundary |= remote;
     }
+    (boundary ? P.boundary_slots : P.interior_slots).push_back(l);
+  }
   return P;
 }
 

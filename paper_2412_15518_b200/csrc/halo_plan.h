@@ -20,6 +20,10 @@ struct HaloPlan {
   std::vector<int> face_src;           // [local slot][6] stage-kernel TMA source codes
   std::vector<int> pull_fused;         // pairs (slot, face): faces the fused step pulls
   std::vector<int> pull_all;           // pairs (slot, face): every face
+  // multi-GPU overlap: faces needing a received slab vs the rest, and the
+  // local leaves with (boundary) / without (interior) such a face
+  std::vector<int> pull_fused_local, pull_fused_remote;
+  std::vector<int> interior_slots, boundary_slots;
   long long local_doubles = 0;         // slab buffer: [local prolonged | send | recv]
   long long send_base = 0, recv_base = 0, total_doubles = 0;
   std::vector<long long> send_off, send_cnt, recv_off, recv_cnt;  // per peer, relative to base
