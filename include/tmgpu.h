@@ -42,6 +42,7 @@ typedef struct tmgpu_error {
 #define TMGPU_FAST 0x2       /* FMA/reciprocal arithmetic: parity within 1e-10 (scaled), not bitwise */
 #define TMGPU_ASYNC 0x4      /* enqueue only; errors latched until tmgpu_forest_check */
 #define TMGPU_EXACT_GHOSTS 0x8 /* step: reference 3-pass full-shell exchange instead of one-round faces */
+#define TMGPU_OVERLAP 0x10   /* multi-GPU step: overlap the NCCL halo with the interior leaves' stage */
 
 /* ---------------------------------------------------------------- hydro
  * Slice contract (reference stage.hpp:8-12, 39-66):

@@ -574,7 +574,9 @@ int tmgpu_forest_step(tmgpu_forest* f, double dt, double cfl, double gamma, int 
   p.count = (int)f->nslots;
   const bool exact = (flags & TMGPU_EXACT_GHOSTS) != 0;
   p.face_src = exact ? nullptr : f->face_src;
-  const bool overlap = !exact && f->world() > 1;
+  // opt-in: measured no faster on C3 at 2-4 GPUs (the split boundary launch
+  // under-fills the GPU), so the default keeps one exchange + one launch
+  const bool overlap = !exact && f->world() > 1 && (flags & TMGPU_OVERLAP);
   for (int stage = 1; stage <= 3 && e == cudaSuccess; ++stage) {
     std::string why;
     if (overlap) {
