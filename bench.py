@@ -39,8 +39,8 @@ ALG_BYTES_PER_CELL = 180.0     # stage kernel, device-resident: 1280 staged cell
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
-    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--fast", action="store_true", help="FMA/reciprocal kernels (1e-10 parity)")
     ap.add_argument("--min-level", type=int, default=2)
