@@ -245,6 +245,29 @@ class Oracle(_Lib):
         L.tmo_tree_plan.argtypes = [C.c_void_p, C.c_int, _i64p, C.c_size_t]
         L.tmo_fill_ghosts_sync.argtypes = [C.c_void_p, C.POINTER(_dp)]
         L.tmo_flag_refinement.argtypes = [C.c_void_p, _dp, C.c_double, C.c_double]
+        _lp = C.POINTER(C.c_long)
+        L.tmo_grav_amr_solve_ex.argtypes = [C.c_long, _ip, _dp, C.c_int, _dp, _dp, _lp]
+        L.tmo_grav_amr_direct.argtypes = [C.c_long, _ip, _dp, _dp, _dp]
+        L.tmo_grav_am_correct.argtypes = [C.c_long, _dp, _dp, _dp, _dp, _dp]
+
+    def grav_amr(self, leaves, mass, flags=0, direct=False):
+        """AMR FMM specification (gravity_amr_oracle.c). leaves: [n, 4] int
+        (level, I, J, K) in canonical order; mass: [n, 512]. Returns
+        (phi[n*512], g[3, n*512], (W/X entries, U-cross entries))."""
+        lv = np.ascontiguousarray(leaves, dtype=np.int32).reshape(-1, 4)
+        m = np.ascontiguousarray(mass, dtype=np.float64).reshape(-1)
+        n = lv.shape[0]
+        assert m.size == n * 512
+        phi, g = np.zeros(n * 512), np.zeros(3 * n * 512)
+        cnt = (C.c_long * 2)()
+        ip = lv.ctypes.data_as(_ip)
+        if direct:
+            r = self.lib.tmo_grav_amr_direct(n, ip, dptr(m), dptr(phi), dptr(g))
+        else:
+            r = self.lib.tmo_grav_amr_solve_ex(n, ip, dptr(m), flags, dptr(phi), dptr(g), cnt)
+        if r != 0:
+            raise ValueError(f"oracle AMR gravity failed ({r})")
+        return phi, g.reshape(3, -1), (cnt[0], cnt[1])
 
     def stage_fused(self, packed_in, count, edge=8, ghost=2, vars=5):
         S = edge + 2 * ghost
@@ -314,6 +337,31 @@ def pack(level, ci, cj, ck) -> int:
 def unpack(p: int):
     p = int(p)
     return p >> 60, (p >> 40) & 0xFFFFF, (p >> 20) & 0xFFFFF, p & 0xFFFFF
+
+
+def leaf_centres(leaves):
+    """Cell centres [n*512, 3] of leaves [n, 4] = (level, I, J, K), unit cube."""
+    lv = np.asarray(leaves, dtype=np.int64).reshape(-1, 4)
+    c = np.arange(512)
+    loc = np.stack([c & 7, (c >> 3) & 7, c >> 6], 1)
+    gl = lv[:, None, 1:] * 8 + loc[None]
+    h = 1.0 / (8.0 * (2.0 ** lv[:, 0]))
+    return ((gl + 0.5) * h[:, None, None]).reshape(-1, 3)
+
+
+def random_forest_leaves(rng, base=1, max_level=3, frac=0.3):
+    """Random (unbalanced) octree over the unit cube: uniform at `base`, then
+    each leaf below max_level refined with probability frac, repeatedly.
+    Returns [n, 4] (level, I, J, K) in canonical (Morton depth-first) order."""
+    def rec(level, i, j, k, out):
+        if level < base or (level < max_level and rng.random() < frac):
+            for c in range(8):
+                rec(level + 1, 2 * i + (c & 1), 2 * j + ((c >> 1) & 1), 2 * k + (c >> 2), out)
+        else:
+            out.append((level, i, j, k))
+    out = []
+    rec(0, 0, 0, 0, out)
+    return np.array(out, dtype=np.int32)
 
 
 def random_state(rng: np.random.Generator, edge=8, ghost=2, euler=True, gamma=1.4):

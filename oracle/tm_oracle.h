@@ -63,6 +63,15 @@ void tmo_grav_m2m(const double* ch, const double* s, double* out);
 void tmo_grav_l2l(const double* L, const double* s, double* out);
 int tmo_grav_solve(int D, const double* mass, double* phi, double* g);
 int tmo_grav_direct(int D, const double* mass, double* phi, double* g);
+/* AMR forest (gravity_amr_oracle.c): leaves [n][4] = (level, I, J, K), mass [n][512] */
+int tmo_grav_amr_solve(long nleaves, const int* leaves, const double* mass, int flags, double* phi,
+                       double* g);
+int tmo_grav_amr_solve_ex(long nleaves, const int* leaves, const double* mass, int flags,
+                          double* phi, double* g, long* counts);
+int tmo_grav_amr_direct(long nleaves, const int* leaves, const double* mass, double* phi, double* g);
+void tmo_grav_am_solve(const double* S, double* R, double* w);
+int tmo_grav_am_correct(long nleaves, const double* mass, const double* pos, double* g,
+                        double* S_out, double* w_out);
 
 #ifdef __cplusplus
 }
