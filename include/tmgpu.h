@@ -43,6 +43,7 @@ typedef struct tmgpu_error {
 #define TMGPU_ASYNC 0x4      /* enqueue only; errors latched until tmgpu_forest_check */
 #define TMGPU_EXACT_GHOSTS 0x8 /* step: reference 3-pass full-shell exchange instead of one-round faces */
 #define TMGPU_OVERLAP 0x10   /* multi-GPU step: overlap the NCCL halo with the interior leaves' stage */
+#define TMGPU_GRAV_AM 0x100  /* gravity: angular-momentum correction (rigid-rotation field) */
 
 /* ---------------------------------------------------------------- hydro
  * Slice contract (reference stage.hpp:8-12, 39-66):
@@ -200,6 +201,26 @@ int tmgpu_gravity_solve(tmgpu_gravity* G, const double* mass, double* phi, doubl
 int tmgpu_gravity_mass_from_arena(tmgpu_gravity* G, const double* arena, const int* leaf_ijk_dev,
                                   long long nleaves, int vars, double dV, void* stream,
                                   tmgpu_error* err);
+
+/* AMR forest (oracle/gravity_amr_oracle.c): adaptive FMM over the cell tree of
+ * the leaves (U, V, W, X lists). leaves: host [n][4] = (level, I, J, K) in
+ * canonical slot order, one root = the unit cube. mass: [n][512] ((k,j,i) per
+ * leaf) or NULL for the workspace masses (tmgpu_gravity_amr_mass_from_arena);
+ * outputs phi[n*512], g[3][n*512] by slot. flags: TMGPU_HOST_PTRS, TMGPU_ASYNC,
+ * TMGPU_GRAV_AM. info: [0] levels, [1] nodes, [2] W/X pairs, [3] U-cross pairs. */
+typedef struct tmgpu_gravity_amr tmgpu_gravity_amr;
+tmgpu_gravity_amr* tmgpu_gravity_amr_create(const int* leaves, long long nleaves, tmgpu_error* err);
+void tmgpu_gravity_amr_destroy(tmgpu_gravity_amr* G);
+int tmgpu_gravity_amr_info(const tmgpu_gravity_amr* G, long long* out);
+int tmgpu_gravity_amr_plan_info(const int* leaves, long long nleaves, long long* out,
+                                tmgpu_error* err); /* host only: plan validation + info */
+int tmgpu_gravity_amr_mass_from_arena(tmgpu_gravity_amr* G, const double* arena, int vars,
+                                      void* stream, tmgpu_error* err);
+int tmgpu_gravity_amr_solve(tmgpu_gravity_amr* G, const double* mass, double* phi, double* g,
+                            int flags, void* stream, tmgpu_error* err);
+int tmgpu_gravity_amr_am_stats(tmgpu_gravity_amr* G, double* out);
+const double* tmgpu_gravity_amr_mass_ptr(const tmgpu_gravity_amr* G);
+
 int tmgpu_selftest_fastmath(int mode, long long n, uint64_t seed, unsigned long long* mismatches,
                             unsigned long long* checked, double* first_bad, tmgpu_error* err);
 

@@ -1,0 +1,41 @@
+// Host plan of the AMR FMM (gravity_amr.cu): the cell tree of a forest laid
+// out as 8^3-cell patches per forest node, and the W/X (M2L) and cross-depth U
+// (P2P) pair lists of our adaptive specification (oracle/gravity_amr_oracle.c).
+// Pure C++ (no CUDA), testable on CPU.
+#pragma once
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+namespace tmgpu {
+
+constexpr int kGravMaxLevel = 15;  // cell depth <= 18; 19-bit global coordinates
+
+struct GravLevel {
+  int n = 0;                    // forest nodes at this level (Morton order)
+  std::vector<int> ijk;         // [n][3] node coordinates
+  std::vector<int> nbr;         // [n][27] same-level node, -1 if none ((dz,dy,dx)+1, x fastest)
+  std::vector<int> child;       // [n][8] child node at level+1 (octant x fastest), -1 for leaves
+  std::vector<int> parent;      // [n] node at level-1 (-1 at level 0)
+  std::vector<int> leaf_slot;   // [n] canonical leaf slot or -1
+  std::vector<int> internal;    // internal node indices
+  // pair lists over the level's cells (flat = node * 512 + (k*8+j)*8+i),
+  // CSR offsets [n*512 + 1]; entries (src_level << 40) | src_flat, sorted
+  // per target by source (depth, gk, gj, gi)
+  std::vector<int64_t> moff, ment;  // W/X: M2L terms into the cell's local expansion
+  std::vector<int64_t> poff, pent;  // cross-depth U: P2P terms (leaf cells only)
+};
+
+struct GravPlan {
+  int nlevels = 0;  // levels 0..nlevels-1
+  std::vector<GravLevel> lv;
+  std::vector<int> slot_level, slot_node;  // per canonical leaf slot
+  long long m_entries = 0, p_entries = 0;
+};
+
+// leaves: [n][4] (level, I, J, K) in canonical order, one root = unit cube.
+// Returns false (why set) unless the leaves tile the cube without overlap.
+bool build_grav_plan(const int* leaves, long long nleaves, GravPlan& plan, std::string* why);
+
+}  // namespace tmgpu

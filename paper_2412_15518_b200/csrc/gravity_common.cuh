@@ -1,0 +1,211 @@
+// Device helpers shared by the uniform (gravity.cu) and AMR (gravity_amr.cu)
+// FMM solvers: the operators of our gravity specification
+// (oracle/gravity_oracle.c), with its exact operation order (-fmad=false).
+#pragma once
+
+#include "tmgpu_internal.h"
+
+namespace tmgpu {
+namespace {
+
+__device__ __forceinline__ int s2(int i, int j) {
+  return (i == 0) ? j : (i == 1) ? (j == 0 ? 1 : 2 + j) : (j == 0 ? 2 : 3 + j);
+}
+
+// The stencil approach: on a uniform level R depends only on
+// the integer offset, so 1/r, D1 and D2 of each of the 7^3 offsets are
+// computed once per level (with m2l's exact operations) and the per-pair M2L
+// reduces to contractions. Table entry: [ir, d1[3], d2[3][3]] = 13 doubles.
+constexpr int kOff = 7, kOff3 = 343, kTab = 13;
+
+__global__ void stencil_table_kernel(double* __restrict__ tab, int D) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (D + 1) * kOff3) return;
+  const int l = t / kOff3, o = t % kOff3;
+  const int dx = o % kOff - 3, dy = (o / kOff) % kOff - 3, dz = o / (kOff * kOff) - 3;
+  double* e = tab + (long long)t * kTab;
+  if (dx == 0 && dy == 0 && dz == 0) {
+    for (int q = 0; q < kTab; ++q) e[q] = 0.0;
+    return;
+  }
+  const double h = 1.0 / (double)(1LL << l);
+  const double R[3] = {-(double)dx * h, -(double)dy * h, -(double)dz * h};
+  const double x = R[0], y = R[1], z = R[2];
+  const double r2 = x * x + y * y + z * z;
+  const double r = sqrt(r2);
+  const double ir = 1.0 / r;
+  const double ir2 = ir * ir;
+  const double ir3 = ir * ir2, ir5 = ir3 * ir2;
+  e[0] = ir;
+  for (int i = 0; i < 3; ++i) e[1 + i] = -R[i] * ir3;
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j) e[4 + 3 * i + j] = 3.0 * R[i] * R[j] * ir5 - (i == j ? ir3 : 0.0);
+}
+
+// m2l with the offset's precomputed geometry: identical arithmetic to m2l()
+__device__ __forceinline__ void m2l_tab(const double* __restrict__ mom,
+                                        const double* __restrict__ e, double out[10]) {
+  const double ir = e[0];
+  double d1[3], d2[3][3];
+#pragma unroll
+  for (int i = 0; i < 3; ++i) d1[i] = e[1 + i];
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int j = 0; j < 3; ++j) d2[i][j] = e[4 + 3 * i + j];
+  const double M = mom[0];
+  const double Dp[3] = {mom[1], mom[2], mom[3]};
+  double Q[3][3];
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int j = 0; j < 3; ++j) Q[i][j] = mom[4 + s2(i, j)];
+  double a = M * ir, b = 0.0, c = 0.0;
+#pragma unroll
+  for (int i = 0; i < 3; ++i) b += Dp[i] * d1[i];
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int j = 0; j < 3; ++j) c += Q[i][j] * d2[i][j];
+  out[0] += -(a - b + 0.5 * c);
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    double bb = 0.0;
+#pragma unroll
+    for (int j = 0; j < 3; ++j) bb += Dp[j] * d2[i][j];
+    out[1 + i] += -(M * d1[i] - bb);
+  }
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int j = i; j < 3; ++j) out[4 + s2(i, j)] += -(M * d2[i][j]);
+}
+
+__device__ __forceinline__ long long cidx(long long n, long long i, long long j, long long k) {
+  return (k * n + j) * n + i;
+}
+
+// m2l with the geometry computed from R, operation for operation as
+// tmo_grav_m2l (used for the AMR W/X list pairs, whose offsets are not on the
+// same-level stencil)
+__device__ __forceinline__ void m2l_direct(const double* __restrict__ mom, double x, double y,
+                                           double z, double out[10]) {
+  const double r2 = x * x + y * y + z * z;
+  const double r = sqrt(r2);
+  const double ir = 1.0 / r;
+  const double ir2 = ir * ir;
+  const double ir3 = ir * ir2, ir5 = ir3 * ir2;
+  const double R[3] = {x, y, z};
+  double e[kTab];
+  e[0] = ir;
+#pragma unroll
+  for (int i = 0; i < 3; ++i) e[1 + i] = -R[i] * ir3;
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int j = 0; j < 3; ++j) e[4 + 3 * i + j] = 3.0 * R[i] * R[j] * ir5 - (i == j ? ir3 : 0.0);
+  m2l_tab(mom, e, out);
+}
+
+__global__ void m2m_kernel(const double* __restrict__ child, double* __restrict__ parent, long long n,
+                           double hc) {
+  const long long n3 = n * n * n;
+  for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < n3;
+       p += (long long)gridDim.x * blockDim.x) {
+    const long long I = p % n, J = (p / n) % n, K = p / (n * n);
+    double o[10];
+#pragma unroll
+    for (int q = 0; q < 10; ++q) o[q] = 0.0;
+    for (int c = 0; c < 2; ++c)
+      for (int b = 0; b < 2; ++b)
+        for (int a = 0; a < 2; ++a) {
+          const double s[3] = {(a - 0.5) * hc, (b - 0.5) * hc, (c - 0.5) * hc};
+          const double* ch = child + cidx(2 * n, 2 * I + a, 2 * J + b, 2 * K + c) * 10;
+          const double M = ch[0];
+          o[0] += M;
+#pragma unroll
+          for (int i = 0; i < 3; ++i) o[1 + i] += ch[1 + i] + M * s[i];
+#pragma unroll
+          for (int i = 0; i < 3; ++i)
+#pragma unroll
+            for (int j = i; j < 3; ++j)
+              o[4 + s2(i, j)] += ch[4 + s2(i, j)] + ch[1 + i] * s[j] + s[i] * ch[1 + j] + M * s[i] * s[j];
+        }
+    double* out = parent + p * 10;
+#pragma unroll
+    for (int q = 0; q < 10; ++q) out[q] = o[q];
+  }
+}
+
+__global__ void __launch_bounds__(128) m2l_kernel(const double* __restrict__ mom,
+                                                  double* __restrict__ loc, long long m,
+                                                  const double* __restrict__ tab) {
+  const long long n3 = m * m * m;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < n3;
+       t += (long long)gridDim.x * blockDim.x) {
+    const long long i = t % m, j = (t / m) % m, k = t / (m * m);
+    double o[10];
+#pragma unroll
+    for (int q = 0; q < 10; ++q) o[q] = 0.0;
+    for (long long dz = -2 - (k & 1); dz <= 3 - (k & 1); ++dz)
+      for (long long dy = -2 - (j & 1); dy <= 3 - (j & 1); ++dy)
+        for (long long dx = -2 - (i & 1); dx <= 3 - (i & 1); ++dx) {
+          if (dx >= -1 && dx <= 1 && dy >= -1 && dy <= 1 && dz >= -1 && dz <= 1) continue;
+          const long long si = i + dx, sj = j + dy, sk = k + dz;
+          if (si < 0 || sj < 0 || sk < 0 || si >= m || sj >= m || sk >= m) continue;
+          m2l_tab(mom + cidx(m, si, sj, sk) * 10,
+                  tab + (((dz + 3) * kOff + (dy + 3)) * kOff + (dx + 3)) * kTab, o);
+        }
+    double* out = loc + t * 10;
+#pragma unroll
+    for (int q = 0; q < 10; ++q) out[q] = o[q];
+  }
+}
+
+__global__ void l2l_kernel(const double* __restrict__ parent, double* __restrict__ loc, long long m,
+                           double h) {
+  const long long n3 = m * m * m;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < n3;
+       t += (long long)gridDim.x * blockDim.x) {
+    const long long i = t % m, j = (t / m) % m, k = t / (m * m);
+    const double s[3] = {((i & 1) - 0.5) * h, ((j & 1) - 0.5) * h, ((k & 1) - 0.5) * h};
+    const double* L = parent + cidx(m / 2, i >> 1, j >> 1, k >> 1) * 10;
+    double Lm[3][3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+      for (int b = 0; b < 3; ++b) Lm[a][b] = L[4 + s2(a, b)];
+    double t1 = 0.0, t2 = 0.0;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) t1 += L[1 + a] * s[a];
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+      for (int b = 0; b < 3; ++b) t2 += Lm[a][b] * s[a] * s[b];
+    double sh[10];
+    sh[0] = L[0] + t1 + 0.5 * t2;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      double u = 0.0;
+#pragma unroll
+      for (int b = 0; b < 3; ++b) u += Lm[a][b] * s[b];
+      sh[1 + a] = L[1 + a] + u;
+    }
+#pragma unroll
+    for (int q = 0; q < 6; ++q) sh[4 + q] = L[4 + q];
+    double* out = loc + t * 10;
+#pragma unroll
+    for (int q = 0; q < 10; ++q) out[q] = sh[q] + out[q];
+  }
+}
+
+unsigned grid_for(long long n) {
+  long long b = (n + 127) / 128;
+  if (b < 1) b = 1;
+  if (b > 148 * 64) b = 148 * 64;
+  return (unsigned)b;
+}
+
+
+}  // namespace
+}  // namespace tmgpu

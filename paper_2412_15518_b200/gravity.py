@@ -90,3 +90,109 @@ class GravitySolver:
         _lib.check(lib.tmgpu_gravity_solve(self.h, None, phi.data_ptr(), g.data_ptr(),
                                            0 if sync else _lib.TMGPU_ASYNC, stream, C.byref(err)),
                    err)
+
+
+_lp = C.POINTER(C.c_longlong)
+lib.tmgpu_gravity_amr_create.restype = _vp
+lib.tmgpu_gravity_amr_create.argtypes = [_vp, C.c_longlong, _ep]
+lib.tmgpu_gravity_amr_destroy.restype = None
+lib.tmgpu_gravity_amr_destroy.argtypes = [_vp]
+lib.tmgpu_gravity_amr_info.restype = C.c_int
+lib.tmgpu_gravity_amr_info.argtypes = [_vp, _lp]
+lib.tmgpu_gravity_amr_plan_info.restype = C.c_int
+lib.tmgpu_gravity_amr_plan_info.argtypes = [_vp, C.c_longlong, _lp, _ep]
+lib.tmgpu_gravity_amr_mass_from_arena.restype = C.c_int
+lib.tmgpu_gravity_amr_mass_from_arena.argtypes = [_vp, _vp, C.c_int, _vp, _ep]
+lib.tmgpu_gravity_amr_solve.restype = C.c_int
+lib.tmgpu_gravity_amr_solve.argtypes = [_vp, _vp, _vp, _vp, C.c_int, _vp, _ep]
+lib.tmgpu_gravity_amr_am_stats.restype = C.c_int
+lib.tmgpu_gravity_amr_am_stats.argtypes = [_vp, C.POINTER(C.c_double)]
+lib.tmgpu_gravity_amr_mass_ptr.restype = _vp
+lib.tmgpu_gravity_amr_mass_ptr.argtypes = [_vp]
+
+GRAV_AM = 0x100
+
+
+def _leaf_array(leaves):
+    lv = np.ascontiguousarray(leaves, dtype=np.int32).reshape(-1, 4)
+    return lv
+
+
+def amr_plan_info(leaves):
+    """Host-only plan build: (levels, nodes, W/X pairs, U-cross pairs)."""
+    lv = _leaf_array(leaves)
+    out = (C.c_longlong * 4)()
+    err = TmgpuError()
+    _lib.check(lib.tmgpu_gravity_amr_plan_info(lv.ctypes.data, lv.shape[0], out, C.byref(err)), err)
+    return tuple(out)
+
+
+def forest_leaf_array(forest):
+    """[n, 4] (level, I, J, K) of a forest's local leaves in slot order."""
+    from .amr import unpack
+
+    return np.array([unpack(int(p)) for p in forest.local_leaves()], dtype=np.int32).reshape(-1, 4)
+
+
+class GravityAMR:
+    """Adaptive FMM over the cell tree of an octree forest (unit-cube root).
+
+    leaves: [n, 4] (level, I, J, K) in canonical slot order (forest_leaf_array).
+    Outputs are per leaf cell in slot order: phi[n*512], g[3, n*512]."""
+
+    def __init__(self, leaves):
+        self.leaves = _leaf_array(leaves)
+        self.n = self.leaves.shape[0]
+        err = TmgpuError()
+        self.h = lib.tmgpu_gravity_amr_create(self.leaves.ctypes.data, self.n, C.byref(err))
+        if not self.h:
+            _lib.check(err.code or _lib.TMGPU_ERR_CUDA, err)
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            lib.tmgpu_gravity_amr_destroy(self.h)
+            self.h = None
+
+    def info(self):
+        out = (C.c_longlong * 4)()
+        lib.tmgpu_gravity_amr_info(self.h, out)
+        return tuple(out)
+
+    def solve(self, mass=None, am=False, phi=None, g=None, stream=None, sync=True):
+        """mass: numpy [n, 512] (host path, returns numpy) or CUDA tensor / None
+        (device path: workspace masses when None; phi, g device tensors)."""
+        flags = GRAV_AM if am else 0
+        err = TmgpuError()
+        ncell = self.n * 512
+        if isinstance(mass, np.ndarray):
+            m = np.ascontiguousarray(mass, dtype=np.float64).reshape(-1)
+            if m.size != ncell:
+                raise ValueError("mass must have n*512 entries")
+            phi_h, g_h = np.zeros(ncell), np.zeros(3 * ncell)
+            _lib.check(lib.tmgpu_gravity_amr_solve(self.h, m.ctypes.data, phi_h.ctypes.data,
+                                                   g_h.ctypes.data, flags | _lib.TMGPU_HOST_PTRS,
+                                                   None, C.byref(err)), err)
+            return phi_h, g_h.reshape(3, -1)
+        import torch
+
+        dev = mass.device if mass is not None else (phi.device if phi is not None else torch.device("cuda"))
+        if phi is None:
+            phi = torch.empty(ncell, dtype=torch.float64, device=dev)
+        if g is None:
+            g = torch.empty(3 * ncell, dtype=torch.float64, device=dev)
+        st = stream if stream is not None else torch.cuda.current_stream(dev).cuda_stream
+        _lib.check(lib.tmgpu_gravity_amr_solve(self.h, None if mass is None else mass.data_ptr(),
+                                               phi.data_ptr(), g.data_ptr(),
+                                               flags | (0 if sync else _lib.TMGPU_ASYNC), st,
+                                               C.byref(err)), err)
+        return phi, g.view(3, -1)
+
+    def mass_from_arena(self, forest, stream=None):
+        err = TmgpuError()
+        _lib.check(lib.tmgpu_gravity_amr_mass_from_arena(self.h, forest.arena_ptr(), forest.vars,
+                                                         stream, C.byref(err)), err)
+
+    def am_stats(self):
+        out = (C.c_double * 22)()
+        lib.tmgpu_gravity_amr_am_stats(self.h, out)
+        return np.array(out)

@@ -139,3 +139,26 @@ def test_am_correct_restated_in_numpy():
     w_np = np.linalg.solve(J, -tau)
     assert np.allclose(w, w_np, rtol=1e-10, atol=1e-14 * np.abs(w_np).max())
     assert np.allclose(g2, g + np.cross(w_np, r).T, rtol=1e-10, atol=1e-12)
+
+
+@pytest.mark.parametrize("seed", [0, 1, 4])
+def test_product_plan_pairs_match_spec(seed):
+    """The product's host plan (csrc/gravity_amr_plan.cpp) generates exactly
+    the specification's W/X and cross-depth U pair counts."""
+    from paper_2412_15518_b200 import gravity as G
+
+    o = O.Oracle()
+    lv = O.random_forest_leaves(np.random.default_rng(seed), base=1, max_level=3, frac=0.3)
+    _, _, cnt = o.grav_amr(lv, np.ones((lv.shape[0], 512)), flags=2)
+    info = G.amr_plan_info(lv)
+    assert (info[2], info[3]) == cnt
+    assert info[0] == lv[:, 0].max() + 1
+
+
+def test_product_plan_rejects_bad_leaves():
+    from paper_2412_15518_b200 import gravity as G
+    lv = uniform_leaves(1)
+    with pytest.raises(ValueError, match="tile"):
+        G.amr_plan_info(lv[:-1])
+    with pytest.raises(ValueError, match="overlap"):
+        G.amr_plan_info(np.concatenate([lv, [[0, 0, 0, 0]]]))
