@@ -150,6 +150,10 @@ int tmgpu_forest_fill_faces(tmgpu_forest* f, void* stream, tmgpu_error* err);
 int tmgpu_forest_max_wavespeed(tmgpu_forest* f, double gamma, double* per_leaf_host, tmgpu_error* err);
 /* SSP-RK3 step (rk3.hpp): 3 x (fill_ghosts_sync -> aggregated
  * stage over all leaves -> rk3_combine); cfl > 0 computes dt on the device */
+/* gravity source in the stage (our spec): g device [3][comp_stride] by
+ * local slot; NULL = pure hydro (the reference's stage) */
+int tmgpu_forest_set_gravity(tmgpu_forest* f, const double* g, long long comp_stride,
+                             tmgpu_error* err);
 int tmgpu_forest_step(tmgpu_forest* f, double dt, double cfl, double gamma, int flags,
                       void* stream, double* dt_used, tmgpu_error* err);
 int tmgpu_forest_check(tmgpu_forest* f, void* stream, tmgpu_error* err);

@@ -245,6 +245,7 @@ class Oracle(_Lib):
         L.tmo_tree_plan.argtypes = [C.c_void_p, C.c_int, _i64p, C.c_size_t]
         L.tmo_fill_ghosts_sync.argtypes = [C.c_void_p, C.POINTER(_dp)]
         L.tmo_flag_refinement.argtypes = [C.c_void_p, _dp, C.c_double, C.c_double]
+        L.tmo_stage_subgrid_grav.argtypes = [_dp, C.c_int, C.c_int, C.c_int, _dp, _dp, _dp, _ip]
         _lp = C.POINTER(C.c_long)
         L.tmo_grav_amr_solve_ex.argtypes = [C.c_long, _ip, _dp, C.c_int, _dp, _dp, _lp]
         L.tmo_grav_amr_direct.argtypes = [C.c_long, _ip, _dp, _dp, _dp]

@@ -85,8 +85,12 @@ void tmo_rusanov_euler(const double* ql, const double* qr, double gamma, int axi
 }
 
 /* ------------------------------------------------------------ stage */
-/* stage.cpp:93-218 at lane width 1 (output is W-invariant, stage.hpp:69). */
-int tmo_stage_subgrid(const double* h, int E, int G, int V, const double* in,
+/* stage.cpp:93-218 at lane width 1 (output is W-invariant, stage.hpp:69).
+ * grav (OUR extension, not in the reference): optional [3][E^3]
+ * gravitational acceleration; after the z update and before the floors,
+ * m_q += dt*(rho*g_q) and E += dt*(rho*((u*gx + v*gy) + w*gz)) with the stage
+ * input's primitives (density floored as in cons -> prim). */
+static int stage_impl(const double* h, int E, int G, int V, const double* in, const double* grav,
                       double* out, int* bad_cell) {
   const int S = E + 2 * G;
   const size_t s2 = (size_t)S * S, s3 = s2 * S;
@@ -175,6 +179,21 @@ int tmo_stage_subgrid(const double* h, int E, int G, int V, const double* in,
   free(cons);
   free(prim);
   free(flux);
+  if (grav && euler && V == 5) {
+    for (int k = 0; k < E; ++k)
+      for (int j = 0; j < E; ++j)
+        for (int i = 0; i < E; ++i) {
+          const size_t c = ((size_t)k * E + j) * E + i;
+          const size_t q = (size_t)(k + G) * s2 + (size_t)(j + G) * S + (i + G);
+          const double rho = stdmax_(in[q], RHO_FLOOR);
+          const double iu = in[s3 + q] / rho, iv = in[2 * s3 + q] / rho, iw = in[3 * s3 + q] / rho;
+          const double gx = grav[c], gy = grav[e3 + c], gz = grav[2 * e3 + c];
+          out[e3 + c] = out[e3 + c] + dt * (rho * gx);
+          out[2 * e3 + c] = out[2 * e3 + c] + dt * (rho * gy);
+          out[3 * e3 + c] = out[3 * e3 + c] + dt * (rho * gz);
+          out[4 * e3 + c] = out[4 * e3 + c] + dt * (rho * ((iu * gx + iv * gy) + iw * gz));
+        }
+  }
   /* stage.cpp:187-208 floors */
   double floor_hits = 0.0;
   if (euler) {
@@ -207,6 +226,16 @@ int tmo_stage_subgrid(const double* h, int E, int G, int V, const double* in,
     }
   out[interior + 6 * face_elems] = floor_hits;
   return 0;
+}
+
+int tmo_stage_subgrid(const double* h, int E, int G, int V, const double* in, double* out,
+                      int* bad_cell) {
+  return stage_impl(h, E, G, V, in, NULL, out, bad_cell);
+}
+
+int tmo_stage_subgrid_grav(const double* h, int E, int G, int V, const double* in,
+                           const double* grav, double* out, int* bad_cell) {
+  return stage_impl(h, E, G, V, in, grav, out, bad_cell);
 }
 
 /* stage.cpp:229-246 make_stage_kernel's fused body */

@@ -28,6 +28,8 @@ double tmo_rusanov_scalar(double a, double l, double r);
 int tmo_stage_subgrid(const double* header8, int edge, int ghost, int vars,
                       const double* in, double* out, int* bad_cell);
 /* returns 0 ok, else 1 + index of the first failing slice in *bad_slice */
+int tmo_stage_subgrid_grav(const double* h, int E, int G, int V, const double* in,
+                           const double* grav, double* out, int* bad_cell);
 int tmo_stage_fused(const double* in, double* out, size_t in_slice, size_t out_slice,
                     size_t count, int edge, int ghost, int vars, size_t* bad_slice,
                     int* bad_cell);

@@ -38,6 +38,8 @@ struct tmgpu_forest {
   double* speeds = nullptr;   // [slot]
   double* diag = nullptr;     // [slot] floor hits of the last stage
   double* dt_dev = nullptr;   // [1]
+  const double* grav = nullptr;  // optional gravity g[3][stride] by local slot (device)
+  long long grav_stride = 0;
   unsigned long long* err_dev = nullptr;
   // reference-exact 3-pass exchange (single GPU only)
   double* staged = nullptr;
@@ -532,6 +534,19 @@ int tmgpu_forest_max_wavespeed(tmgpu_forest* f, double gamma, double* per_leaf_h
 // the rk3_combine epilogue). cfl > 0: dt = cfl * min(dx / max_wavespeed)
 // computed on the device; else `dt` is used. With TMGPU_ASYNC the call only
 // enqueues; tmgpu_forest_check reports errors later.
+// Gravity source for subsequent steps: g = device [3][comp_stride] by local
+// slot (g[q*comp_stride + slot*512 + c]), e.g. tmgpu_gravity_amr_solve's
+// output; NULL disables (pure hydro = the reference's stage).
+int tmgpu_forest_set_gravity(tmgpu_forest* f, const double* g, long long comp_stride,
+                             tmgpu_error* err) {
+  if (err) std::memset(err, 0, sizeof(*err));
+  if (g && comp_stride < f->nslots * 512)
+    return set_err(err, TMGPU_ERR_INVALID, "gravity: component stride below the local cell count");
+  f->grav = g;
+  f->grav_stride = comp_stride;
+  return TMGPU_OK;
+}
+
 int tmgpu_forest_step(tmgpu_forest* f, double dt, double cfl, double gamma, int flags, void* stream,
                       double* dt_used, tmgpu_error* err) {
   if (err) std::memset(err, 0, sizeof(*err));
@@ -571,6 +586,8 @@ int tmgpu_forest_step(tmgpu_forest* f, double dt, double cfl, double gamma, int 
   p.u0 = f->u0;
   p.u0_stride = (long long)V * 512;
   p.err = f->err_dev;
+  p.grav = f->grav;
+  p.grav_stride = f->grav_stride;
   p.count = (int)f->nslots;
   const bool exact = (flags & TMGPU_EXACT_GHOSTS) != 0;
   p.face_src = exact ? nullptr : f->face_src;

@@ -535,6 +535,16 @@ __global__ void __launch_bounds__(kStageThreads, 2)
 #pragma unroll
     for (int v = 0; v < V; ++v) u[v] = acc[v * kE3 + c];
     if constexpr (V == 5) {
+      if (euler && p.grav) {  // gravity source with the stage input's primitives
+        const double* pq = sm + L::B0 + (c >> 3) * 10 + (c & 7);
+        const double rho = pq[0], iu = pq[640], iv = pq[1280], iw = pq[1920];
+        const double* gq = p.grav + (long long)slot * kE3 + c;
+        const double gx = gq[0], gy = gq[p.grav_stride], gz = gq[2 * p.grav_stride];
+        u[1] = u[1] + dt * (rho * gx);
+        u[2] = u[2] + dt * (rho * gy);
+        u[3] = u[3] + dt * (rho * gz);
+        u[4] = u[4] + dt * (rho * ((iu * gx + iv * gy) + iw * gz));
+      }
       if (euler) {  // stage.cpp:187-208
         if (u[0] < kRhoFloor) {
           u[0] = kRhoFloor;

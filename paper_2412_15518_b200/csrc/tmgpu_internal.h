@@ -42,6 +42,12 @@ struct StageLaunch {
   // the leaf's own ghost layers, (nbr << 1) | 1 the same-level neighbour's
   // adjacent interior layers. nullptr: own ghosts everywhere.
   const int* face_src;
+  // optional gravity source (our spec; not in the reference):
+  // g[q*grav_stride + slot*512 + c]; after the z update, before the floors:
+  // m_q += dt*(rho*g_q), E += dt*(rho*((u*gx + v*gy) + w*gz)) with the stage
+  // input's primitives (oracle tmo_stage_subgrid_grav)
+  const double* grav;
+  long long grav_stride;
   unsigned long long* err;  // atomicMin of (slice << 32 | var-major interior index)
   int count;
 };

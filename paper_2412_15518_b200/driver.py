@@ -43,3 +43,45 @@ class HydroDriver:
     def check(self, stream=None) -> None:
         err = TmgpuError()
         _lib.check(lib.tmgpu_forest_check(self.forest.h, stream, C.byref(err)), err, SolverError)
+
+
+lib.tmgpu_forest_set_gravity.restype = C.c_int
+lib.tmgpu_forest_set_gravity.argtypes = [C.c_void_p, C.c_void_p, C.c_longlong, C.POINTER(TmgpuError)]
+
+
+class GravityHydroDriver(HydroDriver):
+    """The gravity + hydro step of the metric (BASELINE.json): per step one AMR
+    FMM solve (paper_2412_15518_b200.gravity.GravityAMR, our specification —
+    the reference has no gravity) on the step's initial state, with
+    the angular-momentum correction, held fixed over the three RK stages as the
+    stage kernel's source term (m += dt*rho*g, E += dt*rho*(v.g); oracle
+    tmo_stage_subgrid_grav)."""
+
+    def __init__(self, forest: Forest, gamma: float = 1.4, cfl: float = 0.4, fast: bool = False,
+                 exact_ghosts: bool = False, am: bool = True):
+        super().__init__(forest, gamma, cfl, fast, exact_ghosts)
+        import torch
+
+        from .gravity import GravityAMR, forest_leaf_array
+
+        if forest.local_count() != forest.leaf_count():
+            raise NotImplementedError("gravity on a distributed forest: use DistGravityHydroDriver")
+        self.am = am
+        self.gravity = GravityAMR(forest_leaf_array(forest))
+        n = forest.local_count() * 512
+        self.phi = torch.empty(n, dtype=torch.float64, device="cuda")
+        self.g = torch.zeros(3 * n, dtype=torch.float64, device="cuda")
+        err = TmgpuError()
+        _lib.check(lib.tmgpu_forest_set_gravity(forest.h, self.g.data_ptr(), n, C.byref(err)), err)
+
+    def solve_gravity(self, stream=None) -> None:
+        self.gravity.mass_from_arena(self.forest, stream)
+        self.gravity.solve(None, am=self.am, phi=self.phi, g=self.g, stream=stream, sync=False)
+
+    def step(self, dt: float | None = None, stream=None, sync: bool = True) -> float | None:
+        self.solve_gravity(stream)
+        return super().step(dt, stream, sync)
+
+    def close(self) -> None:
+        err = TmgpuError()
+        lib.tmgpu_forest_set_gravity(self.forest.h, None, 0, C.byref(err))
