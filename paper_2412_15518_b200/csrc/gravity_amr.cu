@@ -117,42 +117,60 @@ __global__ void amr_m2m_kernel(const GLv* __restrict__ L, int l, const int* __re
   }
 }
 
-// M2L of one level: CTA = (patch, 8x4x4 target tile); source window 12x8x8
-// cells [x0-2, x0+9] x [y0-2, y0+5] x [z0-2, z0+5] of the 27-patch
-// neighbourhood, SoA by component in shared memory (61,440 B).
-constexpr int ATX = 8, ATY = 4, ATZ = 4;
-constexpr int AWX = ATX + 4, AWY = ATY + 4, AWZ = ATZ + 4, AW3 = AWX * AWY * AWZ;
+// M2L of one level: CTA = (patch, z-half of 8x8x4 targets), 256 threads.
+// Warp w owns the 32 targets of one parity class (a, b, c) = (w&1, w>>1&1,
+// w>>2): lane (I, J, K) -> target (2I+a, 2J+b, z0+2K+c). Every lane of a warp
+// then walks the same stencil offsets (no divergence; the tabulated geometry
+// is a warp-uniform broadcast load). The 12x12x8 source window (27-patch
+// neighbourhood, missing patches = zero moments) is stored de-interleaved by
+// parity: 8 sub-grids of 6x6x4 cells with row pitch 6 and plane pitch 40, so a
+// warp's 32 source loads of any offset hit 32 distinct banks (2 wavefronts).
+constexpr int kSubPitchY = 6, kSubPitchZ = 40, kSub = 4 * kSubPitchZ, kWin = 8 * kSub;  // 1280
 
-__global__ void __launch_bounds__(128) amr_m2l_kernel(const GLv* __restrict__ Lv, int l,
-                                                      const double* __restrict__ tab) {
-  extern __shared__ double sm[];
+__device__ __forceinline__ int win_index(int wx, int wy, int wz) {
+  return ((((wz & 1) * 2 + (wy & 1)) * 2 + (wx & 1)) * kSub) + (wz >> 1) * kSubPitchZ +
+         (wy >> 1) * kSubPitchY + (wx >> 1);
+}
+
+__global__ void __launch_bounds__(256, 2) amr_m2l_kernel(const GLv* __restrict__ Lv, int l,
+                                                         const double* __restrict__ tab) {
+  extern __shared__ double sm[];  // [10][kWin] doubles = 102,400 B
   const GLv L = Lv[l];
-  const int n = blockIdx.x >> 2;
-  const int y0 = (blockIdx.x & 1) * ATY, z0 = ((blockIdx.x >> 1) & 1) * ATZ;
+  const int n = blockIdx.x >> 1;
+  const int z0 = (blockIdx.x & 1) * 4;
   const int* nb27 = L.nbr + (long long)n * 27;
-  for (int q = threadIdx.x; q < AW3; q += blockDim.x) {
-    int lx = -2 + q % AWX, ly = y0 - 2 + (q / AWX) % AWY, lz = z0 - 2 + q / (AWX * AWY);
+  for (int q = threadIdx.x; q < 12 * 12 * 8; q += blockDim.x) {
+    const int wx = q % 12, wy = (q / 12) % 12, wz = q / 144;
+    int lx = wx - 2, ly = wy - 2, lz = z0 + wz - 2;
     const int ox = lx < 0 ? -1 : (lx > 7 ? 1 : 0), oy = ly < 0 ? -1 : (ly > 7 ? 1 : 0),
               oz = lz < 0 ? -1 : (lz > 7 ? 1 : 0);
     lx -= 8 * ox, ly -= 8 * oy, lz -= 8 * oz;
     const int nb = nb27[((oz + 1) * 3 + (oy + 1)) * 3 + ox + 1];
     const double* src = L.mom + ((long long)(nb < 0 ? 0 : nb) * 512 + (lz * 8 + ly) * 8 + lx) * 10;
+    const int w = win_index(wx, wy, wz);
 #pragma unroll
-    for (int c = 0; c < 10; ++c) sm[c * AW3 + q] = nb >= 0 ? src[c] : 0.0;
+    for (int c = 0; c < 10; ++c) sm[c * kWin + w] = nb >= 0 ? src[c] : 0.0;
   }
   __syncthreads();
-  const int i = threadIdx.x % ATX, j = y0 + (threadIdx.x / ATX) % ATY, k = z0 + threadIdx.x / (ATX * ATY);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int a = warp & 1, b = (warp >> 1) & 1, c = warp >> 2;
+  const int I = lane & 3, J = (lane >> 2) & 3, K = lane >> 4;
+  const int i = 2 * I + a, j = 2 * J + b, k = z0 + 2 * K + c;
+  const int lane_off = K * kSubPitchZ + J * kSubPitchY + I;
   double o[10];
 #pragma unroll
   for (int q = 0; q < 10; ++q) o[q] = 0.0;
-  for (int dz = -2 - (k & 1); dz <= 3 - (k & 1); ++dz)
-    for (int dy = -2 - (j & 1); dy <= 3 - (j & 1); ++dy)
-      for (int dx = -2 - (i & 1); dx <= 3 - (i & 1); ++dx) {
+  for (int dz = -2 - c; dz <= 3 - c; ++dz)
+    for (int dy = -2 - b; dy <= 3 - b; ++dy)
+      for (int dx = -2 - a; dx <= 3 - a; ++dx) {
         if (dx >= -1 && dx <= 1 && dy >= -1 && dy <= 1 && dz >= -1 && dz <= 1) continue;
-        const int q = ((k + dz - z0 + 2) * AWY + (j + dy - y0 + 2)) * AWX + (i + dx + 2);
+        // window coordinates of the source: (t + d) + 2 (z relative to z0)
+        const int sx = a + dx + 2, sy = b + dy + 2, sz = c + dz + 2;  // + 2*(I, J, K)
+        const int q = ((((sz & 1) * 2 + (sy & 1)) * 2 + (sx & 1)) * kSub) + (sz >> 1) * kSubPitchZ +
+                      (sy >> 1) * kSubPitchY + (sx >> 1) + lane_off;
         double mom_q[10];
 #pragma unroll
-        for (int c = 0; c < 10; ++c) mom_q[c] = sm[c * AW3 + q];
+        for (int cc = 0; cc < 10; ++cc) mom_q[cc] = sm[cc * kWin + q];
         m2l_tab(mom_q, tab + (((dz + 3) * kOff + (dy + 3)) * kOff + (dx + 3)) * kTab, o);
       }
   const long long flat = (long long)n * 512 + (k * 8 + j) * 8 + i;
@@ -358,18 +376,30 @@ __global__ void __launch_bounds__(512) am_slot_kernel(const GLv* __restrict__ Lv
   }
 }
 
-// one CTA: adjacent-pair tree over the (zero-padded, power-of-two) slot sums,
-// then the 3x3 solve of tmo_grav_am_solve -> rw = (R[3], w[3])
-__global__ void __launch_bounds__(1024) am_tree_kernel(double* __restrict__ part, long long P,
-                                                       double* __restrict__ rw) {
-  for (long long st = 1; st < P; st <<= 1) {
-    for (long long a = threadIdx.x; a < P / (2 * st); a += blockDim.x) {
-      const long long c = a * 2 * st;
+// adjacent-pair tree over n (power of two) entries of 16 sums: each CTA
+// reduces a chunk of min(n, 256) consecutive entries (the first levels of the
+// global tree) into out[blockIdx.x]
+__global__ void __launch_bounds__(256) am_tree_pass_kernel(const double* __restrict__ in,
+                                                           double* __restrict__ out, long long n) {
+  __shared__ double v[256][17];
+  const int chunk = n < 256 ? (int)n : 256;
+  const long long base = (long long)blockIdx.x * chunk;
+  const int t = threadIdx.x;
+  if (t < chunk)
 #pragma unroll
-      for (int q = 0; q < 16; ++q) part[c * 16 + q] = part[c * 16 + q] + part[(c + st) * 16 + q];
-    }
+    for (int q = 0; q < 16; ++q) v[t][q] = in[(base + t) * 16 + q];
+  __syncthreads();
+  for (int st = 1; st < chunk; st <<= 1) {
+    if (t < chunk && (t & (2 * st - 1)) == 0)
+#pragma unroll
+      for (int q = 0; q < 16; ++q) v[t][q] = v[t][q] + v[t + st][q];
     __syncthreads();
   }
+  if (t < 16) out[(long long)blockIdx.x * 16 + t] = v[0][t];
+}
+
+// the 3x3 solve of tmo_grav_am_solve on the total sums S -> rw = (R, w, S)
+__global__ void am_solve_kernel(const double* __restrict__ part, double* __restrict__ rw) {
   if (threadIdx.x != 0) return;
   const double* S = part;
   double R[3], w[3];
@@ -440,7 +470,8 @@ struct GravAmrWork {
   double* dloc[3] = {nullptr, nullptr, nullptr};
   double* tab = nullptr;
   double* mass = nullptr;
-  double* part = nullptr;  // [P][16] + rw[22]
+  double* part = nullptr;   // [P][16] + rw[22]
+  double* part2 = nullptr;  // [P/256 + 1][16] tree scratch
   long long nslots = 0, P = 1;
   long long nodes = 0;
 };
@@ -525,9 +556,10 @@ tmgpu_gravity_amr* tmgpu_gravity_amr_create(const int* leaves, long long nleaves
   if (e == cudaSuccess) e = cudaMalloc(&w.tab, (size_t)(Dmax + 1) * kOff3 * kTab * sizeof(double)), track(w.tab);
   if (e == cudaSuccess) e = cudaMalloc(&w.mass, (size_t)w.nslots * 512 * sizeof(double)), track(w.mass);
   if (e == cudaSuccess) e = cudaMalloc(&w.part, ((size_t)w.P * 16 + 22) * sizeof(double)), track(w.part);
+  if (e == cudaSuccess) e = cudaMalloc(&w.part2, ((size_t)w.P / 256 + 1) * 16 * sizeof(double)), track(w.part2);
   if (e == cudaSuccess)
     e = cudaFuncSetAttribute(amr_m2l_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)(10 * AW3 * sizeof(double)));
+                             (int)(10 * kWin * sizeof(double)));
   if (e == cudaSuccess) {
     stencil_table_kernel<<<((Dmax + 1) * kOff3 + 127) / 128, 128>>>(w.tab, Dmax);
     g_launches.fetch_add(1, std::memory_order_relaxed);
@@ -609,7 +641,7 @@ int tmgpu_gravity_amr_solve(tmgpu_gravity_amr* G, const double* mass, double* ph
     m2l_kernel<<<1, 128, 0, st>>>(w.dmom[2], w.dloc[2], 4, w.tab + 2LL * kOff3 * kTab);
     launches += 4;
     for (int l = 0; l < P.nlevels; ++l) {
-      amr_m2l_kernel<<<(unsigned)(P.lv[l].n * 4), 128, 10 * AW3 * sizeof(double), st>>>(
+      amr_m2l_kernel<<<(unsigned)(P.lv[l].n * 2), 256, 10 * kWin * sizeof(double), st>>>(
           w.dev_lv, l, w.tab + (long long)(l + 3) * kOff3 * kTab);
       ++launches;
     }
@@ -626,7 +658,16 @@ int tmgpu_gravity_amr_solve(tmgpu_gravity_amr* G, const double* mass, double* ph
       e = cudaMemsetAsync(w.part, 0, (size_t)w.P * 16 * sizeof(double), st);
       am_slot_kernel<<<(unsigned)w.nslots, 512, 0, st>>>(w.dev_lv, w.nslots, w.slot_level, w.slot_node,
                                                          w.mass, dg, w.part);
-      am_tree_kernel<<<1, 1024, 0, st>>>(w.part, w.P, w.part + w.P * 16);
+      double* bufs[2] = {w.part, w.part2};
+      int cur = 0;
+      for (long long n = w.P; n > 1;) {
+        const long long chunk = n < 256 ? n : 256;
+        am_tree_pass_kernel<<<(unsigned)(n / chunk), 256, 0, st>>>(bufs[cur], bufs[cur ^ 1], n);
+        n /= chunk;
+        cur ^= 1;
+        ++launches;
+      }
+      am_solve_kernel<<<1, 32, 0, st>>>(bufs[cur], w.part + w.P * 16);
       am_apply_kernel<<<grid_for(ncell), 128, 0, st>>>(w.dev_lv, w.nslots, w.slot_level, w.slot_node,
                                                        w.part + w.P * 16, dg);
       launches += 3;
