@@ -154,7 +154,9 @@ __global__ void __launch_bounds__(256, 2) amr_m2l_kernel(const GLv* __restrict__
   __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int a = warp & 1, b = (warp >> 1) & 1, c = warp >> 2;
-  const int I = lane & 3, J = (lane >> 2) & 3, K = lane >> 4;
+  // half-warps take J even / J odd: with the (6, 40) sub-grid pitches every
+  // half-warp's 16 doubles then fall in 16 distinct banks for every offset
+  const int I = lane & 3, K = (lane >> 2) & 1, J = ((lane >> 3) & 1) * 2 + (lane >> 4);
   const int i = 2 * I + a, j = 2 * J + b, k = z0 + 2 * K + c;
   const int lane_off = K * kSubPitchZ + J * kSubPitchY + I;
   double o[10];
@@ -171,7 +173,7 @@ __global__ void __launch_bounds__(256, 2) amr_m2l_kernel(const GLv* __restrict__
         double mom_q[10];
 #pragma unroll
         for (int cc = 0; cc < 10; ++cc) mom_q[cc] = sm[cc * kWin + q];
-        m2l_tab(mom_q, tab + (((dz + 3) * kOff + (dy + 3)) * kOff + (dx + 3)) * kTab, o);
+        m2l_tab10(mom_q, tab + (((dz + 3) * kOff + (dy + 3)) * kOff + (dx + 3)) * kTab10, o);
       }
   const long long flat = (long long)n * 512 + (k * 8 + j) * 8 + i;
   const long long e0 = L.moff[flat], e1 = L.moff[flat + 1];
@@ -469,6 +471,7 @@ struct GravAmrWork {
   double* dmom[3] = {nullptr, nullptr, nullptr};
   double* dloc[3] = {nullptr, nullptr, nullptr};
   double* tab = nullptr;
+  double* tab10 = nullptr;
   double* mass = nullptr;
   double* part = nullptr;   // [P][16] + rw[22]
   double* part2 = nullptr;  // [P/256 + 1][16] tree scratch
@@ -554,6 +557,7 @@ tmgpu_gravity_amr* tmgpu_gravity_amr_create(const int* leaves, long long nleaves
   }
   const int Dmax = P.nlevels - 1 + 3;
   if (e == cudaSuccess) e = cudaMalloc(&w.tab, (size_t)(Dmax + 1) * kOff3 * kTab * sizeof(double)), track(w.tab);
+  if (e == cudaSuccess) e = cudaMalloc(&w.tab10, (size_t)(Dmax + 1) * kOff3 * kTab10 * sizeof(double)), track(w.tab10);
   if (e == cudaSuccess) e = cudaMalloc(&w.mass, (size_t)w.nslots * 512 * sizeof(double)), track(w.mass);
   if (e == cudaSuccess) e = cudaMalloc(&w.part, ((size_t)w.P * 16 + 22) * sizeof(double)), track(w.part);
   if (e == cudaSuccess) e = cudaMalloc(&w.part2, ((size_t)w.P / 256 + 1) * 16 * sizeof(double)), track(w.part2);
@@ -562,7 +566,8 @@ tmgpu_gravity_amr* tmgpu_gravity_amr_create(const int* leaves, long long nleaves
                              (int)(10 * kWin * sizeof(double)));
   if (e == cudaSuccess) {
     stencil_table_kernel<<<((Dmax + 1) * kOff3 + 127) / 128, 128>>>(w.tab, Dmax);
-    g_launches.fetch_add(1, std::memory_order_relaxed);
+    table10_kernel<<<((Dmax + 1) * kOff3 + 127) / 128, 128>>>(w.tab, w.tab10, (Dmax + 1) * kOff3);
+    g_launches.fetch_add(2, std::memory_order_relaxed);
     e = cudaDeviceSynchronize();
   }
   if (e != cudaSuccess) {
@@ -642,7 +647,7 @@ int tmgpu_gravity_amr_solve(tmgpu_gravity_amr* G, const double* mass, double* ph
     launches += 4;
     for (int l = 0; l < P.nlevels; ++l) {
       amr_m2l_kernel<<<(unsigned)(P.lv[l].n * 2), 256, 10 * kWin * sizeof(double), st>>>(
-          w.dev_lv, l, w.tab + (long long)(l + 3) * kOff3 * kTab);
+          w.dev_lv, l, w.tab10 + (long long)(l + 3) * kOff3 * kTab10);
       ++launches;
     }
     l2l_kernel<<<grid_for(512), 128, 0, st>>>(w.dloc[2], w.host_lv[0].loc, 8, 1.0 / 8.0);

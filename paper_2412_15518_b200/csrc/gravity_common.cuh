@@ -81,6 +81,64 @@ __device__ __forceinline__ void m2l_tab(const double* __restrict__ mom,
     for (int j = i; j < 3; ++j) out[4 + s2(i, j)] += -(M * d2[i][j]);
 }
 
+// Same arithmetic as m2l_tab with the symmetric 10-entry geometry
+// [ir, d1[3], d2 xx xy xz yy yz zz]: on lattice offsets 3*R_i*R_j is exact, so
+// d2 is exactly symmetric and the 13-entry table's values are reproduced.
+constexpr int kTab10 = 10;
+
+__device__ __forceinline__ void m2l_tab10(const double* __restrict__ mom,
+                                          const double* __restrict__ e, double out[10]) {
+  const double ir = e[0];
+  double d1[3], d2[3][3];
+#pragma unroll
+  for (int i = 0; i < 3; ++i) d1[i] = e[1 + i];
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int j = 0; j < 3; ++j) d2[i][j] = e[4 + s2(i, j)];
+  const double M = mom[0];
+  const double Dp[3] = {mom[1], mom[2], mom[3]};
+  double Q[3][3];
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int j = 0; j < 3; ++j) Q[i][j] = mom[4 + s2(i, j)];
+  double a = M * ir, b = 0.0, c = 0.0;
+#pragma unroll
+  for (int i = 0; i < 3; ++i) b += Dp[i] * d1[i];
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int j = 0; j < 3; ++j) c += Q[i][j] * d2[i][j];
+  out[0] += -(a - b + 0.5 * c);
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    double bb = 0.0;
+#pragma unroll
+    for (int j = 0; j < 3; ++j) bb += Dp[j] * d2[i][j];
+    out[1 + i] += -(M * d1[i] - bb);
+  }
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int j = i; j < 3; ++j) out[4 + s2(i, j)] += -(M * d2[i][j]);
+}
+
+// 13-entry table -> 10-entry symmetric table (per level: kOff3 entries)
+__global__ void table10_kernel(const double* __restrict__ t13, double* __restrict__ t10, int n) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n) return;
+  const double* e = t13 + (long long)t * kTab;
+  double* o = t10 + (long long)t * kTab10;
+  for (int q = 0; q < 4; ++q) o[q] = e[q];
+  o[4] = e[4];
+  o[5] = e[5];
+  o[6] = e[6];
+  o[7] = e[8];
+  o[8] = e[9];
+  o[9] = e[12];
+}
+
 __device__ __forceinline__ long long cidx(long long n, long long i, long long j, long long k) {
   return (k * n + j) * n + i;
 }
