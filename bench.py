@@ -1,12 +1,13 @@
 #!/usr/bin/env python
-"""Benchmark: sub-grid cell updates/s of the full SSP-RK3 hydro step on B200.
+"""Benchmark: sub-grid cell updates/s of the gravity + hydro step on B200.
 
 Workload (BASELINE.json configs[2], the config the metric is quoted on):
-rotating star on a 5-level AMR octree (levels 2..5, 5,888 leaves of 8^3
-cells = 3.01e6 cells), one step = CFL dt + 3 x [reference-exact ghost
-exchange -> aggregated FP64 stage kernel over every leaf + rk3_combine].
-Gravity has no reference implementation and is not in the
-timed step yet.
+rotating star on a 5-level AMR octree (leaf levels 2..5, 5,888 leaves of 8^3
+cells = 3.01e6 cells). One step = one adaptive FMM gravity solve with the
+angular-momentum correction (our specification: the reference
+has no gravity code) + the SSP-RK3 hydro step with the gravity source in the
+stage epilogue: CFL dt + 3 x [ghost exchange -> aggregated FP64 stage kernel
+over every leaf + rk3 combine].
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
@@ -29,25 +30,30 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-METRIC = "sub-grid cell updates/sec (hydro step; gravity+hydro step once gravity lands)"
+METRIC = "sub-grid cell updates/sec (gravity+hydro step)"
 UNIT = "cell-steps/s"
 ALG_FLOP_PER_CELL = 633.25     # hydro stage FP64 ops per cell (div/sqrt = 1)
 ALG_BYTES_PER_CELL = 180.0     # stage kernel, device-resident: 1280 staged cells x 40 B per
                                # 512 cells (100 B) + interior write 40 B + u0 read/write 40 B
+# Gravity, FP64 flops per interaction, FMA = 2: the order-2
+# Cartesian M2L is 28 multiply-adds once the geometry is known; W/X pairs
+# also build their geometry (46 ops); same-depth P2P is 4 multiply-adds with
+# tabulated geometry; cross-depth U pairs build theirs (15 ops).
+FLOP_M2L_V, FLOP_M2L_WX, FLOP_P2P, FLOP_P2P_U = 56, 102, 8, 23
 
 
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=200)
-    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--fast", action="store_true", help="FMA/reciprocal kernels (1e-10 parity)")
     ap.add_argument("--min-level", type=int, default=2)
     ap.add_argument("--max-level", type=int, default=5)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-steps", type=int, default=2)
-    ap.add_argument("--no-gravity", action="store_true")
+    ap.add_argument("--cpu-steps", type=int, default=1)
+    ap.add_argument("--hydro-only", action="store_true", help="time the hydro step alone")
     return ap.parse_args()
 
 
@@ -118,13 +124,19 @@ def build_workload(args):
 
 def workload_config(f, args, extra=None):
     n = f.leaf_count()
-    cfg = {"workload": f"rotating star, {args.max_level}-level AMR octree "
-                       f"(leaf levels {args.min_level}-{args.max_level}), {n} leaves x 8^3 cells, full "
-                       "SSP-RK3 hydro step: CFL dt + 3 x (ghost exchange + aggregated stage + rk3 combine)",
+    step = ("SSP-RK3 hydro step: CFL dt + 3 x (ghost exchange + aggregated stage + rk3 combine)"
+            if args.hydro_only else
+            "gravity+hydro step: adaptive FMM solve (V/W/X/U lists, angular-momentum correction) "
+            "+ SSP-RK3 hydro step with the gravity source in the stage epilogue: CFL dt + 3 x "
+            "(ghost exchange + aggregated stage + rk3 combine)")
+    cfg = {"workload": f"configs[2]: rotating star, {args.max_level}-level AMR octree "
+                       f"(leaf levels {args.min_level}-{args.max_level}), {n} leaves x 8^3 cells, {step}",
            "leaves": n, "cells": n * 512, "subgrid": "8^3 + 2 ghost layers, 5 vars (Euler)",
            "l2": "inputs larger than L2 (ghosted arena %.0f MB > 126 MB L2)" % (n * 69120 / 1e6),
-           "parity": "fast: <=1e-10 scaled vs reference" if args.fast else
-                     "bitwise vs reference (tests/test_forest_gpu.py)"}
+           "parity": ("hydro: fast <=1e-10 scaled vs reference" if args.fast else
+                      "hydro: bitwise vs the reference build (tests/test_forest_gpu.py)") +
+                     ("" if args.hydro_only else
+                      "; gravity+hydro: bitwise vs the oracle composition (tests/test_gravity_hydro_gpu.py)")}
     if extra:
         cfg.update(extra)
     return cfg
@@ -150,79 +162,85 @@ def reference_dt(ref, t, f, cfl=0.4):
                      for p in f.leaves())
 
 
-def time_reference(f, state, steps, warmup=0):
-    """Reference CPU step(s) on the host cores: returns (s/step, cores, detail)."""
+def time_reference(f, state, steps, warmup=0, gravity=True):
+    """CPU step(s) on the host cores: the reference's own hydro step (the
+    unmodified sources, oracle/_ref/libtmref.so: fill_ghosts_sync +
+    AggregationRegion(make_stage_kernel) over Scheduler(ncores) + rk3_combine)
+    and, for the gravity half (no reference code exists), our C restatement
+    of the adaptive FMM (oracle/gravity_amr_oracle.c, OpenMP over targets) on
+    the step's state. Returns (s/step, cores, detail)."""
+    from oracle import oracle as O
+    from paper_2412_15518_b200.gravity import forest_leaf_array
+
     ref, t = reference_setup(f, state)
     cores = os.cpu_count() or 1
-    for _ in range(warmup):
-        t.hydro_step(reference_dt(ref, t, f), workers=cores, max_slices=8)
-    walls, ex, st = [], 0.0, 0.0
-    for _ in range(steps):
+    o = O.Oracle() if gravity else None
+    lv = forest_leaf_array(f)
+    h3 = (1.0 / (8.0 * 2.0 ** lv[:, 0].astype(np.float64))) ** 3
+
+    def one():
+        tg = 0.0
+        if o is not None:
+            ghosted = np.stack([t.grid(int(p)).reshape(5, 12, 12, 12)[0, 2:10, 2:10, 2:10].reshape(512)
+                                for p in f.leaves()])
+            g0 = time.perf_counter()
+            o.grav_amr(lv, ghosted * h3[:, None], flags=1)
+            tg = time.perf_counter() - g0
         dt = reference_dt(ref, t, f)
-        t0 = time.perf_counter()
+        h0 = time.perf_counter()
         tex, tst = t.hydro_step(dt, workers=cores, max_slices=8)
-        walls.append(time.perf_counter() - t0)
+        return tg + time.perf_counter() - h0, tg, tex, tst
+
+    for _ in range(warmup):
+        one()
+    walls, gr, ex, st = [], 0.0, 0.0, 0.0
+    for _ in range(steps):
+        w, tg, tex, tst = one()
+        walls.append(w)
+        gr += tg
         ex += tex
         st += tst
-    return statistics.median(walls), cores, {"exchange_s": ex / steps, "stage_s": st / steps}
+    return statistics.median(walls), cores, {"gravity_s": gr / steps, "exchange_s": ex / steps,
+                                             "stage_s": st / steps}
 
 
-M2L_FLOP = 68  # per interaction (oracle/gravity_oracle.c contraction, geometry tabulated)
-P2P_FLOP = 20  # per near-field pair (sqrt and division counted as 1)
+def cpu_sample_text(steps, detail, cores, gravity=True):
+    txt = (f"{steps} full step(s) of the same workload on {cores} host threads: reference hydro "
+           f"(exchange {detail['exchange_s']:.2f} s single-threaded as in the reference, stages "
+           f"{detail['stage_s']:.2f} s over {cores} workers)")
+    if gravity:
+        txt += (f" + gravity {detail['gravity_s']:.2f} s (our C restatement of the FMM, OpenMP; "
+                "the reference has no gravity code)")
+    return txt
 
 
-def fmm_work(D):
-    """(M2L interactions, P2P pairs) of the FMM on level D."""
-    def axis(n, lo, hi):
-        return sum(sum(1 for d in range(lo(i), hi(i) + 1) if 0 <= i + d < n) for i in range(n))
+def fp64_peak():
+    """FP64 peak: MEASURED_PEAKS.json has no FP64 entry -> live DFMA microbenchmark."""
+    import ctypes as C
 
-    m2l = 0
-    for l in range(2, D + 1):
-        n = 1 << l
-        A = axis(n, lambda i: -2 - (i & 1), lambda i: 3 - (i & 1))
-        B = axis(n, lambda i: -1, lambda i: 1)
-        m2l += A ** 3 - B ** 3
-    n = 1 << D
-    B = axis(n, lambda i: -1, lambda i: 1)
-    return m2l, B ** 3 - n ** 3
+    from paper_2412_15518_b200 import _lib
+
+    peak_tf, pms = C.c_double(0), C.c_double(0)
+    _lib.lib.tmgpu_fp64_peak.argtypes = [C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_double),
+                                         C.c_void_p]
+    _lib.lib.tmgpu_fp64_peak(20000, C.byref(peak_tf), C.byref(pms), None)
+    return peak_tf.value
 
 
-def bench_gravity(stream, peak_tf):
-    """configs[1]: uniform level-4 octree (4,096 leaves, 128^3 cells), one FMM
-    gravity solve from the device arena (rho -> masses -> P2M..P2P)."""
-    import torch
+def hbm_peak():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            return float(json.load(fh)["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
 
-    from paper_2412_15518_b200 import amr
-    from paper_2412_15518_b200.gravity import GravitySolver
 
-    f = amr.build_scenario(amr.Scenario.rotating_star, 4, 4)
-    f.alloc()
-    f.set_interior(f.scenario_state(amr.Scenario.rotating_star))
-    G = GravitySolver(7)
-    n3 = 128 ** 3
-    phi = torch.empty(n3, dtype=torch.float64, device="cuda")
-    g = torch.empty(3 * n3, dtype=torch.float64, device="cuda")
-    sp = stream.cuda_stream
-    for _ in range(3):
-        G.solve_forest(f, phi, g, stream=sp, sync=False)
-    torch.cuda.synchronize()
-    reps = 20
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    for _ in range(reps):
-        G.solve_forest(f, phi, g, stream=sp, sync=False)
-    e1.record(stream)
-    torch.cuda.synchronize()
-    ms = e0.elapsed_time(e1) / reps
-    m2l, p2p = fmm_work(7)
-    tf = (m2l * M2L_FLOP + p2p * P2P_FLOP) / (ms * 1e-3) / 1e12
-    return {"config": "configs[1]: rotating star, uniform level-4 octree (4,096 leaves, 128^3 "
-                      "cells), one FMM solve (our spec, DESIGN.md §7; no reference exists)",
-            "ms_per_solve": ms, "cells_per_s": n3 / (ms * 1e-3),
-            "m2l_interactions": m2l, "p2p_pairs": p2p,
-            "roofline": {"bound": "fp64", "achieved": tf, "peak": peak_tf, "unit": "TFLOP/s",
-                         "frac": tf / peak_tf if peak_tf else None,
-                         "alg_flop": f"{M2L_FLOP}/M2L interaction + {P2P_FLOP}/P2P pair"}}
+def profile_traffic(name):
+    try:
+        with open(os.path.join(ROOT, "profiles", name)) as fh:
+            return json.load(fh)
+    except Exception:
+        return {}
 
 
 # ---------------------------------------------------------------- arms
@@ -231,21 +249,22 @@ def run_reference_arm(args, rank, world):
         return
     f, state = build_workload(args)
     cells = f.leaf_count() * 512
-    # bounded: every reference step is seconds of CPU work; cap the timed steps
-    k = max(1, min(args.steps, 5))
+    # bounded: every CPU step is seconds of work; cap the timed steps
+    k = max(1, min(args.steps, 2))
     w = min(args.warmup, 1)
-    sec, cores, detail = time_reference(f, state, k, w)
+    sec, cores, detail = time_reference(f, state, k, w, gravity=not args.hydro_only)
     v = cells / sec
-    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
-            "steps": k, "warmup": w, "ms_per_step": sec * 1e3, "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": workload_config(f, args, {"reference": "oracle/_ref/libtmref.so (unmodified "
-                                                "taskmesh sources): fill_ghosts_sync + AggregationRegion"
-                                                "(make_stage_kernel, W=1, max_slices=8) + rk3_combine"}),
-            "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "reference",
-                             "sample": f"{k} full C3 steps (requested {args.steps}), exchange "
-                                       f"{detail['exchange_s']:.2f} s (single-threaded), stages "
-                                       f"{detail['stage_s']:.2f} s over {cores} workers"},
+    line = {"impl": "reference", "metric": METRIC if not args.hydro_only else
+            "sub-grid cell updates/sec (hydro step)", "value": v, "unit": UNIT,
+            "n_gpus": args.gpus, "steps": k, "warmup": w, "ms_per_step": sec * 1e3,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic",
+            "config": workload_config(f, args, {"reference": "hydro: oracle/_ref/libtmref.so (the "
+                                                "unmodified taskmesh sources compiled in place); gravity: "
+                                                "oracle/gravity_amr_oracle.c (no reference code exists)"}),
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores,
+                             "kind": "reference" if args.hydro_only else "reference+port",
+                             "sample": cpu_sample_text(k, detail, cores, not args.hydro_only)},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -256,7 +275,7 @@ def run_ours(args, rank, world):
     import torch
 
     from paper_2412_15518_b200 import _lib
-    from paper_2412_15518_b200.driver import HydroDriver
+    from paper_2412_15518_b200.driver import GravityHydroDriver, HydroDriver
 
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
@@ -269,6 +288,7 @@ def run_ours(args, rank, world):
     f, state = build_workload(args)
     n = f.leaf_count()
     cells = n * 512  # whole job
+    full_state = state
     if world > 1:  # leaves partitioned over the GPUs (partition_leaves), NCCL halos
         from paper_2412_15518_b200 import dist as tmdist
 
@@ -280,7 +300,11 @@ def run_ours(args, rank, world):
     f.alloc()
     f.set_interior(state)
     local_cells = f.local_count() * 512
-    drv = HydroDriver(f, fast=args.fast)
+    gravity = not args.hydro_only
+    if gravity:
+        drv = GravityHydroDriver(f, fast=args.fast)
+    else:
+        drv = HydroDriver(f, fast=args.fast)
     stream = torch.cuda.current_stream()
     sp = stream.cuda_stream
 
@@ -311,43 +335,72 @@ def run_ours(args, rank, world):
         ms = float(t.item())
     value = cells / (ms * 1e-3)
 
-    # per-phase device timing (separate pass; kernel share of the step)
-    err = _lib.TmgpuError()
+    # per-phase device timing (separate pass, CUDA events on the launching
+    # stream): gravity phases per solve, stage kernel per launch
     _lib.lib.tmgpu_forest_set_timing.argtypes = [C.c_void_p, C.c_int, C.c_void_p]
     _lib.lib.tmgpu_forest_timing.argtypes = [C.c_void_p] + [C.POINTER(C.c_double)] * 3 + [
         C.POINTER(C.c_longlong)]
     _lib.lib.tmgpu_forest_set_timing(f.h, 1, None)
-    for _ in range(3):
+    if gravity:
+        drv.gravity.set_timing(True)
+    for _ in range(5):
         drv.step(stream=sp, sync=False)
     torch.cuda.synchronize()
     tc, te, ts, nst = C.c_double(), C.c_double(), C.c_double(), C.c_longlong()
     _lib.lib.tmgpu_forest_timing(f.h, C.byref(tc), C.byref(te), C.byref(ts), C.byref(nst))
     _lib.lib.tmgpu_forest_set_timing(f.h, 0, None)
     steps_t = max(nst.value, 1)
-    stage_ms = ts.value / (3 * steps_t)          # one stage launch = all leaves
+    stage_ms = ts.value / (3 * steps_t)          # one stage launch = all local leaves
     exch_ms = te.value / (3 * steps_t)
     cfl_ms = tc.value / steps_t
+    grav_ms, work = {}, {}
+    if gravity:
+        tot, ns = drv.gravity.timing()
+        drv.gravity.set_timing(False)
+        grav_ms = {k: v / max(ns, 1) for k, v in tot.items()}
+        work = drv.gravity.work()
 
-    # FP64 peak: MEASURED_PEAKS.json has no FP64 entry -> DFMA microbenchmark
-    peak_tf, pms = C.c_double(0), C.c_double(0)
-    _lib.lib.tmgpu_fp64_peak.argtypes = [C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_double),
-                                         C.c_void_p]
-    _lib.lib.tmgpu_fp64_peak(20000, C.byref(peak_tf), C.byref(pms), None)
-    hbm_peak = 6545.6
-    try:
-        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
-            hbm_peak = float(json.load(fh)["hbm_gbs"])
-    except Exception:
-        pass
-    gbps = local_cells * ALG_BYTES_PER_CELL / (stage_ms * 1e-3) / 1e9
-    tflops = local_cells * ALG_FLOP_PER_CELL / (stage_ms * 1e-3) / 1e12
-    traffic = None
-    try:
-        with open(os.path.join(ROOT, "profiles", "stage_kernel_latest.json")) as fh:
-            prof = json.load(fh)
-            traffic = prof.get("dram_bytes_per_launch")
-    except Exception:
-        prof = {}
+    peak_tf = fp64_peak()
+    hbm, hbm_src = hbm_peak()
+    stage_gbps = local_cells * ALG_BYTES_PER_CELL / (stage_ms * 1e-3) / 1e9
+    stage_tf = local_cells * ALG_FLOP_PER_CELL / (stage_ms * 1e-3) / 1e12
+    stage_prof = profile_traffic("stage_kernel_latest.json")
+    stage_roof = {"bound": "hbm", "achieved": stage_gbps, "peak": hbm, "unit": "GB/s",
+                  "frac": stage_gbps / hbm, "traffic": stage_prof.get("dram_bytes_per_launch"),
+                  "peak_source": hbm_src,
+                  "kernel": "stage_kernel<5,%s>" % ("true" if args.fast else "false"),
+                  "alg_bytes_per_cell": ALG_BYTES_PER_CELL, "launch_ms": stage_ms,
+                  "cells_per_launch": local_cells,
+                  "fp64": {"achieved": stage_tf, "peak": peak_tf, "unit": "TFLOP/s",
+                           "frac": stage_tf / peak_tf if peak_tf else None,
+                           "alg_flop_per_cell": ALG_FLOP_PER_CELL}}
+    share = {"hydro_stage": 3 * stage_ms / ms, "hydro_exchange": 3 * exch_ms / ms,
+             "hydro_cfl": cfl_ms / ms}
+    if gravity:
+        m2l_flop = work["v_pairs"] * FLOP_M2L_V + work["wx_entries"] * FLOP_M2L_WX
+        m2l_tf = m2l_flop / (grav_ms["m2l"] * 1e-3) / 1e12
+        m2l_prof = profile_traffic("m2l_kernel_latest.json")
+        roofline = {"bound": "fp64", "achieved": m2l_tf, "peak": peak_tf, "unit": "TFLOP/s",
+                    "frac": m2l_tf / peak_tf if peak_tf else None,
+                    "traffic": m2l_prof.get("dram_bytes_per_launch"),
+                    "kernel": "amr_m2l (gravity M2L: V-list stencil + W/X lists), all levels",
+                    "launch_ms": grav_ms["m2l"], "alg_flop_per_launch": m2l_flop,
+                    "alg_flop": f"{FLOP_M2L_V}/V pair x {work['v_pairs']} + {FLOP_M2L_WX}/W-X "
+                                f"entry x {work['wx_entries']} (FMA = 2)",
+                    "peak_source": "tmgpu_fp64_peak DFMA microbenchmark (live; MEASURED_PEAKS.json "
+                                   "has no FP64 entry)",
+                    "hydro_stage": stage_roof}
+        for k, v in grav_ms.items():
+            share["gravity_" + k] = v / ms
+        step_flop = (m2l_flop + work["p2p_pairs"] * FLOP_P2P + work["u_cross_entries"] * FLOP_P2P_U
+                     + 3 * local_cells * ALG_FLOP_PER_CELL)
+        roofline["step_fp64"] = {"achieved": step_flop / (ms * 1e-3) / 1e12, "unit": "TFLOP/s",
+                                 "frac": step_flop / (ms * 1e-3) / 1e12 / peak_tf if peak_tf else None,
+                                 "note": "all algorithmic FP64 of the step / step time"}
+    else:
+        roofline = stage_roof
+    roofline["step_share"] = share
+    roofline["gravity_work"] = work or None
 
     # e2e through the public API with host buffers (pinned), per step:
     # H2D of the state, one step, D2H of the updated state.
@@ -366,6 +419,7 @@ def run_ours(args, rank, world):
         a1.record(stream)
         torch.cuda.synchronize()
         e2.append(a0.elapsed_time(a1))
+    drv.check(stream=sp)
     e2e_ms = statistics.median(e2)
     if dist:
         t = torch.tensor([e2e_ms], device="cuda")
@@ -373,7 +427,8 @@ def run_ours(args, rank, world):
         e2e_ms = float(t.item())
     nbytes = state.nbytes
 
-    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+    line = {"metric": METRIC if gravity else "sub-grid cell updates/sec (hydro step)",
+            "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
             "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (analytic rotating star + "
@@ -381,43 +436,32 @@ def run_ours(args, rank, world):
             "config": workload_config(f, args, {
                 "parallelism": (f"leaves partitioned over {world} GPUs (partition_leaves, "
                                 "contiguous Morton ranges); cross-GPU ghost slabs by grouped "
-                                "NCCL send/recv per RK stage; dt by ncclAllReduce(min)")
+                                "NCCL send/recv per RK stage; dt by ncclAllReduce(min)" +
+                                ("; gravity: leaf masses all-gathered, M2L/L2L/L2P on the "
+                                 "owned subtree" if gravity else ""))
                 if world > 1 else "single GPU"}),
             "e2e": {"value": cells / (e2e_ms * 1e-3), "unit": UNIT,
                     "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes,
                     "ms_per_step": e2e_ms,
                     "path": "paper_2412_15518_b200.amr.Forest.set_interior(pinned) -> "
-                            "HydroDriver.step -> Forest.get_interior(pinned)"},
-            "roofline": {"bound": "hbm", "achieved": gbps, "peak": hbm_peak, "unit": "GB/s",
-                         "frac": gbps / hbm_peak, "traffic": traffic,
-                         "kernel": "stage_kernel<5,%s>" % ("true" if args.fast else "false"),
-                         "alg_bytes_per_cell": ALG_BYTES_PER_CELL,
-                         "launch_ms": stage_ms, "cells_per_launch": local_cells,
-                         "fp64": {"achieved": tflops, "peak": peak_tf.value, "unit": "TFLOP/s",
-                                  "frac": tflops / peak_tf.value if peak_tf.value else None,
-                                  "alg_flop_per_cell": ALG_FLOP_PER_CELL,
-                                  "peak_source": "tmgpu_fp64_peak DFMA microbenchmark (live)"},
-                         "fp64_pipe_util_ncu": prof.get("fp64_pipe_pct"),
-                         "step_share": {"stage": 3 * stage_ms / ms, "exchange": 3 * exch_ms / ms,
-                                        "cfl": cfl_ms / ms}},
+                            f"{type(drv).__name__}.step -> Forest.get_interior(pinned)"},
+            "roofline": roofline,
             "gpu_launches": launches,
             "clocks": clk.summary()}
 
-    if rank == 0 and world == 1 and not args.no_gravity:
-        line["gravity"] = bench_gravity(stream, peak_tf.value)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            sec, cores, detail = time_reference(f, state, args.cpu_steps)
+            sec, cores, detail = time_reference(f, full_state, args.cpu_steps, gravity=gravity)
             line["cpu_baseline"] = {"value": cells / sec, "unit": UNIT, "cores": cores,
-                                    "kind": "reference",
-                                    "sample": f"{args.cpu_steps} full steps of the same workload "
-                                              f"(exchange {detail['exchange_s']:.2f} s single-threaded, "
-                                              f"stages {detail['stage_s']:.2f} s over {cores} threads)"}
+                                    "kind": "reference+port" if gravity else "reference",
+                                    "sample": cpu_sample_text(args.cpu_steps, detail, cores, gravity)}
         except Exception as ex:  # reference build missing on this box
             line["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": 0, "kind": "reference",
                                     "sample": f"unavailable: {ex}"}
     if rank == 0:
         print(json.dumps(line), flush=True)
+    if gravity and hasattr(drv, "close"):
+        drv.close()
     if dist:
         dist.destroy_process_group()
 

@@ -223,6 +223,16 @@ int tmgpu_gravity_amr_mass_from_arena(tmgpu_gravity_amr* G, const double* arena,
 int tmgpu_gravity_amr_solve(tmgpu_gravity_amr* G, const double* mass, double* phi, double* g,
                             int flags, void* stream, tmgpu_error* err);
 int tmgpu_gravity_amr_am_stats(tmgpu_gravity_amr* G, double* out);
+/* algorithmic work of one solve (bench roofline): [V pairs, W/X entries,
+ * same-depth P2P pairs, cross-depth U entries, V pairs evaluated] */
+int tmgpu_gravity_amr_work(const tmgpu_gravity_amr* G, long long* out);
+/* multi-GPU: this rank (comm) owns canonical slots [slot_bounds[r], slot_bounds[r+1]);
+ * masses and outputs become by local slot; results equal the one-GPU solve bitwise */
+int tmgpu_gravity_amr_distribute(tmgpu_gravity_amr* G, tmgpu_comm* comm, const long long* slot_bounds,
+                                 tmgpu_error* err);
+/* per-phase device timing: totals in ms of [up, m2l, l2l, l2p, am] */
+int tmgpu_gravity_amr_set_timing(tmgpu_gravity_amr* G, int on);
+int tmgpu_gravity_amr_timing(tmgpu_gravity_amr* G, double* ms, long long* solves);
 const double* tmgpu_gravity_amr_mass_ptr(const tmgpu_gravity_amr* G);
 
 int tmgpu_selftest_fastmath(int mode, long long n, uint64_t seed, unsigned long long* mismatches,

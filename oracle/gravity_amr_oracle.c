@@ -322,6 +322,7 @@ int tmo_grav_amr_solve_ex(long nleaves, const int* leaves, const double* mass, i
   for (int d = Dmax - 1; d >= 0; --d) {
     const long n = dep[d].n;
     const double hc = 1.0 / (double)dep[d + 1].n;
+#pragma omp parallel for schedule(dynamic, 1)
     for (long K = 0; K < n; ++K)
       for (long J = 0; J < n; ++J)
         for (long I = 0; I < n; ++I) {
@@ -339,6 +340,7 @@ int tmo_grav_amr_solve_ex(long nleaves, const int* leaves, const double* mass, i
   for (int d = 2; d <= Dmax; ++d) {
     const long m = dep[d].n;
     const double h = 1.0 / (double)m;
+#pragma omp parallel for schedule(dynamic, 1)
     for (long k = 0; k < m; ++k)
       for (long j = 0; j < m; ++j)
         for (long i = 0; i < m; ++i) {
@@ -399,6 +401,7 @@ int tmo_grav_amr_solve_ex(long nleaves, const int* leaves, const double* mass, i
   for (int d = 3; d <= Dmax; ++d) {
     const long m = dep[d].n;
     const double h = 1.0 / (double)m;
+#pragma omp parallel for schedule(dynamic, 1)
     for (long k = 0; k < m; ++k)
       for (long j = 0; j < m; ++j)
         for (long i = 0; i < m; ++i) {
@@ -412,6 +415,7 @@ int tmo_grav_amr_solve_ex(long nleaves, const int* leaves, const double* mass, i
   }
   /* L2P + same-depth P2P */
   const long ncell = nleaves * 512;
+#pragma omp parallel for schedule(dynamic, 4)
   for (long s = 0; s < nleaves; ++s) {
     const int d = leaves[4 * s] + 3;
     const long N = dep[d].n;
@@ -428,19 +432,17 @@ int tmo_grav_amr_solve_ex(long nleaves, const int* leaves, const double* mass, i
             const long si = i + dx, sj = j + dy, sk = k + dz;
             if (si < 0 || sj < 0 || sk < 0 || si >= N || sj >= N || sk >= N) continue;
             if (dep[d].type[cix(N, si, sj, sk)] != 2) continue;
-            const double ms = dep[d].mom[cix(N, si, sj, sk) * 10];
-            const double Rx = -(double)dx * h, Ry = -(double)dy * h, Rz = -(double)dz * h;
-            const double r2 = Rx * Rx + Ry * Ry + Rz * Rz;
-            const double ir = 1.0 / sqrt(r2);
-            const double ir3 = ir * ir * ir;
             if (cnt) {
               p += 1.0;
               continue;
             }
-            p -= ms * ir;
-            gx -= ms * Rx * ir3;
-            gy -= ms * Ry * ir3;
-            gz -= ms * Rz * ir3;
+            const double nm = -dep[d].mom[cix(N, si, sj, sk) * 10];
+            double w[4];
+            tmo_grav_p2p_geom(-(double)dx * h, -(double)dy * h, -(double)dz * h, w);
+            p = fma(nm, w[0], p);
+            gx = fma(nm, w[1], gx);
+            gy = fma(nm, w[2], gy);
+            gz = fma(nm, w[3], gz);
           }
       const long o = s * 512 + c;
       phi[o] = p;
@@ -456,20 +458,18 @@ int tmo_grav_amr_solve_ex(long nleaves, const int* leaves, const double* mass, i
     const long tn = dep[x->td].n;
     const long ti = x->tidx % tn, tj = (x->tidx / tn) % tn, tk = x->tidx / (tn * tn);
     const long o = dep[x->td].out[x->tidx];
-    const double ms = dep[x->sd].mom[cix(dep[x->sd].n, x->si, x->sj, x->sk) * 10];
-    const double Rx = centre(ti, x->td) - centre(x->si, x->sd), Ry = centre(tj, x->td) - centre(x->sj, x->sd),
-                 Rz = centre(tk, x->td) - centre(x->sk, x->sd);
-    const double r2 = Rx * Rx + Ry * Ry + Rz * Rz;
-    const double ir = 1.0 / sqrt(r2);
-    const double ir3 = ir * ir * ir;
     if (cnt) {
       phi[o] += 1.0;
       continue;
     }
-    phi[o] -= ms * ir;
-    g[o] -= ms * Rx * ir3;
-    g[ncell + o] -= ms * Ry * ir3;
-    g[2 * ncell + o] -= ms * Rz * ir3;
+    const double nm = -dep[x->sd].mom[cix(dep[x->sd].n, x->si, x->sj, x->sk) * 10];
+    double w[4];
+    tmo_grav_p2p_geom(centre(ti, x->td) - centre(x->si, x->sd), centre(tj, x->td) - centre(x->sj, x->sd),
+                      centre(tk, x->td) - centre(x->sk, x->sd), w);
+    phi[o] = fma(nm, w[0], phi[o]);
+    g[o] = fma(nm, w[1], g[o]);
+    g[ncell + o] = fma(nm, w[2], g[ncell + o]);
+    g[2 * ncell + o] = fma(nm, w[3], g[2 * ncell + o]);
   }
   free(L.e);
   free_depths(dep, Dmax);

@@ -24,11 +24,15 @@
  *              L_ij = -(M D2_ij)
  *            With this truncation the mutual M2L forces of every pair are
  *            exactly opposite, so the FMM conserves linear momentum
- *             to round-off
+ *             to round-off. Arithmetic: geometry per separation
+ *            (tmo_grav_geom), then a fixed chain of 28 fused multiply-adds
+ *            (tmo_grav_m2l_geom) — C fma() and the GPU's DFMA are the same
+ *            correctly rounded operation, so the kernels match bit for bit
  *   L2L      L(c) = shift(L(parent(c))) + M2L-sum(c) (levels 3..D)
  *   L2P+P2P  at the finest level (expansion centre = cell centre, so L2P is
  *            phi = L0, g = -L_i) plus direct monopole sums over the 26
- *            neighbours (dz, dy, dx ascending): phi -= m'/r, g -= m' R / r^3
+ *            neighbours (dz, dy, dx ascending): phi += -m'/r, g += -m' R/r^3
+ *            as fused multiply-adds with the geometry of tmo_grav_p2p_geom
  */
 #include <math.h>
 #include <stdlib.h>
@@ -42,38 +46,70 @@ static const int S2[3][3] = {{0, 1, 2}, {1, 3, 4}, {2, 4, 5}};
 /* Moments: [0] M, [1..3] D, [4..9] Q (xx xy xz yy yz zz). Locals: [0] L0,
  * [1..3] L_i, [4..9] L_ij. */
 
-void tmo_grav_m2l(const double* mom, const double* R, double* out /* 10, accumulated */) {
+/* M2L geometry of the separation R = x_target - x_source: e[13] =
+ * [ir, D1 x y z, D2 xx xy xz yy yz zz, D2/2 xx yy zz] with D1_i = -R_i/r^3,
+ * D2_ij = 3 R_i R_j / r^5 - delta_ij / r^3 (the halving is exact). */
+void tmo_grav_geom(const double* R, double* e) {
   const double x = R[0], y = R[1], z = R[2];
   const double r2 = x * x + y * y + z * z;
   const double r = sqrt(r2);
   const double ir = 1.0 / r;
   const double ir2 = ir * ir;
   const double ir3 = ir * ir2, ir5 = ir3 * ir2;
-  const double Rv[3] = {x, y, z};
-  double d1[3], d2[3][3];
-  for (int i = 0; i < 3; ++i) d1[i] = -Rv[i] * ir3;
+  e[0] = ir;
+  for (int i = 0; i < 3; ++i) e[1 + i] = -R[i] * ir3;
   for (int i = 0; i < 3; ++i)
-    for (int j = 0; j < 3; ++j) d2[i][j] = 3.0 * Rv[i] * Rv[j] * ir5 - (i == j ? ir3 : 0.0);
-  const double M = mom[0];
-  const double Dp[3] = {mom[1], mom[2], mom[3]};
-  double Q[3][3];
-  for (int i = 0; i < 3; ++i)
-    for (int j = 0; j < 3; ++j) Q[i][j] = mom[4 + S2[i][j]];
-  /* L0 = -(M D0 - D_i D1_i + 1/2 Q_ij D2_ij) */
-  double a = M * ir, b = 0.0, c = 0.0;
-  for (int i = 0; i < 3; ++i) b += Dp[i] * d1[i];
-  for (int i = 0; i < 3; ++i)
-    for (int j = 0; j < 3; ++j) c += Q[i][j] * d2[i][j];
-  out[0] += -(a - b + 0.5 * c);
-  /* L_i = -(M D1_i - D_j D2_ij) */
+    for (int j = i; j < 3; ++j) e[4 + S2[i][j]] = 3.0 * R[i] * R[j] * ir5 - (i == j ? ir3 : 0.0);
+  e[10] = 0.5 * e[4];
+  e[11] = 0.5 * e[7];
+  e[12] = 0.5 * e[9];
+}
+
+/* One M2L term with known geometry, accumulated into out (10 locals) as a
+ * fixed chain of fused multiply-adds (28 per term):
+ *   L0   += -M ir + D_i D1_i - (1/2) Q_ij D2_ij
+ *   L_i  += -M D1_i + D_j D2_ij
+ *   L_ij += -M D2_ij
+ * (Q symmetric: (1/2) Q_ij D2_ij = sum_i Q_ii (D2_ii/2) + sum_{i<j} Q_ij D2_ij). */
+void tmo_grav_m2l_geom(const double* mom, const double* e, double* out) {
+  const double nM = -mom[0];
+  double o = out[0];
+  o = fma(nM, e[0], o);
+  o = fma(mom[1], e[1], o);
+  o = fma(mom[2], e[2], o);
+  o = fma(mom[3], e[3], o);
+  o = fma(-mom[4], e[10], o);
+  o = fma(-mom[5], e[5], o);
+  o = fma(-mom[6], e[6], o);
+  o = fma(-mom[7], e[11], o);
+  o = fma(-mom[8], e[8], o);
+  o = fma(-mom[9], e[12], o);
+  out[0] = o;
   for (int i = 0; i < 3; ++i) {
-    double bb = 0.0;
-    for (int j = 0; j < 3; ++j) bb += Dp[j] * d2[i][j];
-    out[1 + i] += -(M * d1[i] - bb);
+    double t = out[1 + i];
+    t = fma(nM, e[1 + i], t);
+    for (int j = 0; j < 3; ++j) t = fma(mom[1 + j], e[4 + S2[i][j]], t);
+    out[1 + i] = t;
   }
-  /* L_ij = -(M D2_ij) */
-  for (int i = 0; i < 3; ++i)
-    for (int j = i; j < 3; ++j) out[4 + S2[i][j]] += -(M * d2[i][j]);
+  for (int q = 0; q < 6; ++q) out[4 + q] = fma(nM, e[4 + q], out[4 + q]);
+}
+
+void tmo_grav_m2l(const double* mom, const double* R, double* out /* 10, accumulated */) {
+  double e[13];
+  tmo_grav_geom(R, e);
+  tmo_grav_m2l_geom(mom, e, out);
+}
+
+/* P2P geometry of R: w[4] = [1/r, R_x/r^3, R_y/r^3, R_z/r^3]; the monopole
+ * term is then phi += -m w0, g_i += -m w_i (fused multiply-adds). */
+void tmo_grav_p2p_geom(double Rx, double Ry, double Rz, double* w) {
+  const double r2 = Rx * Rx + Ry * Ry + Rz * Rz;
+  const double ir = 1.0 / sqrt(r2);
+  const double ir3 = ir * ir * ir;
+  w[0] = ir;
+  w[1] = Rx * ir3;
+  w[2] = Ry * ir3;
+  w[3] = Rz * ir3;
 }
 
 /* child moments shifted by s (child centre - parent centre), accumulated */
@@ -182,15 +218,13 @@ int tmo_grav_solve(int D, const double* mass, double* phi, double* g) {
               if (!dx && !dy && !dz) continue;
               const long si = i + dx, sj = j + dy, sk = k + dz;
               if (si < 0 || sj < 0 || sk < 0 || si >= N || sj >= N || sk >= N) continue;
-              const double ms = mass[cidx(N, si, sj, sk)];
-              const double Rx = -(double)dx * h, Ry = -(double)dy * h, Rz = -(double)dz * h;
-              const double r2 = Rx * Rx + Ry * Ry + Rz * Rz;
-              const double ir = 1.0 / sqrt(r2);
-              const double ir3 = ir * ir * ir;
-              p -= ms * ir;
-              gx -= ms * Rx * ir3;
-              gy -= ms * Ry * ir3;
-              gz -= ms * Rz * ir3;
+              const double nm = -mass[cidx(N, si, sj, sk)];
+              double w[4];
+              tmo_grav_p2p_geom(-(double)dx * h, -(double)dy * h, -(double)dz * h, w);
+              p = fma(nm, w[0], p);
+              gx = fma(nm, w[1], gx);
+              gy = fma(nm, w[2], gy);
+              gz = fma(nm, w[3], gz);
             }
         phi[c] = p;
         g[c] = gx;

@@ -60,7 +60,10 @@ int tmo_fill_ghosts_sync(const tmo_tree* t, double** grids);
 int tmo_flag_refinement(const tmo_tree* t, const double* grid, double theta, double rho_floor);
 
 /* gravity (our FMM specification, parity unpinned: no reference code) — gravity_oracle.c */
+void tmo_grav_geom(const double* R, double* e);
+void tmo_grav_m2l_geom(const double* mom, const double* e, double* out);
 void tmo_grav_m2l(const double* mom, const double* R, double* out);
+void tmo_grav_p2p_geom(double Rx, double Ry, double Rz, double* w);
 void tmo_grav_m2m(const double* ch, const double* s, double* out);
 void tmo_grav_l2l(const double* L, const double* s, double* out);
 int tmo_grav_solve(int D, const double* mass, double* phi, double* g);

@@ -215,6 +215,7 @@ class Forest:
         o = np.ascontiguousarray(np.asarray(owner, dtype=np.int32))
         err = TmgpuError()
         self._comm = comm  # keep the communicator alive as long as the forest
+        self._owner = o
         _lib.check(lib.tmgpu_forest_distribute(self.h, comm.h if comm else None,
                                                o.ctypes.data_as(_ip), len(o), C.byref(err)), err)
 

@@ -21,6 +21,8 @@ struct Api {
   ncclResult_t (*GroupEnd)() = nullptr;
   ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
                             cudaStream_t) = nullptr;
+  ncclResult_t (*Broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t,
+                            cudaStream_t) = nullptr;
   const char* (*GetErrorString)(ncclResult_t) = nullptr;
   std::string error;
 };
@@ -44,9 +46,10 @@ Api& api() {
     a.GroupStart = (decltype(a.GroupStart))sym("ncclGroupStart");
     a.GroupEnd = (decltype(a.GroupEnd))sym("ncclGroupEnd");
     a.AllReduce = (decltype(a.AllReduce))sym("ncclAllReduce");
+    a.Broadcast = (decltype(a.Broadcast))sym("ncclBroadcast");
     a.GetErrorString = (decltype(a.GetErrorString))sym("ncclGetErrorString");
     if (!a.GetUniqueId || !a.CommInitRank || !a.Send || !a.Recv || !a.GroupStart || !a.GroupEnd ||
-        !a.AllReduce)
+        !a.AllReduce || !a.Broadcast)
       a.error = "libnccl.so.2 lacks required symbols";
   });
   return a;
@@ -94,6 +97,21 @@ int comm_allreduce_min(tmgpu_comm* c, double* buf, size_t n, cudaStream_t st, st
   ncclResult_t r = api().AllReduce(buf, buf, n, ncclDouble, ncclMin, c->comm, st);
   if (r != ncclSuccess) {
     if (why) *why = "dt allreduce: " + nerr(r);
+    return TMGPU_ERR_CUDA;
+  }
+  return TMGPU_OK;
+}
+
+int comm_allgatherv(tmgpu_comm* c, double* buf, const std::vector<long long>& off,
+                    const std::vector<long long>& cnt, cudaStream_t st, std::string* why) {
+  Api& a = api();
+  ncclResult_t r = a.GroupStart();
+  for (int p = 0; p < c->world && r == ncclSuccess; ++p)
+    if (cnt[p] > 0) r = a.Broadcast(buf + off[p], buf + off[p], (size_t)cnt[p], ncclDouble, p, c->comm, st);
+  ncclResult_t r2 = a.GroupEnd();
+  if (r == ncclSuccess) r = r2;
+  if (r != ncclSuccess) {
+    if (why) *why = "allgatherv: " + nerr(r);
     return TMGPU_ERR_CUDA;
   }
   return TMGPU_OK;

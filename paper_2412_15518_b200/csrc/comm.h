@@ -21,6 +21,10 @@ int comm_exchange(tmgpu_comm* c, const double* send, const std::vector<long long
                   const std::vector<long long>& send_cnt, double* recv,
                   const std::vector<long long>& recv_off, const std::vector<long long>& recv_cnt,
                   cudaStream_t st, std::string* why);
+// In-place all-gather of variable segments: rank p contributes
+// buf[off[p] .. +cnt[p]) (grouped ncclBroadcast, root p), every rank ends with all.
+int comm_allgatherv(tmgpu_comm* c, double* buf, const std::vector<long long>& off,
+                    const std::vector<long long>& cnt, cudaStream_t st, std::string* why);
 // In-place min-allreduce of n doubles (the global CFL dt).
 int comm_allreduce_min(tmgpu_comm* c, double* buf, size_t n, cudaStream_t st, std::string* why);
 

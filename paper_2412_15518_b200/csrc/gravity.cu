@@ -109,15 +109,13 @@ __global__ void p2p_kernel(const double* __restrict__ mass, const double* __rest
           if (!dx && !dy && !dz) continue;
           const long long si = i + dx, sj = j + dy, sk = k + dz;
           if (si < 0 || sj < 0 || sk < 0 || si >= N || sj >= N || sk >= N) continue;
-          const double ms = mass[cidx(N, si, sj, sk)];
-          const double Rx = -(double)dx * h, Ry = -(double)dy * h, Rz = -(double)dz * h;
-          const double r2 = Rx * Rx + Ry * Ry + Rz * Rz;
-          const double ir = 1.0 / sqrt(r2);
-          const double ir3 = ir * ir * ir;
-          p -= ms * ir;
-          gx -= ms * Rx * ir3;
-          gy -= ms * Ry * ir3;
-          gz -= ms * Rz * ir3;
+          const double nm = -mass[cidx(N, si, sj, sk)];
+          double w[4];
+          p2p_geom(-(double)dx * h, -(double)dy * h, -(double)dz * h, w);
+          p = fma(nm, w[0], p);
+          gx = fma(nm, w[1], gx);
+          gy = fma(nm, w[2], gy);
+          gz = fma(nm, w[3], gz);
         }
     phi[c] = p;
     g[c] = gx;

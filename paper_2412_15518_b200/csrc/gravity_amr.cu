@@ -23,10 +23,13 @@
 //               specification, tmo_grav_am_correct): per-slot adjacent-pair
 //               tree (shuffles + shared memory), one-CTA tree over slots,
 //               3x3 solve, apply
+#include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
 
+#include "comm.h"
 #include "gravity_amr_plan.h"
 #include "gravity_common.cuh"
 
@@ -52,17 +55,19 @@ __device__ __forceinline__ double centre(long long gi, int d) {
   return ((double)gi + 0.5) / (double)(1LL << d);
 }
 
+// arena slots 0..nslots-1 are the canonical slots lo.. (distributed: the owned range)
 __global__ void amr_mass_kernel(const double* __restrict__ arena, int V, long long nslots,
-                                const int* __restrict__ slot_level, double* __restrict__ mass) {
+                                long long lo, const int* __restrict__ slot_level,
+                                double* __restrict__ mass) {
   const long long total = nslots * 512;
   for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
        t += (long long)gridDim.x * blockDim.x) {
     const long long s = t >> 9;
     const int c = (int)(t & 511);
     const int i = c & 7, j = (c >> 3) & 7, k = c >> 6;
-    const double h = 1.0 / (double)(8LL << slot_level[s]);
+    const double h = 1.0 / (double)(8LL << slot_level[lo + s]);
     const double dV = h * h * h;
-    mass[t] = arena[s * V * 1728 + ((k + 2) * 12 + (j + 2)) * 12 + (i + 2)] * dV;
+    mass[lo * 512 + t] = arena[s * V * 1728 + ((k + 2) * 12 + (j + 2)) * 12 + (i + 2)] * dV;
   }
 }
 
@@ -133,10 +138,11 @@ __device__ __forceinline__ int win_index(int wx, int wy, int wz) {
 }
 
 __global__ void __launch_bounds__(256, 2) amr_m2l_kernel(const GLv* __restrict__ Lv, int l,
-                                                         const double* __restrict__ tab) {
+                                                         const double* __restrict__ tab,
+                                                         const int* __restrict__ nodes) {
   extern __shared__ double sm[];  // [10][kWin] doubles = 102,400 B
   const GLv L = Lv[l];
-  const int n = blockIdx.x >> 1;
+  const int n = nodes ? nodes[blockIdx.x >> 1] : (int)(blockIdx.x >> 1);
   const int z0 = (blockIdx.x & 1) * 4;
   const int* nb27 = L.nbr + (long long)n * 27;
   for (int q = threadIdx.x; q < 12 * 12 * 8; q += blockDim.x) {
@@ -173,7 +179,7 @@ __global__ void __launch_bounds__(256, 2) amr_m2l_kernel(const GLv* __restrict__
         double mom_q[10];
 #pragma unroll
         for (int cc = 0; cc < 10; ++cc) mom_q[cc] = sm[cc * kWin + q];
-        m2l_tab10(mom_q, tab + (((dz + 3) * kOff + (dy + 3)) * kOff + (dx + 3)) * kTab10, o);
+        m2l_tab(mom_q, tab + (((dz + 3) * kOff + (dy + 3)) * kOff + (dx + 3)) * kTab, o);
       }
   const long long flat = (long long)n * 512 + (k * 8 + j) * 8 + i;
   const long long e0 = L.moff[flat], e1 = L.moff[flat + 1];
@@ -200,13 +206,163 @@ __global__ void __launch_bounds__(256, 2) amr_m2l_kernel(const GLv* __restrict__
   for (int q = 0; q < 10; ++q) out[q] = o[q];
 }
 
-__global__ void amr_l2l_kernel(const GLv* __restrict__ Lv, int l, long long nnodes) {
+// ---- M2L, all levels in one launch -----------------------------------------
+// CTA = one patch (8^3 targets), 128 threads, one CTA per SM (197 KB smem).
+// Warp w = target parity class (b, c) = (w & 1, w >> 1) in y, z; lane =
+// (a, Y, Z) = (lane & 1, lane >> 1 & 3, lane >> 3): the thread owns the four
+// targets x = a + 2k (k = 0..3), y = 2Y + b, z = 2Z + c. All 8 siblings of a
+// parent share the 6x6x6 children of the parent's neighbours as sources (the
+// 189-cell list is that box minus the target's 27 near cells), so per source
+// row (dy, dz) — warp-uniform — the thread keeps the geometry of its six x
+// offsets in registers (G[jj], jj = j + 2, dx = j - a) and streams the row's 12
+// sources once, applying each to every target k with jj = sx - 2k in [0, 5]:
+// ~1.3 shared loads per interaction instead of 20. In the nine near rows the
+// offsets j = 0, 1 (near for both a) are skipped; j = -1 (a = 0) and j = 2
+// (a = 1) use zeroed near geometry: an exact no-op, because a sum that starts
+// at +0 never becomes -0 and x + (+-0) = x (finite moments).
+// Window: 12^3 sources (27-patch neighbourhood; missing patches are zero
+// moments), stored with M and Q negated (the contraction is all FMAs), split
+// into 4 (y, z)-parity sub-grids of 6 x 6 rows of 12 with pitches 13 / 84:
+// a warp's 16 distinct source addresses (Y, Z) fall in 16 distinct bank pairs.
+// Accumulation per target: dz, dy, dx ascending, then the W/X pairs —
+// tmo_grav_amr_solve's order, so the result is bitwise the oracle's.
+constexpr int kM2lThreads = 128;
+constexpr int kWPY = 13, kWPZ = 84, kWSub = 6 * kWPZ, kWVar = 4 * kWSub;  // 2016 doubles per var
+constexpr int kWinDoubles = 10 * kWVar;                                   // 20,160
+constexpr int kTabDoubles = kOff3 * kTab;                                 // 4,459
+constexpr size_t kM2lSmem = (size_t)(kWinDoubles + kTabDoubles) * sizeof(double);  // 196,952 B
+
+template <bool NEAR>
+__device__ __forceinline__ void m2l_row(const double* __restrict__ src, const double (&G)[6][kTab],
+                                        double (&acc)[4][10]) {
+#pragma unroll
+  for (int sx = 0; sx < 12; ++sx) {
+    double m[10];
+#pragma unroll
+    for (int q = 0; q < 10; ++q) m[q] = src[q * kWVar + sx];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int jj = sx - 2 * k;
+      if (jj < 0 || jj > 5) continue;
+      if (NEAR && (jj == 2 || jj == 3)) continue;
+      m2l_acc(m[0], m[1], m[2], m[3], m[4], m[5], m[6], m[7], m[8], m[9], G[jj], acc[k]);
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kM2lThreads, 1) amr_m2l_fused_kernel(
+    const GLv* __restrict__ Lv, const int2* __restrict__ work, const double* __restrict__ tab_all) {
+  extern __shared__ double sm[];
+  double* win = sm;
+  double* tabs = sm + kWinDoubles;
+  const int2 wk = work[blockIdx.x];
+  const int l = wk.x, n = wk.y;
+  const GLv L = Lv[l];
+  const int* nb27 = L.nbr + (long long)n * 27;
+  // level geometry (depth l + 3) with the 27 near offsets zeroed
+  const double* tab = tab_all + (long long)(l + 3) * kOff3 * kTab;
+  for (int q = threadIdx.x; q < kTabDoubles; q += kM2lThreads) {
+    const int o = q / kTab;
+    const int dx = o % kOff - 3, dy = (o / kOff) % kOff - 3, dz = o / (kOff * kOff) - 3;
+    const bool near = dx >= -1 && dx <= 1 && dy >= -1 && dy <= 1 && dz >= -1 && dz <= 1;
+    tabs[q] = near ? 0.0 : tab[q];
+  }
+  for (int q = threadIdx.x; q < 1728; q += kM2lThreads) {
+    const int wx = q % 12, wy = (q / 12) % 12, wz = q / 144;
+    int lx = wx - 2, ly = wy - 2, lz = wz - 2;
+    const int ox = lx < 0 ? -1 : (lx > 7 ? 1 : 0), oy = ly < 0 ? -1 : (ly > 7 ? 1 : 0),
+              oz = lz < 0 ? -1 : (lz > 7 ? 1 : 0);
+    lx -= 8 * ox, ly -= 8 * oy, lz -= 8 * oz;
+    const int nb = nb27[((oz + 1) * 3 + (oy + 1)) * 3 + ox + 1];
+    double v[10];
+    if (nb >= 0) {
+      const double2* s2p = reinterpret_cast<const double2*>(
+          L.mom + ((long long)nb * 512 + (lz * 8 + ly) * 8 + lx) * 10);
+#pragma unroll
+      for (int h = 0; h < 5; ++h) {
+        const double2 t = s2p[h];
+        v[2 * h] = t.x;
+        v[2 * h + 1] = t.y;
+      }
+    } else {
+#pragma unroll
+      for (int h = 0; h < 10; ++h) v[h] = 0.0;
+    }
+    const int w = ((wz & 1) * 2 + (wy & 1)) * kWSub + (wz >> 1) * kWPZ + (wy >> 1) * kWPY + wx;
+    win[w] = -v[0];
+#pragma unroll
+    for (int h = 1; h < 4; ++h) win[h * kWVar + w] = v[h];
+#pragma unroll
+    for (int h = 4; h < 10; ++h) win[h * kWVar + w] = -v[h];
+  }
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int b = warp & 1, c = warp >> 1;
+  const int a = lane & 1, Y = (lane >> 1) & 3, Z = lane >> 3;
+  double acc[4][10];
+#pragma unroll
+  for (int k = 0; k < 4; ++k)
+#pragma unroll
+    for (int q = 0; q < 10; ++q) acc[k][q] = 0.0;
+  // table row base of this lane's x parity: entry (dx + 3) = jj + 1 - a
+  const double* tab_lane = tabs + (1 - a) * kTab;
+  for (int iz = 0; iz < 6; ++iz) {
+    const int dz = iz - 2 - c;
+    for (int iy = 0; iy < 6; ++iy) {
+      const int dy = iy - 2 - b;
+      const double* trow = tab_lane + ((dz + 3) * kOff + (dy + 3)) * kOff * kTab;
+      double G[6][kTab];
+#pragma unroll
+      for (int jj = 0; jj < 6; ++jj)
+#pragma unroll
+        for (int q = 0; q < kTab; ++q) G[jj][q] = trow[jj * kTab + q];
+      // source row: window y = 2Y + iy, z = 2Z + iz (parent-aligned, parity-free)
+      const double* src = win + ((iz & 1) * 2 + (iy & 1)) * kWSub + (Z + (iz >> 1)) * kWPZ +
+                          (Y + (iy >> 1)) * kWPY;
+      if (dz >= -1 && dz <= 1 && dy >= -1 && dy <= 1)
+        m2l_row<true>(src, G, acc);
+      else
+        m2l_row<false>(src, G, acc);
+    }
+  }
+  const int y = 2 * Y + b, z = 2 * Z + c, d = l + 3;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int x = a + 2 * k;
+    const long long flat = (long long)n * 512 + (z * 8 + y) * 8 + x;
+    const long long e0 = L.moff[flat], e1 = L.moff[flat + 1];
+    if (e0 < e1) {  // W/X pairs (AMR level jumps), sorted by source
+      const double cx = centre(8LL * L.ijk[3 * n] + x, d), cy = centre(8LL * L.ijk[3 * n + 1] + y, d),
+                   cz = centre(8LL * L.ijk[3 * n + 2] + z, d);
+      for (long long e = e0; e < e1; ++e) {
+        const long long enc = L.ment[e];
+        const int sl = (int)(enc >> 40);
+        const long long sf = enc & ((1LL << 40) - 1);
+        const GLv S = Lv[sl];
+        const long long sn = sf >> 9;
+        const int sc = (int)(sf & 511);
+        const int sd = sl + 3;
+        const double sx = centre(8LL * S.ijk[3 * sn] + (sc & 7), sd),
+                     sy = centre(8LL * S.ijk[3 * sn + 1] + ((sc >> 3) & 7), sd),
+                     sz = centre(8LL * S.ijk[3 * sn + 2] + (sc >> 6), sd);
+        m2l_direct(S.mom + sf * 10, cx - sx, cy - sy, cz - sz, acc[k]);
+      }
+    }
+    double2* out = reinterpret_cast<double2*>(L.loc + flat * 10);
+#pragma unroll
+    for (int h = 0; h < 5; ++h) out[h] = make_double2(acc[k][2 * h], acc[k][2 * h + 1]);
+  }
+}
+
+__global__ void amr_l2l_kernel(const GLv* __restrict__ Lv, int l, long long nnodes,
+                               const int* __restrict__ nodes) {
   const GLv L = Lv[l], P = Lv[l - 1];
   const double h = 1.0 / (double)(1LL << (l + 3));
-  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < nnodes * 512;
-       t += (long long)gridDim.x * blockDim.x) {
-    const long long n = t >> 9;
-    const int c = (int)(t & 511);
+  for (long long tt = blockIdx.x * (long long)blockDim.x + threadIdx.x; tt < nnodes * 512;
+       tt += (long long)gridDim.x * blockDim.x) {
+    const long long n = nodes ? nodes[tt >> 9] : tt >> 9;
+    const int c = (int)(tt & 511);
+    const long long t = n * 512 + c;
     const int i = c & 7, j = (c >> 3) & 7, k = c >> 6;
     const int pn = L.parent[n];
     const int pi = (L.ijk[3 * n] & 1) * 4 + (i >> 1), pj = (L.ijk[3 * n + 1] & 1) * 4 + (j >> 1),
@@ -244,13 +400,13 @@ __global__ void amr_l2l_kernel(const GLv* __restrict__ Lv, int l, long long nnod
 
 // L2P + P2P at the leaf cells, output by canonical slot: phi[s*512 + c],
 // g[q*ncell + s*512 + c]
-__global__ void amr_l2p_kernel(const GLv* __restrict__ Lv, long long nslots,
+__global__ void amr_l2p_kernel(const GLv* __restrict__ Lv, long long nslots, long long lo,
                                const int* __restrict__ slot_level, const int* __restrict__ slot_node,
                                double* __restrict__ phi, double* __restrict__ g) {
-  const long long ncell = nslots * 512;
+  const long long ncell = nslots * 512;  // outputs by local slot (canonical slot lo + s)
   for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < ncell;
        t += (long long)gridDim.x * blockDim.x) {
-    const long long s = t >> 9;
+    const long long s = lo + (t >> 9);
     const int c = (int)(t & 511);
     const int i = c & 7, j = (c >> 3) & 7, k = c >> 6;
     const int l = slot_level[s], n = slot_node[s];
@@ -271,15 +427,13 @@ __global__ void amr_l2p_kernel(const GLv* __restrict__ Lv, long long nslots,
           lx -= 8 * ox, ly -= 8 * oy, lz -= 8 * oz;
           const int nb = nb27[((oz + 1) * 3 + (oy + 1)) * 3 + ox + 1];
           if (nb < 0 || L.leaf_slot[nb] < 0) continue;
-          const double ms = L.mom[((long long)nb * 512 + (lz * 8 + ly) * 8 + lx) * 10];
-          const double Rx = -(double)dx * h, Ry = -(double)dy * h, Rz = -(double)dz * h;
-          const double r2 = Rx * Rx + Ry * Ry + Rz * Rz;
-          const double ir = 1.0 / sqrt(r2);
-          const double ir3 = ir * ir * ir;
-          p -= ms * ir;
-          gx -= ms * Rx * ir3;
-          gy -= ms * Ry * ir3;
-          gz -= ms * Rz * ir3;
+          const double nm = -L.mom[((long long)nb * 512 + (lz * 8 + ly) * 8 + lx) * 10];
+          double w[4];
+          p2p_geom(-(double)dx * h, -(double)dy * h, -(double)dz * h, w);
+          p = fma(nm, w[0], p);
+          gx = fma(nm, w[1], gx);
+          gy = fma(nm, w[2], gy);
+          gz = fma(nm, w[3], gz);
         }
     const long long e0 = L.poff[flat], e1 = L.poff[flat + 1];
     if (e0 < e1) {
@@ -293,17 +447,15 @@ __global__ void amr_l2p_kernel(const GLv* __restrict__ Lv, long long nslots,
         const long long sn = sf >> 9;
         const int sc = (int)(sf & 511);
         const int sd = sl + 3;
-        const double ms = S.mom[sf * 10];
-        const double Rx = cx - centre(8LL * S.ijk[3 * sn] + (sc & 7), sd),
-                     Ry = cy - centre(8LL * S.ijk[3 * sn + 1] + ((sc >> 3) & 7), sd),
-                     Rz = cz - centre(8LL * S.ijk[3 * sn + 2] + (sc >> 6), sd);
-        const double r2 = Rx * Rx + Ry * Ry + Rz * Rz;
-        const double ir = 1.0 / sqrt(r2);
-        const double ir3 = ir * ir * ir;
-        p -= ms * ir;
-        gx -= ms * Rx * ir3;
-        gy -= ms * Ry * ir3;
-        gz -= ms * Rz * ir3;
+        const double nm = -S.mom[sf * 10];
+        double w[4];
+        p2p_geom(cx - centre(8LL * S.ijk[3 * sn] + (sc & 7), sd),
+                 cy - centre(8LL * S.ijk[3 * sn + 1] + ((sc >> 3) & 7), sd),
+                 cz - centre(8LL * S.ijk[3 * sn + 2] + (sc >> 6), sd), w);
+        p = fma(nm, w[0], p);
+        gx = fma(nm, w[1], gx);
+        gy = fma(nm, w[2], gy);
+        gz = fma(nm, w[3], gz);
       }
     }
     phi[t] = p;
@@ -324,19 +476,21 @@ __device__ __forceinline__ void cell_pos(const GLv* __restrict__ Lv, int l, int 
 }
 
 // one CTA (512 threads) per slot: adjacent-pair tree over its 512 cells
+// block b = local slot b (canonical slot lo + b): g local [3][nslots*512]
 __global__ void __launch_bounds__(512) am_slot_kernel(const GLv* __restrict__ Lv, long long nslots,
+                                                      long long lo,
                                                       const int* __restrict__ slot_level,
                                                       const int* __restrict__ slot_node,
                                                       const double* __restrict__ mass,
                                                       const double* __restrict__ g,
                                                       double* __restrict__ part) {
   __shared__ double red[16][16];  // [warp][value]
-  const long long s = blockIdx.x;
+  const long long s = lo + blockIdx.x;
   const int c = threadIdx.x;
-  const long long ncell = nslots * 512, t = s * 512 + c;
+  const long long ncell = nslots * 512, t = (long long)blockIdx.x * 512 + c;
   double x[3];
   cell_pos(Lv, slot_level[s], slot_node[s], c, x);
-  const double m = mass[t], gx = g[t], gy = g[ncell + t], gz = g[2 * ncell + t];
+  const double m = mass[s * 512 + c], gx = g[t], gy = g[ncell + t], gz = g[2 * ncell + t];
   double v[16];
   v[0] = m;
   v[1] = m * x[0];
@@ -432,14 +586,14 @@ __global__ void am_solve_kernel(const double* __restrict__ part, double* __restr
   for (int q = 0; q < 16; ++q) rw[6 + q] = S[q];
 }
 
-__global__ void am_apply_kernel(const GLv* __restrict__ Lv, long long nslots,
+__global__ void am_apply_kernel(const GLv* __restrict__ Lv, long long nslots, long long lo,
                                 const int* __restrict__ slot_level, const int* __restrict__ slot_node,
                                 const double* __restrict__ rw, double* __restrict__ g) {
   const long long ncell = nslots * 512;
   const double R0 = rw[0], R1 = rw[1], R2 = rw[2], w0 = rw[3], w1 = rw[4], w2 = rw[5];
   for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < ncell;
        t += (long long)gridDim.x * blockDim.x) {
-    const long long s = t >> 9;
+    const long long s = lo + (t >> 9);
     double x[3];
     cell_pos(Lv, slot_level[s], slot_node[s], (int)(t & 511), x);
     const double dx = x[0] - R0, dy = x[1] - R1, dz = x[2] - R2;
@@ -460,8 +614,63 @@ cudaError_t upload(const std::vector<T>& v, T** out) {
 
 }  // namespace
 
+// Algorithmic work of one solve (bench roofline): interactions with an
+// existing source, counted per neighbour-patch offset from the plan.
+void count_work(const GravPlan& P, long long out[5]) {
+  long long vtab[27] = {0}, ptab[27] = {0};
+  for (int c = 0; c < 512; ++c) {
+    const int i = c & 7, j = (c >> 3) & 7, k = c >> 6;
+    for (int dz = -2 - (k & 1); dz <= 3 - (k & 1); ++dz)
+      for (int dy = -2 - (j & 1); dy <= 3 - (j & 1); ++dy)
+        for (int dx = -2 - (i & 1); dx <= 3 - (i & 1); ++dx) {
+          const bool near = dx >= -1 && dx <= 1 && dy >= -1 && dy <= 1 && dz >= -1 && dz <= 1;
+          const int ox = (i + dx + 8) / 8 - 1, oy = (j + dy + 8) / 8 - 1, oz = (k + dz + 8) / 8 - 1;
+          const int o = ((oz + 1) * 3 + (oy + 1)) * 3 + ox + 1;
+          if (!near) ++vtab[o];
+          else if (dx || dy || dz) ++ptab[o];
+        }
+  }
+  long long v = 0, vk = 0, p = 0;
+  for (const GravLevel& L : P.lv)
+    for (int n = 0; n < L.n; ++n) {
+      vk += 512 * 189;  // the kernel's 189 offsets x 512 targets
+      for (int o = 0; o < 27; ++o) {
+        const int nb = L.nbr[(size_t)n * 27 + o];
+        if (nb < 0) continue;
+        v += vtab[o];
+        if (L.leaf_slot[n] >= 0 && L.leaf_slot[nb] >= 0) p += ptab[o];
+      }
+    }
+  // dense depth 2 (4^3 cells, every cell exists): the uniform 189-stencil
+  for (int t = 0; t < 64; ++t) {
+    const int i = t & 3, j = (t >> 2) & 3, k = t >> 4;
+    for (int dz = -2 - (k & 1); dz <= 3 - (k & 1); ++dz)
+      for (int dy = -2 - (j & 1); dy <= 3 - (j & 1); ++dy)
+        for (int dx = -2 - (i & 1); dx <= 3 - (i & 1); ++dx) {
+          if (dx >= -1 && dx <= 1 && dy >= -1 && dy <= 1 && dz >= -1 && dz <= 1) continue;
+          if (i + dx >= 0 && i + dx < 4 && j + dy >= 0 && j + dy < 4 && k + dz >= 0 && k + dz < 4) ++v;
+        }
+  }
+  out[0] = v;
+  out[1] = P.m_entries;
+  out[2] = p;
+  out[3] = P.p_entries;
+  out[4] = vk;
+}
+
+// per-phase device timing of solves (bench): events at the phase boundaries
+constexpr int kGravPhases = 5;  // up (P2M, M2M, dense), m2l, l2l, l2p, am
+struct GravTimingRec {
+  cudaEvent_t ev[kGravPhases + 1];
+};
+
 struct GravAmrWork {
   GravPlan plan;
+  long long work[5] = {0, 0, 0, 0, 0};
+  bool timing = false;
+  std::vector<GravTimingRec> pending;
+  double phase_ms[kGravPhases] = {0, 0, 0, 0, 0};
+  long long timed_solves = 0;
   std::vector<GLv> host_lv;
   std::vector<void*> allocs;
   GLv* dev_lv = nullptr;
@@ -471,13 +680,45 @@ struct GravAmrWork {
   double* dmom[3] = {nullptr, nullptr, nullptr};
   double* dloc[3] = {nullptr, nullptr, nullptr};
   double* tab = nullptr;
-  double* tab10 = nullptr;
   double* mass = nullptr;
   double* part = nullptr;   // [P][16] + rw[22]
   double* part2 = nullptr;  // [P/256 + 1][16] tree scratch
   long long nslots = 0, P = 1;
   long long nodes = 0;
+  // distributed (tmgpu_gravity_amr_distribute): this rank owns canonical
+  // slots [lo, hi); M2L/L2L run over the owned leaves' ancestors only
+  tmgpu_comm* comm = nullptr;
+  long long lo = 0, hi = 0;
+  std::vector<long long> seg_lo, seg_cnt;  // per rank (slots)
+  std::vector<int*> need;                  // per level device node list (nullptr = all)
+  std::vector<long long> nneed;
+  int2* m2l_work = nullptr;  // fused M2L launch: (level, node) per CTA
+  long long m2l_ctas = 0;
+  bool legacy_m2l = false;   // TMGPU_M2L_LEGACY=1: per-level launches (A/B)
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
 };
+
+// (level, node) list of the fused M2L launch: every needed node of every level
+static cudaError_t build_m2l_work(GravAmrWork& w, const std::vector<std::vector<int>>* need) {
+  std::vector<int2> wk;
+  for (int l = 0; l < w.plan.nlevels; ++l) {
+    if (need) {
+      for (int n : (*need)[l]) wk.push_back(make_int2(l, n));
+    } else {
+      for (int n = 0; n < w.plan.lv[l].n; ++n) wk.push_back(make_int2(l, n));
+    }
+  }
+  if (w.m2l_work) {
+    cudaFree(w.m2l_work);
+    w.allocs.erase(std::find(w.allocs.begin(), w.allocs.end(), (void*)w.m2l_work));
+    w.m2l_work = nullptr;
+  }
+  w.m2l_ctas = (long long)wk.size();
+  cudaError_t e = upload(wk, &w.m2l_work);
+  if (w.m2l_work) w.allocs.push_back(w.m2l_work);
+  return e;
+}
 
 }  // namespace tmgpu
 
@@ -491,6 +732,11 @@ extern "C" {
 
 void tmgpu_gravity_amr_destroy(tmgpu_gravity_amr* G) {
   if (!G) return;
+  for (auto& r : G->w.pending)
+    for (auto& e : r.ev) cudaEventDestroy(e);
+  if (G->w.ev_fork) cudaEventDestroy(G->w.ev_fork);
+  if (G->w.ev_join) cudaEventDestroy(G->w.ev_join);
+  if (G->w.side) cudaStreamDestroy(G->w.side);
   for (void* p : G->w.allocs)
     if (p) cudaFree(p);
   delete G;
@@ -507,12 +753,17 @@ tmgpu_gravity_amr* tmgpu_gravity_amr_create(const int* leaves, long long nleaves
     return nullptr;
   }
   const GravPlan& P = w.plan;
+  count_work(P, w.work);
   w.nslots = nleaves;
+  w.hi = nleaves;
   while (w.P < nleaves) w.P <<= 1;
   cudaError_t e = cudaSuccess;
   auto track = [&](void* p) { w.allocs.push_back(p); };
   w.host_lv.resize(P.nlevels);
   w.internal.assign(P.nlevels, nullptr);
+  w.need.assign(P.nlevels, nullptr);
+  w.nneed.assign(P.nlevels, 0);
+  for (int l = 0; l < P.nlevels; ++l) w.nneed[l] = P.lv[l].n;
   for (int l = 0; l < P.nlevels && e == cudaSuccess; ++l) {
     const GravLevel& L = P.lv[l];
     GLv& g = w.host_lv[l];
@@ -557,17 +808,26 @@ tmgpu_gravity_amr* tmgpu_gravity_amr_create(const int* leaves, long long nleaves
   }
   const int Dmax = P.nlevels - 1 + 3;
   if (e == cudaSuccess) e = cudaMalloc(&w.tab, (size_t)(Dmax + 1) * kOff3 * kTab * sizeof(double)), track(w.tab);
-  if (e == cudaSuccess) e = cudaMalloc(&w.tab10, (size_t)(Dmax + 1) * kOff3 * kTab10 * sizeof(double)), track(w.tab10);
   if (e == cudaSuccess) e = cudaMalloc(&w.mass, (size_t)w.nslots * 512 * sizeof(double)), track(w.mass);
   if (e == cudaSuccess) e = cudaMalloc(&w.part, ((size_t)w.P * 16 + 22) * sizeof(double)), track(w.part);
   if (e == cudaSuccess) e = cudaMalloc(&w.part2, ((size_t)w.P / 256 + 1) * 16 * sizeof(double)), track(w.part2);
   if (e == cudaSuccess)
     e = cudaFuncSetAttribute(amr_m2l_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)(10 * kWin * sizeof(double)));
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(amr_m2l_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)kM2lSmem);
+  if (e == cudaSuccess) e = build_m2l_work(w, nullptr);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&w.side, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&w.ev_fork, cudaEventDisableTiming);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&w.ev_join, cudaEventDisableTiming);
+  {
+    const char* env = std::getenv("TMGPU_M2L_LEGACY");
+    w.legacy_m2l = env && env[0] == '1';
+  }
   if (e == cudaSuccess) {
     stencil_table_kernel<<<((Dmax + 1) * kOff3 + 127) / 128, 128>>>(w.tab, Dmax);
-    table10_kernel<<<((Dmax + 1) * kOff3 + 127) / 128, 128>>>(w.tab, w.tab10, (Dmax + 1) * kOff3);
-    g_launches.fetch_add(2, std::memory_order_relaxed);
+    g_launches.fetch_add(1, std::memory_order_relaxed);
     e = cudaDeviceSynchronize();
   }
   if (e != cudaSuccess) {
@@ -608,7 +868,8 @@ int tmgpu_gravity_amr_mass_from_arena(tmgpu_gravity_amr* G, const double* arena,
   if (err) std::memset(err, 0, sizeof(*err));
   GravAmrWork& w = G->w;
   cudaStream_t st = as_stream(stream);
-  amr_mass_kernel<<<grid_for(w.nslots * 512), 128, 0, st>>>(arena, vars, w.nslots, w.slot_level, w.mass);
+  amr_mass_kernel<<<grid_for((w.hi - w.lo) * 512), 128, 0, st>>>(arena, vars, w.hi - w.lo, w.lo,
+                                                                 w.slot_level, w.mass);
   g_launches.fetch_add(1, std::memory_order_relaxed);
   return cuda_err(err, cudaGetLastError(), "tmgpu_gravity_amr_mass_from_arena");
 }
@@ -619,18 +880,32 @@ int tmgpu_gravity_amr_solve(tmgpu_gravity_amr* G, const double* mass, double* ph
   GravAmrWork& w = G->w;
   const GravPlan& P = w.plan;
   cudaStream_t st = as_stream(stream);
-  const long long ncell = w.nslots * 512;
+  const long long nloc = w.hi - w.lo;  // output slots (all of them on one GPU)
+  const long long ncell = w.nslots * 512, nout = nloc * 512;
   const bool host = (flags & TMGPU_HOST_PTRS) != 0;
   cudaError_t e = cudaSuccess;
+  std::string why;
   double *dphi = phi, *dg = g;
-  if (mass)
-    e = cudaMemcpyAsync(w.mass, mass, ncell * sizeof(double),
+  if (mass)  // this rank's masses (all of them on one GPU)
+    e = cudaMemcpyAsync(w.mass + w.lo * 512, mass, nout * sizeof(double),
                         host ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice, st);
   if (host && e == cudaSuccess) {
-    e = cudaMallocAsync(&dphi, ncell * sizeof(double), st);
-    if (e == cudaSuccess) e = cudaMallocAsync(&dg, 3 * ncell * sizeof(double), st);
+    e = cudaMallocAsync(&dphi, nout * sizeof(double), st);
+    if (e == cudaSuccess) e = cudaMallocAsync(&dg, 3 * nout * sizeof(double), st);
   }
-  if (e == cudaSuccess) {
+  GravTimingRec rec;
+  const bool timed = w.timing && e == cudaSuccess;
+  if (timed) {
+    for (auto& ev : rec.ev) cudaEventCreate(&ev);
+    cudaEventRecord(rec.ev[0], st);
+  }
+  int rc = TMGPU_OK;
+  if (e == cudaSuccess && w.comm) {  // every rank needs every leaf mass for the upward pass
+    std::vector<long long> off(w.seg_lo.size()), cnt(w.seg_cnt.size());
+    for (size_t r = 0; r < off.size(); ++r) off[r] = w.seg_lo[r] * 512, cnt[r] = w.seg_cnt[r] * 512;
+    rc = comm_allgatherv(w.comm, w.mass, off, cnt, st, &why);
+  }
+  if (e == cudaSuccess && rc == TMGPU_OK) {
     long long launches = 0;
     amr_p2m_kernel<<<grid_for(ncell), 128, 0, st>>>(w.mass, w.nslots, w.slot_level, w.slot_node, w.dev_lv);
     ++launches;
@@ -643,26 +918,49 @@ int tmgpu_gravity_amr_solve(tmgpu_gravity_amr* G, const double* mass, double* ph
     m2m_kernel<<<1, 128, 0, st>>>(w.host_lv[0].mom, w.dmom[2], 4, 1.0 / 8.0);
     m2m_kernel<<<1, 128, 0, st>>>(w.dmom[2], w.dmom[1], 2, 1.0 / 4.0);
     m2m_kernel<<<1, 128, 0, st>>>(w.dmom[1], w.dmom[0], 1, 1.0 / 2.0);
-    m2l_kernel<<<1, 128, 0, st>>>(w.dmom[2], w.dloc[2], 4, w.tab + 2LL * kOff3 * kTab);
+    // the dense depth-2 M2L (one small CTA) overlaps the patch M2L on a side stream
+    cudaEventRecord(w.ev_fork, st);
+    cudaStreamWaitEvent(w.side, w.ev_fork, 0);
+    m2l_kernel<<<1, 128, 0, w.side>>>(w.dmom[2], w.dloc[2], 4, w.tab + 2LL * kOff3 * kTab);
+    cudaEventRecord(w.ev_join, w.side);
     launches += 4;
-    for (int l = 0; l < P.nlevels; ++l) {
-      amr_m2l_kernel<<<(unsigned)(P.lv[l].n * 2), 256, 10 * kWin * sizeof(double), st>>>(
-          w.dev_lv, l, w.tab10 + (long long)(l + 3) * kOff3 * kTab10);
+    if (timed) cudaEventRecord(rec.ev[1], st);
+    if (w.legacy_m2l) {
+      for (int l = 0; l < P.nlevels; ++l) {
+        if (!w.nneed[l]) continue;
+        amr_m2l_kernel<<<(unsigned)(w.nneed[l] * 2), 256, 10 * kWin * sizeof(double), st>>>(
+            w.dev_lv, l, w.tab + (long long)(l + 3) * kOff3 * kTab, w.need[l]);
+        ++launches;
+      }
+    } else if (w.m2l_ctas) {
+      amr_m2l_fused_kernel<<<(unsigned)w.m2l_ctas, kM2lThreads, kM2lSmem, st>>>(w.dev_lv, w.m2l_work,
+                                                                               w.tab);
       ++launches;
     }
+    cudaStreamWaitEvent(st, w.ev_join, 0);
+    if (timed) cudaEventRecord(rec.ev[2], st);
     l2l_kernel<<<grid_for(512), 128, 0, st>>>(w.dloc[2], w.host_lv[0].loc, 8, 1.0 / 8.0);
     ++launches;
     for (int l = 1; l < P.nlevels; ++l) {
-      amr_l2l_kernel<<<grid_for((long long)P.lv[l].n * 512), 128, 0, st>>>(w.dev_lv, l, P.lv[l].n);
+      if (!w.nneed[l]) continue;
+      amr_l2l_kernel<<<grid_for(w.nneed[l] * 512), 128, 0, st>>>(w.dev_lv, l, w.nneed[l], w.need[l]);
       ++launches;
     }
-    amr_l2p_kernel<<<grid_for(ncell), 128, 0, st>>>(w.dev_lv, w.nslots, w.slot_level, w.slot_node,
-                                                    dphi, dg);
+    if (timed) cudaEventRecord(rec.ev[3], st);
+    amr_l2p_kernel<<<grid_for(nout), 128, 0, st>>>(w.dev_lv, nloc, w.lo, w.slot_level, w.slot_node,
+                                                   dphi, dg);
     ++launches;
+    if (timed) cudaEventRecord(rec.ev[4], st);
     if (flags & TMGPU_GRAV_AM) {
       e = cudaMemsetAsync(w.part, 0, (size_t)w.P * 16 * sizeof(double), st);
-      am_slot_kernel<<<(unsigned)w.nslots, 512, 0, st>>>(w.dev_lv, w.nslots, w.slot_level, w.slot_node,
-                                                         w.mass, dg, w.part);
+      if (nloc)
+        am_slot_kernel<<<(unsigned)nloc, 512, 0, st>>>(w.dev_lv, nloc, w.lo, w.slot_level, w.slot_node,
+                                                       w.mass, dg, w.part);
+      if (w.comm && e == cudaSuccess) {  // identical global pair tree on every rank
+        std::vector<long long> off(w.seg_lo.size()), cnt(w.seg_cnt.size());
+        for (size_t r = 0; r < off.size(); ++r) off[r] = w.seg_lo[r] * 16, cnt[r] = w.seg_cnt[r] * 16;
+        rc = comm_allgatherv(w.comm, w.part, off, cnt, st, &why);
+      }
       double* bufs[2] = {w.part, w.part2};
       int cur = 0;
       for (long long n = w.P; n > 1;) {
@@ -673,16 +971,20 @@ int tmgpu_gravity_amr_solve(tmgpu_gravity_amr* G, const double* mass, double* ph
         ++launches;
       }
       am_solve_kernel<<<1, 32, 0, st>>>(bufs[cur], w.part + w.P * 16);
-      am_apply_kernel<<<grid_for(ncell), 128, 0, st>>>(w.dev_lv, w.nslots, w.slot_level, w.slot_node,
-                                                       w.part + w.P * 16, dg);
+      am_apply_kernel<<<grid_for(nout), 128, 0, st>>>(w.dev_lv, nloc, w.lo, w.slot_level, w.slot_node,
+                                                      w.part + w.P * 16, dg);
       launches += 3;
     }
     g_launches.fetch_add(launches, std::memory_order_relaxed);
     if (e == cudaSuccess) e = cudaGetLastError();
   }
+  if (timed) {
+    cudaEventRecord(rec.ev[kGravPhases], st);
+    w.pending.push_back(rec);
+  }
   if (host) {
-    if (e == cudaSuccess) e = cudaMemcpyAsync(phi, dphi, ncell * sizeof(double), cudaMemcpyDeviceToHost, st);
-    if (e == cudaSuccess) e = cudaMemcpyAsync(g, dg, 3 * ncell * sizeof(double), cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(phi, dphi, nout * sizeof(double), cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(g, dg, 3 * nout * sizeof(double), cudaMemcpyDeviceToHost, st);
     if (dphi && dphi != phi) cudaFreeAsync(dphi, st);
     if (dg && dg != g) cudaFreeAsync(dg, st);
     cudaError_t e2 = cudaStreamSynchronize(st);
@@ -691,7 +993,63 @@ int tmgpu_gravity_amr_solve(tmgpu_gravity_amr* G, const double* mass, double* ph
     cudaError_t e2 = cudaStreamSynchronize(st);
     if (e == cudaSuccess) e = e2;
   }
+  if (rc != TMGPU_OK) return set_err(err, rc, why.c_str());
   return cuda_err(err, e, "tmgpu_gravity_amr_solve");
+}
+
+// Distributed solve: rank comm_rank(comm) owns canonical slots
+// [slot_bounds[r], slot_bounds[r+1]) (contiguous ranges, partition_leaves).
+// Every rank keeps the whole tree's moments (leaf masses all-gathered, then
+// the replicated upward pass); M2L and L2L run only over the ancestors of the
+// owned leaves, L2P and the AM correction's per-slot sums only over the owned
+// slots (the sums are all-gathered, so every rank reduces the identical global
+// pair tree). Outputs (phi, g) and masses are then by local slot; the result
+// equals the one-GPU solve bit for bit.
+int tmgpu_gravity_amr_distribute(tmgpu_gravity_amr* G, tmgpu_comm* comm, const long long* slot_bounds,
+                                 tmgpu_error* err) {
+  if (err) std::memset(err, 0, sizeof(*err));
+  if (!G || !comm || !slot_bounds) return set_err(err, TMGPU_ERR_INVALID, "gravity distribute: null argument");
+  GravAmrWork& w = G->w;
+  const GravPlan& P = w.plan;
+  const int R = comm_world(comm), me = comm_rank(comm);
+  if (slot_bounds[0] != 0 || slot_bounds[R] != w.nslots)
+    return set_err(err, TMGPU_ERR_INVALID, "gravity distribute: slot bounds must cover [0, nslots)");
+  for (int r = 0; r < R; ++r)
+    if (slot_bounds[r + 1] < slot_bounds[r])
+      return set_err(err, TMGPU_ERR_INVALID, "gravity distribute: slot bounds not ascending");
+  w.comm = comm;
+  w.lo = slot_bounds[me];
+  w.hi = slot_bounds[me + 1];
+  w.seg_lo.assign(slot_bounds, slot_bounds + R);
+  w.seg_cnt.resize(R);
+  for (int r = 0; r < R; ++r) w.seg_cnt[r] = slot_bounds[r + 1] - slot_bounds[r];
+  std::vector<std::vector<char>> mark(P.nlevels);
+  for (int l = 0; l < P.nlevels; ++l) mark[l].assign(P.lv[l].n, 0);
+  for (long long s = w.lo; s < w.hi; ++s) {
+    int l = P.slot_level[s], n = P.slot_node[s];
+    while (l >= 0 && n >= 0 && !mark[l][n]) {
+      mark[l][n] = 1;
+      n = P.lv[l].parent[n];
+      --l;
+    }
+  }
+  cudaError_t e = cudaSuccess;
+  std::vector<std::vector<int>> lists(P.nlevels);
+  for (int l = 0; l < P.nlevels && e == cudaSuccess; ++l) {
+    std::vector<int>& ids = lists[l];
+    for (int n = 0; n < P.lv[l].n; ++n)
+      if (mark[l][n]) ids.push_back(n);
+    if (w.need[l]) {  // an earlier distribute
+      cudaFree(w.need[l]);
+      w.allocs.erase(std::find(w.allocs.begin(), w.allocs.end(), (void*)w.need[l]));
+    }
+    w.need[l] = nullptr;
+    w.nneed[l] = (long long)ids.size();
+    e = upload(ids, &w.need[l]);
+    if (w.need[l]) w.allocs.push_back(w.need[l]);
+  }
+  if (e == cudaSuccess) e = build_m2l_work(w, &lists);
+  return cuda_err(err, e, "tmgpu_gravity_amr_distribute");
 }
 
 // AM-correction sums of the last solve with TMGPU_GRAV_AM: out[0..2] centre of
@@ -702,6 +1060,53 @@ int tmgpu_gravity_amr_am_stats(tmgpu_gravity_amr* G, double* out) {
                  cudaSuccess
              ? TMGPU_OK
              : TMGPU_ERR_CUDA;
+}
+
+// Algorithmic work of one solve: [0] V-list M2L pairs with an existing source
+// (incl. the dense depth-2 level), [1] W/X M2L entries, [2] same-depth P2P
+// pairs, [3] cross-depth U entries, [4] V-list pairs the kernel evaluates
+// (missing neighbour patches as zero moments).
+int tmgpu_gravity_amr_work(const tmgpu_gravity_amr* G, long long* out) {
+  if (!G || !out) return TMGPU_ERR_INVALID;
+  for (int q = 0; q < 5; ++q) out[q] = G->w.work[q];
+  return TMGPU_OK;
+}
+
+// Per-phase device timing (CUDA events on the solve's stream): on != 0 starts
+// recording (and clears the totals); tmgpu_gravity_amr_timing syncs on the
+// recorded events and returns ms totals [up, m2l, l2l, l2p, am] and the count.
+int tmgpu_gravity_amr_set_timing(tmgpu_gravity_amr* G, int on) {
+  if (!G) return TMGPU_ERR_INVALID;
+  GravAmrWork& w = G->w;
+  w.timing = on != 0;
+  if (on) {
+    for (auto& r : w.pending)
+      for (auto& e : r.ev) cudaEventDestroy(e);
+    w.pending.clear();
+    for (double& x : w.phase_ms) x = 0.0;
+    w.timed_solves = 0;
+  }
+  return TMGPU_OK;
+}
+
+int tmgpu_gravity_amr_timing(tmgpu_gravity_amr* G, double* ms, long long* solves) {
+  if (!G) return TMGPU_ERR_INVALID;
+  GravAmrWork& w = G->w;
+  for (auto& r : w.pending) {
+    if (cudaEventSynchronize(r.ev[kGravPhases]) != cudaSuccess) return TMGPU_ERR_CUDA;
+    for (int q = 0; q < kGravPhases; ++q) {
+      float t = 0.f;
+      cudaEventElapsedTime(&t, r.ev[q], r.ev[q + 1]);
+      w.phase_ms[q] += t;
+    }
+    for (auto& e : r.ev) cudaEventDestroy(e);
+    ++w.timed_solves;
+  }
+  w.pending.clear();
+  if (ms)
+    for (int q = 0; q < kGravPhases; ++q) ms[q] = w.phase_ms[q];
+  if (solves) *solves = w.timed_solves;
+  return TMGPU_OK;
 }
 
 // Leaf-cell masses currently in the workspace ([slot][512], device pointer).

@@ -13,10 +13,30 @@ __device__ __forceinline__ int s2(int i, int j) {
 }
 
 // The stencil approach: on a uniform level R depends only on
-// the integer offset, so 1/r, D1 and D2 of each of the 7^3 offsets are
-// computed once per level (with m2l's exact operations) and the per-pair M2L
-// reduces to contractions. Table entry: [ir, d1[3], d2[3][3]] = 13 doubles.
+// the integer offset, so the geometry of each of the 7^3 offsets is computed
+// once per level (tmo_grav_geom's exact operations) and the per-pair M2L
+// reduces to the 28-FMA contraction. Entry: [ir, D1 x y z, D2 xx xy xz yy yz
+// zz, D2/2 xx yy zz] = 13 doubles.
 constexpr int kOff = 7, kOff3 = 343, kTab = 13;
+
+__device__ __forceinline__ void m2l_geom(double x, double y, double z, double* __restrict__ e) {
+  const double r2 = x * x + y * y + z * z;
+  const double r = sqrt(r2);
+  const double ir = 1.0 / r;
+  const double ir2 = ir * ir;
+  const double ir3 = ir * ir2, ir5 = ir3 * ir2;
+  const double R[3] = {x, y, z};
+  e[0] = ir;
+#pragma unroll
+  for (int i = 0; i < 3; ++i) e[1 + i] = -R[i] * ir3;
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int j = i; j < 3; ++j) e[4 + s2(i, j)] = 3.0 * R[i] * R[j] * ir5 - (i == j ? ir3 : 0.0);
+  e[10] = 0.5 * e[4];
+  e[11] = 0.5 * e[7];
+  e[12] = 0.5 * e[9];
+}
 
 __global__ void stencil_table_kernel(double* __restrict__ tab, int D) {
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
@@ -29,139 +49,62 @@ __global__ void stencil_table_kernel(double* __restrict__ tab, int D) {
     return;
   }
   const double h = 1.0 / (double)(1LL << l);
-  const double R[3] = {-(double)dx * h, -(double)dy * h, -(double)dz * h};
-  const double x = R[0], y = R[1], z = R[2];
-  const double r2 = x * x + y * y + z * z;
-  const double r = sqrt(r2);
-  const double ir = 1.0 / r;
-  const double ir2 = ir * ir;
-  const double ir3 = ir * ir2, ir5 = ir3 * ir2;
-  e[0] = ir;
-  for (int i = 0; i < 3; ++i) e[1 + i] = -R[i] * ir3;
-  for (int i = 0; i < 3; ++i)
-    for (int j = 0; j < 3; ++j) e[4 + 3 * i + j] = 3.0 * R[i] * R[j] * ir5 - (i == j ? ir3 : 0.0);
+  m2l_geom(-(double)dx * h, -(double)dy * h, -(double)dz * h, e);
 }
 
-// m2l with the offset's precomputed geometry: identical arithmetic to m2l()
-__device__ __forceinline__ void m2l_tab(const double* __restrict__ mom,
-                                        const double* __restrict__ e, double out[10]) {
-  const double ir = e[0];
-  double d1[3], d2[3][3];
+// One M2L term with known geometry: the fixed 28-FMA chain of
+// tmo_grav_m2l_geom. nM = -M and nQ = -Q (negation is exact, and fma(-a, b, c)
+// is the same correctly rounded operation either way).
+__device__ __forceinline__ void m2l_acc(double nM, double Dx, double Dy, double Dz, double nQxx,
+                                        double nQxy, double nQxz, double nQyy, double nQyz,
+                                        double nQzz, const double* __restrict__ e, double out[10]) {
+  double o = out[0];
+  o = fma(nM, e[0], o);
+  o = fma(Dx, e[1], o);
+  o = fma(Dy, e[2], o);
+  o = fma(Dz, e[3], o);
+  o = fma(nQxx, e[10], o);
+  o = fma(nQxy, e[5], o);
+  o = fma(nQxz, e[6], o);
+  o = fma(nQyy, e[11], o);
+  o = fma(nQyz, e[8], o);
+  o = fma(nQzz, e[12], o);
+  out[0] = o;
+  // D2 rows: x (xx xy xz) = e4 e5 e6, y (xy yy yz) = e5 e7 e8, z (xz yz zz) = e6 e8 e9
+  out[1] = fma(Dz, e[6], fma(Dy, e[5], fma(Dx, e[4], fma(nM, e[1], out[1]))));
+  out[2] = fma(Dz, e[8], fma(Dy, e[7], fma(Dx, e[5], fma(nM, e[2], out[2]))));
+  out[3] = fma(Dz, e[9], fma(Dy, e[8], fma(Dx, e[6], fma(nM, e[3], out[3]))));
 #pragma unroll
-  for (int i = 0; i < 3; ++i) d1[i] = e[1 + i];
-#pragma unroll
-  for (int i = 0; i < 3; ++i)
-#pragma unroll
-    for (int j = 0; j < 3; ++j) d2[i][j] = e[4 + 3 * i + j];
-  const double M = mom[0];
-  const double Dp[3] = {mom[1], mom[2], mom[3]};
-  double Q[3][3];
-#pragma unroll
-  for (int i = 0; i < 3; ++i)
-#pragma unroll
-    for (int j = 0; j < 3; ++j) Q[i][j] = mom[4 + s2(i, j)];
-  double a = M * ir, b = 0.0, c = 0.0;
-#pragma unroll
-  for (int i = 0; i < 3; ++i) b += Dp[i] * d1[i];
-#pragma unroll
-  for (int i = 0; i < 3; ++i)
-#pragma unroll
-    for (int j = 0; j < 3; ++j) c += Q[i][j] * d2[i][j];
-  out[0] += -(a - b + 0.5 * c);
-#pragma unroll
-  for (int i = 0; i < 3; ++i) {
-    double bb = 0.0;
-#pragma unroll
-    for (int j = 0; j < 3; ++j) bb += Dp[j] * d2[i][j];
-    out[1 + i] += -(M * d1[i] - bb);
-  }
-#pragma unroll
-  for (int i = 0; i < 3; ++i)
-#pragma unroll
-    for (int j = i; j < 3; ++j) out[4 + s2(i, j)] += -(M * d2[i][j]);
+  for (int q = 0; q < 6; ++q) out[4 + q] = fma(nM, e[4 + q], out[4 + q]);
 }
 
-// Same arithmetic as m2l_tab with the symmetric 10-entry geometry
-// [ir, d1[3], d2 xx xy xz yy yz zz]: on lattice offsets 3*R_i*R_j is exact, so
-// d2 is exactly symmetric and the 13-entry table's values are reproduced.
-constexpr int kTab10 = 10;
-
-__device__ __forceinline__ void m2l_tab10(const double* __restrict__ mom,
-                                          const double* __restrict__ e, double out[10]) {
-  const double ir = e[0];
-  double d1[3], d2[3][3];
-#pragma unroll
-  for (int i = 0; i < 3; ++i) d1[i] = e[1 + i];
-#pragma unroll
-  for (int i = 0; i < 3; ++i)
-#pragma unroll
-    for (int j = 0; j < 3; ++j) d2[i][j] = e[4 + s2(i, j)];
-  const double M = mom[0];
-  const double Dp[3] = {mom[1], mom[2], mom[3]};
-  double Q[3][3];
-#pragma unroll
-  for (int i = 0; i < 3; ++i)
-#pragma unroll
-    for (int j = 0; j < 3; ++j) Q[i][j] = mom[4 + s2(i, j)];
-  double a = M * ir, b = 0.0, c = 0.0;
-#pragma unroll
-  for (int i = 0; i < 3; ++i) b += Dp[i] * d1[i];
-#pragma unroll
-  for (int i = 0; i < 3; ++i)
-#pragma unroll
-    for (int j = 0; j < 3; ++j) c += Q[i][j] * d2[i][j];
-  out[0] += -(a - b + 0.5 * c);
-#pragma unroll
-  for (int i = 0; i < 3; ++i) {
-    double bb = 0.0;
-#pragma unroll
-    for (int j = 0; j < 3; ++j) bb += Dp[j] * d2[i][j];
-    out[1 + i] += -(M * d1[i] - bb);
-  }
-#pragma unroll
-  for (int i = 0; i < 3; ++i)
-#pragma unroll
-    for (int j = i; j < 3; ++j) out[4 + s2(i, j)] += -(M * d2[i][j]);
+__device__ __forceinline__ void m2l_tab(const double* __restrict__ mom, const double* __restrict__ e,
+                                        double out[10]) {
+  m2l_acc(-mom[0], mom[1], mom[2], mom[3], -mom[4], -mom[5], -mom[6], -mom[7], -mom[8], -mom[9], e,
+          out);
 }
 
-// 13-entry table -> 10-entry symmetric table (per level: kOff3 entries)
-__global__ void table10_kernel(const double* __restrict__ t13, double* __restrict__ t10, int n) {
-  const int t = blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= n) return;
-  const double* e = t13 + (long long)t * kTab;
-  double* o = t10 + (long long)t * kTab10;
-  for (int q = 0; q < 4; ++q) o[q] = e[q];
-  o[4] = e[4];
-  o[5] = e[5];
-  o[6] = e[6];
-  o[7] = e[8];
-  o[8] = e[9];
-  o[9] = e[12];
+// P2P geometry (tmo_grav_p2p_geom): w = [1/r, R/r^3]
+__device__ __forceinline__ void p2p_geom(double Rx, double Ry, double Rz, double w[4]) {
+  const double r2 = Rx * Rx + Ry * Ry + Rz * Rz;
+  const double ir = 1.0 / sqrt(r2);
+  const double ir3 = ir * ir * ir;
+  w[0] = ir;
+  w[1] = Rx * ir3;
+  w[2] = Ry * ir3;
+  w[3] = Rz * ir3;
 }
 
 __device__ __forceinline__ long long cidx(long long n, long long i, long long j, long long k) {
   return (k * n + j) * n + i;
 }
 
-// m2l with the geometry computed from R, operation for operation as
-// tmo_grav_m2l (used for the AMR W/X list pairs, whose offsets are not on the
-// same-level stencil)
+// M2L with the geometry computed from R (tmo_grav_m2l), for the AMR W/X list
+// pairs, whose offsets are not on the same-level stencil
 __device__ __forceinline__ void m2l_direct(const double* __restrict__ mom, double x, double y,
                                            double z, double out[10]) {
-  const double r2 = x * x + y * y + z * z;
-  const double r = sqrt(r2);
-  const double ir = 1.0 / r;
-  const double ir2 = ir * ir;
-  const double ir3 = ir * ir2, ir5 = ir3 * ir2;
-  const double R[3] = {x, y, z};
   double e[kTab];
-  e[0] = ir;
-#pragma unroll
-  for (int i = 0; i < 3; ++i) e[1 + i] = -R[i] * ir3;
-#pragma unroll
-  for (int i = 0; i < 3; ++i)
-#pragma unroll
-    for (int j = 0; j < 3; ++j) e[4 + 3 * i + j] = 3.0 * R[i] * R[j] * ir5 - (i == j ? ir3 : 0.0);
+  m2l_geom(x, y, z, e);
   m2l_tab(mom, e, out);
 }
 

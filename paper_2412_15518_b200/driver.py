@@ -9,9 +9,11 @@ from __future__ import annotations
 
 import ctypes as C
 
+import numpy as np
+
 from . import _lib
 from ._lib import TmgpuError, lib
-from .amr import Forest
+from .amr import Forest, unpack
 from .hydro import SolverError
 
 
@@ -55,19 +57,27 @@ class GravityHydroDriver(HydroDriver):
     the reference has no gravity) on the step's initial state, with
     the angular-momentum correction, held fixed over the three RK stages as the
     stage kernel's source term (m += dt*rho*g, E += dt*rho*(v.g); oracle
-    tmo_stage_subgrid_grav)."""
+    tmo_stage_subgrid_grav).
+
+    On a distributed forest (Forest.distribute) the solve is distributed the
+    same way: leaf masses all-gathered over NCCL, M2L/L2L/L2P on the ancestors
+    of the owned leaves (GravityAMR.distribute); bitwise equal to one GPU."""
 
     def __init__(self, forest: Forest, gamma: float = 1.4, cfl: float = 0.4, fast: bool = False,
                  exact_ghosts: bool = False, am: bool = True):
         super().__init__(forest, gamma, cfl, fast, exact_ghosts)
         import torch
 
-        from .gravity import GravityAMR, forest_leaf_array
+        from .gravity import GravityAMR
 
-        if forest.local_count() != forest.leaf_count():
-            raise NotImplementedError("gravity on a distributed forest: use DistGravityHydroDriver")
         self.am = am
-        self.gravity = GravityAMR(forest_leaf_array(forest))
+        leaves = np.array([unpack(int(p)) for p in forest.leaves()], dtype=np.int32).reshape(-1, 4)
+        self.gravity = GravityAMR(leaves)
+        comm = getattr(forest, "_comm", None)
+        if forest.local_count() != forest.leaf_count():
+            if comm is None:
+                raise ValueError("distributed forest without a communicator")
+            self.gravity.distribute(comm, forest._owner)
         n = forest.local_count() * 512
         self.phi = torch.empty(n, dtype=torch.float64, device="cuda")
         self.g = torch.zeros(3 * n, dtype=torch.float64, device="cuda")

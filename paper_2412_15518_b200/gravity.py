@@ -107,6 +107,14 @@ lib.tmgpu_gravity_amr_solve.restype = C.c_int
 lib.tmgpu_gravity_amr_solve.argtypes = [_vp, _vp, _vp, _vp, C.c_int, _vp, _ep]
 lib.tmgpu_gravity_amr_am_stats.restype = C.c_int
 lib.tmgpu_gravity_amr_am_stats.argtypes = [_vp, C.POINTER(C.c_double)]
+lib.tmgpu_gravity_amr_work.restype = C.c_int
+lib.tmgpu_gravity_amr_work.argtypes = [_vp, _lp]
+lib.tmgpu_gravity_amr_set_timing.restype = C.c_int
+lib.tmgpu_gravity_amr_set_timing.argtypes = [_vp, C.c_int]
+lib.tmgpu_gravity_amr_timing.restype = C.c_int
+lib.tmgpu_gravity_amr_timing.argtypes = [_vp, C.POINTER(C.c_double), _lp]
+lib.tmgpu_gravity_amr_distribute.restype = C.c_int
+lib.tmgpu_gravity_amr_distribute.argtypes = [_vp, _vp, _lp, _ep]
 lib.tmgpu_gravity_amr_mass_ptr.restype = _vp
 lib.tmgpu_gravity_amr_mass_ptr.argtypes = [_vp]
 
@@ -163,7 +171,7 @@ class GravityAMR:
         (device path: workspace masses when None; phi, g device tensors)."""
         flags = GRAV_AM if am else 0
         err = TmgpuError()
-        ncell = self.n * 512
+        ncell = self.local_cells()
         if isinstance(mass, np.ndarray):
             m = np.ascontiguousarray(mass, dtype=np.float64).reshape(-1)
             if m.size != ncell:
@@ -191,6 +199,46 @@ class GravityAMR:
         err = TmgpuError()
         _lib.check(lib.tmgpu_gravity_amr_mass_from_arena(self.h, forest.arena_ptr(), forest.vars,
                                                          stream, C.byref(err)), err)
+
+    def distribute(self, comm, owner) -> None:
+        """Multi-GPU solve: this rank owns the canonical slots with
+        owner[s] == comm.rank (contiguous ranges, partition_leaves). Masses
+        (mass_from_arena / solve) and outputs become by local slot; the result
+        equals the one-GPU solve bit for bit (csrc/gravity_amr.cu)."""
+        o = np.asarray(owner)
+        if len(o) != self.n:
+            raise ValueError("owner must have one entry per leaf")
+        if np.any(np.diff(o) < 0):
+            raise ValueError("owner ranges must be contiguous and ascending")
+        bounds = np.searchsorted(o, np.arange(comm.world + 1), side="left").astype(np.int64)
+        bounds[-1] = self.n
+        self._comm = comm
+        self.lo, self.hi = int(bounds[comm.rank]), int(bounds[comm.rank + 1])
+        err = TmgpuError()
+        _lib.check(lib.tmgpu_gravity_amr_distribute(self.h, comm.h, bounds.ctypes.data_as(_lp),
+                                                    C.byref(err)), err)
+
+    def local_cells(self) -> int:
+        return (getattr(self, "hi", self.n) - getattr(self, "lo", 0)) * 512
+
+    def work(self):
+        """Algorithmic work of one solve: dict of interaction counts."""
+        out = (C.c_longlong * 5)()
+        lib.tmgpu_gravity_amr_work(self.h, out)
+        return {"v_pairs": out[0], "wx_entries": out[1], "p2p_pairs": out[2],
+                "u_cross_entries": out[3], "v_pairs_evaluated": out[4]}
+
+    def set_timing(self, on: bool) -> None:
+        lib.tmgpu_gravity_amr_set_timing(self.h, int(on))
+
+    PHASES = ("up", "m2l", "l2l", "l2p", "am")
+
+    def timing(self):
+        """(ms totals per phase, solves timed) since set_timing(True)."""
+        ms = (C.c_double * 5)()
+        n = C.c_longlong()
+        _lib.check(lib.tmgpu_gravity_amr_timing(self.h, ms, C.byref(n)), TmgpuError())
+        return dict(zip(self.PHASES, ms)), n.value
 
     def am_stats(self):
         out = (C.c_double * 22)()

@@ -1,8 +1,9 @@
 """torchrun helper for test_distributed: partitioned steps on N GPUs vs one GPU.
 
 Each rank owns a contiguous range of canonical leaves; after 3 SSP-RK3 steps
-the ranks gather their interiors on rank 0, which reruns the same steps on
-one GPU and compares bitwise."""
+(hydro, or gravity+hydro with `--gravity`: distributed FMM solve + hydro) the
+ranks gather their interiors (and the last gravity field) on rank 0, which
+reruns the same steps on one GPU and compares bitwise."""
 import os
 import sys
 
@@ -12,7 +13,7 @@ import torch.distributed as tdist
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2412_15518_b200 import amr, dist  # noqa: E402
-from paper_2412_15518_b200.driver import HydroDriver  # noqa: E402
+from paper_2412_15518_b200.driver import GravityHydroDriver, HydroDriver  # noqa: E402
 
 
 def main():
@@ -20,6 +21,9 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", rank))
     torch.cuda.set_device(local)
     tdist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    gravity = "--gravity" in sys.argv
+    args = [a for a in sys.argv[1:] if a != "--gravity"]
+    Drv = GravityHydroDriver if gravity else HydroDriver
     kind, lo, hi = amr.Scenario.rotating_star, 2, 4
     f = amr.build_scenario(kind, lo, hi)
     state = f.scenario_state(kind)
@@ -29,28 +33,38 @@ def main():
     f.alloc()
     a, b = dist.local_range(owner, rank)
     f.set_interior(np.ascontiguousarray(state[a:b]))
-    drv = HydroDriver(f)
+    drv = Drv(f)
     dts = [drv.step() for _ in range(3)]
     mine = torch.from_numpy(f.get_interior()).cuda()
     sizes = [dist.local_range(owner, r)[1] - dist.local_range(owner, r)[0] for r in range(world)]
     gathered = [torch.zeros((s, 5, 512), dtype=torch.float64, device="cuda") for s in sizes]
     tdist.all_gather(gathered, mine)
+    if gravity:
+        gl = [torch.zeros((3, s * 512), dtype=torch.float64, device="cuda") for s in sizes]
+        tdist.all_gather(gl, drv.g.view(3, -1).contiguous())
     if rank == 0:
         multi = torch.cat(gathered).cpu().numpy()
         g = amr.build_scenario(kind, lo, hi)
         g.alloc()
         g.set_interior(state)
-        d1 = HydroDriver(g)
+        d1 = Drv(g)
         dts1 = [d1.step() for _ in range(3)]
         single = g.get_interior()
         assert dts == dts1, (dts, dts1)
+        if gravity:
+            gm = torch.cat(gl, dim=1).cpu().numpy()
+            gs = d1.g.view(3, -1).cpu().numpy()
+            assert gm.tobytes() == gs.tobytes(), "gravity field differs"
+            d1.close()
         if multi.tobytes() == single.tobytes():
             print("BITWISE_OK", world, f.leaf_count(), dts)
         else:
             bad = np.nonzero((multi != single).any(axis=(1, 2)))[0]
             print("MISMATCH leaves", bad[:20], len(bad))
-        if len(sys.argv) > 1:
-            np.savez(sys.argv[1], multi=multi, single=single)
+        if args:
+            np.savez(args[0], multi=multi, single=single)
+    if gravity:
+        drv.close()
     tdist.barrier()
     tdist.destroy_process_group()
 

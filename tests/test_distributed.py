@@ -83,3 +83,20 @@ def test_partitioned_step_bitwise_equals_single_gpu():
                         "29531", script, out], capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     assert "BITWISE_OK" in r.stdout, r.stdout[-3000:]
+
+
+@pytest.mark.gpu
+def test_partitioned_gravity_hydro_step_bitwise_equals_single_gpu():
+    """Distributed FMM (mass all-gather, owned-subtree M2L/L2L/L2P, all-gathered
+    AM sums) + partitioned hydro == one GPU, bitwise (state and gravity field)."""
+    import torch
+
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs 2 GPUs (gpurun --gpus 2)")
+    script = os.path.join(ROOT, "tests", "mgpu_step.py")
+    n = min(torch.cuda.device_count(), 4)
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+                        f"--nproc-per-node={n}", "--master-addr", "127.0.0.1", "--master-port",
+                        "29532", script, "--gravity"], capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    assert "BITWISE_OK" in r.stdout, r.stdout[-3000:]
