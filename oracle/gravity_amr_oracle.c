@@ -21,7 +21,8 @@
  *   P2M   leaf cells: (m, 0, 0)
  *   M2M   internal cells from their 8 children, (c, b, a) loop order
  *   V     every existing cell at depth >= 2: the 189-cell stencil of the
- *         uniform spec (dz, dy, dx ascending), skipping missing/outside cells
+ *         uniform spec (two partial sums over the lower / upper three source
+ *         planes, dz, dy, dx ascending, then added), skipping missing/outside cells
  *   W, X  for every leaf cell b (canonical leaf order, cells (k,j,i)), every
  *         internal colleague Y (same depth, max|offset| = 1, dz,dy,dx
  *         ascending) is visited: each child y (z,y,x order) adjacent to b
@@ -346,6 +347,7 @@ int tmo_grav_amr_solve_ex(long nleaves, const int* leaves, const double* mass, i
         for (long i = 0; i < m; ++i) {
           if (!dep[d].type[cix(m, i, j, k)]) continue;
           double* out = dep[d].loc + cix(m, i, j, k) * 10;
+          double part[2][10] = {{0}};  /* lower / upper three source planes */
           for (long dz = -2 - (k & 1); dz <= 3 - (k & 1); ++dz)
             for (long dy = -2 - (j & 1); dy <= 3 - (j & 1); ++dy)
               for (long dx = -2 - (i & 1); dx <= 3 - (i & 1); ++dx) {
@@ -354,8 +356,9 @@ int tmo_grav_amr_solve_ex(long nleaves, const int* leaves, const double* mass, i
                 if (si < 0 || sj < 0 || sk < 0 || si >= m || sj >= m || sk >= m) continue;
                 if (!dep[d].type[cix(m, si, sj, sk)]) continue;
                 const double R[3] = {-(double)dx * h, -(double)dy * h, -(double)dz * h};
-                m2l_k(dep[d].mom + cix(m, si, sj, sk) * 10, R, out, cnt);
+                m2l_k(dep[d].mom + cix(m, si, sj, sk) * 10, R, part[dz + (k & 1) >= 1], cnt);
               }
+          for (int q = 0; q < 10; ++q) out[q] = part[0][q] + part[1][q];
         }
   }
   /* W / X / U-cross lists */

@@ -17,7 +17,10 @@
  *   M2L      at every level l >= 2, target cell c sums over the cells c' whose
  *            parent is one of the 27 neighbours of parent(c) but with
  *            max|c - c'| >= 2 (the 189-cell interaction list), loops dz, dy, dx
- *            ascending; R = x_c - x_c'; order-2 Cartesian multipoles -> local
+ *            ascending, as two partial sums — sources in the lower three planes
+ *            (z' < 2 (z >> 1) + 1) and in the upper three — added at the end
+ *            (the GPU gives each half its own thread); R = x_c - x_c';
+ *            order-2 Cartesian multipoles -> local
  *            Taylor coefficients truncated at |alpha| + |beta| <= 2 (Dehnen):
  *              L0   = -(M/r - D_i D1_i + Q_ij D2_ij / 2)
  *              L_i  = -(M D1_i - D_j D2_ij)
@@ -25,8 +28,8 @@
  *            With this truncation the mutual M2L forces of every pair are
  *            exactly opposite, so the FMM conserves linear momentum
  *             to round-off. Arithmetic: geometry per separation
- *            (tmo_grav_geom), then a fixed chain of 28 fused multiply-adds
- *            (tmo_grav_m2l_geom) — C fma() and the GPU's DFMA are the same
+ *            (tmo_grav_geom), then a fixed sequence of 27 fused multiply-adds,
+ *            one product and one add (tmo_grav_m2l_geom) — C fma() and the GPU's DFMA are the same
  *            correctly rounded operation, so the kernels match bit for bit
  *   L2L      L(c) = shift(L(parent(c))) + M2L-sum(c) (levels 3..D)
  *   L2P+P2P  at the finest level (expansion centre = cell centre, so L2P is
@@ -65,16 +68,16 @@ void tmo_grav_geom(const double* R, double* e) {
   e[12] = 0.5 * e[9];
 }
 
-/* One M2L term with known geometry, accumulated into out (10 locals) as a
- * fixed chain of fused multiply-adds (28 per term):
- *   L0   += -M ir + D_i D1_i - (1/2) Q_ij D2_ij
- *   L_i  += -M D1_i + D_j D2_ij
- *   L_ij += -M D2_ij
+/* One M2L term with known geometry, accumulated into out (10 locals):
+ *   L0   += t,  t = -M ir + D_i D1_i - (1/2) Q_ij D2_ij, formed on its own
+ *          (one product, then a chain of 9 fused multiply-adds) and then added,
+ *          so the long L0 chain does not serialise successive terms
+ *   L_i  += -M D1_i + D_j D2_ij   (4 fused multiply-adds into L_i)
+ *   L_ij += -M D2_ij              (1 fused multiply-add)
  * (Q symmetric: (1/2) Q_ij D2_ij = sum_i Q_ii (D2_ii/2) + sum_{i<j} Q_ij D2_ij). */
 void tmo_grav_m2l_geom(const double* mom, const double* e, double* out) {
   const double nM = -mom[0];
-  double o = out[0];
-  o = fma(nM, e[0], o);
+  double o = nM * e[0];
   o = fma(mom[1], e[1], o);
   o = fma(mom[2], e[2], o);
   o = fma(mom[3], e[3], o);
@@ -84,7 +87,7 @@ void tmo_grav_m2l_geom(const double* mom, const double* e, double* out) {
   o = fma(-mom[7], e[11], o);
   o = fma(-mom[8], e[8], o);
   o = fma(-mom[9], e[12], o);
-  out[0] = o;
+  out[0] = out[0] + o;
   for (int i = 0; i < 3; ++i) {
     double t = out[1 + i];
     t = fma(nM, e[1 + i], t);
@@ -179,6 +182,7 @@ int tmo_grav_solve(int D, const double* mass, double* phi, double* g) {
       for (long j = 0; j < m; ++j)
         for (long i = 0; i < m; ++i) {
           double* out = loc[l] + cidx(m, i, j, k) * 10;
+          double part[2][10] = {{0}};
           for (long dz = -2 - (k & 1); dz <= 3 - (k & 1); ++dz)
             for (long dy = -2 - (j & 1); dy <= 3 - (j & 1); ++dy)
               for (long dx = -2 - (i & 1); dx <= 3 - (i & 1); ++dx) {
@@ -186,8 +190,9 @@ int tmo_grav_solve(int D, const double* mass, double* phi, double* g) {
                 const long si = i + dx, sj = j + dy, sk = k + dz;
                 if (si < 0 || sj < 0 || sk < 0 || si >= m || sj >= m || sk >= m) continue;
                 const double R[3] = {-(double)dx * h, -(double)dy * h, -(double)dz * h};
-                tmo_grav_m2l(mom[l] + cidx(m, si, sj, sk) * 10, R, out);
+                tmo_grav_m2l(mom[l] + cidx(m, si, sj, sk) * 10, R, part[dz + (k & 1) >= 1]);
               }
+          for (int q = 0; q < 10; ++q) out[q] = part[0][q] + part[1][q];
         }
   }
   /* L2L, levels 3..D: loc = shift(parent) + own M2L sum */

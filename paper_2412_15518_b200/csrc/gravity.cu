@@ -75,9 +75,9 @@ __global__ void __launch_bounds__(128) m2l_tiled_kernel(const double* __restrict
   __syncthreads();
   const int tx = threadIdx.x % TBX, ty = (threadIdx.x / TBX) % TBY, tz = threadIdx.x / (TBX * TBY);
   const long long i = x0 + tx, j = y0 + ty, k = z0 + tz;
-  double o[10];
+  double o[2][10];  // lower / upper three source planes (tmo_grav_solve)
 #pragma unroll
-  for (int q = 0; q < 10; ++q) o[q] = 0.0;
+  for (int q = 0; q < 10; ++q) o[0][q] = o[1][q] = 0.0;
   for (long long dz = -2 - (k & 1); dz <= 3 - (k & 1); ++dz)
     for (long long dy = -2 - (j & 1); dy <= 3 - (j & 1); ++dy)
       for (long long dx = -2 - (i & 1); dx <= 3 - (i & 1); ++dx) {
@@ -88,11 +88,12 @@ __global__ void __launch_bounds__(128) m2l_tiled_kernel(const double* __restrict
         double mom_q[10];
 #pragma unroll
         for (int c = 0; c < 10; ++c) mom_q[c] = sm[c * SB3 + q];
-        m2l_tab(mom_q, tab + (((dz + 3) * kOff + (dy + 3)) * kOff + (dx + 3)) * kTab, o);
+        m2l_tab(mom_q, tab + (((dz + 3) * kOff + (dy + 3)) * kOff + (dx + 3)) * kTab,
+                o[dz + (k & 1) >= 1]);
       }
   double* out = loc + cidx(m, i, j, k) * 10;
 #pragma unroll
-  for (int q = 0; q < 10; ++q) out[q] = o[q];
+  for (int q = 0; q < 10; ++q) out[q] = o[0][q] + o[1][q];
 }
 
 __global__ void p2p_kernel(const double* __restrict__ mass, const double* __restrict__ loc,

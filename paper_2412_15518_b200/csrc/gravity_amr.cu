@@ -47,6 +47,8 @@ struct GLv {
   const long long* ment;
   const long long* poff;
   const long long* pent;
+  const int* mgeo;  // W/X entry -> row of the W/X geometry table
+  const int* pgeo;  // cross-depth U entry -> row of the P2P geometry table
 };
 
 namespace {
@@ -122,95 +124,13 @@ __global__ void amr_m2m_kernel(const GLv* __restrict__ L, int l, const int* __re
   }
 }
 
-// M2L of one level: CTA = (patch, z-half of 8x8x4 targets), 256 threads.
-// Warp w owns the 32 targets of one parity class (a, b, c) = (w&1, w>>1&1,
-// w>>2): lane (I, J, K) -> target (2I+a, 2J+b, z0+2K+c). Every lane of a warp
-// then walks the same stencil offsets (no divergence; the tabulated geometry
-// is a warp-uniform broadcast load). The 12x12x8 source window (27-patch
-// neighbourhood, missing patches = zero moments) is stored de-interleaved by
-// parity: 8 sub-grids of 6x6x4 cells with row pitch 6 and plane pitch 40, so a
-// warp's 32 source loads of any offset hit 32 distinct banks (2 wavefronts).
-constexpr int kSubPitchY = 6, kSubPitchZ = 40, kSub = 4 * kSubPitchZ, kWin = 8 * kSub;  // 1280
-
-__device__ __forceinline__ int win_index(int wx, int wy, int wz) {
-  return ((((wz & 1) * 2 + (wy & 1)) * 2 + (wx & 1)) * kSub) + (wz >> 1) * kSubPitchZ +
-         (wy >> 1) * kSubPitchY + (wx >> 1);
-}
-
-__global__ void __launch_bounds__(256, 2) amr_m2l_kernel(const GLv* __restrict__ Lv, int l,
-                                                         const double* __restrict__ tab,
-                                                         const int* __restrict__ nodes) {
-  extern __shared__ double sm[];  // [10][kWin] doubles = 102,400 B
-  const GLv L = Lv[l];
-  const int n = nodes ? nodes[blockIdx.x >> 1] : (int)(blockIdx.x >> 1);
-  const int z0 = (blockIdx.x & 1) * 4;
-  const int* nb27 = L.nbr + (long long)n * 27;
-  for (int q = threadIdx.x; q < 12 * 12 * 8; q += blockDim.x) {
-    const int wx = q % 12, wy = (q / 12) % 12, wz = q / 144;
-    int lx = wx - 2, ly = wy - 2, lz = z0 + wz - 2;
-    const int ox = lx < 0 ? -1 : (lx > 7 ? 1 : 0), oy = ly < 0 ? -1 : (ly > 7 ? 1 : 0),
-              oz = lz < 0 ? -1 : (lz > 7 ? 1 : 0);
-    lx -= 8 * ox, ly -= 8 * oy, lz -= 8 * oz;
-    const int nb = nb27[((oz + 1) * 3 + (oy + 1)) * 3 + ox + 1];
-    const double* src = L.mom + ((long long)(nb < 0 ? 0 : nb) * 512 + (lz * 8 + ly) * 8 + lx) * 10;
-    const int w = win_index(wx, wy, wz);
-#pragma unroll
-    for (int c = 0; c < 10; ++c) sm[c * kWin + w] = nb >= 0 ? src[c] : 0.0;
-  }
-  __syncthreads();
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int a = warp & 1, b = (warp >> 1) & 1, c = warp >> 2;
-  // half-warps take J even / J odd: with the (6, 40) sub-grid pitches every
-  // half-warp's 16 doubles then fall in 16 distinct banks for every offset
-  const int I = lane & 3, K = (lane >> 2) & 1, J = ((lane >> 3) & 1) * 2 + (lane >> 4);
-  const int i = 2 * I + a, j = 2 * J + b, k = z0 + 2 * K + c;
-  const int lane_off = K * kSubPitchZ + J * kSubPitchY + I;
-  double o[10];
-#pragma unroll
-  for (int q = 0; q < 10; ++q) o[q] = 0.0;
-  for (int dz = -2 - c; dz <= 3 - c; ++dz)
-    for (int dy = -2 - b; dy <= 3 - b; ++dy)
-      for (int dx = -2 - a; dx <= 3 - a; ++dx) {
-        if (dx >= -1 && dx <= 1 && dy >= -1 && dy <= 1 && dz >= -1 && dz <= 1) continue;
-        // window coordinates of the source: (t + d) + 2 (z relative to z0)
-        const int sx = a + dx + 2, sy = b + dy + 2, sz = c + dz + 2;  // + 2*(I, J, K)
-        const int q = ((((sz & 1) * 2 + (sy & 1)) * 2 + (sx & 1)) * kSub) + (sz >> 1) * kSubPitchZ +
-                      (sy >> 1) * kSubPitchY + (sx >> 1) + lane_off;
-        double mom_q[10];
-#pragma unroll
-        for (int cc = 0; cc < 10; ++cc) mom_q[cc] = sm[cc * kWin + q];
-        m2l_tab(mom_q, tab + (((dz + 3) * kOff + (dy + 3)) * kOff + (dx + 3)) * kTab, o);
-      }
-  const long long flat = (long long)n * 512 + (k * 8 + j) * 8 + i;
-  const long long e0 = L.moff[flat], e1 = L.moff[flat + 1];
-  if (e0 < e1) {  // W/X pairs (AMR level jumps), sorted by source
-    const int d = l + 3;
-    const double cx = centre(8LL * L.ijk[3 * n] + i, d), cy = centre(8LL * L.ijk[3 * n + 1] + j, d),
-                 cz = centre(8LL * L.ijk[3 * n + 2] + k, d);
-    for (long long e = e0; e < e1; ++e) {
-      const long long enc = L.ment[e];
-      const int sl = (int)(enc >> 40);
-      const long long sf = enc & ((1LL << 40) - 1);
-      const GLv S = Lv[sl];
-      const long long sn = sf >> 9;
-      const int sc = (int)(sf & 511);
-      const int sd = sl + 3;
-      const double sx = centre(8LL * S.ijk[3 * sn] + (sc & 7), sd),
-                   sy = centre(8LL * S.ijk[3 * sn + 1] + ((sc >> 3) & 7), sd),
-                   sz = centre(8LL * S.ijk[3 * sn + 2] + (sc >> 6), sd);
-      m2l_direct(S.mom + sf * 10, cx - sx, cy - sy, cz - sz, o);
-    }
-  }
-  double* out = L.loc + flat * 10;
-#pragma unroll
-  for (int q = 0; q < 10; ++q) out[q] = o[q];
-}
-
 // ---- M2L, all levels in one launch -----------------------------------------
-// CTA = one patch (8^3 targets), 128 threads, one CTA per SM (197 KB smem).
-// Warp w = target parity class (b, c) = (w & 1, w >> 1) in y, z; lane =
-// (a, Y, Z) = (lane & 1, lane >> 1 & 3, lane >> 3): the thread owns the four
-// targets x = a + 2k (k = 0..3), y = 2Y + b, z = 2Z + c. All 8 siblings of a
+// CTA = one patch (8^3 targets), 256 threads, one CTA per SM (197 KB smem).
+// Warp w = target parity class (b, c) = (w & 1, w >> 1 & 1) in y, z and source
+// half h = w >> 2 (the lower / upper three source planes of the spec's two
+// partial sums); lane = (a, Y, Z) = (lane & 1, lane >> 1 & 3, lane >> 3): the
+// thread owns the four targets x = a + 2k (k = 0..3), y = 2Y + b, z = 2Z + c,
+// over its half of the source planes. All 8 siblings of a
 // parent share the 6x6x6 children of the parent's neighbours as sources (the
 // 189-cell list is that box minus the target's 27 near cells), so per source
 // row (dy, dz) — warp-uniform — the thread keeps the geometry of its six x
@@ -221,17 +141,24 @@ __global__ void __launch_bounds__(256, 2) amr_m2l_kernel(const GLv* __restrict__
 // (a = 1) use zeroed near geometry: an exact no-op, because a sum that starts
 // at +0 never becomes -0 and x + (+-0) = x (finite moments).
 // Window: 12^3 sources (27-patch neighbourhood; missing patches are zero
-// moments), stored with M and Q negated (the contraction is all FMAs), split
-// into 4 (y, z)-parity sub-grids of 6 x 6 rows of 12 with pitches 13 / 84:
-// a warp's 16 distinct source addresses (Y, Z) fall in 16 distinct bank pairs.
-// Accumulation per target: dz, dy, dx ascending, then the W/X pairs —
+// moments) filled by cp.async, split into 4 (y, z)-parity sub-grids of 6 x 6
+// rows of 12 with pitches 13 / 84: a warp's 16 distinct source addresses
+// (Y, Z) fall in 16 distinct bank pairs.
+// Accumulation per target: two partial sums (lower / upper source planes),
+// dz, dy, dx ascending, added; the W/X pairs follow in amr_wx_kernel —
 // tmo_grav_amr_solve's order, so the result is bitwise the oracle's.
-constexpr int kM2lThreads = 128;
+constexpr int kM2lThreads = 256;
 constexpr int kWPY = 13, kWPZ = 84, kWSub = 6 * kWPZ, kWVar = 4 * kWSub;  // 2016 doubles per var
 constexpr int kWinDoubles = 10 * kWVar;                                   // 20,160
 constexpr int kTabDoubles = kOff3 * kTab;                                 // 4,459
 constexpr size_t kM2lSmem = (size_t)(kWinDoubles + kTabDoubles) * sizeof(double);  // 196,952 B
 
+// One source row: each source's moments are loaded once and applied to every
+// target k it interacts with (jj = sx - 2k in [0, 5]). The operations are
+// m2l_acc's, issued moment-major (all uses of -M, then Dx, Dy, Dz, then Q, each
+// across the targets) so consecutive DFMAs share their first operand (operand
+// reuse cache: two register reads per DFMA instead of three); every output's
+// own chain keeps m2l_acc's order, so the result is the same bit for bit.
 template <bool NEAR>
 __device__ __forceinline__ void m2l_row(const double* __restrict__ src, const double (&G)[6][kTab],
                                         double (&acc)[4][10]) {
@@ -240,14 +167,62 @@ __device__ __forceinline__ void m2l_row(const double* __restrict__ src, const do
     double m[10];
 #pragma unroll
     for (int q = 0; q < 10; ++q) m[q] = src[q * kWVar + sx];
+    bool v[4];
+    int jj[4];
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
-      const int jj = sx - 2 * k;
-      if (jj < 0 || jj > 5) continue;
-      if (NEAR && (jj == 2 || jj == 3)) continue;
-      m2l_acc(m[0], m[1], m[2], m[3], m[4], m[5], m[6], m[7], m[8], m[9], G[jj], acc[k]);
+      jj[k] = sx - 2 * k;
+      v[k] = jj[k] >= 0 && jj[k] <= 5 && !(NEAR && (jj[k] == 2 || jj[k] == 3));
+      if (!v[k]) jj[k] = 0;
     }
+    const double nM = -m[0];
+    double t[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      if (v[k]) t[k] = nM * G[jj[k]][0];
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      if (v[k]) {
+#pragma unroll
+        for (int i = 0; i < 3; ++i) acc[k][1 + i] = fma(nM, G[jj[k]][1 + i], acc[k][1 + i]);
+#pragma unroll
+        for (int q = 0; q < 6; ++q) acc[k][4 + q] = fma(nM, G[jj[k]][4 + q], acc[k][4 + q]);
+      }
+    // dipole: D_x pairs with (e1 | e4 e5 e6), D_y (e2 | e5 e7 e8), D_z (e3 | e6 e8 e9)
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+      const double D = m[1 + d];
+      const int r0 = d == 0 ? 4 : (d == 1 ? 5 : 6), r1 = d == 0 ? 5 : (d == 1 ? 7 : 8),
+                r2 = d == 0 ? 6 : (d == 1 ? 8 : 9);
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        if (v[k]) {
+          t[k] = fma(D, G[jj[k]][1 + d], t[k]);
+          acc[k][1] = fma(D, G[jj[k]][r0], acc[k][1]);
+          acc[k][2] = fma(D, G[jj[k]][r1], acc[k][2]);
+          acc[k][3] = fma(D, G[jj[k]][r2], acc[k][3]);
+        }
+    }
+    // quadrupole into L0: Qxx (e10) Qxy (e5) Qxz (e6) Qyy (e11) Qyz (e8) Qzz (e12)
+#pragma unroll
+    for (int q = 0; q < 6; ++q) {
+      const double nQ = -m[4 + q];
+      const int e = q == 0 ? 10 : (q == 1 ? 5 : (q == 2 ? 6 : (q == 3 ? 11 : (q == 4 ? 8 : 12))));
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        if (v[k]) t[k] = fma(nQ, G[jj[k]][e], t[k]);
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      if (v[k]) acc[k][0] = acc[k][0] + t[k];
   }
+}
+
+__device__ __forceinline__ void cp_async8(double* smem, const double* gmem, bool valid) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(sa), "l"(gmem),
+               "r"(valid ? 8 : 0)
+               : "memory");
 }
 
 __global__ void __launch_bounds__(kM2lThreads, 1) amr_m2l_fused_kernel(
@@ -259,13 +234,14 @@ __global__ void __launch_bounds__(kM2lThreads, 1) amr_m2l_fused_kernel(
   const int l = wk.x, n = wk.y;
   const GLv L = Lv[l];
   const int* nb27 = L.nbr + (long long)n * 27;
-  // level geometry (depth l + 3) with the 27 near offsets zeroed
+  // asynchronous fill (cp.async, 8-byte elements, zero-fill for missing
+  // patches and for the 27 near offsets of the level's geometry table)
   const double* tab = tab_all + (long long)(l + 3) * kOff3 * kTab;
   for (int q = threadIdx.x; q < kTabDoubles; q += kM2lThreads) {
     const int o = q / kTab;
     const int dx = o % kOff - 3, dy = (o / kOff) % kOff - 3, dz = o / (kOff * kOff) - 3;
     const bool near = dx >= -1 && dx <= 1 && dy >= -1 && dy <= 1 && dz >= -1 && dz <= 1;
-    tabs[q] = near ? 0.0 : tab[q];
+    cp_async8(tabs + q, tab + q, !near);
   }
   for (int q = threadIdx.x; q < 1728; q += kM2lThreads) {
     const int wx = q % 12, wy = (q / 12) % 12, wz = q / 144;
@@ -274,30 +250,15 @@ __global__ void __launch_bounds__(kM2lThreads, 1) amr_m2l_fused_kernel(
               oz = lz < 0 ? -1 : (lz > 7 ? 1 : 0);
     lx -= 8 * ox, ly -= 8 * oy, lz -= 8 * oz;
     const int nb = nb27[((oz + 1) * 3 + (oy + 1)) * 3 + ox + 1];
-    double v[10];
-    if (nb >= 0) {
-      const double2* s2p = reinterpret_cast<const double2*>(
-          L.mom + ((long long)nb * 512 + (lz * 8 + ly) * 8 + lx) * 10);
+    const double* src = L.mom + ((long long)(nb < 0 ? n : nb) * 512 + (lz * 8 + ly) * 8 + lx) * 10;
+    double* dst = win + ((wz & 1) * 2 + (wy & 1)) * kWSub + (wz >> 1) * kWPZ + (wy >> 1) * kWPY + wx;
 #pragma unroll
-      for (int h = 0; h < 5; ++h) {
-        const double2 t = s2p[h];
-        v[2 * h] = t.x;
-        v[2 * h + 1] = t.y;
-      }
-    } else {
-#pragma unroll
-      for (int h = 0; h < 10; ++h) v[h] = 0.0;
-    }
-    const int w = ((wz & 1) * 2 + (wy & 1)) * kWSub + (wz >> 1) * kWPZ + (wy >> 1) * kWPY + wx;
-    win[w] = -v[0];
-#pragma unroll
-    for (int h = 1; h < 4; ++h) win[h * kWVar + w] = v[h];
-#pragma unroll
-    for (int h = 4; h < 10; ++h) win[h * kWVar + w] = -v[h];
+    for (int h = 0; h < 10; ++h) cp_async8(dst + h * kWVar, src + h, nb >= 0);
   }
+  asm volatile("cp.async.wait_all;\n" ::: "memory");
   __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int b = warp & 1, c = warp >> 1;
+  const int b = warp & 1, c = (warp >> 1) & 1, half = warp >> 2;
   const int a = lane & 1, Y = (lane >> 1) & 3, Z = lane >> 3;
   double acc[4][10];
 #pragma unroll
@@ -306,7 +267,8 @@ __global__ void __launch_bounds__(kM2lThreads, 1) amr_m2l_fused_kernel(
     for (int q = 0; q < 10; ++q) acc[k][q] = 0.0;
   // table row base of this lane's x parity: entry (dx + 3) = jj + 1 - a
   const double* tab_lane = tabs + (1 - a) * kTab;
-  for (int iz = 0; iz < 6; ++iz) {
+  // this warp's half of the source planes: iz = dz + 2 + c in [3 half, 3 half + 2]
+  for (int iz = 3 * half; iz < 3 * half + 3; ++iz) {
     const int dz = iz - 2 - c;
     for (int iy = 0; iy < 6; ++iy) {
       const int dy = iy - 2 - b;
@@ -325,32 +287,90 @@ __global__ void __launch_bounds__(kM2lThreads, 1) amr_m2l_fused_kernel(
         m2l_row<false>(src, G, acc);
     }
   }
-  const int y = 2 * Y + b, z = 2 * Z + c, d = l + 3;
+  // upper-half warps hand their partial sums to the lower-half warps (the
+  // window is dead after the barrier): V = lower + upper, as the oracle adds
+  __syncthreads();
+  const int pair = threadIdx.x & 127;
+  if (half) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+#pragma unroll
+      for (int q = 0; q < 10; ++q) win[(k * 10 + q) * 128 + pair] = acc[k][q];
+  }
+  __syncthreads();
+  if (half) return;
+  const int y = 2 * Y + b, z = 2 * Z + c;
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
-    const int x = a + 2 * k;
-    const long long flat = (long long)n * 512 + (z * 8 + y) * 8 + x;
-    const long long e0 = L.moff[flat], e1 = L.moff[flat + 1];
-    if (e0 < e1) {  // W/X pairs (AMR level jumps), sorted by source
-      const double cx = centre(8LL * L.ijk[3 * n] + x, d), cy = centre(8LL * L.ijk[3 * n + 1] + y, d),
-                   cz = centre(8LL * L.ijk[3 * n + 2] + z, d);
-      for (long long e = e0; e < e1; ++e) {
-        const long long enc = L.ment[e];
-        const int sl = (int)(enc >> 40);
-        const long long sf = enc & ((1LL << 40) - 1);
-        const GLv S = Lv[sl];
-        const long long sn = sf >> 9;
-        const int sc = (int)(sf & 511);
-        const int sd = sl + 3;
-        const double sx = centre(8LL * S.ijk[3 * sn] + (sc & 7), sd),
-                     sy = centre(8LL * S.ijk[3 * sn + 1] + ((sc >> 3) & 7), sd),
-                     sz = centre(8LL * S.ijk[3 * sn + 2] + (sc >> 6), sd);
-        m2l_direct(S.mom + sf * 10, cx - sx, cy - sy, cz - sz, acc[k]);
-      }
-    }
+    const long long flat = (long long)n * 512 + (z * 8 + y) * 8 + a + 2 * k;
+    double v[10];
+#pragma unroll
+    for (int q = 0; q < 10; ++q) v[q] = acc[k][q] + win[(k * 10 + q) * 128 + pair];
     double2* out = reinterpret_cast<double2*>(L.loc + flat * 10);
 #pragma unroll
-    for (int h = 0; h < 5; ++h) out[h] = make_double2(acc[k][2 * h], acc[k][2 * h + 1]);
+    for (int h = 0; h < 5; ++h) out[h] = make_double2(v[2 * h], v[2 * h + 1]);
+  }
+}
+
+// W/X pairs (AMR level jumps) after the V-list sums, in the list's sorted
+// order, one thread per target with entries (targets sorted by entry count);
+// geometry from the plan's separation table (m2l_geom of each distinct R).
+__global__ void amr_wx_kernel(const GLv* __restrict__ Lv, const int* __restrict__ tlev,
+                              const long long* __restrict__ tflat, long long ntarget,
+                              const double* __restrict__ geo) {
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < ntarget;
+       t += (long long)gridDim.x * blockDim.x) {
+    const int l = tlev[t];
+    const long long flat = tflat[t];
+    double* loc = Lv[l].loc + flat * 10;
+    const long long* moff = Lv[l].moff;
+    const long long* ment = Lv[l].ment;
+    const int* mgeo = Lv[l].mgeo;
+    double acc[10];
+#pragma unroll
+    for (int h = 0; h < 5; ++h) {
+      const double2 v = reinterpret_cast<const double2*>(loc)[h];
+      acc[2 * h] = v.x;
+      acc[2 * h + 1] = v.y;
+    }
+    const long long e0 = moff[flat], e1 = moff[flat + 1];
+    long long e = e0;
+    for (; e + 1 < e1; e += 2) {  // two entries' loads in flight, applied in order
+      const long long enc0 = ment[e], enc1 = ment[e + 1];
+      const double* g0 = geo + (long long)mgeo[e] * kTab;
+      const double* g1 = geo + (long long)mgeo[e + 1] * kTab;
+      const double* p0 = Lv[enc0 >> 40].mom + (enc0 & ((1LL << 40) - 1)) * 10;
+      const double* p1 = Lv[enc1 >> 40].mom + (enc1 & ((1LL << 40) - 1)) * 10;
+      double m0[10], m1[10], G0[kTab], G1[kTab];
+#pragma unroll
+      for (int q = 0; q < 10; ++q) m0[q] = __ldg(p0 + q), m1[q] = __ldg(p1 + q);
+#pragma unroll
+      for (int q = 0; q < kTab; ++q) G0[q] = __ldg(g0 + q), G1[q] = __ldg(g1 + q);
+      m2l_tab(m0, G0, acc);
+      m2l_tab(m1, G1, acc);
+    }
+    if (e < e1) {
+      const long long enc = ment[e];
+      const double* mom = Lv[enc >> 40].mom + (enc & ((1LL << 40) - 1)) * 10;
+      m2l_tab(mom, geo + (long long)mgeo[e] * kTab, acc);
+    }
+#pragma unroll
+    for (int h = 0; h < 5; ++h)
+      reinterpret_cast<double2*>(loc)[h] = make_double2(acc[2 * h], acc[2 * h + 1]);
+  }
+}
+
+__global__ void sep_geom_kernel(const double* __restrict__ sep, long long n, double* __restrict__ geo,
+                                int p2p) {
+  const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (t >= n) return;
+  const double x = sep[3 * t], y = sep[3 * t + 1], z = sep[3 * t + 2];
+  if (p2p) {
+    double w[4];
+    p2p_geom(x, y, z, w);
+    for (int q = 0; q < 4; ++q) geo[4 * t + q] = w[q];
+  } else {
+    m2l_geom(x, y, z, geo + t * kTab);
   }
 }
 
@@ -402,7 +422,8 @@ __global__ void amr_l2l_kernel(const GLv* __restrict__ Lv, int l, long long nnod
 // g[q*ncell + s*512 + c]
 __global__ void amr_l2p_kernel(const GLv* __restrict__ Lv, long long nslots, long long lo,
                                const int* __restrict__ slot_level, const int* __restrict__ slot_node,
-                               double* __restrict__ phi, double* __restrict__ g) {
+                               const double* __restrict__ ugeo, double* __restrict__ phi,
+                               double* __restrict__ g) {
   const long long ncell = nslots * 512;  // outputs by local slot (canonical slot lo + s)
   for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < ncell;
        t += (long long)gridDim.x * blockDim.x) {
@@ -436,27 +457,14 @@ __global__ void amr_l2p_kernel(const GLv* __restrict__ Lv, long long nslots, lon
           gz = fma(nm, w[3], gz);
         }
     const long long e0 = L.poff[flat], e1 = L.poff[flat + 1];
-    if (e0 < e1) {
-      const double cx = centre(8LL * L.ijk[3 * n] + i, d), cy = centre(8LL * L.ijk[3 * n + 1] + j, d),
-                   cz = centre(8LL * L.ijk[3 * n + 2] + k, d);
-      for (long long e = e0; e < e1; ++e) {
-        const long long enc = L.pent[e];
-        const int sl = (int)(enc >> 40);
-        const long long sf = enc & ((1LL << 40) - 1);
-        const GLv S = Lv[sl];
-        const long long sn = sf >> 9;
-        const int sc = (int)(sf & 511);
-        const int sd = sl + 3;
-        const double nm = -S.mom[sf * 10];
-        double w[4];
-        p2p_geom(cx - centre(8LL * S.ijk[3 * sn] + (sc & 7), sd),
-                 cy - centre(8LL * S.ijk[3 * sn + 1] + ((sc >> 3) & 7), sd),
-                 cz - centre(8LL * S.ijk[3 * sn + 2] + (sc >> 6), sd), w);
-        p = fma(nm, w[0], p);
-        gx = fma(nm, w[1], gx);
-        gy = fma(nm, w[2], gy);
-        gz = fma(nm, w[3], gz);
-      }
+    for (long long e = e0; e < e1; ++e) {  // cross-depth U pairs, sorted by source
+      const long long enc = L.pent[e];
+      const double nm = -Lv[enc >> 40].mom[(enc & ((1LL << 40) - 1)) * 10];
+      const double* w = ugeo + (long long)L.pgeo[e] * 4;
+      p = fma(nm, w[0], p);
+      gx = fma(nm, w[1], gx);
+      gy = fma(nm, w[2], gy);
+      gz = fma(nm, w[3], gz);
     }
     phi[t] = p;
     g[t] = gx;
@@ -694,7 +702,11 @@ struct GravAmrWork {
   std::vector<long long> nneed;
   int2* m2l_work = nullptr;  // fused M2L launch: (level, node) per CTA
   long long m2l_ctas = 0;
-  bool legacy_m2l = false;   // TMGPU_M2L_LEGACY=1: per-level launches (A/B)
+  int* wx_tlev = nullptr;         // W/X kernel targets (level, flat), by entry count
+  long long* wx_tflat = nullptr;
+  long long wx_targets = 0;
+  double* wx_geo = nullptr;  // [distinct W/X separations][13]
+  double* u_geo = nullptr;   // [distinct cross-depth U separations][4]
   cudaStream_t side = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
 };
@@ -709,14 +721,38 @@ static cudaError_t build_m2l_work(GravAmrWork& w, const std::vector<std::vector<
       for (int n = 0; n < w.plan.lv[l].n; ++n) wk.push_back(make_int2(l, n));
     }
   }
-  if (w.m2l_work) {
-    cudaFree(w.m2l_work);
-    w.allocs.erase(std::find(w.allocs.begin(), w.allocs.end(), (void*)w.m2l_work));
-    w.m2l_work = nullptr;
-  }
+  auto drop = [&w](void*& p) {
+    if (!p) return;
+    cudaFree(p);
+    w.allocs.erase(std::find(w.allocs.begin(), w.allocs.end(), p));
+    p = nullptr;
+  };
+  drop(reinterpret_cast<void*&>(w.m2l_work));
+  drop(reinterpret_cast<void*&>(w.wx_tlev));
+  drop(reinterpret_cast<void*&>(w.wx_tflat));
   w.m2l_ctas = (long long)wk.size();
+  // targets with W/X entries among the M2L patches, most entries first
+  std::vector<std::pair<long long, std::pair<int, long long>>> tg;
+  for (const int2& x : wk) {
+    const GravLevel& L = w.plan.lv[x.x];
+    for (int c = 0; c < 512; ++c) {
+      const long long f = (long long)x.y * 512 + c;
+      const long long cnt = L.moff[f + 1] - L.moff[f];
+      if (cnt) tg.push_back({-cnt, {x.x, f}});
+    }
+  }
+  std::stable_sort(tg.begin(), tg.end(),
+                   [](const auto& p, const auto& q) { return p.first < q.first; });
+  std::vector<int> tl(tg.size());
+  std::vector<long long> tf(tg.size());
+  for (size_t i = 0; i < tg.size(); ++i) tl[i] = tg[i].second.first, tf[i] = tg[i].second.second;
+  w.wx_targets = (long long)tg.size();
   cudaError_t e = upload(wk, &w.m2l_work);
   if (w.m2l_work) w.allocs.push_back(w.m2l_work);
+  if (e == cudaSuccess) e = upload(tl, &w.wx_tlev);
+  if (w.wx_tlev) w.allocs.push_back(w.wx_tlev);
+  if (e == cudaSuccess) e = upload(tf, &w.wx_tflat);
+  if (w.wx_tflat) w.allocs.push_back(w.wx_tflat);
   return e;
 }
 
@@ -790,9 +826,12 @@ tmgpu_gravity_amr* tmgpu_gravity_amr_create(const int* leaves, long long nleaves
       e = upload(reinterpret_cast<const std::vector<long long>&>(L.poff), &poff), track(poff);
     if (e == cudaSuccess)
       e = upload(reinterpret_cast<const std::vector<long long>&>(L.pent), &pent), track(pent);
+    int *mgeo = nullptr, *pgeo = nullptr;
+    if (e == cudaSuccess) e = upload(L.mgeo, &mgeo), track(mgeo);
+    if (e == cudaSuccess) e = upload(L.pgeo, &pgeo), track(pgeo);
     if (e != cudaSuccess) break;
     g.ijk = ijk, g.nbr = nbr, g.child = child, g.parent = parent, g.leaf_slot = slot;
-    g.moff = moff, g.ment = ment, g.poff = poff, g.pent = pent;
+    g.moff = moff, g.ment = ment, g.poff = poff, g.pent = pent, g.mgeo = mgeo, g.pgeo = pgeo;
     w.internal[l] = inter;
   }
   if (e == cudaSuccess) e = cudaMalloc(&w.dev_lv, P.nlevels * sizeof(GLv)), track(w.dev_lv);
@@ -812,18 +851,27 @@ tmgpu_gravity_amr* tmgpu_gravity_amr_create(const int* leaves, long long nleaves
   if (e == cudaSuccess) e = cudaMalloc(&w.part, ((size_t)w.P * 16 + 22) * sizeof(double)), track(w.part);
   if (e == cudaSuccess) e = cudaMalloc(&w.part2, ((size_t)w.P / 256 + 1) * 16 * sizeof(double)), track(w.part2);
   if (e == cudaSuccess)
-    e = cudaFuncSetAttribute(amr_m2l_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)(10 * kWin * sizeof(double)));
-  if (e == cudaSuccess)
     e = cudaFuncSetAttribute(amr_m2l_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)kM2lSmem);
   if (e == cudaSuccess) e = build_m2l_work(w, nullptr);
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&w.side, cudaStreamNonBlocking);
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&w.ev_fork, cudaEventDisableTiming);
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&w.ev_join, cudaEventDisableTiming);
-  {
-    const char* env = std::getenv("TMGPU_M2L_LEGACY");
-    w.legacy_m2l = env && env[0] == '1';
+
+  for (int kind = 0; kind < 2 && e == cudaSuccess; ++kind) {
+    const std::vector<double>& sep = kind == 0 ? P.wx_sep : P.u_sep;
+    const long long ns = (long long)sep.size() / 3;
+    double** geo = kind == 0 ? &w.wx_geo : &w.u_geo;
+    double* dsep = nullptr;
+    e = cudaMalloc(geo, (size_t)(ns ? ns : 1) * (kind == 0 ? kTab : 4) * sizeof(double));
+    track(*geo);
+    if (e == cudaSuccess && ns) e = upload(sep, &dsep);
+    if (e == cudaSuccess && ns) {
+      sep_geom_kernel<<<(unsigned)((ns + 127) / 128), 128>>>(dsep, ns, *geo, kind);
+      g_launches.fetch_add(1, std::memory_order_relaxed);
+      e = cudaDeviceSynchronize();
+    }
+    if (dsep) cudaFree(dsep);
   }
   if (e == cudaSuccess) {
     stencil_table_kernel<<<((Dmax + 1) * kOff3 + 127) / 128, 128>>>(w.tab, Dmax);
@@ -845,6 +893,20 @@ int tmgpu_gravity_amr_info(const tmgpu_gravity_amr* G, long long* out) {
   out[2] = G->w.plan.m_entries;
   out[3] = G->w.plan.p_entries;
   return TMGPU_OK;
+}
+
+// Host-only (tests): per-level counts of the patches a rank owning canonical
+// slots [lo, hi) evaluates M2L/L2L for (grav_owned_ancestors); returns levels.
+int tmgpu_gravity_amr_plan_need(const int* leaves, long long nleaves, long long lo, long long hi,
+                                long long* counts, int max_levels, tmgpu_error* err) {
+  if (err) std::memset(err, 0, sizeof(*err));
+  GravPlan P;
+  std::string why;
+  if (!build_grav_plan(leaves, nleaves, P, &why)) return -set_err(err, TMGPU_ERR_INVALID, why.c_str());
+  if (lo < 0 || hi > nleaves || lo > hi) return -set_err(err, TMGPU_ERR_INVALID, "slot range");
+  const auto lists = grav_owned_ancestors(P, lo, hi);
+  for (int l = 0; l < P.nlevels && l < max_levels; ++l) counts[l] = (long long)lists[l].size();
+  return P.nlevels;
 }
 
 // Host-only: build the plan and report info[4] without touching the GPU.
@@ -925,17 +987,17 @@ int tmgpu_gravity_amr_solve(tmgpu_gravity_amr* G, const double* mass, double* ph
     cudaEventRecord(w.ev_join, w.side);
     launches += 4;
     if (timed) cudaEventRecord(rec.ev[1], st);
-    if (w.legacy_m2l) {
-      for (int l = 0; l < P.nlevels; ++l) {
-        if (!w.nneed[l]) continue;
-        amr_m2l_kernel<<<(unsigned)(w.nneed[l] * 2), 256, 10 * kWin * sizeof(double), st>>>(
-            w.dev_lv, l, w.tab + (long long)(l + 3) * kOff3 * kTab, w.need[l]);
+    {
+      if (w.m2l_ctas) {
+        amr_m2l_fused_kernel<<<(unsigned)w.m2l_ctas, kM2lThreads, kM2lSmem, st>>>(w.dev_lv, w.m2l_work,
+                                                                                 w.tab);
         ++launches;
       }
-    } else if (w.m2l_ctas) {
-      amr_m2l_fused_kernel<<<(unsigned)w.m2l_ctas, kM2lThreads, kM2lSmem, st>>>(w.dev_lv, w.m2l_work,
-                                                                               w.tab);
-      ++launches;
+      if (w.wx_targets) {
+        amr_wx_kernel<<<grid_for(w.wx_targets), 128, 0, st>>>(w.dev_lv, w.wx_tlev, w.wx_tflat,
+                                                              w.wx_targets, w.wx_geo);
+        ++launches;
+      }
     }
     cudaStreamWaitEvent(st, w.ev_join, 0);
     if (timed) cudaEventRecord(rec.ev[2], st);
@@ -948,7 +1010,7 @@ int tmgpu_gravity_amr_solve(tmgpu_gravity_amr* G, const double* mass, double* ph
     }
     if (timed) cudaEventRecord(rec.ev[3], st);
     amr_l2p_kernel<<<grid_for(nout), 128, 0, st>>>(w.dev_lv, nloc, w.lo, w.slot_level, w.slot_node,
-                                                   dphi, dg);
+                                                   w.u_geo, dphi, dg);
     ++launches;
     if (timed) cudaEventRecord(rec.ev[4], st);
     if (flags & TMGPU_GRAV_AM) {
@@ -1023,22 +1085,10 @@ int tmgpu_gravity_amr_distribute(tmgpu_gravity_amr* G, tmgpu_comm* comm, const l
   w.seg_lo.assign(slot_bounds, slot_bounds + R);
   w.seg_cnt.resize(R);
   for (int r = 0; r < R; ++r) w.seg_cnt[r] = slot_bounds[r + 1] - slot_bounds[r];
-  std::vector<std::vector<char>> mark(P.nlevels);
-  for (int l = 0; l < P.nlevels; ++l) mark[l].assign(P.lv[l].n, 0);
-  for (long long s = w.lo; s < w.hi; ++s) {
-    int l = P.slot_level[s], n = P.slot_node[s];
-    while (l >= 0 && n >= 0 && !mark[l][n]) {
-      mark[l][n] = 1;
-      n = P.lv[l].parent[n];
-      --l;
-    }
-  }
   cudaError_t e = cudaSuccess;
-  std::vector<std::vector<int>> lists(P.nlevels);
+  std::vector<std::vector<int>> lists = grav_owned_ancestors(P, w.lo, w.hi);
   for (int l = 0; l < P.nlevels && e == cudaSuccess; ++l) {
-    std::vector<int>& ids = lists[l];
-    for (int n = 0; n < P.lv[l].n; ++n)
-      if (mark[l][n]) ids.push_back(n);
+    const std::vector<int>& ids = lists[l];
     if (w.need[l]) {  // an earlier distribute
       cudaFree(w.need[l]);
       w.allocs.erase(std::find(w.allocs.begin(), w.allocs.end(), (void*)w.need[l]));

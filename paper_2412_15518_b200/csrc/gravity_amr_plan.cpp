@@ -24,6 +24,26 @@ struct Pair {
   int64_t skey;
   int64_t enc;
   int8_t kind, tlevel;
+  int8_t sdepth;
+  int64_t tg[3], sg[3];  // global cell coordinates of target and source
+};
+
+inline double centre(int64_t gi, int d) { return ((double)gi + 0.5) / (double)(1LL << d); }
+
+// exact separation key: depths + 2^(dm+1) (x_t - x_s) as integers, dm the finer depth
+struct SepKey {
+  int td, sd;
+  int64_t i[3];
+  bool operator==(const SepKey& o) const {
+    return td == o.td && sd == o.sd && i[0] == o.i[0] && i[1] == o.i[1] && i[2] == o.i[2];
+  }
+};
+struct SepHash {
+  size_t operator()(const SepKey& k) const {
+    uint64_t h = (uint64_t)k.td * 1315423911u + (uint64_t)k.sd * 2654435761u;
+    for (int q = 0; q < 3; ++q) h = h * 1000003u ^ (uint64_t)(k.i[q] + (1LL << 40));
+    return (size_t)h;
+  }
 };
 
 struct Builder {
@@ -45,10 +65,10 @@ struct Builder {
     return ((int64_t)depth << 57) | (g[2] << 38) | (g[1] << 19) | g[0];
   }
 
-  void push(int kind, int tlevel, int64_t tflat, int slevel, int64_t sflat, int sdepth,
-            const int64_t* sg) {
+  void push(int kind, int tlevel, int64_t tflat, const int64_t* tg, int slevel, int64_t sflat,
+            int sdepth, const int64_t* sg) {
     pairs.push_back(Pair{tflat, skey(sdepth, sg), ((int64_t)slevel << 40) | sflat, (int8_t)kind,
-                         (int8_t)tlevel});
+                         (int8_t)tlevel, (int8_t)sdepth, {tg[0], tg[1], tg[2]}, {sg[0], sg[1], sg[2]}});
   }
 
   // b: leaf cell (level lb, flat fb, depth db, global gb); Y: internal cell
@@ -66,14 +86,14 @@ struct Builder {
           const int64_t cf = (int64_t)cn * 512 + (cl[2] * 8 + cl[1]) * 8 + cl[0];
           if (touches(db, gb, dc, cg)) {
             if (is_leaf(lc, cn)) {
-              push(1, lb, fb, lc, cf, dc, cg);
-              push(1, lc, cf, lb, fb, db, gb);
+              push(1, lb, fb, gb, lc, cf, dc, cg);
+              push(1, lc, cf, cg, lb, fb, db, gb);
             } else {
               visit(lb, fb, gb, lc, cn, cl, cg);
             }
           } else {
-            push(0, lb, fb, lc, cf, dc, cg);
-            push(0, lc, cf, lb, fb, db, gb);
+            push(0, lb, fb, gb, lc, cf, dc, cg);
+            push(0, lc, cf, cg, lb, fb, db, gb);
           }
         }
   }
@@ -218,11 +238,27 @@ bool build_grav_plan(const int* leaves, long long nleaves, GravPlan& P, std::str
     L.moff.assign((size_t)L.n * 512 + 1, 0);
     L.poff.assign((size_t)L.n * 512 + 1, 0);
   }
+  std::unordered_map<SepKey, int, SepHash> sep[2];
   for (const Pair& x : B.pairs) {
     GravLevel& L = P.lv[x.tlevel];
     (x.kind == 0 ? L.moff : L.poff)[x.tflat + 1] += 1;
     (x.kind == 0 ? L.ment : L.pent).push_back(x.enc);
     (x.kind == 0 ? P.m_entries : P.p_entries) += 1;
+    const int td = x.tlevel + 3, sd = x.sdepth, dm = std::max(td, sd);
+    SepKey k{td, sd, {0, 0, 0}};
+    for (int q = 0; q < 3; ++q)
+      k.i[q] = (2 * x.tg[q] + 1) * (1LL << (dm - td)) - (2 * x.sg[q] + 1) * (1LL << (dm - sd));
+    std::vector<double>& tab = x.kind == 0 ? P.wx_sep : P.u_sep;
+    auto it = sep[x.kind].find(k);
+    int gi;
+    if (it == sep[x.kind].end()) {
+      gi = (int)(tab.size() / 3);
+      sep[x.kind].emplace(k, gi);
+      for (int q = 0; q < 3; ++q) tab.push_back(centre(x.tg[q], td) - centre(x.sg[q], sd));
+    } else {
+      gi = it->second;
+    }
+    (x.kind == 0 ? L.mgeo : L.pgeo).push_back(gi);
   }
   for (int l = 0; l < P.nlevels; ++l) {
     GravLevel& L = P.lv[l];
@@ -230,6 +266,24 @@ bool build_grav_plan(const int* leaves, long long nleaves, GravPlan& P, std::str
     for (size_t t = 1; t < L.poff.size(); ++t) L.poff[t] += L.poff[t - 1];
   }
   return true;
+}
+
+std::vector<std::vector<int>> grav_owned_ancestors(const GravPlan& P, long long lo, long long hi) {
+  std::vector<std::vector<char>> mark(P.nlevels);
+  for (int l = 0; l < P.nlevels; ++l) mark[l].assign(P.lv[l].n, 0);
+  for (long long s = lo; s < hi; ++s) {
+    int l = P.slot_level[s], n = P.slot_node[s];
+    while (l >= 0 && n >= 0 && !mark[l][n]) {
+      mark[l][n] = 1;
+      n = P.lv[l].parent[n];
+      --l;
+    }
+  }
+  std::vector<std::vector<int>> out(P.nlevels);
+  for (int l = 0; l < P.nlevels; ++l)
+    for (int n = 0; n < P.lv[l].n; ++n)
+      if (mark[l][n]) out[l].push_back(n);
+  return out;
 }
 
 }  // namespace tmgpu

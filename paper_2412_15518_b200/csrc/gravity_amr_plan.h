@@ -25,6 +25,7 @@ struct GravLevel {
   // per target by source (depth, gk, gj, gi)
   std::vector<int64_t> moff, ment;  // W/X: M2L terms into the cell's local expansion
   std::vector<int64_t> poff, pent;  // cross-depth U: P2P terms (leaf cells only)
+  std::vector<int> mgeo, pgeo;      // per entry: index into GravPlan::wx_sep / u_sep
 };
 
 struct GravPlan {
@@ -32,10 +33,20 @@ struct GravPlan {
   std::vector<GravLevel> lv;
   std::vector<int> slot_level, slot_node;  // per canonical leaf slot
   long long m_entries = 0, p_entries = 0;
+  // distinct separations R = x_target - x_source of the W/X and cross-depth U
+  // entries ([k][3], each computed as centre(t) - centre(s) exactly as the
+  // oracle does): the result of that subtraction depends only on the exact
+  // separation, so entries share a geometry table bit for bit
+  std::vector<double> wx_sep, u_sep;
 };
 
 // leaves: [n][4] (level, I, J, K) in canonical order, one root = unit cube.
 // Returns false (why set) unless the leaves tile the cube without overlap.
 bool build_grav_plan(const int* leaves, long long nleaves, GravPlan& plan, std::string* why);
+
+// Multi-GPU: per level, the nodes (ascending) that are ancestors-or-self of the
+// canonical slots [lo, hi) — the patches whose M2L/L2L a rank owning those
+// slots must evaluate (their locals flow down to its leaves).
+std::vector<std::vector<int>> grav_owned_ancestors(const GravPlan& plan, long long lo, long long hi);
 
 }  // namespace tmgpu

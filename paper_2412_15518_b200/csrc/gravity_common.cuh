@@ -52,14 +52,14 @@ __global__ void stencil_table_kernel(double* __restrict__ tab, int D) {
   m2l_geom(-(double)dx * h, -(double)dy * h, -(double)dz * h, e);
 }
 
-// One M2L term with known geometry: the fixed 28-FMA chain of
-// tmo_grav_m2l_geom. nM = -M and nQ = -Q (negation is exact, and fma(-a, b, c)
-// is the same correctly rounded operation either way).
+// One M2L term with known geometry, operation for operation tmo_grav_m2l_geom:
+// the L0 increment is formed on its own and then added (27 FMAs, 1 mul, 1 add).
+// nM = -M and nQ = -Q (negation is exact, and fma(-a, b, c) is the same
+// correctly rounded operation either way).
 __device__ __forceinline__ void m2l_acc(double nM, double Dx, double Dy, double Dz, double nQxx,
                                         double nQxy, double nQxz, double nQyy, double nQyz,
                                         double nQzz, const double* __restrict__ e, double out[10]) {
-  double o = out[0];
-  o = fma(nM, e[0], o);
+  double o = nM * e[0];
   o = fma(Dx, e[1], o);
   o = fma(Dy, e[2], o);
   o = fma(Dz, e[3], o);
@@ -69,7 +69,7 @@ __device__ __forceinline__ void m2l_acc(double nM, double Dx, double Dy, double 
   o = fma(nQyy, e[11], o);
   o = fma(nQyz, e[8], o);
   o = fma(nQzz, e[12], o);
-  out[0] = o;
+  out[0] = out[0] + o;
   // D2 rows: x (xx xy xz) = e4 e5 e6, y (xy yy yz) = e5 e7 e8, z (xz yz zz) = e6 e8 e9
   out[1] = fma(Dz, e[6], fma(Dy, e[5], fma(Dx, e[4], fma(nM, e[1], out[1]))));
   out[2] = fma(Dz, e[8], fma(Dy, e[7], fma(Dx, e[5], fma(nM, e[2], out[2]))));
@@ -145,9 +145,9 @@ __global__ void __launch_bounds__(128) m2l_kernel(const double* __restrict__ mom
   for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < n3;
        t += (long long)gridDim.x * blockDim.x) {
     const long long i = t % m, j = (t / m) % m, k = t / (m * m);
-    double o[10];
+    double o[2][10];  // lower / upper three source planes (tmo_grav_solve)
 #pragma unroll
-    for (int q = 0; q < 10; ++q) o[q] = 0.0;
+    for (int q = 0; q < 10; ++q) o[0][q] = o[1][q] = 0.0;
     for (long long dz = -2 - (k & 1); dz <= 3 - (k & 1); ++dz)
       for (long long dy = -2 - (j & 1); dy <= 3 - (j & 1); ++dy)
         for (long long dx = -2 - (i & 1); dx <= 3 - (i & 1); ++dx) {
@@ -155,11 +155,12 @@ __global__ void __launch_bounds__(128) m2l_kernel(const double* __restrict__ mom
           const long long si = i + dx, sj = j + dy, sk = k + dz;
           if (si < 0 || sj < 0 || sk < 0 || si >= m || sj >= m || sk >= m) continue;
           m2l_tab(mom + cidx(m, si, sj, sk) * 10,
-                  tab + (((dz + 3) * kOff + (dy + 3)) * kOff + (dx + 3)) * kTab, o);
+                  tab + (((dz + 3) * kOff + (dy + 3)) * kOff + (dx + 3)) * kTab,
+                  o[dz + (k & 1) >= 1]);
         }
     double* out = loc + t * 10;
 #pragma unroll
-    for (int q = 0; q < 10; ++q) out[q] = o[q];
+    for (int q = 0; q < 10; ++q) out[q] = o[0][q] + o[1][q];
   }
 }
 

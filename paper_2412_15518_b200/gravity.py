@@ -135,6 +135,23 @@ def amr_plan_info(leaves):
     return tuple(out)
 
 
+lib.tmgpu_gravity_amr_plan_need.restype = C.c_int
+lib.tmgpu_gravity_amr_plan_need.argtypes = [_vp, C.c_longlong, C.c_longlong, C.c_longlong, _lp,
+                                            C.c_int, _ep]
+
+
+def amr_plan_need(leaves, lo: int, hi: int):
+    """Host-only: per-level counts of the patches whose M2L/L2L a rank owning
+    the canonical slots [lo, hi) evaluates (the ancestors of its leaves)."""
+    lv = _leaf_array(leaves)
+    out = (C.c_longlong * 32)()
+    err = TmgpuError()
+    n = lib.tmgpu_gravity_amr_plan_need(lv.ctypes.data, lv.shape[0], lo, hi, out, 32, C.byref(err))
+    if n < 0:
+        _lib.check(-n, err)
+    return list(out[:n])
+
+
 def forest_leaf_array(forest):
     """[n, 4] (level, I, J, K) of a forest's local leaves in slot order."""
     from .amr import unpack

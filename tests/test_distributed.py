@@ -68,6 +68,18 @@ def test_gloo_world2_halo_manifests_agree():
     assert r.stdout.count("HALO_OK") == 2, r.stdout[-2000:]
 
 
+def test_gloo_world2_gravity_partition():
+    """Two processes (gloo, world_size 2): the distributed FMM's slot ranges tile
+    the leaves and the per-rank M2L/L2L patch sets cover the cell tree."""
+    env = dict(os.environ, GLOO_SOCKET_IFNAME="lo")
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+                        "--nproc-per-node=2", "--master-addr", "127.0.0.1", "--master-port",
+                        "29564", os.path.join(ROOT, "tests", "gloo_gravity.py")],
+                       capture_output=True, text=True, timeout=300, env=env)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+    assert r.stdout.count("GRAV_OK") == 2, r.stdout[-2000:]
+
+
 @pytest.mark.gpu
 def test_partitioned_step_bitwise_equals_single_gpu():
     import torch
