@@ -313,7 +313,7 @@ __global__ void __launch_bounds__(kM2lThreads, 1) amr_m2l_fused_kernel(
 }
 
 // W/X pairs (AMR level jumps) after the V-list sums, in the list's sorted
-// order, one thread per target with entries (targets sorted by entry count);
+// order, one thread per target with entries (targets in patch order);
 // geometry from the plan's separation table (m2l_geom of each distinct R).
 __global__ void amr_wx_kernel(const GLv* __restrict__ Lv, const int* __restrict__ tlev,
                               const long long* __restrict__ tflat, long long ntarget,
@@ -418,59 +418,77 @@ __global__ void amr_l2l_kernel(const GLv* __restrict__ Lv, int l, long long nnod
   }
 }
 
-// L2P + P2P at the leaf cells, output by canonical slot: phi[s*512 + c],
-// g[q*ncell + s*512 + c]
-__global__ void amr_l2p_kernel(const GLv* __restrict__ Lv, long long nslots, long long lo,
-                               const int* __restrict__ slot_level, const int* __restrict__ slot_node,
-                               const double* __restrict__ ugeo, double* __restrict__ phi,
-                               double* __restrict__ g) {
-  const long long ncell = nslots * 512;  // outputs by local slot (canonical slot lo + s)
-  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < ncell;
-       t += (long long)gridDim.x * blockDim.x) {
-    const long long s = lo + (t >> 9);
-    const int c = (int)(t & 511);
-    const int i = c & 7, j = (c >> 3) & 7, k = c >> 6;
-    const int l = slot_level[s], n = slot_node[s];
-    const GLv L = Lv[l];
-    const int d = l + 3;
+// L2P + P2P at the leaf cells, output by local slot: phi[s*512 + c],
+// g[q*ncell + s*512 + c]. CTA = 128 cells of one slot (4 CTAs per slot): the
+// 26 same-depth offsets' P2P geometry (p2p_geom of the lattice offset, the
+// same operations as per pair) and the 27 neighbour slots are resolved once
+// into shared memory; neighbour masses come from the leaf-mass array (8-byte,
+// coalesced across the warp), cross-depth U pairs from the plan's geometry
+// table. Term order: 26 offsets dz, dy, dx ascending, then the U pairs.
+__global__ void __launch_bounds__(128) amr_l2p_kernel(const GLv* __restrict__ Lv, long long nslots,
+                                                      long long lo, const int* __restrict__ slot_level,
+                                                      const int* __restrict__ slot_node,
+                                                      const double* __restrict__ mass,
+                                                      const double* __restrict__ ugeo,
+                                                      double* __restrict__ phi, double* __restrict__ g) {
+  __shared__ double w26[27][4];
+  __shared__ long long nbslot[27];
+  const long long ls = blockIdx.x >> 2;  // local slot
+  const long long s = lo + ls;
+  const int l = slot_level[s], n = slot_node[s];
+  const GLv L = Lv[l];
+  const int d = l + 3;
+  if (threadIdx.x < 27) {
+    const int o = threadIdx.x;
+    const int dx = o % 3 - 1, dy = (o / 3) % 3 - 1, dz = o / 9 - 1;
     const double h = 1.0 / (double)(1LL << d);
-    const long long flat = (long long)n * 512 + c;
-    const double* Lc = L.loc + flat * 10;
-    double p = Lc[0], gx = -Lc[1], gy = -Lc[2], gz = -Lc[3];
-    const int* nb27 = L.nbr + (long long)n * 27;
-    for (int dz = -1; dz <= 1; ++dz)
-      for (int dy = -1; dy <= 1; ++dy)
-        for (int dx = -1; dx <= 1; ++dx) {
-          if (!dx && !dy && !dz) continue;
-          int lx = i + dx, ly = j + dy, lz = k + dz;
-          const int ox = lx < 0 ? -1 : (lx > 7 ? 1 : 0), oy = ly < 0 ? -1 : (ly > 7 ? 1 : 0),
-                    oz = lz < 0 ? -1 : (lz > 7 ? 1 : 0);
-          lx -= 8 * ox, ly -= 8 * oy, lz -= 8 * oz;
-          const int nb = nb27[((oz + 1) * 3 + (oy + 1)) * 3 + ox + 1];
-          if (nb < 0 || L.leaf_slot[nb] < 0) continue;
-          const double nm = -L.mom[((long long)nb * 512 + (lz * 8 + ly) * 8 + lx) * 10];
-          double w[4];
-          p2p_geom(-(double)dx * h, -(double)dy * h, -(double)dz * h, w);
-          p = fma(nm, w[0], p);
-          gx = fma(nm, w[1], gx);
-          gy = fma(nm, w[2], gy);
-          gz = fma(nm, w[3], gz);
-        }
-    const long long e0 = L.poff[flat], e1 = L.poff[flat + 1];
-    for (long long e = e0; e < e1; ++e) {  // cross-depth U pairs, sorted by source
-      const long long enc = L.pent[e];
-      const double nm = -Lv[enc >> 40].mom[(enc & ((1LL << 40) - 1)) * 10];
-      const double* w = ugeo + (long long)L.pgeo[e] * 4;
-      p = fma(nm, w[0], p);
-      gx = fma(nm, w[1], gx);
-      gy = fma(nm, w[2], gy);
-      gz = fma(nm, w[3], gz);
-    }
-    phi[t] = p;
-    g[t] = gx;
-    g[ncell + t] = gy;
-    g[2 * ncell + t] = gz;
+    if (o != 13) p2p_geom(-(double)dx * h, -(double)dy * h, -(double)dz * h, w26[o]);
+    const int nb = L.nbr[(long long)n * 27 + o];
+    nbslot[o] = (nb >= 0 && L.leaf_slot[nb] >= 0) ? (long long)L.leaf_slot[nb] : -1;
   }
+  __syncthreads();
+  const long long ncell = nslots * 512;
+  const int c = (int)((blockIdx.x & 3) * 128 + threadIdx.x);
+  const int i = c & 7, j = (c >> 3) & 7, k = c >> 6;
+  const long long flat = (long long)n * 512 + c;
+  const double2* Lc = reinterpret_cast<const double2*>(L.loc + flat * 10);
+  const double2 l01 = Lc[0], l23 = Lc[1];
+  double p = l01.x, gx = -l01.y, gy = -l23.x, gz = -l23.y;
+#pragma unroll
+  for (int dz = -1; dz <= 1; ++dz)
+#pragma unroll
+    for (int dy = -1; dy <= 1; ++dy)
+#pragma unroll
+      for (int dx = -1; dx <= 1; ++dx) {
+        if (!dx && !dy && !dz) continue;
+        int lx = i + dx, ly = j + dy, lz = k + dz;
+        const int ox = lx < 0 ? -1 : (lx > 7 ? 1 : 0), oy = ly < 0 ? -1 : (ly > 7 ? 1 : 0),
+                  oz = lz < 0 ? -1 : (lz > 7 ? 1 : 0);
+        lx -= 8 * ox, ly -= 8 * oy, lz -= 8 * oz;
+        const long long ns = nbslot[((oz + 1) * 3 + (oy + 1)) * 3 + ox + 1];
+        if (ns < 0) continue;
+        const double nm = -mass[ns * 512 + (lz * 8 + ly) * 8 + lx];
+        const double* w = w26[((dz + 1) * 3 + (dy + 1)) * 3 + dx + 1];
+        p = fma(nm, w[0], p);
+        gx = fma(nm, w[1], gx);
+        gy = fma(nm, w[2], gy);
+        gz = fma(nm, w[3], gz);
+      }
+  const long long e0 = L.poff[flat], e1 = L.poff[flat + 1];
+  for (long long e = e0; e < e1; ++e) {  // cross-depth U pairs, sorted by source
+    const long long enc = L.pent[e];
+    const double nm = -Lv[enc >> 40].mom[(enc & ((1LL << 40) - 1)) * 10];
+    const double* w = ugeo + (long long)L.pgeo[e] * 4;
+    p = fma(nm, w[0], p);
+    gx = fma(nm, w[1], gx);
+    gy = fma(nm, w[2], gy);
+    gz = fma(nm, w[3], gz);
+  }
+  const long long t = ls * 512 + c;
+  phi[t] = p;
+  g[t] = gx;
+  g[ncell + t] = gy;
+  g[2 * ncell + t] = gz;
 }
 
 // ---- angular-momentum correction (tmo_grav_am_correct) ---------------------
@@ -731,7 +749,7 @@ static cudaError_t build_m2l_work(GravAmrWork& w, const std::vector<std::vector<
   drop(reinterpret_cast<void*&>(w.wx_tlev));
   drop(reinterpret_cast<void*&>(w.wx_tflat));
   w.m2l_ctas = (long long)wk.size();
-  // targets with W/X entries among the M2L patches, most entries first
+  // targets with W/X entries among the M2L patches, in patch order (source locality)
   std::vector<std::pair<long long, std::pair<int, long long>>> tg;
   for (const int2& x : wk) {
     const GravLevel& L = w.plan.lv[x.x];
@@ -741,8 +759,6 @@ static cudaError_t build_m2l_work(GravAmrWork& w, const std::vector<std::vector<
       if (cnt) tg.push_back({-cnt, {x.x, f}});
     }
   }
-  std::stable_sort(tg.begin(), tg.end(),
-                   [](const auto& p, const auto& q) { return p.first < q.first; });
   std::vector<int> tl(tg.size());
   std::vector<long long> tf(tg.size());
   for (size_t i = 0; i < tg.size(); ++i) tl[i] = tg[i].second.first, tf[i] = tg[i].second.second;
@@ -1009,8 +1025,9 @@ int tmgpu_gravity_amr_solve(tmgpu_gravity_amr* G, const double* mass, double* ph
       ++launches;
     }
     if (timed) cudaEventRecord(rec.ev[3], st);
-    amr_l2p_kernel<<<grid_for(nout), 128, 0, st>>>(w.dev_lv, nloc, w.lo, w.slot_level, w.slot_node,
-                                                   w.u_geo, dphi, dg);
+    if (nloc)
+      amr_l2p_kernel<<<(unsigned)(nloc * 4), 128, 0, st>>>(w.dev_lv, nloc, w.lo, w.slot_level,
+                                                           w.slot_node, w.mass, w.u_geo, dphi, dg);
     ++launches;
     if (timed) cudaEventRecord(rec.ev[4], st);
     if (flags & TMGPU_GRAV_AM) {
