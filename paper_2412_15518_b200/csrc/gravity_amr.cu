@@ -73,18 +73,20 @@ __global__ void amr_mass_kernel(const double* __restrict__ arena, int V, long lo
   }
 }
 
+// leaf cells: moments (m, 0, ..., 0); thread = (cell, 16-byte pair), so a
+// warp writes 512 contiguous bytes of the AoS moments
 __global__ void amr_p2m_kernel(const double* __restrict__ mass, long long nslots,
                                const int* __restrict__ slot_level, const int* __restrict__ slot_node,
                                const GLv* __restrict__ L) {
-  const long long total = nslots * 512;
-  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
-       t += (long long)gridDim.x * blockDim.x) {
+  const long long total = nslots * 512 * 5;
+  for (long long u = blockIdx.x * (long long)blockDim.x + threadIdx.x; u < total;
+       u += (long long)gridDim.x * blockDim.x) {
+    const long long t = u / 5;
+    const int pr = (int)(u - 5 * t);
     const long long s = t >> 9;
     const int c = (int)(t & 511);
-    double* o = L[slot_level[s]].mom + ((long long)slot_node[s] * 512 + c) * 10;
-    o[0] = mass[t];
-#pragma unroll
-    for (int q = 1; q < 10; ++q) o[q] = 0.0;
+    double2* o = reinterpret_cast<double2*>(L[slot_level[s]].mom + ((long long)slot_node[s] * 512 + c) * 10);
+    o[pr] = make_double2(pr == 0 ? mass[t] : 0.0, 0.0);
   }
 }
 
@@ -148,10 +150,10 @@ __global__ void amr_m2m_kernel(const GLv* __restrict__ L, int l, const int* __re
 // dz, dy, dx ascending, added; the W/X pairs follow in amr_wx_kernel —
 // tmo_grav_amr_solve's order, so the result is bitwise the oracle's.
 constexpr int kM2lThreads = 256;
-constexpr int kWPY = 13, kWPZ = 84, kWSub = 6 * kWPZ, kWVar = 4 * kWSub;  // 2016 doubles per var
-constexpr int kWinDoubles = 10 * kWVar;                                   // 20,160
+constexpr int kWPY = 13, kWPZ = 84, kWSub = 6 * kWPZ, kWVar = 4 * kWSub + 2;  // per var (+2: banks)
+constexpr int kWinDoubles = 10 * kWVar;                                   // 20,180
 constexpr int kTabDoubles = kOff3 * kTab;                                 // 4,459
-constexpr size_t kM2lSmem = (size_t)(kWinDoubles + kTabDoubles) * sizeof(double);  // 196,952 B
+constexpr size_t kM2lSmem = (size_t)(kWinDoubles + kTabDoubles) * sizeof(double);  // 197,112 B
 
 // One source row: each source's moments are loaded once and applied to every
 // target k it interacts with (jj = sx - 2k in [0, 5]). The operations are
@@ -243,17 +245,26 @@ __global__ void __launch_bounds__(kM2lThreads, 1) amr_m2l_fused_kernel(
     const bool near = dx >= -1 && dx <= 1 && dy >= -1 && dy <= 1 && dz >= -1 && dz <= 1;
     cp_async8(tabs + q, tab + q, !near);
   }
-  for (int q = threadIdx.x; q < 1728; q += kM2lThreads) {
-    const int wx = q % 12, wy = (q / 12) % 12, wz = q / 144;
-    int lx = wx - 2, ly = wy - 2, lz = wz - 2;
-    const int ox = lx < 0 ? -1 : (lx > 7 ? 1 : 0), oy = ly < 0 ? -1 : (ly > 7 ? 1 : 0),
-              oz = lz < 0 ? -1 : (lz > 7 ? 1 : 0);
-    lx -= 8 * ox, ly -= 8 * oy, lz -= 8 * oz;
-    const int nb = nb27[((oz + 1) * 3 + (oy + 1)) * 3 + ox + 1];
-    const double* src = L.mom + ((long long)(nb < 0 ? n : nb) * 512 + (lz * 8 + ly) * 8 + lx) * 10;
-    double* dst = win + ((wz & 1) * 2 + (wy & 1)) * kWSub + (wz >> 1) * kWPZ + (wy >> 1) * kWPY + wx;
+  // task = (window row (wy, wz), component), component fastest: a warp's
+  // copies of one x position read ~3 consecutive cells' 80-byte moments
+  for (int task = threadIdx.x; task < 1440; task += kM2lThreads) {
+    const int h = task % 10, row = task / 10;
+    const int wy = row % 12, wz = row / 12;
+    int ly = wy - 2, lz = wz - 2;
+    const int oy = ly < 0 ? -1 : (ly > 7 ? 1 : 0), oz = lz < 0 ? -1 : (lz > 7 ? 1 : 0);
+    ly -= 8 * oy, lz -= 8 * oz;
+    const int* nbrow = nb27 + ((oz + 1) * 3 + (oy + 1)) * 3;
+    const int nbs[3] = {nbrow[0], nbrow[1], nbrow[2]};
+    double* dst = win + h * kWVar + ((wz & 1) * 2 + (wy & 1)) * kWSub + (wz >> 1) * kWPZ +
+                  (wy >> 1) * kWPY;
+    const long long rowoff = (long long)(lz * 8 + ly) * 8;
 #pragma unroll
-    for (int h = 0; h < 10; ++h) cp_async8(dst + h * kWVar, src + h, nb >= 0);
+    for (int wx = 0; wx < 12; ++wx) {
+      const int ox = wx < 2 ? -1 : (wx > 9 ? 1 : 0), lx = wx - 2 - 8 * ox;
+      const int nb = nbs[ox + 1];
+      const double* src = L.mom + ((long long)(nb < 0 ? n : nb) * 512 + rowoff + lx) * 10 + h;
+      cp_async8(dst + wx, src, nb >= 0);
+    }
   }
   asm volatile("cp.async.wait_all;\n" ::: "memory");
   __syncthreads();
@@ -985,7 +996,8 @@ int tmgpu_gravity_amr_solve(tmgpu_gravity_amr* G, const double* mass, double* ph
   }
   if (e == cudaSuccess && rc == TMGPU_OK) {
     long long launches = 0;
-    amr_p2m_kernel<<<grid_for(ncell), 128, 0, st>>>(w.mass, w.nslots, w.slot_level, w.slot_node, w.dev_lv);
+    amr_p2m_kernel<<<grid_for(ncell * 5), 128, 0, st>>>(w.mass, w.nslots, w.slot_level, w.slot_node,
+                                                        w.dev_lv);
     ++launches;
     for (int l = P.nlevels - 2; l >= 0; --l) {
       const long long ni = (long long)P.lv[l].internal.size();
