@@ -152,8 +152,9 @@ __global__ void amr_m2m_kernel(const GLv* __restrict__ L, int l, const int* __re
 constexpr int kM2lThreads = 256;
 constexpr int kWPY = 13, kWPZ = 84, kWSub = 6 * kWPZ, kWVar = 4 * kWSub + 2;  // per var (+2: banks)
 constexpr int kWinDoubles = 10 * kWVar;                                   // 20,180
-constexpr int kTabDoubles = kOff3 * kTab;                                 // 4,459
-constexpr size_t kM2lSmem = (size_t)(kWinDoubles + kTabDoubles) * sizeof(double);  // 197,112 B
+constexpr int kTabP = 14;  // shared-memory table entry: 13 doubles + pad (16-byte rows)
+constexpr int kTabDoubles = kOff3 * kTabP;                                // 4,802
+constexpr size_t kM2lSmem = (size_t)(kWinDoubles + kTabDoubles) * sizeof(double);  // 199,856 B
 
 // One source row: each source's moments are loaded once and applied to every
 // target k it interacts with (jj = sx - 2k in [0, 5]). The operations are
@@ -239,11 +240,11 @@ __global__ void __launch_bounds__(kM2lThreads, 1) amr_m2l_fused_kernel(
   // asynchronous fill (cp.async, 8-byte elements, zero-fill for missing
   // patches and for the 27 near offsets of the level's geometry table)
   const double* tab = tab_all + (long long)(l + 3) * kOff3 * kTab;
-  for (int q = threadIdx.x; q < kTabDoubles; q += kM2lThreads) {
+  for (int q = threadIdx.x; q < kOff3 * kTab; q += kM2lThreads) {
     const int o = q / kTab;
     const int dx = o % kOff - 3, dy = (o / kOff) % kOff - 3, dz = o / (kOff * kOff) - 3;
     const bool near = dx >= -1 && dx <= 1 && dy >= -1 && dy <= 1 && dz >= -1 && dz <= 1;
-    cp_async8(tabs + q, tab + q, !near);
+    cp_async8(tabs + o * kTabP + (q - o * kTab), tab + q, !near);
   }
   // task = (window row (wy, wz), component), component fastest: a warp's
   // copies of one x position read ~3 consecutive cells' 80-byte moments
@@ -277,18 +278,25 @@ __global__ void __launch_bounds__(kM2lThreads, 1) amr_m2l_fused_kernel(
 #pragma unroll
     for (int q = 0; q < 10; ++q) acc[k][q] = 0.0;
   // table row base of this lane's x parity: entry (dx + 3) = jj + 1 - a
-  const double* tab_lane = tabs + (1 - a) * kTab;
+  const double* tab_lane = tabs + (1 - a) * kTabP;
   // this warp's half of the source planes: iz = dz + 2 + c in [3 half, 3 half + 2]
   for (int iz = 3 * half; iz < 3 * half + 3; ++iz) {
     const int dz = iz - 2 - c;
     for (int iy = 0; iy < 6; ++iy) {
       const int dy = iy - 2 - b;
-      const double* trow = tab_lane + ((dz + 3) * kOff + (dy + 3)) * kOff * kTab;
+      const double* trow = tab_lane + ((dz + 3) * kOff + (dy + 3)) * kOff * kTabP;
       double G[6][kTab];
 #pragma unroll
-      for (int jj = 0; jj < 6; ++jj)
+      for (int jj = 0; jj < 6; ++jj) {
+        const double2* t2 = reinterpret_cast<const double2*>(trow + jj * kTabP);
 #pragma unroll
-        for (int q = 0; q < kTab; ++q) G[jj][q] = trow[jj * kTab + q];
+        for (int q = 0; q < 6; ++q) {
+          const double2 v = t2[q];
+          G[jj][2 * q] = v.x;
+          G[jj][2 * q + 1] = v.y;
+        }
+        G[jj][12] = trow[jj * kTabP + 12];
+      }
       // source row: window y = 2Y + iy, z = 2Z + iz (parent-aligned, parity-free)
       const double* src = win + ((iz & 1) * 2 + (iy & 1)) * kWSub + (Z + (iz >> 1)) * kWPZ +
                           (Y + (iy >> 1)) * kWPY;
