@@ -661,7 +661,10 @@ cudaError_t upload(const std::vector<T>& v, T** out) {
 
 // Algorithmic work of one solve (bench roofline): interactions with an
 // existing source, counted per neighbour-patch offset from the plan.
-void count_work(const GravPlan& P, long long out[5]) {
+// need: per-level node lists this GPU evaluates M2L for (nullptr = all);
+// [lo, hi): the canonical slots it evaluates L2P/P2P for.
+void count_work(const GravPlan& P, const std::vector<std::vector<int>>* need, long long lo,
+                long long hi, long long out[5]) {
   long long vtab[27] = {0}, ptab[27] = {0};
   for (int c = 0; c < 512; ++c) {
     const int i = c & 7, j = (c >> 3) & 7, k = c >> 6;
@@ -675,17 +678,29 @@ void count_work(const GravPlan& P, long long out[5]) {
           else if (dx || dy || dz) ++ptab[o];
         }
   }
-  long long v = 0, vk = 0, p = 0;
-  for (const GravLevel& L : P.lv)
-    for (int n = 0; n < L.n; ++n) {
+  long long v = 0, vk = 0, p = 0, wx = 0, u = 0;
+  for (int l = 0; l < P.nlevels; ++l) {
+    const GravLevel& L = P.lv[l];
+    auto node = [&](int n) {
       vk += 512 * 189;  // the kernel's 189 offsets x 512 targets
-      for (int o = 0; o < 27; ++o) {
-        const int nb = L.nbr[(size_t)n * 27 + o];
-        if (nb < 0) continue;
-        v += vtab[o];
-        if (L.leaf_slot[n] >= 0 && L.leaf_slot[nb] >= 0) p += ptab[o];
-      }
+      for (int o = 0; o < 27; ++o)
+        if (L.nbr[(size_t)n * 27 + o] >= 0) v += vtab[o];
+      wx += L.moff[(size_t)(n + 1) * 512] - L.moff[(size_t)n * 512];
+    };
+    if (need)
+      for (int n : (*need)[l]) node(n);
+    else
+      for (int n = 0; n < L.n; ++n) node(n);
+  }
+  for (long long s = lo; s < hi; ++s) {
+    const GravLevel& L = P.lv[P.slot_level[s]];
+    const int n = P.slot_node[s];
+    for (int o = 0; o < 27; ++o) {
+      const int nb = L.nbr[(size_t)n * 27 + o];
+      if (nb >= 0 && L.leaf_slot[nb] >= 0) p += ptab[o];
     }
+    u += L.poff[(size_t)(n + 1) * 512] - L.poff[(size_t)n * 512];
+  }
   // dense depth 2 (4^3 cells, every cell exists): the uniform 189-stencil
   for (int t = 0; t < 64; ++t) {
     const int i = t & 3, j = (t >> 2) & 3, k = t >> 4;
@@ -697,9 +712,9 @@ void count_work(const GravPlan& P, long long out[5]) {
         }
   }
   out[0] = v;
-  out[1] = P.m_entries;
+  out[1] = wx;
   out[2] = p;
-  out[3] = P.p_entries;
+  out[3] = u;
   out[4] = vk;
 }
 
@@ -824,7 +839,7 @@ tmgpu_gravity_amr* tmgpu_gravity_amr_create(const int* leaves, long long nleaves
     return nullptr;
   }
   const GravPlan& P = w.plan;
-  count_work(P, w.work);
+  count_work(P, nullptr, 0, nleaves, w.work);
   w.nslots = nleaves;
   w.hi = nleaves;
   while (w.P < nleaves) w.P <<= 1;
@@ -1136,6 +1151,7 @@ int tmgpu_gravity_amr_distribute(tmgpu_gravity_amr* G, tmgpu_comm* comm, const l
     if (w.need[l]) w.allocs.push_back(w.need[l]);
   }
   if (e == cudaSuccess) e = build_m2l_work(w, &lists);
+  count_work(P, &lists, w.lo, w.hi, w.work);  // this GPU's share (bench roofline)
   return cuda_err(err, e, "tmgpu_gravity_amr_distribute");
 }
 
@@ -1149,10 +1165,11 @@ int tmgpu_gravity_amr_am_stats(tmgpu_gravity_amr* G, double* out) {
              : TMGPU_ERR_CUDA;
 }
 
-// Algorithmic work of one solve: [0] V-list M2L pairs with an existing source
-// (incl. the dense depth-2 level), [1] W/X M2L entries, [2] same-depth P2P
-// pairs, [3] cross-depth U entries, [4] V-list pairs the kernel evaluates
-// (missing neighbour patches as zero moments).
+// Algorithmic work of one solve on this GPU (after tmgpu_gravity_amr_distribute:
+// its share): [0] V-list M2L pairs with an existing source (incl. the dense
+// depth-2 level), [1] W/X M2L entries, [2] same-depth P2P pairs, [3] cross-depth
+// U entries, [4] V-list pairs the kernel evaluates (missing neighbour patches as
+// zero moments).
 int tmgpu_gravity_amr_work(const tmgpu_gravity_amr* G, long long* out) {
   if (!G || !out) return TMGPU_ERR_INVALID;
   for (int q = 0; q < 5; ++q) out[q] = G->w.work[q];
