@@ -149,6 +149,9 @@ __global__ void amr_m2m_kernel(const GLv* __restrict__ L, int l, const int* __re
 // Accumulation per target: two partial sums (lower / upper source planes),
 // dz, dy, dx ascending, added; the W/X pairs follow in amr_wx_kernel —
 // tmo_grav_amr_solve's order, so the result is bitwise the oracle's.
+#ifndef TMGPU_M2L_SOURCE_MAJOR
+#define TMGPU_M2L_SOURCE_MAJOR 0
+#endif
 constexpr int kM2lThreads = 256;
 constexpr int kWPY = 13, kWPZ = 84, kWSub = 6 * kWPZ, kWVar = 4 * kWSub + 2;  // per var (+2: banks)
 constexpr int kWinDoubles = 10 * kWVar;                                   // 20,180
@@ -221,6 +224,36 @@ __device__ __forceinline__ void m2l_row(const double* __restrict__ src, const do
   }
 }
 
+// Offset-major variant: per x-offset jj, the geometry (13 registers) is loaded
+// once and applied to the four targets' sources sx = jj + 2k — independent
+// accumulators, so four FMA chains are in flight per thread; every source is
+// loaded twice per row. Each target still sees its sources in dx order.
+template <bool NEAR>
+__device__ __forceinline__ void m2l_row_jj(const double* __restrict__ src,
+                                           const double* __restrict__ trow, double (&acc)[4][10]) {
+#pragma unroll
+  for (int jj = 0; jj < 6; ++jj) {
+    if (NEAR && (jj == 2 || jj == 3)) continue;
+    double G[kTab];
+    const double2* t2 = reinterpret_cast<const double2*>(trow + jj * kTabP);
+#pragma unroll
+    for (int q = 0; q < 6; ++q) {
+      const double2 v = t2[q];
+      G[2 * q] = v.x;
+      G[2 * q + 1] = v.y;
+    }
+    G[12] = trow[jj * kTabP + 12];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int sx = jj + 2 * k;
+      double m[10];
+#pragma unroll
+      for (int q = 0; q < 10; ++q) m[q] = src[q * kWVar + sx];
+      m2l_acc(-m[0], m[1], m[2], m[3], -m[4], -m[5], -m[6], -m[7], -m[8], -m[9], G, acc[k]);
+    }
+  }
+}
+
 __device__ __forceinline__ void cp_async8(double* smem, const double* gmem, bool valid) {
   const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(sa), "l"(gmem),
@@ -285,6 +318,10 @@ __global__ void __launch_bounds__(kM2lThreads, 1) amr_m2l_fused_kernel(
     for (int iy = 0; iy < 6; ++iy) {
       const int dy = iy - 2 - b;
       const double* trow = tab_lane + ((dz + 3) * kOff + (dy + 3)) * kOff * kTabP;
+      // source row: window y = 2Y + iy, z = 2Z + iz (parent-aligned, parity-free)
+      const double* src = win + ((iz & 1) * 2 + (iy & 1)) * kWSub + (Z + (iz >> 1)) * kWPZ +
+                          (Y + (iy >> 1)) * kWPY;
+#if TMGPU_M2L_SOURCE_MAJOR
       double G[6][kTab];
 #pragma unroll
       for (int jj = 0; jj < 6; ++jj) {
@@ -297,13 +334,16 @@ __global__ void __launch_bounds__(kM2lThreads, 1) amr_m2l_fused_kernel(
         }
         G[jj][12] = trow[jj * kTabP + 12];
       }
-      // source row: window y = 2Y + iy, z = 2Z + iz (parent-aligned, parity-free)
-      const double* src = win + ((iz & 1) * 2 + (iy & 1)) * kWSub + (Z + (iz >> 1)) * kWPZ +
-                          (Y + (iy >> 1)) * kWPY;
       if (dz >= -1 && dz <= 1 && dy >= -1 && dy <= 1)
         m2l_row<true>(src, G, acc);
       else
         m2l_row<false>(src, G, acc);
+#else
+      if (dz >= -1 && dz <= 1 && dy >= -1 && dy <= 1)
+        m2l_row_jj<true>(src, trow, acc);
+      else
+        m2l_row_jj<false>(src, trow, acc);
+#endif
     }
   }
   // upper-half warps hand their partial sums to the lower-half warps (the

@@ -17,8 +17,58 @@ __global__ void __launch_bounds__(256) dfma_kernel(double* out, int iters, doubl
   for (int k = 0; k < 8; ++k) s += x[k];
   if (s == 12345.678) out[0] = s;  // never true; keeps the chains live
 }
+// latency/occupancy probe: C independent DFMA chains per thread
+template <int C>
+__global__ void dfma_chains_kernel(double* out, int iters, double a, double b) {
+  double x[C];
+#pragma unroll
+  for (int k = 0; k < C; ++k) x[k] = threadIdx.x * 1e-3 + k;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int k = 0; k < C; ++k) x[k] = fma(x[k], a, b);
+  }
+  double s = 0;
+#pragma unroll
+  for (int k = 0; k < C; ++k) s += x[k];
+  if (s == 12345.678) out[0] = s;
+}
 }  // namespace
 }  // namespace tmgpu
+
+// Diagnostics: DFMA TFLOP/s with `warps` warps per SM (one CTA per SM) and
+// `chains` (1, 2, 4, 8, 16) independent FMA chains per thread.
+extern "C" int tmgpu_fp64_probe(int warps, int chains, int iters, double* tflops) {
+  using namespace tmgpu;
+  double* d = nullptr;
+  if (cudaMalloc(&d, sizeof(double)) != cudaSuccess) return TMGPU_ERR_CUDA;
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  auto launch = [&](int it) {
+    switch (chains) {
+      case 1: dfma_chains_kernel<1><<<sms, 32 * warps>>>(d, it, 0.999999, 1e-7); break;
+      case 2: dfma_chains_kernel<2><<<sms, 32 * warps>>>(d, it, 0.999999, 1e-7); break;
+      case 4: dfma_chains_kernel<4><<<sms, 32 * warps>>>(d, it, 0.999999, 1e-7); break;
+      case 8: dfma_chains_kernel<8><<<sms, 32 * warps>>>(d, it, 0.999999, 1e-7); break;
+      default: dfma_chains_kernel<16><<<sms, 32 * warps>>>(d, it, 0.999999, 1e-7); chains = 16;
+    }
+  };
+  cudaEvent_t t0, t1;
+  cudaEventCreate(&t0);
+  cudaEventCreate(&t1);
+  launch(iters / 10 + 1);
+  cudaEventRecord(t0);
+  launch(iters);
+  cudaEventRecord(t1);
+  cudaError_t e = cudaEventSynchronize(t1);
+  float msf = 0;
+  cudaEventElapsedTime(&msf, t0, t1);
+  cudaEventDestroy(t0);
+  cudaEventDestroy(t1);
+  cudaFree(d);
+  if (e != cudaSuccess) return TMGPU_ERR_CUDA;
+  *tflops = 2.0 * chains * (double)iters * sms * 32.0 * warps / (msf * 1e-3) / 1e12;
+  return TMGPU_OK;
+}
 
 extern "C" int tmgpu_fp64_peak(int iters, double* tflops, double* ms, tmgpu_error* err) {
   using namespace tmgpu;

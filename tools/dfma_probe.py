@@ -1,0 +1,18 @@
+"""DFMA throughput vs warps per SM and independent chains per thread (the FP64
+latency/occupancy trade-off behind the M2L kernel's 8 warps per SM)."""
+import ctypes as C
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2412_15518_b200 import _lib  # noqa: E402
+
+f = _lib.lib.tmgpu_fp64_probe
+f.argtypes = [C.c_int, C.c_int, C.c_int, C.POINTER(C.c_double)]
+for warps in (4, 8, 16, 32):
+    row = []
+    for chains in (1, 2, 4, 8, 16):
+        t = C.c_double()
+        f(warps, chains, 20000, C.byref(t))
+        row.append(f"{t.value:6.2f}")
+    print(f"warps/SM {warps:2d}: chains 1,2,4,8,16 -> TFLOP/s", " ".join(row))
