@@ -234,7 +234,7 @@ int tmgpu_gravity_amr_distribute(tmgpu_gravity_amr* G, tmgpu_comm* comm, const l
  * M2L/L2L for; returns the level count (negative error code on failure) */
 int tmgpu_gravity_amr_plan_need(const int* leaves, long long nleaves, long long lo, long long hi,
                                 long long* counts, int max_levels, tmgpu_error* err);
-/* per-phase device timing: totals in ms of [up, m2l, l2l, l2p, am] */
+/* per-phase device timing: totals in ms of [comm, up, m2l, l2l, l2p, am] */
 int tmgpu_gravity_amr_set_timing(tmgpu_gravity_amr* G, int on);
 int tmgpu_gravity_amr_timing(tmgpu_gravity_amr* G, double* ms, long long* solves);
 const double* tmgpu_gravity_amr_mass_ptr(const tmgpu_gravity_amr* G);

@@ -23,6 +23,8 @@ struct Api {
                             cudaStream_t) = nullptr;
   ncclResult_t (*Broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t,
                             cudaStream_t) = nullptr;
+  ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
   const char* (*GetErrorString)(ncclResult_t) = nullptr;
   std::string error;
 };
@@ -47,9 +49,10 @@ Api& api() {
     a.GroupEnd = (decltype(a.GroupEnd))sym("ncclGroupEnd");
     a.AllReduce = (decltype(a.AllReduce))sym("ncclAllReduce");
     a.Broadcast = (decltype(a.Broadcast))sym("ncclBroadcast");
+    a.AllGather = (decltype(a.AllGather))sym("ncclAllGather");
     a.GetErrorString = (decltype(a.GetErrorString))sym("ncclGetErrorString");
     if (!a.GetUniqueId || !a.CommInitRank || !a.Send || !a.Recv || !a.GroupStart || !a.GroupEnd ||
-        !a.AllReduce || !a.Broadcast)
+        !a.AllReduce || !a.Broadcast || !a.AllGather)
       a.error = "libnccl.so.2 lacks required symbols";
   });
   return a;
@@ -97,6 +100,16 @@ int comm_allreduce_min(tmgpu_comm* c, double* buf, size_t n, cudaStream_t st, st
   ncclResult_t r = api().AllReduce(buf, buf, n, ncclDouble, ncclMin, c->comm, st);
   if (r != ncclSuccess) {
     if (why) *why = "dt allreduce: " + nerr(r);
+    return TMGPU_ERR_CUDA;
+  }
+  return TMGPU_OK;
+}
+
+int comm_allgather(tmgpu_comm* c, const double* send, double* recv, size_t count, cudaStream_t st,
+                   std::string* why) {
+  ncclResult_t r = api().AllGather(send, recv, count, ncclDouble, c->comm, st);
+  if (r != ncclSuccess) {
+    if (why) *why = "allgather: " + nerr(r);
     return TMGPU_ERR_CUDA;
   }
   return TMGPU_OK;

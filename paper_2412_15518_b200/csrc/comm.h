@@ -21,6 +21,9 @@ int comm_exchange(tmgpu_comm* c, const double* send, const std::vector<long long
                   const std::vector<long long>& send_cnt, double* recv,
                   const std::vector<long long>& recv_off, const std::vector<long long>& recv_cnt,
                   cudaStream_t st, std::string* why);
+// ncclAllGather of `count` doubles per rank into recv[world * count].
+int comm_allgather(tmgpu_comm* c, const double* send, double* recv, size_t count, cudaStream_t st,
+                   std::string* why);
 // In-place all-gather of variable segments: rank p contributes
 // buf[off[p] .. +cnt[p]) (grouped ncclBroadcast, root p), every rank ends with all.
 int comm_allgatherv(tmgpu_comm* c, double* buf, const std::vector<long long>& off,

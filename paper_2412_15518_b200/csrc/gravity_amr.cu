@@ -759,7 +759,7 @@ void count_work(const GravPlan& P, const std::vector<std::vector<int>>* need, lo
 }
 
 // per-phase device timing of solves (bench): events at the phase boundaries
-constexpr int kGravPhases = 5;  // up (P2M, M2M, dense), m2l, l2l, l2p, am
+constexpr int kGravPhases = 6;  // comm (mass all-gather), up (P2M, M2M, dense), m2l, l2l, l2p, am
 struct GravTimingRec {
   cudaEvent_t ev[kGravPhases + 1];
 };
@@ -769,7 +769,7 @@ struct GravAmrWork {
   long long work[5] = {0, 0, 0, 0, 0};
   bool timing = false;
   std::vector<GravTimingRec> pending;
-  double phase_ms[kGravPhases] = {0, 0, 0, 0, 0};
+  double phase_ms[kGravPhases] = {0, 0, 0, 0, 0, 0};
   long long timed_solves = 0;
   std::vector<GLv> host_lv;
   std::vector<void*> allocs;
@@ -790,6 +790,8 @@ struct GravAmrWork {
   tmgpu_comm* comm = nullptr;
   long long lo = 0, hi = 0;
   std::vector<long long> seg_lo, seg_cnt;  // per rank (slots)
+  long long seg_max = 0;                   // largest rank segment (slots)
+  double* gather = nullptr;                // [world][seg_max][512] all-gather staging
   std::vector<int*> need;                  // per level device node list (nullptr = all)
   std::vector<long long> nneed;
   int2* m2l_work = nullptr;  // fused M2L launch: (level, node) per CTA
@@ -1052,11 +1054,20 @@ int tmgpu_gravity_amr_solve(tmgpu_gravity_amr* G, const double* mass, double* ph
     cudaEventRecord(rec.ev[0], st);
   }
   int rc = TMGPU_OK;
-  if (e == cudaSuccess && w.comm) {  // every rank needs every leaf mass for the upward pass
-    std::vector<long long> off(w.seg_lo.size()), cnt(w.seg_cnt.size());
-    for (size_t r = 0; r < off.size(); ++r) off[r] = w.seg_lo[r] * 512, cnt[r] = w.seg_cnt[r] * 512;
-    rc = comm_allgatherv(w.comm, w.mass, off, cnt, st, &why);
+  if (e == cudaSuccess && w.comm) {
+    // every rank needs every leaf mass for the upward pass: one ncclAllGather
+    // of the padded per-rank segments, then each segment into place
+    const int R = (int)w.seg_lo.size();
+    const size_t per = (size_t)w.seg_max * 512;
+    double* mine = w.gather + (size_t)comm_rank(w.comm) * per;
+    e = cudaMemcpyAsync(mine, w.mass + w.lo * 512, nout * sizeof(double), cudaMemcpyDeviceToDevice, st);
+    if (e == cudaSuccess) rc = comm_allgather(w.comm, mine, w.gather, per, st, &why);
+    for (int r = 0; r < R && e == cudaSuccess && rc == TMGPU_OK; ++r)
+      if (r != comm_rank(w.comm) && w.seg_cnt[r])
+        e = cudaMemcpyAsync(w.mass + w.seg_lo[r] * 512, w.gather + (size_t)r * per,
+                            (size_t)w.seg_cnt[r] * 512 * sizeof(double), cudaMemcpyDeviceToDevice, st);
   }
+  if (timed) cudaEventRecord(rec.ev[1], st);
   if (e == cudaSuccess && rc == TMGPU_OK) {
     long long launches = 0;
     amr_p2m_kernel<<<grid_for(ncell * 5), 128, 0, st>>>(w.mass, w.nslots, w.slot_level, w.slot_node,
@@ -1077,7 +1088,7 @@ int tmgpu_gravity_amr_solve(tmgpu_gravity_amr* G, const double* mass, double* ph
     m2l_kernel<<<1, 128, 0, w.side>>>(w.dmom[2], w.dloc[2], 4, w.tab + 2LL * kOff3 * kTab);
     cudaEventRecord(w.ev_join, w.side);
     launches += 4;
-    if (timed) cudaEventRecord(rec.ev[1], st);
+    if (timed) cudaEventRecord(rec.ev[2], st);
     {
       if (w.m2l_ctas) {
         amr_m2l_fused_kernel<<<(unsigned)w.m2l_ctas, kM2lThreads, kM2lSmem, st>>>(w.dev_lv, w.m2l_work,
@@ -1091,7 +1102,7 @@ int tmgpu_gravity_amr_solve(tmgpu_gravity_amr* G, const double* mass, double* ph
       }
     }
     cudaStreamWaitEvent(st, w.ev_join, 0);
-    if (timed) cudaEventRecord(rec.ev[2], st);
+    if (timed) cudaEventRecord(rec.ev[3], st);
     l2l_kernel<<<grid_for(512), 128, 0, st>>>(w.dloc[2], w.host_lv[0].loc, 8, 1.0 / 8.0);
     ++launches;
     for (int l = 1; l < P.nlevels; ++l) {
@@ -1099,12 +1110,12 @@ int tmgpu_gravity_amr_solve(tmgpu_gravity_amr* G, const double* mass, double* ph
       amr_l2l_kernel<<<grid_for(w.nneed[l] * 512), 128, 0, st>>>(w.dev_lv, l, w.nneed[l], w.need[l]);
       ++launches;
     }
-    if (timed) cudaEventRecord(rec.ev[3], st);
+    if (timed) cudaEventRecord(rec.ev[4], st);
     if (nloc)
       amr_l2p_kernel<<<(unsigned)(nloc * 4), 128, 0, st>>>(w.dev_lv, nloc, w.lo, w.slot_level,
                                                            w.slot_node, w.mass, w.u_geo, dphi, dg);
     ++launches;
-    if (timed) cudaEventRecord(rec.ev[4], st);
+    if (timed) cudaEventRecord(rec.ev[5], st);
     if (flags & TMGPU_GRAV_AM) {
       e = cudaMemsetAsync(w.part, 0, (size_t)w.P * 16 * sizeof(double), st);
       if (nloc)
@@ -1176,7 +1187,21 @@ int tmgpu_gravity_amr_distribute(tmgpu_gravity_amr* G, tmgpu_comm* comm, const l
   w.hi = slot_bounds[me + 1];
   w.seg_lo.assign(slot_bounds, slot_bounds + R);
   w.seg_cnt.resize(R);
-  for (int r = 0; r < R; ++r) w.seg_cnt[r] = slot_bounds[r + 1] - slot_bounds[r];
+  w.seg_max = 0;
+  for (int r = 0; r < R; ++r) {
+    w.seg_cnt[r] = slot_bounds[r + 1] - slot_bounds[r];
+    w.seg_max = std::max(w.seg_max, w.seg_cnt[r]);
+  }
+  if (w.gather) {
+    cudaFree(w.gather);
+    w.allocs.erase(std::find(w.allocs.begin(), w.allocs.end(), (void*)w.gather));
+    w.gather = nullptr;
+  }
+  {
+    cudaError_t e0 = cudaMalloc(&w.gather, (size_t)R * (w.seg_max ? w.seg_max : 1) * 512 * sizeof(double));
+    if (e0 != cudaSuccess) return cuda_err(err, e0, "tmgpu_gravity_amr_distribute");
+    w.allocs.push_back(w.gather);
+  }
   cudaError_t e = cudaSuccess;
   std::vector<std::vector<int>> lists = grav_owned_ancestors(P, w.lo, w.hi);
   for (int l = 0; l < P.nlevels && e == cudaSuccess; ++l) {
@@ -1218,7 +1243,7 @@ int tmgpu_gravity_amr_work(const tmgpu_gravity_amr* G, long long* out) {
 
 // Per-phase device timing (CUDA events on the solve's stream): on != 0 starts
 // recording (and clears the totals); tmgpu_gravity_amr_timing syncs on the
-// recorded events and returns ms totals [up, m2l, l2l, l2p, am] and the count.
+// recorded events and returns ms totals [comm, up, m2l, l2l, l2p, am] and the count.
 int tmgpu_gravity_amr_set_timing(tmgpu_gravity_amr* G, int on) {
   if (!G) return TMGPU_ERR_INVALID;
   GravAmrWork& w = G->w;

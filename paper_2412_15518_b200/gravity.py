@@ -248,11 +248,11 @@ class GravityAMR:
     def set_timing(self, on: bool) -> None:
         lib.tmgpu_gravity_amr_set_timing(self.h, int(on))
 
-    PHASES = ("up", "m2l", "l2l", "l2p", "am")
+    PHASES = ("comm", "up", "m2l", "l2l", "l2p", "am")
 
     def timing(self):
         """(ms totals per phase, solves timed) since set_timing(True)."""
-        ms = (C.c_double * 5)()
+        ms = (C.c_double * 6)()
         n = C.c_longlong()
         _lib.check(lib.tmgpu_gravity_amr_timing(self.h, ms, C.byref(n)), TmgpuError())
         return dict(zip(self.PHASES, ms)), n.value
