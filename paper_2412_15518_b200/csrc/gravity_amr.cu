@@ -433,86 +433,116 @@ __global__ void sep_geom_kernel(const double* __restrict__ sep, long long n, dou
   }
 }
 
+// parent local (Lp, 10) shifted to the child centre s (tmo_grav_l2l): the
+// first NOUT components (L2P needs only L0 and L_i)
+template <int NOUT>
+__device__ __forceinline__ void l2l_shift(const double* __restrict__ Lp, const double s[3],
+                                          double sh[NOUT]) {
+  double Lm[3][3];
+#pragma unroll
+  for (int a = 0; a < 3; ++a)
+#pragma unroll
+    for (int b = 0; b < 3; ++b) Lm[a][b] = Lp[4 + s2(a, b)];
+  double t1 = 0.0, t2 = 0.0;
+#pragma unroll
+  for (int a = 0; a < 3; ++a) t1 += Lp[1 + a] * s[a];
+#pragma unroll
+  for (int a = 0; a < 3; ++a)
+#pragma unroll
+    for (int b = 0; b < 3; ++b) t2 += Lm[a][b] * s[a] * s[b];
+  sh[0] = Lp[0] + t1 + 0.5 * t2;
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    double u = 0.0;
+#pragma unroll
+    for (int b = 0; b < 3; ++b) u += Lm[a][b] * s[b];
+    sh[1 + a] = Lp[1 + a] + u;
+  }
+#pragma unroll
+  for (int q = 4; q < NOUT; ++q) sh[q] = Lp[q];
+}
+
+// parent's cell and the child-centre offset of cell c of node n at level l
+__device__ __forceinline__ const double* l2l_parent(const GLv& L, const GLv& P, long long n, int c,
+                                                   double h, double s[3]) {
+  const int i = c & 7, j = (c >> 3) & 7, k = c >> 6;
+  const int pn = L.parent[n];
+  const int pi = (L.ijk[3 * n] & 1) * 4 + (i >> 1), pj = (L.ijk[3 * n + 1] & 1) * 4 + (j >> 1),
+            pk = (L.ijk[3 * n + 2] & 1) * 4 + (k >> 1);
+  s[0] = ((i & 1) - 0.5) * h;
+  s[1] = ((j & 1) - 0.5) * h;
+  s[2] = ((k & 1) - 0.5) * h;
+  return P.loc + ((long long)pn * 512 + (pk * 8 + pj) * 8 + pi) * 10;
+}
+
+// L2L of the internal patches of level l (leaf patches get theirs inside L2P)
 __global__ void amr_l2l_kernel(const GLv* __restrict__ Lv, int l, long long nnodes,
                                const int* __restrict__ nodes) {
   const GLv L = Lv[l], P = Lv[l - 1];
   const double h = 1.0 / (double)(1LL << (l + 3));
   for (long long tt = blockIdx.x * (long long)blockDim.x + threadIdx.x; tt < nnodes * 512;
        tt += (long long)gridDim.x * blockDim.x) {
-    const long long n = nodes ? nodes[tt >> 9] : tt >> 9;
+    const long long n = nodes[tt >> 9];
     const int c = (int)(tt & 511);
-    const long long t = n * 512 + c;
-    const int i = c & 7, j = (c >> 3) & 7, k = c >> 6;
-    const int pn = L.parent[n];
-    const int pi = (L.ijk[3 * n] & 1) * 4 + (i >> 1), pj = (L.ijk[3 * n + 1] & 1) * 4 + (j >> 1),
-              pk = (L.ijk[3 * n + 2] & 1) * 4 + (k >> 1);
-    const double* Lp = P.loc + ((long long)pn * 512 + (pk * 8 + pj) * 8 + pi) * 10;
-    const double s[3] = {((i & 1) - 0.5) * h, ((j & 1) - 0.5) * h, ((k & 1) - 0.5) * h};
-    double Lm[3][3];
-#pragma unroll
-    for (int a = 0; a < 3; ++a)
-#pragma unroll
-      for (int b = 0; b < 3; ++b) Lm[a][b] = Lp[4 + s2(a, b)];
-    double t1 = 0.0, t2 = 0.0;
-#pragma unroll
-    for (int a = 0; a < 3; ++a) t1 += Lp[1 + a] * s[a];
-#pragma unroll
-    for (int a = 0; a < 3; ++a)
-#pragma unroll
-      for (int b = 0; b < 3; ++b) t2 += Lm[a][b] * s[a] * s[b];
-    double sh[10];
-    sh[0] = Lp[0] + t1 + 0.5 * t2;
-#pragma unroll
-    for (int a = 0; a < 3; ++a) {
-      double u = 0.0;
-#pragma unroll
-      for (int b = 0; b < 3; ++b) u += Lm[a][b] * s[b];
-      sh[1 + a] = Lp[1 + a] + u;
-    }
-#pragma unroll
-    for (int q = 0; q < 6; ++q) sh[4 + q] = Lp[4 + q];
-    double* out = L.loc + t * 10;
+    double s[3], sh[10];
+    l2l_shift<10>(l2l_parent(L, P, n, c, h, s), s, sh);
+    double* out = L.loc + (n * 512 + c) * 10;
 #pragma unroll
     for (int q = 0; q < 10; ++q) out[q] = sh[q] + out[q];
   }
 }
 
 // L2P + P2P at the leaf cells, output by local slot: phi[s*512 + c],
-// g[q*ncell + s*512 + c]. CTA = 128 cells of one slot (4 CTAs per slot): the
-// 26 same-depth offsets' P2P geometry (p2p_geom of the lattice offset, the
-// same operations as per pair) and the 27 neighbour slots are resolved once
-// into shared memory; neighbour masses come from the leaf-mass array (8-byte,
-// coalesced across the warp), cross-depth U pairs from the plan's geometry
-// table. Term order: 26 offsets dz, dy, dx ascending, then the U pairs.
-__global__ void __launch_bounds__(128) amr_l2p_kernel(const GLv* __restrict__ Lv, long long nslots,
+// g[q*ncell + s*512 + c]. CTA = one slot (512 cells). The leaf patch's L2L is
+// done here (L_q = shift(parent)_q + own M2L sum_q for q = 0..3, the only
+// components L2P uses; level-0 leaves have their final locals). The 26
+// same-depth offsets' P2P geometry (p2p_geom of the lattice offset, the same
+// operations as per pair) and the 27 neighbour slots are resolved once into
+// shared memory; neighbour masses come from the leaf-mass array (coalesced),
+// cross-depth U pairs from the plan's geometry table. Term order: 26 offsets
+// dz, dy, dx ascending, then the U pairs. With `part`, the slot's 16
+// angular-momentum sums follow (am_block_sums: the per-slot pair tree).
+__device__ __forceinline__ void cell_pos(const GLv* __restrict__ Lv, int l, int n, int c, double x[3]);
+__device__ __forceinline__ void am_block_sums(double m, const double x[3], double gx, double gy,
+                                              double gz, double* __restrict__ out16);
+
+__global__ void __launch_bounds__(512) amr_l2p_kernel(const GLv* __restrict__ Lv, long long nslots,
                                                       long long lo, const int* __restrict__ slot_level,
                                                       const int* __restrict__ slot_node,
                                                       const double* __restrict__ mass,
                                                       const double* __restrict__ ugeo,
-                                                      double* __restrict__ phi, double* __restrict__ g) {
+                                                      double* __restrict__ phi, double* __restrict__ g,
+                                                      double* __restrict__ part) {
   __shared__ double w26[27][4];
   __shared__ long long nbslot[27];
-  const long long ls = blockIdx.x >> 2;  // local slot
+  const long long ls = blockIdx.x;  // local slot
   const long long s = lo + ls;
   const int l = slot_level[s], n = slot_node[s];
   const GLv L = Lv[l];
   const int d = l + 3;
+  const double h = 1.0 / (double)(1LL << d);
   if (threadIdx.x < 27) {
     const int o = threadIdx.x;
     const int dx = o % 3 - 1, dy = (o / 3) % 3 - 1, dz = o / 9 - 1;
-    const double h = 1.0 / (double)(1LL << d);
     if (o != 13) p2p_geom(-(double)dx * h, -(double)dy * h, -(double)dz * h, w26[o]);
     const int nb = L.nbr[(long long)n * 27 + o];
     nbslot[o] = (nb >= 0 && L.leaf_slot[nb] >= 0) ? (long long)L.leaf_slot[nb] : -1;
   }
   __syncthreads();
   const long long ncell = nslots * 512;
-  const int c = (int)((blockIdx.x & 3) * 128 + threadIdx.x);
+  const int c = threadIdx.x;
   const int i = c & 7, j = (c >> 3) & 7, k = c >> 6;
   const long long flat = (long long)n * 512 + c;
   const double2* Lc = reinterpret_cast<const double2*>(L.loc + flat * 10);
   const double2 l01 = Lc[0], l23 = Lc[1];
-  double p = l01.x, gx = -l01.y, gy = -l23.x, gz = -l23.y;
+  double loc4[4] = {l01.x, l01.y, l23.x, l23.y};
+  if (l > 0) {
+    double sv[3], sh[4];
+    l2l_shift<4>(l2l_parent(L, Lv[l - 1], n, c, h, sv), sv, sh);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) loc4[q] = sh[q] + loc4[q];
+  }
+  double p = loc4[0], gx = -loc4[1], gy = -loc4[2], gz = -loc4[3];
 #pragma unroll
   for (int dz = -1; dz <= 1; ++dz)
 #pragma unroll
@@ -548,6 +578,11 @@ __global__ void __launch_bounds__(128) amr_l2p_kernel(const GLv* __restrict__ Lv
   g[t] = gx;
   g[ncell + t] = gy;
   g[2 * ncell + t] = gz;
+  if (part) {
+    double x[3];
+    cell_pos(Lv, l, n, c, x);
+    am_block_sums(mass[s * 512 + c], x, gx, gy, gz, part + s * 16);
+  }
 }
 
 // ---- angular-momentum correction (tmo_grav_am_correct) ---------------------
@@ -560,22 +595,12 @@ __device__ __forceinline__ void cell_pos(const GLv* __restrict__ Lv, int l, int 
   x[2] = centre(8LL * L.ijk[3 * n + 2] + (c >> 6), d);
 }
 
-// one CTA (512 threads) per slot: adjacent-pair tree over its 512 cells
-// block b = local slot b (canonical slot lo + b): g local [3][nslots*512]
-__global__ void __launch_bounds__(512) am_slot_kernel(const GLv* __restrict__ Lv, long long nslots,
-                                                      long long lo,
-                                                      const int* __restrict__ slot_level,
-                                                      const int* __restrict__ slot_node,
-                                                      const double* __restrict__ mass,
-                                                      const double* __restrict__ g,
-                                                      double* __restrict__ part) {
+// one CTA (512 threads) = one slot: adjacent-pair tree over its 512 cells'
+// 16 values (warp shuffles, then one thread per value over the 16 warps)
+__device__ __forceinline__ void am_block_sums(double m, const double x[3], double gx, double gy,
+                                              double gz, double* __restrict__ out16) {
   __shared__ double red[16][16];  // [warp][value]
-  const long long s = lo + blockIdx.x;
   const int c = threadIdx.x;
-  const long long ncell = nslots * 512, t = (long long)blockIdx.x * 512 + c;
-  double x[3];
-  cell_pos(Lv, slot_level[s], slot_node[s], c, x);
-  const double m = mass[s * 512 + c], gx = g[t], gy = g[ncell + t], gz = g[2 * ncell + t];
   double v[16];
   v[0] = m;
   v[1] = m * x[0];
@@ -613,7 +638,7 @@ __global__ void __launch_bounds__(512) am_slot_kernel(const GLv* __restrict__ Lv
     for (int st = 1; st < 16; st <<= 1)
 #pragma unroll
       for (int a = 0; a < 16; a += 2 * st) w[a] = w[a] + w[a + st];
-    part[s * 16 + c] = w[0];
+    out16[c] = w[0];
   }
 }
 
@@ -794,6 +819,8 @@ struct GravAmrWork {
   double* gather = nullptr;                // [world][seg_max][512] all-gather staging
   std::vector<int*> need;                  // per level device node list (nullptr = all)
   std::vector<long long> nneed;
+  std::vector<int*> l2l_nodes;      // per level: internal patches needing L2L
+  std::vector<long long> nl2l;
   int2* m2l_work = nullptr;  // fused M2L launch: (level, node) per CTA
   long long m2l_ctas = 0;
   int* wx_tlev = nullptr;         // W/X kernel targets (level, flat), by entry count
@@ -804,6 +831,32 @@ struct GravAmrWork {
   cudaStream_t side = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
 };
+
+// internal patches that need the L2L pass, per level (leaf patches: in L2P)
+static cudaError_t build_l2l_lists(GravAmrWork& w, const std::vector<std::vector<int>>* need) {
+  const GravPlan& P = w.plan;
+  for (auto* p : w.l2l_nodes)
+    if (p) {
+      cudaFree(p);
+      w.allocs.erase(std::find(w.allocs.begin(), w.allocs.end(), (void*)p));
+    }
+  w.l2l_nodes.assign(P.nlevels, nullptr);
+  w.nl2l.assign(P.nlevels, 0);
+  cudaError_t e = cudaSuccess;
+  for (int l = 1; l < P.nlevels && e == cudaSuccess; ++l) {
+    std::vector<int> ids;
+    if (need) {
+      for (int n : (*need)[l])
+        if (P.lv[l].leaf_slot[n] < 0) ids.push_back(n);
+    } else {
+      ids = P.lv[l].internal;
+    }
+    w.nl2l[l] = (long long)ids.size();
+    e = upload(ids, &w.l2l_nodes[l]);
+    if (w.l2l_nodes[l]) w.allocs.push_back(w.l2l_nodes[l]);
+  }
+  return e;
+}
 
 // (level, node) list of the fused M2L launch: every needed node of every level
 static cudaError_t build_m2l_work(GravAmrWork& w, const std::vector<std::vector<int>>* need) {
@@ -946,6 +999,7 @@ tmgpu_gravity_amr* tmgpu_gravity_amr_create(const int* leaves, long long nleaves
     e = cudaFuncSetAttribute(amr_m2l_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)kM2lSmem);
   if (e == cudaSuccess) e = build_m2l_work(w, nullptr);
+  if (e == cudaSuccess) e = build_l2l_lists(w, nullptr);
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&w.side, cudaStreamNonBlocking);
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&w.ev_fork, cudaEventDisableTiming);
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&w.ev_join, cudaEventDisableTiming);
@@ -1106,21 +1160,19 @@ int tmgpu_gravity_amr_solve(tmgpu_gravity_amr* G, const double* mass, double* ph
     l2l_kernel<<<grid_for(512), 128, 0, st>>>(w.dloc[2], w.host_lv[0].loc, 8, 1.0 / 8.0);
     ++launches;
     for (int l = 1; l < P.nlevels; ++l) {
-      if (!w.nneed[l]) continue;
-      amr_l2l_kernel<<<grid_for(w.nneed[l] * 512), 128, 0, st>>>(w.dev_lv, l, w.nneed[l], w.need[l]);
+      if (!w.nl2l[l]) continue;
+      amr_l2l_kernel<<<grid_for(w.nl2l[l] * 512), 128, 0, st>>>(w.dev_lv, l, w.nl2l[l], w.l2l_nodes[l]);
       ++launches;
     }
     if (timed) cudaEventRecord(rec.ev[4], st);
+    const bool am = (flags & TMGPU_GRAV_AM) != 0;
+    if (am) e = cudaMemsetAsync(w.part, 0, (size_t)w.P * 16 * sizeof(double), st);
     if (nloc)
-      amr_l2p_kernel<<<(unsigned)(nloc * 4), 128, 0, st>>>(w.dev_lv, nloc, w.lo, w.slot_level,
-                                                           w.slot_node, w.mass, w.u_geo, dphi, dg);
+      amr_l2p_kernel<<<(unsigned)nloc, 512, 0, st>>>(w.dev_lv, nloc, w.lo, w.slot_level, w.slot_node,
+                                                     w.mass, w.u_geo, dphi, dg, am ? w.part : nullptr);
     ++launches;
     if (timed) cudaEventRecord(rec.ev[5], st);
-    if (flags & TMGPU_GRAV_AM) {
-      e = cudaMemsetAsync(w.part, 0, (size_t)w.P * 16 * sizeof(double), st);
-      if (nloc)
-        am_slot_kernel<<<(unsigned)nloc, 512, 0, st>>>(w.dev_lv, nloc, w.lo, w.slot_level, w.slot_node,
-                                                       w.mass, dg, w.part);
+    if (am) {  // the per-slot sums came with L2P
       if (w.comm && e == cudaSuccess) {  // identical global pair tree on every rank
         std::vector<long long> off(w.seg_lo.size()), cnt(w.seg_cnt.size());
         for (size_t r = 0; r < off.size(); ++r) off[r] = w.seg_lo[r] * 16, cnt[r] = w.seg_cnt[r] * 16;
@@ -1216,6 +1268,7 @@ int tmgpu_gravity_amr_distribute(tmgpu_gravity_amr* G, tmgpu_comm* comm, const l
     if (w.need[l]) w.allocs.push_back(w.need[l]);
   }
   if (e == cudaSuccess) e = build_m2l_work(w, &lists);
+  if (e == cudaSuccess) e = build_l2l_lists(w, &lists);
   count_work(P, &lists, w.lo, w.hi, w.work);  // this GPU's share (bench roofline)
   return cuda_err(err, e, "tmgpu_gravity_amr_distribute");
 }
