@@ -402,25 +402,27 @@ def run_ours(args, rank, world):
     roofline["step_share"] = share
     roofline["gravity_work"] = work or None
 
-    # e2e through the public API with host buffers (pinned), per step:
-    # H2D of the state, one step, D2H of the updated state.
+    # e2e through the public API with host buffers (pinned): every step moves
+    # its whole input H2D and its whole result D2H; HostStepPipeline overlaps
+    # step k+1's H2D and step k-1's D2H with step k's compute (copy streams,
+    # double-buffered staging). Timed from the first H2D to the last D2H.
+    from paper_2412_15518_b200.driver import HostStepPipeline
+
     pin_in = torch.from_numpy(np.ascontiguousarray(state)).pin_memory()
     pin_out = torch.empty_like(pin_in).pin_memory()
-    f.set_interior(pin_in)
-    drv.step(stream=sp)
+    pipe = HostStepPipeline(drv)
+    for _ in range(2):
+        pipe.step(pin_in, pin_out)
+    pipe.synchronize()
     barrier()
-    e2 = []
-    for _ in range(max(3, min(args.steps, 10))):
-        a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a0.record(stream)
-        f.set_interior(pin_in)
-        drv.step(stream=sp, sync=False)
-        f.get_interior(pin_out)
-        a1.record(stream)
-        torch.cuda.synchronize()
-        e2.append(a0.elapsed_time(a1))
-    drv.check(stream=sp)
-    e2e_ms = statistics.median(e2)
+    k_e2e = max(5, min(args.steps, 20))
+    a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a0.record(pipe.h2d)
+    for _ in range(k_e2e):
+        pipe.step(pin_in, pin_out)
+    a1.record(pipe.d2h)
+    pipe.synchronize()
+    e2e_ms = a0.elapsed_time(a1) / k_e2e
     if dist:
         t = torch.tensor([e2e_ms], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -442,9 +444,11 @@ def run_ours(args, rank, world):
                 if world > 1 else "single GPU"}),
             "e2e": {"value": cells / (e2e_ms * 1e-3), "unit": UNIT,
                     "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes,
-                    "ms_per_step": e2e_ms,
-                    "path": "paper_2412_15518_b200.amr.Forest.set_interior(pinned) -> "
-                            f"{type(drv).__name__}.step -> Forest.get_interior(pinned)"},
+                    "ms_per_step": e2e_ms, "steps": k_e2e,
+                    "path": "paper_2412_15518_b200.driver.HostStepPipeline(" + type(drv).__name__ +
+                            ").step(pinned in, pinned out): H2D -> Forest.set_interior -> step -> "
+                            "Forest.get_interior -> D2H, copies overlapped with the neighbouring "
+                            "steps' compute"},
             "roofline": roofline,
             "gpu_launches": launches,
             "clocks": clk.summary()}

@@ -247,24 +247,28 @@ class Forest:
     def arena_ptr(self) -> int:
         return int(lib.tmgpu_forest_arena(self.h) or 0)
 
-    def set_interior(self, compact) -> None:
-        self._interior(compact, True)
+    def set_interior(self, compact, stream=None, sync: bool = True) -> None:
+        """Interior state [local leaves][V][E^3] into the arena (host or device
+        buffer). stream/sync=False: enqueue on that stream and return."""
+        self._interior(compact, True, stream, sync)
 
-    def get_interior(self, out=None):
+    def get_interior(self, out=None, stream=None, sync: bool = True):
         if out is None:
             out = np.zeros((self.local_count(), self.vars, self.edge ** 3))
-        self._interior(out, False)
+        self._interior(out, False, stream, sync)
         return out
 
-    def _interior(self, buf, to_device):
+    def _interior(self, buf, to_device, stream=None, sync=True):
         from .hydro import _addr
 
         ptr, host, st, n = _addr(buf)
         if n != self.local_count() * self.vars * self.edge ** 3:
             raise ValueError("compact interior has the wrong size")
+        if stream is not None:
+            st = stream
+        flags = (_lib.TMGPU_HOST_PTRS if host else 0) | (0 if sync else _lib.TMGPU_ASYNC)
         err = TmgpuError()
-        _lib.check(lib.tmgpu_forest_interior(self.h, ptr, 1 if to_device else 0,
-                                             _lib.TMGPU_HOST_PTRS if host else 0, st,
+        _lib.check(lib.tmgpu_forest_interior(self.h, ptr, 1 if to_device else 0, flags, st,
                                              C.byref(err)), err)
 
     def get_grids(self) -> np.ndarray:

@@ -95,3 +95,65 @@ class GravityHydroDriver(HydroDriver):
     def close(self) -> None:
         err = TmgpuError()
         lib.tmgpu_forest_set_gravity(self.forest.h, None, 0, C.byref(err))
+
+
+class HostStepPipeline:
+    """Stepping from and to host (pinned) buffers with the transfers off the
+    critical path: the host->device copy of step k+1's input runs on one copy
+    stream while step k computes, the device->host copy of step k's result on a
+    second copy stream while step k+1 computes (PCIe is full duplex). Device
+    staging is double-buffered; CUDA events order every buffer reuse, so each
+    step still moves its whole input in and its whole result out.
+
+        pipe = HostStepPipeline(GravityHydroDriver(forest))
+        for _ in range(n):
+            pipe.step(pin_in, pin_out)   # enqueue, returns at once
+        pipe.synchronize()
+    """
+
+    def __init__(self, driver):
+        import torch
+
+        self.driver, self.forest = driver, driver.forest
+        f = self.forest
+        n = f.local_count() * f.vars * f.edge ** 3
+        self.dev_in = [torch.empty(n, dtype=torch.float64, device="cuda") for _ in range(2)]
+        self.dev_out = [torch.empty(n, dtype=torch.float64, device="cuda") for _ in range(2)]
+        self.h2d, self.d2h = torch.cuda.Stream(), torch.cuda.Stream()
+        self.compute = torch.cuda.current_stream()
+        self.in_free, self.out_free = [None, None], [None, None]
+        self.k = 0
+
+    def step(self, pin_in, pin_out, dt: float | None = None) -> None:
+        import torch
+
+        b = self.k & 1
+        cs = self.compute
+        with torch.cuda.stream(self.h2d):
+            if self.in_free[b] is not None:
+                self.h2d.wait_event(self.in_free[b])
+            self.dev_in[b].copy_(pin_in.reshape(-1), non_blocking=True)
+            ev_in = torch.cuda.Event()
+            ev_in.record(self.h2d)
+        cs.wait_event(ev_in)
+        self.forest.set_interior(self.dev_in[b], stream=cs.cuda_stream, sync=False)
+        self.in_free[b] = torch.cuda.Event()
+        self.in_free[b].record(cs)
+        self.driver.step(dt, stream=cs.cuda_stream, sync=False)
+        if self.out_free[b] is not None:
+            cs.wait_event(self.out_free[b])
+        self.forest.get_interior(self.dev_out[b], stream=cs.cuda_stream, sync=False)
+        ev_out = torch.cuda.Event()
+        ev_out.record(cs)
+        with torch.cuda.stream(self.d2h):
+            self.d2h.wait_event(ev_out)
+            pin_out.reshape(-1).copy_(self.dev_out[b], non_blocking=True)
+            self.out_free[b] = torch.cuda.Event()
+            self.out_free[b].record(self.d2h)
+        self.k += 1
+
+    def synchronize(self) -> None:
+        import torch
+
+        torch.cuda.synchronize()
+        self.driver.check()
