@@ -54,6 +54,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-steps", type=int, default=1)
     ap.add_argument("--hydro-only", action="store_true", help="time the hydro step alone")
+    ap.add_argument("--scenario", choices=["star", "dwd"], default="star",
+                    help="star: configs[2] (default); dwd: configs[4] with --max-level 7")
     return ap.parse_args()
 
 
@@ -117,8 +119,9 @@ class ClockSampler:
 def build_workload(args):
     from paper_2412_15518_b200 import amr
 
-    f = amr.build_scenario(amr.Scenario.rotating_star, args.min_level, args.max_level, 0.1)
-    state = f.scenario_state(amr.Scenario.rotating_star)
+    kind = amr.Scenario.rotating_star if args.scenario == "star" else amr.Scenario.double_white_dwarf
+    f = amr.build_scenario(kind, args.min_level, args.max_level, 0.1)
+    state = f.scenario_state(kind)
     return f, state
 
 
@@ -129,7 +132,9 @@ def workload_config(f, args, extra=None):
             "gravity+hydro step: adaptive FMM solve (V/W/X/U lists, angular-momentum correction) "
             "+ SSP-RK3 hydro step with the gravity source in the stage epilogue: CFL dt + 3 x "
             "(ghost exchange + aggregated stage + rk3 combine)")
-    cfg = {"workload": f"configs[2]: rotating star, {args.max_level}-level AMR octree "
+    name = ("configs[2]: rotating star" if args.scenario == "star" else
+            "configs[4]: double-white-dwarf initial model (geometric refinement)")
+    cfg = {"workload": f"{name}, {args.max_level}-level AMR octree "
                        f"(leaf levels {args.min_level}-{args.max_level}), {n} leaves x 8^3 cells, {step}",
            "leaves": n, "cells": n * 512, "subgrid": "8^3 + 2 ghost layers, 5 vars (Euler)",
            "l2": "inputs larger than L2 (ghosted arena %.0f MB > 126 MB L2)" % (n * 69120 / 1e6),

@@ -150,6 +150,12 @@ int tmgpu_forest_fill_faces(tmgpu_forest* f, void* stream, tmgpu_error* err);
 int tmgpu_forest_max_wavespeed(tmgpu_forest* f, double gamma, double* per_leaf_host, tmgpu_error* err);
 /* SSP-RK3 step (rk3.hpp): 3 x (fill_ghosts_sync -> aggregated
  * stage over all leaves -> rk3_combine); cfl > 0 computes dt on the device */
+/* reflux at refinement jumps in every subsequent step (flux_register.hpp:21-63 declared,
+ * SPEC.md:383-391 formula; our restatement, oracle tmo_reflux_apply): the coarse cell
+ * next to a finer face += -dir * (stage weight * dt / dx) * (mean of the 2x2 fine face
+ * fluxes - coarse face flux), after each stage's RK combine; single GPU; re-call after a
+ * topology change. on = 0 turns it off. */
+int tmgpu_forest_set_reflux(tmgpu_forest* f, int on, tmgpu_error* err);
 /* gravity source in the stage (our spec): g device [3][comp_stride] by
  * local slot; NULL = pure hydro (the reference's stage) */
 int tmgpu_forest_set_gravity(tmgpu_forest* f, const double* g, long long comp_stride,

@@ -245,6 +245,7 @@ class Oracle(_Lib):
         L.tmo_tree_plan.argtypes = [C.c_void_p, C.c_int, _i64p, C.c_size_t]
         L.tmo_fill_ghosts_sync.argtypes = [C.c_void_p, C.POINTER(_dp)]
         L.tmo_flag_refinement.argtypes = [C.c_void_p, _dp, C.c_double, C.c_double]
+        L.tmo_reflux_apply.argtypes = [C.c_void_p, C.POINTER(_dp), C.POINTER(_dp), C.c_int, C.c_int, C.c_int, _dp, C.c_double, C.c_double]
         L.tmo_stage_subgrid_grav.argtypes = [_dp, C.c_int, C.c_int, C.c_int, _dp, _dp, _dp, _ip]
         _lp = C.POINTER(C.c_long)
         L.tmo_grav_amr_solve_ex.argtypes = [C.c_long, _ip, _dp, C.c_int, _dp, _dp, _lp]
@@ -325,6 +326,16 @@ class OracleTree:
         arr = (_dp * len(grids))(*[dptr(g) for g in grids])
         if self.L.tmo_fill_ghosts_sync(self.h, arr) != 0:
             raise RuntimeError("oracle ghost fill failed")
+
+    def reflux(self, grids, faces, dx, dt, coef):
+        """tmo_reflux_apply: grids (ghosted, canonical order, modified in place),
+        faces: per leaf [6][V][E^2] stage face fluxes, dx: per-leaf cell size."""
+        ga = (_dp * len(grids))(*[dptr(g) for g in grids])
+        fa = (_dp * len(faces))(*[dptr(f) for f in faces])
+        d = np.ascontiguousarray(dx, dtype=np.float64)
+        if self.L.tmo_reflux_apply(self.h, ga, fa, self.edge, self.ghost, self.vars, dptr(d),
+                                   float(dt), float(coef)) != 0:
+            raise RuntimeError("oracle reflux failed")
 
     def flag(self, grid, theta, rho_floor=1e-10):
         return bool(self.L.tmo_flag_refinement(self.h, dptr(grid), theta, rho_floor))

@@ -726,3 +726,51 @@ int tmo_flag_refinement(const tmo_tree* t, const double* grid, double theta, dou
       }
   return 0;
 }
+
+/* Reflux at refinement jumps — our restatement (parity unpinned): the
+ * reference declares FluxRegister (proj/include/taskmesh/amr/flux_register.hpp:
+ * 21-63) without a definition; SPEC.md:383-391 gives the correction
+ * (sum fine_flux*fine_area - coarse_flux*coarse_area)*dt/volume, the header
+ * the sign -dir, the weight w = stage coefficient * dt, the 2x2 arithmetic
+ * mean (restrict_face) and the sorted (leaf, axis, dir) application order.
+ * faces[l]: leaf l's stage face-flux blocks [6][V][E^2] (stage.hpp:8-12,
+ * block 2*axis+side, entry var*E^2 + c2*E + c1); dx[l] its cell size.
+ * grids: ghosted leaf states after the stage (and its RK combine). */
+int tmo_reflux_apply(const tmo_tree* t, double** grids, double* const* faces, int E, int G, int V,
+                     const double* dx, double dt, double coef) {
+  const int S = E + 2 * G, E2 = E * E, H = E / 2;
+  const double w = coef * dt;
+  for (size_t li = 0; li < t->nleaves; ++li) {
+    const double cw = w / dx[li];
+    for (int axis = 0; axis < 3; ++axis)
+      for (int d = 0; d < 2; ++d) {
+        const int dir = d == 0 ? -1 : 1;
+        uint64_t ids[4];
+        int cnt;
+        if (tmo_tree_face_neighbor(t, t->leaves[li], axis, dir, ids, &cnt) != 2) continue;
+        long fl[4];
+        for (int q = 0; q < 4; ++q) {
+          fl[q] = leaf_index(t, ids[q]);
+          if (fl[q] < 0) return -1;
+        }
+        const int side_c = dir > 0 ? 1 : 0, side_f = 1 - side_c;
+        for (int v = 0; v < V; ++v)
+          for (int c2 = 0; c2 < E; ++c2)
+            for (int c1 = 0; c1 < E; ++c1) {
+              const double* Ff = faces[fl[(c2 / H) * 2 + c1 / H]] + (size_t)((2 * axis + side_f) * V + v) * E2;
+              const int f1 = 2 * (c1 % H), f2 = 2 * (c2 % H);
+              const double mean = (((Ff[f2 * E + f1] + Ff[f2 * E + f1 + 1]) + Ff[(f2 + 1) * E + f1]) +
+                                   Ff[(f2 + 1) * E + f1 + 1]) * 0.25;
+              const double coarse = faces[li][(size_t)((2 * axis + side_c) * V + v) * E2 + c2 * E + c1];
+              const double delta = mean - coarse;
+              int x[3];
+              x[axis] = side_c ? E - 1 : 0;
+              x[(axis + 1) % 3] = c1;
+              x[(axis + 2) % 3] = c2;
+              double* u = grids[li] + (((size_t)v * S + x[2] + G) * S + x[1] + G) * S + x[0] + G;
+              *u = dir > 0 ? *u - cw * delta : *u + cw * delta;
+            }
+      }
+  }
+  return 0;
+}

@@ -57,6 +57,8 @@ int tmo_tree_face_neighbor(const tmo_tree* t, uint64_t leaf, int axis, int dir,
 size_t tmo_tree_plan(const tmo_tree* t, int axis, int64_t* rows, size_t cap);
 /* grids[l] = ghosted grid of canonical leaf l (vars*S^3 doubles) */
 int tmo_fill_ghosts_sync(const tmo_tree* t, double** grids);
+int tmo_reflux_apply(const tmo_tree* t, double** grids, double* const* faces, int E, int G, int V,
+                     const double* dx, double dt, double coef);
 int tmo_flag_refinement(const tmo_tree* t, const double* grid, double theta, double rho_floor);
 
 /* gravity (our FMM specification, parity unpinned: no reference code) — gravity_oracle.c */

@@ -38,6 +38,13 @@ struct tmgpu_forest {
   double* speeds = nullptr;   // [slot]
   double* diag = nullptr;     // [slot] floor hits of the last stage
   double* dt_dev = nullptr;   // [1]
+  // optional reflux (tmgpu_forest_set_reflux): the stage's face fluxes and the
+  // coarse leaves with finer faces (CSR over faces in (axis, dir) order)
+  bool reflux = false;
+  uint64_t reflux_version = ~0ull;
+  double* flux = nullptr;  // [slot][6][V][E^2]
+  int *rf_leaf = nullptr, *rf_off = nullptr, *rf_ad = nullptr, *rf_fine = nullptr;
+  long long rf_n = 0;
   const double* grav = nullptr;  // optional gravity g[3][stride] by local slot (device)
   long long grav_stride = 0;
   unsigned long long* err_dev = nullptr;
@@ -332,6 +339,7 @@ tmgpu_forest* tmgpu_forest_create(int edge, int ghost, int vars, int max_level,
 void tmgpu_forest_destroy(tmgpu_forest* f) {
   if (!f) return;
   free_dev(f);
+  tmgpu_forest_set_reflux(f, 0, nullptr);
   if (f->side) cudaStreamDestroy(f->side);
   if (f->ev_packed) cudaEventDestroy(f->ev_packed);
   if (f->ev_remote) cudaEventDestroy(f->ev_remote);
@@ -580,7 +588,10 @@ int tmgpu_forest_step(tmgpu_forest* f, double dt, double cfl, double gamma, int 
   p.dt_ptr = cfl > 0.0 ? f->dt_dev : nullptr;
   p.out_stride = (long long)V * 1728;
   p.out_ghosted = 1;
-  p.faces = nullptr;
+  if (f->reflux && f->reflux_version != f->forest.topology_version())
+    return fail(err, TMGPU_ERR_INVALID, "reflux: topology changed; call tmgpu_forest_set_reflux again");
+  p.faces = f->reflux ? f->flux : nullptr;
+  p.faces_stride = (long long)6 * V * 64;
   p.diag = f->diag;
   p.diag_stride = 1;
   p.u0 = f->u0;
@@ -635,6 +646,11 @@ int tmgpu_forest_step(tmgpu_forest* f, double dt, double cfl, double gamma, int 
     } else {
       e = launch_stage(V, (flags & TMGPU_FAST) != 0, f->maps[f->cur], p, st);
     }
+    if (e == cudaSuccess && f->reflux) {  // SSP-RK3 stage weights 1, 1/4, 2/3
+      const double coef = stage == 1 ? 1.0 : (stage == 2 ? 0.25 : 2.0 / 3.0);
+      e = launch_reflux(f->arenas[dst], V, f->flux, f->rf_leaf, f->rf_off, f->rf_ad, f->rf_fine, f->rf_n,
+                        f->leaf_dx, p.dt_ptr, dt, coef, st);
+    }
     f->cur = dst;
     if (timed) cudaEventRecord(f->ev[2 * stage + 1], st);
   }
@@ -652,6 +668,64 @@ int tmgpu_forest_step(tmgpu_forest* f, double dt, double cfl, double gamma, int 
   if (cfl > 0.0 && !std::isfinite(dtv))
     return fail(err, TMGPU_ERR_SOLVER, "cfl_dt: no wave speed (s = 0 everywhere)");
   if (w != ~0ull) return solver_err_from_word(err, w, f->plan.loc2gl);
+  return TMGPU_OK;
+}
+
+// Reflux at refinement jumps in every subsequent step (our restatement of
+// SPEC.md:383-391 / flux_register.hpp; single GPU). on = 0 turns it off.
+int tmgpu_forest_set_reflux(tmgpu_forest* f, int on, tmgpu_error* err) {
+  if (err) std::memset(err, 0, sizeof(*err));
+  if (int rc = ready(f, err)) return rc;
+  auto drop = [](int*& p) {
+    if (p) cudaFree(p);
+    p = nullptr;
+  };
+  drop(f->rf_leaf), drop(f->rf_off), drop(f->rf_ad), drop(f->rf_fine);
+  if (f->flux) cudaFree(f->flux);
+  f->flux = nullptr;
+  f->reflux = false;
+  f->rf_n = 0;
+  if (!on) return TMGPU_OK;
+  if (f->world() > 1) return fail(err, TMGPU_ERR_INVALID, "reflux: single GPU only");
+  const int V = f->forest.config().vars;
+  std::vector<int> leaf, off{0}, ad, fine;
+  const auto& leaves = f->forest.leaves();
+  try {
+    for (size_t s = 0; s < leaves.size(); ++s) {
+      bool any = false;
+      for (int axis = 0; axis < 3; ++axis)
+        for (int dir : {-1, +1}) {
+          const FaceNeighbors fn = f->forest.face_neighbor(leaves[s], axis, dir);
+          if (fn.kind != NeighborKind::finer) continue;
+          any = true;
+          ad.push_back(axis);
+          ad.push_back(dir);
+          for (int q = 0; q < 4; ++q) fine.push_back(f->forest.slot_of(fn.ids[q]));
+        }
+      if (any) {
+        leaf.push_back((int)s);
+        off.push_back((int)(ad.size() / 2));
+      }
+    }
+  } catch (const std::exception& ex) {
+    return fail(err, TMGPU_ERR_INVALID, ex.what());
+  }
+  auto up = [](const std::vector<int>& v, int** out) {
+    cudaError_t e = cudaMalloc(out, (v.empty() ? 1 : v.size()) * sizeof(int));
+    if (e == cudaSuccess && !v.empty())
+      e = cudaMemcpy(*out, v.data(), v.size() * sizeof(int), cudaMemcpyHostToDevice);
+    return e;
+  };
+  cudaError_t e = up(leaf, &f->rf_leaf);
+  if (e == cudaSuccess) e = up(off, &f->rf_off);
+  if (e == cudaSuccess) e = up(ad, &f->rf_ad);
+  if (e == cudaSuccess) e = up(fine, &f->rf_fine);
+  if (e == cudaSuccess) e = cudaMalloc(&f->flux, (size_t)f->nslots * 6 * V * 64 * sizeof(double));
+  if (e == cudaSuccess) e = cudaMemset(f->flux, 0, (size_t)f->nslots * 6 * V * 64 * sizeof(double));
+  if (e != cudaSuccess) return cuda_err(err, e, "tmgpu_forest_set_reflux");
+  f->rf_n = (long long)leaf.size();
+  f->reflux = true;
+  f->reflux_version = f->forest.topology_version();
   return TMGPU_OK;
 }
 

@@ -75,6 +75,12 @@ cudaError_t launch_max_wavespeed(const double* in, long long slot_stride, const 
 cudaError_t launch_cfl_reduce(const double* speeds, const double* leaf_dx, long long n, double cfl,
                               double* dt, cudaStream_t stream);
 
+// Reflux of the stage output at the coarse side of refinement jumps (reflux.cu).
+cudaError_t launch_reflux(double* arena, int V, const double* flux, const int* leaf_slot,
+                          const int* face_off, const int* face_ad, const int* fine, long long nleaves,
+                          const double* leaf_dx, const double* dt_ptr, double g_dt, double coef,
+                          cudaStream_t st);
+
 cudaError_t launch_rk3_combine(int stage, const double* u0, const double* v, double* out,
                                long long n, cudaStream_t stream);
 

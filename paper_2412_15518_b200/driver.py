@@ -17,15 +17,26 @@ from .amr import Forest, unpack
 from .hydro import SolverError
 
 
+lib.tmgpu_forest_set_reflux.restype = C.c_int
+lib.tmgpu_forest_set_reflux.argtypes = [C.c_void_p, C.c_int, C.POINTER(TmgpuError)]
+
+
 class HydroDriver:
     def __init__(self, forest: Forest, gamma: float = 1.4, cfl: float = 0.4, fast: bool = False,
-                 exact_ghosts: bool = False):
+                 exact_ghosts: bool = False, reflux: bool = False):
         """exact_ghosts: reference 3-pass full-shell exchange (full ghosted arrays
         bitwise equal to the reference); default one-round face-only exchange
-        (bitwise on every ghost the stage reads, hence on the state)."""
+        (bitwise on every ghost the stage reads, hence on the state).
+        reflux: flux-register correction at refinement jumps after every stage
+        (flux_register.hpp:21-63 declared only; our restatement,
+        oracle tmo_reflux_apply) — conserves mass across level jumps; single GPU."""
         self.forest, self.gamma, self.cfl, self.fast = forest, gamma, cfl, fast
         self.exact_ghosts = exact_ghosts
         self.steps = 0
+        self.reflux = reflux
+        if reflux:
+            err = TmgpuError()
+            _lib.check(lib.tmgpu_forest_set_reflux(forest.h, 1, C.byref(err)), err)
 
     def step(self, dt: float | None = None, stream=None, sync: bool = True) -> float | None:
         """Advance one SSP-RK3 step. dt None: CFL dt on the device. Returns
@@ -64,8 +75,8 @@ class GravityHydroDriver(HydroDriver):
     of the owned leaves (GravityAMR.distribute); bitwise equal to one GPU."""
 
     def __init__(self, forest: Forest, gamma: float = 1.4, cfl: float = 0.4, fast: bool = False,
-                 exact_ghosts: bool = False, am: bool = True):
-        super().__init__(forest, gamma, cfl, fast, exact_ghosts)
+                 exact_ghosts: bool = False, am: bool = True, reflux: bool = False):
+        super().__init__(forest, gamma, cfl, fast, exact_ghosts, reflux)
         import torch
 
         from .gravity import GravityAMR
