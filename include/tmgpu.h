@@ -105,6 +105,7 @@ tmgpu_forest* tmgpu_forest_create(int edge, int ghost, int vars, int max_level,
                                   const int* root_dims, const int* bc, tmgpu_error* err);
 void tmgpu_forest_destroy(tmgpu_forest* f);
 int tmgpu_forest_refine(tmgpu_forest* f, uint64_t packed, tmgpu_error* err);  /* Tree::refine octree.cpp:200-234 */
+int tmgpu_forest_coarsen(tmgpu_forest* f, uint64_t packed, tmgpu_error* err); /* Tree::coarsen octree.cpp:236-293 */
 size_t tmgpu_forest_leaves(tmgpu_forest* f, uint64_t* out, size_t cap);     /* Tree::leaves octree.cpp:52-77 */
 /* Tree::face_neighbor (octree.cpp:92-132): returns kind 0 same, 1 coarser, 2 finer, 3 boundary */
 int tmgpu_forest_face_neighbor(tmgpu_forest* f, uint64_t leaf, int axis, int dir, uint64_t* ids4,
@@ -142,6 +143,13 @@ int tmgpu_forest_interior(tmgpu_forest* f, double* compact, int to_device, int f
 /* whole ghosted arena <-> host [slot][vars][S^3] (SubGrid::raw, subgrid.hpp:59-60) */
 int tmgpu_forest_grids(tmgpu_forest* f, double* ghosted_host, int to_device, tmgpu_error* err);
 /* ghost::fill_ghosts_sync (ghost.cpp:282-296), bitwise on the full ghosted arrays */
+/* AMR regrid with the device data (octree.cpp:149-293 prolong_cell / restrict_cells, same
+ * order incl. cascaded 2:1 refines): refine then coarsen the listed nodes; single GPU */
+int tmgpu_forest_regrid(tmgpu_forest* f, const uint64_t* refine, size_t nr, const uint64_t* coarsen,
+                        size_t nc, tmgpu_error* err);
+/* Tree::flag_refinement (octree.cpp:295-323) per local leaf on the device state: flags[slot] */
+int tmgpu_forest_flag(tmgpu_forest* f, double theta, double rho_floor, int* flags_host,
+                      tmgpu_error* err);
 int tmgpu_forest_fill_ghosts(tmgpu_forest* f, void* stream, tmgpu_error* err);
 /* one-round face-only exchange: every ghost the stage reads, bitwise equal to
  * fill_ghosts_sync; edge/corner ghosts are left untouched */

@@ -163,6 +163,10 @@ class RefTree:
         if self.L.tmref_tree_refine(self.h, packed) != 0:
             raise RuntimeError("reference refine failed")
 
+    def coarsen(self, packed: int) -> None:
+        if self.L.tmref_tree_coarsen(self.h, packed) != 0:
+            raise RuntimeError("reference coarsen failed")
+
     def leaves(self) -> np.ndarray:
         n = self.L.tmref_tree_leaves(self.h, None, 0)
         out = np.zeros(n, dtype=np.uint64)

@@ -39,6 +39,9 @@ _sig("tmgpu_partition_leaves", C.c_int, [_u64p, C.c_size_t, C.c_int, _ip, _ep])
 _sig("tmgpu_forest_create", _vp, [C.c_int, C.c_int, C.c_int, C.c_int, _ip, _ip, _ep])
 _sig("tmgpu_forest_destroy", None, [_vp])
 _sig("tmgpu_forest_refine", C.c_int, [_vp, C.c_uint64, _ep])
+_sig("tmgpu_forest_coarsen", C.c_int, [_vp, C.c_uint64, _ep])
+_sig("tmgpu_forest_regrid", C.c_int, [_vp, _u64p, C.c_size_t, _u64p, C.c_size_t, _ep])
+_sig("tmgpu_forest_flag", C.c_int, [_vp, C.c_double, C.c_double, _ip, _ep])
 _sig("tmgpu_forest_leaves", C.c_size_t, [_vp, _u64p, C.c_size_t])
 _sig("tmgpu_forest_face_neighbor", C.c_int, [_vp, C.c_uint64, C.c_int, C.c_int, _u64p, _ip])
 _sig("tmgpu_forest_plan", C.c_size_t, [_vp, C.c_int, _i64p, C.c_size_t])
@@ -157,6 +160,30 @@ class Forest:
     def refine(self, node) -> None:
         err = TmgpuError()
         _amr_check(lib.tmgpu_forest_refine(self.h, int(node), C.byref(err)), err)
+
+    def coarsen(self, node) -> None:
+        """Tree::coarsen (octree.cpp:236-293), topology only."""
+        err = TmgpuError()
+        _amr_check(lib.tmgpu_forest_coarsen(self.h, int(node), C.byref(err)), err)
+
+    def regrid(self, refine=(), coarsen=()) -> None:
+        """Refine then coarsen with the device data carried along exactly as the
+        reference's Tree::refine / coarsen carry their grids (prolong_cell /
+        restrict_cells, octree.cpp:149-293); the arena is rebuilt. Single GPU."""
+        r = np.ascontiguousarray(np.asarray(refine, dtype=np.uint64))
+        c = np.ascontiguousarray(np.asarray(coarsen, dtype=np.uint64))
+        err = TmgpuError()
+        _amr_check(lib.tmgpu_forest_regrid(self.h, r.ctypes.data_as(_u64p), len(r),
+                                           c.ctypes.data_as(_u64p), len(c), C.byref(err)), err)
+
+    def flag_refinement(self, theta: float, rho_floor: float = 1e-10) -> np.ndarray:
+        """Tree::flag_refinement (octree.cpp:295-323) of every local leaf on the
+        device state (ghosts as they are): bool per slot."""
+        out = np.zeros(self.local_count(), dtype=np.int32)
+        err = TmgpuError()
+        _lib.check(lib.tmgpu_forest_flag(self.h, theta, rho_floor, out.ctypes.data_as(_ip),
+                                         C.byref(err)), err)
+        return out.astype(bool)
 
     def leaves(self) -> np.ndarray:
         n = lib.tmgpu_forest_leaves(self.h, None, 0)

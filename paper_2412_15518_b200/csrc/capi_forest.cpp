@@ -5,6 +5,7 @@
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <unordered_map>
 #include <vector>
 
 #include "comm.h"
@@ -356,6 +357,118 @@ int tmgpu_forest_refine(tmgpu_forest* f, uint64_t packed, tmgpu_error* err) {
   } catch (const std::exception& ex) {
     return fail(err, TMGPU_ERR_AMR, ex.what());
   }
+}
+
+int tmgpu_forest_coarsen(tmgpu_forest* f, uint64_t packed, tmgpu_error* err) {
+  if (err) std::memset(err, 0, sizeof(*err));
+  try {
+    f->forest.coarsen(NodeId::unpack(packed));
+    return TMGPU_OK;
+  } catch (const std::exception& ex) {
+    return fail(err, TMGPU_ERR_AMR, ex.what());
+  }
+}
+
+// Refine then coarsen the given nodes with the device data carried along, as
+// the reference's Tree::refine / coarsen do with their grids (prolong_cell /
+// restrict_cells, octree.cpp:149-293), in the same order (cascaded 2:1
+// refinements included): children get the prolonged interior and zero ghosts,
+// a coarsened parent the restricted interior and zero ghosts, untouched leaves
+// keep their whole block. Then the arena is rebuilt for the new topology.
+// Single GPU. On a topology error the tree keeps the operations done so far
+// (as the reference's) and the device arena is stale (tmgpu_forest_alloc).
+int tmgpu_forest_regrid(tmgpu_forest* f, const uint64_t* refine, size_t nr, const uint64_t* coarsen,
+                        size_t nc, tmgpu_error* err) {
+  if (err) std::memset(err, 0, sizeof(*err));
+  if (int rc = ready(f, err)) return rc;
+  if (f->world() > 1) return fail(err, TMGPU_ERR_INVALID, "regrid: single GPU only");
+  const int V = f->forest.config().vars;
+  const long long stride = (long long)V * 1728;
+  const std::vector<NodeId> old_leaves = f->forest.leaves();
+  double* old = f->arenas[f->cur];
+  std::unordered_map<uint64_t, const double*> pool;
+  for (size_t s = 0; s < old_leaves.size(); ++s) pool[old_leaves[s].packed()] = old + (long long)s * stride;
+  f->forest.clear_oplog();
+  try {
+    for (size_t q = 0; q < nr; ++q) f->forest.refine(NodeId::unpack(refine[q]));
+    for (size_t q = 0; q < nc; ++q) f->forest.coarsen(NodeId::unpack(coarsen[q]));
+  } catch (const std::exception& ex) {
+    return fail(err, TMGPU_ERR_AMR, ex.what());
+  }
+  cudaStream_t st = 0;
+  std::vector<double*> temps;
+  cudaError_t e = cudaSuccess;
+  try {
+  for (const Forest::Op& op : f->forest.oplog()) {
+    if (e != cudaSuccess) break;
+    const NodeId& id = op.node;
+    if (op.refine) {
+      double* ch = nullptr;
+      e = cudaMalloc(&ch, (size_t)8 * stride * sizeof(double));
+      if (e != cudaSuccess) break;
+      temps.push_back(ch);
+      e = cudaMemsetAsync(ch, 0, (size_t)8 * stride * sizeof(double), st);
+      if (e == cudaSuccess) e = launch_prolong(pool.at(id.packed()), ch, V, st);
+      pool.erase(id.packed());
+      for (int b = 0; b < 8; ++b)
+        pool[id.child(b & 1, (b >> 1) & 1, (b >> 2) & 1).packed()] = ch + (long long)b * stride;
+    } else {
+      double* pg = nullptr;
+      e = cudaMalloc(&pg, (size_t)stride * sizeof(double));
+      if (e != cudaSuccess) break;
+      temps.push_back(pg);
+      const double* chp[8];
+      for (int b = 0; b < 8; ++b) {
+        const uint64_t c = id.child(b & 1, (b >> 1) & 1, (b >> 2) & 1).packed();
+        chp[b] = pool.at(c);
+        pool.erase(c);
+      }
+      e = cudaMemsetAsync(pg, 0, (size_t)stride * sizeof(double), st);
+      if (e == cudaSuccess) e = launch_restrict(chp, pg, V, st);
+      pool[id.packed()] = pg;
+    }
+  }
+  f->forest.clear_oplog();
+  // rebuild the device state for the new topology, keeping the old arena alive
+  f->arenas[f->cur] = nullptr;
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  int rc = e == cudaSuccess ? alloc_device(f, err) : TMGPU_ERR_CUDA;
+  if (rc == TMGPU_OK) {
+    const auto& nl = f->forest.leaves();
+    std::vector<const double*> src(nl.size());
+    for (size_t s = 0; s < nl.size(); ++s) src[s] = pool.at(nl[s].packed());
+    const double** dsrc = nullptr;
+    e = cudaMalloc(&dsrc, (src.empty() ? 1 : src.size()) * sizeof(double*));
+    if (e == cudaSuccess && !src.empty())
+      e = cudaMemcpy(dsrc, src.data(), src.size() * sizeof(double*), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = launch_gather_blocks(dsrc, (long long)src.size(), f->arenas[f->cur], stride, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (dsrc) cudaFree(dsrc);
+  }
+  for (double* p : temps) cudaFree(p);
+  cudaFree(old);
+  if (rc != TMGPU_OK) return rc;
+  return cuda_err(err, e, "tmgpu_forest_regrid");
+  } catch (const std::exception& ex) {  // a bookkeeping bug, never expected
+    for (double* p : temps) cudaFree(p);
+    return fail(err, TMGPU_ERR_AMR, std::string("regrid: ") + ex.what());
+  }
+}
+
+// Tree::flag_refinement (octree.cpp:295-323) for every local leaf, on the
+// current device state (ghosts as they are): flags[slot] = 0/1.
+int tmgpu_forest_flag(tmgpu_forest* f, double theta, double rho_floor, int* flags_host,
+                      tmgpu_error* err) {
+  if (err) std::memset(err, 0, sizeof(*err));
+  if (int rc = ready(f, err)) return rc;
+  const int V = f->forest.config().vars;
+  int* d = nullptr;
+  cudaError_t e = cudaMalloc(&d, (f->nslots ? f->nslots : 1) * sizeof(int));
+  if (e == cudaSuccess) e = launch_flag(f->arena(), (long long)V * 1728, f->nslots, theta, rho_floor, d, 0);
+  if (e == cudaSuccess)
+    e = cudaMemcpy(flags_host, d, f->nslots * sizeof(int), cudaMemcpyDeviceToHost);
+  if (d) cudaFree(d);
+  return cuda_err(err, e, "tmgpu_forest_flag");
 }
 
 size_t tmgpu_forest_leaves(tmgpu_forest* f, uint64_t* out, size_t cap) {

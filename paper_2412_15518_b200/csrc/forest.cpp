@@ -175,6 +175,36 @@ void Forest::refine(const NodeId& id) {
   for (int bk = 0; bk < 2; ++bk)
     for (int bj = 0; bj < 2; ++bj)
       for (int bi = 0; bi < 2; ++bi) nodes_[id.child(bi, bj, bk).packed()] = Node{};
+  oplog_.push_back(Op{true, id});
+  cache_valid_ = false;
+  version_ += 1;
+}
+
+void Forest::coarsen(const NodeId& parent) {
+  auto it = nodes_.find(parent.packed());
+  if (it == nodes_.end()) throw AmrError("node not in tree");
+  if (it->second.children_mask != 0xFF) throw AmrError("coarsen of a leaf");
+  for (int b = 0; b < 8; ++b) {
+    auto c = nodes_.find(parent.child(b & 1, (b >> 1) & 1, (b >> 2) & 1).packed());
+    if (c == nodes_.end() || c->second.children_mask)
+      throw AmrError("coarsen requires all 8 children to be leaves");
+  }
+  // balance: a subdivided face neighbour's face children must all be leaves
+  for (int axis = 0; axis < 3; ++axis)
+    for (int dir : {-1, +1}) {
+      NodeId cell;
+      if (!step_cell(*this, parent, axis, dir, cell)) continue;
+      auto nb = nodes_.find(cell.packed());
+      if (nb == nodes_.end() || !nb->second.children_mask) continue;
+      for (const NodeId& fc : face_children(cell, axis, dir)) {
+        auto f = nodes_.find(fc.packed());
+        if (f != nodes_.end() && f->second.children_mask)
+          throw AmrError("coarsen would violate 2:1 balance");
+      }
+    }
+  for (int b = 0; b < 8; ++b) nodes_.erase(parent.child(b & 1, (b >> 1) & 1, (b >> 2) & 1).packed());
+  nodes_[parent.packed()].children_mask = 0;
+  oplog_.push_back(Op{false, parent});
   cache_valid_ = false;
   version_ += 1;
 }

@@ -89,6 +89,15 @@ class Forest {
   uint64_t topology_version() const { return version_; }
 
   void refine(const NodeId& id);  // octree.cpp:200-234 (eager 2:1 cascade)
+  void coarsen(const NodeId& parent);  // octree.cpp:236-293 (2:1 check, all children leaves)
+  // every split / merge in execution order (cascaded refines included): the
+  // sequence the reference's data prolongation/restriction follows (regrid)
+  struct Op {
+    bool refine;
+    NodeId node;
+  };
+  const std::vector<Op>& oplog() const { return oplog_; }
+  void clear_oplog() { oplog_.clear(); }
   std::optional<NodeId> covering_leaf(const NodeId& cell) const;          // octree.cpp:79-90
   FaceNeighbors face_neighbor(const NodeId& leaf, int axis, int dir) const;  // :92-132
   bool is_balanced() const;                                               // :325-361
@@ -107,6 +116,7 @@ class Forest {
   mutable std::unordered_map<uint64_t, int> slot_cache_;
   mutable bool cache_valid_ = false;
   uint64_t version_ = 0;
+  std::vector<Op> oplog_;
 };
 
 // scenario.cpp: analytic refinement + initial data (kinds: 0 rotating star,

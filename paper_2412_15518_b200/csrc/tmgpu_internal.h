@@ -81,6 +81,14 @@ cudaError_t launch_reflux(double* arena, int V, const double* flux, const int* l
                           const double* leaf_dx, const double* dt_ptr, double g_dt, double coef,
                           cudaStream_t st);
 
+// regrid.cu: octree.cpp:149-323 data operations
+cudaError_t launch_prolong(const double* parent, double* children8, int V, cudaStream_t st);
+cudaError_t launch_restrict(const double* const* children, double* parent, int V, cudaStream_t st);
+cudaError_t launch_gather_blocks(const double* const* src_dev, long long n, double* dst, long long stride,
+                                 cudaStream_t st);
+cudaError_t launch_flag(const double* arena, long long stride, long long n, double theta, double rho_floor,
+                        int* flag, cudaStream_t st);
+
 cudaError_t launch_rk3_combine(int stage, const double* u0, const double* v, double* out,
                                long long n, cudaStream_t stream);
 
