@@ -832,6 +832,25 @@ struct GravAmrWork {
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
 };
 
+// Distributed: base[slot * per_slot ..] of every rank's slot range to every
+// rank — one ncclAllGather of the padded per-rank segments through the
+// staging buffer, then each remote segment into place.
+static int allgather_slots(GravAmrWork& w, double* base, int per_slot, cudaStream_t st, cudaError_t* e,
+                           std::string* why) {
+  const int R = (int)w.seg_lo.size(), me = comm_rank(w.comm);
+  const size_t per = (size_t)w.seg_max * per_slot;
+  double* mine = w.gather + (size_t)me * per;
+  *e = cudaMemcpyAsync(mine, base + w.lo * per_slot, (size_t)(w.hi - w.lo) * per_slot * sizeof(double),
+                       cudaMemcpyDeviceToDevice, st);
+  if (*e != cudaSuccess) return TMGPU_OK;
+  int rc = comm_allgather(w.comm, mine, w.gather, per, st, why);
+  for (int r = 0; r < R && *e == cudaSuccess && rc == TMGPU_OK; ++r)
+    if (r != me && w.seg_cnt[r])
+      *e = cudaMemcpyAsync(base + w.seg_lo[r] * per_slot, w.gather + (size_t)r * per,
+                           (size_t)w.seg_cnt[r] * per_slot * sizeof(double), cudaMemcpyDeviceToDevice, st);
+  return rc;
+}
+
 // internal patches that need the L2L pass, per level (leaf patches: in L2P)
 static cudaError_t build_l2l_lists(GravAmrWork& w, const std::vector<std::vector<int>>* need) {
   const GravPlan& P = w.plan;
@@ -1108,19 +1127,8 @@ int tmgpu_gravity_amr_solve(tmgpu_gravity_amr* G, const double* mass, double* ph
     cudaEventRecord(rec.ev[0], st);
   }
   int rc = TMGPU_OK;
-  if (e == cudaSuccess && w.comm) {
-    // every rank needs every leaf mass for the upward pass: one ncclAllGather
-    // of the padded per-rank segments, then each segment into place
-    const int R = (int)w.seg_lo.size();
-    const size_t per = (size_t)w.seg_max * 512;
-    double* mine = w.gather + (size_t)comm_rank(w.comm) * per;
-    e = cudaMemcpyAsync(mine, w.mass + w.lo * 512, nout * sizeof(double), cudaMemcpyDeviceToDevice, st);
-    if (e == cudaSuccess) rc = comm_allgather(w.comm, mine, w.gather, per, st, &why);
-    for (int r = 0; r < R && e == cudaSuccess && rc == TMGPU_OK; ++r)
-      if (r != comm_rank(w.comm) && w.seg_cnt[r])
-        e = cudaMemcpyAsync(w.mass + w.seg_lo[r] * 512, w.gather + (size_t)r * per,
-                            (size_t)w.seg_cnt[r] * 512 * sizeof(double), cudaMemcpyDeviceToDevice, st);
-  }
+  if (e == cudaSuccess && w.comm)  // every rank needs every leaf mass for the upward pass
+    rc = allgather_slots(w, w.mass, 512, st, &e, &why);
   if (timed) cudaEventRecord(rec.ev[1], st);
   if (e == cudaSuccess && rc == TMGPU_OK) {
     long long launches = 0;
@@ -1173,11 +1181,8 @@ int tmgpu_gravity_amr_solve(tmgpu_gravity_amr* G, const double* mass, double* ph
     ++launches;
     if (timed) cudaEventRecord(rec.ev[5], st);
     if (am) {  // the per-slot sums came with L2P
-      if (w.comm && e == cudaSuccess) {  // identical global pair tree on every rank
-        std::vector<long long> off(w.seg_lo.size()), cnt(w.seg_cnt.size());
-        for (size_t r = 0; r < off.size(); ++r) off[r] = w.seg_lo[r] * 16, cnt[r] = w.seg_cnt[r] * 16;
-        rc = comm_allgatherv(w.comm, w.part, off, cnt, st, &why);
-      }
+      if (w.comm && e == cudaSuccess)  // identical global pair tree on every rank
+        rc = allgather_slots(w, w.part, 16, st, &e, &why);
       double* bufs[2] = {w.part, w.part2};
       int cur = 0;
       for (long long n = w.P; n > 1;) {
