@@ -248,6 +248,12 @@ int tmgpu_gravity_amr_distribute(tmgpu_gravity_amr* G, tmgpu_comm* comm, const l
  * M2L/L2L for; returns the level count (negative error code on failure) */
 int tmgpu_gravity_amr_plan_need(const int* leaves, long long nleaves, long long lo, long long hi,
                                 long long* counts, int max_levels, tmgpu_error* err);
+/* host-only: the multipole-moment exchange (LET) plan of rank `me`: out[4] = owned internal
+ * patches, shared top patches, own subtree roots, halo leaf patches; per peer q the send /
+ * receive patch counts and list hashes (rank r's send list to q == q's receive list from r) */
+int tmgpu_gravity_amr_let_plan(const int* leaves, long long nleaves, const long long* bounds, int world,
+                               int me, long long* out, long long* send, long long* recv,
+                               long long* send_hash, long long* recv_hash, tmgpu_error* err);
 /* per-phase device timing: totals in ms of [comm, up, m2l, l2l, l2p, am] */
 int tmgpu_gravity_amr_set_timing(tmgpu_gravity_amr* G, int on);
 int tmgpu_gravity_amr_timing(tmgpu_gravity_amr* G, double* ms, long long* solves);

@@ -74,19 +74,50 @@ __global__ void amr_mass_kernel(const double* __restrict__ arena, int V, long lo
 }
 
 // leaf cells: moments (m, 0, ..., 0); thread = (cell, 16-byte pair), so a
-// warp writes 512 contiguous bytes of the AoS moments
-__global__ void amr_p2m_kernel(const double* __restrict__ mass, long long nslots,
+// warp writes 512 contiguous bytes of the AoS moments; slots lo .. lo+nslots
+__global__ void amr_p2m_kernel(const double* __restrict__ mass, long long nslots, long long lo,
                                const int* __restrict__ slot_level, const int* __restrict__ slot_node,
                                const GLv* __restrict__ L) {
   const long long total = nslots * 512 * 5;
   for (long long u = blockIdx.x * (long long)blockDim.x + threadIdx.x; u < total;
        u += (long long)gridDim.x * blockDim.x) {
-    const long long t = u / 5;
-    const int pr = (int)(u - 5 * t);
+    const long long t = lo * 512 + u / 5;
+    const int pr = (int)(u % 5);
     const long long s = t >> 9;
     const int c = (int)(t & 511);
     double2* o = reinterpret_cast<double2*>(L[slot_level[s]].mom + ((long long)slot_node[s] * 512 + c) * 10);
     o[pr] = make_double2(pr == 0 ? mass[t] : 0.0, 0.0);
+  }
+}
+
+// LET moment exchange: whole patches (512 cells x 10 moments) between the
+// moment arrays and a contiguous buffer (block j of `list` <-> buffer block
+// blk ? blk[j] : j); one CTA per patch
+__global__ void pack_patches_kernel(const GLv* __restrict__ Lv, const int2* __restrict__ list,
+                                    const int* __restrict__ blk, double* __restrict__ buf) {
+  const int2 p = list[blockIdx.x];
+  const double2* src = reinterpret_cast<const double2*>(Lv[p.x].mom + (long long)p.y * 5120);
+  double2* dst = reinterpret_cast<double2*>(buf + (long long)(blk ? blk[blockIdx.x] : blockIdx.x) * 5120);
+  for (int q = threadIdx.x; q < 2560; q += blockDim.x) dst[q] = src[q];
+}
+
+__global__ void unpack_patches_kernel(const GLv* __restrict__ Lv, const int2* __restrict__ list,
+                                      const int* __restrict__ blk, const double* __restrict__ buf) {
+  const int2 p = list[blockIdx.x];
+  const double2* src =
+      reinterpret_cast<const double2*>(buf + (long long)(blk ? blk[blockIdx.x] : blockIdx.x) * 5120);
+  double2* dst = reinterpret_cast<double2*>(Lv[p.x].mom + (long long)p.y * 5120);
+  for (int q = threadIdx.x; q < 2560; q += blockDim.x) dst[q] = src[q];
+}
+
+// masses of received leaf patches (their P2P sources) from their monopoles
+__global__ void halo_mass_kernel(const GLv* __restrict__ Lv, const int* __restrict__ slots, long long n,
+                                 const int* __restrict__ slot_level, const int* __restrict__ slot_node,
+                                 double* __restrict__ mass) {
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < n * 512;
+       t += (long long)gridDim.x * blockDim.x) {
+    const int s = slots[t >> 9], c = (int)(t & 511);
+    mass[(long long)s * 512 + c] = Lv[slot_level[s]].mom[((long long)slot_node[s] * 512 + c) * 10];
   }
 }
 
@@ -816,6 +847,22 @@ struct GravAmrWork {
   long long lo = 0, hi = 0;
   std::vector<long long> seg_lo, seg_cnt;  // per rank (slots)
   long long seg_max = 0;                   // largest rank segment (slots)
+  // locally essential tree (grav_let_plan): device lists and buffers
+  bool let = false;
+  std::vector<int*> let_owned, let_top;    // per level internal patch lists
+  std::vector<long long> n_owned, n_top;
+  int2* roots_all = nullptr;               // every rank's subtree roots, rank-major
+  int* roots_blk = nullptr;                //   their blocks in roots_buf ([rank][max_roots])
+  long long n_roots_all = 0, my_roots_at = 0, n_my_roots = 0, max_roots = 0;
+  double* roots_buf = nullptr;
+  int2* send_list = nullptr;               // peer-major; recv likewise
+  int2* recv_list = nullptr;
+  long long n_send = 0, n_recv = 0;
+  std::vector<long long> send_off, send_cnt, recv_off, recv_cnt;  // in doubles, per peer
+  double* send_buf = nullptr;
+  double* recv_buf = nullptr;
+  int* halo_slots = nullptr;
+  long long n_halo_slots = 0;
   double* gather = nullptr;                // [world][seg_max][512] all-gather staging
   std::vector<int*> need;                  // per level device node list (nullptr = all)
   std::vector<long long> nneed;
@@ -849,6 +896,66 @@ static int allgather_slots(GravAmrWork& w, double* base, int per_slot, cudaStrea
       *e = cudaMemcpyAsync(base + w.seg_lo[r] * per_slot, w.gather + (size_t)r * per,
                            (size_t)w.seg_cnt[r] * per_slot * sizeof(double), cudaMemcpyDeviceToDevice, st);
   return rc;
+}
+
+// device side of grav_let_plan (tmgpu_gravity_amr_distribute)
+static cudaError_t build_let(GravAmrWork& w, const std::vector<long long>& bounds, int me) {
+  const GravPlan& P = w.plan;
+  const GravLetPlan G = grav_let_plan(P, bounds, me);
+  const int R = (int)bounds.size() - 1;
+  auto own = [&w](void* p) {
+    if (p) w.allocs.push_back(p);
+  };
+  cudaError_t e = cudaSuccess;
+  w.let_owned.assign(P.nlevels, nullptr);
+  w.let_top.assign(P.nlevels, nullptr);
+  w.n_owned.assign(P.nlevels, 0);
+  w.n_top.assign(P.nlevels, 0);
+  for (int l = 0; l < P.nlevels && e == cudaSuccess; ++l) {
+    w.n_owned[l] = (long long)G.owned_internal[l].size();
+    w.n_top[l] = (long long)G.top_internal[l].size();
+    e = upload(G.owned_internal[l], &w.let_owned[l]);
+    own(w.let_owned[l]);
+    if (e == cudaSuccess) e = upload(G.top_internal[l], &w.let_top[l]), own(w.let_top[l]);
+  }
+  std::vector<int2> roots;
+  std::vector<int> blk;
+  w.max_roots = 1;
+  for (int r = 0; r < R; ++r) w.max_roots = std::max(w.max_roots, (long long)G.roots[r].size());
+  for (int r = 0; r < R; ++r) {
+    if (r == me) w.my_roots_at = (long long)roots.size(), w.n_my_roots = (long long)G.roots[r].size();
+    for (size_t i = 0; i < G.roots[r].size(); ++i) {
+      roots.push_back(make_int2(G.roots[r][i].level, G.roots[r][i].node));
+      blk.push_back((int)(r * w.max_roots + (long long)i));
+    }
+  }
+  w.n_roots_all = (long long)roots.size();
+  if (e == cudaSuccess) e = upload(roots, &w.roots_all), own(w.roots_all);
+  if (e == cudaSuccess) e = upload(blk, &w.roots_blk), own(w.roots_blk);
+  if (e == cudaSuccess)
+    e = cudaMalloc(&w.roots_buf, (size_t)R * w.max_roots * 5120 * sizeof(double)), own(w.roots_buf);
+  std::vector<int2> sl, rl;
+  w.send_off.assign(R, 0), w.send_cnt.assign(R, 0), w.recv_off.assign(R, 0), w.recv_cnt.assign(R, 0);
+  for (int q = 0; q < R; ++q) {
+    w.send_off[q] = (long long)sl.size() * 5120;
+    w.send_cnt[q] = (long long)G.send[q].size() * 5120;
+    for (const PatchRef& p : G.send[q]) sl.push_back(make_int2(p.level, p.node));
+    w.recv_off[q] = (long long)rl.size() * 5120;
+    w.recv_cnt[q] = (long long)G.recv[q].size() * 5120;
+    for (const PatchRef& p : G.recv[q]) rl.push_back(make_int2(p.level, p.node));
+  }
+  w.n_send = (long long)sl.size();
+  w.n_recv = (long long)rl.size();
+  if (e == cudaSuccess) e = upload(sl, &w.send_list), own(w.send_list);
+  if (e == cudaSuccess) e = upload(rl, &w.recv_list), own(w.recv_list);
+  if (e == cudaSuccess)
+    e = cudaMalloc(&w.send_buf, (size_t)(w.n_send ? w.n_send : 1) * 5120 * sizeof(double)), own(w.send_buf);
+  if (e == cudaSuccess)
+    e = cudaMalloc(&w.recv_buf, (size_t)(w.n_recv ? w.n_recv : 1) * 5120 * sizeof(double)), own(w.recv_buf);
+  w.n_halo_slots = (long long)G.halo_leaf_slots.size();
+  if (e == cudaSuccess) e = upload(G.halo_leaf_slots, &w.halo_slots), own(w.halo_slots);
+  if (e == cudaSuccess) w.let = true;
+  return e;
 }
 
 // internal patches that need the L2L pass, per level (leaf patches: in L2P)
@@ -1074,6 +1181,40 @@ int tmgpu_gravity_amr_plan_need(const int* leaves, long long nleaves, long long 
   return P.nlevels;
 }
 
+// Host-only (tests, diagnostics): the LET plan of rank `me` of `world` with
+// canonical slot bounds[world + 1]: out[0..3] = owned internal, shared top,
+// own subtree roots, halo leaf patches; send[q] / recv[q] = patch counts and
+// send_hash[q] / recv_hash[q] = an order-sensitive hash of the patch lists
+// (rank r's send list to q must equal q's receive list from r).
+int tmgpu_gravity_amr_let_plan(const int* leaves, long long nleaves, const long long* bounds, int world,
+                               int me, long long* out, long long* send, long long* recv,
+                               long long* send_hash, long long* recv_hash, tmgpu_error* err) {
+  if (err) std::memset(err, 0, sizeof(*err));
+  GravPlan P;
+  std::string why;
+  if (!build_grav_plan(leaves, nleaves, P, &why)) return set_err(err, TMGPU_ERR_INVALID, why.c_str());
+  const GravLetPlan G = grav_let_plan(P, std::vector<long long>(bounds, bounds + world + 1), me);
+  out[0] = out[1] = 0;
+  for (int l = 0; l < P.nlevels; ++l) {
+    out[0] += (long long)G.owned_internal[l].size();
+    out[1] += (long long)G.top_internal[l].size();
+  }
+  out[2] = (long long)G.roots[me].size();
+  out[3] = (long long)G.halo_leaf_slots.size();
+  auto hash = [](const std::vector<PatchRef>& v) {
+    unsigned long long h = 1469598103934665603ULL;
+    for (const PatchRef& p : v) h = (h ^ (unsigned long long)(p.level * 1000003LL + p.node)) * 1099511628211ULL;
+    return (long long)(h >> 1);
+  };
+  for (int q = 0; q < world; ++q) {
+    send[q] = (long long)G.send[q].size();
+    recv[q] = (long long)G.recv[q].size();
+    send_hash[q] = hash(G.send[q]);
+    recv_hash[q] = hash(G.recv[q]);
+  }
+  return TMGPU_OK;
+}
+
 // Host-only: build the plan and report info[4] without touching the GPU.
 int tmgpu_gravity_amr_plan_info(const int* leaves, long long nleaves, long long* out,
                                 tmgpu_error* err) {
@@ -1127,19 +1268,47 @@ int tmgpu_gravity_amr_solve(tmgpu_gravity_amr* G, const double* mass, double* ph
     cudaEventRecord(rec.ev[0], st);
   }
   int rc = TMGPU_OK;
-  if (e == cudaSuccess && w.comm)  // every rank needs every leaf mass for the upward pass
-    rc = allgather_slots(w, w.mass, 512, st, &e, &why);
   if (timed) cudaEventRecord(rec.ev[1], st);
   if (e == cudaSuccess && rc == TMGPU_OK) {
     long long launches = 0;
-    amr_p2m_kernel<<<grid_for(ncell * 5), 128, 0, st>>>(w.mass, w.nslots, w.slot_level, w.slot_node,
-                                                        w.dev_lv);
+    if (nloc)
+      amr_p2m_kernel<<<grid_for(nout * 5), 128, 0, st>>>(w.mass, nloc, w.lo, w.slot_level, w.slot_node,
+                                                         w.dev_lv);
     ++launches;
-    for (int l = P.nlevels - 2; l >= 0; --l) {
-      const long long ni = (long long)P.lv[l].internal.size();
+    for (int l = P.nlevels - 2; l >= 0; --l) {  // own subtrees (all of the tree on one GPU)
+      const long long ni = w.let ? w.n_owned[l] : (long long)P.lv[l].internal.size();
       if (!ni) continue;
-      amr_m2m_kernel<<<grid_for(ni * 512), 128, 0, st>>>(w.dev_lv, l, w.internal[l], ni);
+      amr_m2m_kernel<<<grid_for(ni * 512), 128, 0, st>>>(w.dev_lv, l, w.let ? w.let_owned[l] : w.internal[l],
+                                                         ni);
       ++launches;
+    }
+    if (w.let) {
+      // LET moment exchange: subtree roots to everyone, the shared top by M2M,
+      // then the owned patches other ranks read, point to point
+      if (w.n_my_roots)
+        pack_patches_kernel<<<(unsigned)w.n_my_roots, 256, 0, st>>>(
+            w.dev_lv, w.roots_all + w.my_roots_at, w.roots_blk + w.my_roots_at, w.roots_buf);
+      const size_t per = (size_t)w.max_roots * 5120;
+      rc = comm_allgather(w.comm, w.roots_buf + (size_t)comm_rank(w.comm) * per, w.roots_buf, per, st, &why);
+      if (rc == TMGPU_OK && w.n_roots_all)
+        unpack_patches_kernel<<<(unsigned)w.n_roots_all, 256, 0, st>>>(w.dev_lv, w.roots_all, w.roots_blk,
+                                                                       w.roots_buf);
+      for (int l = P.nlevels - 2; l >= 0 && rc == TMGPU_OK; --l) {
+        if (!w.n_top[l]) continue;
+        amr_m2m_kernel<<<grid_for(w.n_top[l] * 512), 128, 0, st>>>(w.dev_lv, l, w.let_top[l], w.n_top[l]);
+        ++launches;
+      }
+      if (rc == TMGPU_OK && w.n_send)
+        pack_patches_kernel<<<(unsigned)w.n_send, 256, 0, st>>>(w.dev_lv, w.send_list, nullptr, w.send_buf);
+      if (rc == TMGPU_OK)
+        rc = comm_exchange(w.comm, w.send_buf, w.send_off, w.send_cnt, w.recv_buf, w.recv_off, w.recv_cnt,
+                           st, &why);
+      if (rc == TMGPU_OK && w.n_recv)
+        unpack_patches_kernel<<<(unsigned)w.n_recv, 256, 0, st>>>(w.dev_lv, w.recv_list, nullptr, w.recv_buf);
+      if (rc == TMGPU_OK && w.n_halo_slots)
+        halo_mass_kernel<<<grid_for(w.n_halo_slots * 512), 128, 0, st>>>(
+            w.dev_lv, w.halo_slots, w.n_halo_slots, w.slot_level, w.slot_node, w.mass);
+      launches += 5;
     }
     m2m_kernel<<<1, 128, 0, st>>>(w.host_lv[0].mom, w.dmom[2], 4, 1.0 / 8.0);
     m2m_kernel<<<1, 128, 0, st>>>(w.dmom[2], w.dmom[1], 2, 1.0 / 4.0);
@@ -1274,6 +1443,7 @@ int tmgpu_gravity_amr_distribute(tmgpu_gravity_amr* G, tmgpu_comm* comm, const l
   }
   if (e == cudaSuccess) e = build_m2l_work(w, &lists);
   if (e == cudaSuccess) e = build_l2l_lists(w, &lists);
+  if (e == cudaSuccess) e = build_let(w, std::vector<long long>(slot_bounds, slot_bounds + R + 1), me);
   count_work(P, &lists, w.lo, w.hi, w.work);  // this GPU's share (bench roofline)
   return cuda_err(err, e, "tmgpu_gravity_amr_distribute");
 }

@@ -286,4 +286,97 @@ std::vector<std::vector<int>> grav_owned_ancestors(const GravPlan& P, long long 
   return out;
 }
 
+// patches whose moments a rank owning slots [lo, hi) reads: the 27-patch
+// neighbourhoods of its M2L patches, their W/X sources, the cross-depth U
+// sources of its leaf cells (mark[l][n] = 1)
+static std::vector<std::vector<char>> moment_reads(const GravPlan& P, long long lo, long long hi) {
+  const auto need = grav_owned_ancestors(P, lo, hi);
+  std::vector<std::vector<char>> mark(P.nlevels);
+  for (int l = 0; l < P.nlevels; ++l) mark[l].assign(P.lv[l].n, 0);
+  auto add_src = [&](int64_t enc) { mark[(int)(enc >> 40)][(int)((enc & ((1LL << 40) - 1)) >> 9)] = 1; };
+  for (int l = 0; l < P.nlevels; ++l) {
+    const GravLevel& L = P.lv[l];
+    for (int n : need[l]) {
+      for (int o = 0; o < 27; ++o) {
+        const int nb = L.nbr[(size_t)n * 27 + o];
+        if (nb >= 0) mark[l][nb] = 1;
+      }
+      for (int64_t e = L.moff[(size_t)n * 512]; e < L.moff[(size_t)(n + 1) * 512]; ++e) add_src(L.ment[e]);
+    }
+  }
+  for (long long s = lo; s < hi; ++s) {
+    const GravLevel& L = P.lv[P.slot_level[s]];
+    const int n = P.slot_node[s];
+    for (int64_t e = L.poff[(size_t)n * 512]; e < L.poff[(size_t)(n + 1) * 512]; ++e) add_src(L.pent[e]);
+  }
+  return mark;
+}
+
+GravLetPlan grav_let_plan(const GravPlan& P, const std::vector<long long>& bounds, int me) {
+  const int R = (int)bounds.size() - 1;
+  auto rank_of = [&](long long slot) {
+    return (int)(std::upper_bound(bounds.begin(), bounds.end(), slot) - bounds.begin()) - 1;
+  };
+  // owner per patch (-1: spans ranks), bottom-up from the leaf slots
+  std::vector<std::vector<int>> own(P.nlevels);
+  for (int l = P.nlevels - 1; l >= 0; --l) {
+    const GravLevel& L = P.lv[l];
+    own[l].assign(L.n, -1);
+    for (int n = 0; n < L.n; ++n) {
+      if (L.leaf_slot[n] >= 0) {
+        own[l][n] = rank_of(L.leaf_slot[n]);
+        continue;
+      }
+      int o = own[l + 1][L.child[(size_t)n * 8]];
+      for (int c = 1; c < 8 && o >= 0; ++c)
+        if (own[l + 1][L.child[(size_t)n * 8 + c]] != o) o = -1;
+      own[l][n] = o;
+    }
+  }
+  GravLetPlan G;
+  G.owned_internal.resize(P.nlevels);
+  G.top_internal.resize(P.nlevels);
+  G.roots.resize(R);
+  G.send.resize(R);
+  G.recv.resize(R);
+  std::vector<std::vector<char>> avail(P.nlevels);  // computed or all-gathered on every rank
+  for (int l = 0; l < P.nlevels; ++l) {
+    const GravLevel& L = P.lv[l];
+    avail[l].assign(L.n, 0);
+    for (int n = 0; n < L.n; ++n) {
+      const int o = own[l][n];
+      const bool leaf = L.leaf_slot[n] >= 0;
+      if (o < 0) {
+        if (!leaf) G.top_internal[l].push_back(n);
+        avail[l][n] = 1;
+        continue;
+      }
+      if (o == me && !leaf) G.owned_internal[l].push_back(n);
+      if (l == 0 || own[l - 1][L.parent[n]] < 0) {
+        G.roots[o].push_back(PatchRef{l, n});
+        avail[l][n] = 1;
+      }
+    }
+  }
+  // point-to-point halo: what rank q reads of rank r's owned, non-root patches
+  for (int q = 0; q < R; ++q) {
+    if (q == me && R == 1) break;
+    const auto reads = moment_reads(P, bounds[q], bounds[q + 1]);
+    for (int l = 0; l < P.nlevels; ++l)
+      for (int n = 0; n < P.lv[l].n; ++n) {
+        if (!reads[l][n]) continue;
+        const int o = own[l][n];
+        if (o == q) continue;
+        // other ranks' leaf patches this rank reads: their masses feed its P2P
+        if (q == me && o >= 0 && P.lv[l].leaf_slot[n] >= 0) G.halo_leaf_slots.push_back(P.lv[l].leaf_slot[n]);
+        if (avail[l][n]) continue;
+        if (q == me)
+          G.recv[o].push_back(PatchRef{l, n});
+        else if (o == me)
+          G.send[q].push_back(PatchRef{l, n});
+      }
+  }
+  return G;
+}
+
 }  // namespace tmgpu

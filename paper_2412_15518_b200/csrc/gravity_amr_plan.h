@@ -49,4 +49,26 @@ bool build_grav_plan(const int* leaves, long long nleaves, GravPlan& plan, std::
 // slots must evaluate (their locals flow down to its leaves).
 std::vector<std::vector<int>> grav_owned_ancestors(const GravPlan& plan, long long lo, long long hi);
 
+// Multi-GPU locally essential tree (the multipole-moment exchange). A patch is
+// owned by rank r when every leaf of its subtree is r's (canonical slots are
+// Morton DFS, so a subtree is a contiguous slot range); patches spanning
+// ranks form the shared top T. Rank r computes its owned subtrees' moments
+// (P2M, M2M), all ranks all-gather the owned subtree roots R (children of T
+// or the root), every rank then computes T by M2M, and the owned patches
+// other ranks read (V-list neighbourhoods, W/X and cross-depth U sources of
+// their targets) are sent point to point. Every moment is computed exactly as
+// on one GPU, so the solve stays bitwise.
+struct PatchRef {
+  int level, node;
+};
+struct GravLetPlan {
+  std::vector<std::vector<int>> owned_internal;  // per level: this rank's owned internal patches
+  std::vector<std::vector<int>> top_internal;    // per level: T (shared) patches
+  std::vector<std::vector<PatchRef>> roots;      // per rank: its owned subtree roots R_r
+  std::vector<std::vector<PatchRef>> send;       // per peer: owned patches the peer reads
+  std::vector<std::vector<PatchRef>> recv;       // per peer: the peer's patches this rank reads
+  std::vector<int> halo_leaf_slots;              // received leaf patches (their masses are read)
+};
+GravLetPlan grav_let_plan(const GravPlan& plan, const std::vector<long long>& slot_bounds, int me);
+
 }  // namespace tmgpu

@@ -152,6 +152,28 @@ def amr_plan_need(leaves, lo: int, hi: int):
     return list(out[:n])
 
 
+lib.tmgpu_gravity_amr_let_plan.restype = C.c_int
+lib.tmgpu_gravity_amr_let_plan.argtypes = [_vp, C.c_longlong, _lp, C.c_int, C.c_int, _lp, _lp, _lp, _lp,
+                                           _lp, _ep]
+
+
+def amr_let_plan(leaves, bounds, me: int):
+    """Host-only: rank `me`'s multipole-moment exchange plan (csrc grav_let_plan):
+    dict with owned/top/roots/halo_leaves counts and per-peer send/recv counts
+    and list hashes."""
+    lv = _leaf_array(leaves)
+    b = np.ascontiguousarray(np.asarray(bounds, dtype=np.int64))
+    world = len(b) - 1
+    out = (C.c_longlong * 4)()
+    arrs = [(C.c_longlong * world)() for _ in range(4)]
+    err = TmgpuError()
+    _lib.check(lib.tmgpu_gravity_amr_let_plan(lv.ctypes.data, lv.shape[0], b.ctypes.data_as(_lp), world,
+                                              me, out, *arrs, C.byref(err)), err)
+    return {"owned_internal": out[0], "top_internal": out[1], "roots": out[2], "halo_leaves": out[3],
+            "send": list(arrs[0]), "recv": list(arrs[1]), "send_hash": list(arrs[2]),
+            "recv_hash": list(arrs[3])}
+
+
 def forest_leaf_array(forest):
     """[n, 4] (level, I, J, K) of a forest's local leaves in slot order."""
     from .amr import unpack

@@ -162,3 +162,29 @@ def test_product_plan_rejects_bad_leaves():
         G.amr_plan_info(lv[:-1])
     with pytest.raises(ValueError, match="overlap"):
         G.amr_plan_info(np.concatenate([lv, [[0, 0, 0, 0]]]))
+
+
+@pytest.mark.parametrize("world", [2, 3, 4, 8])
+def test_let_plan_pairwise_consistent(world):
+    """Multipole-moment exchange (LET, csrc grav_let_plan): rank r's send list to
+    q is q's receive list from r (counts and ordered hashes), and the owned
+    internal patches of all ranks plus the shared top cover every internal patch."""
+    from paper_2412_15518_b200 import amr, dist
+    from paper_2412_15518_b200.gravity import amr_let_plan, amr_plan_info, forest_leaf_array
+
+    f = amr.build_scenario(amr.Scenario.rotating_star, 2, 4)
+    lv = forest_leaf_array(f)
+    owner = np.array(dist.partition(f, world))
+    b = np.searchsorted(owner, np.arange(world + 1))
+    b[-1] = len(owner)
+    plans = [amr_let_plan(lv, b, r) for r in range(world)]
+    for r in range(world):
+        assert plans[r]["send"][r] == 0 and plans[r]["recv"][r] == 0
+        for q in range(world):
+            assert plans[r]["send"][q] == plans[q]["recv"][r]
+            assert plans[r]["send_hash"][q] == plans[q]["recv_hash"][r]
+    tops = {p["top_internal"] for p in plans}
+    assert len(tops) == 1  # every rank computes the same shared top
+    nodes = amr_plan_info(lv)[1]
+    leaves = lv.shape[0]
+    assert sum(p["owned_internal"] for p in plans) + tops.pop() == nodes - leaves
