@@ -168,6 +168,12 @@ int tmgpu_forest_set_reflux(tmgpu_forest* f, int on, tmgpu_error* err);
  * local slot; NULL = pure hydro (the reference's stage) */
 int tmgpu_forest_set_gravity(tmgpu_forest* f, const double* g, long long comp_stride,
                              tmgpu_error* err);
+/* the stream the next steps' gravity is computed on (NULL: the step's stream): the step runs its
+ * CFL reduction and first ghost exchange concurrently and waits for that stream's work (enqueued
+ * before the step call) only before the first stage kernel */
+int tmgpu_forest_set_gravity_stream(tmgpu_forest* f, void* stream, tmgpu_error* err);
+/* `waiter` waits for the work enqueued so far on `signaller` (CUDA streams; NULL = default) */
+int tmgpu_stream_wait(void* waiter, void* signaller);
 int tmgpu_forest_step(tmgpu_forest* f, double dt, double cfl, double gamma, int flags,
                       void* stream, double* dt_used, tmgpu_error* err);
 int tmgpu_forest_check(tmgpu_forest* f, void* stream, tmgpu_error* err);

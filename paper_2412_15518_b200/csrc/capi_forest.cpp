@@ -48,6 +48,11 @@ struct tmgpu_forest {
   long long rf_n = 0;
   const double* grav = nullptr;  // optional gravity g[3][stride] by local slot (device)
   long long grav_stride = 0;
+  // optional: the stream the step's gravity is computed on; the step runs its
+  // CFL reduction and first ghost exchange concurrently and waits for that
+  // stream only before the first stage kernel
+  cudaStream_t grav_stream = nullptr;
+  cudaEvent_t ev_grav = nullptr;
   unsigned long long* err_dev = nullptr;
   // reference-exact 3-pass exchange (single GPU only)
   double* staged = nullptr;
@@ -341,6 +346,7 @@ void tmgpu_forest_destroy(tmgpu_forest* f) {
   if (!f) return;
   free_dev(f);
   tmgpu_forest_set_reflux(f, 0, nullptr);
+  if (f->ev_grav) cudaEventDestroy(f->ev_grav);
   if (f->side) cudaStreamDestroy(f->side);
   if (f->ev_packed) cudaEventDestroy(f->ev_packed);
   if (f->ev_remote) cudaEventDestroy(f->ev_remote);
@@ -681,7 +687,9 @@ int tmgpu_forest_step(tmgpu_forest* f, double dt, double cfl, double gamma, int 
     collect_timing(f);  // events are reused: fold the previous step in first
     cudaEventRecord(f->ev[0], st);
   }
-  if (!(flags & TMGPU_ASYNC)) e = cudaMemsetAsync(f->err_dev, 0xff, sizeof(unsigned long long), st);
+  if (f->grav_stream) e = cudaEventRecord(f->ev_grav, f->grav_stream);  // gravity enqueued so far
+  if (!(flags & TMGPU_ASYNC) && e == cudaSuccess)
+    e = cudaMemsetAsync(f->err_dev, 0xff, sizeof(unsigned long long), st);
   if (e == cudaSuccess && cfl > 0.0) {
     e = launch_max_wavespeed(f->arena(), (long long)V * 1728, nullptr, 0, nullptr, gamma, V, f->nslots,
                              f->speeds, st);
@@ -741,6 +749,7 @@ int tmgpu_forest_step(tmgpu_forest* f, double dt, double cfl, double gamma, int 
       return fail(err, rc, why);
     }
     if (timed) cudaEventRecord(f->ev[2 * stage], st);
+    if (stage == 1 && f->grav_stream && e == cudaSuccess) e = cudaStreamWaitEvent(st, f->ev_grav, 0);
     p.rk_stage = stage;
     p.u0_save = stage == 1 ? f->u0 : nullptr;
     p.u0_save_stride = (long long)V * 512;
@@ -781,6 +790,30 @@ int tmgpu_forest_step(tmgpu_forest* f, double dt, double cfl, double gamma, int 
   if (cfl > 0.0 && !std::isfinite(dtv))
     return fail(err, TMGPU_ERR_SOLVER, "cfl_dt: no wave speed (s = 0 everywhere)");
   if (w != ~0ull) return solver_err_from_word(err, w, f->plan.loc2gl);
+  return TMGPU_OK;
+}
+
+// `waiter` waits for the work enqueued so far on `signaller` (an event
+// recorded and waited on; released once it completes).
+int tmgpu_stream_wait(void* waiter, void* signaller) {
+  cudaEvent_t ev;
+  cudaError_t e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+  if (e == cudaSuccess) e = cudaEventRecord(ev, as_stream(signaller));
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(as_stream(waiter), ev, 0);
+  cudaEventDestroy(ev);
+  return e == cudaSuccess ? TMGPU_OK : TMGPU_ERR_CUDA;
+}
+
+// The stream later steps' gravity is computed on (nullptr: same stream as the
+// step): the step overlaps its CFL reduction and first exchange with it.
+int tmgpu_forest_set_gravity_stream(tmgpu_forest* f, void* stream, tmgpu_error* err) {
+  if (err) std::memset(err, 0, sizeof(*err));
+  if (!f) return fail(err, TMGPU_ERR_INVALID, "null forest");
+  if (!f->ev_grav) {
+    cudaError_t e = cudaEventCreateWithFlags(&f->ev_grav, cudaEventDisableTiming);
+    if (e != cudaSuccess) return cuda_err(err, e, "tmgpu_forest_set_gravity_stream");
+  }
+  f->grav_stream = static_cast<cudaStream_t>(stream);
   return TMGPU_OK;
 }
 

@@ -58,6 +58,10 @@ class HydroDriver:
         _lib.check(lib.tmgpu_forest_check(self.forest.h, stream, C.byref(err)), err, SolverError)
 
 
+lib.tmgpu_stream_wait.restype = C.c_int
+lib.tmgpu_stream_wait.argtypes = [C.c_void_p, C.c_void_p]
+lib.tmgpu_forest_set_gravity_stream.restype = C.c_int
+lib.tmgpu_forest_set_gravity_stream.argtypes = [C.c_void_p, C.c_void_p, C.POINTER(TmgpuError)]
 lib.tmgpu_forest_set_gravity.restype = C.c_int
 lib.tmgpu_forest_set_gravity.argtypes = [C.c_void_p, C.c_void_p, C.c_longlong, C.POINTER(TmgpuError)]
 
@@ -88,7 +92,21 @@ class GravityHydroDriver(HydroDriver):
         if forest.local_count() != forest.leaf_count():
             if comm is None:
                 raise ValueError("distributed forest without a communicator")
-            self.gravity.distribute(comm, forest._owner)
+            # its own NCCL communicator: the moment exchange runs on the gravity
+            # stream concurrently with the hydro step's dt reduction and halo
+            from .dist import Comm
+
+            self.gcomm = Comm.from_torch()
+            self.gravity.distribute(self.gcomm, forest._owner)
+        # multi-GPU: the solve (latency-bound moment exchange and upward pass)
+        # runs on a side stream, overlapped with the CFL reduction and the
+        # first ghost exchange; the first stage kernel waits for it. One GPU:
+        # the step's own stream (the M2L fills the GPU; nothing to overlap)
+        self.gstream = None
+        if forest.local_count() != forest.leaf_count():
+            self.gstream = torch.cuda.Stream()
+            _lib.check(lib.tmgpu_forest_set_gravity_stream(forest.h, self.gstream.cuda_stream,
+                                                           C.byref(TmgpuError())), TmgpuError())
         n = forest.local_count() * 512
         self.phi = torch.empty(n, dtype=torch.float64, device="cuda")
         self.g = torch.zeros(3 * n, dtype=torch.float64, device="cuda")
@@ -96,8 +114,18 @@ class GravityHydroDriver(HydroDriver):
         _lib.check(lib.tmgpu_forest_set_gravity(forest.h, self.g.data_ptr(), n, C.byref(err)), err)
 
     def solve_gravity(self, stream=None) -> None:
-        self.gravity.mass_from_arena(self.forest, stream)
-        self.gravity.solve(None, am=self.am, phi=self.phi, g=self.g, stream=stream, sync=False)
+        """Enqueue the solve (on the gravity stream after the work already on
+        `stream` — the state it reads — when distributed)."""
+        import torch
+
+        gs = stream
+        if self.gstream is not None:
+            if stream is None:
+                stream = torch.cuda.current_stream().cuda_stream
+            lib.tmgpu_stream_wait(self.gstream.cuda_stream, stream)
+            gs = self.gstream.cuda_stream
+        self.gravity.mass_from_arena(self.forest, gs)
+        self.gravity.solve(None, am=self.am, phi=self.phi, g=self.g, stream=gs, sync=False)
 
     def step(self, dt: float | None = None, stream=None, sync: bool = True) -> float | None:
         self.solve_gravity(stream)
@@ -106,6 +134,7 @@ class GravityHydroDriver(HydroDriver):
     def close(self) -> None:
         err = TmgpuError()
         lib.tmgpu_forest_set_gravity(self.forest.h, None, 0, C.byref(err))
+        lib.tmgpu_forest_set_gravity_stream(self.forest.h, None, C.byref(err))
 
 
 class HostStepPipeline:
