@@ -255,33 +255,76 @@ __device__ __forceinline__ void m2l_row(const double* __restrict__ src, const do
   }
 }
 
-// Offset-major variant: per x-offset jj, the geometry (13 registers) is loaded
-// once and applied to the four targets' sources sx = jj + 2k — independent
-// accumulators, so four FMA chains are in flight per thread; every source is
-// loaded twice per row. Each target still sees its sources in dx order.
+// Offset-major rows: per x-offset jj the geometry (13 registers) is loaded
+// once and applied to the four targets' sources sx = jj + 2k. The contraction
+// is m2l_acc's, operation for operation per target, issued target-interleaved:
+// four consecutive DFMAs share the geometry operand (operand reuse cache: two
+// fresh register reads per DFMA instead of three) and form four independent
+// chains. Each target still sees its sources in dx order.
 template <bool NEAR>
 __device__ __forceinline__ void m2l_row_jj(const double* __restrict__ src,
                                            const double* __restrict__ trow, double (&acc)[4][10]) {
 #pragma unroll
   for (int jj = 0; jj < 6; ++jj) {
     if (NEAR && (jj == 2 || jj == 3)) continue;
-    double G[kTab];
+    double e[kTab];
     const double2* t2 = reinterpret_cast<const double2*>(trow + jj * kTabP);
 #pragma unroll
     for (int q = 0; q < 6; ++q) {
       const double2 v = t2[q];
-      G[2 * q] = v.x;
-      G[2 * q + 1] = v.y;
+      e[2 * q] = v.x;
+      e[2 * q + 1] = v.y;
     }
-    G[12] = trow[jj * kTabP + 12];
+    e[12] = trow[jj * kTabP + 12];
+    double m[4][10];
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const int sx = jj + 2 * k;
-      double m[10];
+    for (int k = 0; k < 4; ++k)
 #pragma unroll
-      for (int q = 0; q < 10; ++q) m[q] = src[q * kWVar + sx];
-      m2l_acc(-m[0], m[1], m[2], m[3], -m[4], -m[5], -m[6], -m[7], -m[8], -m[9], G, acc[k]);
+      for (int q = 0; q < 10; ++q) m[k][q] = src[q * kWVar + jj + 2 * k];
+    double t[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) t[k] = -m[k][0] * e[0];
+    // L0 increment: D (e1 e2 e3), then Q (xx e10, xy e5, xz e6, yy e11, yz e8, zz e12)
+#pragma unroll
+    for (int k = 0; k < 4; ++k) t[k] = fma(m[k][1], e[1], t[k]);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) t[k] = fma(m[k][2], e[2], t[k]);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) t[k] = fma(m[k][3], e[3], t[k]);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) t[k] = fma(-m[k][4], e[10], t[k]);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) t[k] = fma(-m[k][5], e[5], t[k]);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) t[k] = fma(-m[k][6], e[6], t[k]);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) t[k] = fma(-m[k][7], e[11], t[k]);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) t[k] = fma(-m[k][8], e[8], t[k]);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) t[k] = fma(-m[k][9], e[12], t[k]);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) acc[k][0] = acc[k][0] + t[k];
+    // L_i: -M D1_i, then D_x, D_y, D_z against the D2 row i
+    // rows: x (e4 e5 e6), y (e5 e7 e8), z (e6 e8 e9)
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+      const int r0 = i == 0 ? 4 : (i == 1 ? 5 : 6), r1 = i == 0 ? 5 : (i == 1 ? 7 : 8),
+                r2 = i == 0 ? 6 : (i == 1 ? 8 : 9);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) acc[k][1 + i] = fma(-m[k][0], e[1 + i], acc[k][1 + i]);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) acc[k][1 + i] = fma(m[k][1], e[r0], acc[k][1 + i]);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) acc[k][1 + i] = fma(m[k][2], e[r1], acc[k][1 + i]);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) acc[k][1 + i] = fma(m[k][3], e[r2], acc[k][1 + i]);
     }
+    // L_ij: -M D2_ij
+#pragma unroll
+    for (int q = 0; q < 6; ++q)
+#pragma unroll
+      for (int k = 0; k < 4; ++k) acc[k][4 + q] = fma(-m[k][0], e[4 + q], acc[k][4 + q]);
   }
 }
 
