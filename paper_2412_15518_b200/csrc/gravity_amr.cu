@@ -448,7 +448,7 @@ __global__ void __launch_bounds__(kM2lThreads, 1) amr_m2l_fused_kernel(
 // W/X pairs (AMR level jumps) after the V-list sums, in the list's sorted
 // order, one thread per target with entries (targets in patch order);
 // geometry from the plan's separation table (m2l_geom of each distinct R).
-__global__ void amr_wx_kernel(const GLv* __restrict__ Lv, const int* __restrict__ tlev,
+__global__ void __launch_bounds__(128, 4) amr_wx_kernel(const GLv* __restrict__ Lv, const int* __restrict__ tlev,
                               const long long* __restrict__ tflat, long long ntarget,
                               const double* __restrict__ geo) {
   for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < ntarget;
@@ -468,21 +468,25 @@ __global__ void amr_wx_kernel(const GLv* __restrict__ Lv, const int* __restrict_
     }
     const long long e0 = moff[flat], e1 = moff[flat + 1];
     long long e = e0;
-    for (; e + 1 < e1; e += 2) {  // two entries' loads in flight, applied in order
-      const long long enc0 = ment[e], enc1 = ment[e + 1];
-      const double* g0 = geo + (long long)mgeo[e] * kTab;
-      const double* g1 = geo + (long long)mgeo[e + 1] * kTab;
-      const double* p0 = Lv[enc0 >> 40].mom + (enc0 & ((1LL << 40) - 1)) * 10;
-      const double* p1 = Lv[enc1 >> 40].mom + (enc1 & ((1LL << 40) - 1)) * 10;
-      double m0[10], m1[10], G0[kTab], G1[kTab];
+    for (; e + 3 < e1; e += 4) {  // four entries' loads in flight, applied in order
+      long long enc[4];
+      int gi[4];
 #pragma unroll
-      for (int q = 0; q < 10; ++q) m0[q] = __ldg(p0 + q), m1[q] = __ldg(p1 + q);
+      for (int u = 0; u < 4; ++u) enc[u] = __ldg(ment + e + u), gi[u] = __ldg(mgeo + e + u);
+      double m[4][10], G[4][kTab];
 #pragma unroll
-      for (int q = 0; q < kTab; ++q) G0[q] = __ldg(g0 + q), G1[q] = __ldg(g1 + q);
-      m2l_tab(m0, G0, acc);
-      m2l_tab(m1, G1, acc);
+      for (int u = 0; u < 4; ++u) {
+        const double* pm = Lv[enc[u] >> 40].mom + (enc[u] & ((1LL << 40) - 1)) * 10;
+        const double* pg = geo + (long long)gi[u] * kTab;
+#pragma unroll
+        for (int q = 0; q < 10; ++q) m[u][q] = __ldg(pm + q);
+#pragma unroll
+        for (int q = 0; q < kTab; ++q) G[u][q] = __ldg(pg + q);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) m2l_tab(m[u], G[u], acc);
     }
-    if (e < e1) {
+    for (; e < e1; ++e) {
       const long long enc = ment[e];
       const double* mom = Lv[enc >> 40].mom + (enc & ((1LL << 40) - 1)) * 10;
       m2l_tab(mom, geo + (long long)mgeo[e] * kTab, acc);
