@@ -36,10 +36,12 @@ ALG_FLOP_PER_CELL = 633.25     # hydro stage FP64 ops per cell
 ALG_BYTES_PER_CELL = 180.0     # stage kernel, device-resident: 1280 staged cells x 40 B per
                                # 512 cells (100 B) + interior write 40 B + u0 read/write 40 B
 # Gravity, FP64 flops per interaction, FMA = 2: the order-2
-# Cartesian M2L is 28 multiply-adds once the geometry is known; W/X pairs
-# also build their geometry (46 ops); same-depth P2P is 4 multiply-adds with
-# tabulated geometry; cross-depth U pairs build theirs (15 ops).
-FLOP_M2L_V, FLOP_M2L_WX, FLOP_P2P, FLOP_P2P_U = 56, 102, 8, 23
+# Cartesian M2L is 28 multiply-adds once the geometry is known (into a leaf
+# patch only L0 and L_i are needed: 22); W/X pairs also build their geometry
+# (46 ops); same-depth P2P is 4 multiply-adds with tabulated geometry;
+# cross-depth U pairs build theirs (15 ops).
+FLOP_M2L_V, FLOP_M2L_V_LEAF, FLOP_M2L_WX, FLOP_P2P, FLOP_P2P_U = 56, 44, 102, 8, 23
+FLOP_M2L_WX_LEAF = FLOP_M2L_WX - (FLOP_M2L_V - FLOP_M2L_V_LEAF)
 
 
 def parse():
@@ -382,7 +384,10 @@ def run_ours(args, rank, world):
     share = {"hydro_stage": 3 * stage_ms / ms, "hydro_exchange": 3 * exch_ms / ms,
              "hydro_cfl": cfl_ms / ms}
     if gravity:
-        m2l_flop = work["v_pairs"] * FLOP_M2L_V + work["wx_entries"] * FLOP_M2L_WX
+        m2l_flop = ((work["v_pairs"] - work["v_pairs_leaf"]) * FLOP_M2L_V +
+                    work["v_pairs_leaf"] * FLOP_M2L_V_LEAF +
+                    (work["wx_entries"] - work["wx_entries_leaf"]) * FLOP_M2L_WX +
+                    work["wx_entries_leaf"] * FLOP_M2L_WX_LEAF)
         m2l_tf = m2l_flop / (grav_ms["m2l"] * 1e-3) / 1e12
         m2l_prof = profile_traffic("m2l_kernel_latest.json")
         roofline = {"bound": "fp64", "achieved": m2l_tf, "peak": peak_tf, "unit": "TFLOP/s",
@@ -390,8 +395,10 @@ def run_ours(args, rank, world):
                     "traffic": m2l_prof.get("dram_bytes_per_launch"),
                     "kernel": "amr_m2l (gravity M2L: V-list stencil + W/X lists), all levels",
                     "launch_ms": grav_ms["m2l"], "alg_flop_per_launch": m2l_flop,
-                    "alg_flop": f"{FLOP_M2L_V}/V pair x {work['v_pairs']} + {FLOP_M2L_WX}/W-X "
-                                f"entry x {work['wx_entries']} (FMA = 2)",
+                    "alg_flop": f"{FLOP_M2L_V}/V pair into internal patches, {FLOP_M2L_V_LEAF} into leaf "
+                                f"patches ({work['v_pairs']} pairs, {work['v_pairs_leaf']} into leaves) + "
+                                f"{FLOP_M2L_WX}/{FLOP_M2L_WX_LEAF} per W-X entry ({work['wx_entries']}) "
+                                "(FMA = 2)",
                     "peak_source": "tmgpu_fp64_peak DFMA microbenchmark (live; MEASURED_PEAKS.json "
                                    "has no FP64 entry)",
                     "hydro_stage": stage_roof}

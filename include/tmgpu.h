@@ -244,7 +244,8 @@ int tmgpu_gravity_amr_solve(tmgpu_gravity_amr* G, const double* mass, double* ph
                             int flags, void* stream, tmgpu_error* err);
 int tmgpu_gravity_amr_am_stats(tmgpu_gravity_amr* G, double* out);
 /* algorithmic work of one solve (bench roofline): [V pairs, W/X entries,
- * same-depth P2P pairs, cross-depth U entries, V pairs evaluated] */
+ * same-depth P2P pairs, cross-depth U entries, V pairs evaluated, V pairs into
+ * leaf patches, W/X entries into leaf patches] (leaf targets need only L0, L_i) */
 int tmgpu_gravity_amr_work(const tmgpu_gravity_amr* G, long long* out);
 /* multi-GPU: this rank (comm) owns canonical slots [slot_bounds[r], slot_bounds[r+1]);
  * masses and outputs become by local slot; results equal the one-GPU solve bitwise */

@@ -180,9 +180,6 @@ __global__ void amr_m2m_kernel(const GLv* __restrict__ L, int l, const int* __re
 // Accumulation per target: two partial sums (lower / upper source planes),
 // dz, dy, dx ascending, added; the W/X pairs follow in amr_wx_kernel —
 // tmo_grav_amr_solve's order, so the result is bitwise the oracle's.
-#ifndef TMGPU_M2L_SOURCE_MAJOR
-#define TMGPU_M2L_SOURCE_MAJOR 0
-#endif
 constexpr int kM2lThreads = 256;
 constexpr int kWPY = 13, kWPZ = 84, kWSub = 6 * kWPZ, kWVar = 4 * kWSub + 2;  // per var (+2: banks)
 constexpr int kWinDoubles = 10 * kWVar;                                   // 20,180
@@ -190,78 +187,13 @@ constexpr int kTabP = 14;  // shared-memory table entry: 13 doubles + pad (16-by
 constexpr int kTabDoubles = kOff3 * kTabP;                                // 4,802
 constexpr size_t kM2lSmem = (size_t)(kWinDoubles + kTabDoubles) * sizeof(double);  // 199,856 B
 
-// One source row: each source's moments are loaded once and applied to every
-// target k it interacts with (jj = sx - 2k in [0, 5]). The operations are
-// m2l_acc's, issued moment-major (all uses of -M, then Dx, Dy, Dz, then Q, each
-// across the targets) so consecutive DFMAs share their first operand (operand
-// reuse cache: two register reads per DFMA instead of three); every output's
-// own chain keeps m2l_acc's order, so the result is the same bit for bit.
-template <bool NEAR>
-__device__ __forceinline__ void m2l_row(const double* __restrict__ src, const double (&G)[6][kTab],
-                                        double (&acc)[4][10]) {
-#pragma unroll
-  for (int sx = 0; sx < 12; ++sx) {
-    double m[10];
-#pragma unroll
-    for (int q = 0; q < 10; ++q) m[q] = src[q * kWVar + sx];
-    bool v[4];
-    int jj[4];
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      jj[k] = sx - 2 * k;
-      v[k] = jj[k] >= 0 && jj[k] <= 5 && !(NEAR && (jj[k] == 2 || jj[k] == 3));
-      if (!v[k]) jj[k] = 0;
-    }
-    const double nM = -m[0];
-    double t[4];
-#pragma unroll
-    for (int k = 0; k < 4; ++k)
-      if (v[k]) t[k] = nM * G[jj[k]][0];
-#pragma unroll
-    for (int k = 0; k < 4; ++k)
-      if (v[k]) {
-#pragma unroll
-        for (int i = 0; i < 3; ++i) acc[k][1 + i] = fma(nM, G[jj[k]][1 + i], acc[k][1 + i]);
-#pragma unroll
-        for (int q = 0; q < 6; ++q) acc[k][4 + q] = fma(nM, G[jj[k]][4 + q], acc[k][4 + q]);
-      }
-    // dipole: D_x pairs with (e1 | e4 e5 e6), D_y (e2 | e5 e7 e8), D_z (e3 | e6 e8 e9)
-#pragma unroll
-    for (int d = 0; d < 3; ++d) {
-      const double D = m[1 + d];
-      const int r0 = d == 0 ? 4 : (d == 1 ? 5 : 6), r1 = d == 0 ? 5 : (d == 1 ? 7 : 8),
-                r2 = d == 0 ? 6 : (d == 1 ? 8 : 9);
-#pragma unroll
-      for (int k = 0; k < 4; ++k)
-        if (v[k]) {
-          t[k] = fma(D, G[jj[k]][1 + d], t[k]);
-          acc[k][1] = fma(D, G[jj[k]][r0], acc[k][1]);
-          acc[k][2] = fma(D, G[jj[k]][r1], acc[k][2]);
-          acc[k][3] = fma(D, G[jj[k]][r2], acc[k][3]);
-        }
-    }
-    // quadrupole into L0: Qxx (e10) Qxy (e5) Qxz (e6) Qyy (e11) Qyz (e8) Qzz (e12)
-#pragma unroll
-    for (int q = 0; q < 6; ++q) {
-      const double nQ = -m[4 + q];
-      const int e = q == 0 ? 10 : (q == 1 ? 5 : (q == 2 ? 6 : (q == 3 ? 11 : (q == 4 ? 8 : 12))));
-#pragma unroll
-      for (int k = 0; k < 4; ++k)
-        if (v[k]) t[k] = fma(nQ, G[jj[k]][e], t[k]);
-    }
-#pragma unroll
-    for (int k = 0; k < 4; ++k)
-      if (v[k]) acc[k][0] = acc[k][0] + t[k];
-  }
-}
-
 // Offset-major rows: per x-offset jj the geometry (13 registers) is loaded
 // once and applied to the four targets' sources sx = jj + 2k. The contraction
 // is m2l_acc's, operation for operation per target, issued target-interleaved:
 // four consecutive DFMAs share the geometry operand (operand reuse cache: two
 // fresh register reads per DFMA instead of three) and form four independent
 // chains. Each target still sees its sources in dx order.
-template <bool NEAR>
+template <bool NEAR, int NOUT>
 __device__ __forceinline__ void m2l_row_jj(const double* __restrict__ src,
                                            const double* __restrict__ trow, double (&acc)[4][10]) {
 #pragma unroll
@@ -320,9 +252,10 @@ __device__ __forceinline__ void m2l_row_jj(const double* __restrict__ src,
 #pragma unroll
       for (int k = 0; k < 4; ++k) acc[k][1 + i] = fma(m[k][3], e[r2], acc[k][1 + i]);
     }
-    // L_ij: -M D2_ij
+    // L_ij: -M D2_ij (leaf patches: L2P reads only L0 and L_i, so NOUT = 4
+    // drops these; the other components are unaffected)
 #pragma unroll
-    for (int q = 0; q < 6; ++q)
+    for (int q = 0; q < NOUT - 4; ++q)
 #pragma unroll
       for (int k = 0; k < 4; ++k) acc[k][4 + q] = fma(-m[k][0], e[4 + q], acc[k][4 + q]);
   }
@@ -335,8 +268,70 @@ __device__ __forceinline__ void cp_async8(double* smem, const double* gmem, bool
                : "memory");
 }
 
+// V-list sums of one patch from the staged window: NOUT = 10 (internal
+// patch, all locals into loc[node]) or 4 (leaf patch: L0, L_i into the
+// compact leaf locals [4][512]).
+template <int NOUT>
+__device__ __forceinline__ void m2l_patch(double* __restrict__ win, const double* __restrict__ tabs,
+                                          double* __restrict__ loc, int n, double* __restrict__ lloc) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int b = warp & 1, c = (warp >> 1) & 1, half = warp >> 2;
+  const int a = lane & 1, Y = (lane >> 1) & 3, Z = lane >> 3;
+  double acc[4][10];
+#pragma unroll
+  for (int k = 0; k < 4; ++k)
+#pragma unroll
+    for (int q = 0; q < 10; ++q) acc[k][q] = 0.0;
+  // table row base of this lane's x parity: entry (dx + 3) = jj + 1 - a
+  const double* tab_lane = tabs + (1 - a) * kTabP;
+  // this warp's half of the source planes: iz = dz + 2 + c in [3 half, 3 half + 2]
+  for (int iz = 3 * half; iz < 3 * half + 3; ++iz) {
+    const int dz = iz - 2 - c;
+    for (int iy = 0; iy < 6; ++iy) {
+      const int dy = iy - 2 - b;
+      const double* trow = tab_lane + ((dz + 3) * kOff + (dy + 3)) * kOff * kTabP;
+      // source row: window y = 2Y + iy, z = 2Z + iz (parent-aligned, parity-free)
+      const double* src = win + ((iz & 1) * 2 + (iy & 1)) * kWSub + (Z + (iz >> 1)) * kWPZ +
+                          (Y + (iy >> 1)) * kWPY;
+      if (dz >= -1 && dz <= 1 && dy >= -1 && dy <= 1)
+        m2l_row_jj<true, NOUT>(src, trow, acc);
+      else
+        m2l_row_jj<false, NOUT>(src, trow, acc);
+    }
+  }
+  // upper-half warps hand their partial sums to the lower-half warps (the
+  // window is dead after the barrier): V = lower + upper, as the oracle adds
+  __syncthreads();
+  const int pair = threadIdx.x & 127;
+  if (half) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+#pragma unroll
+      for (int q = 0; q < NOUT; ++q) win[(k * 10 + q) * 128 + pair] = acc[k][q];
+  }
+  __syncthreads();
+  if (half) return;
+  const int y = 2 * Y + b, z = 2 * Z + c;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int cell = (z * 8 + y) * 8 + a + 2 * k;
+    double v[NOUT];
+#pragma unroll
+    for (int q = 0; q < NOUT; ++q) v[q] = acc[k][q] + win[(k * 10 + q) * 128 + pair];
+    if constexpr (NOUT == 10) {
+      double2* out = reinterpret_cast<double2*>(loc + ((long long)n * 512 + cell) * 10);
+#pragma unroll
+      for (int h = 0; h < 5; ++h) out[h] = make_double2(v[2 * h], v[2 * h + 1]);
+    } else {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) lloc[q * 512 + cell] = v[q];
+    }
+  }
+}
+
 __global__ void __launch_bounds__(kM2lThreads, 1) amr_m2l_fused_kernel(
-    const GLv* __restrict__ Lv, const int2* __restrict__ work, const double* __restrict__ tab_all) {
+    const GLv* __restrict__ Lv, const int2* __restrict__ work, const double* __restrict__ tab_all,
+    double* __restrict__ lloc, long long lo) {
   extern __shared__ double sm[];
   double* win = sm;
   double* tabs = sm + kWinDoubles;
@@ -376,124 +371,85 @@ __global__ void __launch_bounds__(kM2lThreads, 1) amr_m2l_fused_kernel(
   }
   asm volatile("cp.async.wait_all;\n" ::: "memory");
   __syncthreads();
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int b = warp & 1, c = (warp >> 1) & 1, half = warp >> 2;
-  const int a = lane & 1, Y = (lane >> 1) & 3, Z = lane >> 3;
-  double acc[4][10];
+  const int leaf = L.leaf_slot[n];
+  if (leaf >= 0)  // leaf patch: L0, L_i into the compact leaf locals (L2P's input)
+    m2l_patch<4>(win, tabs, L.loc, n, lloc + (long long)(leaf - lo) * 2048);
+  else
+    m2l_patch<10>(win, tabs, L.loc, n, nullptr);
+}
+
+// W/X pairs (AMR level jumps) after the V-list sums, in the list's sorted
+// order, one thread per target with entries (targets in patch order);
+// geometry from the plan's separation table (m2l_geom of each distinct R).
+template <int NOUT>
+__device__ __forceinline__ void wx_entries(const GLv* __restrict__ Lv, const long long* __restrict__ ment,
+                                           const int* __restrict__ mgeo, long long e0, long long e1,
+                                           const double* __restrict__ geo, double* acc) {
+  long long e = e0;
+  for (; e + 3 < e1; e += 4) {  // four entries' loads in flight, applied in order
+    long long enc[4];
+    int gi[4];
 #pragma unroll
-  for (int k = 0; k < 4; ++k)
+    for (int u = 0; u < 4; ++u) enc[u] = __ldg(ment + e + u), gi[u] = __ldg(mgeo + e + u);
+    double m[4][10], G[4][kTab];
 #pragma unroll
-    for (int q = 0; q < 10; ++q) acc[k][q] = 0.0;
-  // table row base of this lane's x parity: entry (dx + 3) = jj + 1 - a
-  const double* tab_lane = tabs + (1 - a) * kTabP;
-  // this warp's half of the source planes: iz = dz + 2 + c in [3 half, 3 half + 2]
-  for (int iz = 3 * half; iz < 3 * half + 3; ++iz) {
-    const int dz = iz - 2 - c;
-    for (int iy = 0; iy < 6; ++iy) {
-      const int dy = iy - 2 - b;
-      const double* trow = tab_lane + ((dz + 3) * kOff + (dy + 3)) * kOff * kTabP;
-      // source row: window y = 2Y + iy, z = 2Z + iz (parent-aligned, parity-free)
-      const double* src = win + ((iz & 1) * 2 + (iy & 1)) * kWSub + (Z + (iz >> 1)) * kWPZ +
-                          (Y + (iy >> 1)) * kWPY;
-#if TMGPU_M2L_SOURCE_MAJOR
-      double G[6][kTab];
+    for (int u = 0; u < 4; ++u) {
+      const double* pm = Lv[enc[u] >> 40].mom + (enc[u] & ((1LL << 40) - 1)) * 10;
+      const double* pg = geo + (long long)gi[u] * kTab;
 #pragma unroll
-      for (int jj = 0; jj < 6; ++jj) {
-        const double2* t2 = reinterpret_cast<const double2*>(trow + jj * kTabP);
+      for (int q = 0; q < 10; ++q) m[u][q] = __ldg(pm + q);
 #pragma unroll
-        for (int q = 0; q < 6; ++q) {
-          const double2 v = t2[q];
-          G[jj][2 * q] = v.x;
-          G[jj][2 * q + 1] = v.y;
-        }
-        G[jj][12] = trow[jj * kTabP + 12];
-      }
-      if (dz >= -1 && dz <= 1 && dy >= -1 && dy <= 1)
-        m2l_row<true>(src, G, acc);
-      else
-        m2l_row<false>(src, G, acc);
-#else
-      if (dz >= -1 && dz <= 1 && dy >= -1 && dy <= 1)
-        m2l_row_jj<true>(src, trow, acc);
-      else
-        m2l_row_jj<false>(src, trow, acc);
-#endif
+      for (int q = 0; q < kTab; ++q) G[u][q] = __ldg(pg + q);
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      if constexpr (NOUT == 10) m2l_tab(m[u], G[u], acc);
+      else m2l_tab4(m[u], G[u], acc);
     }
   }
-  // upper-half warps hand their partial sums to the lower-half warps (the
-  // window is dead after the barrier): V = lower + upper, as the oracle adds
-  __syncthreads();
-  const int pair = threadIdx.x & 127;
-  if (half) {
-#pragma unroll
-    for (int k = 0; k < 4; ++k)
-#pragma unroll
-      for (int q = 0; q < 10; ++q) win[(k * 10 + q) * 128 + pair] = acc[k][q];
-  }
-  __syncthreads();
-  if (half) return;
-  const int y = 2 * Y + b, z = 2 * Z + c;
-#pragma unroll
-  for (int k = 0; k < 4; ++k) {
-    const long long flat = (long long)n * 512 + (z * 8 + y) * 8 + a + 2 * k;
-    double v[10];
-#pragma unroll
-    for (int q = 0; q < 10; ++q) v[q] = acc[k][q] + win[(k * 10 + q) * 128 + pair];
-    double2* out = reinterpret_cast<double2*>(L.loc + flat * 10);
-#pragma unroll
-    for (int h = 0; h < 5; ++h) out[h] = make_double2(v[2 * h], v[2 * h + 1]);
+  for (; e < e1; ++e) {
+    const long long enc = ment[e];
+    const double* mom = Lv[enc >> 40].mom + (enc & ((1LL << 40) - 1)) * 10;
+    if constexpr (NOUT == 10) m2l_tab(mom, geo + (long long)mgeo[e] * kTab, acc);
+    else m2l_tab4(mom, geo + (long long)mgeo[e] * kTab, acc);
   }
 }
 
 // W/X pairs (AMR level jumps) after the V-list sums, in the list's sorted
 // order, one thread per target with entries (targets in patch order);
 // geometry from the plan's separation table (m2l_geom of each distinct R).
+// Leaf-patch targets update their compact L0, L_i only.
 __global__ void __launch_bounds__(128, 4) amr_wx_kernel(const GLv* __restrict__ Lv, const int* __restrict__ tlev,
-                              const long long* __restrict__ tflat, long long ntarget,
-                              const double* __restrict__ geo) {
+                                                        const long long* __restrict__ tflat, long long ntarget,
+                                                        const double* __restrict__ geo,
+                                                        double* __restrict__ lloc, long long lo) {
   for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < ntarget;
        t += (long long)gridDim.x * blockDim.x) {
     const int l = tlev[t];
     const long long flat = tflat[t];
-    double* loc = Lv[l].loc + flat * 10;
     const long long* moff = Lv[l].moff;
-    const long long* ment = Lv[l].ment;
-    const int* mgeo = Lv[l].mgeo;
-    double acc[10];
-#pragma unroll
-    for (int h = 0; h < 5; ++h) {
-      const double2 v = reinterpret_cast<const double2*>(loc)[h];
-      acc[2 * h] = v.x;
-      acc[2 * h + 1] = v.y;
-    }
     const long long e0 = moff[flat], e1 = moff[flat + 1];
-    long long e = e0;
-    for (; e + 3 < e1; e += 4) {  // four entries' loads in flight, applied in order
-      long long enc[4];
-      int gi[4];
+    const int leaf = Lv[l].leaf_slot[flat >> 9];
+    if (leaf >= 0) {
+      double* p = lloc + (long long)(leaf - lo) * 2048 + (flat & 511);
+      double acc[4] = {p[0], p[512], p[1024], p[1536]};
+      wx_entries<4>(Lv, Lv[l].ment, Lv[l].mgeo, e0, e1, geo, acc);
 #pragma unroll
-      for (int u = 0; u < 4; ++u) enc[u] = __ldg(ment + e + u), gi[u] = __ldg(mgeo + e + u);
-      double m[4][10], G[4][kTab];
+      for (int q = 0; q < 4; ++q) p[q * 512] = acc[q];
+    } else {
+      double* loc = Lv[l].loc + flat * 10;
+      double acc[10];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const double* pm = Lv[enc[u] >> 40].mom + (enc[u] & ((1LL << 40) - 1)) * 10;
-        const double* pg = geo + (long long)gi[u] * kTab;
-#pragma unroll
-        for (int q = 0; q < 10; ++q) m[u][q] = __ldg(pm + q);
-#pragma unroll
-        for (int q = 0; q < kTab; ++q) G[u][q] = __ldg(pg + q);
+      for (int h = 0; h < 5; ++h) {
+        const double2 v = reinterpret_cast<const double2*>(loc)[h];
+        acc[2 * h] = v.x;
+        acc[2 * h + 1] = v.y;
       }
+      wx_entries<10>(Lv, Lv[l].ment, Lv[l].mgeo, e0, e1, geo, acc);
 #pragma unroll
-      for (int u = 0; u < 4; ++u) m2l_tab(m[u], G[u], acc);
+      for (int h = 0; h < 5; ++h)
+        reinterpret_cast<double2*>(loc)[h] = make_double2(acc[2 * h], acc[2 * h + 1]);
     }
-    for (; e < e1; ++e) {
-      const long long enc = ment[e];
-      const double* mom = Lv[enc >> 40].mom + (enc & ((1LL << 40) - 1)) * 10;
-      m2l_tab(mom, geo + (long long)mgeo[e] * kTab, acc);
-    }
-#pragma unroll
-    for (int h = 0; h < 5; ++h)
-      reinterpret_cast<double2*>(loc)[h] = make_double2(acc[2 * h], acc[2 * h + 1]);
   }
 }
 
@@ -589,6 +545,7 @@ __global__ void __launch_bounds__(512) amr_l2p_kernel(const GLv* __restrict__ Lv
                                                       const int* __restrict__ slot_node,
                                                       const double* __restrict__ mass,
                                                       const double* __restrict__ ugeo,
+                                                      const double* __restrict__ lloc,
                                                       double* __restrict__ phi, double* __restrict__ g,
                                                       double* __restrict__ part) {
   __shared__ double w26[27][4];
@@ -611,9 +568,8 @@ __global__ void __launch_bounds__(512) amr_l2p_kernel(const GLv* __restrict__ Lv
   const int c = threadIdx.x;
   const int i = c & 7, j = (c >> 3) & 7, k = c >> 6;
   const long long flat = (long long)n * 512 + c;
-  const double2* Lc = reinterpret_cast<const double2*>(L.loc + flat * 10);
-  const double2 l01 = Lc[0], l23 = Lc[1];
-  double loc4[4] = {l01.x, l01.y, l23.x, l23.y};
+  const double* Lc = lloc + ls * 2048 + c;  // compact leaf locals (V + W/X sums)
+  double loc4[4] = {Lc[0], Lc[512], Lc[1024], Lc[1536]};
   if (l > 0) {
     double sv[3], sh[4];
     l2l_shift<4>(l2l_parent(L, Lv[l - 1], n, c, h, sv), sv, sh);
@@ -807,7 +763,7 @@ cudaError_t upload(const std::vector<T>& v, T** out) {
 // need: per-level node lists this GPU evaluates M2L for (nullptr = all);
 // [lo, hi): the canonical slots it evaluates L2P/P2P for.
 void count_work(const GravPlan& P, const std::vector<std::vector<int>>* need, long long lo,
-                long long hi, long long out[5]) {
+                long long hi, long long out[7]) {
   long long vtab[27] = {0}, ptab[27] = {0};
   for (int c = 0; c < 512; ++c) {
     const int i = c & 7, j = (c >> 3) & 7, k = c >> 6;
@@ -821,14 +777,18 @@ void count_work(const GravPlan& P, const std::vector<std::vector<int>>* need, lo
           else if (dx || dy || dz) ++ptab[o];
         }
   }
-  long long v = 0, vk = 0, p = 0, wx = 0, u = 0;
+  long long v = 0, vk = 0, p = 0, wx = 0, u = 0, vleaf = 0, wxleaf = 0;
   for (int l = 0; l < P.nlevels; ++l) {
     const GravLevel& L = P.lv[l];
     auto node = [&](int n) {
       vk += 512 * 189;  // the kernel's 189 offsets x 512 targets
+      long long vn = 0;
       for (int o = 0; o < 27; ++o)
-        if (L.nbr[(size_t)n * 27 + o] >= 0) v += vtab[o];
-      wx += L.moff[(size_t)(n + 1) * 512] - L.moff[(size_t)n * 512];
+        if (L.nbr[(size_t)n * 27 + o] >= 0) vn += vtab[o];
+      const long long wn = L.moff[(size_t)(n + 1) * 512] - L.moff[(size_t)n * 512];
+      v += vn;
+      wx += wn;
+      if (L.leaf_slot[n] >= 0) vleaf += vn, wxleaf += wn;  // L0, L_i only
     };
     if (need)
       for (int n : (*need)[l]) node(n);
@@ -859,6 +819,8 @@ void count_work(const GravPlan& P, const std::vector<std::vector<int>>* need, lo
   out[2] = p;
   out[3] = u;
   out[4] = vk;
+  out[5] = vleaf;
+  out[6] = wxleaf;
 }
 
 // per-phase device timing of solves (bench): events at the phase boundaries
@@ -869,7 +831,7 @@ struct GravTimingRec {
 
 struct GravAmrWork {
   GravPlan plan;
-  long long work[5] = {0, 0, 0, 0, 0};
+  long long work[7] = {0, 0, 0, 0, 0, 0, 0};
   bool timing = false;
   std::vector<GravTimingRec> pending;
   double phase_ms[kGravPhases] = {0, 0, 0, 0, 0, 0};
@@ -884,6 +846,7 @@ struct GravAmrWork {
   double* dloc[3] = {nullptr, nullptr, nullptr};
   double* tab = nullptr;
   double* mass = nullptr;
+  double* lloc = nullptr;   // [slot - lo][4][512] leaf locals L0, L_i (leaf patches only)
   double* part = nullptr;   // [P][16] + rw[22]
   double* part2 = nullptr;  // [P/256 + 1][16] tree scratch
   long long nslots = 0, P = 1;
@@ -1166,6 +1129,7 @@ tmgpu_gravity_amr* tmgpu_gravity_amr_create(const int* leaves, long long nleaves
   const int Dmax = P.nlevels - 1 + 3;
   if (e == cudaSuccess) e = cudaMalloc(&w.tab, (size_t)(Dmax + 1) * kOff3 * kTab * sizeof(double)), track(w.tab);
   if (e == cudaSuccess) e = cudaMalloc(&w.mass, (size_t)w.nslots * 512 * sizeof(double)), track(w.mass);
+  if (e == cudaSuccess) e = cudaMalloc(&w.lloc, (size_t)w.nslots * 2048 * sizeof(double)), track(w.lloc);
   if (e == cudaSuccess) e = cudaMalloc(&w.part, ((size_t)w.P * 16 + 22) * sizeof(double)), track(w.part);
   if (e == cudaSuccess) e = cudaMalloc(&w.part2, ((size_t)w.P / 256 + 1) * 16 * sizeof(double)), track(w.part2);
   if (e == cudaSuccess)
@@ -1370,12 +1334,12 @@ int tmgpu_gravity_amr_solve(tmgpu_gravity_amr* G, const double* mass, double* ph
     {
       if (w.m2l_ctas) {
         amr_m2l_fused_kernel<<<(unsigned)w.m2l_ctas, kM2lThreads, kM2lSmem, st>>>(w.dev_lv, w.m2l_work,
-                                                                                 w.tab);
+                                                                                 w.tab, w.lloc, w.lo);
         ++launches;
       }
       if (w.wx_targets) {
         amr_wx_kernel<<<grid_for(w.wx_targets), 128, 0, st>>>(w.dev_lv, w.wx_tlev, w.wx_tflat,
-                                                              w.wx_targets, w.wx_geo);
+                                                              w.wx_targets, w.wx_geo, w.lloc, w.lo);
         ++launches;
       }
     }
@@ -1393,7 +1357,7 @@ int tmgpu_gravity_amr_solve(tmgpu_gravity_amr* G, const double* mass, double* ph
     if (am) e = cudaMemsetAsync(w.part, 0, (size_t)w.P * 16 * sizeof(double), st);
     if (nloc)
       amr_l2p_kernel<<<(unsigned)nloc, 512, 0, st>>>(w.dev_lv, nloc, w.lo, w.slot_level, w.slot_node,
-                                                     w.mass, w.u_geo, dphi, dg, am ? w.part : nullptr);
+                                                     w.mass, w.u_geo, w.lloc, dphi, dg, am ? w.part : nullptr);
     ++launches;
     if (timed) cudaEventRecord(rec.ev[5], st);
     if (am) {  // the per-slot sums came with L2P
@@ -1509,10 +1473,11 @@ int tmgpu_gravity_amr_am_stats(tmgpu_gravity_amr* G, double* out) {
 // its share): [0] V-list M2L pairs with an existing source (incl. the dense
 // depth-2 level), [1] W/X M2L entries, [2] same-depth P2P pairs, [3] cross-depth
 // U entries, [4] V-list pairs the kernel evaluates (missing neighbour patches as
-// zero moments).
+// zero moments), [5] of [0] into leaf patches, [6] of [1] into leaf patches
+// (those evaluate only L0 and L_i).
 int tmgpu_gravity_amr_work(const tmgpu_gravity_amr* G, long long* out) {
   if (!G || !out) return TMGPU_ERR_INVALID;
-  for (int q = 0; q < 5; ++q) out[q] = G->w.work[q];
+  for (int q = 0; q < 7; ++q) out[q] = G->w.work[q];
   return TMGPU_OK;
 }
 

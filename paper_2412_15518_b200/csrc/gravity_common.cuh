@@ -78,6 +78,27 @@ __device__ __forceinline__ void m2l_acc(double nM, double Dx, double Dy, double 
   for (int q = 0; q < 6; ++q) out[4 + q] = fma(nM, e[4 + q], out[4 + q]);
 }
 
+// m2l_acc without the L_ij terms (leaf targets: L2P reads only L0 and L_i;
+// the other components' operations are unchanged)
+__device__ __forceinline__ void m2l_tab4(const double* __restrict__ mom, const double* __restrict__ e,
+                                         double out[4]) {
+  const double nM = -mom[0], Dx = mom[1], Dy = mom[2], Dz = mom[3];
+  double o = nM * e[0];
+  o = fma(Dx, e[1], o);
+  o = fma(Dy, e[2], o);
+  o = fma(Dz, e[3], o);
+  o = fma(-mom[4], e[10], o);
+  o = fma(-mom[5], e[5], o);
+  o = fma(-mom[6], e[6], o);
+  o = fma(-mom[7], e[11], o);
+  o = fma(-mom[8], e[8], o);
+  o = fma(-mom[9], e[12], o);
+  out[0] = out[0] + o;
+  out[1] = fma(Dz, e[6], fma(Dy, e[5], fma(Dx, e[4], fma(nM, e[1], out[1]))));
+  out[2] = fma(Dz, e[8], fma(Dy, e[7], fma(Dx, e[5], fma(nM, e[2], out[2]))));
+  out[3] = fma(Dz, e[9], fma(Dy, e[8], fma(Dx, e[6], fma(nM, e[3], out[3]))));
+}
+
 __device__ __forceinline__ void m2l_tab(const double* __restrict__ mom, const double* __restrict__ e,
                                         double out[10]) {
   m2l_acc(-mom[0], mom[1], mom[2], mom[3], -mom[4], -mom[5], -mom[6], -mom[7], -mom[8], -mom[9], e,

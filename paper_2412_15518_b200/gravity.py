@@ -262,10 +262,11 @@ class GravityAMR:
 
     def work(self):
         """Algorithmic work of one solve: dict of interaction counts."""
-        out = (C.c_longlong * 5)()
+        out = (C.c_longlong * 7)()
         lib.tmgpu_gravity_amr_work(self.h, out)
         return {"v_pairs": out[0], "wx_entries": out[1], "p2p_pairs": out[2],
-                "u_cross_entries": out[3], "v_pairs_evaluated": out[4]}
+                "u_cross_entries": out[3], "v_pairs_evaluated": out[4], "v_pairs_leaf": out[5],
+                "wx_entries_leaf": out[6]}
 
     def set_timing(self, on: bool) -> None:
         lib.tmgpu_gravity_amr_set_timing(self.h, int(on))
