@@ -22,7 +22,8 @@
  *   M2M   internal cells from their 8 children, (c, b, a) loop order
  *   V     every existing cell at depth >= 2: the 189-cell stencil of the
  *         uniform spec (two partial sums over the lower / upper three source
- *         planes, dz, dy, dx ascending, then added), skipping missing/outside cells
+ *         planes, dz, dy ascending, per row even source x then odd, then
+ *         added), skipping missing/outside cells
  *   W, X  for every leaf cell b (canonical leaf order, cells (k,j,i)), every
  *         internal colleague Y (same depth, max|offset| = 1, dz,dy,dx
  *         ascending) is visited: each child y (z,y,x order) adjacent to b
@@ -350,7 +351,8 @@ int tmo_grav_amr_solve_ex(long nleaves, const int* leaves, const double* mass, i
           double part[2][10] = {{0}};  /* lower / upper three source planes */
           for (long dz = -2 - (k & 1); dz <= 3 - (k & 1); ++dz)
             for (long dy = -2 - (j & 1); dy <= 3 - (j & 1); ++dy)
-              for (long dx = -2 - (i & 1); dx <= 3 - (i & 1); ++dx) {
+              for (int pe = 0; pe < 2; ++pe)  /* even source x, then odd */
+              for (long dx = -2 - (i & 1) + pe; dx <= 3 - (i & 1); dx += 2) {
                 if (labs(dx) <= 1 && labs(dy) <= 1 && labs(dz) <= 1) continue;
                 const long si = i + dx, sj = j + dy, sk = k + dz;
                 if (si < 0 || sj < 0 || sk < 0 || si >= m || sj >= m || sk >= m) continue;

@@ -16,8 +16,9 @@
  *            children in (c, b, a) = (z, y, x) loop order, x fastest
  *   M2L      at every level l >= 2, target cell c sums over the cells c' whose
  *            parent is one of the 27 neighbours of parent(c) but with
- *            max|c - c'| >= 2 (the 189-cell interaction list), loops dz, dy, dx
- *            ascending, as two partial sums — sources in the lower three planes
+ *            max|c - c'| >= 2 (the 189-cell interaction list), loops dz, dy
+ *            ascending and in each row the sources with even x first, then odd
+ *            (dx ascending within each), as two partial sums — sources in the lower three planes
  *            (z' < 2 (z >> 1) + 1) and in the upper three — added at the end
  *            (the GPU gives each half its own thread); R = x_c - x_c';
  *            order-2 Cartesian multipoles -> local
@@ -185,7 +186,8 @@ int tmo_grav_solve(int D, const double* mass, double* phi, double* g) {
           double part[2][10] = {{0}};
           for (long dz = -2 - (k & 1); dz <= 3 - (k & 1); ++dz)
             for (long dy = -2 - (j & 1); dy <= 3 - (j & 1); ++dy)
-              for (long dx = -2 - (i & 1); dx <= 3 - (i & 1); ++dx) {
+              for (int pe = 0; pe < 2; ++pe)  /* even source x, then odd */
+              for (long dx = -2 - (i & 1) + pe; dx <= 3 - (i & 1); dx += 2) {
                 if (labs(dx) <= 1 && labs(dy) <= 1 && labs(dz) <= 1) continue;
                 const long si = i + dx, sj = j + dy, sk = k + dz;
                 if (si < 0 || sj < 0 || sk < 0 || si >= m || sj >= m || sk >= m) continue;

@@ -80,7 +80,8 @@ __global__ void __launch_bounds__(128) m2l_tiled_kernel(const double* __restrict
   for (int q = 0; q < 10; ++q) o[0][q] = o[1][q] = 0.0;
   for (long long dz = -2 - (k & 1); dz <= 3 - (k & 1); ++dz)
     for (long long dy = -2 - (j & 1); dy <= 3 - (j & 1); ++dy)
-      for (long long dx = -2 - (i & 1); dx <= 3 - (i & 1); ++dx) {
+      for (int pe = 0; pe < 2; ++pe)  /* even source x, then odd */
+              for (long long dx = -2 - (i & 1) + pe; dx <= 3 - (i & 1); dx += 2) {
         if (dx >= -1 && dx <= 1 && dy >= -1 && dy <= 1 && dz >= -1 && dz <= 1) continue;
         const long long si = i + dx, sj = j + dy, sk = k + dz;
         if (si < 0 || sj < 0 || sk < 0 || si >= m || sj >= m || sk >= m) continue;

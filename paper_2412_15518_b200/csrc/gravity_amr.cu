@@ -187,77 +187,69 @@ constexpr int kTabP = 14;  // shared-memory table entry: 13 doubles + pad (16-by
 constexpr int kTabDoubles = kOff3 * kTabP;                                // 4,802
 constexpr size_t kM2lSmem = (size_t)(kWinDoubles + kTabDoubles) * sizeof(double);  // 199,856 B
 
-// Offset-major rows: per x-offset jj the geometry (13 registers) is loaded
-// once and applied to the four targets' sources sx = jj + 2k. The contraction
-// is m2l_acc's, operation for operation per target, issued target-interleaved:
-// four consecutive DFMAs share the geometry operand (operand reuse cache: two
-// fresh register reads per DFMA instead of three) and form four independent
-// chains. Each target still sees its sources in dx order.
+// One V-list term (m2l_acc's operations) with raw window moments; NOUT = 4
+// drops the L_ij terms (leaf targets: the other components are unaffected).
+template <int NOUT>
+__device__ __forceinline__ void m2l_term(const double (&m)[10], const double (&e)[kTab], double (&o)[10]) {
+  const double nM = -m[0];
+  double t = nM * e[0];
+  t = fma(m[1], e[1], t);
+  t = fma(m[2], e[2], t);
+  t = fma(m[3], e[3], t);
+  t = fma(-m[4], e[10], t);
+  t = fma(-m[5], e[5], t);
+  t = fma(-m[6], e[6], t);
+  t = fma(-m[7], e[11], t);
+  t = fma(-m[8], e[8], t);
+  t = fma(-m[9], e[12], t);
+  o[0] = o[0] + t;
+  o[1] = fma(m[3], e[6], fma(m[2], e[5], fma(m[1], e[4], fma(nM, e[1], o[1]))));
+  o[2] = fma(m[3], e[8], fma(m[2], e[7], fma(m[1], e[5], fma(nM, e[2], o[2]))));
+  o[3] = fma(m[3], e[9], fma(m[2], e[8], fma(m[1], e[6], fma(nM, e[3], o[3]))));
+#pragma unroll
+  for (int q = 0; q < NOUT - 4; ++q) o[4 + q] = fma(nM, e[4 + q], o[4 + q]);
+}
+
+// One source row, in the specification's order per target: the sources with
+// even window x first, then odd (dx ascending within each). Per parity pass
+// the three x-offsets' geometry (39 registers) is loaded once and the row's six
+// sources of that parity are streamed once, each applied to every target it
+// reaches (jj = sx - 2k in {pe, pe+2, pe+4}): ~6 shared loads per interaction.
+// Near rows skip jj = 2, 3 (near for both x parities); jj = 1 (a = 0) and
+// jj = 4 (a = 1) use zeroed near geometry (exact no-ops, see above).
 template <bool NEAR, int NOUT>
-__device__ __forceinline__ void m2l_row_jj(const double* __restrict__ src,
-                                           const double* __restrict__ trow, double (&acc)[4][10]) {
+__device__ __forceinline__ void m2l_row_par(const double* __restrict__ src,
+                                            const double* __restrict__ trow, double (&acc)[4][10]) {
 #pragma unroll
-  for (int jj = 0; jj < 6; ++jj) {
-    if (NEAR && (jj == 2 || jj == 3)) continue;
-    double e[kTab];
-    const double2* t2 = reinterpret_cast<const double2*>(trow + jj * kTabP);
+  for (int pe = 0; pe < 2; ++pe) {
+    double G[3][kTab];
 #pragma unroll
-    for (int q = 0; q < 6; ++q) {
-      const double2 v = t2[q];
-      e[2 * q] = v.x;
-      e[2 * q + 1] = v.y;
+    for (int t = 0; t < 3; ++t) {
+      if (NEAR && t == 1) continue;
+      const int jj = pe + 2 * t;
+      const double2* t2 = reinterpret_cast<const double2*>(trow + jj * kTabP);
+#pragma unroll
+      for (int q = 0; q < 6; ++q) {
+        const double2 v = t2[q];
+        G[t][2 * q] = v.x;
+        G[t][2 * q + 1] = v.y;
+      }
+      G[t][12] = trow[jj * kTabP + 12];
     }
-    e[12] = trow[jj * kTabP + 12];
-    double m[4][10];
 #pragma unroll
-    for (int k = 0; k < 4; ++k)
+    for (int mi = 0; mi < 6; ++mi) {
+      const int sx = pe + 2 * mi;
+      double m[10];
 #pragma unroll
-      for (int q = 0; q < 10; ++q) m[k][q] = src[q * kWVar + jj + 2 * k];
-    double t[4];
+      for (int q = 0; q < 10; ++q) m[q] = src[q * kWVar + sx];
 #pragma unroll
-    for (int k = 0; k < 4; ++k) t[k] = -m[k][0] * e[0];
-    // L0 increment: D (e1 e2 e3), then Q (xx e10, xy e5, xz e6, yy e11, yz e8, zz e12)
-#pragma unroll
-    for (int k = 0; k < 4; ++k) t[k] = fma(m[k][1], e[1], t[k]);
-#pragma unroll
-    for (int k = 0; k < 4; ++k) t[k] = fma(m[k][2], e[2], t[k]);
-#pragma unroll
-    for (int k = 0; k < 4; ++k) t[k] = fma(m[k][3], e[3], t[k]);
-#pragma unroll
-    for (int k = 0; k < 4; ++k) t[k] = fma(-m[k][4], e[10], t[k]);
-#pragma unroll
-    for (int k = 0; k < 4; ++k) t[k] = fma(-m[k][5], e[5], t[k]);
-#pragma unroll
-    for (int k = 0; k < 4; ++k) t[k] = fma(-m[k][6], e[6], t[k]);
-#pragma unroll
-    for (int k = 0; k < 4; ++k) t[k] = fma(-m[k][7], e[11], t[k]);
-#pragma unroll
-    for (int k = 0; k < 4; ++k) t[k] = fma(-m[k][8], e[8], t[k]);
-#pragma unroll
-    for (int k = 0; k < 4; ++k) t[k] = fma(-m[k][9], e[12], t[k]);
-#pragma unroll
-    for (int k = 0; k < 4; ++k) acc[k][0] = acc[k][0] + t[k];
-    // L_i: -M D1_i, then D_x, D_y, D_z against the D2 row i
-    // rows: x (e4 e5 e6), y (e5 e7 e8), z (e6 e8 e9)
-#pragma unroll
-    for (int i = 0; i < 3; ++i) {
-      const int r0 = i == 0 ? 4 : (i == 1 ? 5 : 6), r1 = i == 0 ? 5 : (i == 1 ? 7 : 8),
-                r2 = i == 0 ? 6 : (i == 1 ? 8 : 9);
-#pragma unroll
-      for (int k = 0; k < 4; ++k) acc[k][1 + i] = fma(-m[k][0], e[1 + i], acc[k][1 + i]);
-#pragma unroll
-      for (int k = 0; k < 4; ++k) acc[k][1 + i] = fma(m[k][1], e[r0], acc[k][1 + i]);
-#pragma unroll
-      for (int k = 0; k < 4; ++k) acc[k][1 + i] = fma(m[k][2], e[r1], acc[k][1 + i]);
-#pragma unroll
-      for (int k = 0; k < 4; ++k) acc[k][1 + i] = fma(m[k][3], e[r2], acc[k][1 + i]);
+      for (int t = 0; t < 3; ++t) {
+        const int k = mi - t;
+        if (k < 0 || k > 3) continue;
+        if (NEAR && t == 1) continue;
+        m2l_term<NOUT>(m, G[t], acc[k]);
+      }
     }
-    // L_ij: -M D2_ij (leaf patches: L2P reads only L0 and L_i, so NOUT = 4
-    // drops these; the other components are unaffected)
-#pragma unroll
-    for (int q = 0; q < NOUT - 4; ++q)
-#pragma unroll
-      for (int k = 0; k < 4; ++k) acc[k][4 + q] = fma(-m[k][0], e[4 + q], acc[k][4 + q]);
   }
 }
 
@@ -294,9 +286,9 @@ __device__ __forceinline__ void m2l_patch(double* __restrict__ win, const double
       const double* src = win + ((iz & 1) * 2 + (iy & 1)) * kWSub + (Z + (iz >> 1)) * kWPZ +
                           (Y + (iy >> 1)) * kWPY;
       if (dz >= -1 && dz <= 1 && dy >= -1 && dy <= 1)
-        m2l_row_jj<true, NOUT>(src, trow, acc);
+        m2l_row_par<true, NOUT>(src, trow, acc);
       else
-        m2l_row_jj<false, NOUT>(src, trow, acc);
+        m2l_row_par<false, NOUT>(src, trow, acc);
     }
   }
   // upper-half warps hand their partial sums to the lower-half warps (the
