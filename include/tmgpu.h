@@ -273,6 +273,8 @@ int tmgpu_selftest_fastmath(int mode, long long n, uint64_t seed, unsigned long 
 int tmgpu_fp64_peak(int iters, double* tflops, double* ms, tmgpu_error* err);
 /* diagnostics: DFMA TFLOP/s with `warps` warps per SM and `chains` independent chains per thread */
 int tmgpu_fp64_probe(int warps, int chains, int iters, double* tflops);
+/* diagnostics: FP64 tensor-core (mma m8n8k4 f64) TFLOP/s, `warps` per SM, `chains` accumulators */
+int tmgpu_dmma_probe(int warps, int chains, int iters, double* tflops);
 
 /* ---------------------------------------------------------------- build info */
 const char* tmgpu_version(void);

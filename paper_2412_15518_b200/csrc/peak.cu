@@ -32,8 +32,59 @@ __global__ void dfma_chains_kernel(double* out, int iters, double a, double b) {
   for (int k = 0; k < C; ++k) s += x[k];
   if (s == 12345.678) out[0] = s;
 }
+// FP64 tensor-core probe: C independent m8n8k4 DMMA accumulators per warp
+template <int C>
+__global__ void dmma_kernel(double* out, int iters, double a0, double b0) {
+  double a = a0 + threadIdx.x * 1e-9, b = b0 - threadIdx.x * 1e-9;
+  double c[C][2];
+#pragma unroll
+  for (int k = 0; k < C; ++k) c[k][0] = c[k][1] = k;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int k = 0; k < C; ++k)
+      asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+                   : "+d"(c[k][0]), "+d"(c[k][1])
+                   : "d"(a), "d"(b));
+  }
+  double s = 0;
+#pragma unroll
+  for (int k = 0; k < C; ++k) s += c[k][0] + c[k][1];
+  if (s == 12345.678) out[0] = s;
+}
 }  // namespace
 }  // namespace tmgpu
+
+// Diagnostics: FP64 tensor-core (DMMA m8n8k4) TFLOP/s with `warps` warps per
+// SM and `chains` independent accumulators per warp (2*8*8*4 flop per MMA).
+extern "C" int tmgpu_dmma_probe(int warps, int chains, int iters, double* tflops) {
+  using namespace tmgpu;
+  double* d = nullptr;
+  if (cudaMalloc(&d, sizeof(double)) != cudaSuccess) return TMGPU_ERR_CUDA;
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  auto launch = [&](int it) {
+    if (chains <= 1) { dmma_kernel<1><<<sms, 32 * warps>>>(d, it, 0.999, 1e-7); chains = 1; }
+    else if (chains <= 2) { dmma_kernel<2><<<sms, 32 * warps>>>(d, it, 0.999, 1e-7); chains = 2; }
+    else if (chains <= 4) { dmma_kernel<4><<<sms, 32 * warps>>>(d, it, 0.999, 1e-7); chains = 4; }
+    else { dmma_kernel<8><<<sms, 32 * warps>>>(d, it, 0.999, 1e-7); chains = 8; }
+  };
+  cudaEvent_t t0, t1;
+  cudaEventCreate(&t0);
+  cudaEventCreate(&t1);
+  launch(iters / 10 + 1);
+  cudaEventRecord(t0);
+  launch(iters);
+  cudaEventRecord(t1);
+  cudaError_t e = cudaEventSynchronize(t1);
+  float msf = 0;
+  cudaEventElapsedTime(&msf, t0, t1);
+  cudaEventDestroy(t0);
+  cudaEventDestroy(t1);
+  cudaFree(d);
+  if (e != cudaSuccess) return TMGPU_ERR_CUDA;
+  *tflops = 2.0 * 8 * 8 * 4 * chains * (double)iters * sms * warps / (msf * 1e-3) / 1e12;
+  return TMGPU_OK;
+}
 
 // Diagnostics: DFMA TFLOP/s with `warps` warps per SM (one CTA per SM) and
 // `chains` (1, 2, 4, 8, 16) independent FMA chains per thread.

@@ -1,5 +1,6 @@
 """DFMA throughput vs warps per SM and independent chains per thread (the FP64
-latency/occupancy trade-off behind the M2L kernel's 8 warps per SM)."""
+latency/occupancy trade-off behind the M2L kernel's 8 warps per SM), and the
+FP64 tensor-core (DMMA) throughput for comparison."""
 import ctypes as C
 import os
 import sys
@@ -16,3 +17,13 @@ for warps in (4, 8, 16, 32):
         f(warps, chains, 20000, C.byref(t))
         row.append(f"{t.value:6.2f}")
     print(f"warps/SM {warps:2d}: chains 1,2,4,8,16 -> TFLOP/s", " ".join(row))
+
+g = _lib.lib.tmgpu_dmma_probe
+g.argtypes = [C.c_int, C.c_int, C.c_int, C.POINTER(C.c_double)]
+for warps in (4, 8, 16, 32):
+    row = []
+    for chains in (1, 2, 4, 8):
+        t = C.c_double()
+        g(warps, chains, 20000, C.byref(t))
+        row.append(f"{t.value:6.2f}")
+    print(f"DMMA m8n8k4 warps/SM {warps:2d}: chains 1,2,4,8 -> TFLOP/s", " ".join(row))
