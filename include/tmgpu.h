@@ -275,6 +275,8 @@ int tmgpu_fp64_peak(int iters, double* tflops, double* ms, tmgpu_error* err);
 int tmgpu_fp64_probe(int warps, int chains, int iters, double* tflops);
 /* diagnostics: FP64 tensor-core (mma m8n8k4 f64) TFLOP/s, `warps` per SM, `chains` accumulators */
 int tmgpu_dmma_probe(int warps, int chains, int iters, double* tflops);
+/* diagnostics: DFMA TFLOP/s when every FMA reads three fresh registers (8 chains per thread) */
+int tmgpu_dfma3_probe(int warps, int iters, double* tflops);
 
 /* ---------------------------------------------------------------- build info */
 const char* tmgpu_version(void);

@@ -32,6 +32,27 @@ __global__ void dfma_chains_kernel(double* out, int iters, double a, double b) {
   for (int k = 0; k < C; ++k) s += x[k];
   if (s == 12345.678) out[0] = s;
 }
+// register-operand probe: each DFMA reads three registers no earlier
+// instruction just read (x = fma(y, z, x) over rotating y, z): the operand
+// bandwidth of the register file, not the pipe, is then the limit
+template <int C>
+__global__ void dfma3_kernel(double* out, int iters, double a, double b) {
+  double x[C], y[C], z[C];
+#pragma unroll
+  for (int k = 0; k < C; ++k)
+    x[k] = threadIdx.x * 1e-3 + k, y[k] = a + k * 1e-9 + threadIdx.x * 1e-12, z[k] = b - k * 1e-9 - threadIdx.x * 1e-12;
+  for (int i = 0; i < iters; i += C) {
+#pragma unroll
+    for (int r = 0; r < C; ++r)
+#pragma unroll
+      for (int k = 0; k < C; ++k) x[k] = fma(y[(k + r) % C], z[(k + 3 * r + 1) % C], x[k]);
+  }
+  double s = 0;
+#pragma unroll
+  for (int k = 0; k < C; ++k) s += x[k];
+  if (s == 12345.678) out[0] = s;
+}
+
 // FP64 tensor-core probe: C independent m8n8k4 DMMA accumulators per warp
 template <int C>
 __global__ void dmma_kernel(double* out, int iters, double a0, double b0) {
@@ -56,6 +77,30 @@ __global__ void dmma_kernel(double* out, int iters, double a0, double b0) {
 
 // Diagnostics: FP64 tensor-core (DMMA m8n8k4) TFLOP/s with `warps` warps per
 // SM and `chains` independent accumulators per warp (2*8*8*4 flop per MMA).
+extern "C" int tmgpu_dfma3_probe(int warps, int iters, double* tflops) {
+  using namespace tmgpu;
+  double* d = nullptr;
+  if (cudaMalloc(&d, sizeof(double)) != cudaSuccess) return TMGPU_ERR_CUDA;
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  cudaEvent_t t0, t1;
+  cudaEventCreate(&t0);
+  cudaEventCreate(&t1);
+  dfma3_kernel<8><<<sms, 32 * warps>>>(d, iters / 10 + 1, 0.999999, 1e-7);
+  cudaEventRecord(t0);
+  dfma3_kernel<8><<<sms, 32 * warps>>>(d, iters, 0.999999, 1e-7);
+  cudaEventRecord(t1);
+  cudaError_t e = cudaEventSynchronize(t1);
+  float msf = 0;
+  cudaEventElapsedTime(&msf, t0, t1);
+  cudaEventDestroy(t0);
+  cudaEventDestroy(t1);
+  cudaFree(d);
+  if (e != cudaSuccess) return TMGPU_ERR_CUDA;
+  *tflops = 2.0 * 8 * (double)iters * sms * 32.0 * warps / (msf * 1e-3) / 1e12;
+  return TMGPU_OK;
+}
+
 extern "C" int tmgpu_dmma_probe(int warps, int chains, int iters, double* tflops) {
   using namespace tmgpu;
   double* d = nullptr;

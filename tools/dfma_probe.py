@@ -27,3 +27,12 @@ for warps in (4, 8, 16, 32):
         g(warps, chains, 20000, C.byref(t))
         row.append(f"{t.value:6.2f}")
     print(f"DMMA m8n8k4 warps/SM {warps:2d}: chains 1,2,4,8 -> TFLOP/s", " ".join(row))
+
+h = _lib.lib.tmgpu_dfma3_probe
+h.argtypes = [C.c_int, C.c_int, C.POINTER(C.c_double)]
+row = []
+for warps in (4, 8, 16, 32):
+    t = C.c_double()
+    h(warps, 20000, C.byref(t))
+    row.append(f"{t.value:6.2f}")
+print("DFMA, three fresh register operands, 8 chains; warps/SM 4,8,16,32 -> TFLOP/s", " ".join(row))
