@@ -135,6 +135,29 @@ __global__ void amr_m2m_kernel(const GLv* __restrict__ L, int l, const int* __re
     double o[10];
 #pragma unroll
     for (int q = 0; q < 10; ++q) o[q] = 0.0;
+    if (Ch.leaf_slot[cn] >= 0) {
+      // leaf child cells carry (m, +0, ..., +0): read only m. Dropping the +0
+      // terms can only turn a +0 term into -0, and a sum started at +0 is the
+      // same either way, so the result is tmo_grav_m2m's bit for bit.
+      for (int cc = 0; cc < 2; ++cc)
+        for (int b = 0; b < 2; ++b)
+          for (int a = 0; a < 2; ++a) {
+            const double s[3] = {(a - 0.5) * hc, (b - 0.5) * hc, (cc - 0.5) * hc};
+            const int ci = ((2 * I) & 7) + a, cj = ((2 * J) & 7) + b, ck = ((2 * K) & 7) + cc;
+            const double M = base[((ck * 8 + cj) * 8 + ci) * 10];
+            o[0] += M;
+#pragma unroll
+            for (int i = 0; i < 3; ++i) o[1 + i] += M * s[i];
+#pragma unroll
+            for (int i = 0; i < 3; ++i)
+#pragma unroll
+              for (int j = i; j < 3; ++j) o[4 + s2(i, j)] += M * s[i] * s[j];
+          }
+      double* out = P.mom + ((long long)n * 512 + c) * 10;
+#pragma unroll
+      for (int q = 0; q < 10; ++q) out[q] = o[q];
+      continue;
+    }
     for (int cc = 0; cc < 2; ++cc)
       for (int b = 0; b < 2; ++b)
         for (int a = 0; a < 2; ++a) {
