@@ -451,8 +451,10 @@ def run_ours(args, rank, world):
                 "parallelism": (f"leaves partitioned over {world} GPUs (partition_leaves, "
                                 "contiguous Morton ranges); cross-GPU ghost slabs by grouped "
                                 "NCCL send/recv per RK stage; dt by ncclAllReduce(min)" +
-                                ("; gravity: leaf masses all-gathered, M2L/L2L/L2P on the "
-                                 "owned subtree" if gravity else ""))
+                                ("; gravity: locally essential tree — owned-subtree upward pass, "
+                                 "subtree-root moments all-gathered, halo moments by grouped NCCL "
+                                 "send/recv, M2L/L2L/L2P on the owned subtree, solve overlapped "
+                                 "with the CFL reduction and first ghost exchange" if gravity else ""))
                 if world > 1 else "single GPU"}),
             "e2e": {"value": cells / (e2e_ms * 1e-3), "unit": UNIT,
                     "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes,

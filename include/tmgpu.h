@@ -247,8 +247,9 @@ int tmgpu_gravity_amr_am_stats(tmgpu_gravity_amr* G, double* out);
  * same-depth P2P pairs, cross-depth U entries, V pairs evaluated, V pairs into
  * leaf patches, W/X entries into leaf patches] (leaf targets need only L0, L_i) */
 int tmgpu_gravity_amr_work(const tmgpu_gravity_amr* G, long long* out);
-/* multi-GPU: this rank (comm) owns canonical slots [slot_bounds[r], slot_bounds[r+1]);
- * masses and outputs become by local slot; results equal the one-GPU solve bitwise */
+/* multi-GPU (locally essential tree, multipole-moment exchange over NCCL): this rank (comm)
+ * owns canonical slots [slot_bounds[r], slot_bounds[r+1]); masses and outputs become by local
+ * slot; results equal the one-GPU solve bitwise */
 int tmgpu_gravity_amr_distribute(tmgpu_gravity_amr* G, tmgpu_comm* comm, const long long* slot_bounds,
                                  tmgpu_error* err);
 /* host-only: per-level counts of the patches a rank owning slots [lo, hi) evaluates

@@ -839,7 +839,7 @@ void count_work(const GravPlan& P, const std::vector<std::vector<int>>* need, lo
 }
 
 // per-phase device timing of solves (bench): events at the phase boundaries
-constexpr int kGravPhases = 6;  // comm (mass all-gather), up (P2M, M2M, dense), m2l, l2l, l2p, am
+constexpr int kGravPhases = 6;  // comm (unused since the LET: 0), up (incl. moment exchange), m2l, l2l, l2p, am
 struct GravTimingRec {
   cudaEvent_t ev[kGravPhases + 1];
 };
@@ -1416,12 +1416,14 @@ int tmgpu_gravity_amr_solve(tmgpu_gravity_amr* G, const double* mass, double* ph
 
 // Distributed solve: rank comm_rank(comm) owns canonical slots
 // [slot_bounds[r], slot_bounds[r+1]) (contiguous ranges, partition_leaves).
-// Every rank keeps the whole tree's moments (leaf masses all-gathered, then
-// the replicated upward pass); M2L and L2L run only over the ancestors of the
-// owned leaves, L2P and the AM correction's per-slot sums only over the owned
-// slots (the sums are all-gathered, so every rank reduces the identical global
-// pair tree). Outputs (phi, g) and masses are then by local slot; the result
-// equals the one-GPU solve bit for bit.
+// Locally essential tree (grav_let_plan): each rank computes its owned
+// subtrees' moments, all-gathers the subtree roots, computes the shared top,
+// and receives the owned patches of others it reads (point to point); M2L and
+// L2L run only over the ancestors of the owned leaves, L2P and the AM
+// correction's per-slot sums only over the owned slots (the sums are
+// all-gathered, so every rank reduces the identical global pair tree).
+// Outputs (phi, g) and masses are then by local slot; the result equals the
+// one-GPU solve bit for bit.
 int tmgpu_gravity_amr_distribute(tmgpu_gravity_amr* G, tmgpu_comm* comm, const long long* slot_bounds,
                                  tmgpu_error* err) {
   if (err) std::memset(err, 0, sizeof(*err));

@@ -74,18 +74,23 @@ class GravityHydroDriver(HydroDriver):
     stage kernel's source term (m += dt*rho*g, E += dt*rho*(v.g); oracle
     tmo_stage_subgrid_grav).
 
-    On a distributed forest (Forest.distribute) the solve is distributed the
-    same way: leaf masses all-gathered over NCCL, M2L/L2L/L2P on the ancestors
-    of the owned leaves (GravityAMR.distribute); bitwise equal to one GPU."""
+    On a distributed forest (Forest.distribute) the solve is distributed as a
+    locally essential tree with a multipole-moment exchange (GravityAMR.distribute);
+    bitwise equal to one GPU. ``regrid`` refines/coarsens with the data carried
+    along (Forest.regrid) and rebuilds the gravity plan (single GPU)."""
 
     def __init__(self, forest: Forest, gamma: float = 1.4, cfl: float = 0.4, fast: bool = False,
                  exact_ghosts: bool = False, am: bool = True, reflux: bool = False):
         super().__init__(forest, gamma, cfl, fast, exact_ghosts, reflux)
+        self.am = am
+        self._setup_gravity()
+
+    def _setup_gravity(self) -> None:
         import torch
 
         from .gravity import GravityAMR
 
-        self.am = am
+        forest = self.forest
         leaves = np.array([unpack(int(p)) for p in forest.leaves()], dtype=np.int32).reshape(-1, 4)
         self.gravity = GravityAMR(leaves)
         comm = getattr(forest, "_comm", None)
@@ -130,6 +135,17 @@ class GravityHydroDriver(HydroDriver):
     def step(self, dt: float | None = None, stream=None, sync: bool = True) -> float | None:
         self.solve_gravity(stream)
         return super().step(dt, stream, sync)
+
+    def regrid(self, refine=(), coarsen=()) -> None:
+        """Refine then coarsen leaves with the state carried along (the
+        reference's prolong_cell / restrict_cells, Forest.regrid), then rebuild
+        the gravity plan and field for the new topology (and the reflux plan)."""
+        self.close()
+        self.forest.regrid(refine, coarsen)
+        if self.reflux:
+            err = TmgpuError()
+            _lib.check(lib.tmgpu_forest_set_reflux(self.forest.h, 1, C.byref(err)), err)
+        self._setup_gravity()
 
     def close(self) -> None:
         err = TmgpuError()

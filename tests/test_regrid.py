@@ -115,3 +115,36 @@ def test_flag_refinement_equals_reference(ref, theta):
     want = np.array([t.flag(int(p), theta) for p in f.leaves()])
     assert (got == want).all()
     assert 0 < got.sum() < len(got) or theta == 0.2
+
+
+@pytest.mark.gpu
+def test_gravity_hydro_driver_steps_across_a_regrid():
+    """Refine during a run: the driver carries the state along (regrid), rebuilds
+    the gravity plan, and the next step equals a fresh driver on the regridded
+    forest started from the same (regridded) state."""
+    from paper_2412_15518_b200.driver import GravityHydroDriver
+
+    def run(regrid_first):
+        f = amr.build_scenario(amr.Scenario.rotating_star, 1, 3)
+        f.alloc()
+        f.set_interior(f.scenario_state(amr.Scenario.rotating_star))
+        d = GravityHydroDriver(f)
+        d.step(dt=1e-3)
+        lv = [int(p) for p in f.leaves()]
+        d.regrid(refine=[p for p in lv if amr.unpack(p)[0] == 1][:2])
+        state = f.get_grids()
+        if regrid_first:
+            d.step(dt=1e-3)
+            out = f.get_interior()
+        else:
+            d.close()
+            d2 = GravityHydroDriver(f)
+            f.set_grids(state)
+            d2.step(dt=1e-3)
+            out = f.get_interior()
+            d2.close()
+        return out, f.leaf_count()
+
+    a, na = run(True)
+    b, nb = run(False)
+    assert na == nb and a.tobytes() == b.tobytes()
