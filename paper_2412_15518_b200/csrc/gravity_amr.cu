@@ -53,8 +53,11 @@ struct GLv {
 
 namespace {
 
+// ((double)gi + 0.5) / 2^d as the oracle writes it; dividing by a power of two
+// is exact, so multiplying by the exact 2^-d gives the same bits without a
+// division sequence
 __device__ __forceinline__ double centre(long long gi, int d) {
-  return ((double)gi + 0.5) / (double)(1LL << d);
+  return ((double)gi + 0.5) * __longlong_as_double((long long)(1023 - d) << 52);
 }
 
 // arena slots 0..nslots-1 are the canonical slots lo.. (distributed: the owned range)
@@ -468,6 +471,22 @@ __global__ void __launch_bounds__(128, 4) amr_wx_kernel(const GLv* __restrict__ 
   }
 }
 
+// P2P geometry of the 26 same-depth lattice offsets at every cell depth
+// (p2p_geom, the per-pair operations): [depth][27][4], centre entry zero
+__global__ void p2p_table_kernel(double* __restrict__ tab, int D) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (D + 1) * 27) return;
+  const int dpt = t / 27, o = t % 27;
+  const int dx = o % 3 - 1, dy = (o / 3) % 3 - 1, dz = o / 9 - 1;
+  double* e = tab + (long long)t * 4;
+  if (o == 13) {
+    for (int q = 0; q < 4; ++q) e[q] = 0.0;
+    return;
+  }
+  const double h = 1.0 / (double)(1LL << dpt);
+  p2p_geom(-(double)dx * h, -(double)dy * h, -(double)dz * h, e);
+}
+
 __global__ void sep_geom_kernel(const double* __restrict__ sep, long long n, double* __restrict__ geo,
                                 int p2p) {
   const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
@@ -561,6 +580,8 @@ __global__ void __launch_bounds__(512) amr_l2p_kernel(const GLv* __restrict__ Lv
                                                       const double* __restrict__ mass,
                                                       const double* __restrict__ ugeo,
                                                       const double* __restrict__ lloc,
+                                                      const double* __restrict__ p2p_tab,
+                                                      const int* __restrict__ slot_nbs,
                                                       double* __restrict__ phi, double* __restrict__ g,
                                                       double* __restrict__ part) {
   __shared__ double w26[27][4];
@@ -571,12 +592,11 @@ __global__ void __launch_bounds__(512) amr_l2p_kernel(const GLv* __restrict__ Lv
   const GLv L = Lv[l];
   const int d = l + 3;
   const double h = 1.0 / (double)(1LL << d);
-  if (threadIdx.x < 27) {
+  if (threadIdx.x < 27) {  // precomputed per depth / per slot (tables built at create)
     const int o = threadIdx.x;
-    const int dx = o % 3 - 1, dy = (o / 3) % 3 - 1, dz = o / 9 - 1;
-    if (o != 13) p2p_geom(-(double)dx * h, -(double)dy * h, -(double)dz * h, w26[o]);
-    const int nb = L.nbr[(long long)n * 27 + o];
-    nbslot[o] = (nb >= 0 && L.leaf_slot[nb] >= 0) ? (long long)L.leaf_slot[nb] : -1;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) w26[o][q] = p2p_tab[((long long)d * 27 + o) * 4 + q];
+    nbslot[o] = slot_nbs[s * 27 + o];
   }
   __syncthreads();
   const long long ncell = nslots * 512;
@@ -862,6 +882,8 @@ struct GravAmrWork {
   double* tab = nullptr;
   double* mass = nullptr;
   double* lloc = nullptr;   // [slot - lo][4][512] leaf locals L0, L_i (leaf patches only)
+  double* p2p_tab = nullptr;  // [depth][27][4] same-depth P2P geometry
+  int* slot_nbs = nullptr;    // [slot][27] same-depth neighbour leaf slot or -1
   double* part = nullptr;   // [P][16] + rw[22]
   double* part2 = nullptr;  // [P/256 + 1][16] tree scratch
   long long nslots = 0, P = 1;
@@ -1145,6 +1167,18 @@ tmgpu_gravity_amr* tmgpu_gravity_amr_create(const int* leaves, long long nleaves
   if (e == cudaSuccess) e = cudaMalloc(&w.tab, (size_t)(Dmax + 1) * kOff3 * kTab * sizeof(double)), track(w.tab);
   if (e == cudaSuccess) e = cudaMalloc(&w.mass, (size_t)w.nslots * 512 * sizeof(double)), track(w.mass);
   if (e == cudaSuccess) e = cudaMalloc(&w.lloc, (size_t)w.nslots * 2048 * sizeof(double)), track(w.lloc);
+  if (e == cudaSuccess) {
+    std::vector<int> nbs((size_t)nleaves * 27, -1);
+    for (long long sl = 0; sl < nleaves; ++sl) {
+      const GravLevel& L = P.lv[P.slot_level[sl]];
+      const int nd = P.slot_node[sl];
+      for (int o = 0; o < 27; ++o) {
+        const int nb = L.nbr[(size_t)nd * 27 + o];
+        nbs[(size_t)sl * 27 + o] = nb >= 0 ? L.leaf_slot[nb] : -1;
+      }
+    }
+    e = upload(nbs, &w.slot_nbs), track(w.slot_nbs);
+  }
   if (e == cudaSuccess) e = cudaMalloc(&w.part, ((size_t)w.P * 16 + 22) * sizeof(double)), track(w.part);
   if (e == cudaSuccess) e = cudaMalloc(&w.part2, ((size_t)w.P / 256 + 1) * 16 * sizeof(double)), track(w.part2);
   if (e == cudaSuccess)
@@ -1171,7 +1205,10 @@ tmgpu_gravity_amr* tmgpu_gravity_amr_create(const int* leaves, long long nleaves
     }
     if (dsep) cudaFree(dsep);
   }
+  if (e == cudaSuccess) e = cudaMalloc(&w.p2p_tab, (size_t)(Dmax + 1) * 27 * 4 * sizeof(double)), track(w.p2p_tab);
   if (e == cudaSuccess) {
+    p2p_table_kernel<<<((Dmax + 1) * 27 + 127) / 128, 128>>>(w.p2p_tab, Dmax);
+    g_launches.fetch_add(1, std::memory_order_relaxed);
     stencil_table_kernel<<<((Dmax + 1) * kOff3 + 127) / 128, 128>>>(w.tab, Dmax);
     g_launches.fetch_add(1, std::memory_order_relaxed);
     e = cudaDeviceSynchronize();
@@ -1372,7 +1409,8 @@ int tmgpu_gravity_amr_solve(tmgpu_gravity_amr* G, const double* mass, double* ph
     if (am) e = cudaMemsetAsync(w.part, 0, (size_t)w.P * 16 * sizeof(double), st);
     if (nloc)
       amr_l2p_kernel<<<(unsigned)nloc, 512, 0, st>>>(w.dev_lv, nloc, w.lo, w.slot_level, w.slot_node,
-                                                     w.mass, w.u_geo, w.lloc, dphi, dg, am ? w.part : nullptr);
+                                                     w.mass, w.u_geo, w.lloc, w.p2p_tab, w.slot_nbs, dphi, dg,
+                                                     am ? w.part : nullptr);
     ++launches;
     if (timed) cudaEventRecord(rec.ev[5], st);
     if (am) {  // the per-slot sums came with L2P
