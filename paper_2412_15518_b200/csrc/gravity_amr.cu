@@ -390,7 +390,9 @@ __global__ void __launch_bounds__(kM2lThreads, 1) amr_m2l_fused_kernel(
   asm volatile("cp.async.wait_all;\n" ::: "memory");
   __syncthreads();
   const int leaf = L.leaf_slot[n];
-  if (leaf >= 0)  // leaf patch: L0, L_i into the compact leaf locals (L2P's input)
+  // leaf patch below the root: L0, L_i into the compact leaf locals (L2P's
+  // input); a leaf root keeps all ten (the dense levels' L2L adds into them)
+  if (leaf >= 0 && l > 0)
     m2l_patch<4>(win, tabs, L.loc, n, lloc + (long long)(leaf - lo) * 2048);
   else
     m2l_patch<10>(win, tabs, L.loc, n, nullptr);
@@ -448,7 +450,7 @@ __global__ void __launch_bounds__(128, 4) amr_wx_kernel(const GLv* __restrict__ 
     const long long* moff = Lv[l].moff;
     const long long e0 = moff[flat], e1 = moff[flat + 1];
     const int leaf = Lv[l].leaf_slot[flat >> 9];
-    if (leaf >= 0) {
+    if (leaf >= 0 && l > 0) {
       double* p = lloc + (long long)(leaf - lo) * 2048 + (flat & 511);
       double acc[4] = {p[0], p[512], p[1024], p[1536]};
       wx_entries<4>(Lv, Lv[l].ment, Lv[l].mgeo, e0, e1, geo, acc);
@@ -603,9 +605,15 @@ __global__ void __launch_bounds__(512) amr_l2p_kernel(const GLv* __restrict__ Lv
   const int c = threadIdx.x;
   const int i = c & 7, j = (c >> 3) & 7, k = c >> 6;
   const long long flat = (long long)n * 512 + c;
-  const double* Lc = lloc + ls * 2048 + c;  // compact leaf locals (V + W/X sums)
-  double loc4[4] = {Lc[0], Lc[512], Lc[1024], Lc[1536]};
-  if (l > 0) {
+  double loc4[4];
+  if (l == 0) {  // a leaf root: the full locals, with the dense levels' L2L already added
+    const double* Lr = L.loc + flat * 10;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) loc4[q] = Lr[q];
+  } else {  // compact leaf locals (V + W/X sums) + the parent's shift
+    const double* Lc = lloc + ls * 2048 + c;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) loc4[q] = Lc[q * 512];
     double sv[3], sh[4];
     l2l_shift<4>(l2l_parent(L, Lv[l - 1], n, c, h, sv), sv, sh);
 #pragma unroll

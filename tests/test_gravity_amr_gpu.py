@@ -67,3 +67,27 @@ def test_amr_gravity_from_forest_arena_device_path():
     tq = np.cross(x - stats[:3], (gg * mm).T).sum(0)
     scale = (np.linalg.norm(x - stats[:3], axis=1) * np.linalg.norm(gg, axis=0) * mm).sum()
     assert np.abs(tq).max() / scale < 1e-14
+
+
+@pytest.mark.parametrize("am", [False, True])
+def test_amr_gravity_single_leaf_root(am):
+    """Edge case: the whole domain one leaf (level 0): the root patch is a leaf,
+    its locals come from the dense levels' L2L and its own V sums."""
+    o = O.Oracle()
+    lv = np.array([[0, 0, 0, 0]], dtype=np.int32)
+    m = masses(lv, "random", 11)
+    pr, gr, cnt = o.grav_amr(lv, m, flags=1 if am else 0)
+    phi, g = G.GravityAMR(lv).solve(m, am=am)
+    assert phi.tobytes() == pr.tobytes()
+    assert g.tobytes() == gr.tobytes()
+
+
+def test_amr_gravity_level1_uniform():
+    """Edge case: eight level-1 leaves (every patch a leaf, one internal root)."""
+    o = O.Oracle()
+    lv = uniform_leaves(1)
+    m = masses(lv, "star", 12)
+    pr, gr, _ = o.grav_amr(lv, m, flags=1)
+    phi, g = G.GravityAMR(lv).solve(m, am=True)
+    assert phi.tobytes() == pr.tobytes()
+    assert g.tobytes() == gr.tobytes()
