@@ -103,12 +103,14 @@ class GravityHydroDriver(HydroDriver):
 
             self.gcomm = Comm.from_torch()
             self.gravity.distribute(self.gcomm, forest._owner)
-        # multi-GPU: the solve (latency-bound moment exchange and upward pass)
-        # runs on a side stream, overlapped with the CFL reduction and the
-        # first ghost exchange; the first stage kernel waits for it. One GPU:
-        # the step's own stream (the M2L fills the GPU; nothing to overlap)
+        # the solve runs on a side stream, overlapped with the CFL reduction and
+        # the first ghost exchange (multi-GPU: also the latency-bound moment
+        # exchange); the first stage kernel waits for it. TMGPU_GRAVITY_OVERLAP=0
+        # keeps it on the step's stream (same results, bit for bit)
+        import os
+
         self.gstream = None
-        if forest.local_count() != forest.leaf_count():
+        if os.environ.get("TMGPU_GRAVITY_OVERLAP", "1") != "0":
             self.gstream = torch.cuda.Stream()
             _lib.check(lib.tmgpu_forest_set_gravity_stream(forest.h, self.gstream.cuda_stream,
                                                            C.byref(TmgpuError())), TmgpuError())
