@@ -56,6 +56,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-steps", type=int, default=1)
     ap.add_argument("--hydro-only", action="store_true", help="time the hydro step alone")
+    ap.add_argument("--halo", choices=["nccl", "peer"], default="peer",
+                    help="N>1 ghost-slab transport: NCCL send/recv or peer-memory stores")
     ap.add_argument("--scenario", choices=["star", "dwd"], default="star",
                     help="star: configs[2] (default); dwd: configs[4] with --max-level 7")
     return ap.parse_args()
@@ -305,6 +307,8 @@ def run_ours(args, rank, world):
         lo, hi = tmdist.local_range(owner, rank)
         state = np.ascontiguousarray(state[lo:hi])
     f.alloc()
+    if world > 1 and args.halo == "peer":
+        f.set_peer(True)
     f.set_interior(state)
     local_cells = f.local_count() * 512
     gravity = not args.hydro_only
@@ -412,6 +416,11 @@ def run_ours(args, rank, world):
     else:
         roofline = stage_roof
     roofline["step_share"] = share
+    if gravity:
+        roofline["step_share_note"] = (
+            "device-event phase times / step time; the gravity solve runs on its own stream "
+            "concurrently with the CFL reduction and the first ghost exchange, whose interval "
+            "includes the wait for it, so the shares overlap")
     roofline["gravity_work"] = work or None
 
     # e2e through the public API with host buffers (pinned): every step moves
@@ -449,8 +458,11 @@ def run_ours(args, rank, world):
             "1e-3 density noise, std::mt19937_64)",
             "config": workload_config(f, args, {
                 "parallelism": (f"leaves partitioned over {world} GPUs (partition_leaves, "
-                                "contiguous Morton ranges); cross-GPU ghost slabs by grouped "
-                                "NCCL send/recv per RK stage; dt by ncclAllReduce(min)" +
+                                "contiguous Morton ranges); cross-GPU ghost slabs " +
+                                ("packed straight into the receivers' buffers over NVLink (CUDA "
+                                 "IPC peer memory, flag-word sync)" if args.halo == "peer" else
+                                 "by grouped NCCL send/recv") + " per RK stage; dt by "
+                                "ncclAllReduce(min)" +
                                 ("; gravity: locally essential tree — owned-subtree upward pass, "
                                  "subtree-root moments all-gathered, halo moments by grouped NCCL "
                                  "send/recv, M2L/L2L/L2P on the owned subtree, solve overlapped "

@@ -172,6 +172,12 @@ int tmgpu_forest_set_gravity(tmgpu_forest* f, const double* g, long long comp_st
  * CFL reduction and first ghost exchange concurrently and waits for that stream's work (enqueued
  * before the step call) only before the first stage kernel */
 int tmgpu_forest_set_gravity_stream(tmgpu_forest* f, void* stream, tmgpu_error* err);
+/* multi-GPU ghost exchange over peer memory instead of NCCL send/recv (collective over the
+ * forest's communicator; 2..8 ranks on one node with CUDA IPC): each rank packs its cross-GPU
+ * slabs straight into the receivers' buffers and synchronises by flag words (a wait that does
+ * not complete within 5 s traps). Re-call after tmgpu_forest_alloc; on = 0 returns to NCCL.
+ * No reference counterpart (the reference moves ghosts through HPX channels). */
+int tmgpu_forest_set_peer(tmgpu_forest* f, int on, tmgpu_error* err);
 /* `waiter` waits for the work enqueued so far on `signaller` (CUDA streams; NULL = default) */
 int tmgpu_stream_wait(void* waiter, void* signaller);
 int tmgpu_forest_step(tmgpu_forest* f, double dt, double cfl, double gamma, int flags,

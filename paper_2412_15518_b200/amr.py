@@ -52,6 +52,7 @@ _sig("tmgpu_forest_exchanges", C.c_uint64, [_vp])
 _sig("tmgpu_forest_scenario_refine", C.c_int, [_vp, C.c_int, C.c_int, C.c_int, C.c_double, _ep])
 _sig("tmgpu_forest_scenario_fill", C.c_int, [_vp, C.c_int, C.c_uint64, _vp, _ep])
 _sig("tmgpu_forest_alloc", C.c_int, [_vp, _ep])
+_sig("tmgpu_forest_set_peer", C.c_int, [_vp, C.c_int, _ep])
 _sig("tmgpu_forest_arena", _vp, [_vp])
 _sig("tmgpu_forest_interior", C.c_int, [_vp, _vp, C.c_int, C.c_int, _vp, _ep])
 _sig("tmgpu_forest_grids", C.c_int, [_vp, _vp, C.c_int, _ep])
@@ -270,6 +271,12 @@ class Forest:
         """(Re)allocate the zeroed device arena for the current topology."""
         err = TmgpuError()
         _lib.check(lib.tmgpu_forest_alloc(self.h, C.byref(err)), err)
+
+    def set_peer(self, on: bool = True) -> None:
+        """Collective: move the cross-GPU ghost slabs through peer memory (CUDA
+        IPC over NVLink) instead of NCCL send/recv; re-call after alloc()."""
+        err = TmgpuError()
+        _lib.check(lib.tmgpu_forest_set_peer(self.h, 1 if on else 0, C.byref(err)), err)
 
     def arena_ptr(self) -> int:
         return int(lib.tmgpu_forest_arena(self.h) or 0)

@@ -77,6 +77,15 @@ struct tmgpu_forest {
   int n_pull_local = 0, n_pull_remote = 0, n_interior = 0, n_boundary = 0;
   cudaStream_t side = nullptr;
   cudaEvent_t ev_packed = nullptr, ev_remote = nullptr;
+  // peer-memory exchange (tmgpu_forest_set_peer), valid for `peer_version`
+  bool peer = false;
+  uint64_t peer_version = ~0ull;
+  unsigned long long peer_seq = 0;
+  PeerTab ptab{};
+  unsigned long long* peer_flags = nullptr;
+  PackItem* pack_peer = nullptr;
+  int2* pull_peer = nullptr;  // pull_local ++ pull_remote
+  void* peer_opened[2 * kMaxPeers] = {};
   StageMaps maps[2]{};
   uint64_t exchanges = 0;  // ghost exchanges performed (structural counter)
   // optional per-phase device timing: events [start, cfl, (exch, stage) x 3]
@@ -108,7 +117,25 @@ void collect_timing(tmgpu_forest* f) {
   f->pending_timed = 0;
 }
 
+void peer_close(tmgpu_forest* f) {
+  if (f->peer_flags || f->peer) cudaDeviceSynchronize();
+  for (void*& p : f->peer_opened) {
+    if (p) cudaIpcCloseMemHandle(p);
+    p = nullptr;
+  }
+  for (void* p : {(void*)f->peer_flags, (void*)f->pack_peer, (void*)f->pull_peer})
+    if (p) cudaFree(p);
+  f->peer_flags = nullptr;
+  f->pack_peer = nullptr;
+  f->pull_peer = nullptr;
+  f->ptab = PeerTab{};
+  f->peer = false;
+  f->peer_version = ~0ull;
+  f->peer_seq = 0;
+}
+
 void free_dev(tmgpu_forest* f) {
+  peer_close(f);
   auto fr = [](void* p) {
     if (p) cudaFree(p);
   };
@@ -282,6 +309,26 @@ int exchange(tmgpu_forest* f, cudaStream_t st, ExchangeMode mode, std::string* w
   } else {
     const bool all = mode == kFaces;
     const double* prev = all ? f->arena() : f->arenas[f->cur ^ 1];
+    if (f->peer) {
+      if (f->peer_version != f->forest.topology_version()) {
+        if (why) *why = "peer exchange: topology changed; call tmgpu_forest_set_peer again";
+        return TMGPU_ERR_INVALID;
+      }
+      const unsigned long long seq = ++f->peer_seq;
+      e = halo_pack_peer(f->arena(), prev, V, f->pack_peer, f->n_pack, f->slabs, f->ptab, seq, st);
+      // every face: one list whose faces all wait for the senders
+      if (e == cudaSuccess)
+        e = all ? halo_pull_peer(f->arena(), V, f->faces, f->pull_all, 0, f->n_pull_all, f->slabs,
+                                 f->ptab, seq, st)
+                : halo_pull_peer(f->arena(), V, f->faces, f->pull_peer, f->n_pull_local,
+                                 f->n_pull_fused, f->slabs, f->ptab, seq, st);
+      if (e != cudaSuccess) {
+        if (why) *why = std::string("peer ghost exchange: ") + cudaGetErrorString(e);
+        return TMGPU_ERR_CUDA;
+      }
+      f->exchanges += 1;
+      return TMGPU_OK;
+    }
     e = halo_pack(f->arena(), prev, V, f->pack, f->n_pack, f->slabs, st);
     if (e == cudaSuccess && f->world() > 1) {
       const HaloPlan& P = f->plan;
@@ -725,7 +772,7 @@ int tmgpu_forest_step(tmgpu_forest* f, double dt, double cfl, double gamma, int 
   p.face_src = exact ? nullptr : f->face_src;
   // opt-in: measured no faster on C3 at 2-4 GPUs (the split boundary launch
   // under-fills the GPU), so the default keeps one exchange + one launch
-  const bool overlap = !exact && f->world() > 1 && (flags & TMGPU_OVERLAP);
+  const bool overlap = !exact && f->world() > 1 && !f->peer && (flags & TMGPU_OVERLAP);
   for (int stage = 1; stage <= 3 && e == cudaSuccess; ++stage) {
     std::string why;
     if (overlap) {
@@ -748,8 +795,9 @@ int tmgpu_forest_step(tmgpu_forest* f, double dt, double cfl, double gamma, int 
     } else if (int rc = exchange(f, st, exact ? kExact : kFused, &why)) {
       return fail(err, rc, why);
     }
-    if (timed) cudaEventRecord(f->ev[2 * stage], st);
+    // (stage 1's exchange interval includes the wait for a concurrent gravity solve)
     if (stage == 1 && f->grav_stream && e == cudaSuccess) e = cudaStreamWaitEvent(st, f->ev_grav, 0);
+    if (timed) cudaEventRecord(f->ev[2 * stage], st);
     p.rk_stage = stage;
     p.u0_save = stage == 1 ? f->u0 : nullptr;
     p.u0_save_stride = (long long)V * 512;
@@ -802,6 +850,116 @@ int tmgpu_stream_wait(void* waiter, void* signaller) {
   if (e == cudaSuccess) e = cudaStreamWaitEvent(as_stream(waiter), ev, 0);
   cudaEventDestroy(ev);
   return e == cudaSuccess ? TMGPU_OK : TMGPU_ERR_CUDA;
+}
+
+// Peer-memory halo exchange (collective over the forest's communicator): every
+// rank exports its slab buffer and flag words by CUDA IPC, learns where its
+// slabs land in each receiver's buffer, and rewrites its cross-rank pack items
+// to store there directly (halo.h PeerTab). on = 0 returns to NCCL send/recv.
+// Re-call after tmgpu_forest_alloc (a new topology or distribution).
+int tmgpu_forest_set_peer(tmgpu_forest* f, int on, tmgpu_error* err) {
+  if (err) std::memset(err, 0, sizeof(*err));
+  if (int rc = ready(f, err)) return rc;
+  peer_close(f);
+  if (!on) return TMGPU_OK;
+  const int world = f->world(), me = f->rank();
+  if (world < 2) return fail(err, TMGPU_ERR_INVALID, "peer exchange needs a communicator with 2+ ranks");
+  if (world > kMaxPeers) return fail(err, TMGPU_ERR_INVALID, "peer exchange supports up to 8 ranks");
+  const HaloPlan& P = f->plan;
+  cudaError_t e = cudaMalloc((void**)&f->peer_flags, (3 * world + 1) * sizeof(unsigned long long));
+  if (e == cudaSuccess) e = cudaMemset(f->peer_flags, 0, (3 * world + 1) * sizeof(unsigned long long));
+  // per rank: slab handle, flag handle (8 doubles each), recv_base, recv_off[world]
+  constexpr int kRec = 32;
+  std::vector<double> rec(kRec, 0.0), all((size_t)kRec * world, 0.0);
+  cudaIpcMemHandle_t hs{}, hf{};
+  if (e == cudaSuccess) e = cudaIpcGetMemHandle(&hs, f->slabs);
+  if (e == cudaSuccess) e = cudaIpcGetMemHandle(&hf, f->peer_flags);
+  static_assert(sizeof(cudaIpcMemHandle_t) == 64, "IPC handle size");
+  std::memcpy(&rec[0], &hs, 64);
+  std::memcpy(&rec[8], &hf, 64);
+  rec[16] = (double)P.recv_base;
+  for (int p = 0; p < world; ++p) rec[17 + p] = (double)P.recv_off[p];
+  double* dbuf = nullptr;
+  if (e == cudaSuccess) e = cudaMalloc((void**)&dbuf, sizeof(double) * kRec * (world + 1));
+  if (e == cudaSuccess) e = cudaMemcpy(dbuf, rec.data(), sizeof(double) * kRec, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) {
+    if (dbuf) cudaFree(dbuf);
+    peer_close(f);
+    return cuda_err(err, e, "tmgpu_forest_set_peer");
+  }
+  std::string why;
+  int rc = comm_allgather(f->comm, dbuf, dbuf + kRec, kRec, nullptr, &why);
+  if (rc == TMGPU_OK) {
+    e = cudaMemcpy(all.data(), dbuf + kRec, sizeof(double) * kRec * world, cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) rc = cuda_err(err, e, "tmgpu_forest_set_peer");
+  } else {
+    fail(err, rc, why);
+  }
+  cudaFree(dbuf);
+  if (rc != TMGPU_OK) {
+    peer_close(f);
+    return rc;
+  }
+  PeerTab t{};
+  t.mine = f->peer_flags;
+  t.me = me;
+  t.world = world;
+  for (int q = 0; q < world && e == cudaSuccess; ++q) {
+    if (q == me) continue;
+    if (P.recv_cnt[q] > 0) t.recv_mask |= 1u << q;
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, &all[(size_t)q * kRec], 64);
+    e = cudaIpcOpenMemHandle(&f->peer_opened[2 * q], h, cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess) break;
+    std::memcpy(&h, &all[(size_t)q * kRec + 8], 64);
+    e = cudaIpcOpenMemHandle(&f->peer_opened[2 * q + 1], h, cudaIpcMemLazyEnablePeerAccess);
+    t.slabs[q] = static_cast<double*>(f->peer_opened[2 * q]);
+    t.flags[q] = static_cast<unsigned long long*>(f->peer_opened[2 * q + 1]);
+  }
+  // cross-rank items: local prolonged first, then by destination rank; the
+  // offset becomes the receiver's (recv_base + recv_off[me] + position)
+  std::vector<PackItem> items;
+  items.reserve(P.pack.size());
+  for (const PackItem& it : P.pack)
+    if (it.out < P.send_base) items.push_back(it);
+  for (int q = 0; q < world; ++q) {
+    if (q == me) continue;
+    const long long lo = P.send_base + P.send_off[q], hi = lo + P.send_cnt[q];
+    const long long dst = (long long)all[(size_t)q * kRec + 16] + (long long)all[(size_t)q * kRec + 17 + me];
+    for (PackItem it : P.pack)
+      if (it.out >= lo && it.out < hi) {
+        it.out = (int32_t)(dst + (it.out - lo));
+        it.pad[0] = (int8_t)(q + 1);
+        items.push_back(it);
+        t.n_send[q] += 1;
+      }
+  }
+  if (e == cudaSuccess && items.size() != P.pack.size()) e = cudaErrorInvalidValue;
+  std::vector<int> pulls = P.pull_fused_local;
+  pulls.insert(pulls.end(), P.pull_fused_remote.begin(), P.pull_fused_remote.end());
+  e = upload(&f->pack_peer, items, e);
+  e = upload((int**)&f->pull_peer, pulls, e);
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) {
+    peer_close(f);
+    return cuda_err(err, e, "tmgpu_forest_set_peer");
+  }
+  // every rank has zeroed its flags and mapped its peers before anyone signals
+  dbuf = nullptr;
+  e = cudaMalloc((void**)&dbuf, sizeof(double) * (world + 1));
+  if (e == cudaSuccess) rc = comm_allgather(f->comm, dbuf, dbuf + 1, 1, nullptr, &why);
+  if (e == cudaSuccess && rc == TMGPU_OK) e = cudaDeviceSynchronize();
+  if (dbuf) cudaFree(dbuf);
+  if (e != cudaSuccess || rc != TMGPU_OK) {
+    peer_close(f);
+    return e != cudaSuccess ? cuda_err(err, e, "tmgpu_forest_set_peer") : fail(err, rc, why);
+  }
+  f->ptab = t;
+  f->peer = true;
+  f->peer_version = f->forest.topology_version();
+  f->peer_seq = 0;
+  return TMGPU_OK;
 }
 
 // The stream later steps' gravity is computed on (nullptr: same stream as the

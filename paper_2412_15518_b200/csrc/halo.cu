@@ -30,14 +30,11 @@ __device__ __forceinline__ void compose(int axis, int na, int v1, int v2, int& x
 //   same       ((var*E + f2)*E + f1)*G + la   value for destination ghost layer la
 //   prolonged  ((var*E + f2)*E + f1)*G + dd   ghost.cpp:161-186 order
 //   restricted ((var*H + c2)*H + c1)*G + dd   ghost.cpp:204-224 order
-__global__ void __launch_bounds__(128) pack_kernel(const double* __restrict__ arena,
-                                                   const double* __restrict__ prev, int V,
-                                                   const PackItem* __restrict__ items,
-                                                   double* __restrict__ slabs) {
-  const PackItem it = items[blockIdx.x];
+__device__ __forceinline__ void pack_item(const double* __restrict__ arena,
+                                          const double* __restrict__ prev, int V,
+                                          const PackItem& it, double* out) {
   const double* src = arena + (long long)it.src * V * S3;
   const double* gsrc = prev + (long long)it.src * V * S3;
-  double* out = slabs + it.out;
   const int axis = it.axis, dir = it.dir;
   if (it.kind == 0) {
     for (int n = threadIdx.x; n < V * E * E * G; n += blockDim.x) {
@@ -82,6 +79,14 @@ __global__ void __launch_bounds__(128) pack_kernel(const double* __restrict__ ar
       out[n] = acc * 0.125;
     }
   }
+}
+
+__global__ void __launch_bounds__(128) pack_kernel(const double* __restrict__ arena,
+                                                   const double* __restrict__ prev, int V,
+                                                   const PackItem* __restrict__ items,
+                                                   double* __restrict__ slabs) {
+  const PackItem it = items[blockIdx.x];
+  pack_item(arena, prev, V, it, slabs + it.out);
 }
 
 template <int AXIS>
@@ -146,11 +151,10 @@ __device__ __forceinline__ void pull_face(double* __restrict__ arena, int V, int
   }
 }
 
-__global__ void __launch_bounds__(128) pull_kernel(double* __restrict__ arena, int V,
-                                                   const FaceSrc* __restrict__ faces,
-                                                   const int2* __restrict__ items,
-                                                   const double* __restrict__ slabs) {
-  const int2 it = items[blockIdx.x];  // (slot, face = 2*axis + (dir > 0))
+__device__ __forceinline__ void pull_item(double* __restrict__ arena, int V,
+                                          const FaceSrc* __restrict__ faces, int2 it,
+                                          const double* __restrict__ slabs) {
+  // it = (slot, face = 2*axis + (dir > 0))
   const FaceSrc fs = faces[(long long)it.x * 6 + it.y];
   const int axis = it.y >> 1, dir = (it.y & 1) ? 1 : -1;
   if (axis == 0)
@@ -159,6 +163,107 @@ __global__ void __launch_bounds__(128) pull_kernel(double* __restrict__ arena, i
     pull_face<1>(arena, V, it.x, dir, fs, slabs);
   else
     pull_face<2>(arena, V, it.x, dir, fs, slabs);
+}
+
+__global__ void __launch_bounds__(128) pull_kernel(double* __restrict__ arena, int V,
+                                                   const FaceSrc* __restrict__ faces,
+                                                   const int2* __restrict__ items,
+                                                   const double* __restrict__ slabs) {
+  pull_item(arena, V, faces, items[blockIdx.x], slabs);
+}
+
+// ---- peer-memory exchange (PeerTab in halo.h) -------------------------------
+// Flags are monotonic exchange sequence numbers; a wait that does not see its
+// value within kSpinNs traps (loud failure instead of a hung GPU).
+constexpr unsigned long long kSpinNs = 5000000000ull;
+
+__device__ __forceinline__ unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+__device__ void spin_geq(const unsigned long long* p, unsigned long long v) {
+  if (ld_acquire_sys(p) >= v) return;
+  const unsigned long long t0 = globaltimer();
+  while (ld_acquire_sys(p) < v) {
+    __nanosleep(100);
+    if (globaltimer() - t0 > kSpinNs) {
+      printf("tmgpu peer halo: timeout waiting for flag %p >= %llu\n", (const void*)p, v);
+      __trap();
+    }
+  }
+}
+
+// Pack straight into the destination rank's receive region. Items with
+// pad[0] = q + 1 go to peer q: the CTA first waits until q has consumed the
+// previous exchange's slabs (WAR), and the last of q's CTAs raises q's
+// arrival flag after a system-scope fence.
+__global__ void __launch_bounds__(128) pack_peer_kernel(const double* __restrict__ arena,
+                                                        const double* __restrict__ prev, int V,
+                                                        const PackItem* __restrict__ items,
+                                                        double* __restrict__ slabs, PeerTab t,
+                                                        unsigned long long seq) {
+  const PackItem it = items[blockIdx.x];
+  const int q = it.pad[0] - 1;
+  if (q < 0) {
+    pack_item(arena, prev, V, it, slabs + it.out);
+    return;
+  }
+  if (threadIdx.x == 0) spin_geq(t.mine + t.world + q, seq - 1);
+  __syncthreads();
+  pack_item(arena, prev, V, it, t.slabs[q] + it.out);
+  __threadfence_system();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long* cnt = t.mine + 2 * t.world + q;
+    if (atomicAdd(cnt, 1ull) == (unsigned long long)t.n_send[q] - 1) {
+      *cnt = 0;
+      __threadfence_system();
+      st_release_sys(t.flags[q] + t.me, seq);
+    }
+  }
+}
+
+// Pull with items [0, n_local) needing no received slab and [n_local, n) that
+// do: those CTAs wait for every sender's arrival flag; the last of them tells
+// each sender that its slabs are consumed.
+__global__ void __launch_bounds__(128) pull_peer_kernel(double* __restrict__ arena, int V,
+                                                        const FaceSrc* __restrict__ faces,
+                                                        const int2* __restrict__ items,
+                                                        const double* __restrict__ slabs,
+                                                        PeerTab t, int n_local, int n_remote,
+                                                        unsigned long long seq) {
+  const bool remote = (int)blockIdx.x >= n_local;
+  if (remote) {
+    if (threadIdx.x == 0)
+      for (int s = 0; s < t.world; ++s)
+        if (t.recv_mask >> s & 1u) spin_geq(t.mine + s, seq);
+    __syncthreads();
+  }
+  pull_item(arena, V, faces, items[blockIdx.x], slabs);
+  if (!remote) return;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long* cnt = t.mine + 3 * t.world;
+    if (atomicAdd(cnt, 1ull) == (unsigned long long)n_remote - 1) {
+      *cnt = 0;
+      __threadfence_system();
+      for (int s = 0; s < t.world; ++s)
+        if (t.recv_mask >> s & 1u) st_release_sys(t.flags[s] + t.world + t.me, seq);
+    }
+  }
 }
 
 }  // namespace
@@ -175,6 +280,25 @@ cudaError_t halo_pull(double* arena, int V, const FaceSrc* faces, const int2* it
                       const double* slabs, cudaStream_t st) {
   if (n_items <= 0) return cudaSuccess;
   pull_kernel<<<n_items, 128, 0, st>>>(arena, V, faces, items, slabs);
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return cudaGetLastError();
+}
+
+cudaError_t halo_pack_peer(const double* arena, const double* prev, int V, const PackItem* items,
+                           int n_items, double* slabs, const PeerTab& t, unsigned long long seq,
+                           cudaStream_t st) {
+  if (n_items <= 0) return cudaSuccess;
+  pack_peer_kernel<<<n_items, 128, 0, st>>>(arena, prev, V, items, slabs, t, seq);
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return cudaGetLastError();
+}
+
+cudaError_t halo_pull_peer(double* arena, int V, const FaceSrc* faces, const int2* items,
+                           int n_local, int n_items, const double* slabs, const PeerTab& t,
+                           unsigned long long seq, cudaStream_t st) {
+  if (n_items <= 0) return cudaSuccess;
+  pull_peer_kernel<<<n_items, 128, 0, st>>>(arena, V, faces, items, slabs, t, n_local,
+                                            n_items - n_local, seq);
   g_launches.fetch_add(1, std::memory_order_relaxed);
   return cudaGetLastError();
 }

@@ -26,7 +26,7 @@ struct alignas(16) PackItem {
   int32_t src;  // local slot of the source leaf
   int32_t out;  // offset (doubles) into the slab buffer
   int8_t kind, axis, dir, qt1, qt2;
-  int8_t pad[3];
+  int8_t pad[3];  // peer exchange: pad[0] = destination rank + 1 (0 = this rank)
 };
 
 // Where a destination face gets its ghosts. kind as NeighborKind (0 same,
@@ -42,6 +42,28 @@ struct alignas(16) FaceSrc {
 
 // Slab sizes in doubles per kind (V vars).
 inline int slab_doubles(int kind, int V) { return kind == 2 ? V * 2 * 4 * 4 : V * 2 * 8 * 8; }
+
+// Peer-memory exchange (opt-in, tmgpu_forest_set_peer): senders pack straight
+// into the receivers' slab buffers (CUDA IPC over NVLink/NVSwitch) and
+// synchronise through flag words instead of NCCL send/recv.
+constexpr int kMaxPeers = 8;
+struct PeerTab {
+  double* slabs[kMaxPeers];               // peers' slab buffers (IPC-mapped; [me] unused)
+  unsigned long long* flags[kMaxPeers];   // peers' flag words
+  // this rank's flag words: [0,w) arrival seq from sender s, [w,2w) consumption
+  // seq by receiver q, [2w,3w) per-peer pack CTA counters, [3w] pull counter
+  unsigned long long* mine;
+  int n_send[kMaxPeers];                  // pack items (CTAs) per destination peer
+  int me, world;
+  unsigned recv_mask;                     // peers this rank receives slabs from
+};
+
+cudaError_t halo_pack_peer(const double* arena, const double* prev, int V, const PackItem* items,
+                           int n_items, double* slabs, const PeerTab& t, unsigned long long seq,
+                           cudaStream_t st);
+cudaError_t halo_pull_peer(double* arena, int V, const FaceSrc* faces, const int2* items,
+                           int n_local, int n_items, const double* slabs, const PeerTab& t,
+                           unsigned long long seq, cudaStream_t st);
 
 cudaError_t halo_pack(const double* arena, const double* prev, int V, const PackItem* items,
                       int n_items, double* slabs, cudaStream_t st);

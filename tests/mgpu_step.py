@@ -22,7 +22,8 @@ def main():
     torch.cuda.set_device(local)
     tdist.init_process_group("nccl", device_id=torch.device("cuda", local))
     gravity = "--gravity" in sys.argv
-    args = [a for a in sys.argv[1:] if a != "--gravity"]
+    peer = "--peer" in sys.argv
+    args = [a for a in sys.argv[1:] if a not in ("--gravity", "--peer")]
     Drv = GravityHydroDriver if gravity else HydroDriver
     kind, lo, hi = amr.Scenario.rotating_star, 2, 4
     f = amr.build_scenario(kind, lo, hi)
@@ -31,6 +32,8 @@ def main():
     comm = dist.Comm.from_torch()
     f.distribute(comm, owner)
     f.alloc()
+    if peer:
+        f.set_peer(True)
     a, b = dist.local_range(owner, rank)
     f.set_interior(np.ascontiguousarray(state[a:b]))
     drv = Drv(f)

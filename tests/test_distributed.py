@@ -112,3 +112,23 @@ def test_partitioned_gravity_hydro_step_bitwise_equals_single_gpu():
                         "29532", script, "--gravity"], capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     assert "BITWISE_OK" in r.stdout, r.stdout[-3000:]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("gravity", [False, True])
+def test_peer_halo_step_bitwise_equals_single_gpu(gravity):
+    """Ghost slabs stored straight into the peers' buffers (CUDA IPC, flag-word
+    sync) instead of NCCL send/recv: same bits as one GPU."""
+    import torch
+
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs 2 GPUs (gpurun --gpus 2)")
+    script = os.path.join(ROOT, "tests", "mgpu_step.py")
+    n = min(torch.cuda.device_count(), 4)
+    extra = ["--peer"] + (["--gravity"] if gravity else [])
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+                        f"--nproc-per-node={n}", "--master-addr", "127.0.0.1", "--master-port",
+                        str(29533 + int(gravity)), script] + extra, capture_output=True, text=True,
+                       timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    assert "BITWISE_OK" in r.stdout, r.stdout[-3000:]
