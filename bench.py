@@ -422,6 +422,12 @@ def run_ours(args, rank, world):
             "concurrently with the CFL reduction and the first ghost exchange, whose interval "
             "includes the wait for it, so the shares overlap")
     roofline["gravity_work"] = work or None
+    if dist:  # per-rank phase times (ms per step, device events): the load balance
+        mine = {"cfl": cfl_ms, "exchange": 3 * exch_ms, "stage": 3 * stage_ms,
+                **{"gravity_" + k: v for k, v in grav_ms.items()}}
+        ranks = [None] * world
+        dist.all_gather_object(ranks, {k: round(v, 4) for k, v in mine.items()})
+        roofline["phase_ms_by_rank"] = ranks
 
     # e2e through the public API with host buffers (pinned): every step moves
     # its whole input H2D and its whole result D2H; HostStepPipeline overlaps

@@ -258,6 +258,11 @@ int tmgpu_gravity_amr_work(const tmgpu_gravity_amr* G, long long* out);
  * slot; results equal the one-GPU solve bitwise */
 int tmgpu_gravity_amr_distribute(tmgpu_gravity_amr* G, tmgpu_comm* comm, const long long* slot_bounds,
                                  tmgpu_error* err);
+/* multi-GPU moment exchange over peer memory (collective; 2..8 ranks of one node, CUDA IPC):
+ * subtree roots and halo patches are stored straight into the peers' moment arrays with
+ * flag-word synchronisation (a wait that does not complete within 5 s traps) instead of the
+ * NCCL all-gather + send/recv. Re-call after tmgpu_gravity_amr_distribute; on = 0 returns to NCCL. */
+int tmgpu_gravity_amr_set_peer(tmgpu_gravity_amr* G, int on, tmgpu_error* err);
 /* host-only: per-level counts of the patches a rank owning slots [lo, hi) evaluates
  * M2L/L2L for; returns the level count (negative error code on failure) */
 int tmgpu_gravity_amr_plan_need(const int* leaves, long long nleaves, long long lo, long long hi,
@@ -268,7 +273,8 @@ int tmgpu_gravity_amr_plan_need(const int* leaves, long long nleaves, long long 
 int tmgpu_gravity_amr_let_plan(const int* leaves, long long nleaves, const long long* bounds, int world,
                                int me, long long* out, long long* send, long long* recv,
                                long long* send_hash, long long* recv_hash, tmgpu_error* err);
-/* per-phase device timing: totals in ms of [comm, up, m2l, l2l, l2p, am] */
+/* per-phase device timing: totals in ms of [up (P2M + owned-subtree M2M), let (subtree-root
+ * all-gather, shared-top M2M, halo-moment exchange; the top on one GPU), m2l, l2l, l2p, am] */
 int tmgpu_gravity_amr_set_timing(tmgpu_gravity_amr* G, int on);
 int tmgpu_gravity_amr_timing(tmgpu_gravity_amr* G, double* ms, long long* solves);
 const double* tmgpu_gravity_amr_mass_ptr(const tmgpu_gravity_amr* G);

@@ -277,6 +277,7 @@ class Forest:
         IPC over NVLink) instead of NCCL send/recv; re-call after alloc()."""
         err = TmgpuError()
         _lib.check(lib.tmgpu_forest_set_peer(self.h, 1 if on else 0, C.byref(err)), err)
+        self._peer = bool(on)
 
     def arena_ptr(self) -> int:
         return int(lib.tmgpu_forest_arena(self.h) or 0)

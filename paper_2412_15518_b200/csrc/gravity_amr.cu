@@ -32,6 +32,7 @@
 #include "comm.h"
 #include "gravity_amr_plan.h"
 #include "gravity_common.cuh"
+#include "peer.cuh"
 
 namespace tmgpu {
 
@@ -866,10 +867,20 @@ void count_work(const GravPlan& P, const std::vector<std::vector<int>>* need, lo
   out[6] = wxleaf;
 }
 
+constexpr int kMaxLetPeers = 8;
+
 // per-phase device timing of solves (bench): events at the phase boundaries
-constexpr int kGravPhases = 6;  // comm (unused since the LET: 0), up (incl. moment exchange), m2l, l2l, l2p, am
+constexpr int kGravPhases = 6;  // up (P2M + owned M2M), let (moment exchange + top), m2l, l2l, l2p, am
 struct GravTimingRec {
   cudaEvent_t ev[kGravPhases + 1];
+};
+
+struct LetPeer {
+  unsigned long long* flags[kMaxLetPeers];  // peers' flag words (IPC-mapped)
+  unsigned long long* mine;                 // this rank's flag words (GravAmrWork::pflags)
+  int n_push[kMaxLetPeers];                 // push CTAs per destination
+  int me, world, nl;
+  unsigned recv_mask;                       // ranks that store patches into this one
 };
 
 struct GravAmrWork {
@@ -932,7 +943,75 @@ struct GravAmrWork {
   double* u_geo = nullptr;   // [distinct cross-depth U separations][4]
   cudaStream_t side = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  // peer-memory LET exchange (tmgpu_gravity_amr_set_peer): subtree roots and
+  // halo patches stored straight into the peers' level moment arrays
+  bool peer = false;
+  unsigned long long peer_seq = 0;
+  LetPeer pt{};
+  unsigned long long* pflags = nullptr;  // [0,R) arrival, [R,2R) consumption, [2R,3R) push counters
+  int4* push = nullptr;                  // (level, node, destination rank) per CTA
+  long long n_push = 0;
+  double** peer_mom = nullptr;           // [R][nlevels] peers' moment arrays
+  std::vector<void*> peer_opened;
 };
+
+// Peer LET exchange: one CTA per (patch, destination) copies the patch's 512
+// cells x 10 moments into the destination's moment array at the same (level,
+// node) — after the destination has consumed the previous solve's patches —
+// and the last CTA for a destination raises its arrival flag.
+__global__ void __launch_bounds__(256) let_push_kernel(const GLv* __restrict__ Lv,
+                                                       const int4* __restrict__ items,
+                                                       double* const* __restrict__ peer_mom, LetPeer t,
+                                                       unsigned long long seq) {
+  const int4 it = items[blockIdx.x];
+  const int q = it.z;
+  if (threadIdx.x == 0) spin_geq(t.mine + t.world + q, seq - 1);
+  __syncthreads();
+  const double2* src = reinterpret_cast<const double2*>(Lv[it.x].mom + (long long)it.y * 5120);
+  double2* dst = reinterpret_cast<double2*>(peer_mom[q * t.nl + it.x] + (long long)it.y * 5120);
+  for (int k = threadIdx.x; k < 2560; k += blockDim.x) dst[k] = src[k];
+  __threadfence_system();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long* cnt = t.mine + 2 * t.world + q;
+    if (atomicAdd(cnt, 1ull) == (unsigned long long)t.n_push[q] - 1) {
+      *cnt = 0;
+      __threadfence_system();
+      st_release_sys(t.flags[q] + t.me, seq);
+    }
+  }
+}
+
+__global__ void let_wait_kernel(LetPeer t, unsigned long long seq) {
+  if (threadIdx.x == 0)
+    for (int s = 0; s < t.world; ++s)
+      if (t.recv_mask >> s & 1u) spin_geq(t.mine + s, seq);
+}
+
+// after the solve's last reader of received patches (L2P)
+__global__ void let_done_kernel(LetPeer t, unsigned long long seq) {
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    for (int s = 0; s < t.world; ++s)
+      if (t.recv_mask >> s & 1u) st_release_sys(t.flags[s] + t.world + t.me, seq);
+  }
+}
+
+static void let_peer_close(GravAmrWork& w) {
+  if (w.pflags || w.peer) cudaDeviceSynchronize();
+  for (void* p : w.peer_opened)
+    if (p) cudaIpcCloseMemHandle(p);
+  w.peer_opened.clear();
+  for (void* p : {(void*)w.pflags, (void*)w.push, (void*)w.peer_mom})
+    if (p) cudaFree(p);
+  w.pflags = nullptr;
+  w.push = nullptr;
+  w.peer_mom = nullptr;
+  w.n_push = 0;
+  w.pt = LetPeer{};
+  w.peer = false;
+  w.peer_seq = 0;
+}
 
 // Distributed: base[slot * per_slot ..] of every rank's slot range to every
 // rank — one ncclAllGather of the padded per-rank segments through the
@@ -1099,6 +1178,7 @@ void tmgpu_gravity_amr_destroy(tmgpu_gravity_amr* G) {
   if (G->w.ev_fork) cudaEventDestroy(G->w.ev_fork);
   if (G->w.ev_join) cudaEventDestroy(G->w.ev_join);
   if (G->w.side) cudaStreamDestroy(G->w.side);
+  let_peer_close(G->w);
   for (void* p : G->w.allocs)
     if (p) cudaFree(p);
   delete G;
@@ -1339,7 +1419,6 @@ int tmgpu_gravity_amr_solve(tmgpu_gravity_amr* G, const double* mass, double* ph
     cudaEventRecord(rec.ev[0], st);
   }
   int rc = TMGPU_OK;
-  if (timed) cudaEventRecord(rec.ev[1], st);
   if (e == cudaSuccess && rc == TMGPU_OK) {
     long long launches = 0;
     if (nloc)
@@ -1353,7 +1432,26 @@ int tmgpu_gravity_amr_solve(tmgpu_gravity_amr* G, const double* mass, double* ph
                                                          ni);
       ++launches;
     }
-    if (w.let) {
+    if (timed) cudaEventRecord(rec.ev[1], st);
+    if (w.peer) {
+      // roots to every peer and halo patches to their readers, straight into
+      // the peers' moment arrays; then the shared top as below
+      const unsigned long long seq = ++w.peer_seq;
+      if (w.n_push)
+        let_push_kernel<<<(unsigned)w.n_push, 256, 0, st>>>(w.dev_lv, w.push, w.peer_mom, w.pt, seq);
+      let_wait_kernel<<<1, 32, 0, st>>>(w.pt, seq);
+      launches += 2;
+      for (int l = P.nlevels - 2; l >= 0; --l) {
+        if (!w.n_top[l]) continue;
+        amr_m2m_kernel<<<grid_for(w.n_top[l] * 512), 128, 0, st>>>(w.dev_lv, l, w.let_top[l], w.n_top[l]);
+        ++launches;
+      }
+      if (w.n_halo_slots) {
+        halo_mass_kernel<<<grid_for(w.n_halo_slots * 512), 128, 0, st>>>(
+            w.dev_lv, w.halo_slots, w.n_halo_slots, w.slot_level, w.slot_node, w.mass);
+        ++launches;
+      }
+    } else if (w.let) {
       // LET moment exchange: subtree roots to everyone, the shared top by M2M,
       // then the owned patches other ranks read, point to point
       if (w.n_my_roots)
@@ -1420,6 +1518,10 @@ int tmgpu_gravity_amr_solve(tmgpu_gravity_amr* G, const double* mass, double* ph
                                                      w.mass, w.u_geo, w.lloc, w.p2p_tab, w.slot_nbs, dphi, dg,
                                                      am ? w.part : nullptr);
     ++launches;
+    if (w.peer) {  // every received patch has been read (M2L, W/X, top M2M, L2P)
+      let_done_kernel<<<1, 32, 0, st>>>(w.pt, w.peer_seq);
+      ++launches;
+    }
     if (timed) cudaEventRecord(rec.ev[5], st);
     if (am) {  // the per-slot sums came with L2P
       if (w.comm && e == cudaSuccess)  // identical global pair tree on every rank
@@ -1482,6 +1584,7 @@ int tmgpu_gravity_amr_distribute(tmgpu_gravity_amr* G, tmgpu_comm* comm, const l
   for (int r = 0; r < R; ++r)
     if (slot_bounds[r + 1] < slot_bounds[r])
       return set_err(err, TMGPU_ERR_INVALID, "gravity distribute: slot bounds not ascending");
+  let_peer_close(w);  // a new distribution needs a new tmgpu_gravity_amr_set_peer
   w.comm = comm;
   w.lo = slot_bounds[me];
   w.hi = slot_bounds[me + 1];
@@ -1520,6 +1623,97 @@ int tmgpu_gravity_amr_distribute(tmgpu_gravity_amr* G, tmgpu_comm* comm, const l
   if (e == cudaSuccess) e = build_let(w, std::vector<long long>(slot_bounds, slot_bounds + R + 1), me);
   count_work(P, &lists, w.lo, w.hi, w.work);  // this GPU's share (bench roofline)
   return cuda_err(err, e, "tmgpu_gravity_amr_distribute");
+}
+
+// Peer-memory LET moment exchange (collective over the solver's communicator):
+// exports every level's moment array and the flag words by CUDA IPC and
+// replaces the root all-gather + halo send/recv with let_push_kernel. on = 0
+// returns to NCCL. Re-call after tmgpu_gravity_amr_distribute.
+int tmgpu_gravity_amr_set_peer(tmgpu_gravity_amr* G, int on, tmgpu_error* err) {
+  if (err) std::memset(err, 0, sizeof(*err));
+  if (!G) return set_err(err, TMGPU_ERR_INVALID, "null gravity solver");
+  GravAmrWork& w = G->w;
+  let_peer_close(w);
+  if (!on) return TMGPU_OK;
+  if (!w.let || !w.comm) return set_err(err, TMGPU_ERR_INVALID, "gravity peer exchange: call distribute first");
+  const GravPlan& P = w.plan;
+  const int R = comm_world(w.comm), me = comm_rank(w.comm), nl = P.nlevels;
+  if (R < 2 || R > kMaxLetPeers)
+    return set_err(err, TMGPU_ERR_INVALID, "gravity peer exchange supports 2..8 ranks");
+  std::vector<long long> bounds(R + 1);
+  for (int r = 0; r < R; ++r) bounds[r] = w.seg_lo[r];
+  bounds[R] = w.seg_lo[R - 1] + w.seg_cnt[R - 1];
+  const GravLetPlan L = grav_let_plan(P, bounds, me);
+  cudaError_t e = cudaMalloc((void**)&w.pflags, 3 * R * sizeof(unsigned long long));
+  if (e == cudaSuccess) e = cudaMemset(w.pflags, 0, 3 * R * sizeof(unsigned long long));
+  // per rank: flag handle, then one moment-array handle per level (8 doubles each)
+  const int rec_n = 8 * (1 + nl);
+  std::vector<double> rec(rec_n, 0.0), all((size_t)rec_n * R, 0.0);
+  cudaIpcMemHandle_t h{};
+  if (e == cudaSuccess) e = cudaIpcGetMemHandle(&h, w.pflags);
+  std::memcpy(&rec[0], &h, 64);
+  for (int l = 0; l < nl && e == cudaSuccess; ++l) {
+    e = cudaIpcGetMemHandle(&h, w.host_lv[l].mom);
+    std::memcpy(&rec[8 * (1 + l)], &h, 64);
+  }
+  double* dbuf = nullptr;
+  if (e == cudaSuccess) e = cudaMalloc((void**)&dbuf, sizeof(double) * rec_n * (R + 1));
+  if (e == cudaSuccess) e = cudaMemcpy(dbuf, rec.data(), sizeof(double) * rec_n, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  std::string why;
+  int rc = TMGPU_OK;
+  if (e == cudaSuccess) {
+    rc = comm_allgather(w.comm, dbuf, dbuf + rec_n, rec_n, nullptr, &why);
+    if (rc == TMGPU_OK)
+      e = cudaMemcpy(all.data(), dbuf + rec_n, sizeof(double) * rec_n * R, cudaMemcpyDeviceToHost);
+  }
+  if (dbuf) cudaFree(dbuf);
+  LetPeer t{};
+  t.mine = w.pflags;
+  t.me = me;
+  t.world = R;
+  t.nl = nl;
+  std::vector<double*> pm((size_t)R * nl, nullptr);
+  for (int q = 0; q < R && e == cudaSuccess && rc == TMGPU_OK; ++q) {
+    if (q == me) continue;
+    if (!L.roots[q].empty() || !L.recv[q].empty()) t.recv_mask |= 1u << q;
+    for (int k = 0; k <= nl && e == cudaSuccess; ++k) {
+      std::memcpy(&h, &all[(size_t)q * rec_n + 8 * k], 64);
+      void* p = nullptr;
+      e = cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess);
+      if (e != cudaSuccess) break;
+      w.peer_opened.push_back(p);
+      if (k == 0)
+        t.flags[q] = static_cast<unsigned long long*>(p);
+      else
+        pm[(size_t)q * nl + (k - 1)] = static_cast<double*>(p);
+    }
+  }
+  std::vector<int4> items;
+  for (int q = 0; q < R; ++q) {
+    if (q == me) continue;
+    for (const PatchRef& r : L.roots[me]) items.push_back(make_int4(r.level, r.node, q, 0));
+    for (const PatchRef& r : L.send[q]) items.push_back(make_int4(r.level, r.node, q, 0));
+    t.n_push[q] = (int)(L.roots[me].size() + L.send[q].size());
+  }
+  w.n_push = (long long)items.size();
+  if (e == cudaSuccess && rc == TMGPU_OK) e = upload(items, &w.push);
+  if (e == cudaSuccess && rc == TMGPU_OK) e = upload(pm, &w.peer_mom);
+  if (e == cudaSuccess && rc == TMGPU_OK) e = cudaDeviceSynchronize();
+  // every rank has zeroed its flags and mapped its peers before anyone pushes
+  if (e == cudaSuccess && rc == TMGPU_OK) {
+    e = cudaMalloc((void**)&dbuf, sizeof(double) * (R + 1));
+    if (e == cudaSuccess) rc = comm_allgather(w.comm, dbuf, dbuf + 1, 1, nullptr, &why);
+    if (e == cudaSuccess && rc == TMGPU_OK) e = cudaDeviceSynchronize();
+    if (dbuf) cudaFree(dbuf);
+  }
+  if (e != cudaSuccess || rc != TMGPU_OK) {
+    let_peer_close(w);
+    return e != cudaSuccess ? cuda_err(err, e, "tmgpu_gravity_amr_set_peer") : set_err(err, rc, why.c_str());
+  }
+  w.pt = t;
+  w.peer = true;
+  return TMGPU_OK;
 }
 
 // AM-correction sums of the last solve with TMGPU_GRAV_AM: out[0..2] centre of

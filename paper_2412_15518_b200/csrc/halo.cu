@@ -1,5 +1,6 @@
 // Pack / pull kernels of the one-round face exchange (see halo.h).
 #include "halo.h"
+#include "peer.cuh"
 #include "tmgpu_internal.h"
 
 namespace tmgpu {
@@ -172,38 +173,7 @@ __global__ void __launch_bounds__(128) pull_kernel(double* __restrict__ arena, i
   pull_item(arena, V, faces, items[blockIdx.x], slabs);
 }
 
-// ---- peer-memory exchange (PeerTab in halo.h) -------------------------------
-// Flags are monotonic exchange sequence numbers; a wait that does not see its
-// value within kSpinNs traps (loud failure instead of a hung GPU).
-constexpr unsigned long long kSpinNs = 5000000000ull;
-
-__device__ __forceinline__ unsigned long long globaltimer() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-  return t;
-}
-
-__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
-  unsigned long long v;
-  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-  return v;
-}
-
-__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
-  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-
-__device__ void spin_geq(const unsigned long long* p, unsigned long long v) {
-  if (ld_acquire_sys(p) >= v) return;
-  const unsigned long long t0 = globaltimer();
-  while (ld_acquire_sys(p) < v) {
-    __nanosleep(100);
-    if (globaltimer() - t0 > kSpinNs) {
-      printf("tmgpu peer halo: timeout waiting for flag %p >= %llu\n", (const void*)p, v);
-      __trap();
-    }
-  }
-}
+// ---- peer-memory exchange (PeerTab in halo.h; flag helpers in peer.cuh) ---
 
 // Pack straight into the destination rank's receive region. Items with
 // pad[0] = q + 1 go to peer q: the CTA first waits until q has consumed the

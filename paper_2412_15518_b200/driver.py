@@ -103,6 +103,8 @@ class GravityHydroDriver(HydroDriver):
 
             self.gcomm = Comm.from_torch()
             self.gravity.distribute(self.gcomm, forest._owner)
+            if getattr(forest, "_peer", False):  # the forest's halo is over peer memory
+                self.gravity.set_peer(True)
         # the solve runs on a side stream, overlapped with the CFL reduction and
         # the first ghost exchange (multi-GPU: also the latency-bound moment
         # exchange); the first stage kernel waits for it. TMGPU_GRAVITY_OVERLAP=0

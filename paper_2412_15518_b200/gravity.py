@@ -115,6 +115,8 @@ lib.tmgpu_gravity_amr_timing.restype = C.c_int
 lib.tmgpu_gravity_amr_timing.argtypes = [_vp, C.POINTER(C.c_double), _lp]
 lib.tmgpu_gravity_amr_distribute.restype = C.c_int
 lib.tmgpu_gravity_amr_distribute.argtypes = [_vp, _vp, _lp, _ep]
+lib.tmgpu_gravity_amr_set_peer.restype = C.c_int
+lib.tmgpu_gravity_amr_set_peer.argtypes = [_vp, C.c_int, _ep]
 lib.tmgpu_gravity_amr_mass_ptr.restype = _vp
 lib.tmgpu_gravity_amr_mass_ptr.argtypes = [_vp]
 
@@ -257,6 +259,13 @@ class GravityAMR:
         _lib.check(lib.tmgpu_gravity_amr_distribute(self.h, comm.h, bounds.ctypes.data_as(_lp),
                                                     C.byref(err)), err)
 
+    def set_peer(self, on: bool = True) -> None:
+        """Collective (after distribute): the moment exchange stores the subtree
+        roots and halo patches straight into the peers' moment arrays (CUDA IPC
+        over NVLink) instead of NCCL all-gather + send/recv; same bits."""
+        err = TmgpuError()
+        _lib.check(lib.tmgpu_gravity_amr_set_peer(self.h, 1 if on else 0, C.byref(err)), err)
+
     def local_cells(self) -> int:
         return (getattr(self, "hi", self.n) - getattr(self, "lo", 0)) * 512
 
@@ -271,7 +280,7 @@ class GravityAMR:
     def set_timing(self, on: bool) -> None:
         lib.tmgpu_gravity_amr_set_timing(self.h, int(on))
 
-    PHASES = ("comm", "up", "m2l", "l2l", "l2p", "am")
+    PHASES = ("up", "let", "m2l", "l2l", "l2p", "am")
 
     def timing(self):
         """(ms totals per phase, solves timed) since set_timing(True)."""
