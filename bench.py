@@ -307,8 +307,13 @@ def run_ours(args, rank, world):
         lo, hi = tmdist.local_range(owner, rank)
         state = np.ascontiguousarray(state[lo:hi])
     f.alloc()
+    halo = "nccl"
     if world > 1 and args.halo == "peer":
-        f.set_peer(True)
+        try:  # collective; every rank agrees on the outcome
+            f.set_peer(True)
+            halo = "peer"
+        except Exception as ex:  # noqa: BLE001 - reported in the JSON line
+            halo = f"nccl (peer setup failed: {ex})"
     f.set_interior(state)
     local_cells = f.local_count() * 512
     gravity = not args.hydro_only
@@ -466,12 +471,16 @@ def run_ours(args, rank, world):
                 "parallelism": (f"leaves partitioned over {world} GPUs (partition_leaves, "
                                 "contiguous Morton ranges); cross-GPU ghost slabs " +
                                 ("packed straight into the receivers' buffers over NVLink (CUDA "
-                                 "IPC peer memory, flag-word sync)" if args.halo == "peer" else
-                                 "by grouped NCCL send/recv") + " per RK stage; dt by "
+                                 "IPC peer memory, flag-word sync)" if halo == "peer" else
+                                 "by grouped NCCL send/recv" + halo[4:]) + " per RK stage; dt by "
                                 "ncclAllReduce(min)" +
                                 ("; gravity: locally essential tree — owned-subtree upward pass, "
-                                 "subtree-root moments all-gathered, halo moments by grouped NCCL "
-                                 "send/recv, M2L/L2L/L2P on the owned subtree, solve overlapped "
+                                 "subtree-root and halo moments " +
+                                 ("stored straight into the peers' moment arrays (CUDA IPC)"
+                                  if getattr(drv, "moment_transport", "") == "peer" else
+                                  "by NCCL all-gather + grouped send/recv " +
+                                  getattr(drv, "moment_transport", "nccl")[4:]) +
+                                 ", M2L/L2L/L2P on the owned subtree, solve overlapped "
                                  "with the CFL reduction and first ghost exchange" if gravity else ""))
                 if world > 1 else "single GPU"}),
             "e2e": {"value": cells / (e2e_ms * 1e-3), "unit": UNIT,

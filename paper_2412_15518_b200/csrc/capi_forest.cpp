@@ -866,11 +866,28 @@ int tmgpu_forest_set_peer(tmgpu_forest* f, int on, tmgpu_error* err) {
   if (world < 2) return fail(err, TMGPU_ERR_INVALID, "peer exchange needs a communicator with 2+ ranks");
   if (world > kMaxPeers) return fail(err, TMGPU_ERR_INVALID, "peer exchange supports up to 8 ranks");
   const HaloPlan& P = f->plan;
-  cudaError_t e = cudaMalloc((void**)&f->peer_flags, (3 * world + 1) * sizeof(unsigned long long));
-  if (e == cudaSuccess) e = cudaMemset(f->peer_flags, 0, (3 * world + 1) * sizeof(unsigned long long));
-  // per rank: slab handle, flag handle (8 doubles each), recv_base, recv_off[world]
-  constexpr int kRec = 32;
+  // per rank: slab handle, flag handle (8 doubles each), recv_base, recv_off[world], status
+  constexpr int kRec = 32, kOk = kRec - 1;
   std::vector<double> rec(kRec, 0.0), all((size_t)kRec * world, 0.0);
+  double* dbuf = nullptr;
+  cudaError_t e = cudaMalloc((void**)&dbuf, sizeof(double) * kRec * (world + 1));
+  if (e != cudaSuccess) return cuda_err(err, e, "tmgpu_forest_set_peer");
+  // every rank takes part in both all-gathers whatever fails locally, and all
+  // ranks agree on the outcome (a one-sided peer mode would deadlock)
+  auto agree = [&](bool ok, double* out, std::string* why) {
+    rec[kOk] = ok ? 1.0 : 0.0;
+    cudaError_t ce = cudaMemcpy(dbuf, rec.data(), sizeof(double) * kRec, cudaMemcpyHostToDevice);
+    if (ce == cudaSuccess) ce = cudaDeviceSynchronize();
+    int rc = ce == cudaSuccess ? comm_allgather(f->comm, dbuf, dbuf + kRec, kRec, nullptr, why) : TMGPU_ERR_CUDA;
+    if (rc == TMGPU_OK)
+      ce = cudaMemcpy(out, dbuf + kRec, sizeof(double) * kRec * world, cudaMemcpyDeviceToHost);
+    if (rc != TMGPU_OK || ce != cudaSuccess) return false;
+    for (int q = 0; q < world; ++q)
+      if (out[(size_t)q * kRec + kOk] != 1.0) return false;
+    return true;
+  };
+  e = cudaMalloc((void**)&f->peer_flags, (3 * world + 1) * sizeof(unsigned long long));
+  if (e == cudaSuccess) e = cudaMemset(f->peer_flags, 0, (3 * world + 1) * sizeof(unsigned long long));
   cudaIpcMemHandle_t hs{}, hf{};
   if (e == cudaSuccess) e = cudaIpcGetMemHandle(&hs, f->slabs);
   if (e == cudaSuccess) e = cudaIpcGetMemHandle(&hf, f->peer_flags);
@@ -879,33 +896,13 @@ int tmgpu_forest_set_peer(tmgpu_forest* f, int on, tmgpu_error* err) {
   std::memcpy(&rec[8], &hf, 64);
   rec[16] = (double)P.recv_base;
   for (int p = 0; p < world; ++p) rec[17 + p] = (double)P.recv_off[p];
-  double* dbuf = nullptr;
-  if (e == cudaSuccess) e = cudaMalloc((void**)&dbuf, sizeof(double) * kRec * (world + 1));
-  if (e == cudaSuccess) e = cudaMemcpy(dbuf, rec.data(), sizeof(double) * kRec, cudaMemcpyHostToDevice);
-  if (e == cudaSuccess) e = cudaDeviceSynchronize();
-  if (e != cudaSuccess) {
-    if (dbuf) cudaFree(dbuf);
-    peer_close(f);
-    return cuda_err(err, e, "tmgpu_forest_set_peer");
-  }
-  std::string why;
-  int rc = comm_allgather(f->comm, dbuf, dbuf + kRec, kRec, nullptr, &why);
-  if (rc == TMGPU_OK) {
-    e = cudaMemcpy(all.data(), dbuf + kRec, sizeof(double) * kRec * world, cudaMemcpyDeviceToHost);
-    if (e != cudaSuccess) rc = cuda_err(err, e, "tmgpu_forest_set_peer");
-  } else {
-    fail(err, rc, why);
-  }
-  cudaFree(dbuf);
-  if (rc != TMGPU_OK) {
-    peer_close(f);
-    return rc;
-  }
+  std::string why = "peer exchange: setup failed on a rank";
+  bool ok = agree(e == cudaSuccess, all.data(), &why);
   PeerTab t{};
   t.mine = f->peer_flags;
   t.me = me;
   t.world = world;
-  for (int q = 0; q < world && e == cudaSuccess; ++q) {
+  for (int q = 0; q < world && ok && e == cudaSuccess; ++q) {
     if (q == me) continue;
     if (P.recv_cnt[q] > 0) t.recv_mask |= 1u << q;
     cudaIpcMemHandle_t h;
@@ -917,43 +914,39 @@ int tmgpu_forest_set_peer(tmgpu_forest* f, int on, tmgpu_error* err) {
     t.slabs[q] = static_cast<double*>(f->peer_opened[2 * q]);
     t.flags[q] = static_cast<unsigned long long*>(f->peer_opened[2 * q + 1]);
   }
-  // cross-rank items: local prolonged first, then by destination rank; the
-  // offset becomes the receiver's (recv_base + recv_off[me] + position)
-  std::vector<PackItem> items;
-  items.reserve(P.pack.size());
-  for (const PackItem& it : P.pack)
-    if (it.out < P.send_base) items.push_back(it);
-  for (int q = 0; q < world; ++q) {
-    if (q == me) continue;
-    const long long lo = P.send_base + P.send_off[q], hi = lo + P.send_cnt[q];
-    const long long dst = (long long)all[(size_t)q * kRec + 16] + (long long)all[(size_t)q * kRec + 17 + me];
-    for (PackItem it : P.pack)
-      if (it.out >= lo && it.out < hi) {
-        it.out = (int32_t)(dst + (it.out - lo));
-        it.pad[0] = (int8_t)(q + 1);
-        items.push_back(it);
-        t.n_send[q] += 1;
-      }
+  if (ok) {
+    // cross-rank items: local prolonged first, then by destination rank; the
+    // offset becomes the receiver's (recv_base + recv_off[me] + position)
+    std::vector<PackItem> items;
+    items.reserve(P.pack.size());
+    for (const PackItem& it : P.pack)
+      if (it.out < P.send_base) items.push_back(it);
+    for (int q = 0; q < world; ++q) {
+      if (q == me) continue;
+      const long long lo = P.send_base + P.send_off[q], hi = lo + P.send_cnt[q];
+      const long long dst = (long long)all[(size_t)q * kRec + 16] + (long long)all[(size_t)q * kRec + 17 + me];
+      for (PackItem it : P.pack)
+        if (it.out >= lo && it.out < hi) {
+          it.out = (int32_t)(dst + (it.out - lo));
+          it.pad[0] = (int8_t)(q + 1);
+          items.push_back(it);
+          t.n_send[q] += 1;
+        }
+    }
+    if (e == cudaSuccess && items.size() != P.pack.size()) e = cudaErrorInvalidValue;
+    std::vector<int> pulls = P.pull_fused_local;
+    pulls.insert(pulls.end(), P.pull_fused_remote.begin(), P.pull_fused_remote.end());
+    e = upload(&f->pack_peer, items, e);
+    e = upload((int**)&f->pull_peer, pulls, e);
+    if (e == cudaSuccess) e = cudaDeviceSynchronize();
+    // every rank has zeroed its flags and mapped its peers before anyone signals
+    std::vector<double> all2((size_t)kRec * world);
+    ok = agree(e == cudaSuccess, all2.data(), &why);
   }
-  if (e == cudaSuccess && items.size() != P.pack.size()) e = cudaErrorInvalidValue;
-  std::vector<int> pulls = P.pull_fused_local;
-  pulls.insert(pulls.end(), P.pull_fused_remote.begin(), P.pull_fused_remote.end());
-  e = upload(&f->pack_peer, items, e);
-  e = upload((int**)&f->pull_peer, pulls, e);
-  if (e == cudaSuccess) e = cudaDeviceSynchronize();
-  if (e != cudaSuccess) {
+  cudaFree(dbuf);
+  if (!ok) {
     peer_close(f);
-    return cuda_err(err, e, "tmgpu_forest_set_peer");
-  }
-  // every rank has zeroed its flags and mapped its peers before anyone signals
-  dbuf = nullptr;
-  e = cudaMalloc((void**)&dbuf, sizeof(double) * (world + 1));
-  if (e == cudaSuccess) rc = comm_allgather(f->comm, dbuf, dbuf + 1, 1, nullptr, &why);
-  if (e == cudaSuccess && rc == TMGPU_OK) e = cudaDeviceSynchronize();
-  if (dbuf) cudaFree(dbuf);
-  if (e != cudaSuccess || rc != TMGPU_OK) {
-    peer_close(f);
-    return e != cudaSuccess ? cuda_err(err, e, "tmgpu_forest_set_peer") : fail(err, rc, why);
+    return e != cudaSuccess ? cuda_err(err, e, "tmgpu_forest_set_peer") : fail(err, TMGPU_ERR_CUDA, why);
   }
   f->ptab = t;
   f->peer = true;

@@ -1644,11 +1644,27 @@ int tmgpu_gravity_amr_set_peer(tmgpu_gravity_amr* G, int on, tmgpu_error* err) {
   for (int r = 0; r < R; ++r) bounds[r] = w.seg_lo[r];
   bounds[R] = w.seg_lo[R - 1] + w.seg_cnt[R - 1];
   const GravLetPlan L = grav_let_plan(P, bounds, me);
-  cudaError_t e = cudaMalloc((void**)&w.pflags, 3 * R * sizeof(unsigned long long));
-  if (e == cudaSuccess) e = cudaMemset(w.pflags, 0, 3 * R * sizeof(unsigned long long));
-  // per rank: flag handle, then one moment-array handle per level (8 doubles each)
-  const int rec_n = 8 * (1 + nl);
+  // per rank: flag handle, one moment-array handle per level (8 doubles each), status
+  const int rec_n = 8 * (1 + nl) + 1, k_ok = rec_n - 1;
   std::vector<double> rec(rec_n, 0.0), all((size_t)rec_n * R, 0.0);
+  double* dbuf = nullptr;
+  cudaError_t e = cudaMalloc((void**)&dbuf, sizeof(double) * rec_n * (R + 1));
+  if (e != cudaSuccess) return cuda_err(err, e, "tmgpu_gravity_amr_set_peer");
+  std::string why = "gravity peer exchange: setup failed on a rank";
+  // every rank takes part in both all-gathers and all agree on the outcome
+  auto agree = [&](bool ok, double* out) {
+    rec[k_ok] = ok ? 1.0 : 0.0;
+    cudaError_t ce = cudaMemcpy(dbuf, rec.data(), sizeof(double) * rec_n, cudaMemcpyHostToDevice);
+    if (ce == cudaSuccess) ce = cudaDeviceSynchronize();
+    int rc = ce == cudaSuccess ? comm_allgather(w.comm, dbuf, dbuf + rec_n, rec_n, nullptr, &why) : TMGPU_ERR_CUDA;
+    if (rc == TMGPU_OK) ce = cudaMemcpy(out, dbuf + rec_n, sizeof(double) * rec_n * R, cudaMemcpyDeviceToHost);
+    if (rc != TMGPU_OK || ce != cudaSuccess) return false;
+    for (int q = 0; q < R; ++q)
+      if (out[(size_t)q * rec_n + k_ok] != 1.0) return false;
+    return true;
+  };
+  e = cudaMalloc((void**)&w.pflags, 3 * R * sizeof(unsigned long long));
+  if (e == cudaSuccess) e = cudaMemset(w.pflags, 0, 3 * R * sizeof(unsigned long long));
   cudaIpcMemHandle_t h{};
   if (e == cudaSuccess) e = cudaIpcGetMemHandle(&h, w.pflags);
   std::memcpy(&rec[0], &h, 64);
@@ -1656,25 +1672,14 @@ int tmgpu_gravity_amr_set_peer(tmgpu_gravity_amr* G, int on, tmgpu_error* err) {
     e = cudaIpcGetMemHandle(&h, w.host_lv[l].mom);
     std::memcpy(&rec[8 * (1 + l)], &h, 64);
   }
-  double* dbuf = nullptr;
-  if (e == cudaSuccess) e = cudaMalloc((void**)&dbuf, sizeof(double) * rec_n * (R + 1));
-  if (e == cudaSuccess) e = cudaMemcpy(dbuf, rec.data(), sizeof(double) * rec_n, cudaMemcpyHostToDevice);
-  if (e == cudaSuccess) e = cudaDeviceSynchronize();
-  std::string why;
-  int rc = TMGPU_OK;
-  if (e == cudaSuccess) {
-    rc = comm_allgather(w.comm, dbuf, dbuf + rec_n, rec_n, nullptr, &why);
-    if (rc == TMGPU_OK)
-      e = cudaMemcpy(all.data(), dbuf + rec_n, sizeof(double) * rec_n * R, cudaMemcpyDeviceToHost);
-  }
-  if (dbuf) cudaFree(dbuf);
+  bool ok = agree(e == cudaSuccess, all.data());
   LetPeer t{};
   t.mine = w.pflags;
   t.me = me;
   t.world = R;
   t.nl = nl;
   std::vector<double*> pm((size_t)R * nl, nullptr);
-  for (int q = 0; q < R && e == cudaSuccess && rc == TMGPU_OK; ++q) {
+  for (int q = 0; q < R && ok && e == cudaSuccess; ++q) {
     if (q == me) continue;
     if (!L.roots[q].empty() || !L.recv[q].empty()) t.recv_mask |= 1u << q;
     for (int k = 0; k <= nl && e == cudaSuccess; ++k) {
@@ -1689,27 +1694,26 @@ int tmgpu_gravity_amr_set_peer(tmgpu_gravity_amr* G, int on, tmgpu_error* err) {
         pm[(size_t)q * nl + (k - 1)] = static_cast<double*>(p);
     }
   }
-  std::vector<int4> items;
-  for (int q = 0; q < R; ++q) {
-    if (q == me) continue;
-    for (const PatchRef& r : L.roots[me]) items.push_back(make_int4(r.level, r.node, q, 0));
-    for (const PatchRef& r : L.send[q]) items.push_back(make_int4(r.level, r.node, q, 0));
-    t.n_push[q] = (int)(L.roots[me].size() + L.send[q].size());
+  if (ok) {
+    std::vector<int4> items;
+    for (int q = 0; q < R; ++q) {
+      if (q == me) continue;
+      for (const PatchRef& r : L.roots[me]) items.push_back(make_int4(r.level, r.node, q, 0));
+      for (const PatchRef& r : L.send[q]) items.push_back(make_int4(r.level, r.node, q, 0));
+      t.n_push[q] = (int)(L.roots[me].size() + L.send[q].size());
+    }
+    w.n_push = (long long)items.size();
+    if (e == cudaSuccess && !items.empty()) e = upload(items, &w.push);
+    if (e == cudaSuccess) e = upload(pm, &w.peer_mom);
+    if (e == cudaSuccess) e = cudaDeviceSynchronize();
+    // every rank has zeroed its flags and mapped its peers before anyone pushes
+    std::vector<double> all2((size_t)rec_n * R);
+    ok = agree(e == cudaSuccess, all2.data());
   }
-  w.n_push = (long long)items.size();
-  if (e == cudaSuccess && rc == TMGPU_OK) e = upload(items, &w.push);
-  if (e == cudaSuccess && rc == TMGPU_OK) e = upload(pm, &w.peer_mom);
-  if (e == cudaSuccess && rc == TMGPU_OK) e = cudaDeviceSynchronize();
-  // every rank has zeroed its flags and mapped its peers before anyone pushes
-  if (e == cudaSuccess && rc == TMGPU_OK) {
-    e = cudaMalloc((void**)&dbuf, sizeof(double) * (R + 1));
-    if (e == cudaSuccess) rc = comm_allgather(w.comm, dbuf, dbuf + 1, 1, nullptr, &why);
-    if (e == cudaSuccess && rc == TMGPU_OK) e = cudaDeviceSynchronize();
-    if (dbuf) cudaFree(dbuf);
-  }
-  if (e != cudaSuccess || rc != TMGPU_OK) {
+  cudaFree(dbuf);
+  if (!ok) {
     let_peer_close(w);
-    return e != cudaSuccess ? cuda_err(err, e, "tmgpu_gravity_amr_set_peer") : set_err(err, rc, why.c_str());
+    return e != cudaSuccess ? cuda_err(err, e, "tmgpu_gravity_amr_set_peer") : set_err(err, TMGPU_ERR_CUDA, why.c_str());
   }
   w.pt = t;
   w.peer = true;

@@ -103,8 +103,13 @@ class GravityHydroDriver(HydroDriver):
 
             self.gcomm = Comm.from_torch()
             self.gravity.distribute(self.gcomm, forest._owner)
+            self.moment_transport = "nccl"
             if getattr(forest, "_peer", False):  # the forest's halo is over peer memory
-                self.gravity.set_peer(True)
+                try:  # collective; every rank agrees on the outcome
+                    self.gravity.set_peer(True)
+                    self.moment_transport = "peer"
+                except (_lib.CudaError, RuntimeError) as ex:
+                    self.moment_transport = f"nccl (peer setup failed: {ex})"
         # the solve runs on a side stream, overlapped with the CFL reduction and
         # the first ghost exchange (multi-GPU: also the latency-bound moment
         # exchange); the first stage kernel waits for it. TMGPU_GRAVITY_OVERLAP=0
