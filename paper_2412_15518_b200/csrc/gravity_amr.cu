@@ -877,11 +877,15 @@ struct GravTimingRec {
 
 struct LetPeer {
   unsigned long long* flags[kMaxLetPeers];  // peers' flag words (IPC-mapped)
+  double* part[kMaxLetPeers];               // peers' AM sum arrays (IPC-mapped)
   unsigned long long* mine;                 // this rank's flag words (GravAmrWork::pflags)
   int n_push[kMaxLetPeers];                 // push CTAs per destination
   int me, world, nl;
   unsigned recv_mask;                       // ranks that store patches into this one
+  unsigned am_mask;                         // ranks that store AM sums into this one
+  long long seg_at, seg_n;                  // this rank's AM sums: part[seg_at, seg_at + seg_n)
 };
+constexpr int kAmPushCtas = 16;  // CTAs per destination of am_push_kernel
 
 struct GravAmrWork {
   GravPlan plan;
@@ -948,7 +952,8 @@ struct GravAmrWork {
   bool peer = false;
   unsigned long long peer_seq = 0;
   LetPeer pt{};
-  unsigned long long* pflags = nullptr;  // [0,R) arrival, [R,2R) consumption, [2R,3R) push counters
+  // [0,R) moment arrival, [R,2R) consumption, [2R,3R) push counters, [3R,4R) AM-sum arrival
+  unsigned long long* pflags = nullptr;
   int4* push = nullptr;                  // (level, node, destination rank) per CTA
   long long n_push = 0;
   double** peer_mom = nullptr;           // [R][nlevels] peers' moment arrays
@@ -988,13 +993,45 @@ __global__ void let_wait_kernel(LetPeer t, unsigned long long seq) {
       if (t.recv_mask >> s & 1u) spin_geq(t.mine + s, seq);
 }
 
-// after the solve's last reader of received patches (L2P)
+// after the solve's last reader of received patches and AM sums: every rank
+// that stores into this one may store the next solve's
 __global__ void let_done_kernel(LetPeer t, unsigned long long seq) {
   if (threadIdx.x == 0) {
     __threadfence_system();
+    const unsigned from = t.recv_mask | t.am_mask;
     for (int s = 0; s < t.world; ++s)
-      if (t.recv_mask >> s & 1u) st_release_sys(t.flags[s] + t.world + t.me, seq);
+      if (from >> s & 1u) st_release_sys(t.flags[s] + t.world + t.me, seq);
   }
+}
+
+// AM sums: this rank's slot segment of `part` to every peer (same offsets),
+// kAmPushCtas CTAs per destination; arrival flags at [3R + me].
+__global__ void __launch_bounds__(256) am_push_kernel(const double* __restrict__ part, LetPeer t,
+                                                      unsigned long long seq) {
+  int q = blockIdx.x / kAmPushCtas;
+  q += q >= t.me;
+  const int c = blockIdx.x % kAmPushCtas;
+  if (threadIdx.x == 0) spin_geq(t.mine + t.world + q, seq - 1);
+  __syncthreads();
+  const long long per = (t.seg_n + kAmPushCtas - 1) / kAmPushCtas;
+  const long long b = t.seg_at + c * per, e = min(t.seg_at + t.seg_n, b + per);
+  for (long long k = b + threadIdx.x; k < e; k += blockDim.x) t.part[q][k] = part[k];
+  __threadfence_system();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long* cnt = t.mine + 2 * t.world + q;
+    if (atomicAdd(cnt, 1ull) == (unsigned long long)kAmPushCtas - 1) {
+      *cnt = 0;
+      __threadfence_system();
+      st_release_sys(t.flags[q] + 3 * t.world + t.me, seq);
+    }
+  }
+}
+
+__global__ void am_wait_kernel(LetPeer t, unsigned long long seq) {
+  if (threadIdx.x == 0)
+    for (int s = 0; s < t.world; ++s)
+      if (t.am_mask >> s & 1u) spin_geq(t.mine + 3 * t.world + s, seq);
 }
 
 static void let_peer_close(GravAmrWork& w) {
@@ -1512,20 +1549,25 @@ int tmgpu_gravity_amr_solve(tmgpu_gravity_amr* G, const double* mass, double* ph
     }
     if (timed) cudaEventRecord(rec.ev[4], st);
     const bool am = (flags & TMGPU_GRAV_AM) != 0;
-    if (am) e = cudaMemsetAsync(w.part, 0, (size_t)w.P * 16 * sizeof(double), st);
+    // peer mode: peers store their segments straight into `part`; zero ours only
+    if (am && w.peer)
+      e = cudaMemsetAsync(w.part + w.lo * 16, 0, (size_t)(w.hi - w.lo) * 16 * sizeof(double), st);
+    else if (am)
+      e = cudaMemsetAsync(w.part, 0, (size_t)w.P * 16 * sizeof(double), st);
     if (nloc)
       amr_l2p_kernel<<<(unsigned)nloc, 512, 0, st>>>(w.dev_lv, nloc, w.lo, w.slot_level, w.slot_node,
                                                      w.mass, w.u_geo, w.lloc, w.p2p_tab, w.slot_nbs, dphi, dg,
                                                      am ? w.part : nullptr);
     ++launches;
-    if (w.peer) {  // every received patch has been read (M2L, W/X, top M2M, L2P)
-      let_done_kernel<<<1, 32, 0, st>>>(w.pt, w.peer_seq);
-      ++launches;
-    }
     if (timed) cudaEventRecord(rec.ev[5], st);
     if (am) {  // the per-slot sums came with L2P
-      if (w.comm && e == cudaSuccess)  // identical global pair tree on every rank
+      if (w.peer && e == cudaSuccess) {  // identical global pair tree on every rank
+        am_push_kernel<<<(unsigned)((w.pt.world - 1) * kAmPushCtas), 256, 0, st>>>(w.part, w.pt, w.peer_seq);
+        am_wait_kernel<<<1, 32, 0, st>>>(w.pt, w.peer_seq);
+        launches += 2;
+      } else if (w.comm && e == cudaSuccess) {
         rc = allgather_slots(w, w.part, 16, st, &e, &why);
+      }
       double* bufs[2] = {w.part, w.part2};
       int cur = 0;
       for (long long n = w.P; n > 1;) {
@@ -1539,6 +1581,10 @@ int tmgpu_gravity_amr_solve(tmgpu_gravity_amr* G, const double* mass, double* ph
       am_apply_kernel<<<grid_for(nout), 128, 0, st>>>(w.dev_lv, nloc, w.lo, w.slot_level, w.slot_node,
                                                       w.part + w.P * 16, dg);
       launches += 3;
+    }
+    if (w.peer) {  // every received patch and AM sum has been read
+      let_done_kernel<<<1, 32, 0, st>>>(w.pt, w.peer_seq);
+      ++launches;
     }
     g_launches.fetch_add(launches, std::memory_order_relaxed);
     if (e == cudaSuccess) e = cudaGetLastError();
@@ -1644,8 +1690,9 @@ int tmgpu_gravity_amr_set_peer(tmgpu_gravity_amr* G, int on, tmgpu_error* err) {
   for (int r = 0; r < R; ++r) bounds[r] = w.seg_lo[r];
   bounds[R] = w.seg_lo[R - 1] + w.seg_cnt[R - 1];
   const GravLetPlan L = grav_let_plan(P, bounds, me);
-  // per rank: flag handle, one moment-array handle per level (8 doubles each), status
-  const int rec_n = 8 * (1 + nl) + 1, k_ok = rec_n - 1;
+  // per rank: flag handle, AM-sum handle, one moment-array handle per level (8 doubles
+  // each), status
+  const int rec_n = 8 * (2 + nl) + 1, k_ok = rec_n - 1;
   std::vector<double> rec(rec_n, 0.0), all((size_t)rec_n * R, 0.0);
   double* dbuf = nullptr;
   cudaError_t e = cudaMalloc((void**)&dbuf, sizeof(double) * rec_n * (R + 1));
@@ -1663,14 +1710,16 @@ int tmgpu_gravity_amr_set_peer(tmgpu_gravity_amr* G, int on, tmgpu_error* err) {
       if (out[(size_t)q * rec_n + k_ok] != 1.0) return false;
     return true;
   };
-  e = cudaMalloc((void**)&w.pflags, 3 * R * sizeof(unsigned long long));
-  if (e == cudaSuccess) e = cudaMemset(w.pflags, 0, 3 * R * sizeof(unsigned long long));
+  e = cudaMalloc((void**)&w.pflags, 4 * R * sizeof(unsigned long long));
+  if (e == cudaSuccess) e = cudaMemset(w.pflags, 0, 4 * R * sizeof(unsigned long long));
   cudaIpcMemHandle_t h{};
   if (e == cudaSuccess) e = cudaIpcGetMemHandle(&h, w.pflags);
   std::memcpy(&rec[0], &h, 64);
+  if (e == cudaSuccess) e = cudaIpcGetMemHandle(&h, w.part);
+  std::memcpy(&rec[8], &h, 64);
   for (int l = 0; l < nl && e == cudaSuccess; ++l) {
     e = cudaIpcGetMemHandle(&h, w.host_lv[l].mom);
-    std::memcpy(&rec[8 * (1 + l)], &h, 64);
+    std::memcpy(&rec[8 * (2 + l)], &h, 64);
   }
   bool ok = agree(e == cudaSuccess, all.data());
   LetPeer t{};
@@ -1678,11 +1727,14 @@ int tmgpu_gravity_amr_set_peer(tmgpu_gravity_amr* G, int on, tmgpu_error* err) {
   t.me = me;
   t.world = R;
   t.nl = nl;
+  t.seg_at = w.lo * 16;
+  t.seg_n = (w.hi - w.lo) * 16;
   std::vector<double*> pm((size_t)R * nl, nullptr);
   for (int q = 0; q < R && ok && e == cudaSuccess; ++q) {
     if (q == me) continue;
     if (!L.roots[q].empty() || !L.recv[q].empty()) t.recv_mask |= 1u << q;
-    for (int k = 0; k <= nl && e == cudaSuccess; ++k) {
+    t.am_mask |= 1u << q;
+    for (int k = 0; k < nl + 2 && e == cudaSuccess; ++k) {
       std::memcpy(&h, &all[(size_t)q * rec_n + 8 * k], 64);
       void* p = nullptr;
       e = cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess);
@@ -1690,8 +1742,10 @@ int tmgpu_gravity_amr_set_peer(tmgpu_gravity_amr* G, int on, tmgpu_error* err) {
       w.peer_opened.push_back(p);
       if (k == 0)
         t.flags[q] = static_cast<unsigned long long*>(p);
+      else if (k == 1)
+        t.part[q] = static_cast<double*>(p);
       else
-        pm[(size_t)q * nl + (k - 1)] = static_cast<double*>(p);
+        pm[(size_t)q * nl + (k - 2)] = static_cast<double*>(p);
     }
   }
   if (ok) {
