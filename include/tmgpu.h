@@ -175,7 +175,7 @@ int tmgpu_forest_set_gravity_stream(tmgpu_forest* f, void* stream, tmgpu_error* 
 /* multi-GPU ghost exchange over peer memory instead of NCCL send/recv (collective over the
  * forest's communicator; 2..8 ranks on one node with CUDA IPC): each rank packs its cross-GPU
  * slabs straight into the receivers' buffers and synchronises by flag words (a wait that does
- * not complete within 5 s traps). Re-call after tmgpu_forest_alloc; on = 0 returns to NCCL.
+ * not complete within 20 s traps). Re-call after tmgpu_forest_alloc; on = 0 returns to NCCL.
  * No reference counterpart (the reference moves ghosts through HPX channels). */
 int tmgpu_forest_set_peer(tmgpu_forest* f, int on, tmgpu_error* err);
 /* `waiter` waits for the work enqueued so far on `signaller` (CUDA streams; NULL = default) */
@@ -260,7 +260,7 @@ int tmgpu_gravity_amr_distribute(tmgpu_gravity_amr* G, tmgpu_comm* comm, const l
                                  tmgpu_error* err);
 /* multi-GPU moment exchange over peer memory (collective; 2..8 ranks of one node, CUDA IPC):
  * subtree roots and halo patches are stored straight into the peers' moment arrays with
- * flag-word synchronisation (a wait that does not complete within 5 s traps) instead of the
+ * flag-word synchronisation (a wait that does not complete within 20 s traps) instead of the
  * NCCL all-gather + send/recv. Re-call after tmgpu_gravity_amr_distribute; on = 0 returns to NCCL. */
 int tmgpu_gravity_amr_set_peer(tmgpu_gravity_amr* G, int on, tmgpu_error* err);
 /* host-only: per-level counts of the patches a rank owning slots [lo, hi) evaluates

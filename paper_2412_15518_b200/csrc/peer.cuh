@@ -1,14 +1,14 @@
 // Device helpers of the peer-memory exchanges (halo.cu, gravity_amr.cu): flag
 // words are monotonic sequence numbers stored with release / loaded with
 // acquire semantics at system scope; a wait that does not see its value within
-// kPeerSpinNs traps (a loud failure instead of a hung GPU).
+// kPeerSpinNs (20 s) traps (a loud failure instead of a hung GPU).
 #pragma once
 
 #include <cstdio>
 
 namespace tmgpu {
 
-constexpr unsigned long long kPeerSpinNs = 5000000000ull;
+constexpr unsigned long long kPeerSpinNs = 20000000000ull;  // 20 s
 
 __device__ __forceinline__ unsigned long long peer_globaltimer() {
   unsigned long long t;
