@@ -1311,7 +1311,11 @@ tmgpu_gravity_amr* tmgpu_gravity_amr_create(const int* leaves, long long nleaves
                              (int)kM2lSmem);
   if (e == cudaSuccess) e = build_m2l_work(w, nullptr);
   if (e == cudaSuccess) e = build_l2l_lists(w, nullptr);
-  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&w.side, cudaStreamNonBlocking);
+  // the one-CTA dense top M2L on a high-priority stream: its CTA takes the first
+  // free SM instead of queueing behind every CTA of the concurrent patch M2L
+  int prio_lo = 0, prio_hi = 0;
+  if (e == cudaSuccess) e = cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi);
+  if (e == cudaSuccess) e = cudaStreamCreateWithPriority(&w.side, cudaStreamNonBlocking, prio_hi);
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&w.ev_fork, cudaEventDisableTiming);
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&w.ev_join, cudaEventDisableTiming);
 
