@@ -86,7 +86,7 @@ class ExecutorPool:
             raise AggError(err.message.decode())
 
     def __del__(self):
-        if getattr(self, "h", None):
+        if getattr(self, "h", None) and lib is not None:  # lib is None at interpreter exit
             lib.tmgpu_execpool_destroy(self.h)
             self.h = None
 

@@ -153,7 +153,7 @@ class Forest:
             raise AmrError(err.message.decode())
 
     def __del__(self):
-        if getattr(self, "h", None):
+        if getattr(self, "h", None) and lib is not None:  # lib is None at interpreter exit
             lib.tmgpu_forest_destroy(self.h)
             self.h = None
 

@@ -50,7 +50,7 @@ class Comm:
         return Comm(rank, world, bytes(t.cpu().tolist()))
 
     def __del__(self):
-        if getattr(self, "h", None):
+        if getattr(self, "h", None) and lib is not None:  # lib is None at interpreter exit
             lib.tmgpu_comm_destroy(self.h)
             self.h = None
 

@@ -40,7 +40,7 @@ class GravitySolver:
             _lib.check(err.code or _lib.TMGPU_ERR_CUDA, err)
 
     def __del__(self):
-        if getattr(self, "h", None):
+        if getattr(self, "h", None) and lib is not None:  # lib is None at interpreter exit
             lib.tmgpu_gravity_destroy(self.h)
             self.h = None
 
@@ -198,7 +198,7 @@ class GravityAMR:
             _lib.check(err.code or _lib.TMGPU_ERR_CUDA, err)
 
     def __del__(self):
-        if getattr(self, "h", None):
+        if getattr(self, "h", None) and lib is not None:  # lib is None at interpreter exit
             lib.tmgpu_gravity_amr_destroy(self.h)
             self.h = None
 
