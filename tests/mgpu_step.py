@@ -3,7 +3,8 @@
 Each rank owns a contiguous range of canonical leaves; after 3 SSP-RK3 steps
 (hydro, or gravity+hydro with `--gravity`: distributed FMM solve + hydro) the
 ranks gather their interiors (and the last gravity field) on rank 0, which
-reruns the same steps on one GPU and compares bitwise."""
+reruns the same steps on one GPU and compares bitwise (state, gravity field,
+and the merged checkpoint file's bytes)."""
 import os
 import sys
 
@@ -12,7 +13,7 @@ import torch
 import torch.distributed as tdist
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-from paper_2412_15518_b200 import amr, dist  # noqa: E402
+from paper_2412_15518_b200 import amr, checkpoint, dist  # noqa: E402
 from paper_2412_15518_b200.driver import GravityHydroDriver, HydroDriver  # noqa: E402
 
 
@@ -38,6 +39,7 @@ def main():
     f.set_interior(np.ascontiguousarray(state[a:b]))
     drv = Drv(f)
     dts = [drv.step() for _ in range(3)]
+    ckpt = checkpoint.save(None, f, time=sum(dts), step=3)  # collective: rank 0 merges
     mine = torch.from_numpy(f.get_interior()).cuda()
     sizes = [dist.local_range(owner, r)[1] - dist.local_range(owner, r)[0] for r in range(world)]
     gathered = [torch.zeros((s, 5, 512), dtype=torch.float64, device="cuda") for s in sizes]
@@ -54,6 +56,7 @@ def main():
         dts1 = [d1.step() for _ in range(3)]
         single = g.get_interior()
         assert dts == dts1, (dts, dts1)
+        assert ckpt == checkpoint.encode(g.leaves(), single, sum(dts1), 3), "checkpoint differs"
         if gravity:
             gm = torch.cat(gl, dim=1).cpu().numpy()
             gs = d1.g.view(3, -1).cpu().numpy()
