@@ -3,16 +3,25 @@
 
 Workload (BASELINE.json configs[2], the config the metric is quoted on):
 rotating star on a 5-level AMR octree (leaf levels 2..5, 5,888 leaves of 8^3
-cells = 3.01e6 cells). One step = one adaptive FMM gravity solve with the
-angular-momentum correction (our specification: the reference
-has no gravity code) + the SSP-RK3 hydro step with the gravity source in the
-stage epilogue: CFL dt + 3 x [ghost exchange -> aggregated FP64 stage kernel
-over every leaf + rk3 combine].
+cells = 3.01e6 cells). One step = the SSP-RK3 hydro step with self-gravity:
+CFL dt + 3 x [adaptive FMM gravity solve on the stage's input state (the
+angular-momentum correction included; our specification, DESIGN.md §7 — the
+reference has no gravity code) || ghost exchange -> aggregated FP64 stage
+kernel over every leaf with the gravity source + rk3 combine]. That is the
+paper's coupling, one FMM iteration per hydro iteration (PAPER.md:240);
+--solves-per-step 6 runs the paper's count (a second solve per
+stage on the provisional state), 1 the round-1 step (one solve held over the
+stages).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                  [--scenario star|dwd|sod|sedov] [--solves-per-step 1|3|6]
 
-N>1 runs under torchrun, one rank per GPU; the timed region is bracketed by
-a barrier + device synchronisation and the max over ranks is reported.
+--scenario sod|sedov: BASELINE.json configs[3] (hydro-only, 6-level AMR);
+dwd: configs[4] (7-level AMR). N>1 runs under torchrun, one rank per GPU;
+the timed region is bracketed by a barrier + device synchronisation and the
+max over ranks is reported. The reference arm (--impl reference) builds its
+workload on the reference's own Tree (oracle/_ref/libtmref.so) and imports
+nothing from the product.
 """
 from __future__ import annotations
 
@@ -44,6 +53,15 @@ FLOP_M2L_V, FLOP_M2L_V_LEAF, FLOP_M2L_WX, FLOP_P2P, FLOP_P2P_U = 56, 44, 102, 8,
 FLOP_M2L_WX_LEAF = FLOP_M2L_WX - (FLOP_M2L_V - FLOP_M2L_V_LEAF)
 
 
+# scenario -> (kind, default min/max leaf level, bc, name)
+SCENARIOS = {
+    "star": (0, 2, 5, (0, 0, 0), "configs[2]: rotating star"),
+    "dwd": (1, 2, 7, (0, 0, 0), "configs[4]: double-white-dwarf initial model (geometric refinement)"),
+    "sod": (2, 2, 6, (0, 1, 1), "configs[3]: Sod shock tube (periodic x, reflective y/z)"),
+    "sedov": (3, 2, 6, (0, 0, 0), "configs[3]: Sedov blast (E0 = 1 in the 8 central cells)"),
+}
+
+
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -51,16 +69,27 @@ def parse():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--fast", action="store_true", help="FMA/reciprocal kernels (1e-10 parity)")
-    ap.add_argument("--min-level", type=int, default=2)
-    ap.add_argument("--max-level", type=int, default=5)
+    ap.add_argument("--min-level", type=int, default=None)
+    ap.add_argument("--max-level", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-steps", type=int, default=1)
+    ap.add_argument("--cpu-budget", type=float, default=150.0,
+                    help="reference arm: stop timing steps after this many seconds")
     ap.add_argument("--hydro-only", action="store_true", help="time the hydro step alone")
+    ap.add_argument("--solves-per-step", type=int, choices=[1, 3, 6], default=3,
+                    help="FMM solves per step: 3 = one per RK stage (default), 6 = the paper's "
+                         "count, 1 = once per step")
     ap.add_argument("--halo", choices=["nccl", "peer"], default="peer",
                     help="N>1 ghost-slab transport: NCCL send/recv or peer-memory stores")
-    ap.add_argument("--scenario", choices=["star", "dwd"], default="star",
-                    help="star: configs[2] (default); dwd: configs[4] with --max-level 7")
-    return ap.parse_args()
+    ap.add_argument("--scenario", choices=list(SCENARIOS), default="star")
+    a = ap.parse_args()
+    kind, lo, hi, bc, _ = SCENARIOS[a.scenario]
+    a.min_level = lo if a.min_level is None else a.min_level
+    a.max_level = hi if a.max_level is None else a.max_level
+    a.kind, a.bc = kind, bc
+    if a.scenario in ("sod", "sedov"):
+        a.hydro_only = True  # configs[3] is hydro-only
+    return a
 
 
 # ---------------------------------------------------------------- clocks
@@ -123,117 +152,112 @@ class ClockSampler:
 def build_workload(args):
     from paper_2412_15518_b200 import amr
 
-    kind = amr.Scenario.rotating_star if args.scenario == "star" else amr.Scenario.double_white_dwarf
-    f = amr.build_scenario(kind, args.min_level, args.max_level, 0.1)
-    state = f.scenario_state(kind)
+    f = amr.build_scenario(amr.Scenario(args.kind), args.min_level, args.max_level, 0.1, bc=args.bc)
+    state = f.scenario_state(amr.Scenario(args.kind))
     return f, state
 
 
-def workload_config(f, args, extra=None):
-    n = f.leaf_count()
-    step = ("SSP-RK3 hydro step: CFL dt + 3 x (ghost exchange + aggregated stage + rk3 combine)"
-            if args.hydro_only else
-            "gravity+hydro step: adaptive FMM solve (V/W/X/U lists, angular-momentum correction) "
-            "+ SSP-RK3 hydro step with the gravity source in the stage epilogue: CFL dt + 3 x "
-            "(ghost exchange + aggregated stage + rk3 combine)")
-    name = ("configs[2]: rotating star" if args.scenario == "star" else
-            "configs[4]: double-white-dwarf initial model (geometric refinement)")
+def step_text(args):
+    if args.hydro_only:
+        return "SSP-RK3 hydro step: CFL dt + 3 x (ghost exchange + aggregated stage + rk3 combine)"
+    sps = args.solves_per_step
+    how = {1: "1 adaptive FMM solve per step (on the initial state, held over the 3 stages)",
+           3: "3 adaptive FMM solves per step (one per RK stage on its input state, PAPER.md:240)",
+           6: "6 adaptive FMM solves per step (the paper's count, PAPER.md:241: per stage on its "
+              "input state + on its provisional state, trapezoid source)"}[sps]
+    return ("gravity+hydro step: " + how + " (V/W/X/U lists, angular-momentum correction) + SSP-RK3 "
+            "hydro step with the gravity source in the stage epilogue: CFL dt + 3 x (ghost exchange + "
+            "aggregated stage + rk3 combine)")
+
+
+def workload_config(n, args, extra=None):
+    name = SCENARIOS[args.scenario][4]
     cfg = {"workload": f"{name}, {args.max_level}-level AMR octree "
-                       f"(leaf levels {args.min_level}-{args.max_level}), {n} leaves x 8^3 cells, {step}",
+                       f"(leaf levels {args.min_level}-{args.max_level}), {n} leaves x 8^3 cells, "
+                       f"{step_text(args)}",
            "leaves": n, "cells": n * 512, "subgrid": "8^3 + 2 ghost layers, 5 vars (Euler)",
+           "solves_per_step": 0 if args.hydro_only else args.solves_per_step,
            "l2": "inputs larger than L2 (ghosted arena %.0f MB > 126 MB L2)" % (n * 69120 / 1e6),
            "parity": ("hydro: fast <=1e-10 scaled vs reference" if args.fast else
                       "hydro: bitwise vs the reference build (tests/test_forest_gpu.py)") +
                      ("" if args.hydro_only else
-                      "; gravity+hydro: bitwise vs the oracle composition (tests/test_gravity_hydro_gpu.py)")}
+                      "; gravity+hydro: bitwise vs the oracle composition at this size "
+                      "(tests/test_gravity_c3_gpu.py, tests/test_gravity_hydro_gpu.py)")}
     if extra:
         cfg.update(extra)
     return cfg
 
 
-def reference_setup(f, state):
-    """The same topology + initial state inside the UNMODIFIED reference."""
+def time_reference(args, steps, warmup=0, budget_s=None):
+    """The CPU step on the host cores, entirely on the reference side: the
+    workload is built on the reference's own Tree (oracle/ref_capi.cpp
+    tmref_tree_scenario/_fill, the same leaves and bits as the GPU arm's,
+    tests/test_forest.py), and one step is tmref_gravity_hydro_step: the
+    reference's hydro (fill_ghosts_sync single-threaded as in the reference,
+    AggregationRegion(make_stage_kernel) over Scheduler(ncores), rk3_combine)
+    with the CFL dt inside the call, plus — gravity, which the reference does
+    not have — the patch-sparse CPU restatement of our FMM
+    (oracle/gravity_amr_sparse.c: tabulated geometry, SIMD V lists, OpenMP;
+    its topology plan built once, like the GPU's) at the same solves per step.
+    Returns (median s/step, cores, mean phase seconds, steps timed, leaves, detail)."""
     from oracle import oracle as O
-    sys.path.insert(0, os.path.join(ROOT, "tests"))
-    from helpers import interior_to_ghosted, replay_on_reference
 
     ref = O.Ref()
-    t = replay_on_reference(ref, f, int(max(int(p) >> 60 for p in f.leaves())))
-    g = interior_to_ghosted(state)
-    for i, p in enumerate(f.leaves()):
-        t.grid(int(p))[:] = g[i]
-    return ref, t
-
-
-def reference_dt(ref, t, f, cfl=0.4):
-    h = ref.encode_header(1, 1.0, 0.0)
-    return cfl * min(t.cell_size(int(p) >> 60) / ref.max_wavespeed(h, t.grid(int(p)).copy())
-                     for p in f.leaves())
-
-
-def time_reference(f, state, steps, warmup=0, gravity=True):
-    """CPU step(s) on the host cores: the reference's own hydro step (the
-    unmodified sources, oracle/_ref/libtmref.so: fill_ghosts_sync +
-    AggregationRegion(make_stage_kernel) over Scheduler(ncores) + rk3_combine)
-    and, for the gravity half (no reference code exists), our C restatement
-    of the adaptive FMM (oracle/gravity_amr_oracle.c, OpenMP over targets) on
-    the step's state. Returns (s/step, cores, detail)."""
-    from oracle import oracle as O
-    from paper_2412_15518_b200.gravity import forest_leaf_array
-
-    ref, t = reference_setup(f, state)
+    t = ref.tree(max_level=args.max_level, bc=args.bc)
+    t.scenario(args.kind, args.min_level, args.max_level, 0.1)
+    n = len(t.leaves())
     cores = os.cpu_count() or 1
+    gravity = not args.hydro_only
     o = O.Oracle() if gravity else None
-    lv = forest_leaf_array(f)
-    h3 = (1.0 / (8.0 * 2.0 ** lv[:, 0].astype(np.float64))) ** 3
+    g0 = time.perf_counter()
+    plan = o.grav_plan(t.leaf_levels()) if gravity else None
+    plan_s = time.perf_counter() - g0
+    sps = args.solves_per_step if gravity else 0
 
     def one():
-        tg = 0.0
-        if o is not None:
-            ghosted = np.stack([t.grid(int(p)).reshape(5, 12, 12, 12)[0, 2:10, 2:10, 2:10].reshape(512)
-                                for p in f.leaves()])
-            g0 = time.perf_counter()
-            o.grav_amr(lv, ghosted * h3[:, None], flags=1)
-            tg = time.perf_counter() - g0
-        dt = reference_dt(ref, t, f)
-        h0 = time.perf_counter()
-        tex, tst = t.hydro_step(dt, workers=cores, max_slices=8)
-        return tg + time.perf_counter() - h0, tg, tex, tst
+        w0 = time.perf_counter()
+        _, secs = t.gravity_hydro_step(cfl=0.4, workers=cores, max_slices=8, solves_per_step=sps,
+                                       plan=plan)
+        return time.perf_counter() - w0, secs
 
     for _ in range(warmup):
         one()
-    walls, gr, ex, st = [], 0.0, 0.0, 0.0
+    walls, tot = [], {}
+    t_start = time.perf_counter()
     for _ in range(steps):
-        w, tg, tex, tst = one()
+        w, secs = one()
         walls.append(w)
-        gr += tg
-        ex += tex
-        st += tst
-    return statistics.median(walls), cores, {"gravity_s": gr / steps, "exchange_s": ex / steps,
-                                             "stage_s": st / steps}
+        for k, v in secs.items():
+            tot[k] = tot.get(k, 0.0) + v
+        if budget_s is not None and time.perf_counter() - t_start > budget_s:
+            break
+    k = len(walls)
+    detail = {key: v / k for key, v in tot.items()}
+    detail["gravity_plan_s"] = plan_s
+    detail["fast_oracle"] = bool(o.fast) if o is not None else None
+    return statistics.median(walls), cores, k, n, detail
 
 
-def cpu_sample_text(steps, detail, cores, gravity=True):
-    txt = (f"{steps} full step(s) of the same workload on {cores} host threads: reference hydro "
-           f"(exchange {detail['exchange_s']:.2f} s single-threaded as in the reference, stages "
-           f"{detail['stage_s']:.2f} s over {cores} workers)")
+def cpu_sample_text(steps, detail, cores, args):
+    gravity = not args.hydro_only
+    txt = (f"{steps} full step(s) of the same workload (built on the reference Tree) on {cores} host "
+           f"threads: reference hydro (CFL dt {detail['cfl_s']:.3f} s, exchange {detail['exchange_s']:.2f} s "
+           f"single-threaded as in the reference, stages {detail['stage_s']:.2f} s over {cores} workers)")
     if gravity:
-        txt += (f" + gravity {detail['gravity_s']:.2f} s (our C restatement of the FMM, OpenMP; "
-                "the reference has no gravity code)")
+        txt += (f" + gravity {detail['gravity_s']:.2f} s for {args.solves_per_step} solves (the patch-sparse "
+                "CPU restatement of our FMM, oracle/gravity_amr_sparse.c: tabulated geometry, "
+                f"{'AVX2 ' if detail.get('fast_oracle') else ''}SIMD V lists, OpenMP; plan built once in "
+                f"{detail['gravity_plan_s']:.2f} s, untimed like the GPU's; the reference has no gravity code)")
     return txt
 
 
-def fp64_peak():
-    """FP64 peak: MEASURED_PEAKS.json has no FP64 entry -> live DFMA microbenchmark."""
-    import ctypes as C
+def fp64_peaks():
+    """(DFMA, DMMA) FP64 TFLOP/s measured live by tools/probes/libtmprobe.so
+    (diagnostics, not the product library; MEASURED_PEAKS.json has no FP64 entry)."""
+    sys.path.insert(0, os.path.join(ROOT, "tools", "probes"))
+    import probe
 
-    from paper_2412_15518_b200 import _lib
-
-    peak_tf, pms = C.c_double(0), C.c_double(0)
-    _lib.lib.tmgpu_fp64_peak.argtypes = [C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_double),
-                                         C.c_void_p]
-    _lib.lib.tmgpu_fp64_peak(20000, C.byref(peak_tf), C.byref(pms), None)
-    return peak_tf.value
+    return probe.fp64_peaks()
 
 
 def hbm_peak():
@@ -254,27 +278,34 @@ def profile_traffic(name):
 
 # ---------------------------------------------------------------- arms
 def run_reference_arm(args, rank, world):
+    """The reference's CPU path on this box's host cores; rank 0 only. Imports
+    nothing from the product (paper_2412_15518_b200)."""
     if rank != 0:
         return
-    f, state = build_workload(args)
-    cells = f.leaf_count() * 512
-    # bounded: every CPU step is seconds of work; cap the timed steps
-    k = max(1, min(args.steps, 2))
     w = min(args.warmup, 1)
-    sec, cores, detail = time_reference(f, state, k, w, gravity=not args.hydro_only)
+    sec, cores, k, n, detail = time_reference(args, args.steps, w, budget_s=args.cpu_budget)
+    cells = n * 512
     v = cells / sec
-    line = {"impl": "reference", "metric": METRIC if not args.hydro_only else
-            "sub-grid cell updates/sec (hydro step)", "value": v, "unit": UNIT,
-            "n_gpus": args.gpus, "steps": k, "warmup": w, "ms_per_step": sec * 1e3,
+    line = {"impl": "reference",
+            "metric": METRIC if not args.hydro_only else "sub-grid cell updates/sec (hydro step)",
+            "value": v, "unit": UNIT, "n_gpus": args.gpus, "steps": k, "warmup": w, "ms_per_step": sec * 1e3,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic",
-            "config": workload_config(f, args, {"reference": "hydro: oracle/_ref/libtmref.so (the "
-                                                "unmodified taskmesh sources compiled in place); gravity: "
-                                                "oracle/gravity_amr_oracle.c (no reference code exists)"}),
+            "config": workload_config(n, args, {
+                "reference": "hydro: oracle/_ref/libtmref.so (the unmodified taskmesh sources compiled in "
+                             "place); workload built on the reference Tree (tmref_tree_scenario); gravity: "
+                             "oracle/gravity_amr_sparse.c (no reference code exists)",
+                "same_steps": k == args.steps,
+                "steps_note": None if k == args.steps else
+                f"stopped after {k} of {args.steps} steps (--cpu-budget {args.cpu_budget:.0f} s)"}),
             "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores,
                              "kind": "reference" if args.hydro_only else "reference+port",
-                             "sample": cpu_sample_text(k, detail, cores, not args.hydro_only)},
+                             "sample": cpu_sample_text(k, detail, cores, args)},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    if not args.hydro_only:  # the hydro part of the same steps
+        hs = detail["cfl_s"] + detail["exchange_s"] + detail["stage_s"]
+        line["hydro_only"] = {"value": cells / hs, "unit": UNIT, "s_per_step": hs,
+                              "note": "CFL + exchange + stage time of the same steps (no gravity)"}
     print(json.dumps(line), flush=True)
 
 
@@ -297,7 +328,6 @@ def run_ours(args, rank, world):
     f, state = build_workload(args)
     n = f.leaf_count()
     cells = n * 512  # whole job
-    full_state = state
     if world > 1:  # leaves partitioned over the GPUs (partition_leaves), NCCL halos
         from paper_2412_15518_b200 import dist as tmdist
 
@@ -318,7 +348,7 @@ def run_ours(args, rank, world):
     local_cells = f.local_count() * 512
     gravity = not args.hydro_only
     if gravity:
-        drv = GravityHydroDriver(f, fast=args.fast)
+        drv = GravityHydroDriver(f, fast=args.fast, solves_per_step=args.solves_per_step)
     else:
         drv = HydroDriver(f, fast=args.fast)
     stream = torch.cuda.current_stream()
@@ -373,10 +403,11 @@ def run_ours(args, rank, world):
     if gravity:
         tot, ns = drv.gravity.timing()
         drv.gravity.set_timing(False)
-        grav_ms = {k: v / max(ns, 1) for k, v in tot.items()}
+        grav_ms = {k: v / max(ns, 1) for k, v in tot.items()}  # per solve
         work = drv.gravity.work()
+    sps = args.solves_per_step if gravity else 0
 
-    peak_tf = fp64_peak()
+    peak_tf, peak_dmma = fp64_peaks()
     hbm, hbm_src = hbm_peak()
     stage_gbps = local_cells * ALG_BYTES_PER_CELL / (stage_ms * 1e-3) / 1e9
     stage_tf = local_cells * ALG_FLOP_PER_CELL / (stage_ms * 1e-3) / 1e12
@@ -389,6 +420,7 @@ def run_ours(args, rank, world):
                   "cells_per_launch": local_cells,
                   "fp64": {"achieved": stage_tf, "peak": peak_tf, "unit": "TFLOP/s",
                            "frac": stage_tf / peak_tf if peak_tf else None,
+                           "peak_dmma": peak_dmma, "frac_vs_dmma": stage_tf / peak_dmma if peak_dmma else None,
                            "alg_flop_per_cell": ALG_FLOP_PER_CELL}}
     share = {"hydro_stage": 3 * stage_ms / ms, "hydro_exchange": 3 * exch_ms / ms,
              "hydro_cfl": cfl_ms / ms}
@@ -401,6 +433,7 @@ def run_ours(args, rank, world):
         m2l_prof = profile_traffic("m2l_kernel_latest.json")
         roofline = {"bound": "fp64", "achieved": m2l_tf, "peak": peak_tf, "unit": "TFLOP/s",
                     "frac": m2l_tf / peak_tf if peak_tf else None,
+                    "peak_dmma": peak_dmma, "frac_vs_dmma": m2l_tf / peak_dmma if peak_dmma else None,
                     "traffic": m2l_prof.get("dram_bytes_per_launch"),
                     "kernel": "amr_m2l (gravity M2L: V-list stencil + W/X lists), all levels",
                     "launch_ms": grav_ms["m2l"], "alg_flop_per_launch": m2l_flop,
@@ -408,12 +441,15 @@ def run_ours(args, rank, world):
                                 f"patches ({work['v_pairs']} pairs, {work['v_pairs_leaf']} into leaves) + "
                                 f"{FLOP_M2L_WX}/{FLOP_M2L_WX_LEAF} per W-X entry ({work['wx_entries']}) "
                                 "(FMA = 2)",
-                    "peak_source": "tmgpu_fp64_peak DFMA microbenchmark (live; MEASURED_PEAKS.json "
-                                   "has no FP64 entry)",
+                    "peak_source": "live DFMA microbenchmark (tools/probes/libtmprobe.so "
+                                   "tmgpu_fp64_peak; the M2L is DFMA code); peak_dmma = the FP64 "
+                                   "tensor-core (DMMA m8n8k4) probe, the chip's FP64 ceiling "
+                                   "(MEASURED_PEAKS.json has no FP64 entry)",
+                    "launch_note": "one M2L launch per solve; %d solves per step" % sps,
                     "hydro_stage": stage_roof}
         for k, v in grav_ms.items():
-            share["gravity_" + k] = v / ms
-        step_flop = (m2l_flop + work["p2p_pairs"] * FLOP_P2P + work["u_cross_entries"] * FLOP_P2P_U
+            share["gravity_" + k] = sps * v / ms
+        step_flop = (sps * (m2l_flop + work["p2p_pairs"] * FLOP_P2P + work["u_cross_entries"] * FLOP_P2P_U)
                      + 3 * local_cells * ALG_FLOP_PER_CELL)
         roofline["step_fp64"] = {"achieved": step_flop / (ms * 1e-3) / 1e12, "unit": "TFLOP/s",
                                  "frac": step_flop / (ms * 1e-3) / 1e12 / peak_tf if peak_tf else None,
@@ -423,13 +459,13 @@ def run_ours(args, rank, world):
     roofline["step_share"] = share
     if gravity:
         roofline["step_share_note"] = (
-            "device-event phase times / step time; the gravity solve runs on its own stream "
-            "concurrently with the CFL reduction and the first ghost exchange, whose interval "
-            "includes the wait for it, so the shares overlap")
+            "device-event phase times x occurrences per step / step time; every gravity solve runs "
+            "on its own stream concurrently with its stage's ghost exchange (stage 1: and the CFL "
+            "reduction), whose interval includes the wait for it, so the shares overlap")
     roofline["gravity_work"] = work or None
     if dist:  # per-rank phase times (ms per step, device events): the load balance
         mine = {"cfl": cfl_ms, "exchange": 3 * exch_ms, "stage": 3 * stage_ms,
-                **{"gravity_" + k: v for k, v in grav_ms.items()}}
+                **{"gravity_" + k: sps * v for k, v in grav_ms.items()}}
         ranks = [None] * world
         dist.all_gather_object(ranks, {k: round(v, 4) for k, v in mine.items()})
         roofline["phase_ms_by_rank"] = ranks
@@ -461,13 +497,39 @@ def run_ours(args, rank, world):
         e2e_ms = float(t.item())
     nbytes = state.nbytes
 
+    # hydro-only step on the same forest and state (the gravity solver detached):
+    # the number the reference's own hydro step is compared with
+    hydro_only = None
+    if gravity:
+        drv.close()
+        hdrv = HydroDriver(f, fast=args.fast)
+        for _ in range(3):
+            hdrv.step(stream=sp, sync=False)
+        hdrv.check(stream=sp)
+        barrier()
+        kh = max(10, args.steps)
+        h0, h1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        h0.record(stream)
+        for _ in range(kh):
+            hdrv.step(stream=sp, sync=False)
+        h1.record(stream)
+        barrier()
+        hdrv.check(stream=sp)
+        hms = h0.elapsed_time(h1) / kh
+        if dist:
+            t = torch.tensor([hms], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            hms = float(t.item())
+        hydro_only = {"value": cells / (hms * 1e-3), "unit": UNIT, "ms_per_step": hms, "steps": kh,
+                      "note": "the SSP-RK3 hydro step alone on the same forest (device-resident)"}
+
     line = {"metric": METRIC if gravity else "sub-grid cell updates/sec (hydro step)",
             "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
             "scaling": "strong",
-            "vs_baseline": None, "dtype": "f64", "data": "synthetic (analytic rotating star + "
-            "1e-3 density noise, std::mt19937_64)",
-            "config": workload_config(f, args, {
+            "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (analytic %s, scenario.cpp; std::mt19937_64 density noise)" % args.scenario,
+            "config": workload_config(n, args, {
                 "parallelism": (f"leaves partitioned over {world} GPUs (partition_leaves, "
                                 "contiguous Morton ranges); cross-GPU ghost slabs " +
                                 ("packed straight into the receivers' buffers over NVLink (CUDA "
@@ -480,8 +542,8 @@ def run_ours(args, rank, world):
                                   if getattr(drv, "moment_transport", "") == "peer" else
                                   "by NCCL all-gather + grouped send/recv " +
                                   getattr(drv, "moment_transport", "nccl")[4:]) +
-                                 ", M2L/L2L/L2P on the owned subtree, solve overlapped "
-                                 "with the CFL reduction and first ghost exchange" if gravity else ""))
+                                 ", M2L/L2L/L2P on the owned subtree, every solve overlapped "
+                                 "with its stage's ghost exchange" if gravity else ""))
                 if world > 1 else "single GPU"}),
             "e2e": {"value": cells / (e2e_ms * 1e-3), "unit": UNIT,
                     "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes,
@@ -494,19 +556,23 @@ def run_ours(args, rank, world):
             "gpu_launches": launches,
             "clocks": clk.summary()}
 
+    if hydro_only:
+        line["hydro_only"] = hydro_only
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            sec, cores, detail = time_reference(f, full_state, args.cpu_steps, gravity=gravity)
+            sec, cores, k, _, detail = time_reference(args, args.cpu_steps, 0)
             line["cpu_baseline"] = {"value": cells / sec, "unit": UNIT, "cores": cores,
                                     "kind": "reference+port" if gravity else "reference",
-                                    "sample": cpu_sample_text(args.cpu_steps, detail, cores, gravity)}
+                                    "sample": cpu_sample_text(k, detail, cores, args)}
+            if hydro_only:
+                hs = detail["cfl_s"] + detail["exchange_s"] + detail["stage_s"]
+                hydro_only["cpu_reference_value"] = cells / hs
+                hydro_only["ratio_vs_cpu_reference"] = hydro_only["value"] / (cells / hs)
         except Exception as ex:  # reference build missing on this box
             line["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": 0, "kind": "reference",
                                     "sample": f"unavailable: {ex}"}
     if rank == 0:
         print(json.dumps(line), flush=True)
-    if gravity and hasattr(drv, "close"):
-        drv.close()
     if dist:
         dist.destroy_process_group()
 

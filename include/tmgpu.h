@@ -101,6 +101,7 @@ int tmgpu_partition_leaves(const uint64_t* weights, size_t n, int localities, in
  * Node ids are NodeId::packed() (octree.hpp:29-33); bc[a]: 0 periodic,
  * 1 reflective. */
 typedef struct tmgpu_forest tmgpu_forest;
+typedef struct tmgpu_gravity_amr tmgpu_gravity_amr; /* gravity section below */
 tmgpu_forest* tmgpu_forest_create(int edge, int ghost, int vars, int max_level,
                                   const int* root_dims, const int* bc, tmgpu_error* err);
 void tmgpu_forest_destroy(tmgpu_forest* f);
@@ -168,6 +169,18 @@ int tmgpu_forest_set_reflux(tmgpu_forest* f, int on, tmgpu_error* err);
  * local slot; NULL = pure hydro (the reference's stage) */
 int tmgpu_forest_set_gravity(tmgpu_forest* f, const double* g, long long comp_stride,
                              tmgpu_error* err);
+/* self-gravity solved inside the step by the adaptive FMM G (created on this forest's leaves,
+ * distributed like it): solves_per_step 1 = once on the step's initial state, held over the three
+ * RK stages; 3 = before every RK stage on that stage's input state (the paper's hydro coupling,
+ * PAPER.md:240); 6 = the paper's count: per stage a second solve on the stage's
+ * provisional density moves the source to the trapezoid of the two fields (grav_source.cu; not
+ * with TMGPU_EXACT_GHOSTS). grav_flags: TMGPU_GRAV_AM. phi [n*512], g and g2 [3][comp_stride]
+ * (g2 and rho_tilde [n*512] only for 6) are device buffers by local slot the caller keeps alive;
+ * g holds the last stage-input field. Solves run on the gravity stream when one is set (each
+ * overlapping that stage's ghost exchange). G NULL turns it off. */
+int tmgpu_forest_set_gravity_solver(tmgpu_forest* f, tmgpu_gravity_amr* G, int solves_per_step,
+                                    int grav_flags, double* phi, double* g, double* g2,
+                                    double* rho_tilde, long long comp_stride, tmgpu_error* err);
 /* the stream the next steps' gravity is computed on (NULL: the step's stream): the step runs its
  * CFL reduction and first ghost exchange concurrently and waits for that stream's work (enqueued
  * before the step call) only before the first stage kernel */
@@ -203,13 +216,21 @@ size_t tmgpu_execpool_pick_index(tmgpu_execpool* p);                     /* pick
 int tmgpu_execpool_acquire_at(tmgpu_execpool* p, size_t index, tmgpu_error* err); /* acquire_at */
 void tmgpu_execpool_release(tmgpu_execpool* p, size_t index);            /* ExecutorLease::reset */
 uint64_t tmgpu_execpool_in_flight(tmgpu_execpool* p, size_t index);
-/* kind 0: y = 2x + 1 test kernel (test_aggregator.cpp:17-29); kind 1: the hydro
- * stage (make_stage_kernel, stage.cpp:229-246; slice sizes from the geometry).
+/* kind 1: the hydro stage (make_stage_kernel, stage.cpp:229-246; slice sizes from the
+ * geometry); other kinds are rejected (use tmgpu_region_create_kernel).
  * counters: optional uint64[3] {launches, fused_slices, solo_launches}. */
 tmgpu_region* tmgpu_region_create(tmgpu_execpool* pool, int kind, size_t in_slice,
                                   size_t out_slice, int edge, int ghost, int vars, int flags,
                                   size_t max_slices, size_t capacity, uint64_t* counters,
                                   tmgpu_error* err);
+/* A device kernel registered like a reference KernelSpec (aggregator.hpp:94-106): launch one
+ * aggregated kernel over `count` packed DEVICE slices at in + s*in_slice on `stream`; return 0
+ * or non-zero (the whole batch fails, aggregator.cpp:164-167). */
+typedef int (*tmgpu_device_kernel)(const double* in, double* out, size_t in_slice, size_t out_slice,
+                                   size_t count, void* stream, void* user);
+tmgpu_region* tmgpu_region_create_kernel(tmgpu_execpool* pool, tmgpu_device_kernel fn, void* user,
+                                         size_t in_slice, size_t out_slice, size_t max_slices,
+                                         size_t capacity, uint64_t* counters, tmgpu_error* err);
 long long tmgpu_region_submit(tmgpu_region* r, const double* input, size_t len,
                               tmgpu_error* err);                          /* submit_slice */
 int tmgpu_region_flush(tmgpu_region* r, tmgpu_error* err);              /* flush */
@@ -238,7 +259,6 @@ int tmgpu_gravity_mass_from_arena(tmgpu_gravity* G, const double* arena, const i
  * leaf) or NULL for the workspace masses (tmgpu_gravity_amr_mass_from_arena);
  * outputs phi[n*512], g[3][n*512] by slot. flags: TMGPU_HOST_PTRS, TMGPU_ASYNC,
  * TMGPU_GRAV_AM. info: [0] levels, [1] nodes, [2] W/X pairs, [3] U-cross pairs. */
-typedef struct tmgpu_gravity_amr tmgpu_gravity_amr;
 tmgpu_gravity_amr* tmgpu_gravity_amr_create(const int* leaves, long long nleaves, tmgpu_error* err);
 void tmgpu_gravity_amr_destroy(tmgpu_gravity_amr* G);
 int tmgpu_gravity_amr_info(const tmgpu_gravity_amr* G, long long* out);
@@ -246,6 +266,9 @@ int tmgpu_gravity_amr_plan_info(const int* leaves, long long nleaves, long long*
                                 tmgpu_error* err); /* host only: plan validation + info */
 int tmgpu_gravity_amr_mass_from_arena(tmgpu_gravity_amr* G, const double* arena, int vars,
                                       void* stream, tmgpu_error* err);
+/* masses from a device density [n][512] by local slot (m = rho * h^3, as mass_from_arena) */
+int tmgpu_gravity_amr_mass_from_density(tmgpu_gravity_amr* G, const double* rho, void* stream,
+                                        tmgpu_error* err);
 int tmgpu_gravity_amr_solve(tmgpu_gravity_amr* G, const double* mass, double* phi, double* g,
                             int flags, void* stream, tmgpu_error* err);
 int tmgpu_gravity_amr_am_stats(tmgpu_gravity_amr* G, double* out);
@@ -278,18 +301,6 @@ int tmgpu_gravity_amr_let_plan(const int* leaves, long long nleaves, const long 
 int tmgpu_gravity_amr_set_timing(tmgpu_gravity_amr* G, int on);
 int tmgpu_gravity_amr_timing(tmgpu_gravity_amr* G, double* ms, long long* solves);
 const double* tmgpu_gravity_amr_mass_ptr(const tmgpu_gravity_amr* G);
-
-int tmgpu_selftest_fastmath(int mode, long long n, uint64_t seed, unsigned long long* mismatches,
-                            unsigned long long* checked, double* first_bad, tmgpu_error* err);
-
-/* FP64 DFMA throughput microbenchmark (roofline denominator) */
-int tmgpu_fp64_peak(int iters, double* tflops, double* ms, tmgpu_error* err);
-/* diagnostics: DFMA TFLOP/s with `warps` warps per SM and `chains` independent chains per thread */
-int tmgpu_fp64_probe(int warps, int chains, int iters, double* tflops);
-/* diagnostics: FP64 tensor-core (mma m8n8k4 f64) TFLOP/s, `warps` per SM, `chains` accumulators */
-int tmgpu_dmma_probe(int warps, int chains, int iters, double* tflops);
-/* diagnostics: DFMA TFLOP/s when every FMA reads three fresh registers (8 chains per thread) */
-int tmgpu_dfma3_probe(int warps, int iters, double* tflops);
 
 /* ---------------------------------------------------------------- build info */
 const char* tmgpu_version(void);

@@ -101,6 +101,12 @@ class Ref(_Lib):
         L.tmref_tree_create.argtypes = [C.c_int] * 4 + [_ip, _ip]
         L.tmref_tree_destroy.argtypes = [C.c_void_p]
         L.tmref_tree_refine.argtypes = [C.c_void_p, C.c_uint64]
+        L.tmref_tree_is_leaf.argtypes = [C.c_void_p, C.c_uint64]
+        L.tmref_gravity_hydro_step.argtypes = [C.c_void_p, C.c_double, C.c_double, C.c_double, C.c_uint,
+                                               C.c_size_t, C.c_int, C.c_void_p, C.c_void_p, C.c_int,
+                                               _dp, _dp, C.c_char_p, C.c_size_t]
+        L.tmref_tree_scenario.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_double]
+        L.tmref_tree_scenario_fill.argtypes = [C.c_void_p, C.c_int, C.c_uint64]
         L.tmref_tree_coarsen.argtypes = [C.c_void_p, C.c_uint64]
         L.tmref_tree_leaves.restype = C.c_size_t
         L.tmref_tree_leaves.argtypes = [C.c_void_p, _u64p, C.c_size_t]
@@ -167,6 +173,26 @@ class RefTree:
         if self.L.tmref_tree_coarsen(self.h, packed) != 0:
             raise RuntimeError("reference coarsen failed")
 
+    def is_leaf(self, packed: int) -> bool:
+        return bool(self.L.tmref_tree_is_leaf(self.h, packed))
+
+    def scenario(self, kind: int, min_level: int, max_level: int, theta: float = 0.1,
+                 seed: int = 2412518) -> None:
+        """Build a BASELINE.json scenario on the reference Tree (ref_capi.cpp
+        tmref_tree_scenario / _fill): 0 star, 1 DWD, 2 Sod, 3 Sedov."""
+        if self.L.tmref_tree_scenario(self.h, kind, min_level, max_level, theta) != 0:
+            raise RuntimeError("reference scenario refine failed")
+        if self.L.tmref_tree_scenario_fill(self.h, kind, seed) != 0:
+            raise RuntimeError("reference scenario fill failed")
+
+    def leaf_levels(self) -> np.ndarray:
+        """[n, 4] (level, I, J, K) of the leaves in leaves() order (NodeId::unpack,
+        octree.hpp:35-41)."""
+        p = self.leaves()
+        return np.stack([(p >> np.uint64(60)), (p >> np.uint64(40)) & np.uint64(0xFFFFF),
+                         (p >> np.uint64(20)) & np.uint64(0xFFFFF), p & np.uint64(0xFFFFF)],
+                        axis=1).astype(np.int32)
+
     def leaves(self) -> np.ndarray:
         n = self.L.tmref_tree_leaves(self.h, None, 0)
         out = np.zeros(n, dtype=np.uint64)
@@ -204,6 +230,24 @@ class RefTree:
         self.L.tmref_tree_plan(self.h, axis, rows.ctypes.data_as(_i64p), n)
         return rows
 
+    def gravity_hydro_step(self, dt=0.0, cfl=0.4, gamma=1.4, workers=1, max_slices=8,
+                           solves_per_step=0, plan=None, grav_flags=1):
+        """The bench's CPU step (ref_capi.cpp tmref_gravity_hydro_step): the
+        reference's hydro + `plan` (an Oracle GravPlan, the patch-sparse FMM)
+        per the cadence; cfl > 0 computes dt inside. Returns (dt, seconds dict)."""
+        secs = (C.c_double * 4)()
+        used = C.c_double(0)
+        err = C.create_string_buffer(256)
+        fn = C.cast(plan.L.tmo_grav_plan_solve, C.c_void_p) if plan is not None else None
+        rc = self.L.tmref_gravity_hydro_step(self.h, dt, cfl, gamma, workers, max_slices,
+                                             solves_per_step if plan is not None else 0, fn,
+                                             plan.h if plan is not None else None, grav_flags,
+                                             C.byref(used), secs, err, 256)
+        if rc != 0:
+            raise RuntimeError(f"reference gravity+hydro step failed: {err.value.decode()}")
+        return used.value, {"exchange_s": secs[0], "stage_s": secs[1], "gravity_s": secs[2],
+                            "cfl_s": secs[3]}
+
     def hydro_step(self, dt, gamma=1.4, workers=1, lane_width=1, max_slices=8):
         tex, tst = C.c_double(0), C.c_double(0)
         err = C.create_string_buffer(256)
@@ -214,11 +258,30 @@ class RefTree:
         return tex.value, tst.value
 
 
-class Oracle(_Lib):
-    """Our plain-C restatement (oracle/tm_oracle.c)."""
+def host_has_avx2_fma() -> bool:
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if line.startswith("flags"):
+                    f = set(line.split(":", 1)[1].split())
+                    return {"avx2", "fma", "bmi2"} <= f
+    except OSError:
+        pass
+    return False
 
-    def __init__(self):
-        super().__init__("liboracle.so")
+
+class Oracle(_Lib):
+    """Our plain-C restatement (oracle/tm_oracle.c, gravity_*.c).
+
+    fast=None picks liboracle_fast.so (the same sources, -O3 -march=x86-64-v3)
+    on hosts with AVX2 + FMA, else the portable liboracle.so; both give the
+    same bits (tests/test_gravity_amr.py)."""
+
+    def __init__(self, fast=None):
+        if fast is None:
+            fast = host_has_avx2_fma() and os.path.exists(os.path.join(REF_DIR, "liboracle_fast.so"))
+        super().__init__("liboracle_fast.so" if fast else "liboracle.so")
+        self.fast = bool(fast)
         L = self.lib
         for f in ("tmo_minmod_scalar", "tmo_minmod_lane"):
             getattr(L, f).restype = C.c_double
@@ -253,13 +316,19 @@ class Oracle(_Lib):
         L.tmo_stage_subgrid_grav.argtypes = [_dp, C.c_int, C.c_int, C.c_int, _dp, _dp, _dp, _ip]
         _lp = C.POINTER(C.c_long)
         L.tmo_grav_amr_solve_ex.argtypes = [C.c_long, _ip, _dp, C.c_int, _dp, _dp, _lp]
+        L.tmo_grav_amr_sparse.argtypes = [C.c_long, _ip, _dp, C.c_int, _dp, _dp, _lp]
+        L.tmo_grav_plan_create.restype = C.c_void_p
+        L.tmo_grav_plan_create.argtypes = [C.c_long, _ip, _ip]
+        L.tmo_grav_plan_solve.argtypes = [C.c_void_p, _dp, C.c_int, _dp, _dp, _lp]
+        L.tmo_grav_plan_destroy.argtypes = [C.c_void_p]
         L.tmo_grav_amr_direct.argtypes = [C.c_long, _ip, _dp, _dp, _dp]
         L.tmo_grav_am_correct.argtypes = [C.c_long, _dp, _dp, _dp, _dp, _dp]
 
-    def grav_amr(self, leaves, mass, flags=0, direct=False):
-        """AMR FMM specification (gravity_amr_oracle.c). leaves: [n, 4] int
-        (level, I, J, K) in canonical order; mass: [n, 512]. Returns
-        (phi[n*512], g[3, n*512], (W/X entries, U-cross entries))."""
+    def grav_amr(self, leaves, mass, flags=0, direct=False, sparse=False):
+        """AMR FMM specification (gravity_amr_oracle.c; sparse=True: the
+        patch-sparse restatement gravity_amr_sparse.c, same bits, any depth).
+        leaves: [n, 4] int (level, I, J, K) in canonical order; mass: [n, 512].
+        Returns (phi[n*512], g[3, n*512], (W/X entries, U-cross entries))."""
         lv = np.ascontiguousarray(leaves, dtype=np.int32).reshape(-1, 4)
         m = np.ascontiguousarray(mass, dtype=np.float64).reshape(-1)
         n = lv.shape[0]
@@ -269,11 +338,19 @@ class Oracle(_Lib):
         ip = lv.ctypes.data_as(_ip)
         if direct:
             r = self.lib.tmo_grav_amr_direct(n, ip, dptr(m), dptr(phi), dptr(g))
+        elif sparse:
+            r = self.lib.tmo_grav_amr_sparse(n, ip, dptr(m), flags, dptr(phi), dptr(g), cnt)
         else:
             r = self.lib.tmo_grav_amr_solve_ex(n, ip, dptr(m), flags, dptr(phi), dptr(g), cnt)
         if r != 0:
             raise ValueError(f"oracle AMR gravity failed ({r})")
         return phi, g.reshape(3, -1), (cnt[0], cnt[1])
+
+    def grav_plan(self, leaves):
+        """Patch-sparse solver with the topology work done once (like the GPU's
+        GravityAMR): returns a GravPlan whose solve(mass, flags) gives the bits
+        of grav_amr."""
+        return GravPlan(self, leaves)
 
     def stage_fused(self, packed_in, count, edge=8, ghost=2, vars=5):
         S = edge + 2 * ghost
@@ -291,6 +368,32 @@ class Oracle(_Lib):
 
     def tree(self, leaves, edge=8, ghost=2, vars=5, root_dims=(1, 1, 1), bc=(0, 0, 0)):
         return OracleTree(self, leaves, edge, ghost, vars, root_dims, bc)
+
+
+class GravPlan:
+    def __init__(self, o: "Oracle", leaves):
+        self.L = o.lib
+        self.lv = np.ascontiguousarray(leaves, dtype=np.int32).reshape(-1, 4)
+        self.n = self.lv.shape[0]
+        rc = C.c_int(0)
+        self.h = self.L.tmo_grav_plan_create(self.n, self.lv.ctypes.data_as(_ip), C.byref(rc))
+        if not self.h:
+            raise ValueError(f"oracle gravity plan failed ({rc.value})")
+
+    def solve(self, mass, flags=0):
+        m = np.ascontiguousarray(mass, dtype=np.float64).reshape(-1)
+        assert m.size == self.n * 512
+        phi, g = np.zeros(self.n * 512), np.zeros(3 * self.n * 512)
+        cnt = (C.c_long * 2)()
+        r = self.L.tmo_grav_plan_solve(self.h, dptr(m), flags, dptr(phi), dptr(g), cnt)
+        if r != 0:
+            raise ValueError(f"oracle AMR gravity failed ({r})")
+        return phi, g.reshape(3, -1), (cnt[0], cnt[1])
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            self.L.tmo_grav_plan_destroy(self.h)
+            self.h = None
 
 
 class OracleTree:

@@ -75,6 +75,16 @@ int tmo_grav_amr_solve(long nleaves, const int* leaves, const double* mass, int 
                        double* g);
 int tmo_grav_amr_solve_ex(long nleaves, const int* leaves, const double* mass, int flags,
                           double* phi, double* g, long* counts);
+/* patch-sparse restatement (gravity_amr_sparse.c): bitwise equal to tmo_grav_amr_solve_ex,
+ * any depth, OpenMP; the CPU baseline of the gravity half */
+int tmo_grav_amr_sparse(long nleaves, const int* leaves, const double* mass, int flags, double* phi,
+                        double* g, long* counts);
+/* the same split like the GPU solver: plan (topology, lists) once, solve per mass field */
+typedef struct tmo_grav_plan tmo_grav_plan;
+tmo_grav_plan* tmo_grav_plan_create(long nleaves, const int* leaves, int* rc);
+int tmo_grav_plan_solve(tmo_grav_plan* P, const double* mass, int flags, double* phi, double* g,
+                        long* counts);
+void tmo_grav_plan_destroy(tmo_grav_plan* P);
 int tmo_grav_amr_direct(long nleaves, const int* leaves, const double* mass, double* phi, double* g);
 void tmo_grav_am_solve(const double* S, double* R, double* w);
 int tmo_grav_am_correct(long nleaves, const double* mass, const double* pos, double* g,

@@ -24,6 +24,7 @@ TMGPU_HOST_PTRS = 0x1
 TMGPU_FAST = 0x2
 TMGPU_ASYNC = 0x4
 TMGPU_EXACT_GHOSTS = 0x8
+TMGPU_GRAV_AM = 0x100
 TMGPU_OVERLAP = 0x10
 
 

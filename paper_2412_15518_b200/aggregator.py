@@ -40,6 +40,8 @@ _sig("tmgpu_execpool_release", None, [_vp, C.c_size_t])
 _sig("tmgpu_execpool_in_flight", C.c_uint64, [_vp, C.c_size_t])
 _sig("tmgpu_region_create", _vp, [_vp, C.c_int, C.c_size_t, C.c_size_t, C.c_int, C.c_int, C.c_int,
                                   C.c_int, C.c_size_t, C.c_size_t, C.POINTER(C.c_uint64), _ep])
+_sig("tmgpu_region_create_kernel", _vp, [_vp, _vp, _vp, C.c_size_t, C.c_size_t, C.c_size_t, C.c_size_t,
+                                         C.POINTER(C.c_uint64), _ep])
 _sig("tmgpu_region_submit", C.c_longlong, [_vp, _vp, C.c_size_t, _ep])
 _sig("tmgpu_region_flush", C.c_int, [_vp, _ep])
 _sig("tmgpu_region_wait", C.c_int, [_vp, C.c_longlong, _ep])
@@ -157,28 +159,41 @@ class SliceFuture:
         return np.ctypeslib.as_array(p, shape=(r.out_slice,))
 
 
+class DeviceKernel:
+    """A device kernel registered like a reference KernelSpec (aggregator.hpp:94-106):
+    ``fn`` is the address of a C function with the tmgpu_device_kernel signature
+    (include/tmgpu.h) that launches one aggregated kernel over packed device
+    slices; ``user`` is passed through."""
+
+    def __init__(self, fn: int, in_slice: int, out_slice: int, user: int | None = None):
+        if not fn:
+            raise AggError("null kernel function")
+        self.fn, self.in_slice, self.out_slice, self.user = fn, in_slice, out_slice, user
+
+
 class AggregationRegion:
     """Work-aggregation region for one device kernel (aggregator.hpp:138-172).
 
-    kernel: "affine" (y = 2x + 1 over in_slice doubles, the reference tests'
-    toy kernel) or a StageGeom (the hydro stage, make_stage_kernel)."""
+    kernel: a StageGeom (the hydro stage, make_stage_kernel) or a DeviceKernel."""
 
     def __init__(self, execs: ExecutorPool, kernel, max_slices: int, capacity_slices: int,
-                 counters: AggCounters | None = None, slice_len: int = 0, fast: bool = False):
+                 counters: AggCounters | None = None, fast: bool = False):
         err = TmgpuError()
-        if isinstance(kernel, StageGeom):
-            kind, ins, outs, g = 1, kernel.in_slice(), kernel.out_slice(), kernel
-        elif kernel == "affine":
-            kind, ins, outs, g = 0, slice_len, slice_len, StageGeom()
-        else:
-            raise ValueError("kernel must be 'affine' or a StageGeom")
+        cnt = counters._buf if counters is not None else None
         self.execs, self.counters = execs, counters
-        self.in_slice, self.out_slice = ins, outs
-        self.h = lib.tmgpu_region_create(execs.h, kind, ins, outs, g.edge, g.ghost, g.vars,
-                                         _lib.TMGPU_FAST if fast else 0, max_slices,
-                                         capacity_slices,
-                                         counters._buf if counters is not None else None,
-                                         C.byref(err))
+        if isinstance(kernel, StageGeom):
+            g = kernel
+            self.in_slice, self.out_slice = g.in_slice(), g.out_slice()
+            self.h = lib.tmgpu_region_create(execs.h, 1, self.in_slice, self.out_slice, g.edge, g.ghost,
+                                             g.vars, _lib.TMGPU_FAST if fast else 0, max_slices,
+                                             capacity_slices, cnt, C.byref(err))
+        elif isinstance(kernel, DeviceKernel):
+            self.in_slice, self.out_slice = kernel.in_slice, kernel.out_slice
+            self.h = lib.tmgpu_region_create_kernel(execs.h, kernel.fn, kernel.user, kernel.in_slice,
+                                                    kernel.out_slice, max_slices, capacity_slices, cnt,
+                                                    C.byref(err))
+        else:
+            raise ValueError("kernel must be a StageGeom or a DeviceKernel")
         if not self.h:
             _agg_check(err.code or _lib.TMGPU_ERR_AGG, err)
         self._lock = threading.Lock()

@@ -29,9 +29,6 @@
 
 namespace tmgpu {
 
-cudaError_t launch_affine(const double* in, double* out, long long in_slice, long long out_slice,
-                          long long count, cudaStream_t st);  // aggregator_kernels.cu
-
 namespace {
 
 struct Pool {
@@ -91,7 +88,9 @@ struct tmgpu_execpool {
 
 struct tmgpu_region {
   tmgpu_execpool* pool = nullptr;
-  int kind = 0;  // 0 affine test kernel (y = 2x + 1), 1 hydro stage
+  int kind = 0;  // 0 custom device kernel (fn, user), 1 hydro stage
+  tmgpu_device_kernel fn = nullptr;
+  void* user = nullptr;
   int edge = 8, ghost = 2, vars = 5, flags = 0;
   size_t in_slice = 0, out_slice = 0, max_slices = 1, capacity = 0;
   uint64_t* counters = nullptr;  // [launches, fused_slices, solo_launches]
@@ -157,9 +156,10 @@ int launch_locked(tmgpu_region* r, tmgpu_error* err) {  // aggregator.cpp:132-17
   unsigned long long* word = r->d_err + first;  // batch error word lives at its first slot
   if (e == cudaSuccess) e = cudaMemsetAsync(word, 0xff, sizeof(unsigned long long), st);
   if (e == cudaSuccess) {
-    if (r->kind == 0) {
-      e = launch_affine(r->d_in + first * r->in_slice, r->d_out + first * r->out_slice,
-                        (long long)r->in_slice, (long long)r->out_slice, (long long)count, st);
+    if (r->kind == 0) {  // KernelSpec::fn of a registered kernel (aggregator.hpp:94-106)
+      const int rc = r->fn(r->d_in + first * r->in_slice, r->d_out + first * r->out_slice, r->in_slice,
+                           r->out_slice, count, st, r->user);
+      if (rc != 0) e = cudaErrorLaunchFailure;
     } else {
       StageMaps maps;
       std::string why;
@@ -256,15 +256,14 @@ uint64_t tmgpu_execpool_in_flight(tmgpu_execpool* p, size_t index) {
 }
 
 // ------------------------------------------------------------- AggregationRegion
-// kind 0: the reference tests' toy kernel y = 2x + 1 (test_aggregator.cpp:17-29);
-// kind 1: hydro::make_stage_kernel(geom) (stage.cpp:229-246) on the device.
+// kind 1: hydro::make_stage_kernel(geom) (stage.cpp:229-246) on the device;
+// any other registered kernel through tmgpu_region_create_kernel.
 // counters: optional uint64[3] {launches, fused_slices, solo_launches}
 // (AggCounters, aggregator.hpp:87-92), updated under the region lock.
-tmgpu_region* tmgpu_region_create(tmgpu_execpool* pool, int kind, size_t in_slice,
-                                  size_t out_slice, int edge, int ghost, int vars, int flags,
-                                  size_t max_slices, size_t capacity, uint64_t* counters,
-                                  tmgpu_error* err) {
-  if (err) std::memset(err, 0, sizeof(*err));
+namespace {
+tmgpu_region* region_new(tmgpu_execpool* pool, int kind, size_t in_slice, size_t out_slice, int edge, int ghost,
+                         int vars, int flags, size_t max_slices, size_t capacity, uint64_t* counters,
+                         tmgpu_device_kernel fn, void* user, tmgpu_error* err) {
   if (!pool) {
     set_err(err, TMGPU_ERR_AGG, "null executor pool");
     return nullptr;
@@ -288,6 +287,8 @@ tmgpu_region* tmgpu_region_create(tmgpu_execpool* pool, int kind, size_t in_slic
   auto* r = new tmgpu_region;
   r->pool = pool;
   r->kind = kind;
+  r->fn = fn;
+  r->user = user;
   r->edge = edge;
   r->ghost = ghost;
   r->vars = vars;
@@ -317,8 +318,41 @@ tmgpu_region* tmgpu_region_create(tmgpu_execpool* pool, int kind, size_t in_slic
   r->pinned = pool->p.select_locked();  // pick_index (aggregator.cpp:98)
   return r;
 }
+}  // namespace
+
+tmgpu_region* tmgpu_region_create(tmgpu_execpool* pool, int kind, size_t in_slice,
+                                  size_t out_slice, int edge, int ghost, int vars, int flags,
+                                  size_t max_slices, size_t capacity, uint64_t* counters,
+                                  tmgpu_error* err) {
+  if (err) std::memset(err, 0, sizeof(*err));
+  if (kind != 1) {
+    set_err(err, TMGPU_ERR_INVALID, "region kind must be 1 (hydro stage); use tmgpu_region_create_kernel");
+    return nullptr;
+  }
+  return region_new(pool, kind, in_slice, out_slice, edge, ghost, vars, flags, max_slices, capacity, counters,
+                    nullptr, nullptr, err);
+}
 
 // submit_slice (aggregator.cpp:106-124): returns the slice ticket (>= 0) or -1.
+// A region over any device kernel (the reference's KernelRegistry holds
+// arbitrary KernelSpecs, aggregator.hpp:94-116): fn(d_in, d_out, in_slice,
+// out_slice, count, stream, user) launches one aggregated kernel over `count`
+// packed device slices on `stream` and returns 0 (else the batch fails).
+tmgpu_region* tmgpu_region_create_kernel(tmgpu_execpool* pool, tmgpu_device_kernel fn, void* user,
+                                         size_t in_slice, size_t out_slice, size_t max_slices,
+                                         size_t capacity, uint64_t* counters, tmgpu_error* err) {
+  if (err) std::memset(err, 0, sizeof(*err));
+  if (!fn) {
+    set_err(err, TMGPU_ERR_AGG, "null kernel function");
+    return nullptr;
+  }
+  if (in_slice == 0 || out_slice == 0) {
+    set_err(err, TMGPU_ERR_AGG, "slice sizes must be positive");
+    return nullptr;
+  }
+  return region_new(pool, 0, in_slice, out_slice, 0, 0, 0, 0, max_slices, capacity, counters, fn, user, err);
+}
+
 long long tmgpu_region_submit(tmgpu_region* r, const double* input, size_t len, tmgpu_error* err) {
   if (err) std::memset(err, 0, sizeof(*err));
   std::lock_guard<std::mutex> lk(r->mu);

@@ -53,6 +53,12 @@ struct tmgpu_forest {
   // stream only before the first stage kernel
   cudaStream_t grav_stream = nullptr;
   cudaEvent_t ev_grav = nullptr;
+  // optional in-step self-gravity (tmgpu_forest_set_gravity_solver)
+  tmgpu_gravity_amr* gsolver = nullptr;
+  int g_cadence = 0, g_flags = 0;
+  double *g_phi = nullptr, *g_a = nullptr, *g_b = nullptr, *rho_tilde = nullptr;
+  long long g_stride = 0;
+  cudaEvent_t ev_fork = nullptr;
   unsigned long long* err_dev = nullptr;
   // reference-exact 3-pass exchange (single GPU only)
   double* staged = nullptr;
@@ -394,6 +400,7 @@ void tmgpu_forest_destroy(tmgpu_forest* f) {
   free_dev(f);
   tmgpu_forest_set_reflux(f, 0, nullptr);
   if (f->ev_grav) cudaEventDestroy(f->ev_grav);
+  if (f->ev_fork) cudaEventDestroy(f->ev_fork);
   if (f->side) cudaStreamDestroy(f->side);
   if (f->ev_packed) cudaEventDestroy(f->ev_packed);
   if (f->ev_remote) cudaEventDestroy(f->ev_remote);
@@ -721,6 +728,64 @@ int tmgpu_forest_set_gravity(tmgpu_forest* f, const double* g, long long comp_st
   return TMGPU_OK;
 }
 
+int tmgpu_forest_set_gravity_solver(tmgpu_forest* f, tmgpu_gravity_amr* G, int solves_per_step,
+                                    int grav_flags, double* phi, double* g, double* g2,
+                                    double* rho_tilde, long long comp_stride, tmgpu_error* err) {
+  if (err) std::memset(err, 0, sizeof(*err));
+  if (!f) return fail(err, TMGPU_ERR_INVALID, "null forest");
+  if (!G) {
+    f->gsolver = nullptr;
+    f->g_cadence = 0;
+    return TMGPU_OK;
+  }
+  if (int rc = ready(f, err)) return rc;
+  if (solves_per_step != 1 && solves_per_step != 3 && solves_per_step != 6)
+    return fail(err, TMGPU_ERR_INVALID, "gravity solver: solves_per_step must be 1, 3 or 6");
+  if (!phi || !g || (solves_per_step == 6 && (!g2 || !rho_tilde)))
+    return fail(err, TMGPU_ERR_INVALID, "gravity solver: missing field buffer");
+  if (comp_stride < f->nslots * 512)
+    return fail(err, TMGPU_ERR_INVALID, "gravity: component stride below the local cell count");
+  if (!f->ev_fork) {
+    cudaError_t e = cudaEventCreateWithFlags(&f->ev_fork, cudaEventDisableTiming);
+    if (e == cudaSuccess && !f->ev_grav) e = cudaEventCreateWithFlags(&f->ev_grav, cudaEventDisableTiming);
+    if (e != cudaSuccess) return cuda_err(err, e, "tmgpu_forest_set_gravity_solver");
+  }
+  f->gsolver = G;
+  f->g_cadence = solves_per_step;
+  f->g_flags = grav_flags & TMGPU_GRAV_AM;
+  f->g_phi = phi;
+  f->g_a = g;
+  f->g_b = g2;
+  f->rho_tilde = rho_tilde;
+  f->g_stride = comp_stride;
+  f->grav = nullptr;  // the solver's field replaces an external one
+  return TMGPU_OK;
+}
+
+namespace {
+// One in-step gravity solve on the gravity stream (forked from `st` after the
+// work enqueued so far): masses from the arena's interior density (rho NULL)
+// or from a compact density, then the FMM into (g_phi, gout). The caller makes
+// `st` wait for f->ev_grav before reading gout.
+int grav_solve(tmgpu_forest* f, cudaStream_t st, const double* arena, const double* rho, double* gout,
+               tmgpu_error* err) {
+  cudaStream_t gs = f->grav_stream ? f->grav_stream : st;
+  cudaError_t e = cudaSuccess;
+  if (gs != st) {
+    e = cudaEventRecord(f->ev_fork, st);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(gs, f->ev_fork, 0);
+    if (e != cudaSuccess) return cuda_err(err, e, "tmgpu_forest_step: gravity fork");
+  }
+  int rc = arena ? tmgpu_gravity_amr_mass_from_arena(f->gsolver, arena, f->forest.config().vars, gs, err)
+                 : tmgpu_gravity_amr_mass_from_density(f->gsolver, rho, gs, err);
+  if (rc == TMGPU_OK)
+    rc = tmgpu_gravity_amr_solve(f->gsolver, nullptr, f->g_phi, gout, f->g_flags | TMGPU_ASYNC, gs, err);
+  if (rc != TMGPU_OK) return rc;
+  e = cudaEventRecord(f->ev_grav, gs);
+  return cuda_err(err, e, "tmgpu_forest_step: gravity join");
+}
+}  // namespace
+
 int tmgpu_forest_step(tmgpu_forest* f, double dt, double cfl, double gamma, int flags, void* stream,
                       double* dt_used, tmgpu_error* err) {
   if (err) std::memset(err, 0, sizeof(*err));
@@ -729,12 +794,19 @@ int tmgpu_forest_step(tmgpu_forest* f, double dt, double cfl, double gamma, int 
   if (V != 5) return fail(err, TMGPU_ERR_INVALID, "the hydro step is Euler (vars 5)");
   cudaStream_t st = as_stream(stream);
   cudaError_t e = cudaSuccess;
+  const int cadence = f->gsolver ? f->g_cadence : 0;
+  if (cadence == 6 && (flags & TMGPU_EXACT_GHOSTS))
+    return fail(err, TMGPU_ERR_INVALID, "the 6-solve gravity cadence needs the fused (ping-pong) step");
   const bool timed = f->timing;
   if (timed) {
     collect_timing(f);  // events are reused: fold the previous step in first
     cudaEventRecord(f->ev[0], st);
   }
-  if (f->grav_stream) e = cudaEventRecord(f->ev_grav, f->grav_stream);  // gravity enqueued so far
+  if (cadence) {  // stage 1's solve on the step's initial state, overlapping the CFL and exchange
+    if (int rc = grav_solve(f, st, f->arena(), nullptr, f->g_a, err)) return rc;
+  } else if (f->grav_stream) {
+    e = cudaEventRecord(f->ev_grav, f->grav_stream);  // gravity enqueued so far
+  }
   if (!(flags & TMGPU_ASYNC) && e == cudaSuccess)
     e = cudaMemsetAsync(f->err_dev, 0xff, sizeof(unsigned long long), st);
   if (e == cudaSuccess && cfl > 0.0) {
@@ -765,8 +837,8 @@ int tmgpu_forest_step(tmgpu_forest* f, double dt, double cfl, double gamma, int 
   p.u0 = f->u0;
   p.u0_stride = (long long)V * 512;
   p.err = f->err_dev;
-  p.grav = f->grav;
-  p.grav_stride = f->grav_stride;
+  p.grav = cadence ? f->g_a : f->grav;
+  p.grav_stride = cadence ? f->g_stride : f->grav_stride;
   p.count = (int)f->nslots;
   const bool exact = (flags & TMGPU_EXACT_GHOSTS) != 0;
   p.face_src = exact ? nullptr : f->face_src;
@@ -775,6 +847,9 @@ int tmgpu_forest_step(tmgpu_forest* f, double dt, double cfl, double gamma, int 
   const bool overlap = !exact && f->world() > 1 && !f->peer && (flags & TMGPU_OVERLAP);
   for (int stage = 1; stage <= 3 && e == cudaSuccess; ++stage) {
     std::string why;
+    if (stage > 1 && cadence >= 3) {  // this stage's field from its input state
+      if (int rc = grav_solve(f, st, f->arena(), nullptr, f->g_a, err)) return rc;
+    }
     if (overlap) {
       // pack (all slabs) -> [side: NCCL halo, remote pulls] || [main: local pulls,
       // interior leaves' stage] -> join -> boundary leaves' stage
@@ -795,10 +870,12 @@ int tmgpu_forest_step(tmgpu_forest* f, double dt, double cfl, double gamma, int 
     } else if (int rc = exchange(f, st, exact ? kExact : kFused, &why)) {
       return fail(err, rc, why);
     }
-    // (stage 1's exchange interval includes the wait for a concurrent gravity solve)
-    if (stage == 1 && f->grav_stream && e == cudaSuccess) e = cudaStreamWaitEvent(st, f->ev_grav, 0);
+    // (the exchange interval includes the wait for a concurrent gravity solve)
+    if (e == cudaSuccess && ((cadence && (stage == 1 || cadence >= 3)) || (!cadence && stage == 1 && f->grav_stream)))
+      e = cudaStreamWaitEvent(st, f->ev_grav, 0);
     if (timed) cudaEventRecord(f->ev[2 * stage], st);
     p.rk_stage = stage;
+    p.rho_save = cadence == 6 ? f->rho_tilde : nullptr;
     p.u0_save = stage == 1 ? f->u0 : nullptr;
     p.u0_save_stride = (long long)V * 512;
     // exact: in place (each CTA reads only its own block); fused: ping-pong
@@ -820,6 +897,14 @@ int tmgpu_forest_step(tmgpu_forest* f, double dt, double cfl, double gamma, int 
       const double coef = stage == 1 ? 1.0 : (stage == 2 ? 0.25 : 2.0 / 3.0);
       e = launch_reflux(f->arenas[dst], V, f->flux, f->rf_leaf, f->rf_off, f->rf_ad, f->rf_fine, f->rf_n,
                         f->leaf_dx, p.dt_ptr, dt, coef, st);
+    }
+    if (e == cudaSuccess && cadence == 6) {  // second solve on the provisional density, trapezoid source
+      if (int rc = grav_solve(f, st, nullptr, f->rho_tilde, f->g_b, err)) return rc;
+      e = cudaStreamWaitEvent(st, f->ev_grav, 0);
+      const double w = stage == 1 ? 1.0 : (stage == 2 ? 0.25 : 2.0 / 3.0);
+      if (e == cudaSuccess)
+        e = launch_grav_correct(f->arenas[f->cur], f->arenas[dst], f->nslots, f->g_a, f->g_b, f->g_stride,
+                                p.dt_ptr, dt, w, st);
     }
     f->cur = dst;
     if (timed) cudaEventRecord(f->ev[2 * stage + 1], st);

@@ -566,6 +566,7 @@ __global__ void __launch_bounds__(kStageThreads, 2)
 #pragma unroll
     for (int v = 0; v < V; ++v)
       if (!isfinite(u[v])) bad = min(bad, (unsigned)(v * kE3 + c));
+    if (p.rho_save) p.rho_save[(long long)slot * kE3 + c] = u[0];
     const int z = c >> 6, y = (c >> 3) & 7, x = c & 7;
 #pragma unroll
     for (int v = 0; v < V; ++v) {

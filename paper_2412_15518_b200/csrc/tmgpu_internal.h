@@ -48,6 +48,10 @@ struct StageLaunch {
   // input's primitives (oracle tmo_stage_subgrid_grav)
   const double* grav;
   long long grav_stride;
+  // optional [slot][E^3]: the stage update's density after the floors and
+  // before the RK3 combine (the provisional state a second gravity solve of
+  // the 6-solve cadence reads; tmgpu_forest_set_gravity_solver)
+  double* rho_save;
   unsigned long long* err;  // atomicMin of (slice << 32 | var-major interior index)
   int count;
 };
@@ -88,6 +92,13 @@ cudaError_t launch_gather_blocks(const double* const* src_dev, long long n, doub
                                  cudaStream_t st);
 cudaError_t launch_flag(const double* arena, long long stride, long long n, double theta, double rho_floor,
                         int* flag, cudaStream_t st);
+
+// 6-solve cadence: the stage's gravity source moved to the trapezoid of the
+// solves on the stage input (ga) and on its provisional density (gb); after
+// the RK3 combine, scaled by the stage weight w (grav_source.cu)
+cudaError_t launch_grav_correct(const double* in_arena, double* out_arena, long long nslots, const double* ga,
+                                const double* gb, long long gstride, const double* dt_ptr, double g_dt,
+                                double w, cudaStream_t st);
 
 cudaError_t launch_rk3_combine(int stage, const double* u0, const double* v, double* out,
                                long long n, cudaStream_t stream);

@@ -66,13 +66,29 @@ lib.tmgpu_forest_set_gravity.restype = C.c_int
 lib.tmgpu_forest_set_gravity.argtypes = [C.c_void_p, C.c_void_p, C.c_longlong, C.POINTER(TmgpuError)]
 
 
+lib.tmgpu_forest_set_gravity_solver.restype = C.c_int
+lib.tmgpu_forest_set_gravity_solver.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_void_p,
+                                                C.c_void_p, C.c_void_p, C.c_void_p, C.c_longlong,
+                                                C.POINTER(TmgpuError)]
+
+
 class GravityHydroDriver(HydroDriver):
-    """The gravity + hydro step of the metric (BASELINE.json): per step one AMR
-    FMM solve (paper_2412_15518_b200.gravity.GravityAMR, our specification —
-    the reference has no gravity) on the step's initial state, with
-    the angular-momentum correction, held fixed over the three RK stages as the
-    stage kernel's source term (m += dt*rho*g, E += dt*rho*(v.g); oracle
-    tmo_stage_subgrid_grav).
+    """The gravity + hydro step of the metric (BASELINE.json): the SSP-RK3 hydro
+    step with self-gravity from the AMR FMM (paper_2412_15518_b200.gravity.GravityAMR,
+    our specification — the reference has no gravity), with the
+    angular-momentum correction, as the stage kernel's source term (m += dt*rho*g,
+    E += dt*rho*(v.g); oracle tmo_stage_subgrid_grav). The solves run inside the
+    step (tmgpu_forest_set_gravity_solver):
+
+      solves_per_step=3  (default) before every RK stage on that stage's input
+                         state — the paper's coupling, one FMM iteration per
+                         hydro iteration
+      solves_per_step=6  the paper's count: per stage a second
+                         solve on the stage's provisional density moves the
+                         source to the trapezoid of the two fields
+                         (csrc/grav_source.cu)
+      solves_per_step=1  once per step on the initial state, held over the
+                         three stages (round-1 behaviour)
 
     On a distributed forest (Forest.distribute) the solve is distributed as a
     locally essential tree with a multipole-moment exchange (GravityAMR.distribute);
@@ -80,9 +96,13 @@ class GravityHydroDriver(HydroDriver):
     along (Forest.regrid) and rebuilds the gravity plan (single GPU)."""
 
     def __init__(self, forest: Forest, gamma: float = 1.4, cfl: float = 0.4, fast: bool = False,
-                 exact_ghosts: bool = False, am: bool = True, reflux: bool = False):
+                 exact_ghosts: bool = False, am: bool = True, reflux: bool = False,
+                 solves_per_step: int = 3):
+        if solves_per_step not in (1, 3, 6):
+            raise ValueError("solves_per_step must be 1, 3 or 6")
         super().__init__(forest, gamma, cfl, fast, exact_ghosts, reflux)
         self.am = am
+        self.solves_per_step = solves_per_step
         self._setup_gravity()
 
     def _setup_gravity(self) -> None:
@@ -110,10 +130,10 @@ class GravityHydroDriver(HydroDriver):
                     self.moment_transport = "peer"
                 except (_lib.CudaError, RuntimeError) as ex:
                     self.moment_transport = f"nccl (peer setup failed: {ex})"
-        # the solve runs on a side stream, overlapped with the CFL reduction and
-        # the first ghost exchange (multi-GPU: also the latency-bound moment
-        # exchange); the first stage kernel waits for it. TMGPU_GRAVITY_OVERLAP=0
-        # keeps it on the step's stream (same results, bit for bit)
+        # the solves run on a side stream, each overlapped with its stage's ghost
+        # exchange (stage 1: also the CFL reduction; multi-GPU: the latency-bound
+        # moment exchange); the stage kernel waits for it. TMGPU_GRAVITY_OVERLAP=0
+        # keeps them on the step's stream (same results, bit for bit)
         import os
 
         self.gstream = None
@@ -124,26 +144,20 @@ class GravityHydroDriver(HydroDriver):
         n = forest.local_count() * 512
         self.phi = torch.empty(n, dtype=torch.float64, device="cuda")
         self.g = torch.zeros(3 * n, dtype=torch.float64, device="cuda")
+        six = self.solves_per_step == 6
+        self.g2 = torch.zeros(3 * n, dtype=torch.float64, device="cuda") if six else None
+        self.rho_tilde = torch.zeros(n, dtype=torch.float64, device="cuda") if six else None
         err = TmgpuError()
-        _lib.check(lib.tmgpu_forest_set_gravity(forest.h, self.g.data_ptr(), n, C.byref(err)), err)
+        _lib.check(lib.tmgpu_forest_set_gravity_solver(
+            forest.h, self.gravity.h, self.solves_per_step, _lib.TMGPU_GRAV_AM if self.am else 0,
+            self.phi.data_ptr(), self.g.data_ptr(), self.g2.data_ptr() if six else None,
+            self.rho_tilde.data_ptr() if six else None, n, C.byref(err)), err)
 
     def solve_gravity(self, stream=None) -> None:
-        """Enqueue the solve (on the gravity stream after the work already on
-        `stream` — the state it reads — when distributed)."""
-        import torch
-
-        gs = stream
-        if self.gstream is not None:
-            if stream is None:
-                stream = torch.cuda.current_stream().cuda_stream
-            lib.tmgpu_stream_wait(self.gstream.cuda_stream, stream)
-            gs = self.gstream.cuda_stream
-        self.gravity.mass_from_arena(self.forest, gs)
-        self.gravity.solve(None, am=self.am, phi=self.phi, g=self.g, stream=gs, sync=False)
-
-    def step(self, dt: float | None = None, stream=None, sync: bool = True) -> float | None:
-        self.solve_gravity(stream)
-        return super().step(dt, stream, sync)
+        """Enqueue one stand-alone solve on the current state into (phi, g)
+        (the step solves by itself; this is for inspection)."""
+        self.gravity.mass_from_arena(self.forest, stream)
+        self.gravity.solve(None, am=self.am, phi=self.phi, g=self.g, stream=stream, sync=False)
 
     def regrid(self, refine=(), coarsen=()) -> None:
         """Refine then coarsen leaves with the state carried along (the
@@ -158,6 +172,8 @@ class GravityHydroDriver(HydroDriver):
 
     def close(self) -> None:
         err = TmgpuError()
+        lib.tmgpu_forest_set_gravity_solver(self.forest.h, None, 0, 0, None, None, None, None, 0,
+                                            C.byref(err))
         lib.tmgpu_forest_set_gravity(self.forest.h, None, 0, C.byref(err))
         lib.tmgpu_forest_set_gravity_stream(self.forest.h, None, C.byref(err))
 

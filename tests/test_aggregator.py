@@ -64,6 +64,22 @@ def test_pool_contract_errors():
 
 
 # ------------------------------------------------------------------ regions (GPU)
+def affine(n):
+    """The reference tests' toy kernel y = 2x + 1 (test_aggregator.cpp:17-29) as a
+    registered device kernel; it lives in tools/probes/libtmprobe.so, not in the
+    product library."""
+    import ctypes as C
+    import os
+    import sys
+
+    sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                                    "tools", "probes"))
+    import probe
+
+    fn = C.cast(probe.load().tmprobe_affine_launch, C.c_void_p).value
+    return A.DeviceKernel(fn, n, n)
+
+
 class Rig:
     def __init__(self):
         self.execs = A.ExecutorPool(4)
@@ -78,7 +94,7 @@ def test_full_batch_launches_once():
     """test_aggregator.cpp:91-107."""
     rig = Rig()
     busy = rig.pin_all_busy()
-    region = A.AggregationRegion(rig.execs, "affine", 4, 16, rig.counters, slice_len=4)
+    region = A.AggregationRegion(rig.execs, affine(4), 4, 16, rig.counters)
     futs = [region.submit_slice([1, 2, 3, 4]) for _ in range(4)]
     outs = A.when_all(futs)
     assert rig.counters.launches == 1 and rig.counters.fused_slices == 4
@@ -92,7 +108,7 @@ def test_five_submits_busy_launch_4_plus_1():
     """test_aggregator.cpp:109-122."""
     rig = Rig()
     busy = rig.pin_all_busy()
-    region = A.AggregationRegion(rig.execs, "affine", 4, 16, rig.counters, slice_len=2)
+    region = A.AggregationRegion(rig.execs, affine(2), 4, 16, rig.counters)
     futs = [region.submit_slice([0, 0]) for _ in range(5)]
     assert rig.counters.launches == 1
     region.flush()
@@ -105,7 +121,7 @@ def test_five_submits_busy_launch_4_plus_1():
 def test_idle_executor_launches_immediately():
     """test_aggregator.cpp:124-134."""
     rig = Rig()
-    region = A.AggregationRegion(rig.execs, "affine", 4, 16, rig.counters, slice_len=2)
+    region = A.AggregationRegion(rig.execs, affine(2), 4, 16, rig.counters)
     f = region.submit_slice([5, 6])
     assert rig.counters.launches == 1 and rig.counters.fused_slices == 1
     assert f.get()[0] == 11.0
@@ -116,11 +132,11 @@ def test_flush_empty_and_idempotent():
     """test_aggregator.cpp:136-159."""
     rig = Rig()
     busy = rig.pin_all_busy()
-    region = A.AggregationRegion(rig.execs, "affine", 4, 16, rig.counters, slice_len=2)
+    region = A.AggregationRegion(rig.execs, affine(2), 4, 16, rig.counters)
     region.flush()
     region.flush()
     assert rig.counters.launches == 0
-    r2 = A.AggregationRegion(rig.execs, "affine", 8, 16, rig.counters, slice_len=2)
+    r2 = A.AggregationRegion(rig.execs, affine(2), 8, 16, rig.counters)
     futs = [r2.submit_slice([0, 0]) for _ in range(3)]
     r2.flush()
     r2.flush()
@@ -133,14 +149,14 @@ def test_flush_empty_and_idempotent():
 def test_contract_errors():
     """test_aggregator.cpp:161-170."""
     rig = Rig()
-    region = A.AggregationRegion(rig.execs, "affine", 4, 16, rig.counters, slice_len=2)
+    region = A.AggregationRegion(rig.execs, affine(2), 4, 16, rig.counters)
     with pytest.raises(A.AggError):
         region.submit_slice([1, 2, 3])
     region.flush()
     with pytest.raises(A.AggError):
         region.submit_slice([1, 2])
     with pytest.raises(A.AggError):
-        A.AggregationRegion(rig.execs, "affine", 0, 16, slice_len=2)
+        A.AggregationRegion(rig.execs, affine(2), 0, 16)
 
 
 @pytest.mark.gpu
@@ -152,7 +168,7 @@ def test_fused_equals_solo_bitwise(max_slices):
     solo = 2.0 * inputs + 1.0
     rig = Rig()
     busy = rig.pin_all_busy()
-    region = A.AggregationRegion(rig.execs, "affine", max_slices, 100, rig.counters, slice_len=8)
+    region = A.AggregationRegion(rig.execs, affine(8), max_slices, 100, rig.counters)
     futs = [region.submit_slice(s) for s in inputs]
     region.flush()
     for f, want in zip(futs, solo):
@@ -166,7 +182,7 @@ def test_monotone_batching():
     """test_aggregator.cpp:209-223."""
     rig = Rig()
     busy = rig.pin_all_busy()
-    region = A.AggregationRegion(rig.execs, "affine", 4, 28, rig.counters, slice_len=2)
+    region = A.AggregationRegion(rig.execs, affine(2), 4, 28, rig.counters)
     futs = [region.submit_slice([0, 0]) for _ in range(28)]
     assert rig.counters.launches == 7
     region.flush()
@@ -179,7 +195,7 @@ def test_monotone_batching():
 def test_no_lost_slices_under_concurrency():
     """test_aggregator.cpp:225-247: 3 submitter threads x 200."""
     rig = Rig()
-    region = A.AggregationRegion(rig.execs, "affine", 8, 600, rig.counters, slice_len=4)
+    region = A.AggregationRegion(rig.execs, affine(4), 8, 600, rig.counters)
     futs, mu = [], threading.Lock()
 
     def work():
@@ -201,7 +217,7 @@ def test_no_lost_slices_under_concurrency():
 def test_in_flight_returns_to_zero():
     """test_aggregator.cpp:249-262."""
     rig = Rig()
-    region = A.AggregationRegion(rig.execs, "affine", 2, 32, rig.counters, slice_len=2)
+    region = A.AggregationRegion(rig.execs, affine(2), 2, 32, rig.counters)
     futs = [region.submit_slice([0, 0]) for _ in range(32)]
     region.flush()
     A.when_all(futs)

@@ -11,12 +11,14 @@ pytestmark = pytest.mark.gpu
 @pytest.mark.parametrize("mode,n", [(0, 1 << 31), (1, 1 << 31), (2, 1 << 30), (3, 1 << 31),
                                     (4, 1 << 31)])
 def test_fastmath_bitwise(mode, n):
-    from paper_2412_15518_b200 import _lib
+    import os
+    import sys
 
-    f = _lib.lib.tmgpu_selftest_fastmath
-    f.restype = C.c_int
-    f.argtypes = [C.c_int, C.c_longlong, C.c_uint64, C.POINTER(C.c_ulonglong),
-                  C.POINTER(C.c_ulonglong), C.POINTER(C.c_double), C.c_void_p]
+    sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                                    "tools", "probes"))
+    import probe  # tools/probes/libtmprobe.so: the self-test is not in the product library
+
+    f = probe.load().tmgpu_selftest_fastmath
     bad, chk = C.c_ulonglong(0), C.c_ulonglong(0)
     first = (C.c_double * 2)()
     assert f(mode, n, 0x2412_15518 + mode, C.byref(bad), C.byref(chk), first, None) == 0

@@ -140,3 +140,25 @@ def test_scenario_state_is_deterministic():
     b = f.scenario_state(amr.Scenario.rotating_star, 7)
     assert a.tobytes() == b.tobytes()
     assert np.all(a[:, 0] > 0) and np.isfinite(a).all()
+
+
+@pytest.mark.parametrize("kind,lo,hi,bc", [(amr.Scenario.rotating_star, 2, 5, (0, 0, 0)),
+                                           (amr.Scenario.double_white_dwarf, 2, 5, (0, 0, 0)),
+                                           (amr.Scenario.sod, 2, 5, (0, 1, 1)),
+                                           (amr.Scenario.sedov, 2, 5, (0, 0, 0))])
+def test_scenarios_built_on_the_reference_tree_match(ref, kind, lo, hi, bc):
+    """bench.py's reference arm builds its workload on the reference Tree
+    (oracle/ref_capi.cpp tmref_tree_scenario/_fill): the same leaves in the
+    same order and the same initial state, bit for bit, as the product's
+    scenario (csrc/scenario.cpp) the GPU arm times."""
+    t = ref.tree(max_level=hi, bc=bc)
+    t.scenario(int(kind), lo, hi, 0.1)
+    f = amr.build_scenario(kind, lo, hi, 0.1, bc=bc)
+    assert np.array_equal(t.leaves(), np.array(f.leaves(), dtype=np.uint64))
+    st = f.scenario_state(kind)
+    for i, p in enumerate(f.leaves()):
+        g = t.grid(int(p)).reshape(5, 12, 12, 12)
+        assert g[:, 2:10, 2:10, 2:10].reshape(5, 512).tobytes() == st[i].tobytes()
+        assert not g[:, :2].any()  # ghosts zero
+    lv = t.leaf_levels()
+    assert [tuple(r) for r in lv[:3]] == [amr.unpack(int(p)) for p in f.leaves()[:3]]

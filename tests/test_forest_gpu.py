@@ -147,3 +147,21 @@ def test_uniform_l4_conservation_and_fast_mode():
     scale = np.abs(out).max(axis=(0, 2))
     for v in range(5):
         assert np.all(np.abs(o2[:, v] - out[:, v]) <= 1e-9 * scale[v])
+
+
+@pytest.mark.parametrize("kind,bc,leaves", [(amr.Scenario.sod, (0, 1, 1), 19104),
+                                            (amr.Scenario.sedov, (0, 0, 0), 6672)])
+def test_c4_sod_sedov_6level_step_bitwise_vs_reference(ref, kind, bc, leaves):
+    """BASELINE.json configs[3] at full size (hydro-only, 6-level AMR, leaf
+    levels 2..6): two device steps vs the reference's own composed step
+    (fill_ghosts_sync + AggregationRegion(make_stage_kernel) + rk3_combine)."""
+    f, t = _step_pair(ref, kind, 2, 6, bc)
+    assert f.leaf_count() == leaves
+    mask = interior_mask()
+    drv = HydroDriver(f)
+    for step in range(2):
+        dt = drv.step()
+        t.hydro_step(dt, workers=8, max_slices=8)
+        grids = f.get_grids()
+        for i, p in enumerate(f.leaves()):
+            assert grids[i][mask].tobytes() == t.grid(int(p))[mask].tobytes(), f"step {step} leaf {i}"

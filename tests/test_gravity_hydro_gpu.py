@@ -1,9 +1,8 @@
-"""The gravity + hydro step (GravityHydroDriver) vs the oracle composition:
-AMR FMM specification (gravity_amr_oracle.c, with the angular-momentum
-correction) -> per RK stage: ghost fill (tmo_fill_ghosts_sync) -> stage with the
-gravity source (tmo_stage_subgrid_grav) -> rk3_combine. Bitwise."""
-import ctypes as C
-
+"""The gravity + hydro step (GravityHydroDriver) vs the oracle composition
+(tests/helpers.py oracle_gravity_step): AMR FMM specification
+(gravity_amr_oracle.c, with the angular-momentum correction) at 1, 3 or 6
+solves per step -> per RK stage: ghost fill (tmo_fill_ghosts_sync) -> stage
+with the gravity source (tmo_stage_subgrid_grav) -> rk3_combine. Bitwise."""
 import numpy as np
 import pytest
 
@@ -12,45 +11,17 @@ from paper_2412_15518_b200 import amr
 from paper_2412_15518_b200.driver import GravityHydroDriver
 from paper_2412_15518_b200.gravity import forest_leaf_array
 
-from helpers import interior_to_ghosted
+from helpers import interior_to_ghosted, oracle_gravity_step
 
 pytestmark = pytest.mark.gpu
 
-dp = C.POINTER(C.c_double)
-ip = C.POINTER(C.c_int)
 
 
-def oracle_gravity_step(o, t, grids, lv, dt, gamma=1.4):
-    n = len(grids)
-    h = 1.0 / (8.0 * 2.0 ** lv[:, 0].astype(np.float64))
-    interior = [g.reshape(5, 12, 12, 12)[:, 2:10, 2:10, 2:10].reshape(5, 512).copy() for g in grids]
-    m = np.stack([u[0] for u in interior]) * (h * h * h)[:, None]
-    _, gfield, _ = o.grav_amr(lv, m, flags=1)
-    u0 = interior
-    bad = (C.c_int * 3)()
-    for stage in (1, 2, 3):
-        t.fill_ghosts(grids)
-        outs = []
-        for i in range(n):
-            hdr = np.array([1.0, h[i], dt, gamma, 0.0, 0.0, 0.0, 0.0])
-            out = np.zeros(5 * 512 + 6 * 5 * 64 + 1)
-            gi = np.ascontiguousarray(gfield[:, i * 512:(i + 1) * 512])
-            rc = o.lib.tmo_stage_subgrid_grav(hdr.ctypes.data_as(dp), 8, 2, 5, grids[i].ctypes.data_as(dp),
-                                              gi.ctypes.data_as(dp), out.ctypes.data_as(dp), bad)
-            assert rc == 0
-            v = out[:2560].reshape(5, 512)
-            if stage == 2:
-                v = u0[i] + 0.25 * (v - u0[i])
-            elif stage == 3:
-                v = u0[i] + (2.0 / 3.0) * (v - u0[i])
-            outs.append(v)
-        for i in range(n):
-            grids[i].reshape(5, 12, 12, 12)[:, 2:10, 2:10, 2:10] = outs[i].reshape(5, 8, 8, 8)
-    return grids
-
-
+@pytest.mark.parametrize("cadence", [1, 3, 6])
 @pytest.mark.parametrize("exact", [False, True])
-def test_gravity_hydro_step_bitwise_vs_oracle(exact):
+def test_gravity_hydro_step_bitwise_vs_oracle(exact, cadence):
+    if exact and cadence == 6:
+        pytest.skip("the 6-solve cadence runs on the fused (ping-pong) step only")
     f = amr.build_scenario(amr.Scenario.rotating_star, 1, 3)
     st = f.scenario_state(amr.Scenario.rotating_star)
     f.alloc()
@@ -59,15 +30,45 @@ def test_gravity_hydro_step_bitwise_vs_oracle(exact):
     o = O.Oracle()
     t = o.tree([int(p) for p in f.leaves()])
     grids = [np.ascontiguousarray(g) for g in interior_to_ghosted(st)]
-    drv = GravityHydroDriver(f, am=True, exact_ghosts=exact)
+    drv = GravityHydroDriver(f, am=True, exact_ghosts=exact, solves_per_step=cadence)
     dt = 2e-3
     for step in range(2):
         drv.step(dt=dt)
-        grids = oracle_gravity_step(o, t, grids, lv, dt)
+        grids = oracle_gravity_step(o, t, grids, lv, dt, cadence)
         got = f.get_interior()
         want = np.stack([g.reshape(5, 12, 12, 12)[:, 2:10, 2:10, 2:10].reshape(5, 512) for g in grids])
         assert got.tobytes() == want.tobytes(), f"step {step}"
-    # gravity changes the step: the same step without it differs
+    drv.close()
+
+
+def test_gravity_cadences_differ_and_converge():
+    """The three cadences are different schemes (not relabellings) and agree
+    to O(dt^2) relative: per-stage fields differ from the held field."""
+    res = {}
+    for cad in (1, 3, 6):
+        f = amr.build_scenario(amr.Scenario.rotating_star, 2, 3)
+        st = f.scenario_state(amr.Scenario.rotating_star)
+        f.alloc()
+        f.set_interior(st)
+        drv = GravityHydroDriver(f, am=True, solves_per_step=cad)
+        for _ in range(2):
+            drv.step(dt=2e-3)
+        res[cad] = f.get_interior()
+        drv.close()
+    m1, m3, m6 = (res[c][:, 1:4] for c in (1, 3, 6))
+    scale = np.abs(m3).max()
+    assert np.abs(m1 - m3).max() > 0 and np.abs(m3 - m6).max() > 0
+    assert np.abs(m1 - m3).max() < 1e-2 * scale and np.abs(m3 - m6).max() < 1e-2 * scale
+
+
+def test_gravity_cadence_rejects_bad_arguments():
+    f = amr.build_scenario(amr.Scenario.rotating_star, 1, 2)
+    f.alloc()
+    with pytest.raises(ValueError):
+        GravityHydroDriver(f, solves_per_step=2)
+    drv = GravityHydroDriver(f, solves_per_step=6, exact_ghosts=True)
+    with pytest.raises(Exception, match="6-solve"):
+        drv.step(dt=1e-3)
     drv.close()
 
 

@@ -5,10 +5,11 @@ import ctypes as C
 import os
 import sys
 
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-from paper_2412_15518_b200 import _lib  # noqa: E402
+sys.path.insert(0, os.path.join(os.path.dirname(os.path.abspath(__file__)), "probes"))
+import probe  # noqa: E402  tools/probes/libtmprobe.so
 
-f = _lib.lib.tmgpu_fp64_probe
+plib = probe.load()
+f = plib.tmgpu_fp64_probe
 f.argtypes = [C.c_int, C.c_int, C.c_int, C.POINTER(C.c_double)]
 for warps in (4, 8, 16, 32):
     row = []
@@ -18,7 +19,7 @@ for warps in (4, 8, 16, 32):
         row.append(f"{t.value:6.2f}")
     print(f"warps/SM {warps:2d}: chains 1,2,4,8,16 -> TFLOP/s", " ".join(row))
 
-g = _lib.lib.tmgpu_dmma_probe
+g = plib.tmgpu_dmma_probe
 g.argtypes = [C.c_int, C.c_int, C.c_int, C.POINTER(C.c_double)]
 for warps in (4, 8, 16, 32):
     row = []
@@ -28,7 +29,7 @@ for warps in (4, 8, 16, 32):
         row.append(f"{t.value:6.2f}")
     print(f"DMMA m8n8k4 warps/SM {warps:2d}: chains 1,2,4,8 -> TFLOP/s", " ".join(row))
 
-h = _lib.lib.tmgpu_dfma3_probe
+h = plib.tmgpu_dfma3_probe
 h.argtypes = [C.c_int, C.c_int, C.POINTER(C.c_double)]
 row = []
 for warps in (4, 8, 16, 32):

@@ -1,9 +1,10 @@
-// Device self-test of fastmath.cuh: bitwise comparison of the branch-free
+// NOT PRODUCT CODE (tools/probes -> libtmprobe.so, loaded by tests/test_fastmath_gpu.py):
+// device self-test of the product's fastmath.cuh: bitwise comparison of the branch-free
 // division / square root with the IEEE operators over random operands.
 #include <cstdint>
 
 #include "fastmath.cuh"
-#include "tmgpu_internal.h"
+#include "tmgpu_internal.h"  // error codes, cuda_err (product header, -I)
 
 namespace tmgpu {
 namespace {
@@ -80,7 +81,6 @@ extern "C" int tmgpu_selftest_fastmath(int mode, long long n, uint64_t seed,
   if (e == cudaSuccess) e = cudaMemset(f, 0, 2 * sizeof(double));
   if (e == cudaSuccess) {
     fm_selftest_kernel<<<148 * 16, 256>>>(seed, n, mode, d, d + 1, f);
-    g_launches.fetch_add(1);
     e = cudaDeviceSynchronize();
   }
   unsigned long long h[2] = {0, 0};

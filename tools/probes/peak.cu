@@ -1,6 +1,7 @@
-// FP64 pipe peak microbenchmark (roofline denominator: MEASURED_PEAKS.json has
+// NOT PRODUCT CODE (tools/probes -> tools/probes/libtmprobe.so, loaded by bench.py and
+// tools/*): FP64 pipe peak microbenchmark (roofline denominator: MEASURED_PEAKS.json has
 // no FP64 entry). Each thread runs 8 independent DFMA chains; FLOP = 2 per FMA.
-#include "tmgpu_internal.h"
+#include "tmgpu_internal.h"  // error codes, cuda_err (product header, -I)
 
 namespace tmgpu {
 namespace {
@@ -184,7 +185,6 @@ extern "C" int tmgpu_fp64_peak(int iters, double* tflops, double* ms, tmgpu_erro
   e = cudaEventSynchronize(t1);
   float msf = 0;
   cudaEventElapsedTime(&msf, t0, t1);
-  g_launches.fetch_add(2);
   cudaEventDestroy(t0);
   cudaEventDestroy(t1);
   cudaFree(d);

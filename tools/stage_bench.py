@@ -53,8 +53,10 @@ for _ in range(a.iters):
 ms = float(np.median(t))
 cells = a.count * 512
 peak = C.c_double(0); pms = C.c_double(0)
-_lib.lib.tmgpu_fp64_peak.argtypes = [C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_double), C.c_void_p]
-_lib.lib.tmgpu_fp64_peak(20000, C.byref(peak), C.byref(pms), None)
+sys.path.insert(0, os.path.join(os.path.dirname(os.path.abspath(__file__)), "probes"))
+import probe  # noqa: E402  tools/probes/libtmprobe.so
+
+probe.load().tmgpu_fp64_peak(20000, C.byref(peak), C.byref(pms), None)
 res = {"count": a.count, "fast": a.fast, "ms_median": ms, "ms_min": min(t),
        "cell_stage_per_s": cells / (ms * 1e-3),
        "slice_GBps": a.count * (ins + outs) * 8 / (ms * 1e-3) / 1e9,
