@@ -247,9 +247,26 @@ __device__ __forceinline__ void m2l_term(const double (&m)[10], const double (&e
 // reaches (jj = sx - 2k in {pe, pe+2, pe+4}): ~6 shared loads per interaction.
 // Near rows skip jj = 2, 3 (near for both x parities); jj = 1 (a = 0) and
 // jj = 4 (a = 1) use zeroed near geometry (exact no-ops, see above).
+// The same term for a source whose D and Q are +0 (a leaf cell, or a missing
+// cell's zero moments): every dropped operation is an exact no-op (see
+// amr_m2l_mono_kernel), so this is m2l_term's result bit for bit.
+template <int NOUT>
+__device__ __forceinline__ void m2l_term_mono(const double nM, const double (&e)[kTab], double (&o)[10]) {
+  o[0] = o[0] + nM * e[0];
+  o[1] = fma(nM, e[1], o[1]);
+  o[2] = fma(nM, e[2], o[2]);
+  o[3] = fma(nM, e[3], o[3]);
+#pragma unroll
+  for (int q = 0; q < NOUT - 4; ++q) o[4 + q] = fma(nM, e[4 + q], o[4 + q]);
+}
+
+// full[0..2]: does any lane of the warp take a source of this row from an
+// internal patch at x-offset -1, 0, +1 (warp votes; a warp whose sources in a
+// group are all leaf cells runs the monopole term for the group)
 template <bool NEAR, int NOUT>
 __device__ __forceinline__ void m2l_row_par(const double* __restrict__ src,
-                                            const double* __restrict__ trow, double (&acc)[4][10]) {
+                                            const double* __restrict__ trow, double (&acc)[4][10],
+                                            const bool (&full)[3]) {
 #pragma unroll
   for (int pe = 0; pe < 2; ++pe) {
     double G[3][kTab];
@@ -269,15 +286,27 @@ __device__ __forceinline__ void m2l_row_par(const double* __restrict__ src,
 #pragma unroll
     for (int mi = 0; mi < 6; ++mi) {
       const int sx = pe + 2 * mi;
-      double m[10];
+      const int grp = sx < 2 ? 0 : (sx > 9 ? 2 : 1);
+      if (full[grp]) {
+        double m[10];
 #pragma unroll
-      for (int q = 0; q < 10; ++q) m[q] = src[q * kWVar + sx];
+        for (int q = 0; q < 10; ++q) m[q] = src[q * kWVar + sx];
 #pragma unroll
-      for (int t = 0; t < 3; ++t) {
-        const int k = mi - t;
-        if (k < 0 || k > 3) continue;
-        if (NEAR && t == 1) continue;
-        m2l_term<NOUT>(m, G[t], acc[k]);
+        for (int t = 0; t < 3; ++t) {
+          const int k = mi - t;
+          if (k < 0 || k > 3) continue;
+          if (NEAR && t == 1) continue;
+          m2l_term<NOUT>(m, G[t], acc[k]);
+        }
+      } else {
+        const double nM = -src[sx];
+#pragma unroll
+        for (int t = 0; t < 3; ++t) {
+          const int k = mi - t;
+          if (k < 0 || k > 3) continue;
+          if (NEAR && t == 1) continue;
+          m2l_term_mono<NOUT>(nM, G[t], acc[k]);
+        }
       }
     }
   }
@@ -295,7 +324,8 @@ __device__ __forceinline__ void cp_async8(double* smem, const double* gmem, bool
 // compact leaf locals [4][512]).
 template <int NOUT>
 __device__ __forceinline__ void m2l_patch(double* __restrict__ win, const double* __restrict__ tabs,
-                                          double* __restrict__ loc, int n, double* __restrict__ lloc) {
+                                          double* __restrict__ loc, int n, double* __restrict__ lloc,
+                                          unsigned internal27) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int b = warp & 1, c = (warp >> 1) & 1, half = warp >> 2;
   const int a = lane & 1, Y = (lane >> 1) & 3, Z = lane >> 3;
@@ -315,10 +345,17 @@ __device__ __forceinline__ void m2l_patch(double* __restrict__ win, const double
       // source row: window y = 2Y + iy, z = 2Z + iz (parent-aligned, parity-free)
       const double* src = win + ((iz & 1) * 2 + (iy & 1)) * kWSub + (Z + (iz >> 1)) * kWPZ +
                           (Y + (iy >> 1)) * kWPY;
+      // this lane's source row lies in neighbour row (oy, oz); internal patches there?
+      const int wy = 2 * Y + iy, wz = 2 * Z + iz;
+      const int oy = wy < 2 ? 0 : (wy > 9 ? 2 : 1), oz = wz < 2 ? 0 : (wz > 9 ? 2 : 1);
+      const unsigned rowbits = (internal27 >> ((oz * 3 + oy) * 3)) & 7u;
+      const bool full[3] = {__any_sync(0xffffffffu, rowbits & 1u) != 0,
+                            __any_sync(0xffffffffu, rowbits & 2u) != 0,
+                            __any_sync(0xffffffffu, rowbits & 4u) != 0};
       if (dz >= -1 && dz <= 1 && dy >= -1 && dy <= 1)
-        m2l_row_par<true, NOUT>(src, trow, acc);
+        m2l_row_par<true, NOUT>(src, trow, acc, full);
       else
-        m2l_row_par<false, NOUT>(src, trow, acc);
+        m2l_row_par<false, NOUT>(src, trow, acc, full);
     }
   }
   // upper-half warps hand their partial sums to the lower-half warps (the
@@ -391,51 +428,191 @@ __global__ void __launch_bounds__(kM2lThreads, 1) amr_m2l_fused_kernel(
       cp_async8(dst + wx, src, nb >= 0);
     }
   }
+  // neighbour patches that are internal (full moments): bit o of internal27
+  unsigned internal27 = 0;
+  for (int o = 0; o < 27; ++o) {
+    const int nb = nb27[o];
+    if (nb >= 0 && L.leaf_slot[nb] < 0) internal27 |= 1u << o;
+  }
   asm volatile("cp.async.wait_all;\n" ::: "memory");
   __syncthreads();
   const int leaf = L.leaf_slot[n];
   // leaf patch below the root: L0, L_i into the compact leaf locals (L2P's
   // input); a leaf root keeps all ten (the dense levels' L2L adds into them)
   if (leaf >= 0 && l > 0)
-    m2l_patch<4>(win, tabs, L.loc, n, lloc + (long long)(leaf - lo) * 2048);
+    m2l_patch<4>(win, tabs, L.loc, n, lloc + (long long)(leaf - lo) * 2048, internal27);
   else
-    m2l_patch<10>(win, tabs, L.loc, n, nullptr);
+    m2l_patch<10>(win, tabs, L.loc, n, nullptr, internal27);
+}
+
+// ---- M2L of leaf patches among leaf patches (monopole sources) -------------
+// A leaf patch whose existing 27 neighbours are all leaf patches (5,000 of the
+// 6,729 patches on C3) has only leaf cells as V sources, and a leaf cell's
+// moments are (m, +0, ..., +0). Every D/Q term of the specification's M2L term
+// is then an exact no-op (fma(+-0, e, x) = x for x != 0, and an accumulator that
+// starts at +0 never becomes -0; the same argument as amr_m2m_kernel's leaf
+// children), so per interaction only
+//   t = -m * e0;  L0 = L0 + t;  L_i = fma(-m, e_i, L_i)        (i = 1..3)
+// remain — 5 of the 23 operations into a leaf target, bit for bit the full
+// term's result. The source window is then the 12^3 masses (from the compact
+// [slot][512] mass array, not the 80-byte moments), 16 KB instead of 161 KB,
+// so several CTAs share an SM. Thread mapping, source order and the two
+// partial sums are m2l_patch's.
+constexpr int kMonoWin = 2048;  // >= 4 * kWSub + 2 (window) and the 4 x 4 x 128 partial sums
+constexpr size_t kMonoSmem = (size_t)(kMonoWin + kOff3 * 4) * sizeof(double);  // 27,360 B
+
+template <bool NEAR>
+__device__ __forceinline__ void mono_row(const double* __restrict__ src, const double* __restrict__ trow,
+                                         double (&acc)[4][4]) {
+#pragma unroll
+  for (int pe = 0; pe < 2; ++pe) {
+    double G[3][4];
+#pragma unroll
+    for (int t = 0; t < 3; ++t) {
+      if (NEAR && t == 1) continue;
+      const double2* t2 = reinterpret_cast<const double2*>(trow + (pe + 2 * t) * 4);
+      const double2 u = t2[0], v = t2[1];
+      G[t][0] = u.x, G[t][1] = u.y, G[t][2] = v.x, G[t][3] = v.y;
+    }
+#pragma unroll
+    for (int mi = 0; mi < 6; ++mi) {
+      const double nM = -src[pe + 2 * mi];
+#pragma unroll
+      for (int t = 0; t < 3; ++t) {
+        const int k = mi - t;
+        if (k < 0 || k > 3) continue;
+        if (NEAR && t == 1) continue;
+        acc[k][0] = acc[k][0] + nM * G[t][0];
+        acc[k][1] = fma(nM, G[t][1], acc[k][1]);
+        acc[k][2] = fma(nM, G[t][2], acc[k][2]);
+        acc[k][3] = fma(nM, G[t][3], acc[k][3]);
+      }
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kM2lThreads, 4) amr_m2l_mono_kernel(
+    const long long* __restrict__ slots, const int* __restrict__ slot_level, const double* __restrict__ mass,
+    const int* __restrict__ slot_nbs, const double* __restrict__ tab_all, double* __restrict__ lloc,
+    long long lo) {
+  extern __shared__ double sm[];
+  double* win = sm;
+  double* tabs = sm + kMonoWin;
+  const long long s = slots[blockIdx.x];
+  const int l = slot_level[s];
+  const double* tab = tab_all + (long long)(l + 3) * kOff3 * kTab;
+  for (int q = threadIdx.x; q < kOff3 * 4; q += kM2lThreads) {
+    const int o = q >> 2;
+    const int dx = o % kOff - 3, dy = (o / kOff) % kOff - 3, dz = o / (kOff * kOff) - 3;
+    const bool near = dx >= -1 && dx <= 1 && dy >= -1 && dy <= 1 && dz >= -1 && dz <= 1;
+    cp_async8(tabs + q, tab + (long long)o * kTab + (q & 3), !near);
+  }
+  const int* nb27 = slot_nbs + s * 27;
+  for (int t = threadIdx.x; t < 1728; t += kM2lThreads) {
+    const int wx = t % 12, wy = (t / 12) % 12, wz = t / 144;
+    const int ox = wx < 2 ? -1 : (wx > 9 ? 1 : 0), oy = wy < 2 ? -1 : (wy > 9 ? 1 : 0),
+              oz = wz < 2 ? -1 : (wz > 9 ? 1 : 0);
+    const int nb = nb27[((oz + 1) * 3 + (oy + 1)) * 3 + ox + 1];
+    const int lx = wx - 2 - 8 * ox, ly = wy - 2 - 8 * oy, lz = wz - 2 - 8 * oz;
+    double* dst = win + ((wz & 1) * 2 + (wy & 1)) * kWSub + (wz >> 1) * kWPZ + (wy >> 1) * kWPY + wx;
+    cp_async8(dst, mass + ((long long)(nb < 0 ? s : nb) * 512 + (lz * 8 + ly) * 8 + lx), nb >= 0);
+  }
+  asm volatile("cp.async.wait_all;\n" ::: "memory");
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int b = warp & 1, c = (warp >> 1) & 1, half = warp >> 2;
+  const int a = lane & 1, Y = (lane >> 1) & 3, Z = lane >> 3;
+  double acc[4][4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) acc[k][q] = 0.0;
+  const double* tab_lane = tabs + (1 - a) * 4;
+  for (int iz = 3 * half; iz < 3 * half + 3; ++iz) {
+    const int dz = iz - 2 - c;
+#pragma unroll 2
+    for (int iy = 0; iy < 6; ++iy) {
+      const int dy = iy - 2 - b;
+      const double* trow = tab_lane + ((dz + 3) * kOff + (dy + 3)) * kOff * 4;
+      const double* src = win + ((iz & 1) * 2 + (iy & 1)) * kWSub + (Z + (iz >> 1)) * kWPZ + (Y + (iy >> 1)) * kWPY;
+      if (dz >= -1 && dz <= 1 && dy >= -1 && dy <= 1)
+        mono_row<true>(src, trow, acc);
+      else
+        mono_row<false>(src, trow, acc);
+    }
+  }
+  __syncthreads();  // the window is dead: the upper half hands over its partial sums
+  const int pair = threadIdx.x & 127;
+  if (half) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) win[(k * 4 + q) * 128 + pair] = acc[k][q];
+  }
+  __syncthreads();
+  if (half) return;
+  const int y = 2 * Y + b, z = 2 * Z + c;
+  double* out = lloc + (s - lo) * 2048;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int cell = (z * 8 + y) * 8 + a + 2 * k;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) out[q * 512 + cell] = acc[k][q] + win[(k * 4 + q) * 128 + pair];
+  }
 }
 
 // W/X pairs (AMR level jumps) after the V-list sums, in the list's sorted
 // order, one thread per target with entries (targets in patch order);
 // geometry from the plan's separation table (m2l_geom of each distinct R).
+// mgeo[e] < 0 marks an entry whose source is a leaf cell (moments (m, +0, ...)):
+// its geometry row is ~mgeo[e] and the monopole term is applied (bit for bit
+// the full term, see amr_m2l_mono_kernel), reading 1 moment and 4 geometry
+// values instead of 10 and 13.
+template <int NOUT>
+__device__ __forceinline__ void wx_mono(double nM, const double* __restrict__ e, double* acc) {
+  acc[0] = acc[0] + nM * __ldg(e);
+  acc[1] = fma(nM, __ldg(e + 1), acc[1]);
+  acc[2] = fma(nM, __ldg(e + 2), acc[2]);
+  acc[3] = fma(nM, __ldg(e + 3), acc[3]);
+#pragma unroll
+  for (int q = 0; q < NOUT - 4; ++q) acc[4 + q] = fma(nM, __ldg(e + 4 + q), acc[4 + q]);
+}
+
 template <int NOUT>
 __device__ __forceinline__ void wx_entries(const GLv* __restrict__ Lv, const long long* __restrict__ ment,
                                            const int* __restrict__ mgeo, long long e0, long long e1,
                                            const double* __restrict__ geo, double* acc) {
   long long e = e0;
-  for (; e + 3 < e1; e += 4) {  // four entries' loads in flight, applied in order
+  for (; e + 3 < e1; e += 4) {  // four entries' first loads in flight, applied in order
     long long enc[4];
     int gi[4];
+    double m0[4];
 #pragma unroll
     for (int u = 0; u < 4; ++u) enc[u] = __ldg(ment + e + u), gi[u] = __ldg(mgeo + e + u);
-    double m[4][10], G[4][kTab];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) m0[u] = __ldg(Lv[enc[u] >> 40].mom + (enc[u] & ((1LL << 40) - 1)) * 10);
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
-      const double* pm = Lv[enc[u] >> 40].mom + (enc[u] & ((1LL << 40) - 1)) * 10;
-      const double* pg = geo + (long long)gi[u] * kTab;
-#pragma unroll
-      for (int q = 0; q < 10; ++q) m[u][q] = __ldg(pm + q);
-#pragma unroll
-      for (int q = 0; q < kTab; ++q) G[u][q] = __ldg(pg + q);
-    }
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      if constexpr (NOUT == 10) m2l_tab(m[u], G[u], acc);
-      else m2l_tab4(m[u], G[u], acc);
+      if (gi[u] < 0) {
+        wx_mono<NOUT>(-m0[u], geo + (long long)(~gi[u]) * kTab, acc);
+      } else {
+        const double* pm = Lv[enc[u] >> 40].mom + (enc[u] & ((1LL << 40) - 1)) * 10;
+        if constexpr (NOUT == 10) m2l_tab(pm, geo + (long long)gi[u] * kTab, acc);
+        else m2l_tab4(pm, geo + (long long)gi[u] * kTab, acc);
+      }
     }
   }
   for (; e < e1; ++e) {
     const long long enc = ment[e];
     const double* mom = Lv[enc >> 40].mom + (enc & ((1LL << 40) - 1)) * 10;
-    if constexpr (NOUT == 10) m2l_tab(mom, geo + (long long)mgeo[e] * kTab, acc);
-    else m2l_tab4(mom, geo + (long long)mgeo[e] * kTab, acc);
+    const int gi = mgeo[e];
+    if (gi < 0) {
+      wx_mono<NOUT>(-mom[0], geo + (long long)(~gi) * kTab, acc);
+    } else if constexpr (NOUT == 10) {
+      m2l_tab(mom, geo + (long long)gi * kTab, acc);
+    } else {
+      m2l_tab4(mom, geo + (long long)gi * kTab, acc);
+    }
   }
 }
 
@@ -591,7 +768,8 @@ __global__ void __launch_bounds__(512) amr_l2p_kernel(const GLv* __restrict__ Lv
                                                       double* __restrict__ phi, double* __restrict__ g,
                                                       double* __restrict__ part) {
   __shared__ double w26[27][4];
-  __shared__ long long nbslot[27];
+  __shared__ double mw[1000];  // masses of the patch and its one-cell halo, [z 10][y 10][x 10]
+  __shared__ unsigned valid27;  // bit o: same-depth neighbour leaf patch o exists
   const long long ls = blockIdx.x;  // local slot
   const long long s = lo + ls;
   const int l = slot_level[s], n = slot_node[s];
@@ -602,8 +780,18 @@ __global__ void __launch_bounds__(512) amr_l2p_kernel(const GLv* __restrict__ Lv
     const int o = threadIdx.x;
 #pragma unroll
     for (int q = 0; q < 4; ++q) w26[o][q] = p2p_tab[((long long)d * 27 + o) * 4 + q];
-    nbslot[o] = slot_nbs[s * 27 + o];
+    const unsigned bit = __ballot_sync(0x07ffffffu, slot_nbs[s * 27 + o] >= 0);
+    if (o == 0) valid27 = bit;
   }
+  for (int t = threadIdx.x; t < 1000; t += blockDim.x) {  // staged once: 26 reads per cell hit smem
+    const int wx = t % 10, wy = (t / 10) % 10, wz = t / 100;
+    const int ox = wx < 1 ? -1 : (wx > 8 ? 1 : 0), oy = wy < 1 ? -1 : (wy > 8 ? 1 : 0),
+              oz = wz < 1 ? -1 : (wz > 8 ? 1 : 0);
+    const int nb = slot_nbs[s * 27 + ((oz + 1) * 3 + (oy + 1)) * 3 + ox + 1];
+    const int lx = wx - 1 - 8 * ox, ly = wy - 1 - 8 * oy, lz = wz - 1 - 8 * oz;
+    cp_async8(mw + t, mass + ((long long)(nb < 0 ? s : nb) * 512 + (lz * 8 + ly) * 8 + lx), nb >= 0);
+  }
+  asm volatile("cp.async.wait_all;\n" ::: "memory");
   __syncthreads();
   const long long ncell = nslots * 512;
   const int c = threadIdx.x;
@@ -631,13 +819,11 @@ __global__ void __launch_bounds__(512) amr_l2p_kernel(const GLv* __restrict__ Lv
 #pragma unroll
       for (int dx = -1; dx <= 1; ++dx) {
         if (!dx && !dy && !dz) continue;
-        int lx = i + dx, ly = j + dy, lz = k + dz;
+        const int lx = i + dx, ly = j + dy, lz = k + dz;
         const int ox = lx < 0 ? -1 : (lx > 7 ? 1 : 0), oy = ly < 0 ? -1 : (ly > 7 ? 1 : 0),
                   oz = lz < 0 ? -1 : (lz > 7 ? 1 : 0);
-        lx -= 8 * ox, ly -= 8 * oy, lz -= 8 * oz;
-        const long long ns = nbslot[((oz + 1) * 3 + (oy + 1)) * 3 + ox + 1];
-        if (ns < 0) continue;
-        const double nm = -mass[ns * 512 + (lz * 8 + ly) * 8 + lx];
+        if (!((valid27 >> (((oz + 1) * 3 + (oy + 1)) * 3 + ox + 1)) & 1u)) continue;
+        const double nm = -mw[((lz + 1) * 10 + (ly + 1)) * 10 + lx + 1];
         const double* w = w26[((dz + 1) * 3 + (dy + 1)) * 3 + dx + 1];
         p = fma(nm, w[0], p);
         gx = fma(nm, w[1], gx);
@@ -943,6 +1129,8 @@ struct GravAmrWork {
   std::vector<long long> nl2l;
   int2* m2l_work = nullptr;  // fused M2L launch: (level, node) per CTA
   long long m2l_ctas = 0;
+  long long* mono_slots = nullptr;  // amr_m2l_mono_kernel: leaf patches among leaf patches (slot)
+  long long mono_ctas = 0;
   int* wx_tlev = nullptr;         // W/X kernel targets (level, flat), by entry count
   long long* wx_tflat = nullptr;
   long long wx_targets = 0;
@@ -1160,13 +1348,29 @@ static cudaError_t build_l2l_lists(GravAmrWork& w, const std::vector<std::vector
 
 // (level, node) list of the fused M2L launch: every needed node of every level
 static cudaError_t build_m2l_work(GravAmrWork& w, const std::vector<std::vector<int>>* need) {
-  std::vector<int2> wk;
+  std::vector<int2> wk, wk_all;
+  std::vector<long long> mono;
   for (int l = 0; l < w.plan.nlevels; ++l) {
     if (need) {
-      for (int n : (*need)[l]) wk.push_back(make_int2(l, n));
+      for (int n : (*need)[l]) wk_all.push_back(make_int2(l, n));
     } else {
-      for (int n = 0; n < w.plan.lv[l].n; ++n) wk.push_back(make_int2(l, n));
+      for (int n = 0; n < w.plan.lv[l].n; ++n) wk_all.push_back(make_int2(l, n));
     }
+  }
+  // leaf patches (below the root) whose existing neighbours are all leaf
+  // patches go to the monopole-source kernel; the rest to the fused kernel
+  const bool mono_on = std::getenv("TMGPU_M2L_MONO") == nullptr || std::getenv("TMGPU_M2L_MONO")[0] != '0';
+  for (const int2& x : wk_all) {
+    const GravLevel& L = w.plan.lv[x.x];
+    bool all_leaf = mono_on && x.x > 0 && L.leaf_slot[x.y] >= 0;
+    for (int o = 0; o < 27 && all_leaf; ++o) {
+      const int nb = L.nbr[(size_t)x.y * 27 + o];
+      if (nb >= 0 && L.leaf_slot[nb] < 0) all_leaf = false;
+    }
+    if (all_leaf)
+      mono.push_back(L.leaf_slot[x.y]);
+    else
+      wk.push_back(x);
   }
   auto drop = [&w](void*& p) {
     if (!p) return;
@@ -1175,12 +1379,14 @@ static cudaError_t build_m2l_work(GravAmrWork& w, const std::vector<std::vector<
     p = nullptr;
   };
   drop(reinterpret_cast<void*&>(w.m2l_work));
+  drop(reinterpret_cast<void*&>(w.mono_slots));
+  w.mono_ctas = (long long)mono.size();
   drop(reinterpret_cast<void*&>(w.wx_tlev));
   drop(reinterpret_cast<void*&>(w.wx_tflat));
   w.m2l_ctas = (long long)wk.size();
   // targets with W/X entries among the M2L patches, in patch order (source locality)
   std::vector<std::pair<long long, std::pair<int, long long>>> tg;
-  for (const int2& x : wk) {
+  for (const int2& x : wk_all) {
     const GravLevel& L = w.plan.lv[x.x];
     for (int c = 0; c < 512; ++c) {
       const long long f = (long long)x.y * 512 + c;
@@ -1194,6 +1400,8 @@ static cudaError_t build_m2l_work(GravAmrWork& w, const std::vector<std::vector<
   w.wx_targets = (long long)tg.size();
   cudaError_t e = upload(wk, &w.m2l_work);
   if (w.m2l_work) w.allocs.push_back(w.m2l_work);
+  if (e == cudaSuccess) e = upload(mono, &w.mono_slots);
+  if (w.mono_slots) w.allocs.push_back(w.mono_slots);
   if (e == cudaSuccess) e = upload(tl, &w.wx_tlev);
   if (w.wx_tlev) w.allocs.push_back(w.wx_tlev);
   if (e == cudaSuccess) e = upload(tf, &w.wx_tflat);
@@ -1273,7 +1481,15 @@ tmgpu_gravity_amr* tmgpu_gravity_amr_create(const int* leaves, long long nleaves
     if (e == cudaSuccess)
       e = upload(reinterpret_cast<const std::vector<long long>&>(L.pent), &pent), track(pent);
     int *mgeo = nullptr, *pgeo = nullptr;
-    if (e == cudaSuccess) e = upload(L.mgeo, &mgeo), track(mgeo);
+    if (e == cudaSuccess) {  // leaf-cell sources marked ~row (monopole term in amr_wx_kernel)
+      std::vector<int> mg(L.mgeo);
+      for (size_t q = 0; q < mg.size(); ++q) {
+        const long long enc = L.ment[q];
+        const GravLevel& S = P.lv[enc >> 40];
+        if (S.leaf_slot[(size_t)((enc & ((1LL << 40) - 1)) >> 9)] >= 0) mg[q] = ~mg[q];
+      }
+      e = upload(mg, &mgeo), track(mgeo);
+    }
     if (e == cudaSuccess) e = upload(L.pgeo, &pgeo), track(pgeo);
     if (e != cudaSuccess) break;
     g.ijk = ijk, g.nbr = nbr, g.child = child, g.parent = parent, g.leaf_slot = slot;
@@ -1546,6 +1762,11 @@ int tmgpu_gravity_amr_solve(tmgpu_gravity_amr* G, const double* mass, double* ph
     launches += 4;
     if (timed) cudaEventRecord(rec.ev[2], st);
     {
+      if (w.mono_ctas) {  // leaf patches among leaf patches: monopole sources, several CTAs per SM
+        amr_m2l_mono_kernel<<<(unsigned)w.mono_ctas, kM2lThreads, kMonoSmem, st>>>(
+            w.mono_slots, w.slot_level, w.mass, w.slot_nbs, w.tab, w.lloc, w.lo);
+        ++launches;
+      }
       if (w.m2l_ctas) {
         amr_m2l_fused_kernel<<<(unsigned)w.m2l_ctas, kM2lThreads, kM2lSmem, st>>>(w.dev_lv, w.m2l_work,
                                                                                  w.tab, w.lloc, w.lo);

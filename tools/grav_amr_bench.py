@@ -42,8 +42,17 @@ G.mass_from_arena(f)
 for am in (False, True):
     ms = timed(lambda: G.solve(None, am=am, phi=phi, g=g, sync=False), reps)
     print(f"solve am={am}: {ms:.3f} ms  ({n / ms / 1e3:.3e} cells/s)")
+G.set_timing(True)
+for _ in range(reps):
+    G.solve(None, am=True, phi=phi, g=g, sync=False)
+torch.cuda.synchronize()
+tot, ns = G.timing()
+G.set_timing(False)
+print("phases ms/solve:", {k: round(v / ns, 4) for k, v in tot.items()})
 hd = HydroDriver(f)
 print(f"hydro step: {timed(lambda: hd.step(sync=False), reps):.3f} ms")
-gd = GravityHydroDriver(f)
-print(f"gravity+hydro step: {timed(lambda: gd.step(sync=False), reps):.3f} ms")
-gd.check()
+for sps in (1, 3, 6):
+    gd = GravityHydroDriver(f, solves_per_step=sps)
+    print(f"gravity+hydro step ({sps} solves): {timed(lambda: gd.step(sync=False), reps):.3f} ms")
+    gd.check()
+    gd.close()
