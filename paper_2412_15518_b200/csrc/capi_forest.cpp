@@ -2,6 +2,7 @@
 // 3-pass, or the one-round face exchange with cross-GPU halos) and the
 // SSP-RK3 hydro step (include/tmgpu.h, "forest" section).
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -845,6 +846,16 @@ int tmgpu_forest_step(tmgpu_forest* f, double dt, double cfl, double gamma, int 
   // opt-in: measured no faster on C3 at 2-4 GPUs (the split boundary launch
   // under-fills the GPU), so the default keeps one exchange + one launch
   const bool overlap = !exact && f->world() > 1 && !f->peer && (flags & TMGPU_OVERLAP);
+  // opt-in (TMGPU_SPLIT_STAGE=1): split each gravity stage so its update
+  // overlaps the stage's solve (stage_kernel with p.defer, then
+  // stage_epilogue_kernel once the field is there; the same bits; needs the
+  // ping-pong arenas). Measured on C3 (3 solves): 5.39 ms vs 5.35 ms fused — the
+  // solve already fills the GPU and the epilogue's extra pass costs 125 us.
+  static const bool split_env = [] {
+    const char* v = std::getenv("TMGPU_SPLIT_STAGE");
+    return v && v[0] == '1';
+  }();
+  const bool split = split_env && cadence && !exact && !overlap && f->grav_stream;
   for (int stage = 1; stage <= 3 && e == cudaSuccess; ++stage) {
     std::string why;
     if (stage > 1 && cadence >= 3) {  // this stage's field from its input state
@@ -870,9 +881,13 @@ int tmgpu_forest_step(tmgpu_forest* f, double dt, double cfl, double gamma, int 
     } else if (int rc = exchange(f, st, exact ? kExact : kFused, &why)) {
       return fail(err, rc, why);
     }
-    // (the exchange interval includes the wait for a concurrent gravity solve)
-    if (e == cudaSuccess && ((cadence && (stage == 1 || cadence >= 3)) || (!cadence && stage == 1 && f->grav_stream)))
-      e = cudaStreamWaitEvent(st, f->ev_grav, 0);
+    // does this stage wait for a gravity solve on the gravity stream? With the
+    // split stage the update runs concurrently with the solve and only the
+    // epilogue waits; otherwise the stage kernel waits (and the exchange
+    // interval includes the wait)
+    const bool wait_grav =
+        (cadence && (stage == 1 || cadence >= 3)) || (!cadence && stage == 1 && f->grav_stream);
+    if (e == cudaSuccess && wait_grav && !split) e = cudaStreamWaitEvent(st, f->ev_grav, 0);
     if (timed) cudaEventRecord(f->ev[2 * stage], st);
     p.rk_stage = stage;
     p.rho_save = cadence == 6 ? f->rho_tilde : nullptr;
@@ -890,6 +905,14 @@ int tmgpu_forest_step(tmgpu_forest* f, double dt, double cfl, double gamma, int 
       e = launch_stage(V, (flags & TMGPU_FAST) != 0, f->maps[f->cur], pi, st);
       if (e == cudaSuccess) e = cudaStreamWaitEvent(st, f->ev_remote, 0);
       if (e == cudaSuccess) e = launch_stage(V, (flags & TMGPU_FAST) != 0, f->maps[f->cur], pb, st);
+    } else if (split) {  // update || gravity solve, then the epilogue with the field
+      StageLaunch pa = p;
+      pa.defer = 1;
+      pa.grav = nullptr;
+      pa.rho_save = nullptr;
+      e = launch_stage(V, (flags & TMGPU_FAST) != 0, f->maps[f->cur], pa, st);
+      if (e == cudaSuccess && wait_grav) e = cudaStreamWaitEvent(st, f->ev_grav, 0);
+      if (e == cudaSuccess) e = launch_stage_epilogue((flags & TMGPU_FAST) != 0, f->arenas[f->cur], p, st);
     } else {
       e = launch_stage(V, (flags & TMGPU_FAST) != 0, f->maps[f->cur], p, st);
     }

@@ -50,7 +50,16 @@ struct GLv {
   const long long* pent;
   const int* mgeo;  // W/X entry -> row of the W/X geometry table
   const int* pgeo;  // cross-depth U entry -> row of the P2P geometry table
+  double* unm;      // cross-depth U entry -> -(source mass), gathered per solve (amr_u_gather_kernel)
+  long long nu;     // cross-depth U entries of this level
 };
+
+// P2P geometry of the 26 same-depth lattice offsets at unit spacing (depth 0):
+// at depth d the table is this one scaled exactly by 2^d (1/r) and 2^2d
+// (R/r^3) — every operation of p2p_geom commutes with power-of-two scaling —
+// so L2P scales the neighbour masses instead and reads the geometry from the
+// constant bank (no shared-memory traffic)
+__constant__ double c_p2p_unit[27][4];
 
 namespace {
 
@@ -310,6 +319,11 @@ __device__ __forceinline__ void m2l_row_par(const double* __restrict__ src,
       }
     }
   }
+}
+
+__device__ __forceinline__ void cp_async16(double* smem, const double* gmem) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem) : "memory");
 }
 
 __device__ __forceinline__ void cp_async8(double* smem, const double* gmem, bool valid) {
@@ -743,6 +757,18 @@ __global__ void amr_l2l_kernel(const GLv* __restrict__ Lv, int l, long long nnod
   }
 }
 
+// -(source mass) of every cross-depth U entry, gathered in parallel over the
+// entries before L2P (whose per-target loop then reads them contiguously
+// instead of chasing entry -> moment); grid.y = level
+__global__ void amr_u_gather_kernel(const GLv* __restrict__ Lv) {
+  const GLv L = Lv[blockIdx.y];
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < L.nu;
+       e += (long long)gridDim.x * blockDim.x) {
+    const long long enc = __ldg(L.pent + e);
+    L.unm[e] = -__ldg(Lv[enc >> 40].mom + (enc & ((1LL << 40) - 1)) * 10);
+  }
+}
+
 // L2P + P2P at the leaf cells, output by local slot: phi[s*512 + c],
 // g[q*ncell + s*512 + c]. CTA = one slot (512 cells). The leaf patch's L2L is
 // done here (L_q = shift(parent)_q + own M2L sum_q for q = 0..3, the only
@@ -756,8 +782,12 @@ __global__ void amr_l2l_kernel(const GLv* __restrict__ Lv, int l, long long nnod
 __device__ __forceinline__ void cell_pos(const GLv* __restrict__ Lv, int l, int n, int c, double x[3]);
 __device__ __forceinline__ void am_block_sums(double m, const double x[3], double gx, double gy,
                                               double gz, double* __restrict__ out16);
+__device__ __forceinline__ void am_block_sums2(double m0, const double x0[3], const double g0[3], double m1,
+                                               const double x1[3], const double g1[3], double* __restrict__ out16);
 
-__global__ void __launch_bounds__(512) amr_l2p_kernel(const GLv* __restrict__ Lv, long long nslots,
+constexpr int kL2pThreads = 256;  // two cells per thread: 4 CTAs per SM overlap their prologues
+
+__global__ void __launch_bounds__(kL2pThreads, 4) amr_l2p_kernel(const GLv* __restrict__ Lv, long long nslots,
                                                       long long lo, const int* __restrict__ slot_level,
                                                       const int* __restrict__ slot_node,
                                                       const double* __restrict__ mass,
@@ -767,34 +797,67 @@ __global__ void __launch_bounds__(512) amr_l2p_kernel(const GLv* __restrict__ Lv
                                                       const int* __restrict__ slot_nbs,
                                                       double* __restrict__ phi, double* __restrict__ g,
                                                       double* __restrict__ part) {
+  // everything the cell needs from memory is staged up front by cp.async, so
+  // the loads overlap each other instead of forming per-thread chains:
+  //   mw   masses of the patch and its one-cell halo, [z 10][y 10][x pitch 24]
+  //        (pitch 24: the two rows of a half-warp fall in disjoint banks)
+  //   ll   the leaf's compact V + W/X locals [4][512]
+  //   pl   the 4^3 parent cells above the patch, [cell][10] (the L2L input)
   __shared__ double w26[27][4];
-  __shared__ double mw[1000];  // masses of the patch and its one-cell halo, [z 10][y 10][x 10]
+  __shared__ __align__(16) double mw[10 * 240];
+  __shared__ __align__(16) double ll[2048];
+  __shared__ __align__(16) double pl[640];
   __shared__ unsigned valid27;  // bit o: same-depth neighbour leaf patch o exists
+  __shared__ int nbs[27];
   const long long ls = blockIdx.x;  // local slot
   const long long s = lo + ls;
   const int l = slot_level[s], n = slot_node[s];
   const GLv L = Lv[l];
   const int d = l + 3;
   const double h = 1.0 / (double)(1LL << d);
-  if (threadIdx.x < 27) {  // precomputed per depth / per slot (tables built at create)
+  if (threadIdx.x < 27) {  // the 27 neighbour slots, resolved once
     const int o = threadIdx.x;
-#pragma unroll
-    for (int q = 0; q < 4; ++q) w26[o][q] = p2p_tab[((long long)d * 27 + o) * 4 + q];
-    const unsigned bit = __ballot_sync(0x07ffffffu, slot_nbs[s * 27 + o] >= 0);
+    const int nb = slot_nbs[s * 27 + o];
+    nbs[o] = nb;
+    const unsigned bit = __ballot_sync(0x07ffffffu, nb >= 0);
     if (o == 0) valid27 = bit;
   }
-  for (int t = threadIdx.x; t < 1000; t += blockDim.x) {  // staged once: 26 reads per cell hit smem
+  __syncthreads();
+  for (int t = threadIdx.x; t < 1000; t += blockDim.x) {
     const int wx = t % 10, wy = (t / 10) % 10, wz = t / 100;
     const int ox = wx < 1 ? -1 : (wx > 8 ? 1 : 0), oy = wy < 1 ? -1 : (wy > 8 ? 1 : 0),
               oz = wz < 1 ? -1 : (wz > 8 ? 1 : 0);
-    const int nb = slot_nbs[s * 27 + ((oz + 1) * 3 + (oy + 1)) * 3 + ox + 1];
+    const int nb = nbs[((oz + 1) * 3 + (oy + 1)) * 3 + ox + 1];
     const int lx = wx - 1 - 8 * ox, ly = wy - 1 - 8 * oy, lz = wz - 1 - 8 * oz;
-    cp_async8(mw + t, mass + ((long long)(nb < 0 ? s : nb) * 512 + (lz * 8 + ly) * 8 + lx), nb >= 0);
+    cp_async8(mw + (wz * 10 + wy) * 24 + wx, mass + ((long long)(nb < 0 ? s : nb) * 512 + (lz * 8 + ly) * 8 + lx),
+              nb >= 0);
+  }
+  if (l > 0) {
+    const double* src = lloc + ls * 2048;
+    for (int t = threadIdx.x; t < 1024; t += blockDim.x) cp_async16(ll + 2 * t, src + 2 * t);
+    const GLv P = Lv[l - 1];
+    const int pn = L.parent[n];
+    const int bx = (L.ijk[3 * n] & 1) * 4, by = (L.ijk[3 * n + 1] & 1) * 4, bz = (L.ijk[3 * n + 2] & 1) * 4;
+    for (int t = threadIdx.x; t < 320; t += blockDim.x) {  // 16 rows of 4 cells x 10 = 20 x 16 B
+      const int row = t / 20, q = t % 20;
+      const double* r = P.loc + ((long long)pn * 512 + ((bz + (row >> 2)) * 8 + (by + (row & 3))) * 8 + bx) * 10;
+      cp_async16(pl + row * 40 + 2 * q, r + 2 * q);
+    }
   }
   asm volatile("cp.async.wait_all;\n" ::: "memory");
   __syncthreads();
+  // masses scaled by 2^d for the unit-spacing constant geometry (exact)
+  const double sc1 = (double)(1LL << d);
+  for (int t = threadIdx.x; t < 1000; t += blockDim.x) {
+    double* m = mw + ((t / 100) * 10 + (t / 10) % 10) * 24 + t % 10;
+    *m = *m * sc1;
+  }
+  __syncthreads();
   const long long ncell = nslots * 512;
-  const int c = threadIdx.x;
+  double keep[2][3];  // the two cells' g for the angular-momentum sums
+#pragma unroll
+  for (int hc = 0; hc < 2; ++hc) {
+  const int c = threadIdx.x + hc * kL2pThreads;
   const int i = c & 7, j = (c >> 3) & 7, k = c >> 6;
   const long long flat = (long long)n * 512 + c;
   double loc4[4];
@@ -802,12 +865,12 @@ __global__ void __launch_bounds__(512) amr_l2p_kernel(const GLv* __restrict__ Lv
     const double* Lr = L.loc + flat * 10;
 #pragma unroll
     for (int q = 0; q < 4; ++q) loc4[q] = Lr[q];
-  } else {  // compact leaf locals (V + W/X sums) + the parent's shift
-    const double* Lc = lloc + ls * 2048 + c;
+  } else {  // compact leaf locals (V + W/X sums) + the parent's shift (l2l_parent's cell)
 #pragma unroll
-    for (int q = 0; q < 4; ++q) loc4[q] = Lc[q * 512];
-    double sv[3], sh[4];
-    l2l_shift<4>(l2l_parent(L, Lv[l - 1], n, c, h, sv), sv, sh);
+    for (int q = 0; q < 4; ++q) loc4[q] = ll[q * 512 + c];
+    const double sv[3] = {((i & 1) - 0.5) * h, ((j & 1) - 0.5) * h, ((k & 1) - 0.5) * h};
+    double sh[4];
+    l2l_shift<4>(pl + (((k >> 1) * 4 + (j >> 1)) * 4 + (i >> 1)) * 10, sv, sh);
 #pragma unroll
     for (int q = 0; q < 4; ++q) loc4[q] = sh[q] + loc4[q];
   }
@@ -823,17 +886,35 @@ __global__ void __launch_bounds__(512) amr_l2p_kernel(const GLv* __restrict__ Lv
         const int ox = lx < 0 ? -1 : (lx > 7 ? 1 : 0), oy = ly < 0 ? -1 : (ly > 7 ? 1 : 0),
                   oz = lz < 0 ? -1 : (lz > 7 ? 1 : 0);
         if (!((valid27 >> (((oz + 1) * 3 + (oy + 1)) * 3 + ox + 1)) & 1u)) continue;
-        const double nm = -mw[((lz + 1) * 10 + (ly + 1)) * 10 + lx + 1];
-        const double* w = w26[((dz + 1) * 3 + (dy + 1)) * 3 + dx + 1];
-        p = fma(nm, w[0], p);
-        gx = fma(nm, w[1], gx);
-        gy = fma(nm, w[2], gy);
-        gz = fma(nm, w[3], gz);
+        // -m 2^d and -m 2^2d against the unit geometry: p2p_geom's terms exactly
+        const double nm1 = -mw[((lz + 1) * 10 + (ly + 1)) * 24 + lx + 1], nm2 = nm1 * sc1;
+        const int o = ((dz + 1) * 3 + (dy + 1)) * 3 + dx + 1;
+        p = fma(nm1, c_p2p_unit[o][0], p);
+        gx = fma(nm2, c_p2p_unit[o][1], gx);
+        gy = fma(nm2, c_p2p_unit[o][2], gy);
+        gz = fma(nm2, c_p2p_unit[o][3], gz);
       }
   const long long e0 = L.poff[flat], e1 = L.poff[flat + 1];
-  for (long long e = e0; e < e1; ++e) {  // cross-depth U pairs, sorted by source
-    const long long enc = L.pent[e];
-    const double nm = -Lv[enc >> 40].mom[(enc & ((1LL << 40) - 1)) * 10];
+  long long e = e0;
+  for (; e + 3 < e1; e += 4) {  // cross-depth U pairs, sorted by source: 4 entries' loads in flight
+    double nm[4], w[4][4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      nm[u] = __ldg(L.unm + e + u);
+      const double2* w2 = reinterpret_cast<const double2*>(ugeo + (long long)__ldg(L.pgeo + e + u) * 4);
+      const double2 a = __ldg(w2), b = __ldg(w2 + 1);
+      w[u][0] = a.x, w[u][1] = a.y, w[u][2] = b.x, w[u][3] = b.y;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      p = fma(nm[u], w[u][0], p);
+      gx = fma(nm[u], w[u][1], gx);
+      gy = fma(nm[u], w[u][2], gy);
+      gz = fma(nm[u], w[u][3], gz);
+    }
+  }
+  for (; e < e1; ++e) {
+    const double nm = L.unm[e];
     const double* w = ugeo + (long long)L.pgeo[e] * 4;
     p = fma(nm, w[0], p);
     gx = fma(nm, w[1], gx);
@@ -845,10 +926,14 @@ __global__ void __launch_bounds__(512) amr_l2p_kernel(const GLv* __restrict__ Lv
   g[t] = gx;
   g[ncell + t] = gy;
   g[2 * ncell + t] = gz;
+  keep[hc][0] = gx, keep[hc][1] = gy, keep[hc][2] = gz;
+  }
   if (part) {
-    double x[3];
-    cell_pos(Lv, l, n, c, x);
-    am_block_sums(mass[s * 512 + c], x, gx, gy, gz, part + s * 16);
+    double x0[3], x1[3];
+    const int c0 = threadIdx.x, c1 = threadIdx.x + kL2pThreads;
+    cell_pos(Lv, l, n, c0, x0);
+    cell_pos(Lv, l, n, c1, x1);
+    am_block_sums2(mass[s * 512 + c0], x0, keep[0], mass[s * 512 + c1], x1, keep[1], part + s * 16);
   }
 }
 
@@ -898,6 +983,63 @@ __device__ __forceinline__ void am_block_sums(double m, const double x[3], doubl
     for (int q = 0; q < 16; ++q) red[warp][q] = v[q];
   __syncthreads();
   if (c < 16) {  // thread q: tree over the 16 warps for value q
+    double w[16];
+#pragma unroll
+    for (int a = 0; a < 16; ++a) w[a] = red[a][c];
+#pragma unroll
+    for (int st = 1; st < 16; st <<= 1)
+#pragma unroll
+      for (int a = 0; a < 16; a += 2 * st) w[a] = w[a] + w[a + st];
+    out16[c] = w[0];
+  }
+}
+
+// am_block_sums for 256 threads holding cells t and t + 256: the same
+// adjacent-pair tree (warp trees over cells [32w, 32w + 32), then the 16 warp
+// sums), the two halves' warp trees done one after the other
+__device__ __forceinline__ void am_warp_tree(double m, const double x[3], const double gg[3], double v[16]) {
+  v[0] = m;
+  v[1] = m * x[0];
+  v[2] = m * x[1];
+  v[3] = m * x[2];
+  v[4] = m * gg[0];
+  v[5] = m * gg[1];
+  v[6] = m * gg[2];
+  v[7] = m * (x[1] * gg[2] - x[2] * gg[1]);
+  v[8] = m * (x[2] * gg[0] - x[0] * gg[2]);
+  v[9] = m * (x[0] * gg[1] - x[1] * gg[0]);
+  v[10] = v[1] * x[0];
+  v[11] = v[1] * x[1];
+  v[12] = v[1] * x[2];
+  v[13] = v[2] * x[1];
+  v[14] = v[2] * x[2];
+  v[15] = v[3] * x[2];
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int st = 1; st < 32; st <<= 1)
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+      const double o = __shfl_down_sync(0xffffffffu, v[q], st);
+      if ((lane & (2 * st - 1)) == 0) v[q] = v[q] + o;
+    }
+}
+
+__device__ __forceinline__ void am_block_sums2(double m0, const double x0[3], const double g0[3], double m1,
+                                               const double x1[3], const double g1[3], double* __restrict__ out16) {
+  __shared__ double red[16][16];  // [warp of 32 cells][value]
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double v[16];
+  am_warp_tree(m0, x0, g0, v);
+  if (lane == 0)
+#pragma unroll
+    for (int q = 0; q < 16; ++q) red[warp][q] = v[q];
+  am_warp_tree(m1, x1, g1, v);
+  if (lane == 0)
+#pragma unroll
+    for (int q = 0; q < 16; ++q) red[warp + 8][q] = v[q];
+  __syncthreads();
+  if (threadIdx.x < 16) {
+    const int c = threadIdx.x;
     double w[16];
 #pragma unroll
     for (int a = 0; a < 16; ++a) w[a] = red[a][c];
@@ -1131,6 +1273,7 @@ struct GravAmrWork {
   long long m2l_ctas = 0;
   long long* mono_slots = nullptr;  // amr_m2l_mono_kernel: leaf patches among leaf patches (slot)
   long long mono_ctas = 0;
+  long long u_max = 0;  // most cross-depth U entries of a level
   int* wx_tlev = nullptr;         // W/X kernel targets (level, flat), by entry count
   long long* wx_tflat = nullptr;
   long long wx_targets = 0;
@@ -1494,6 +1637,9 @@ tmgpu_gravity_amr* tmgpu_gravity_amr_create(const int* leaves, long long nleaves
     if (e != cudaSuccess) break;
     g.ijk = ijk, g.nbr = nbr, g.child = child, g.parent = parent, g.leaf_slot = slot;
     g.moff = moff, g.ment = ment, g.poff = poff, g.pent = pent, g.mgeo = mgeo, g.pgeo = pgeo;
+    g.nu = (long long)L.pent.size();
+    w.u_max = std::max(w.u_max, g.nu);
+    if (e == cudaSuccess) e = cudaMalloc(&g.unm, (size_t)(g.nu ? g.nu : 1) * sizeof(double)), track(g.unm);
     w.internal[l] = inter;
   }
   if (e == cudaSuccess) e = cudaMalloc(&w.dev_lv, P.nlevels * sizeof(GLv)), track(w.dev_lv);
@@ -1557,6 +1703,7 @@ tmgpu_gravity_amr* tmgpu_gravity_amr_create(const int* leaves, long long nleaves
   if (e == cudaSuccess) {
     p2p_table_kernel<<<((Dmax + 1) * 27 + 127) / 128, 128>>>(w.p2p_tab, Dmax);
     g_launches.fetch_add(1, std::memory_order_relaxed);
+    e = cudaMemcpyToSymbol(c_p2p_unit, w.p2p_tab, 27 * 4 * sizeof(double), 0, cudaMemcpyDeviceToDevice);
     stencil_table_kernel<<<((Dmax + 1) * kOff3 + 127) / 128, 128>>>(w.tab, Dmax);
     g_launches.fetch_add(1, std::memory_order_relaxed);
     e = cudaDeviceSynchronize();
@@ -1794,8 +1941,13 @@ int tmgpu_gravity_amr_solve(tmgpu_gravity_amr* G, const double* mass, double* ph
       e = cudaMemsetAsync(w.part + w.lo * 16, 0, (size_t)(w.hi - w.lo) * 16 * sizeof(double), st);
     else if (am)
       e = cudaMemsetAsync(w.part, 0, (size_t)w.P * 16 * sizeof(double), st);
+    if (w.u_max) {  // U entries' source masses, gathered in parallel
+      amr_u_gather_kernel<<<dim3((unsigned)std::min<long long>((w.u_max + 255) / 256, 1184), P.nlevels), 256, 0, st>>>(
+          w.dev_lv);
+      ++launches;
+    }
     if (nloc)
-      amr_l2p_kernel<<<(unsigned)nloc, 512, 0, st>>>(w.dev_lv, nloc, w.lo, w.slot_level, w.slot_node,
+      amr_l2p_kernel<<<(unsigned)nloc, kL2pThreads, 0, st>>>(w.dev_lv, nloc, w.lo, w.slot_level, w.slot_node,
                                                      w.mass, w.u_geo, w.lloc, w.p2p_tab, w.slot_nbs, dphi, dg,
                                                      am ? w.part : nullptr);
     ++launches;

@@ -180,6 +180,16 @@ cudaError_t launch_stage(int V, bool fast, const StageMaps& m, const StageLaunch
   return cudaErrorInvalidValue;
 }
 
+cudaError_t launch_stage_epilogue(bool fast, const double* in_arena, const StageLaunch& p, cudaStream_t stream) {
+  if (p.count <= 0) return cudaSuccess;
+  if (fast)
+    stage_epilogue_kernel<true><<<p.count, 256, 0, stream>>>(in_arena, p);
+  else
+    stage_epilogue_kernel<false><<<p.count, 256, 0, stream>>>(in_arena, p);
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_max_wavespeed(const double* in, long long slot_stride, const double* hdr,
                                  long long hdr_stride, const double* leaf_dx, double g_gamma,
                                  int V, long long count, double* result, cudaStream_t stream) {

@@ -382,6 +382,68 @@ __device__ __forceinline__ void axis_pass(const double* __restrict__ sm, double*
   }
 }
 
+// ------------------------------------------------------------------ epilogue
+// Gravity source (our spec): after the z update, before the
+// floors, with the stage input's primitives (oracle tmo_stage_subgrid_grav).
+__device__ __forceinline__ void grav_source(double (&u)[5], const StageLaunch& p, int slot, int c, double dt,
+                                            double rho, double iu, double iv, double iw) {
+  const double* gq = p.grav + (long long)slot * kE3 + c;
+  const double gx = gq[0], gy = gq[p.grav_stride], gz = gq[2 * p.grav_stride];
+  u[1] = u[1] + dt * (rho * gx);
+  u[2] = u[2] + dt * (rho * gy);
+  u[3] = u[3] + dt * (rho * gz);
+  u[4] = u[4] + dt * (rho * ((iu * gx + iv * gy) + iw * gz));
+}
+
+// stage.cpp:187-208 density and pressure floors; returns the floor hits
+template <bool FAST>
+__device__ __forceinline__ unsigned euler_floors(double (&u)[5], double gm1) {
+  unsigned hits = 0;
+  if (u[0] < kRhoFloor) {
+    u[0] = kRhoFloor;
+    ++hits;
+  }
+  double ke;
+  if constexpr (!FAST) {
+    ke = 0.5 * (u[1] * u[1] + u[2] * u[2] + u[3] * u[3]) / u[0];
+  } else {
+    ke = 0.5 * fma(u[1], u[1], fma(u[2], u[2], u[3] * u[3])) * __drcp_rn(u[0]);
+  }
+  const double pr = gm1 * (u[4] - ke);
+  if (pr < kPressureFloor) {
+    u[4] = kPressureFloor / gm1 + ke;
+    ++hits;
+  }
+  return hits;
+}
+
+// finiteness (stage.cpp:209-216), provisional density, RK3 combine
+// (rk3.hpp:18-27) with u0p [V][E^3] (or none), store
+template <int V>
+__device__ __forceinline__ void finish_cell(double (&u)[V], const StageLaunch& p, int slot, int c,
+                                            const double* u0p, double* outp, unsigned& bad) {
+#pragma unroll
+  for (int v = 0; v < V; ++v)
+    if (!isfinite(u[v])) bad = min(bad, (unsigned)(v * kE3 + c));
+  if (p.rho_save) p.rho_save[(long long)slot * kE3 + c] = u[0];
+  const int z = c >> 6, y = (c >> 3) & 7, x = c & 7;
+#pragma unroll
+  for (int v = 0; v < V; ++v) {
+    double o = u[v];
+    if (u0p) {
+      const double a0 = u0p[v * kE3 + c];
+      if (p.rk_stage == 2)
+        o = a0 + 0.25 * (o - a0);
+      else if (p.rk_stage == 3)
+        o = a0 + (2.0 / 3.0) * (o - a0);
+    }
+    if (p.out_ghosted)
+      outp[((v * kS + z + 2) * kS + y + 2) * kS + x + 2] = o;
+    else
+      outp[v * kE3 + c] = o;
+  }
+}
+
 template <int V, bool FAST>
 __global__ void __launch_bounds__(kStageThreads, 2)
     stage_kernel(const __grid_constant__ CUtensorMap tm_i, const __grid_constant__ CUtensorMap tm_x,
@@ -403,7 +465,7 @@ __global__ void __launch_bounds__(kStageThreads, 2)
     s_hits = 0;
     s_bad = 0xffffffffu;
     mbar_init(bar, 1);
-    const bool want_u0 = p.u0 && p.rk_stage >= 2;
+    const bool want_u0 = p.u0 && p.rk_stage >= 2 && !p.defer;
     mbar_expect_tx(bar, L::kTxBytes + (want_u0 ? (uint32_t)(V * kE3 * 8) : 0u));
     if (want_u0)  // u0 block rides the same barrier; consumed in the epilogue
       bulk_load(smem + L::kU0, p.u0 + (long long)slot * p.u0_stride, V * kE3 * 8, bar);
@@ -527,8 +589,16 @@ __global__ void __launch_bounds__(kStageThreads, 2)
   __syncthreads();
 
   // ---- phase 4: floors, finiteness, RK3 combine, store
-  unsigned int hits = 0, bad = 0xffffffffu;
   double* outp = p.out + (long long)slot * p.out_stride;
+  if (p.defer) {  // split step: the raw update; stage_epilogue_kernel finishes it
+    for (int c = tid; c < kE3; c += kStageThreads) {
+      const int z = c >> 6, y = (c >> 3) & 7, x = c & 7;
+#pragma unroll
+      for (int v = 0; v < V; ++v) outp[((v * kS + z + 2) * kS + y + 2) * kS + x + 2] = acc[v * kE3 + c];
+    }
+    return;
+  }
+  unsigned int hits = 0, bad = 0xffffffffu;
   const double* u0p = (p.u0 && p.rk_stage >= 2) ? smem + L::kU0 : nullptr;
   for (int c = tid; c < kE3; c += kStageThreads) {
     double u[V];
@@ -537,52 +607,11 @@ __global__ void __launch_bounds__(kStageThreads, 2)
     if constexpr (V == 5) {
       if (euler && p.grav) {  // gravity source with the stage input's primitives
         const double* pq = sm + L::B0 + (c >> 3) * 10 + (c & 7);
-        const double rho = pq[0], iu = pq[640], iv = pq[1280], iw = pq[1920];
-        const double* gq = p.grav + (long long)slot * kE3 + c;
-        const double gx = gq[0], gy = gq[p.grav_stride], gz = gq[2 * p.grav_stride];
-        u[1] = u[1] + dt * (rho * gx);
-        u[2] = u[2] + dt * (rho * gy);
-        u[3] = u[3] + dt * (rho * gz);
-        u[4] = u[4] + dt * (rho * ((iu * gx + iv * gy) + iw * gz));
+        grav_source(u, p, slot, c, dt, pq[0], pq[640], pq[1280], pq[1920]);
       }
-      if (euler) {  // stage.cpp:187-208
-        if (u[0] < kRhoFloor) {
-          u[0] = kRhoFloor;
-          ++hits;
-        }
-        double ke, pr;
-        if constexpr (!FAST) {
-          ke = 0.5 * (u[1] * u[1] + u[2] * u[2] + u[3] * u[3]) / u[0];
-        } else {
-          ke = 0.5 * fma(u[1], u[1], fma(u[2], u[2], u[3] * u[3])) * __drcp_rn(u[0]);
-        }
-        pr = gm1 * (u[4] - ke);
-        if (pr < kPressureFloor) {
-          u[4] = kPressureFloor / gm1 + ke;
-          ++hits;
-        }
-      }
+      if (euler) hits += euler_floors<FAST>(u, gm1);
     }
-#pragma unroll
-    for (int v = 0; v < V; ++v)
-      if (!isfinite(u[v])) bad = min(bad, (unsigned)(v * kE3 + c));
-    if (p.rho_save) p.rho_save[(long long)slot * kE3 + c] = u[0];
-    const int z = c >> 6, y = (c >> 3) & 7, x = c & 7;
-#pragma unroll
-    for (int v = 0; v < V; ++v) {
-      double o = u[v];
-      if (u0p) {  // rk3.hpp:18-27
-        const double a0 = u0p[v * kE3 + c];
-        if (p.rk_stage == 2)
-          o = a0 + 0.25 * (o - a0);
-        else if (p.rk_stage == 3)
-          o = a0 + (2.0 / 3.0) * (o - a0);
-      }
-      if (p.out_ghosted)
-        outp[((v * kS + z + 2) * kS + y + 2) * kS + x + 2] = o;
-      else
-        outp[v * kE3 + c] = o;
-    }
+    finish_cell<V>(u, p, slot, c, u0p, outp, bad);
   }
   // block reductions (integer counts: order-free, exact as double)
   if (hits) atomicAdd(&s_hits, hits);
@@ -592,6 +621,62 @@ __global__ void __launch_bounds__(kStageThreads, 2)
     if (p.diag) p.diag[(long long)slot * p.diag_stride] = (double)s_hits;
     if (s_bad != 0xffffffffu && p.err)
       atomicMin(p.err, ((unsigned long long)slot << 32) | s_bad);
+  }
+}
+
+// Second half of a split stage (the gravity step: the update of every cell is
+// computed by stage_kernel with p.defer while the stage's gravity solve runs,
+// and finished here once the field exists): gravity source with the stage
+// input's primitives (recomputed from the input arena by the stage kernel's own
+// cons -> prim operations), floors, finiteness, provisional density, RK3
+// combine, store — stage_kernel's phase 4 bit for bit. One CTA per slot.
+template <bool FAST>
+__global__ void __launch_bounds__(256) stage_epilogue_kernel(const double* __restrict__ in_arena,
+                                                             const StageLaunch p) {
+  __shared__ unsigned int s_hits, s_bad;
+  const int tid = threadIdx.x;
+  const int slot = p.index ? p.index[blockIdx.x] : blockIdx.x;
+  if (tid == 0) s_hits = 0, s_bad = 0xffffffffu;
+  const double dt = p.dt_ptr ? *p.dt_ptr : p.g_dt;
+  const double gm1 = p.g_gamma - 1.0;
+  const double* inp = in_arena + (long long)slot * p.out_stride;
+  double* outp = p.out + (long long)slot * p.out_stride;
+  const double* u0p = (p.u0 && p.rk_stage >= 2) ? p.u0 + (long long)slot * p.u0_stride : nullptr;
+  __syncthreads();
+  unsigned int hits = 0, bad = 0xffffffffu;
+  for (int c = tid; c < kE3; c += blockDim.x) {
+    const int z = c >> 6, y = (c >> 3) & 7, x = c & 7;
+    const long long q = ((long long)(z + 2) * kS + y + 2) * kS + x + 2;
+    double u[5];
+#pragma unroll
+    for (int v = 0; v < 5; ++v) u[v] = outp[v * kS * kS * kS + q];
+    if (p.grav) {
+      const double rho = stdmax_(inp[q], kRhoFloor);
+      const double m1 = inp[kS * kS * kS + q], m2 = inp[2 * kS * kS * kS + q], m3 = inp[3 * kS * kS * kS + q];
+      double iu, iv, iw;
+      if constexpr (!FAST) {
+        const double yr = __drcp_rn(rho);
+        const bool rok = exp_ok(rho) && exp_ok(yr);
+        iu = div_rn(m1, rho, yr, rok);
+        iv = div_rn(m2, rho, yr, rok);
+        iw = div_rn(m3, rho, yr, rok);
+      } else {
+        const double ir = __drcp_rn(rho);
+        iu = m1 * ir;
+        iv = m2 * ir;
+        iw = m3 * ir;
+      }
+      grav_source(u, p, slot, c, dt, rho, iu, iv, iw);
+    }
+    hits += euler_floors<FAST>(u, gm1);
+    finish_cell<5>(u, p, slot, c, u0p, outp, bad);
+  }
+  if (hits) atomicAdd(&s_hits, hits);
+  if (bad != 0xffffffffu) atomicMin(&s_bad, bad);
+  __syncthreads();
+  if (tid == 0) {
+    if (p.diag) p.diag[(long long)slot * p.diag_stride] = (double)s_hits;
+    if (s_bad != 0xffffffffu && p.err) atomicMin(p.err, ((unsigned long long)slot << 32) | s_bad);
   }
 }
 

@@ -52,6 +52,9 @@ struct StageLaunch {
   // before the RK3 combine (the provisional state a second gravity solve of
   // the 6-solve cadence reads; tmgpu_forest_set_gravity_solver)
   double* rho_save;
+  // split stage (gravity step): store the raw update only; the floors, the
+  // source, finiteness and the combine follow in stage_epilogue_kernel
+  int defer;
   unsigned long long* err;  // atomicMin of (slice << 32 | var-major interior index)
   int count;
 };
@@ -71,6 +74,9 @@ int make_stage_maps(const double* base, int V, long long slot_stride, long long 
 
 cudaError_t launch_stage(int V, bool fast, const StageMaps& maps, const StageLaunch& p,
                          cudaStream_t stream);
+
+// the second half of a split stage (stage_kernel.cuh stage_epilogue_kernel)
+cudaError_t launch_stage_epilogue(bool fast, const double* in_arena, const StageLaunch& p, cudaStream_t stream);
 
 cudaError_t launch_max_wavespeed(const double* in, long long slot_stride, const double* hdr,
                                  long long hdr_stride, const double* leaf_dx, double g_gamma,

@@ -138,7 +138,7 @@ class GravityHydroDriver(HydroDriver):
 
         self.gstream = None
         if os.environ.get("TMGPU_GRAVITY_OVERLAP", "1") != "0":
-            self.gstream = torch.cuda.Stream()
+            self.gstream = torch.cuda.Stream(priority=-1)  # the critical path: first pick of SMs
             _lib.check(lib.tmgpu_forest_set_gravity_stream(forest.h, self.gstream.cuda_stream,
                                                            C.byref(TmgpuError())), TmgpuError())
         n = forest.local_count() * 512
