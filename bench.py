@@ -44,13 +44,14 @@ UNIT = "cell-steps/s"
 ALG_FLOP_PER_CELL = 633.25     # hydro stage FP64 ops per cell (div/sqrt = 1)
 ALG_BYTES_PER_CELL = 180.0     # stage kernel, device-resident: 1280 staged cells x 40 B per
                                # 512 cells (100 B) + interior write 40 B + u0 read/write 40 B
-# Gravity, FP64 flops per interaction, FMA = 2: the order-2
-# Cartesian M2L is 28 multiply-adds once the geometry is known (into a leaf
-# patch only L0 and L_i are needed: 22); W/X pairs also build their geometry
-# (46 ops); same-depth P2P is 4 multiply-adds with tabulated geometry;
-# cross-depth U pairs build theirs (15 ops).
-FLOP_M2L_V, FLOP_M2L_V_LEAF, FLOP_M2L_WX, FLOP_P2P, FLOP_P2P_U = 56, 44, 102, 8, 23
-FLOP_M2L_WX_LEAF = FLOP_M2L_WX - (FLOP_M2L_V - FLOP_M2L_V_LEAF)
+# Gravity, FP64 flops per interaction, FMA = 2, geometry tabulated
+# (per stencil offset for V, per distinct separation for W/X and U, built once
+# with the plan). The order-2 Cartesian M2L is 28 multiply-adds; into a leaf
+# patch only L0 and L_i are needed (22); a leaf-cell source has D = Q = 0, so
+# its term is the monopole one: 1 mul + 1 add + 3 FMA into L0, L_i (8 flops),
+# + 6 FMA into L_ij for an internal target (20). By (target, source) kind:
+FLOP_M2L = {"ll": 8, "li": 44, "il": 20, "ii": 56}
+FLOP_P2P, FLOP_P2P_U = 8, 8  # 4 FMA per same-depth or cross-depth pair
 
 
 # scenario -> (kind, default min/max leaf level, bc, name)
@@ -425,22 +426,20 @@ def run_ours(args, rank, world):
     share = {"hydro_stage": 3 * stage_ms / ms, "hydro_exchange": 3 * exch_ms / ms,
              "hydro_cfl": cfl_ms / ms}
     if gravity:
-        m2l_flop = ((work["v_pairs"] - work["v_pairs_leaf"]) * FLOP_M2L_V +
-                    work["v_pairs_leaf"] * FLOP_M2L_V_LEAF +
-                    (work["wx_entries"] - work["wx_entries_leaf"]) * FLOP_M2L_WX +
-                    work["wx_entries_leaf"] * FLOP_M2L_WX_LEAF)
+        m2l_flop = sum((work["v_" + k] + work["wx_" + k]) * f for k, f in FLOP_M2L.items())
         m2l_tf = m2l_flop / (grav_ms["m2l"] * 1e-3) / 1e12
         m2l_prof = profile_traffic("m2l_kernel_latest.json")
         roofline = {"bound": "fp64", "achieved": m2l_tf, "peak": peak_tf, "unit": "TFLOP/s",
                     "frac": m2l_tf / peak_tf if peak_tf else None,
                     "peak_dmma": peak_dmma, "frac_vs_dmma": m2l_tf / peak_dmma if peak_dmma else None,
                     "traffic": m2l_prof.get("dram_bytes_per_launch"),
-                    "kernel": "amr_m2l (gravity M2L: V-list stencil + W/X lists), all levels",
+                    "kernel": "gravity M2L phase: amr_m2l_mono (leaf patches among leaf patches) + "
+                              "amr_m2l_fused (the rest) + amr_wx (W/X lists), all levels",
                     "launch_ms": grav_ms["m2l"], "alg_flop_per_launch": m2l_flop,
-                    "alg_flop": f"{FLOP_M2L_V}/V pair into internal patches, {FLOP_M2L_V_LEAF} into leaf "
-                                f"patches ({work['v_pairs']} pairs, {work['v_pairs_leaf']} into leaves) + "
-                                f"{FLOP_M2L_WX}/{FLOP_M2L_WX_LEAF} per W-X entry ({work['wx_entries']}) "
-                                "(FMA = 2)",
+                    "alg_flop": "per V pair / W-X entry by (target, source) kind (l leaf, i internal): "
+                                + ", ".join(f"{k} {f} x {work['v_' + k] + work['wx_' + k]}"
+                                            for k, f in FLOP_M2L.items())
+                                + " (FMA = 2; a leaf source's D, Q are zero)",
                     "peak_source": "live DFMA microbenchmark (tools/probes/libtmprobe.so "
                                    "tmgpu_fp64_peak; the M2L is DFMA code); peak_dmma = the FP64 "
                                    "tensor-core (DMMA m8n8k4) probe, the chip's FP64 ceiling "

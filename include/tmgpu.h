@@ -272,9 +272,12 @@ int tmgpu_gravity_amr_mass_from_density(tmgpu_gravity_amr* G, const double* rho,
 int tmgpu_gravity_amr_solve(tmgpu_gravity_amr* G, const double* mass, double* phi, double* g,
                             int flags, void* stream, tmgpu_error* err);
 int tmgpu_gravity_amr_am_stats(tmgpu_gravity_amr* G, double* out);
-/* algorithmic work of one solve (bench roofline): [V pairs, W/X entries,
+/* algorithmic work of one solve (bench roofline), out[15]: [V pairs, W/X entries,
  * same-depth P2P pairs, cross-depth U entries, V pairs evaluated, V pairs into
- * leaf patches, W/X entries into leaf patches] (leaf targets need only L0, L_i) */
+ * leaf patches, W/X entries into leaf patches] (leaf targets need only L0, L_i), then
+ * V pairs and W/X entries by (target, source) kind: [7..10] V (leaf<-leaf,
+ * leaf<-internal, internal<-leaf, internal<-internal), [11..14] W/X likewise (a leaf
+ * source's D and Q are zero: its term is the monopole one) */
 int tmgpu_gravity_amr_work(const tmgpu_gravity_amr* G, long long* out);
 /* multi-GPU (locally essential tree, multipole-moment exchange over NCCL): this rank (comm)
  * owns canonical slots [slot_bounds[r], slot_bounds[r+1]); masses and outputs become by local

@@ -1137,8 +1137,10 @@ cudaError_t upload(const std::vector<T>& v, T** out) {
 // existing source, counted per neighbour-patch offset from the plan.
 // need: per-level node lists this GPU evaluates M2L for (nullptr = all);
 // [lo, hi): the canonical slots it evaluates L2P/P2P for.
+constexpr int kWorkCounts = 15;
+
 void count_work(const GravPlan& P, const std::vector<std::vector<int>>* need, long long lo,
-                long long hi, long long out[7]) {
+                long long hi, long long out[kWorkCounts]) {
   long long vtab[27] = {0}, ptab[27] = {0};
   for (int c = 0; c < 512; ++c) {
     const int i = c & 7, j = (c >> 3) & 7, k = c >> 6;
@@ -1153,14 +1155,25 @@ void count_work(const GravPlan& P, const std::vector<std::vector<int>>* need, lo
         }
   }
   long long v = 0, vk = 0, p = 0, wx = 0, u = 0, vleaf = 0, wxleaf = 0;
+  long long vt[4] = {0, 0, 0, 0}, wt[4] = {0, 0, 0, 0};  // by (target internal?, source internal?)
   for (int l = 0; l < P.nlevels; ++l) {
     const GravLevel& L = P.lv[l];
     auto node = [&](int n) {
       vk += 512 * 189;  // the kernel's 189 offsets x 512 targets
       long long vn = 0;
-      for (int o = 0; o < 27; ++o)
-        if (L.nbr[(size_t)n * 27 + o] >= 0) vn += vtab[o];
+      const int ti = L.leaf_slot[n] >= 0 ? 0 : 2;
+      for (int o = 0; o < 27; ++o) {
+        const int nb = L.nbr[(size_t)n * 27 + o];
+        if (nb < 0) continue;
+        vn += vtab[o];
+        vt[ti + (L.leaf_slot[nb] >= 0 ? 0 : 1)] += vtab[o];
+      }
       const long long wn = L.moff[(size_t)(n + 1) * 512] - L.moff[(size_t)n * 512];
+      for (long long e = L.moff[(size_t)n * 512]; e < L.moff[(size_t)(n + 1) * 512]; ++e) {
+        const long long enc = L.ment[(size_t)e];
+        const GravLevel& S = P.lv[enc >> 40];
+        wt[ti + (S.leaf_slot[(size_t)((enc & ((1LL << 40) - 1)) >> 9)] >= 0 ? 0 : 1)] += 1;
+      }
       v += vn;
       wx += wn;
       if (L.leaf_slot[n] >= 0) vleaf += vn, wxleaf += wn;  // L0, L_i only
@@ -1196,6 +1209,7 @@ void count_work(const GravPlan& P, const std::vector<std::vector<int>>* need, lo
   out[4] = vk;
   out[5] = vleaf;
   out[6] = wxleaf;
+  for (int q = 0; q < 4; ++q) out[7 + q] = vt[q], out[11 + q] = wt[q];
 }
 
 constexpr int kMaxLetPeers = 8;
@@ -1220,7 +1234,7 @@ constexpr int kAmPushCtas = 16;  // CTAs per destination of am_push_kernel
 
 struct GravAmrWork {
   GravPlan plan;
-  long long work[7] = {0, 0, 0, 0, 0, 0, 0};
+  long long work[kWorkCounts] = {};
   bool timing = false;
   std::vector<GravTimingRec> pending;
   double phase_ms[kGravPhases] = {0, 0, 0, 0, 0, 0};
@@ -2184,7 +2198,7 @@ int tmgpu_gravity_amr_am_stats(tmgpu_gravity_amr* G, double* out) {
 // (those evaluate only L0 and L_i).
 int tmgpu_gravity_amr_work(const tmgpu_gravity_amr* G, long long* out) {
   if (!G || !out) return TMGPU_ERR_INVALID;
-  for (int q = 0; q < 7; ++q) out[q] = G->w.work[q];
+  for (int q = 0; q < kWorkCounts; ++q) out[q] = G->w.work[q];
   return TMGPU_OK;
 }
 

@@ -271,11 +271,13 @@ class GravityAMR:
 
     def work(self):
         """Algorithmic work of one solve: dict of interaction counts."""
-        out = (C.c_longlong * 7)()
+        out = (C.c_longlong * 15)()
         lib.tmgpu_gravity_amr_work(self.h, out)
+        kinds = ("ll", "li", "il", "ii")  # (target, source): l leaf, i internal
         return {"v_pairs": out[0], "wx_entries": out[1], "p2p_pairs": out[2],
                 "u_cross_entries": out[3], "v_pairs_evaluated": out[4], "v_pairs_leaf": out[5],
-                "wx_entries_leaf": out[6]}
+                "wx_entries_leaf": out[6], **{"v_" + k: out[7 + q] for q, k in enumerate(kinds)},
+                **{"wx_" + k: out[11 + q] for q, k in enumerate(kinds)}}
 
     def set_timing(self, on: bool) -> None:
         lib.tmgpu_gravity_amr_set_timing(self.h, int(on))
