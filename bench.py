@@ -572,7 +572,10 @@ def run_ours(args, rank, world):
                                     "sample": f"unavailable: {ex}"}
     if rank == 0:
         print(json.dumps(line), flush=True)
-    if dist:
+    if dist:  # collective teardown of the peer-memory exchanges, then the group
+        (hdrv if gravity else drv).release_peers()
+        if gravity:
+            drv.release_peers()
         dist.destroy_process_group()
 
 

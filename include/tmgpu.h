@@ -143,6 +143,11 @@ int tmgpu_forest_interior(tmgpu_forest* f, double* compact, int to_device, int f
                           tmgpu_error* err);
 /* whole ghosted arena <-> host [slot][vars][S^3] (SubGrid::raw, subgrid.hpp:59-60) */
 int tmgpu_forest_grids(tmgpu_forest* f, double* ghosted_host, int to_device, tmgpu_error* err);
+/* either arena by role (0 = current state, 1 = the other ping-pong arena), whole ghosted
+ * blocks <-> host [slot][vars][S^3]: a resumable checkpoint holds both (the step carries their
+ * ghost layers across exchanges) */
+int tmgpu_forest_arena_grids(tmgpu_forest* f, int which, double* ghosted_host, int to_device,
+                             tmgpu_error* err);
 /* ghost::fill_ghosts_sync (ghost.cpp:282-296), bitwise on the full ghosted arrays */
 /* AMR regrid with the device data (octree.cpp:149-293 prolong_cell / restrict_cells, same
  * order incl. cascaded 2:1 refines): refine then coarsen the listed nodes; single GPU */

@@ -317,6 +317,23 @@ class Forest:
         err = TmgpuError()
         _lib.check(lib.tmgpu_forest_grids(self.h, g.ctypes.data, 1, C.byref(err)), err)
 
+    def arena_grids(self, which: int, grids: np.ndarray | None = None) -> np.ndarray | None:
+        """Whole ghosted blocks [local][V*S^3] of the current (which=0) or the
+        other ping-pong arena (which=1); with `grids`, write them instead."""
+        lib.tmgpu_forest_arena_grids.restype = C.c_int
+        lib.tmgpu_forest_arena_grids.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_int,
+                                                 C.POINTER(TmgpuError)]
+        err = TmgpuError()
+        if grids is None:
+            out = np.zeros((self.local_count(), self.vars * self.stride ** 3))
+            _lib.check(lib.tmgpu_forest_arena_grids(self.h, which, out.ctypes.data, 0, C.byref(err)), err)
+            return out
+        g = np.ascontiguousarray(grids, dtype=np.float64)
+        if g.size != self.local_count() * self.vars * self.stride ** 3:
+            raise ValueError("grids must hold every local leaf's ghosted block")
+        _lib.check(lib.tmgpu_forest_arena_grids(self.h, which, g.ctypes.data, 1, C.byref(err)), err)
+        return None
+
     def fill_ghosts(self, stream=None) -> None:
         """ghost::fill_ghosts_sync (ghost.cpp:282-296) on the device."""
         err = TmgpuError()

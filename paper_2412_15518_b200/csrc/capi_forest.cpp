@@ -124,12 +124,23 @@ void collect_timing(tmgpu_forest* f) {
   f->pending_timed = 0;
 }
 
-void peer_close(tmgpu_forest* f) {
+// Release the peer exchange. collective = true (tmgpu_forest_set_peer, called
+// on every rank): a barrier after every rank's last exchange, then each rank
+// unmaps its peers' buffers, a second barrier, and only then the buffers this
+// rank exported are freed — freeing exported memory a peer still maps is
+// undefined (a lagging peer's last consumption-flag store lands in it).
+// collective = false (destroy / re-alloc on one rank): local release only;
+// callers tear a peer forest down with tmgpu_forest_set_peer(f, 0) first.
+void peer_close(tmgpu_forest* f, bool collective = false) {
   if (f->peer_flags || f->peer) cudaDeviceSynchronize();
+  const bool coll = collective && f->peer && f->world() > 1;
+  std::string why;
+  if (coll) comm_barrier(f->comm, &why);
   for (void*& p : f->peer_opened) {
     if (p) cudaIpcCloseMemHandle(p);
     p = nullptr;
   }
+  if (coll) comm_barrier(f->comm, &why);
   for (void* p : {(void*)f->peer_flags, (void*)f->pack_peer, (void*)f->pull_peer})
     if (p) cudaFree(p);
   f->peer_flags = nullptr;
@@ -678,6 +689,26 @@ int tmgpu_forest_grids(tmgpu_forest* f, double* ghosted_host, int to_device, tmg
   return cuda_err(err, e, "tmgpu_forest_grids");
 }
 
+// Either ghosted arena by role: which 0 = the current state, 1 = the other
+// (ping-pong) arena. The step carries both arenas' ghost layers across
+// exchanges (prolongation reads coarse cells next to the face, which can be
+// ghosts last written several exchanges earlier), so a bitwise resumable
+// checkpoint stores and restores both.
+int tmgpu_forest_arena_grids(tmgpu_forest* f, int which, double* ghosted_host, int to_device,
+                             tmgpu_error* err) {
+  if (err) std::memset(err, 0, sizeof(*err));
+  if (int rc = ready(f, err)) return rc;
+  if (which != 0 && which != 1) return fail(err, TMGPU_ERR_INVALID, "arena role must be 0 (current) or 1 (other)");
+  double* a = f->arenas[f->cur ^ which];
+  if (!a) return fail(err, TMGPU_ERR_INVALID, "no second arena");
+  const size_t bytes = (size_t)f->nslots * f->forest.config().vars * 1728 * sizeof(double);
+  cudaError_t e = cudaDeviceSynchronize();
+  if (e == cudaSuccess)
+    e = to_device ? cudaMemcpy(a, ghosted_host, bytes, cudaMemcpyHostToDevice)
+                  : cudaMemcpy(ghosted_host, a, bytes, cudaMemcpyDeviceToHost);
+  return cuda_err(err, e, "tmgpu_forest_arena_grids");
+}
+
 int tmgpu_forest_fill_ghosts(tmgpu_forest* f, void* stream, tmgpu_error* err) {
   if (err) std::memset(err, 0, sizeof(*err));
   if (int rc = ready(f, err)) return rc;
@@ -968,7 +999,7 @@ int tmgpu_stream_wait(void* waiter, void* signaller) {
 int tmgpu_forest_set_peer(tmgpu_forest* f, int on, tmgpu_error* err) {
   if (err) std::memset(err, 0, sizeof(*err));
   if (int rc = ready(f, err)) return rc;
-  peer_close(f);
+  peer_close(f, /*collective=*/true);
   if (!on) return TMGPU_OK;
   const int world = f->world(), me = f->rank();
   if (world < 2) return fail(err, TMGPU_ERR_INVALID, "peer exchange needs a communicator with 2+ ranks");
@@ -1007,6 +1038,7 @@ int tmgpu_forest_set_peer(tmgpu_forest* f, int on, tmgpu_error* err) {
   std::string why = "peer exchange: setup failed on a rank";
   bool ok = agree(e == cudaSuccess, all.data(), &why);
   PeerTab t{};
+  t.spin_ns = peer_spin_ns();
   t.mine = f->peer_flags;
   t.me = me;
   t.world = world;

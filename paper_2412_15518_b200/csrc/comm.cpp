@@ -105,6 +105,26 @@ int comm_allreduce_min(tmgpu_comm* c, double* buf, size_t n, cudaStream_t st, st
   return TMGPU_OK;
 }
 
+int comm_barrier(tmgpu_comm* c, std::string* why) {
+  if (!c || comm_world(c) < 2) return TMGPU_OK;
+  double* d = nullptr;
+  cudaError_t e = cudaDeviceSynchronize();
+  if (e == cudaSuccess) e = cudaMalloc(&d, sizeof(double));
+  if (e == cudaSuccess) e = cudaMemset(d, 0, sizeof(double));
+  if (e != cudaSuccess) {
+    if (why) *why = std::string("barrier: ") + cudaGetErrorString(e);
+    return TMGPU_ERR_CUDA;
+  }
+  int rc = comm_allreduce_min(c, d, 1, nullptr, why);
+  e = cudaDeviceSynchronize();
+  cudaFree(d);
+  if (rc == TMGPU_OK && e != cudaSuccess) {
+    if (why) *why = std::string("barrier: ") + cudaGetErrorString(e);
+    rc = TMGPU_ERR_CUDA;
+  }
+  return rc;
+}
+
 int comm_allgather(tmgpu_comm* c, const double* send, double* recv, size_t count, cudaStream_t st,
                    std::string* why) {
   ncclResult_t r = api().AllGather(send, recv, count, ncclDouble, c->comm, st);

@@ -28,6 +28,9 @@ int comm_allgather(tmgpu_comm* c, const double* send, double* recv, size_t count
 // buf[off[p] .. +cnt[p]) (grouped ncclBroadcast, root p), every rank ends with all.
 int comm_allgatherv(tmgpu_comm* c, double* buf, const std::vector<long long>& off,
                     const std::vector<long long>& cnt, cudaStream_t st, std::string* why);
+// Barrier over the communicator (a one-double all-reduce, synchronised on the
+// host): every rank's earlier device work is complete when it returns.
+int comm_barrier(tmgpu_comm* c, std::string* why);
 // In-place min-allreduce of n doubles (the global CFL dt).
 int comm_allreduce_min(tmgpu_comm* c, double* buf, size_t n, cudaStream_t st, std::string* why);
 

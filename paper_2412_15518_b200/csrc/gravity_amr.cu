@@ -1229,6 +1229,7 @@ struct LetPeer {
   unsigned recv_mask;                       // ranks that store patches into this one
   unsigned am_mask;                         // ranks that store AM sums into this one
   long long seg_at, seg_n;                  // this rank's AM sums: part[seg_at, seg_at + seg_n)
+  unsigned long long spin_ns;               // flag-wait limit (peer_spin_ns(); 0 = none)
 };
 constexpr int kAmPushCtas = 16;  // CTAs per destination of am_push_kernel
 
@@ -1318,7 +1319,7 @@ __global__ void __launch_bounds__(256) let_push_kernel(const GLv* __restrict__ L
                                                        unsigned long long seq) {
   const int4 it = items[blockIdx.x];
   const int q = it.z;
-  if (threadIdx.x == 0) spin_geq(t.mine + t.world + q, seq - 1);
+  if (threadIdx.x == 0) spin_geq(t.mine + t.world + q, seq - 1, t.spin_ns);
   __syncthreads();
   const double2* src = reinterpret_cast<const double2*>(Lv[it.x].mom + (long long)it.y * 5120);
   double2* dst = reinterpret_cast<double2*>(peer_mom[q * t.nl + it.x] + (long long)it.y * 5120);
@@ -1338,7 +1339,7 @@ __global__ void __launch_bounds__(256) let_push_kernel(const GLv* __restrict__ L
 __global__ void let_wait_kernel(LetPeer t, unsigned long long seq) {
   if (threadIdx.x == 0)
     for (int s = 0; s < t.world; ++s)
-      if (t.recv_mask >> s & 1u) spin_geq(t.mine + s, seq);
+      if (t.recv_mask >> s & 1u) spin_geq(t.mine + s, seq, t.spin_ns);
 }
 
 // after the solve's last reader of received patches and AM sums: every rank
@@ -1359,7 +1360,7 @@ __global__ void __launch_bounds__(256) am_push_kernel(const double* __restrict__
   int q = blockIdx.x / kAmPushCtas;
   q += q >= t.me;
   const int c = blockIdx.x % kAmPushCtas;
-  if (threadIdx.x == 0) spin_geq(t.mine + t.world + q, seq - 1);
+  if (threadIdx.x == 0) spin_geq(t.mine + t.world + q, seq - 1, t.spin_ns);
   __syncthreads();
   const long long per = (t.seg_n + kAmPushCtas - 1) / kAmPushCtas;
   const long long b = t.seg_at + c * per, e = min(t.seg_at + t.seg_n, b + per);
@@ -1379,14 +1380,21 @@ __global__ void __launch_bounds__(256) am_push_kernel(const double* __restrict__
 __global__ void am_wait_kernel(LetPeer t, unsigned long long seq) {
   if (threadIdx.x == 0)
     for (int s = 0; s < t.world; ++s)
-      if (t.am_mask >> s & 1u) spin_geq(t.mine + 3 * t.world + s, seq);
+      if (t.am_mask >> s & 1u) spin_geq(t.mine + 3 * t.world + s, seq, t.spin_ns);
 }
 
-static void let_peer_close(GravAmrWork& w) {
+// collective (tmgpu_gravity_amr_set_peer on every rank): barrier, unmap the
+// peers' buffers, barrier, then free what this rank exported (see the forest's
+// peer_close); otherwise a local release (destroy)
+static void let_peer_close(GravAmrWork& w, bool collective = false) {
   if (w.pflags || w.peer) cudaDeviceSynchronize();
+  const bool coll = collective && w.peer && w.comm && comm_world(w.comm) > 1;
+  std::string why;
+  if (coll) comm_barrier(w.comm, &why);
   for (void* p : w.peer_opened)
     if (p) cudaIpcCloseMemHandle(p);
   w.peer_opened.clear();
+  if (coll) comm_barrier(w.comm, &why);
   for (void* p : {(void*)w.pflags, (void*)w.push, (void*)w.peer_mom})
     if (p) cudaFree(p);
   w.pflags = nullptr;
@@ -2085,7 +2093,7 @@ int tmgpu_gravity_amr_set_peer(tmgpu_gravity_amr* G, int on, tmgpu_error* err) {
   if (err) std::memset(err, 0, sizeof(*err));
   if (!G) return set_err(err, TMGPU_ERR_INVALID, "null gravity solver");
   GravAmrWork& w = G->w;
-  let_peer_close(w);
+  let_peer_close(w, /*collective=*/true);
   if (!on) return TMGPU_OK;
   if (!w.let || !w.comm) return set_err(err, TMGPU_ERR_INVALID, "gravity peer exchange: call distribute first");
   const GravPlan& P = w.plan;
@@ -2129,6 +2137,7 @@ int tmgpu_gravity_amr_set_peer(tmgpu_gravity_amr* G, int on, tmgpu_error* err) {
   }
   bool ok = agree(e == cudaSuccess, all.data());
   LetPeer t{};
+  t.spin_ns = peer_spin_ns();
   t.mine = w.pflags;
   t.me = me;
   t.world = R;

@@ -190,7 +190,7 @@ __global__ void __launch_bounds__(128) pack_peer_kernel(const double* __restrict
     pack_item(arena, prev, V, it, slabs + it.out);
     return;
   }
-  if (threadIdx.x == 0) spin_geq(t.mine + t.world + q, seq - 1);
+  if (threadIdx.x == 0) spin_geq(t.mine + t.world + q, seq - 1, t.spin_ns);
   __syncthreads();
   pack_item(arena, prev, V, it, t.slabs[q] + it.out);
   __threadfence_system();
@@ -218,7 +218,7 @@ __global__ void __launch_bounds__(128) pull_peer_kernel(double* __restrict__ are
   if (remote) {
     if (threadIdx.x == 0)
       for (int s = 0; s < t.world; ++s)
-        if (t.recv_mask >> s & 1u) spin_geq(t.mine + s, seq);
+        if (t.recv_mask >> s & 1u) spin_geq(t.mine + s, seq, t.spin_ns);
     __syncthreads();
   }
   pull_item(arena, V, faces, items[blockIdx.x], slabs);

@@ -56,6 +56,7 @@ struct PeerTab {
   int n_send[kMaxPeers];                  // pack items (CTAs) per destination peer
   int me, world;
   unsigned recv_mask;                     // peers this rank receives slabs from
+  unsigned long long spin_ns;             // flag-wait limit (peer_spin_ns(); 0 = none)
 };
 
 cudaError_t halo_pack_peer(const double* arena, const double* prev, int V, const PackItem* items,

@@ -7,6 +7,7 @@
 #include <atomic>
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 #include <string>
 
 #include "../../include/tmgpu.h"
@@ -124,6 +125,15 @@ inline int cuda_err(tmgpu_error* err, cudaError_t e, const char* where) {
     std::snprintf(err->message, sizeof(err->message), "%s: %s", where, cudaGetErrorString(e));
   }
   return TMGPU_ERR_CUDA;
+}
+
+// Flag-wait limit of the peer-memory exchanges (peer.cuh spin_geq), read at
+// peer setup: TMGPU_PEER_TIMEOUT_S seconds, default 20, 0 = wait forever.
+inline unsigned long long peer_spin_ns() {
+  const char* v = std::getenv("TMGPU_PEER_TIMEOUT_S");
+  if (!v || !*v) return 20000000000ull;
+  const double s = std::atof(v);
+  return s <= 0.0 ? 0ull : (unsigned long long)(s * 1e9);
 }
 
 inline cudaStream_t as_stream(void* s) {

@@ -57,6 +57,12 @@ class HydroDriver:
         err = TmgpuError()
         _lib.check(lib.tmgpu_forest_check(self.forest.h, stream, C.byref(err)), err, SolverError)
 
+    def release_peers(self) -> None:
+        """Collective: return a peer-memory forest to NCCL exchanges on every rank
+        (amr.Forest.set_peer(False): barrier, unmap, barrier, free)."""
+        if getattr(self.forest, "_peer", False):
+            self.forest.set_peer(False)
+
 
 lib.tmgpu_stream_wait.restype = C.c_int
 lib.tmgpu_stream_wait.argtypes = [C.c_void_p, C.c_void_p]
@@ -169,6 +175,16 @@ class GravityHydroDriver(HydroDriver):
             err = TmgpuError()
             _lib.check(lib.tmgpu_forest_set_reflux(self.forest.h, 1, C.byref(err)), err)
         self._setup_gravity()
+
+    def release_peers(self) -> None:
+        """Collective on a distributed forest: tear the peer-memory exchanges down
+        on every rank (barrier, unmap, barrier, free) before the forest or the
+        solver is destroyed (freeing memory a peer still maps is undefined)."""
+        self.close()
+        if getattr(self, "moment_transport", "") == "peer":
+            self.gravity.set_peer(False)
+            self.moment_transport = "nccl"
+        super().release_peers()
 
     def close(self) -> None:
         err = TmgpuError()

@@ -17,9 +17,13 @@ state = f.scenario_state(amr.Scenario.rotating_star)
 owner = np.asarray(dist.partition(f, world))
 mine = owner == rank
 buf = checkpoint.save(None, f, time=0.25, step=3, state=state[mine], keys=f.leaves()[mine])
-if rank == 0:
-    single = checkpoint.encode(f.leaves(), state, time=0.25, step=3)
-    print("CKPT_OK" if buf == single else "CKPT_MISMATCH", rank, len(buf))
-else:
-    print("CKPT_OK" if buf is None else "CKPT_MISMATCH", rank)
+single = checkpoint.encode(f.leaves(), state, time=0.25, step=3)
+ok = (buf == single) if rank == 0 else (buf is None)
+# with a path: every rank writes its own byte range, nothing is gathered
+path = os.environ.get("CKPT_PATH", "/tmp/gloo_ckpt.tmck")
+ret = checkpoint.save(path, f, time=0.25, step=3, state=state[mine], keys=f.leaves()[mine])
+tdist.barrier()
+with open(path, "rb") as fh:
+    ok = ok and ret is None and fh.read() == single
+print("CKPT_OK" if ok else "CKPT_MISMATCH", rank)
 tdist.destroy_process_group()

@@ -40,6 +40,11 @@ def main():
     drv = Drv(f)
     dts = [drv.step() for _ in range(3)]
     ckpt = checkpoint.save(None, f, time=sum(dts), step=3)  # collective: rank 0 merges
+    # collective, nothing gathered: every rank writes its own byte range
+    cpath = os.path.join(os.environ.get("TMPDIR", "/tmp"), f"mgpu_ckpt_{os.getpid() if rank == 0 else 0}.tmck")
+    cpath = [cpath]
+    tdist.broadcast_object_list(cpath, src=0)
+    assert checkpoint.save(cpath[0], f, time=sum(dts), step=3) is None
     mine = torch.from_numpy(f.get_interior()).cuda()
     sizes = [dist.local_range(owner, r)[1] - dist.local_range(owner, r)[0] for r in range(world)]
     gathered = [torch.zeros((s, 5, 512), dtype=torch.float64, device="cuda") for s in sizes]
@@ -57,6 +62,9 @@ def main():
         single = g.get_interior()
         assert dts == dts1, (dts, dts1)
         assert ckpt == checkpoint.encode(g.leaves(), single, sum(dts1), 3), "checkpoint differs"
+        with open(cpath[0], "rb") as fh:
+            assert fh.read() == ckpt, "ranged checkpoint write differs"
+        os.remove(cpath[0])
         if gravity:
             gm = torch.cat(gl, dim=1).cpu().numpy()
             gs = d1.g.view(3, -1).cpu().numpy()
@@ -69,8 +77,7 @@ def main():
             print("MISMATCH leaves", bad[:20], len(bad))
         if args:
             np.savez(args[0], multi=multi, single=single)
-    if gravity:
-        drv.close()
+    drv.release_peers()  # collective peer-exchange teardown (also closes the gravity solver)
     tdist.barrier()
     tdist.destroy_process_group()
 
