@@ -54,6 +54,12 @@ constexpr double kPressureFloor = 1e-12;  // euler.hpp:16
 // Each face slab is TMA-loaded either from the leaf's own ghost cells or,
 // for a same-level neighbour, straight from the neighbour's interior
 // (StageLaunch::face_src): the same-level ghost copy is fused into the load.
+// Accumulator layout: x rows of 8 cells at a pitch of 9 doubles, so the x-axis
+// update (lanes on consecutive (y, z) pencils) hits distinct banks instead of
+// the two a row pitch of 8 would give; y and z updates stay unit-stride.
+constexpr int kAccV = 64 * 9;  // per var
+__device__ __forceinline__ int acc_at(int c) { return (c >> 3) * 9 + (c & 7); }
+
 template <int V>
 struct Lay {
   static constexpr int B0 = 0;
@@ -64,8 +70,8 @@ struct Lay {
   static constexpr int ZL = YH + V * 128;
   static constexpr int ZH = ZL + V * 128;
   static constexpr int kStaged = ZH + V * 128;  // = V*1408 doubles
-  static constexpr int kAcc = kStaged;          // accumulator [V][E^3]
-  static constexpr int kU0 = kAcc + V * kE3;     // RK3 u0 block [V][E^3] (bulk-copied)
+  static constexpr int kAcc = kStaged;          // accumulator [V][64 rows][9] (acc_at)
+  static constexpr int kU0 = kAcc + V * kAccV;   // RK3 u0 block [V][E^3] (bulk-copied)
   static constexpr int kDoubles = kU0 + V * kE3;
   static constexpr int kBytes = kDoubles * 8 + 64;  // + mbarrier/scratch
   static constexpr uint32_t kTxBytes = (uint32_t)(V * 1408 * 8);
@@ -371,7 +377,7 @@ __device__ __forceinline__ void axis_pass(const double* __restrict__ sm, double*
         const int ci = interior_index(AXIS, 3 * r + k, c1, c2);
 #pragma unroll
         for (int v = 0; v < V; ++v) {
-          double& o = acc[v * kE3 + ci];
+          double& o = acc[v * kAccV + acc_at(ci)];
           if constexpr (FAST)
             o = fma(-cdt, D[k][v], o);
           else
@@ -538,7 +544,7 @@ __global__ void __launch_bounds__(kStageThreads, 2)
     if (interior) {
       const int ci = c;
 #pragma unroll
-      for (int v = 0; v < V; ++v) acc[v * kE3 + ci] = u[v];
+      for (int v = 0; v < V; ++v) acc[v * kAccV + acc_at(ci)] = u[v];
       if (p.u0_save) {
         double* u0s = p.u0_save + (long long)slot * p.u0_save_stride;
 #pragma unroll
@@ -594,7 +600,7 @@ __global__ void __launch_bounds__(kStageThreads, 2)
     for (int c = tid; c < kE3; c += kStageThreads) {
       const int z = c >> 6, y = (c >> 3) & 7, x = c & 7;
 #pragma unroll
-      for (int v = 0; v < V; ++v) outp[((v * kS + z + 2) * kS + y + 2) * kS + x + 2] = acc[v * kE3 + c];
+      for (int v = 0; v < V; ++v) outp[((v * kS + z + 2) * kS + y + 2) * kS + x + 2] = acc[v * kAccV + acc_at(c)];
     }
     return;
   }
@@ -603,7 +609,7 @@ __global__ void __launch_bounds__(kStageThreads, 2)
   for (int c = tid; c < kE3; c += kStageThreads) {
     double u[V];
 #pragma unroll
-    for (int v = 0; v < V; ++v) u[v] = acc[v * kE3 + c];
+    for (int v = 0; v < V; ++v) u[v] = acc[v * kAccV + acc_at(c)];
     if constexpr (V == 5) {
       if (euler && p.grav) {  // gravity source with the stage input's primitives
         const double* pq = sm + L::B0 + (c >> 3) * 10 + (c & 7);
