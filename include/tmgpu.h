@@ -200,6 +200,15 @@ int tmgpu_forest_set_peer(tmgpu_forest* f, int on, tmgpu_error* err);
 int tmgpu_stream_wait(void* waiter, void* signaller);
 int tmgpu_forest_step(tmgpu_forest* f, double dt, double cfl, double gamma, int flags,
                       void* stream, double* dt_used, tmgpu_error* err);
+/* the step with its input and output as compact interiors [slot][vars][E^3] in device memory
+ * (either may be NULL): the input is scattered into the arena by the step's first pass (fused
+ * with the CFL wave speeds when cfl > 0; stage 1's gravity masses read it directly) and the
+ * output written by the last stage's epilogue (a separate gather with reflux or the 6-solve
+ * cadence, whose corrections follow that stage) — the end-to-end path's copies without
+ * separate scatter/gather passes. Equal to set_interior + step + get_interior, bit for bit. */
+int tmgpu_forest_step_io(tmgpu_forest* f, const double* in_compact, double* out_compact, double dt,
+                         double cfl, double gamma, int flags, void* stream, double* dt_used,
+                         tmgpu_error* err);
 int tmgpu_forest_check(tmgpu_forest* f, void* stream, tmgpu_error* err);
 /* per-phase device timing (CUDA events) of subsequent steps: accumulated ms */
 int tmgpu_forest_set_timing(tmgpu_forest* f, int on, tmgpu_error* err);
@@ -274,6 +283,10 @@ int tmgpu_gravity_amr_mass_from_arena(tmgpu_gravity_amr* G, const double* arena,
 /* masses from a device density [n][512] by local slot (m = rho * h^3, as mass_from_arena) */
 int tmgpu_gravity_amr_mass_from_density(tmgpu_gravity_amr* G, const double* rho, void* stream,
                                         tmgpu_error* err);
+/* the same from a density at slot stride `slot_stride` doubles (>= 512), e.g. var 0 of compact
+ * interiors [n][vars][512] (slot_stride = vars * 512) */
+int tmgpu_gravity_amr_mass_from_compact(tmgpu_gravity_amr* G, const double* rho, long long slot_stride,
+                                        void* stream, tmgpu_error* err);
 int tmgpu_gravity_amr_solve(tmgpu_gravity_amr* G, const double* mass, double* phi, double* g,
                             int flags, void* stream, tmgpu_error* err);
 int tmgpu_gravity_amr_am_stats(tmgpu_gravity_amr* G, double* out);

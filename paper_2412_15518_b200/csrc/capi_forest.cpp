@@ -800,7 +800,7 @@ namespace {
 // or from a compact density, then the FMM into (g_phi, gout). The caller makes
 // `st` wait for f->ev_grav before reading gout.
 int grav_solve(tmgpu_forest* f, cudaStream_t st, const double* arena, const double* rho, double* gout,
-               tmgpu_error* err) {
+               tmgpu_error* err, long long rho_stride = 512) {
   cudaStream_t gs = f->grav_stream ? f->grav_stream : st;
   cudaError_t e = cudaSuccess;
   if (gs != st) {
@@ -809,7 +809,7 @@ int grav_solve(tmgpu_forest* f, cudaStream_t st, const double* arena, const doub
     if (e != cudaSuccess) return cuda_err(err, e, "tmgpu_forest_step: gravity fork");
   }
   int rc = arena ? tmgpu_gravity_amr_mass_from_arena(f->gsolver, arena, f->forest.config().vars, gs, err)
-                 : tmgpu_gravity_amr_mass_from_density(f->gsolver, rho, gs, err);
+                 : tmgpu_gravity_amr_mass_from_compact(f->gsolver, rho, rho_stride, gs, err);
   if (rc == TMGPU_OK)
     rc = tmgpu_gravity_amr_solve(f->gsolver, nullptr, f->g_phi, gout, f->g_flags | TMGPU_ASYNC, gs, err);
   if (rc != TMGPU_OK) return rc;
@@ -820,6 +820,12 @@ int grav_solve(tmgpu_forest* f, cudaStream_t st, const double* arena, const doub
 
 int tmgpu_forest_step(tmgpu_forest* f, double dt, double cfl, double gamma, int flags, void* stream,
                       double* dt_used, tmgpu_error* err) {
+  return tmgpu_forest_step_io(f, nullptr, nullptr, dt, cfl, gamma, flags, stream, dt_used, err);
+}
+
+int tmgpu_forest_step_io(tmgpu_forest* f, const double* in_compact, double* out_compact, double dt,
+                         double cfl, double gamma, int flags, void* stream, double* dt_used,
+                         tmgpu_error* err) {
   if (err) std::memset(err, 0, sizeof(*err));
   if (int rc = ready(f, err)) return rc;
   const int V = f->forest.config().vars;
@@ -835,15 +841,21 @@ int tmgpu_forest_step(tmgpu_forest* f, double dt, double cfl, double gamma, int 
     cudaEventRecord(f->ev[0], st);
   }
   if (cadence) {  // stage 1's solve on the step's initial state, overlapping the CFL and exchange
-    if (int rc = grav_solve(f, st, f->arena(), nullptr, f->g_a, err)) return rc;
+    const int rc = in_compact ? grav_solve(f, st, nullptr, in_compact, f->g_a, err, (long long)V * 512)
+                              : grav_solve(f, st, f->arena(), nullptr, f->g_a, err);
+    if (rc) return rc;
   } else if (f->grav_stream) {
     e = cudaEventRecord(f->ev_grav, f->grav_stream);  // gravity enqueued so far
   }
   if (!(flags & TMGPU_ASYNC) && e == cudaSuccess)
     e = cudaMemsetAsync(f->err_dev, 0xff, sizeof(unsigned long long), st);
+  if (e == cudaSuccess && in_compact && !(cfl > 0.0))  // input scatter (fused below when cfl > 0)
+    e = interior_copy(f->arena(), const_cast<double*>(in_compact), V, f->nslots, true, st);
   if (e == cudaSuccess && cfl > 0.0) {
-    e = launch_max_wavespeed(f->arena(), (long long)V * 1728, nullptr, 0, nullptr, gamma, V, f->nslots,
-                             f->speeds, st);
+    e = in_compact ? launch_scatter_wavespeed(in_compact, f->arena(), (long long)V * 1728, gamma, f->nslots,
+                                              f->speeds, st)
+                   : launch_max_wavespeed(f->arena(), (long long)V * 1728, nullptr, 0, nullptr, gamma, V,
+                                          f->nslots, f->speeds, st);
     if (e == cudaSuccess) e = launch_cfl_reduce(f->speeds, f->leaf_dx, f->nslots, cfl, f->dt_dev, st);
     if (e == cudaSuccess && f->world() > 1) {  // global dt: min over ranks (exact)
       std::string why;
@@ -887,6 +899,9 @@ int tmgpu_forest_step(tmgpu_forest* f, double dt, double cfl, double gamma, int 
     return v && v[0] == '1';
   }();
   const bool split = split_env && cadence && !exact && !overlap && f->grav_stream;
+  // a correction after the last stage (reflux, the 6-solve source) rules out
+  // writing the output from the stage epilogue: gather after the loop instead
+  const bool late_fix = f->reflux || cadence == 6;
   for (int stage = 1; stage <= 3 && e == cudaSuccess; ++stage) {
     std::string why;
     if (stage > 1 && cadence >= 3) {  // this stage's field from its input state
@@ -921,6 +936,7 @@ int tmgpu_forest_step(tmgpu_forest* f, double dt, double cfl, double gamma, int 
     if (e == cudaSuccess && wait_grav && !split) e = cudaStreamWaitEvent(st, f->ev_grav, 0);
     if (timed) cudaEventRecord(f->ev[2 * stage], st);
     p.rk_stage = stage;
+    p.out_compact = (stage == 3 && !late_fix) ? out_compact : nullptr;
     p.rho_save = cadence == 6 ? f->rho_tilde : nullptr;
     p.u0_save = stage == 1 ? f->u0 : nullptr;
     p.u0_save_stride = (long long)V * 512;
@@ -963,6 +979,8 @@ int tmgpu_forest_step(tmgpu_forest* f, double dt, double cfl, double gamma, int 
     f->cur = dst;
     if (timed) cudaEventRecord(f->ev[2 * stage + 1], st);
   }
+  if (e == cudaSuccess && out_compact && late_fix)
+    e = interior_copy(f->arena(), out_compact, V, f->nslots, false, st);
   if (timed && e == cudaSuccess) f->pending_timed = 1;
   if (e != cudaSuccess) return cuda_err(err, e, "tmgpu_forest_step");
   if (flags & TMGPU_ASYNC) return TMGPU_OK;

@@ -72,10 +72,11 @@ __device__ __forceinline__ double centre(long long gi, int d) {
 
 // arena slots 0..nslots-1 are the canonical slots lo.. (distributed: the owned range)
 // V > 0: density from a ghosted arena [slot][V][12^3]; V == 0: from a compact
-// [slot][512] density (the stage's provisional density, 6-solve cadence)
+// density at slot stride cstride (the stage's provisional density [slot][512],
+// 6-solve cadence; or var 0 of compact interiors [slot][V][512])
 __global__ void amr_mass_kernel(const double* __restrict__ arena, int V, long long nslots,
                                 long long lo, const int* __restrict__ slot_level,
-                                double* __restrict__ mass) {
+                                double* __restrict__ mass, long long cstride = 512) {
   const long long total = nslots * 512;
   for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
        t += (long long)gridDim.x * blockDim.x) {
@@ -84,7 +85,7 @@ __global__ void amr_mass_kernel(const double* __restrict__ arena, int V, long lo
     const int i = c & 7, j = (c >> 3) & 7, k = c >> 6;
     const double h = 1.0 / (double)(8LL << slot_level[lo + s]);
     const double dV = h * h * h;
-    const double rho = V ? arena[s * V * 1728 + ((k + 2) * 12 + (j + 2)) * 12 + (i + 2)] : arena[t];
+    const double rho = V ? arena[s * V * 1728 + ((k + 2) * 12 + (j + 2)) * 12 + (i + 2)] : arena[s * cstride + c];
     mass[lo * 512 + t] = rho * dV;
   }
 }
@@ -1824,12 +1825,17 @@ int tmgpu_gravity_amr_mass_from_arena(tmgpu_gravity_amr* G, const double* arena,
 
 int tmgpu_gravity_amr_mass_from_density(tmgpu_gravity_amr* G, const double* rho, void* stream,
                                         tmgpu_error* err) {
+  return tmgpu_gravity_amr_mass_from_compact(G, rho, 512, stream, err);
+}
+
+int tmgpu_gravity_amr_mass_from_compact(tmgpu_gravity_amr* G, const double* rho, long long slot_stride,
+                                        void* stream, tmgpu_error* err) {
   if (err) std::memset(err, 0, sizeof(*err));
-  if (!G || !rho) return set_err(err, TMGPU_ERR_INVALID, "gravity mass_from_density: null argument");
+  if (!G || !rho || slot_stride < 512) return set_err(err, TMGPU_ERR_INVALID, "gravity mass_from_compact: bad argument");
   GravAmrWork& w = G->w;
   cudaStream_t st = as_stream(stream);
   amr_mass_kernel<<<grid_for((w.hi - w.lo) * 512), 128, 0, st>>>(rho, 0, w.hi - w.lo, w.lo, w.slot_level,
-                                                                 w.mass);
+                                                                 w.mass, slot_stride);
   g_launches.fetch_add(1, std::memory_order_relaxed);
   return cuda_err(err, cudaGetLastError(), "tmgpu_gravity_amr_mass_from_density");
 }

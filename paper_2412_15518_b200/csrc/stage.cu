@@ -94,6 +94,48 @@ __global__ void __launch_bounds__(256) max_wavespeed_kernel(const double* __rest
   }
 }
 
+// The step's first pass when its input arrives as compact interiors
+// [slot][V][E^3] (tmgpu_forest_step_io): each CTA copies its slot's interior
+// into the ghosted arena (the scatter of tmgpu_forest_interior) and, from the
+// same registers, computes max_wavespeed exactly as max_wavespeed_kernel
+// (Euler; the reference's floors and divisions): one read of the input
+// instead of a scatter pass plus a wavespeed pass over the arena.
+__global__ void __launch_bounds__(256) scatter_wavespeed_kernel(const double* __restrict__ compact,
+                                                                double* __restrict__ arena,
+                                                                long long slot_stride, double gamma,
+                                                                double* __restrict__ result) {
+  const int s = blockIdx.x;
+  __shared__ double red[8];
+  const double* src = compact + (long long)s * 5 * kE3;
+  double* g = arena + (long long)s * slot_stride;
+  const int s3 = kS * kS * kS;
+  double smax = 0.0;
+  for (int c = threadIdx.x; c < kE3; c += blockDim.x) {
+    const int i = kG + (c & 7), j = kG + ((c >> 3) & 7), k = kG + (c >> 6);
+    const int o = (k * kS + j) * kS + i;
+    double u[5];
+#pragma unroll
+    for (int v = 0; v < 5; ++v) {
+      u[v] = src[v * kE3 + c];
+      g[v * s3 + o] = u[v];
+    }
+    const double rho = stdmax_(u[0], kRhoFloor);
+    const double iu = u[1] / rho, iv = u[2] / rho, iw = u[3] / rho;
+    const double ke = 0.5 * rho * (iu * iu + iv * iv + iw * iw);
+    const double pr = stdmax_((gamma - 1.0) * (u[4] - ke), kPressureFloor);
+    const double sp = sqrt(iu * iu + iv * iv + iw * iw) + sqrt(gamma * pr / rho);
+    smax = stdmax_(smax, sp);
+  }
+  for (int off = 16; off > 0; off >>= 1) smax = stdmax_(smax, __shfl_xor_sync(0xffffffffu, smax, off));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = smax;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double m = red[0];
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) m = stdmax_(m, red[w]);
+    result[s] = m;
+  }
+}
+
 // rk3.hpp:18-27
 __global__ void rk3_combine_kernel(int stage, const double* __restrict__ u0,
                                    const double* __restrict__ v, double* __restrict__ out,
@@ -196,6 +238,14 @@ cudaError_t launch_max_wavespeed(const double* in, long long slot_stride, const 
   if (count <= 0) return cudaSuccess;
   max_wavespeed_kernel<<<(unsigned)count, 256, 0, stream>>>(in, slot_stride, hdr, hdr_stride,
                                                             leaf_dx, g_gamma, V, result);
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_scatter_wavespeed(const double* compact, double* arena, long long slot_stride, double gamma,
+                                     long long count, double* result, cudaStream_t stream) {
+  if (count <= 0) return cudaSuccess;
+  scatter_wavespeed_kernel<<<(unsigned)count, 256, 0, stream>>>(compact, arena, slot_stride, gamma, result);
   g_launches.fetch_add(1, std::memory_order_relaxed);
   return cudaGetLastError();
 }

@@ -447,6 +447,7 @@ __device__ __forceinline__ void finish_cell(double (&u)[V], const StageLaunch& p
       outp[((v * kS + z + 2) * kS + y + 2) * kS + x + 2] = o;
     else
       outp[v * kE3 + c] = o;
+    if (p.out_compact) p.out_compact[((long long)slot * V + v) * kE3 + c] = o;
   }
 }
 

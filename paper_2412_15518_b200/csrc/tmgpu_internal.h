@@ -56,6 +56,9 @@ struct StageLaunch {
   // split stage (gravity step): store the raw update only; the floors, the
   // source, finiteness and the combine follow in stage_epilogue_kernel
   int defer;
+  // optional second output: the final values also as compact interiors
+  // [slot][V][E^3] (tmgpu_forest_step_io's output, fused into the last stage)
+  double* out_compact;
   unsigned long long* err;  // atomicMin of (slice << 32 | var-major interior index)
   int count;
 };
@@ -82,6 +85,10 @@ cudaError_t launch_stage_epilogue(bool fast, const double* in_arena, const Stage
 cudaError_t launch_max_wavespeed(const double* in, long long slot_stride, const double* hdr,
                                  long long hdr_stride, const double* leaf_dx, double g_gamma,
                                  int V, long long count, double* result, cudaStream_t stream);
+
+// compact interiors [slot][5][E^3] -> arena + max_wavespeed per slot (the step_io input pass)
+cudaError_t launch_scatter_wavespeed(const double* compact, double* arena, long long slot_stride, double gamma,
+                                     long long count, double* result, cudaStream_t stream);
 
 cudaError_t launch_cfl_reduce(const double* speeds, const double* leaf_dx, long long n, double cfl,
                               double* dt, cudaStream_t stream);

@@ -17,6 +17,9 @@ from .amr import Forest, unpack
 from .hydro import SolverError
 
 
+lib.tmgpu_forest_step_io.restype = C.c_int
+lib.tmgpu_forest_step_io.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_double, C.c_double, C.c_double,
+                                     C.c_int, C.c_void_p, C.POINTER(C.c_double), C.POINTER(TmgpuError)]
 lib.tmgpu_forest_set_reflux.restype = C.c_int
 lib.tmgpu_forest_set_reflux.argtypes = [C.c_void_p, C.c_int, C.POINTER(TmgpuError)]
 
@@ -38,17 +41,21 @@ class HydroDriver:
             err = TmgpuError()
             _lib.check(lib.tmgpu_forest_set_reflux(forest.h, 1, C.byref(err)), err)
 
-    def step(self, dt: float | None = None, stream=None, sync: bool = True) -> float | None:
+    def step(self, dt: float | None = None, stream=None, sync: bool = True, io=None) -> float | None:
         """Advance one SSP-RK3 step. dt None: CFL dt on the device. Returns
         the dt used (None when sync=False; errors are then latched until
-        ``check``)."""
+        ``check``). io = (dev_in, dev_out): the step's input and/or output as
+        compact interiors [local][V][E^3] in device memory (tensors or None) —
+        scattered / gathered inside the step's own passes (tmgpu_forest_step_io)."""
         flags = ((_lib.TMGPU_FAST if self.fast else 0) | (0 if sync else _lib.TMGPU_ASYNC) |
                  (_lib.TMGPU_EXACT_GHOSTS if self.exact_ghosts else 0))
         used = C.c_double(0.0)
         err = TmgpuError()
-        rc = lib.tmgpu_forest_step(self.forest.h, float(dt or 0.0),
-                                   self.cfl if dt is None else 0.0, self.gamma, flags, stream,
-                                   C.byref(used), C.byref(err))
+        din, dout = io if io is not None else (None, None)
+        rc = lib.tmgpu_forest_step_io(self.forest.h, None if din is None else din.data_ptr(),
+                                      None if dout is None else dout.data_ptr(), float(dt or 0.0),
+                                      self.cfl if dt is None else 0.0, self.gamma, flags, stream,
+                                      C.byref(used), C.byref(err))
         _lib.check(rc, err, SolverError)
         self.steps += 1
         return used.value if sync else None
@@ -200,7 +207,9 @@ class HostStepPipeline:
     stream while step k computes, the device->host copy of step k's result on a
     second copy stream while step k+1 computes (PCIe is full duplex). Device
     staging is double-buffered; CUDA events order every buffer reuse, so each
-    step still moves its whole input in and its whole result out.
+    step still moves its whole input in and its whole result out. The step
+    itself reads the input staging buffer in its first pass and writes the output
+    staging buffer from its last stage (tmgpu_forest_step_io).
 
         pipe = HostStepPipeline(GravityHydroDriver(forest))
         for _ in range(n):
@@ -233,13 +242,13 @@ class HostStepPipeline:
             ev_in = torch.cuda.Event()
             ev_in.record(self.h2d)
         cs.wait_event(ev_in)
-        self.forest.set_interior(self.dev_in[b], stream=cs.cuda_stream, sync=False)
-        self.in_free[b] = torch.cuda.Event()
-        self.in_free[b].record(cs)
-        self.driver.step(dt, stream=cs.cuda_stream, sync=False)
         if self.out_free[b] is not None:
             cs.wait_event(self.out_free[b])
-        self.forest.get_interior(self.dev_out[b], stream=cs.cuda_stream, sync=False)
+        # the step reads its input straight from the staging buffer and its last
+        # stage writes the output staging buffer (no separate scatter / gather)
+        self.driver.step(dt, stream=cs.cuda_stream, sync=False, io=(self.dev_in[b], self.dev_out[b]))
+        self.in_free[b] = torch.cuda.Event()
+        self.in_free[b].record(cs)
         ev_out = torch.cuda.Event()
         ev_out.record(cs)
         with torch.cuda.stream(self.d2h):

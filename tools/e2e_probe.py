@@ -41,10 +41,14 @@ def with_io():
 
 
 print("step + dev I/O %.3f ms" % timed(with_io))
+print("step_io        %.3f ms" % timed(lambda: drv.step(stream=cs.cuda_stream, sync=False, io=(dev, out))))
 pin_in = torch.from_numpy(np.ascontiguousarray(state)).pin_memory()
 pin_out = torch.empty_like(pin_in).pin_memory()
 pipe = HostStepPipeline(drv)
 print("pipeline       %.3f ms" % timed(lambda: pipe.step(pin_in, pin_out), pipe.h2d))
+K = 100
+print("pipeline x100  %.3f ms" % timed(lambda: pipe.step(pin_in, pin_out), pipe.h2d))
+K = 30
 s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
 
 
