@@ -1,5 +1,6 @@
 // C ABI: hydro stage entry points (include/tmgpu.h). Host-side only; the
 // kernels live in stage.cu.
+#include <algorithm>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -86,6 +87,151 @@ int stage_fused_device(const double* in, double* out, size_t in_slice, size_t ou
   return TMGPU_OK;
 }
 
+// ---- host-pointer path (the drop-in's KernelFn over RegionBuffers) --------
+// The reference calls KernelFn with its region's host buffers (pageable heap,
+// bufferpool.cpp) from arbitrary scheduler workers, concurrently. Each calling
+// thread keeps a context: two streams, device slice buffers and pinned bounce
+// buffers for a chunk of slices each, allocated once and grown on demand. A
+// call is chunked: while the GPU runs chunk c (H2D, the fused stage, D2H on
+// stream c % 2) the thread copies chunk c + 1 into the other pinned buffer and
+// chunk c - 1's results out of it — one cudaMemcpyAsync per direction per
+// chunk, no allocation, no pageable DMA.
+constexpr size_t kChunkSlices = 64;
+
+struct HostCtx {
+  cudaStream_t st[2] = {nullptr, nullptr};
+  cudaEvent_t done[2] = {nullptr, nullptr};
+  double *d_in[2] = {}, *d_out[2] = {}, *h_in[2] = {}, *h_out[2] = {};
+  unsigned long long *d_err = nullptr, *h_err = nullptr;  // 2 words
+  size_t cap_in = 0, cap_out = 0;  // doubles per buffer
+  bool ok = false;
+  ~HostCtx() {
+    for (int b = 0; b < 2; ++b) {
+      if (st[b]) cudaStreamSynchronize(st[b]);
+      if (done[b]) cudaEventDestroy(done[b]);
+      if (st[b]) cudaStreamDestroy(st[b]);
+      cudaFree(d_in[b]);
+      cudaFree(d_out[b]);
+      cudaFreeHost(h_in[b]);
+      cudaFreeHost(h_out[b]);
+    }
+    cudaFree(d_err);
+    cudaFreeHost(h_err);
+  }
+  cudaError_t reserve(size_t in_doubles, size_t out_doubles) {
+    cudaError_t e = cudaSuccess;
+    if (!ok) {
+      for (int b = 0; b < 2 && e == cudaSuccess; ++b) {
+        e = cudaStreamCreateWithFlags(&st[b], cudaStreamNonBlocking);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&done[b], cudaEventDisableTiming);
+      }
+      if (e == cudaSuccess) e = cudaMalloc(&d_err, 2 * sizeof(unsigned long long));
+      if (e == cudaSuccess) e = cudaMallocHost(&h_err, 2 * sizeof(unsigned long long));
+      if (e != cudaSuccess) return e;
+      ok = true;
+    }
+    if (in_doubles > cap_in) {
+      for (int b = 0; b < 2 && e == cudaSuccess; ++b) {
+        cudaFree(d_in[b]);
+        cudaFreeHost(h_in[b]);
+        d_in[b] = h_in[b] = nullptr;
+        e = cudaMalloc(&d_in[b], in_doubles * sizeof(double));
+        if (e == cudaSuccess) e = cudaMallocHost(&h_in[b], in_doubles * sizeof(double));
+      }
+      cap_in = e == cudaSuccess ? in_doubles : 0;
+    }
+    if (e == cudaSuccess && out_doubles > cap_out) {
+      for (int b = 0; b < 2 && e == cudaSuccess; ++b) {
+        cudaFree(d_out[b]);
+        cudaFreeHost(h_out[b]);
+        d_out[b] = h_out[b] = nullptr;
+        e = cudaMalloc(&d_out[b], out_doubles * sizeof(double));
+        if (e == cudaSuccess) e = cudaMallocHost(&h_out[b], out_doubles * sizeof(double));
+      }
+      cap_out = e == cudaSuccess ? out_doubles : 0;
+    }
+    return e;
+  }
+};
+
+HostCtx& host_ctx() {
+  thread_local HostCtx ctx;
+  return ctx;
+}
+
+// enqueue one chunk of `n` slices (already in h_in[b]) on stream b
+cudaError_t enqueue_chunk(HostCtx& C, int b, size_t n, size_t in_slice, size_t out_slice, int vars, bool fast,
+                          std::string* why) {
+  cudaStream_t st = C.st[b];
+  cudaError_t e = cudaMemcpyAsync(C.d_in[b], C.h_in[b], n * in_slice * sizeof(double), cudaMemcpyHostToDevice, st);
+  if (e == cudaSuccess) e = cudaMemsetAsync(C.d_err + b, 0xff, sizeof(unsigned long long), st);
+  StageMaps maps;
+  if (e == cudaSuccess && make_stage_maps(C.d_in[b] + kHeader, vars, (long long)in_slice, (long long)n, &maps, why) !=
+                              TMGPU_OK)
+    e = cudaErrorInvalidValue;
+  if (e == cudaSuccess) {
+    const size_t e3 = (size_t)vars * 512;
+    double* out = C.d_out[b];
+    StageLaunch p{};
+    p.hdr = C.d_in[b];
+    p.hdr_stride = (long long)in_slice;
+    p.out = out;
+    p.out_stride = (long long)out_slice;
+    p.faces = out + e3;
+    p.faces_stride = (long long)out_slice;
+    p.diag = out + e3 + 6 * (size_t)vars * 64;
+    p.diag_stride = (long long)out_slice;
+    p.err = C.d_err + b;
+    p.count = (int)n;
+    e = launch_stage(vars, fast, maps, p, st);
+  }
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(C.h_out[b], C.d_out[b], n * out_slice * sizeof(double), cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(C.h_err + b, C.d_err + b, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaEventRecord(C.done[b], st);
+  return e;
+}
+
+int stage_fused_host(const double* in, double* out, size_t in_slice, size_t out_slice, size_t count, int vars,
+                     bool fast, tmgpu_error* err) {
+  HostCtx& C = host_ctx();
+  const size_t K = std::min(count, kChunkSlices);
+  cudaError_t e = C.reserve(K * in_slice, K * out_slice);
+  if (e != cudaSuccess) return cuda_err(err, e, "tmgpu_stage_fused host staging");
+  const size_t nch = (count + K - 1) / K;
+  std::string why;
+  unsigned long long first_bad = ~0ull;  // (global slice << 32 | index) of the first failure
+  auto retire = [&](size_t c) -> cudaError_t {  // results of chunk c out of its pinned buffer
+    const int b = (int)(c & 1);
+    cudaError_t r = cudaEventSynchronize(C.done[b]);
+    if (r != cudaSuccess) return r;
+    const size_t n = std::min(K, count - c * K);
+    std::memcpy(out + c * K * out_slice, C.h_out[b], n * out_slice * sizeof(double));
+    const unsigned long long w = C.h_err[b];
+    if (w != ~0ull && first_bad == ~0ull)
+      first_bad = (((unsigned long long)(c * K) + (w >> 32)) << 32) | (w & 0xffffffffull);
+    return cudaSuccess;
+  };
+  for (size_t c = 0; c < nch && e == cudaSuccess; ++c) {
+    const int b = (int)(c & 1);
+    if (c >= 2) e = retire(c - 2);  // frees buffer b (the GPU has moved on to chunk c - 1)
+    if (e != cudaSuccess) break;
+    const size_t n = std::min(K, count - c * K);
+    std::memcpy(C.h_in[b], in + c * K * in_slice, n * in_slice * sizeof(double));
+    e = enqueue_chunk(C, b, n, in_slice, out_slice, vars, fast, &why);
+  }
+  for (size_t c = nch >= 2 ? nch - 2 : 0; c < nch && e == cudaSuccess; ++c) e = retire(c);
+  if (e != cudaSuccess) {
+    cudaStreamSynchronize(C.st[0]);
+    cudaStreamSynchronize(C.st[1]);
+    if (!why.empty()) return set_err(err, TMGPU_ERR_INVALID, why.c_str());
+    return cuda_err(err, e, "tmgpu_stage_fused");
+  }
+  if (first_bad != ~0ull) return solver_error(err, first_bad);
+  return TMGPU_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -116,29 +262,7 @@ int tmgpu_stage_fused(const double* in, double* out, size_t in_slice, size_t out
   if (!(flags & TMGPU_HOST_PTRS))
     return stage_fused_device(in, out, in_slice, out_slice, count, vars, fast, st, err);
 
-  // Host buffers: stage through stream-ordered device allocations.
-  keep_pool_warm();
-  const size_t in_bytes = count * in_slice * sizeof(double);
-  const size_t out_bytes = count * out_slice * sizeof(double);
-  double *d_in = nullptr, *d_out = nullptr;
-  cudaError_t e = cudaMallocAsync(&d_in, in_bytes, st);
-  if (e == cudaSuccess) e = cudaMallocAsync(&d_out, out_bytes, st);
-  if (e == cudaSuccess) e = cudaMemcpyAsync(d_in, in, in_bytes, cudaMemcpyHostToDevice, st);
-  int rc = TMGPU_OK;
-  if (e == cudaSuccess) {
-    rc = stage_fused_device(d_in, d_out, in_slice, out_slice, count, vars, fast, st, err);
-    if (rc == TMGPU_OK || rc == TMGPU_ERR_SOLVER) {
-      cudaError_t e2 = cudaMemcpyAsync(out, d_out, out_bytes, cudaMemcpyDeviceToHost, st);
-      if (e2 == cudaSuccess) e2 = cudaStreamSynchronize(st);
-      if (e2 != cudaSuccess && rc == TMGPU_OK) rc = cuda_err(err, e2, "tmgpu_stage_fused D2H");
-    }
-  } else {
-    rc = cuda_err(err, e, "tmgpu_stage_fused H2D");
-  }
-  if (d_in) cudaFreeAsync(d_in, st);
-  if (d_out) cudaFreeAsync(d_out, st);
-  cudaStreamSynchronize(st);
-  return rc;
+  return stage_fused_host(in, out, in_slice, out_slice, count, vars, fast, err);
 }
 
 int tmgpu_stage_subgrid(const double* header8, int edge, int ghost, int vars, unsigned lane_width,
