@@ -108,6 +108,7 @@ void tmgpu_forest_destroy(tmgpu_forest* f);
 int tmgpu_forest_refine(tmgpu_forest* f, uint64_t packed, tmgpu_error* err);  /* Tree::refine octree.cpp:200-234 */
 int tmgpu_forest_coarsen(tmgpu_forest* f, uint64_t packed, tmgpu_error* err); /* Tree::coarsen octree.cpp:236-293 */
 size_t tmgpu_forest_leaves(tmgpu_forest* f, uint64_t* out, size_t cap);     /* Tree::leaves octree.cpp:52-77 */
+int tmgpu_forest_is_leaf(tmgpu_forest* f, uint64_t packed);                   /* Node::is_leaf octree.hpp:77 */
 /* Tree::face_neighbor (octree.cpp:92-132): returns kind 0 same, 1 coarser, 2 finer, 3 boundary */
 int tmgpu_forest_face_neighbor(tmgpu_forest* f, uint64_t leaf, int axis, int dir, uint64_t* ids4,
                                int* count);

@@ -144,7 +144,7 @@ class Forest:
     def __init__(self, edge=8, ghost=2, vars=5, max_level=10, root_dims=(1, 1, 1),
                  bc=(0, 0, 0)):
         err = TmgpuError()
-        self.edge, self.ghost, self.vars = edge, ghost, vars
+        self.edge, self.ghost, self.vars, self.max_level = edge, ghost, vars, max_level
         self.stride = edge + 2 * ghost
         self.root_dims, self.bc = tuple(root_dims), tuple(int(b) for b in bc)
         self.h = lib.tmgpu_forest_create(edge, ghost, vars, max_level, (C.c_int * 3)(*root_dims),
@@ -191,6 +191,11 @@ class Forest:
         out = np.zeros(n, dtype=np.uint64)
         lib.tmgpu_forest_leaves(self.h, out.ctypes.data_as(_u64p), n)
         return out
+
+    def is_leaf(self, node) -> bool:
+        lib.tmgpu_forest_is_leaf.restype = C.c_int
+        lib.tmgpu_forest_is_leaf.argtypes = [C.c_void_p, C.c_uint64]
+        return bool(lib.tmgpu_forest_is_leaf(self.h, int(node)))
 
     def leaf_count(self) -> int:
         return int(lib.tmgpu_forest_leaves(self.h, None, 0))
@@ -317,17 +322,28 @@ class Forest:
         err = TmgpuError()
         _lib.check(lib.tmgpu_forest_grids(self.h, g.ctypes.data, 1, C.byref(err)), err)
 
-    def arena_grids(self, which: int, grids: np.ndarray | None = None) -> np.ndarray | None:
+    def arena_grids(self, which: int, grids=None, out=None):
         """Whole ghosted blocks [local][V*S^3] of the current (which=0) or the
-        other ping-pong arena (which=1); with `grids`, write them instead."""
+        other ping-pong arena (which=1); with `grids`, write them instead.
+        `grids` / `out` may also be CUDA tensors (device-to-device copy)."""
         lib.tmgpu_forest_arena_grids.restype = C.c_int
         lib.tmgpu_forest_arena_grids.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_int,
                                                  C.POINTER(TmgpuError)]
         err = TmgpuError()
+        n = self.local_count() * self.vars * self.stride ** 3
         if grids is None:
-            out = np.zeros((self.local_count(), self.vars * self.stride ** 3))
-            _lib.check(lib.tmgpu_forest_arena_grids(self.h, which, out.ctypes.data, 0, C.byref(err)), err)
+            if out is None:
+                out = np.zeros((self.local_count(), self.vars * self.stride ** 3))
+            ptr = out.data_ptr() if hasattr(out, "data_ptr") else out.ctypes.data
+            if out.numel() if hasattr(out, "numel") else out.size != n:
+                raise ValueError("out must hold every local leaf's ghosted block")
+            _lib.check(lib.tmgpu_forest_arena_grids(self.h, which, ptr, 0, C.byref(err)), err)
             return out
+        if hasattr(grids, "data_ptr"):  # CUDA tensor
+            if grids.numel() != n or not grids.is_contiguous():
+                raise ValueError("grids must be a contiguous block of every local leaf")
+            _lib.check(lib.tmgpu_forest_arena_grids(self.h, which, grids.data_ptr(), 1, C.byref(err)), err)
+            return None
         g = np.ascontiguousarray(grids, dtype=np.float64)
         if g.size != self.local_count() * self.vars * self.stride ** 3:
             raise ValueError("grids must hold every local leaf's ghosted block")

@@ -543,6 +543,10 @@ int tmgpu_forest_flag(tmgpu_forest* f, double theta, double rho_floor, int* flag
   return cuda_err(err, e, "tmgpu_forest_flag");
 }
 
+int tmgpu_forest_is_leaf(tmgpu_forest* f, uint64_t packed) {
+  return f && f->forest.is_leaf(NodeId::unpack(packed)) ? 1 : 0;
+}
+
 size_t tmgpu_forest_leaves(tmgpu_forest* f, uint64_t* out, size_t cap) {
   const auto& lv = f->forest.leaves();
   for (size_t i = 0; i < lv.size() && i < cap; ++i) out[i] = lv[i].packed();
@@ -702,10 +706,10 @@ int tmgpu_forest_arena_grids(tmgpu_forest* f, int which, double* ghosted_host, i
   double* a = f->arenas[f->cur ^ which];
   if (!a) return fail(err, TMGPU_ERR_INVALID, "no second arena");
   const size_t bytes = (size_t)f->nslots * f->forest.config().vars * 1728 * sizeof(double);
-  cudaError_t e = cudaDeviceSynchronize();
+  cudaError_t e = cudaDeviceSynchronize();  // the buffer may be host or device memory (UVA)
   if (e == cudaSuccess)
-    e = to_device ? cudaMemcpy(a, ghosted_host, bytes, cudaMemcpyHostToDevice)
-                  : cudaMemcpy(ghosted_host, a, bytes, cudaMemcpyDeviceToHost);
+    e = to_device ? cudaMemcpy(a, ghosted_host, bytes, cudaMemcpyDefault)
+                  : cudaMemcpy(ghosted_host, a, bytes, cudaMemcpyDefault);
   return cuda_err(err, e, "tmgpu_forest_arena_grids");
 }
 

@@ -70,6 +70,21 @@ class HydroDriver:
         if getattr(self.forest, "_peer", False):
             self.forest.set_peer(False)
 
+    def regrid(self, refine=(), coarsen=()) -> None:
+        """Refine then coarsen with the state carried along (Forest.regrid; on a
+        distributed forest the collective dist.regrid, which re-partitions). Every
+        face ghost is filled first (prolongation reads the parent's face ghosts)."""
+        self.forest.fill_faces()
+        if self.forest.local_count() != self.forest.leaf_count():
+            from . import dist
+
+            dist.regrid(self.forest, refine, coarsen)
+        else:
+            self.forest.regrid(refine, coarsen)
+        if self.reflux:
+            err = TmgpuError()
+            _lib.check(lib.tmgpu_forest_set_reflux(self.forest.h, 1, C.byref(err)), err)
+
 
 lib.tmgpu_stream_wait.restype = C.c_int
 lib.tmgpu_stream_wait.argtypes = [C.c_void_p, C.c_void_p]
@@ -174,10 +189,20 @@ class GravityHydroDriver(HydroDriver):
 
     def regrid(self, refine=(), coarsen=()) -> None:
         """Refine then coarsen leaves with the state carried along (the
-        reference's prolong_cell / restrict_cells, Forest.regrid), then rebuild
-        the gravity plan and field for the new topology (and the reflux plan)."""
+        reference's prolong_cell / restrict_cells, Forest.regrid; on a
+        distributed forest the collective dist.regrid, which re-partitions), then
+        rebuild the gravity plan and field for the new topology (and the reflux
+        plan)."""
         self.close()
-        self.forest.regrid(refine, coarsen)
+        if getattr(self, "moment_transport", "") == "peer":
+            self.gravity.set_peer(False)  # collective, before the solver goes away
+        self.forest.fill_faces()  # every face ghost valid: prolongation reads the parent's
+        if self.forest.local_count() != self.forest.leaf_count():
+            from . import dist
+
+            dist.regrid(self.forest, refine, coarsen)
+        else:
+            self.forest.regrid(refine, coarsen)
         if self.reflux:
             err = TmgpuError()
             _lib.check(lib.tmgpu_forest_set_reflux(self.forest.h, 1, C.byref(err)), err)

@@ -17,6 +17,37 @@ from paper_2412_15518_b200 import amr, checkpoint, dist  # noqa: E402
 from paper_2412_15518_b200.driver import GravityHydroDriver, HydroDriver  # noqa: E402
 
 
+def regrid_lists(f):
+    """A deterministic refine + coarsen request every rank computes alike: three
+    level-3 leaves refined, then up to two parents of 8 leaf children (not among
+    them) coarsened where the 2:1 rule allows (tried on a topology copy)."""
+    lv = [int(p) for p in f.leaves()]
+    refine = [p for p in lv if amr.unpack(p)[0] == 3][::97][:3]
+    g = dist.replay_topology(f, lv)
+    for p in refine:
+        g.refine(p)
+    have = set(int(p) for p in g.leaves())
+    coarsen = []
+    for p in sorted(have):
+        lvl, i, j, k = amr.unpack(p)
+        if lvl < 2:
+            continue
+        par = amr.pack(lvl - 1, i >> 1, j >> 1, k >> 1)
+        kids = [amr.pack(lvl, 2 * (i >> 1) + (b & 1), 2 * (j >> 1) + ((b >> 1) & 1), 2 * (k >> 1) + (b >> 2))
+                for b in range(8)]
+        if par in coarsen or not all(c in have for c in kids):
+            continue
+        try:
+            g.coarsen(par)
+        except amr.AmrError:
+            continue
+        have = set(int(q) for q in g.leaves())
+        coarsen.append(par)
+        if len(coarsen) == 2:
+            break
+    return refine, coarsen
+
+
 def main():
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     local = int(os.environ.get("LOCAL_RANK", rank))
@@ -24,7 +55,8 @@ def main():
     tdist.init_process_group("nccl", device_id=torch.device("cuda", local))
     gravity = "--gravity" in sys.argv
     peer = "--peer" in sys.argv
-    args = [a for a in sys.argv[1:] if a not in ("--gravity", "--peer")]
+    regrid = "--regrid" in sys.argv
+    args = [a for a in sys.argv[1:] if a not in ("--gravity", "--peer", "--regrid")]
     Drv = GravityHydroDriver if gravity else HydroDriver
     kind, lo, hi = amr.Scenario.rotating_star, 2, 4
     f = amr.build_scenario(kind, lo, hi)
@@ -39,6 +71,11 @@ def main():
     f.set_interior(np.ascontiguousarray(state[a:b]))
     drv = Drv(f)
     dts = [drv.step() for _ in range(3)]
+    if regrid:  # collective regrid + re-partition, then more steps
+        rl, cl = regrid_lists(f)
+        drv.regrid(rl, cl)
+        dts += [drv.step() for _ in range(2)]
+        owner = f._owner
     ckpt = checkpoint.save(None, f, time=sum(dts), step=3)  # collective: rank 0 merges
     # collective, nothing gathered: every rank writes its own byte range
     cpath = os.path.join(os.environ.get("TMPDIR", "/tmp"), f"mgpu_ckpt_{os.getpid() if rank == 0 else 0}.tmck")
@@ -59,6 +96,10 @@ def main():
         g.set_interior(state)
         d1 = Drv(g)
         dts1 = [d1.step() for _ in range(3)]
+        if regrid:
+            d1.regrid(rl, cl)
+            dts1 += [d1.step() for _ in range(2)]
+            assert np.array_equal(g.leaves(), f.leaves())
         single = g.get_interior()
         assert dts == dts1, (dts, dts1)
         assert ckpt == checkpoint.encode(g.leaves(), single, sum(dts1), 3), "checkpoint differs"

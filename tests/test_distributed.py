@@ -132,3 +132,24 @@ def test_peer_halo_step_bitwise_equals_single_gpu(gravity):
                        timeout=900)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     assert "BITWISE_OK" in r.stdout, r.stdout[-3000:]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("extra", [["--regrid"], ["--regrid", "--gravity", "--peer"]])
+def test_distributed_regrid_bitwise_equals_single_gpu(extra):
+    """Collective regrid of a distributed forest (dist.regrid: refine with 2:1
+    cascades and coarsen with the data carried along, re-partition, blocks moved
+    to their new owners; peer exchanges rebuilt) and two more steps == the same
+    on one GPU, bitwise (state, gravity field, checkpoint bytes)."""
+    import torch
+
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs 2 GPUs (gpurun --gpus 2)")
+    script = os.path.join(ROOT, "tests", "mgpu_step.py")
+    n = min(torch.cuda.device_count(), 4)
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+                        f"--nproc-per-node={n}", "--master-addr", "127.0.0.1", "--master-port",
+                        str(29541 + len(extra)), script] + extra, capture_output=True, text=True,
+                       timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    assert "BITWISE_OK" in r.stdout, r.stdout[-3000:]
