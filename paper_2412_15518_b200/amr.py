@@ -335,7 +335,7 @@ class Forest:
             if out is None:
                 out = np.zeros((self.local_count(), self.vars * self.stride ** 3))
             ptr = out.data_ptr() if hasattr(out, "data_ptr") else out.ctypes.data
-            if out.numel() if hasattr(out, "numel") else out.size != n:
+            if (out.numel() if hasattr(out, "numel") else out.size) != n:
                 raise ValueError("out must hold every local leaf's ghosted block")
             _lib.check(lib.tmgpu_forest_arena_grids(self.h, which, ptr, 0, C.byref(err)), err)
             return out
