@@ -77,6 +77,9 @@ def parse():
     ap.add_argument("--cpu-budget", type=float, default=150.0,
                     help="reference arm: stop timing steps after this many seconds")
     ap.add_argument("--hydro-only", action="store_true", help="time the hydro step alone")
+    ap.add_argument("--reflux", action="store_true",
+                    help="flux-register correction at level jumps after every stage (SPEC.md:485; "
+                         "across GPUs too); off by default: the reference's composed step has none")
     ap.add_argument("--solves-per-step", type=int, choices=[1, 3, 6], default=3,
                     help="FMM solves per step: 3 = one per RK stage (default), 6 = the paper's "
                          "count, 1 = once per step")
@@ -178,6 +181,7 @@ def workload_config(n, args, extra=None):
                        f"{step_text(args)}",
            "leaves": n, "cells": n * 512, "subgrid": "8^3 + 2 ghost layers, 5 vars (Euler)",
            "solves_per_step": 0 if args.hydro_only else args.solves_per_step,
+           "reflux": bool(getattr(args, "reflux", False)),
            "l2": "inputs larger than L2 (ghosted arena %.0f MB > 126 MB L2)" % (n * 69120 / 1e6),
            "parity": ("hydro: fast <=1e-10 scaled vs reference" if args.fast else
                       "hydro: bitwise vs the reference build (tests/test_forest_gpu.py)") +
@@ -349,9 +353,10 @@ def run_ours(args, rank, world):
     local_cells = f.local_count() * 512
     gravity = not args.hydro_only
     if gravity:
-        drv = GravityHydroDriver(f, fast=args.fast, solves_per_step=args.solves_per_step)
+        drv = GravityHydroDriver(f, fast=args.fast, solves_per_step=args.solves_per_step,
+                                 reflux=args.reflux)
     else:
-        drv = HydroDriver(f, fast=args.fast)
+        drv = HydroDriver(f, fast=args.fast, reflux=args.reflux)
     stream = torch.cuda.current_stream()
     sp = stream.cuda_stream
 

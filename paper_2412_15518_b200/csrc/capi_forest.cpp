@@ -47,6 +47,11 @@ struct tmgpu_forest {
   double* flux = nullptr;  // [slot][6][V][E^2]
   int *rf_leaf = nullptr, *rf_off = nullptr, *rf_ad = nullptr, *rf_fine = nullptr;
   long long rf_n = 0;
+  // distributed reflux: fine face blocks exchanged after every stage (NCCL)
+  int2* rf_send_items = nullptr;  // (local slot, face) per send entry, peer-major
+  long long rf_nsend = 0, rf_nrecv = 0;
+  double *rf_sbuf = nullptr, *rf_rbuf = nullptr;
+  std::vector<long long> rf_send_off, rf_send_cnt, rf_recv_off, rf_recv_cnt;  // doubles per peer
   const double* grav = nullptr;  // optional gravity g[3][stride] by local slot (device)
   long long grav_stride = 0;
   // optional: the stream the step's gravity is computed on; the step runs its
@@ -969,8 +974,17 @@ int tmgpu_forest_step_io(tmgpu_forest* f, const double* in_compact, double* out_
     }
     if (e == cudaSuccess && f->reflux) {  // SSP-RK3 stage weights 1, 1/4, 2/3
       const double coef = stage == 1 ? 1.0 : (stage == 2 ? 0.25 : 2.0 / 3.0);
-      e = launch_reflux(f->arenas[dst], V, f->flux, f->rf_leaf, f->rf_off, f->rf_ad, f->rf_fine, f->rf_n,
-                        f->leaf_dx, p.dt_ptr, dt, coef, st);
+      if (f->world() > 1) {  // fine face blocks of coarse leaves on other GPUs
+        e = launch_flux_pack(f->flux, V, f->rf_send_items, f->rf_nsend, f->rf_sbuf, st);
+        std::string why;
+        if (e == cudaSuccess)
+          if (int rc = comm_exchange(f->comm, f->rf_sbuf, f->rf_send_off, f->rf_send_cnt, f->rf_rbuf,
+                                     f->rf_recv_off, f->rf_recv_cnt, st, &why))
+            return fail(err, rc, why);
+      }
+      if (e == cudaSuccess)
+        e = launch_reflux(f->arenas[dst], V, f->flux, f->rf_leaf, f->rf_off, f->rf_ad, f->rf_fine, f->rf_n,
+                          f->leaf_dx, p.dt_ptr, dt, coef, st, f->rf_rbuf);
     }
     if (e == cudaSuccess && cadence == 6) {  // second solve on the provisional density, trapezoid source
       if (int rc = grav_solve(f, st, nullptr, f->rho_tilde, f->g_b, err)) return rc;
@@ -1140,35 +1154,83 @@ int tmgpu_forest_set_reflux(tmgpu_forest* f, int on, tmgpu_error* err) {
     p = nullptr;
   };
   drop(f->rf_leaf), drop(f->rf_off), drop(f->rf_ad), drop(f->rf_fine);
-  if (f->flux) cudaFree(f->flux);
+  for (void* q : {(void*)f->flux, (void*)f->rf_send_items, (void*)f->rf_sbuf, (void*)f->rf_rbuf})
+    if (q) cudaFree(q);
   f->flux = nullptr;
+  f->rf_send_items = nullptr;
+  f->rf_sbuf = f->rf_rbuf = nullptr;
+  f->rf_nsend = f->rf_nrecv = 0;
   f->reflux = false;
   f->rf_n = 0;
   if (!on) return TMGPU_OK;
-  if (f->world() > 1) return fail(err, TMGPU_ERR_INVALID, "reflux: single GPU only");
   const int V = f->forest.config().vars;
-  std::vector<int> leaf, off{0}, ad, fine;
+  const int world = f->world(), me = f->rank();
+  // canonical leaf -> owner and local slot (owned ranges are contiguous)
   const auto& leaves = f->forest.leaves();
+  std::vector<int> owner(leaves.size(), 0), local(leaves.size(), -1);
+  if (world > 1) owner = f->owner;
+  {
+    int next = 0;
+    for (size_t g = 0; g < leaves.size(); ++g)
+      if (owner[g] == me) local[g] = next++;
+  }
+  // Coarse leaves with finer faces, in canonical order, faces (axis, dir), the
+  // fine quadrants in face_neighbor order. A fine leaf on another GPU becomes
+  // a received block: both sides walk this same global order, so the
+  // receiver's per-peer list and the sender's per-destination list agree.
+  std::vector<int> leaf, off{0}, ad, fine;
+  std::vector<std::vector<int>> recv_pos(world);         // per peer: entry positions in `fine`
+  std::vector<std::vector<int2>> send_items(world);      // per destination: (local slot, face)
   try {
     for (size_t s = 0; s < leaves.size(); ++s) {
+      const bool mine = owner[s] == me;
       bool any = false;
       for (int axis = 0; axis < 3; ++axis)
         for (int dir : {-1, +1}) {
           const FaceNeighbors fn = f->forest.face_neighbor(leaves[s], axis, dir);
           if (fn.kind != NeighborKind::finer) continue;
-          any = true;
-          ad.push_back(axis);
-          ad.push_back(dir);
-          for (int q = 0; q < 4; ++q) fine.push_back(f->forest.slot_of(fn.ids[q]));
+          const int side_f = dir > 0 ? 0 : 1;  // the fine leaves' face toward the coarse leaf
+          if (mine) {
+            any = true;
+            ad.push_back(axis);
+            ad.push_back(dir);
+          }
+          for (int q = 0; q < 4; ++q) {
+            const int fs = (int)f->forest.slot_of(fn.ids[q]);
+            if (mine) {
+              if (owner[fs] == me) {
+                fine.push_back(local[fs]);
+              } else {
+                recv_pos[owner[fs]].push_back((int)fine.size());
+                fine.push_back(0);  // patched below to -(1 + received entry)
+              }
+            } else if (owner[fs] == me) {
+              send_items[owner[s]].push_back(make_int2(local[fs], 2 * axis + side_f));
+            }
+          }
         }
       if (any) {
-        leaf.push_back((int)s);
+        leaf.push_back(local[s]);
         off.push_back((int)(ad.size() / 2));
       }
     }
   } catch (const std::exception& ex) {
     return fail(err, TMGPU_ERR_INVALID, ex.what());
   }
+  std::vector<int2> sitems;
+  f->rf_send_off.assign(world, 0), f->rf_send_cnt.assign(world, 0);
+  f->rf_recv_off.assign(world, 0), f->rf_recv_cnt.assign(world, 0);
+  long long nr = 0;
+  for (int q = 0; q < world; ++q) {
+    f->rf_recv_off[q] = nr * V * 64;
+    for (int pos : recv_pos[q]) fine[pos] = -(int)(1 + nr++);
+    f->rf_recv_cnt[q] = (long long)recv_pos[q].size() * V * 64;
+    f->rf_send_off[q] = (long long)sitems.size() * V * 64;
+    sitems.insert(sitems.end(), send_items[q].begin(), send_items[q].end());
+    f->rf_send_cnt[q] = (long long)send_items[q].size() * V * 64;
+  }
+  f->rf_nsend = (long long)sitems.size();
+  f->rf_nrecv = nr;
   auto up = [](const std::vector<int>& v, int** out) {
     cudaError_t e = cudaMalloc(out, (v.empty() ? 1 : v.size()) * sizeof(int));
     if (e == cudaSuccess && !v.empty())
@@ -1181,6 +1243,13 @@ int tmgpu_forest_set_reflux(tmgpu_forest* f, int on, tmgpu_error* err) {
   if (e == cudaSuccess) e = up(fine, &f->rf_fine);
   if (e == cudaSuccess) e = cudaMalloc(&f->flux, (size_t)f->nslots * 6 * V * 64 * sizeof(double));
   if (e == cudaSuccess) e = cudaMemset(f->flux, 0, (size_t)f->nslots * 6 * V * 64 * sizeof(double));
+  if (e == cudaSuccess && f->rf_nsend) {
+    e = cudaMalloc(&f->rf_send_items, sitems.size() * sizeof(int2));
+    if (e == cudaSuccess)
+      e = cudaMemcpy(f->rf_send_items, sitems.data(), sitems.size() * sizeof(int2), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMalloc(&f->rf_sbuf, (size_t)f->rf_nsend * V * 64 * sizeof(double));
+  }
+  if (e == cudaSuccess && f->rf_nrecv) e = cudaMalloc(&f->rf_rbuf, (size_t)f->rf_nrecv * V * 64 * sizeof(double));
   if (e != cudaSuccess) return cuda_err(err, e, "tmgpu_forest_set_reflux");
   f->rf_n = (long long)leaf.size();
   f->reflux = true;

@@ -97,7 +97,10 @@ cudaError_t launch_cfl_reduce(const double* speeds, const double* leaf_dx, long 
 cudaError_t launch_reflux(double* arena, int V, const double* flux, const int* leaf_slot,
                           const int* face_off, const int* face_ad, const int* fine, long long nleaves,
                           const double* leaf_dx, const double* dt_ptr, double g_dt, double coef,
-                          cudaStream_t st);
+                          cudaStream_t st, const double* rflux = nullptr);
+// distributed reflux: pack the face flux blocks other GPUs need (reflux.cu)
+cudaError_t launch_flux_pack(const double* flux, int V, const int2* items, long long n, double* out,
+                             cudaStream_t st);
 
 // regrid.cu: octree.cpp:149-323 data operations
 cudaError_t launch_prolong(const double* parent, double* children8, int V, cudaStream_t st);

@@ -32,7 +32,9 @@ class HydroDriver:
         (bitwise on every ghost the stage reads, hence on the state).
         reflux: flux-register correction at refinement jumps after every stage
         (flux_register.hpp:21-63 declared only; our restatement,
-        oracle tmo_reflux_apply) — conserves mass across level jumps; single GPU."""
+        oracle tmo_reflux_apply) — conserves mass across level jumps; on a
+        distributed forest the fine face blocks of coarse leaves on other GPUs
+        are exchanged after every stage (the same bits as one GPU)."""
         self.forest, self.gamma, self.cfl, self.fast = forest, gamma, cfl, fast
         self.exact_ghosts = exact_ghosts
         self.steps = 0

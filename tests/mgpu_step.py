@@ -56,7 +56,8 @@ def main():
     gravity = "--gravity" in sys.argv
     peer = "--peer" in sys.argv
     regrid = "--regrid" in sys.argv
-    args = [a for a in sys.argv[1:] if a not in ("--gravity", "--peer", "--regrid")]
+    reflux = "--reflux" in sys.argv
+    args = [a for a in sys.argv[1:] if a not in ("--gravity", "--peer", "--regrid", "--reflux")]
     Drv = GravityHydroDriver if gravity else HydroDriver
     kind, lo, hi = amr.Scenario.rotating_star, 2, 4
     f = amr.build_scenario(kind, lo, hi)
@@ -69,7 +70,7 @@ def main():
         f.set_peer(True)
     a, b = dist.local_range(owner, rank)
     f.set_interior(np.ascontiguousarray(state[a:b]))
-    drv = Drv(f)
+    drv = Drv(f, reflux=reflux)
     dts = [drv.step() for _ in range(3)]
     if regrid:  # collective regrid + re-partition, then more steps
         rl, cl = regrid_lists(f)
@@ -94,7 +95,7 @@ def main():
         g = amr.build_scenario(kind, lo, hi)
         g.alloc()
         g.set_interior(state)
-        d1 = Drv(g)
+        d1 = Drv(g, reflux=reflux)
         dts1 = [d1.step() for _ in range(3)]
         if regrid:
             d1.regrid(rl, cl)

@@ -135,12 +135,14 @@ def test_peer_halo_step_bitwise_equals_single_gpu(gravity):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("extra", [["--regrid"], ["--regrid", "--gravity", "--peer"]])
-def test_distributed_regrid_bitwise_equals_single_gpu(extra):
+@pytest.mark.parametrize("extra", [["--regrid"], ["--regrid", "--gravity", "--peer"], ["--reflux"],
+                                   ["--reflux", "--gravity", "--peer", "--regrid"]])
+def test_distributed_regrid_reflux_bitwise_equals_single_gpu(extra):
     """Collective regrid of a distributed forest (dist.regrid: refine with 2:1
     cascades and coarsen with the data carried along, re-partition, blocks moved
-    to their new owners; peer exchanges rebuilt) and two more steps == the same
-    on one GPU, bitwise (state, gravity field, checkpoint bytes)."""
+    to their new owners; peer exchanges rebuilt) and two more steps, and/or
+    reflux with the fine face blocks exchanged across GPUs after every stage ==
+    the same on one GPU, bitwise (state, gravity field, checkpoint bytes)."""
     import torch
 
     if torch.cuda.device_count() < 2:
@@ -149,7 +151,8 @@ def test_distributed_regrid_bitwise_equals_single_gpu(extra):
     n = min(torch.cuda.device_count(), 4)
     r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
                         f"--nproc-per-node={n}", "--master-addr", "127.0.0.1", "--master-port",
-                        str(29541 + len(extra)), script] + extra, capture_output=True, text=True,
+                        str(29541 + len(extra) + 7 * ("--reflux" in extra)), script] + extra,
+                       capture_output=True, text=True,
                        timeout=900)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     assert "BITWISE_OK" in r.stdout, r.stdout[-3000:]
