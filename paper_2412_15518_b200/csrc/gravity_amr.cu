@@ -90,20 +90,20 @@ __global__ void amr_mass_kernel(const double* __restrict__ arena, int V, long lo
   }
 }
 
-// leaf cells: moments (m, 0, ..., 0); thread = (cell, 16-byte pair), so a
-// warp writes 512 contiguous bytes of the AoS moments; slots lo .. lo+nslots
+// leaf cells: moments (m, 0, ..., 0). The moment arrays are zeroed when the
+// solver is created and nothing writes a leaf patch's D and Q afterwards (M2M
+// writes internal patches; received patches arrive with their owner's +0s),
+// so P2M stores only m; slots lo .. lo+nslots
 __global__ void amr_p2m_kernel(const double* __restrict__ mass, long long nslots, long long lo,
                                const int* __restrict__ slot_level, const int* __restrict__ slot_node,
                                const GLv* __restrict__ L) {
-  const long long total = nslots * 512 * 5;
+  const long long total = nslots * 512;
   for (long long u = blockIdx.x * (long long)blockDim.x + threadIdx.x; u < total;
        u += (long long)gridDim.x * blockDim.x) {
-    const long long t = lo * 512 + u / 5;
-    const int pr = (int)(u % 5);
+    const long long t = lo * 512 + u;
     const long long s = t >> 9;
     const int c = (int)(t & 511);
-    double2* o = reinterpret_cast<double2*>(L[slot_level[s]].mom + ((long long)slot_node[s] * 512 + c) * 10);
-    o[pr] = make_double2(pr == 0 ? mass[t] : 0.0, 0.0);
+    L[slot_level[s]].mom[((long long)slot_node[s] * 512 + c) * 10] = mass[t];
   }
 }
 
@@ -1658,6 +1658,7 @@ tmgpu_gravity_amr* tmgpu_gravity_amr_create(const int* leaves, long long nleaves
     w.nodes += L.n;
     e = cudaMalloc(&g.mom, ncell * 10 * sizeof(double));
     track(g.mom);
+    if (e == cudaSuccess) e = cudaMemset(g.mom, 0, ncell * 10 * sizeof(double));  // leaf D, Q stay +0
     if (e == cudaSuccess) e = cudaMalloc(&g.loc, ncell * 10 * sizeof(double)), track(g.loc);
     int *ijk, *nbr, *child, *parent, *slot, *inter;
     long long *moff, *ment, *poff, *pent;
@@ -1902,8 +1903,8 @@ int tmgpu_gravity_amr_solve(tmgpu_gravity_amr* G, const double* mass, double* ph
   if (e == cudaSuccess && rc == TMGPU_OK) {
     long long launches = 0;
     if (nloc)
-      amr_p2m_kernel<<<grid_for(nout * 5), 128, 0, st>>>(w.mass, nloc, w.lo, w.slot_level, w.slot_node,
-                                                         w.dev_lv);
+      amr_p2m_kernel<<<grid_for(nout), 128, 0, st>>>(w.mass, nloc, w.lo, w.slot_level, w.slot_node,
+                                                     w.dev_lv);
     ++launches;
     for (int l = P.nlevels - 2; l >= 0; --l) {  // own subtrees (all of the tree on one GPU)
       const long long ni = w.let ? w.n_owned[l] : (long long)P.lv[l].internal.size();
