@@ -21,15 +21,9 @@
  *   P2M   leaf cells: (m, 0, 0)
  *   M2M   internal cells from their 8 children, (c, b, a) loop order
  *   V     every existing cell at depth >= 2: the 189-cell stencil of the
- *         uniform spec, skipping missing/outside cells, as four partial sums —
- *         by source kind (leaf cells, whose moments are (m, 0, 0); internal
- *         cells) and by lower / upper three source planes — each in the
- *         stencil order (dz, dy ascending, per row even source x then odd):
- *         V = (leaf_lo + leaf_hi) + (internal_lo + internal_hi). A target whose
- *         sources are all of one kind gets the plain two-half sum (x + 0 = x),
- *         so on a uniform forest this is the uniform specification's V; the
- *         kind split lets the GPU evaluate the monopole (leaf) and multipole
- *         (internal) sources in different kernels
+ *         uniform spec (two partial sums over the lower / upper three source
+ *         planes, dz, dy ascending, per row even source x then odd, then
+ *         added), skipping missing/outside cells
  *   W, X  for every leaf cell b (canonical leaf order, cells (k,j,i)), every
  *         internal colleague Y (same depth, max|offset| = 1, dz,dy,dx
  *         ascending) is visited: each child y (z,y,x order) adjacent to b
@@ -354,8 +348,7 @@ int tmo_grav_amr_solve_ex(long nleaves, const int* leaves, const double* mass, i
         for (long i = 0; i < m; ++i) {
           if (!dep[d].type[cix(m, i, j, k)]) continue;
           double* out = dep[d].loc + cix(m, i, j, k) * 10;
-          /* [source kind: 0 leaf cell, 1 internal cell][lower / upper three source planes] */
-          double part[2][2][10] = {{{0}}};
+          double part[2][10] = {{0}};  /* lower / upper three source planes */
           for (long dz = -2 - (k & 1); dz <= 3 - (k & 1); ++dz)
             for (long dy = -2 - (j & 1); dy <= 3 - (j & 1); ++dy)
               for (int pe = 0; pe < 2; ++pe)  /* even source x, then odd */
@@ -363,13 +356,11 @@ int tmo_grav_amr_solve_ex(long nleaves, const int* leaves, const double* mass, i
                 if (labs(dx) <= 1 && labs(dy) <= 1 && labs(dz) <= 1) continue;
                 const long si = i + dx, sj = j + dy, sk = k + dz;
                 if (si < 0 || sj < 0 || sk < 0 || si >= m || sj >= m || sk >= m) continue;
-                const uint8_t st = dep[d].type[cix(m, si, sj, sk)];
-                if (!st) continue;
+                if (!dep[d].type[cix(m, si, sj, sk)]) continue;
                 const double R[3] = {-(double)dx * h, -(double)dy * h, -(double)dz * h};
-                m2l_k(dep[d].mom + cix(m, si, sj, sk) * 10, R, part[st == 1][dz + (k & 1) >= 1], cnt);
+                m2l_k(dep[d].mom + cix(m, si, sj, sk) * 10, R, part[dz + (k & 1) >= 1], cnt);
               }
-          for (int q = 0; q < 10; ++q)
-            out[q] = (part[0][0][q] + part[0][1][q]) + (part[1][0][q] + part[1][1][q]);
+          for (int q = 0; q < 10; ++q) out[q] = part[0][q] + part[1][q];
         }
   }
   /* W / X / U-cross lists */

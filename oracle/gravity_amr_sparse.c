@@ -247,13 +247,12 @@ static inline void m2l_any(const double* mom, const double* e, double* out, int 
 }
 
 /* V list of one target cell (global coords at depth d): the specification's
- * four partial sums (source kind x lower / upper source planes) over the
- * 189-cell stencil; sources resolve through the target node's 27 neighbours
- * (depth >= 3; lvleaf marks leaf nodes) or the dense depth-2 array (internal) */
+ * two partial sums over the 189-cell stencil; sources resolve through the
+ * target node's 27 neighbours (depth >= 3) or the dense depth-2 array */
 static void vlist_cell(const SForest* F, int d, const double* tab, long gi, long gj, long gk, const int* nb27,
-                       const double* lvmom, const int* lvleaf, double* out, int full, int cnt) {
+                       const double* lvmom, double* out, int full, int cnt) {
   const long m = 1L << d;
-  double part[2][2][10];
+  double part[2][10];
   memset(part, 0, sizeof(part));
   const long I0 = (gi >> 3) - 1, J0 = (gj >> 3) - 1, K0 = (gk >> 3) - 1;
   for (long dz = -2 - (gk & 1); dz <= 3 - (gk & 1); ++dz)
@@ -264,7 +263,6 @@ static void vlist_cell(const SForest* F, int d, const double* tab, long gi, long
           const long si = gi + dx, sj = gj + dy, sk = gk + dz;
           if (si < 0 || sj < 0 || sk < 0 || si >= m || sj >= m || sk >= m) continue;
           const double* src;
-          int kind = 1; /* internal */
           if (d < 3) {
             src = F->dmom[d] + cix(m, si, sj, sk) * 10;
           } else {
@@ -272,13 +270,11 @@ static void vlist_cell(const SForest* F, int d, const double* tab, long gi, long
             const int q = nb27[o];
             if (q < 0) continue; /* missing cell */
             src = lvmom + ((long)q * 512 + lcell(si, sj, sk)) * 10;
-            kind = lvleaf[q] >= 0 ? 0 : 1;
           }
-          m2l_any(src, tab + (((dz + 3) * 7 + (dy + 3)) * 7 + (dx + 3)) * 13, part[kind][dz + (gk & 1) >= 1],
-                  full, cnt);
+          m2l_any(src, tab + (((dz + 3) * 7 + (dy + 3)) * 7 + (dx + 3)) * 13, part[dz + (gk & 1) >= 1], full, cnt);
         }
   const int nq = full ? 10 : 4;
-  for (int q = 0; q < nq; ++q) out[q] = (part[0][0][q] + part[0][1][q]) + (part[1][0][q] + part[1][1][q]);
+  for (int q = 0; q < nq; ++q) out[q] = part[0][q] + part[1][q];
 }
 
 
@@ -340,18 +336,14 @@ static inline void vst(double* p, V4 a) {
 
 #define WIN_Q 1728 /* doubles per component: [wz 12][wy 12][parity 2][half-x 6] */
 
-/* one source kind's partial sums (want_leaf: the leaf-node neighbours, else
- * the internal ones; the other kind's cells are zero moments, exact no-ops):
- * loc[cell][q] = lower half + upper half */
-static void vlist_node_kind(const int* nb27, const double* lvmom, const int* lvleaf, int want_leaf,
-                            const double* tab, double* loc, int full, double* win) {
+static void vlist_node(const int* nb27, const double* lvmom, const double* tab, double* loc, int full,
+                       double* win) {
   for (int wz = 0; wz < 12; ++wz)
     for (int wy = 0; wy < 12; ++wy)
       for (int wx = 0; wx < 12; ++wx) {
         const int oz = wz < 2 ? -1 : (wz > 9 ? 1 : 0), oy = wy < 2 ? -1 : (wy > 9 ? 1 : 0),
                   ox = wx < 2 ? -1 : (wx > 9 ? 1 : 0);
-        int q = nb27[((oz + 1) * 3 + (oy + 1)) * 3 + ox + 1];
-        if (q >= 0 && (lvleaf[q] >= 0) != (want_leaf != 0)) q = -1;
+        const int q = nb27[((oz + 1) * 3 + (oy + 1)) * 3 + ox + 1];
         const int at = (wz * 12 + wy) * 12 + (wx & 1) * 6 + (wx >> 1);
         if (q < 0) {
           for (int c = 0; c < 10; ++c) win[c * WIN_Q + at] = 0.0;
@@ -403,25 +395,6 @@ static void vlist_node_kind(const int* nb27, const double* lvmom, const int* lvl
           for (int x = 0; x < 4; ++x) loc[((k * 8 + j) * 8 + a + 2 * x) * 10 + c] = v[x];
         }
       }
-}
-
-/* V lists of one node patch: leaf-source and internal-source partial sums,
- * V = (leaf_lo + leaf_hi) + (internal_lo + internal_hi); a kind without
- * neighbours contributes +0 (x + 0 = x: skipped) */
-static void vlist_node(const int* nb27, const double* lvmom, const int* lvleaf, const double* tab, double* loc,
-                       int full, double* win, double* tmp) {
-  int has[2] = {0, 0};
-  for (int o = 0; o < 27; ++o)
-    if (nb27[o] >= 0) has[lvleaf[nb27[o]] >= 0 ? 0 : 1] = 1;
-  if (has[0] && has[1]) {
-    const int nq = full ? 10 : 4;
-    vlist_node_kind(nb27, lvmom, lvleaf, 1, tab, loc, full, win);
-    vlist_node_kind(nb27, lvmom, lvleaf, 0, tab, tmp, full, win);
-    for (int c = 0; c < 512; ++c)
-      for (int q = 0; q < nq; ++q) loc[c * 10 + q] = loc[c * 10 + q] + tmp[c * 10 + q];
-  } else {
-    vlist_node_kind(nb27, lvmom, lvleaf, has[0], tab, loc, full, win);
-  }
 }
 
 typedef struct {
@@ -750,13 +723,12 @@ int tmo_grav_plan_solve(tmo_grav_plan* P, const double* mass, int flags, double*
   PHASE("p2m+m2m");
   /* V lists: dense depth 2, then every patch */
   for (long t = 0; t < 64; ++t)
-    vlist_cell(&F, 2, tab + 2 * 343 * 13, t & 3, (t >> 2) & 3, t >> 4, NULL, NULL, NULL, F.dloc[2] + t * 10, 1, cnt);
+    vlist_cell(&F, 2, tab + 2 * 343 * 13, t & 3, (t >> 2) & 3, t >> 4, NULL, NULL, F.dloc[2] + t * 10, 1, cnt);
   {
     const long nodes = F.base[nl];
 #pragma omp parallel
     {
       double* win = cnt ? NULL : (double*)malloc(10 * WIN_Q * sizeof(double));
-      double* tmp = cnt ? NULL : (double*)malloc(5120 * sizeof(double));
 #pragma omp for schedule(dynamic, 1)
       for (long f = 0; f < nodes; ++f) {
         int l = 0;
@@ -767,16 +739,15 @@ int tmo_grav_plan_solve(tmo_grav_plan* P, const double* mass, int flags, double*
         const double* tb = tab + (size_t)d * 343 * 13;
         const int full = L->leaf[q] < 0 || l == 0; /* a leaf root keeps all ten */
         if (win) {
-          vlist_node(L->nb + q * 27, L->mom, L->leaf, tb, L->loc + (long)q * 5120, full, win, tmp);
+          vlist_node(L->nb + q * 27, L->mom, tb, L->loc + (long)q * 5120, full, win);
           continue;
         }
         const long I = L->I[q], J = L->J[q], K = L->K[q];
         for (int c = 0; c < 512; ++c)
           vlist_cell(&F, d, tb, 8 * I + (c & 7), 8 * J + ((c >> 3) & 7), 8 * K + (c >> 6), L->nb + q * 27,
-                     L->mom, L->leaf, L->loc + ((long)q * 512 + c) * 10, full, cnt);
+                     L->mom, L->loc + ((long)q * 512 + c) * 10, full, cnt);
       }
       free(win);
-      free(tmp);
     }
   }
   PHASE("v-list");

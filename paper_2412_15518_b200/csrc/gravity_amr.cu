@@ -271,9 +271,8 @@ __device__ __forceinline__ void m2l_term_mono(const double nM, const double (&e)
 }
 
 // full[0..2]: does any lane of the warp take a source of this row from an
-// internal patch at x-offset -1, 0, +1 (warp votes): this kernel sums the
-// internal sources only (the window holds zero moments for leaf and missing
-// cells: exact no-ops), so a group with none in any lane is skipped
+// internal patch at x-offset -1, 0, +1 (warp votes; a warp whose sources in a
+// group are all leaf cells runs the monopole term for the group)
 template <bool NEAR, int NOUT>
 __device__ __forceinline__ void m2l_row_par(const double* __restrict__ src,
                                             const double* __restrict__ trow, double (&acc)[4][10],
@@ -298,7 +297,7 @@ __device__ __forceinline__ void m2l_row_par(const double* __restrict__ src,
     for (int mi = 0; mi < 6; ++mi) {
       const int sx = pe + 2 * mi;
       const int grp = sx < 2 ? 0 : (sx > 9 ? 2 : 1);
-      if (full[grp]) {  // some lane's source here is an internal cell (the others: zero moments)
+      if (full[grp]) {
         double m[10];
 #pragma unroll
         for (int q = 0; q < 10; ++q) m[q] = src[q * kWVar + sx];
@@ -308,6 +307,15 @@ __device__ __forceinline__ void m2l_row_par(const double* __restrict__ src,
           if (k < 0 || k > 3) continue;
           if (NEAR && t == 1) continue;
           m2l_term<NOUT>(m, G[t], acc[k]);
+        }
+      } else {
+        const double nM = -src[sx];
+#pragma unroll
+        for (int t = 0; t < 3; ++t) {
+          const int k = mi - t;
+          if (k < 0 || k > 3) continue;
+          if (NEAR && t == 1) continue;
+          m2l_term_mono<NOUT>(nM, G[t], acc[k]);
         }
       }
     }
@@ -332,7 +340,7 @@ __device__ __forceinline__ void cp_async8(double* smem, const double* gmem, bool
 template <int NOUT>
 __device__ __forceinline__ void m2l_patch(double* __restrict__ win, const double* __restrict__ tabs,
                                           double* __restrict__ loc, int n, double* __restrict__ lloc,
-                                          unsigned internal27, bool has_leaf) {
+                                          unsigned internal27) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int b = warp & 1, c = (warp >> 1) & 1, half = warp >> 2;
   const int a = lane & 1, Y = (lane >> 1) & 3, Z = lane >> 3;
@@ -378,9 +386,6 @@ __device__ __forceinline__ void m2l_patch(double* __restrict__ win, const double
   __syncthreads();
   if (half) return;
   const int y = 2 * Y + b, z = 2 * Z + c;
-  // V = (leaf_lo + leaf_hi) + (internal_lo + internal_hi): the leaf-source sum
-  // is amr_m2l_mono_kernel's output where the patch has leaf neighbours,
-  // otherwise it is +0 and V is the internal sum (x + 0 = x)
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
     const int cell = (z * 8 + y) * 8 + a + 2 * k;
@@ -390,17 +395,10 @@ __device__ __forceinline__ void m2l_patch(double* __restrict__ win, const double
     if constexpr (NOUT == 10) {
       double2* out = reinterpret_cast<double2*>(loc + ((long long)n * 512 + cell) * 10);
 #pragma unroll
-      for (int h = 0; h < 5; ++h) {
-        if (has_leaf) {
-          const double2 s0 = out[h];
-          out[h] = make_double2(s0.x + v[2 * h], s0.y + v[2 * h + 1]);
-        } else {
-          out[h] = make_double2(v[2 * h], v[2 * h + 1]);
-        }
-      }
+      for (int h = 0; h < 5; ++h) out[h] = make_double2(v[2 * h], v[2 * h + 1]);
     } else {
 #pragma unroll
-      for (int q = 0; q < 4; ++q) lloc[q * 512 + cell] = lloc[q * 512 + cell] + v[q];
+      for (int q = 0; q < 4; ++q) lloc[q * 512 + cell] = v[q];
     }
   }
 }
@@ -441,18 +439,15 @@ __global__ void __launch_bounds__(kM2lThreads, 1) amr_m2l_fused_kernel(
     for (int wx = 0; wx < 12; ++wx) {
       const int ox = wx < 2 ? -1 : (wx > 9 ? 1 : 0), lx = wx - 2 - 8 * ox;
       const int nb = nbs[ox + 1];
-      const bool internal_src = nb >= 0 && L.leaf_slot[nb] < 0;  // leaf sources: amr_m2l_mono_kernel
-      const double* src = L.mom + ((long long)(internal_src ? nb : n) * 512 + rowoff + lx) * 10 + h;
-      cp_async8(dst + wx, src, internal_src);
+      const double* src = L.mom + ((long long)(nb < 0 ? n : nb) * 512 + rowoff + lx) * 10 + h;
+      cp_async8(dst + wx, src, nb >= 0);
     }
   }
   // neighbour patches that are internal (full moments): bit o of internal27
   unsigned internal27 = 0;
-  bool has_leaf = false;
   for (int o = 0; o < 27; ++o) {
     const int nb = nb27[o];
     if (nb >= 0 && L.leaf_slot[nb] < 0) internal27 |= 1u << o;
-    if (nb >= 0 && L.leaf_slot[nb] >= 0) has_leaf = true;
   }
   asm volatile("cp.async.wait_all;\n" ::: "memory");
   __syncthreads();
@@ -460,50 +455,39 @@ __global__ void __launch_bounds__(kM2lThreads, 1) amr_m2l_fused_kernel(
   // leaf patch below the root: L0, L_i into the compact leaf locals (L2P's
   // input); a leaf root keeps all ten (the dense levels' L2L adds into them)
   if (leaf >= 0 && l > 0)
-    m2l_patch<4>(win, tabs, L.loc, n, lloc + (long long)(leaf - lo) * 2048, internal27, has_leaf);
+    m2l_patch<4>(win, tabs, L.loc, n, lloc + (long long)(leaf - lo) * 2048, internal27);
   else
-    m2l_patch<10>(win, tabs, L.loc, n, nullptr, internal27, has_leaf);
+    m2l_patch<10>(win, tabs, L.loc, n, nullptr, internal27);
 }
 
-// ---- M2L from leaf-cell sources (monopole sources) -------------------------
-// The specification splits every target's V sum by source kind:
-// V = (leaf_lo + leaf_hi) + (internal_lo + internal_hi). A leaf cell's moments
-// are (m, +0, ..., +0), so every D/Q term of a leaf source's M2L term is an
-// exact no-op (fma(+-0, e, x) = x for x != 0, and an accumulator that starts
-// at +0 never becomes -0; the same argument as amr_m2m_kernel's leaf
-// children), leaving per interaction only
-//   t = -m * e0;  L0 = L0 + t;  L_i = fma(-m, e_i, L_i);  L_ij = fma(-m, e_ij, L_ij)
-// — 5 of the 23 operations into a leaf target, 11 of 29 into an internal one,
-// bit for bit the full term's result. This kernel evaluates the leaf-source
-// sums of every patch that has leaf neighbours (leaf patches: all of them, a
-// leaf's own cells being sources; on C3 531M of the 618M V pairs); the window is
-// the 12^3 source masses (internal and missing neighbours zero: no-ops), 16 KB,
-// so several CTAs share an SM. amr_m2l_fused_kernel then adds the internal-
-// source sums of the patches with internal neighbours. Thread mapping, source
-// order and the two plane halves are m2l_patch's. NOUT = 4: leaf patches below
-// the root (L0, L_i into the compact leaf locals); 10: internal patches and a
-// leaf root (all locals into loc).
-template <int NOUT>
-struct MonoCfg {
-  static constexpr int kWin = NOUT == 4 ? 2048 : 4 * 10 * 128;  // window / partial-sum exchange
-  static constexpr size_t kSmem = (size_t)(kWin + kOff3 * NOUT) * sizeof(double);
-};
+// ---- M2L of leaf patches among leaf patches (monopole sources) -------------
+// A leaf patch whose existing 27 neighbours are all leaf patches (5,000 of the
+// 6,729 patches on C3) has only leaf cells as V sources, and a leaf cell's
+// moments are (m, +0, ..., +0). Every D/Q term of the specification's M2L term
+// is then an exact no-op (fma(+-0, e, x) = x for x != 0, and an accumulator that
+// starts at +0 never becomes -0; the same argument as amr_m2m_kernel's leaf
+// children), so per interaction only
+//   t = -m * e0;  L0 = L0 + t;  L_i = fma(-m, e_i, L_i)        (i = 1..3)
+// remain — 5 of the 23 operations into a leaf target, bit for bit the full
+// term's result. The source window is then the 12^3 masses (from the compact
+// [slot][512] mass array, not the 80-byte moments), 16 KB instead of 161 KB,
+// so several CTAs share an SM. Thread mapping, source order and the two
+// partial sums are m2l_patch's.
+constexpr int kMonoWin = 2048;  // >= 4 * kWSub + 2 (window) and the 4 x 4 x 128 partial sums
+constexpr size_t kMonoSmem = (size_t)(kMonoWin + kOff3 * 4) * sizeof(double);  // 27,360 B
 
-template <int NOUT, bool NEAR>
+template <bool NEAR>
 __device__ __forceinline__ void mono_row(const double* __restrict__ src, const double* __restrict__ trow,
-                                         double (&acc)[4][NOUT]) {
+                                         double (&acc)[4][4]) {
 #pragma unroll
   for (int pe = 0; pe < 2; ++pe) {
-    double G[3][NOUT];
+    double G[3][4];
 #pragma unroll
     for (int t = 0; t < 3; ++t) {
       if (NEAR && t == 1) continue;
-      const double2* t2 = reinterpret_cast<const double2*>(trow + (pe + 2 * t) * NOUT);
-#pragma unroll
-      for (int q = 0; q < NOUT / 2; ++q) {
-        const double2 u = t2[q];
-        G[t][2 * q] = u.x, G[t][2 * q + 1] = u.y;
-      }
+      const double2* t2 = reinterpret_cast<const double2*>(trow + (pe + 2 * t) * 4);
+      const double2 u = t2[0], v = t2[1];
+      G[t][0] = u.x, G[t][1] = u.y, G[t][2] = v.x, G[t][3] = v.y;
     }
 #pragma unroll
     for (int mi = 0; mi < 6; ++mi) {
@@ -514,64 +498,62 @@ __device__ __forceinline__ void mono_row(const double* __restrict__ src, const d
         if (k < 0 || k > 3) continue;
         if (NEAR && t == 1) continue;
         acc[k][0] = acc[k][0] + nM * G[t][0];
-#pragma unroll
-        for (int q = 1; q < NOUT; ++q) acc[k][q] = fma(nM, G[t][q], acc[k][q]);
+        acc[k][1] = fma(nM, G[t][1], acc[k][1]);
+        acc[k][2] = fma(nM, G[t][2], acc[k][2]);
+        acc[k][3] = fma(nM, G[t][3], acc[k][3]);
       }
     }
   }
 }
 
-template <int NOUT>
-__global__ void __launch_bounds__(kM2lThreads, NOUT == 4 ? 4 : 1) amr_m2l_mono_kernel(
-    const GLv* __restrict__ Lv, const int2* __restrict__ work, const double* __restrict__ tab_all,
-    double* __restrict__ lloc, long long lo) {
-  using Cfg = MonoCfg<NOUT>;
+__global__ void __launch_bounds__(kM2lThreads, 4) amr_m2l_mono_kernel(
+    const long long* __restrict__ slots, const int* __restrict__ slot_level, const double* __restrict__ mass,
+    const int* __restrict__ slot_nbs, const double* __restrict__ tab_all, double* __restrict__ lloc,
+    long long lo) {
   extern __shared__ double sm[];
   double* win = sm;
-  double* tabs = sm + Cfg::kWin;
-  const int2 wk = work[blockIdx.x];
-  const int l = wk.x, n = wk.y;
-  const GLv L = Lv[l];
+  double* tabs = sm + kMonoWin;
+  const long long s = slots[blockIdx.x];
+  const int l = slot_level[s];
   const double* tab = tab_all + (long long)(l + 3) * kOff3 * kTab;
-  for (int q = threadIdx.x; q < kOff3 * NOUT; q += kM2lThreads) {
-    const int o = q / NOUT;
+  for (int q = threadIdx.x; q < kOff3 * 4; q += kM2lThreads) {
+    const int o = q >> 2;
     const int dx = o % kOff - 3, dy = (o / kOff) % kOff - 3, dz = o / (kOff * kOff) - 3;
     const bool near = dx >= -1 && dx <= 1 && dy >= -1 && dy <= 1 && dz >= -1 && dz <= 1;
-    cp_async8(tabs + q, tab + (long long)o * kTab + (q - o * NOUT), !near);
+    cp_async8(tabs + q, tab + (long long)o * kTab + (q & 3), !near);
   }
-  const int* nb27 = L.nbr + (long long)n * 27;
+  const int* nb27 = slot_nbs + s * 27;
   for (int t = threadIdx.x; t < 1728; t += kM2lThreads) {
     const int wx = t % 12, wy = (t / 12) % 12, wz = t / 144;
     const int ox = wx < 2 ? -1 : (wx > 9 ? 1 : 0), oy = wy < 2 ? -1 : (wy > 9 ? 1 : 0),
               oz = wz < 2 ? -1 : (wz > 9 ? 1 : 0);
     const int nb = nb27[((oz + 1) * 3 + (oy + 1)) * 3 + ox + 1];
-    const bool leaf_src = nb >= 0 && L.leaf_slot[nb] >= 0;
     const int lx = wx - 2 - 8 * ox, ly = wy - 2 - 8 * oy, lz = wz - 2 - 8 * oz;
     double* dst = win + ((wz & 1) * 2 + (wy & 1)) * kWSub + (wz >> 1) * kWPZ + (wy >> 1) * kWPY + wx;
-    cp_async8(dst, L.mom + ((long long)(leaf_src ? nb : n) * 512 + (lz * 8 + ly) * 8 + lx) * 10, leaf_src);
+    cp_async8(dst, mass + ((long long)(nb < 0 ? s : nb) * 512 + (lz * 8 + ly) * 8 + lx), nb >= 0);
   }
   asm volatile("cp.async.wait_all;\n" ::: "memory");
   __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int b = warp & 1, c = (warp >> 1) & 1, half = warp >> 2;
   const int a = lane & 1, Y = (lane >> 1) & 3, Z = lane >> 3;
-  double acc[4][NOUT];
+  double acc[4][4];
 #pragma unroll
   for (int k = 0; k < 4; ++k)
 #pragma unroll
-    for (int q = 0; q < NOUT; ++q) acc[k][q] = 0.0;
-  const double* tab_lane = tabs + (1 - a) * NOUT;
+    for (int q = 0; q < 4; ++q) acc[k][q] = 0.0;
+  const double* tab_lane = tabs + (1 - a) * 4;
   for (int iz = 3 * half; iz < 3 * half + 3; ++iz) {
     const int dz = iz - 2 - c;
 #pragma unroll 2
     for (int iy = 0; iy < 6; ++iy) {
       const int dy = iy - 2 - b;
-      const double* trow = tab_lane + ((dz + 3) * kOff + (dy + 3)) * kOff * NOUT;
+      const double* trow = tab_lane + ((dz + 3) * kOff + (dy + 3)) * kOff * 4;
       const double* src = win + ((iz & 1) * 2 + (iy & 1)) * kWSub + (Z + (iz >> 1)) * kWPZ + (Y + (iy >> 1)) * kWPY;
       if (dz >= -1 && dz <= 1 && dy >= -1 && dy <= 1)
-        mono_row<NOUT, true>(src, trow, acc);
+        mono_row<true>(src, trow, acc);
       else
-        mono_row<NOUT, false>(src, trow, acc);
+        mono_row<false>(src, trow, acc);
     }
   }
   __syncthreads();  // the window is dead: the upper half hands over its partial sums
@@ -580,25 +562,17 @@ __global__ void __launch_bounds__(kM2lThreads, NOUT == 4 ? 4 : 1) amr_m2l_mono_k
 #pragma unroll
     for (int k = 0; k < 4; ++k)
 #pragma unroll
-      for (int q = 0; q < NOUT; ++q) win[(k * NOUT + q) * 128 + pair] = acc[k][q];
+      for (int q = 0; q < 4; ++q) win[(k * 4 + q) * 128 + pair] = acc[k][q];
   }
   __syncthreads();
   if (half) return;
   const int y = 2 * Y + b, z = 2 * Z + c;
+  double* out = lloc + (s - lo) * 2048;
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
     const int cell = (z * 8 + y) * 8 + a + 2 * k;
-    if constexpr (NOUT == 4) {
-      double* out = lloc + ((long long)L.leaf_slot[n] - lo) * 2048;
 #pragma unroll
-      for (int q = 0; q < 4; ++q) out[q * 512 + cell] = acc[k][q] + win[(k * 4 + q) * 128 + pair];
-    } else {
-      double2* out = reinterpret_cast<double2*>(L.loc + ((long long)n * 512 + cell) * 10);
-#pragma unroll
-      for (int h = 0; h < 5; ++h)
-        out[h] = make_double2(acc[k][2 * h] + win[(k * 10 + 2 * h) * 128 + pair],
-                              acc[k][2 * h + 1] + win[(k * 10 + 2 * h + 1) * 128 + pair]);
-    }
+    for (int q = 0; q < 4; ++q) out[q * 512 + cell] = acc[k][q] + win[(k * 4 + q) * 128 + pair];
   }
 }
 
@@ -1313,9 +1287,8 @@ struct GravAmrWork {
   std::vector<long long> nl2l;
   int2* m2l_work = nullptr;  // fused M2L launch: (level, node) per CTA
   long long m2l_ctas = 0;
-  int2* mono_work = nullptr;    // amr_m2l_mono_kernel<4>: (level, node) of leaf patches below the root
-  int2* mono10_work = nullptr;  // amr_m2l_mono_kernel<10>: internal patches with leaf neighbours, a leaf root
-  long long mono_ctas = 0, mono10_ctas = 0;
+  long long* mono_slots = nullptr;  // amr_m2l_mono_kernel: leaf patches among leaf patches (slot)
+  long long mono_ctas = 0;
   long long u_max = 0;  // most cross-depth U entries of a level
   int* wx_tlev = nullptr;         // W/X kernel targets (level, flat), by entry count
   long long* wx_tflat = nullptr;
@@ -1541,7 +1514,8 @@ static cudaError_t build_l2l_lists(GravAmrWork& w, const std::vector<std::vector
 
 // (level, node) list of the fused M2L launch: every needed node of every level
 static cudaError_t build_m2l_work(GravAmrWork& w, const std::vector<std::vector<int>>* need) {
-  std::vector<int2> wk, wk_all, mono, mono10;
+  std::vector<int2> wk, wk_all;
+  std::vector<long long> mono;
   for (int l = 0; l < w.plan.nlevels; ++l) {
     if (need) {
       for (int n : (*need)[l]) wk_all.push_back(make_int2(l, n));
@@ -1549,20 +1523,20 @@ static cudaError_t build_m2l_work(GravAmrWork& w, const std::vector<std::vector<
       for (int n = 0; n < w.plan.lv[l].n; ++n) wk_all.push_back(make_int2(l, n));
     }
   }
-  // the leaf-source sums of every patch with leaf neighbours (its own cells
-  // included) -> amr_m2l_mono_kernel (NOUT 4: leaf patches below the root;
-  // 10: internal patches and a leaf root); the internal-source sums of every
-  // patch with internal neighbours -> amr_m2l_fused_kernel, after them
+  // leaf patches (below the root) whose existing neighbours are all leaf
+  // patches go to the monopole-source kernel; the rest to the fused kernel
+  const bool mono_on = std::getenv("TMGPU_M2L_MONO") == nullptr || std::getenv("TMGPU_M2L_MONO")[0] != '0';
   for (const int2& x : wk_all) {
     const GravLevel& L = w.plan.lv[x.x];
-    bool any_leaf = false, any_int = false;
-    for (int o = 0; o < 27; ++o) {
+    bool all_leaf = mono_on && x.x > 0 && L.leaf_slot[x.y] >= 0;
+    for (int o = 0; o < 27 && all_leaf; ++o) {
       const int nb = L.nbr[(size_t)x.y * 27 + o];
-      if (nb < 0) continue;
-      (L.leaf_slot[nb] >= 0 ? any_leaf : any_int) = true;
+      if (nb >= 0 && L.leaf_slot[nb] < 0) all_leaf = false;
     }
-    if (any_leaf) (L.leaf_slot[x.y] >= 0 && x.x > 0 ? mono : mono10).push_back(x);
-    if (any_int) wk.push_back(x);
+    if (all_leaf)
+      mono.push_back(L.leaf_slot[x.y]);
+    else
+      wk.push_back(x);
   }
   auto drop = [&w](void*& p) {
     if (!p) return;
@@ -1571,10 +1545,8 @@ static cudaError_t build_m2l_work(GravAmrWork& w, const std::vector<std::vector<
     p = nullptr;
   };
   drop(reinterpret_cast<void*&>(w.m2l_work));
-  drop(reinterpret_cast<void*&>(w.mono_work));
-  drop(reinterpret_cast<void*&>(w.mono10_work));
+  drop(reinterpret_cast<void*&>(w.mono_slots));
   w.mono_ctas = (long long)mono.size();
-  w.mono10_ctas = (long long)mono10.size();
   drop(reinterpret_cast<void*&>(w.wx_tlev));
   drop(reinterpret_cast<void*&>(w.wx_tflat));
   w.m2l_ctas = (long long)wk.size();
@@ -1594,10 +1566,8 @@ static cudaError_t build_m2l_work(GravAmrWork& w, const std::vector<std::vector<
   w.wx_targets = (long long)tg.size();
   cudaError_t e = upload(wk, &w.m2l_work);
   if (w.m2l_work) w.allocs.push_back(w.m2l_work);
-  if (e == cudaSuccess) e = upload(mono, &w.mono_work);
-  if (w.mono_work) w.allocs.push_back(w.mono_work);
-  if (e == cudaSuccess) e = upload(mono10, &w.mono10_work);
-  if (w.mono10_work) w.allocs.push_back(w.mono10_work);
+  if (e == cudaSuccess) e = upload(mono, &w.mono_slots);
+  if (w.mono_slots) w.allocs.push_back(w.mono_slots);
   if (e == cudaSuccess) e = upload(tl, &w.wx_tlev);
   if (w.wx_tlev) w.allocs.push_back(w.wx_tlev);
   if (e == cudaSuccess) e = upload(tf, &w.wx_tflat);
@@ -1728,9 +1698,6 @@ tmgpu_gravity_amr* tmgpu_gravity_amr_create(const int* leaves, long long nleaves
   if (e == cudaSuccess)
     e = cudaFuncSetAttribute(amr_m2l_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)kM2lSmem);
-  if (e == cudaSuccess)
-    e = cudaFuncSetAttribute(amr_m2l_mono_kernel<10>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)MonoCfg<10>::kSmem);
   if (e == cudaSuccess) e = build_m2l_work(w, nullptr);
   if (e == cudaSuccess) e = build_l2l_lists(w, nullptr);
   // the one-CTA dense top M2L on a high-priority stream: its CTA takes the first
@@ -1971,14 +1938,9 @@ int tmgpu_gravity_amr_solve(tmgpu_gravity_amr* G, const double* mass, double* ph
     launches += 4;
     if (timed) cudaEventRecord(rec.ev[2], st);
     {
-      if (w.mono_ctas) {  // leaf-source sums: monopole terms, several CTAs per SM
-        amr_m2l_mono_kernel<4><<<(unsigned)w.mono_ctas, kM2lThreads, MonoCfg<4>::kSmem, st>>>(
-            w.dev_lv, w.mono_work, w.tab, w.lloc, w.lo);
-        ++launches;
-      }
-      if (w.mono10_ctas) {
-        amr_m2l_mono_kernel<10><<<(unsigned)w.mono10_ctas, kM2lThreads, MonoCfg<10>::kSmem, st>>>(
-            w.dev_lv, w.mono10_work, w.tab, w.lloc, w.lo);
+      if (w.mono_ctas) {  // leaf patches among leaf patches: monopole sources, several CTAs per SM
+        amr_m2l_mono_kernel<<<(unsigned)w.mono_ctas, kM2lThreads, kMonoSmem, st>>>(
+            w.mono_slots, w.slot_level, w.mass, w.slot_nbs, w.tab, w.lloc, w.lo);
         ++launches;
       }
       if (w.m2l_ctas) {
