@@ -1297,6 +1297,8 @@ struct GravAmrWork {
   double* u_geo = nullptr;   // [distinct cross-depth U separations][4]
   cudaStream_t side = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  cudaStream_t side2 = nullptr;  // the mono M2L, concurrent with the fused one
+  cudaEvent_t ev_fork2 = nullptr, ev_join2 = nullptr;
   // peer-memory LET exchange (tmgpu_gravity_amr_set_peer): subtree roots and
   // halo patches stored straight into the peers' level moment arrays
   bool peer = false;
@@ -1538,6 +1540,10 @@ static cudaError_t build_m2l_work(GravAmrWork& w, const std::vector<std::vector<
     else
       wk.push_back(x);
   }
+  // the heavier internal patches (all ten locals) first: the last waves are
+  // then the lighter leaf patches, and the concurrent mono kernel fills the tail
+  std::stable_partition(wk.begin(), wk.end(),
+                        [&](const int2& x) { return w.plan.lv[x.x].leaf_slot[x.y] < 0 || x.x == 0; });
   auto drop = [&w](void*& p) {
     if (!p) return;
     cudaFree(p);
@@ -1592,6 +1598,9 @@ void tmgpu_gravity_amr_destroy(tmgpu_gravity_amr* G) {
   if (G->w.ev_fork) cudaEventDestroy(G->w.ev_fork);
   if (G->w.ev_join) cudaEventDestroy(G->w.ev_join);
   if (G->w.side) cudaStreamDestroy(G->w.side);
+  if (G->w.side2) cudaStreamDestroy(G->w.side2);
+  if (G->w.ev_join2) cudaEventDestroy(G->w.ev_join2);
+  if (G->w.ev_fork2) cudaEventDestroy(G->w.ev_fork2);
   let_peer_close(G->w);
   for (void* p : G->w.allocs)
     if (p) cudaFree(p);
@@ -1707,6 +1716,9 @@ tmgpu_gravity_amr* tmgpu_gravity_amr_create(const int* leaves, long long nleaves
   if (e == cudaSuccess) e = cudaStreamCreateWithPriority(&w.side, cudaStreamNonBlocking, prio_hi);
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&w.ev_fork, cudaEventDisableTiming);
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&w.ev_join, cudaEventDisableTiming);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&w.side2, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&w.ev_join2, cudaEventDisableTiming);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&w.ev_fork2, cudaEventDisableTiming);
 
   for (int kind = 0; kind < 2 && e == cudaSuccess; ++kind) {
     const std::vector<double>& sep = kind == 0 ? P.wx_sep : P.u_sep;
@@ -1867,6 +1879,18 @@ int tmgpu_gravity_amr_solve(tmgpu_gravity_amr* G, const double* mass, double* ph
     cudaEventRecord(rec.ev[0], st);
   }
   int rc = TMGPU_OK;
+  // the mono M2L needs only the leaf masses (and, distributed, the halo
+  // leaves' masses that come with the moment exchange): on one GPU it starts
+  // now on its own stream and overlaps the whole upward pass
+  const bool mono_early = !w.let && w.mono_ctas > 0;
+  if (e == cudaSuccess && mono_early) {
+    cudaEventRecord(w.ev_fork2, st);
+    cudaStreamWaitEvent(w.side2, w.ev_fork2, 0);
+    amr_m2l_mono_kernel<<<(unsigned)w.mono_ctas, kM2lThreads, kMonoSmem, w.side2>>>(
+        w.mono_slots, w.slot_level, w.mass, w.slot_nbs, w.tab, w.lloc, w.lo);
+    cudaEventRecord(w.ev_join2, w.side2);
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+  }
   if (e == cudaSuccess && rc == TMGPU_OK) {
     long long launches = 0;
     if (nloc)
@@ -1938,16 +1962,22 @@ int tmgpu_gravity_amr_solve(tmgpu_gravity_amr* G, const double* mass, double* ph
     launches += 4;
     if (timed) cudaEventRecord(rec.ev[2], st);
     {
-      if (w.mono_ctas) {  // leaf patches among leaf patches: monopole sources, several CTAs per SM
-        amr_m2l_mono_kernel<<<(unsigned)w.mono_ctas, kM2lThreads, kMonoSmem, st>>>(
-            w.mono_slots, w.slot_level, w.mass, w.slot_nbs, w.tab, w.lloc, w.lo);
-        ++launches;
-      }
+      // the fused kernel (1 CTA/SM) first on the solve's stream, the mono kernel
+      // (4 CTAs/SM, independent outputs) on a second stream: its CTAs take the
+      // SMs the fused kernel's last waves leave idle; both join before W/X
       if (w.m2l_ctas) {
         amr_m2l_fused_kernel<<<(unsigned)w.m2l_ctas, kM2lThreads, kM2lSmem, st>>>(w.dev_lv, w.m2l_work,
                                                                                  w.tab, w.lloc, w.lo);
         ++launches;
       }
+      if (w.mono_ctas && !mono_early) {  // leaf patches among leaf patches: monopole sources
+        cudaStreamWaitEvent(w.side2, w.ev_fork, 0);
+        amr_m2l_mono_kernel<<<(unsigned)w.mono_ctas, kM2lThreads, kMonoSmem, w.side2>>>(
+            w.mono_slots, w.slot_level, w.mass, w.slot_nbs, w.tab, w.lloc, w.lo);
+        cudaEventRecord(w.ev_join2, w.side2);
+        ++launches;
+      }
+      if (w.mono_ctas) cudaStreamWaitEvent(st, w.ev_join2, 0);
       if (w.wx_targets) {
         amr_wx_kernel<<<grid_for(w.wx_targets), 128, 0, st>>>(w.dev_lv, w.wx_tlev, w.wx_tflat,
                                                               w.wx_targets, w.wx_geo, w.lloc, w.lo);
