@@ -296,7 +296,8 @@ int tmgpu_gravity_amr_am_stats(tmgpu_gravity_amr* G, double* out);
  * leaf patches, W/X entries into leaf patches] (leaf targets need only L0, L_i), then
  * V pairs and W/X entries by (target, source) kind: [7..10] V (leaf<-leaf,
  * leaf<-internal, internal<-leaf, internal<-internal), [11..14] W/X likewise (a leaf
- * source's D and Q are zero: its term is the monopole one) */
+ * source's D and Q are zero: its term is the monopole one), [15] V pairs of the patches the
+ * monopole-source kernel takes (leaf patches whose neighbours are all leaves; out holds 16) */
 int tmgpu_gravity_amr_work(const tmgpu_gravity_amr* G, long long* out);
 /* multi-GPU (locally essential tree, multipole-moment exchange over NCCL): this rank (comm)
  * owns canonical slots [slot_bounds[r], slot_bounds[r+1]); masses and outputs become by local
@@ -319,7 +320,9 @@ int tmgpu_gravity_amr_let_plan(const int* leaves, long long nleaves, const long 
                                int me, long long* out, long long* send, long long* recv,
                                long long* send_hash, long long* recv_hash, tmgpu_error* err);
 /* per-phase device timing: totals in ms of [up (P2M + owned-subtree M2M), let (subtree-root
- * all-gather, shared-top M2M, halo-moment exchange; the top on one GPU), m2l, l2l, l2p, am] */
+ * all-gather, shared-top M2M, halo-moment exchange; the top on one GPU), m2l, l2l, l2p, am,
+ * then the M2L kernels alone: mono, fused, W/X] (ms holds 9). A timed solve runs those three
+ * kernels one after another on the solve's stream (untimed solves overlap them). */
 int tmgpu_gravity_amr_set_timing(tmgpu_gravity_amr* G, int on);
 int tmgpu_gravity_amr_timing(tmgpu_gravity_amr* G, double* ms, long long* solves);
 const double* tmgpu_gravity_amr_mass_ptr(const tmgpu_gravity_amr* G);

@@ -66,6 +66,11 @@ struct tmgpu_forest {
   long long g_stride = 0;
   cudaEvent_t ev_fork = nullptr;
   unsigned long long* err_dev = nullptr;
+  // grow-only device scratch kept across topology changes (regrid's prolonged
+  // and restricted blocks, its gather table, flag output): one allocation
+  // reused by every later regrid instead of a cudaMalloc per operation
+  char* scratch = nullptr;
+  size_t scratch_bytes = 0;
   // reference-exact 3-pass exchange (single GPU only)
   double* staged = nullptr;
   GhostFill* fills[3] = {nullptr, nullptr, nullptr};
@@ -208,6 +213,18 @@ cudaError_t upload(T** dst, const std::vector<T>& v, cudaError_t e) {
   e = cudaMalloc((void**)dst, v.empty() ? 16 : v.size() * sizeof(T));
   if (e == cudaSuccess && !v.empty())
     e = cudaMemcpy(*dst, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice);
+  return e;
+}
+
+// At least `bytes` of the forest's device scratch (contents not kept on growth).
+cudaError_t scratch_reserve(tmgpu_forest* f, size_t bytes) {
+  if (bytes <= f->scratch_bytes) return cudaSuccess;
+  bytes = std::max(bytes, f->scratch_bytes + f->scratch_bytes / 2);  // amortised growth
+  if (f->scratch) cudaFree(f->scratch);
+  f->scratch = nullptr;
+  f->scratch_bytes = 0;
+  cudaError_t e = cudaMalloc((void**)&f->scratch, bytes);
+  if (e == cudaSuccess) f->scratch_bytes = bytes;
   return e;
 }
 
@@ -416,6 +433,7 @@ void tmgpu_forest_destroy(tmgpu_forest* f) {
   if (!f) return;
   free_dev(f);
   tmgpu_forest_set_reflux(f, 0, nullptr);
+  if (f->scratch) cudaFree(f->scratch);
   if (f->ev_grav) cudaEventDestroy(f->ev_grav);
   if (f->ev_fork) cudaEventDestroy(f->ev_fork);
   if (f->side) cudaStreamDestroy(f->side);
@@ -473,34 +491,38 @@ int tmgpu_forest_regrid(tmgpu_forest* f, const uint64_t* refine, size_t nr, cons
     return fail(err, TMGPU_ERR_AMR, ex.what());
   }
   cudaStream_t st = 0;
-  std::vector<double*> temps;
-  cudaError_t e = cudaSuccess;
+  // every prolonged / restricted block lives until the final gather (a later
+  // operation may read an earlier one's output), so size the scratch for all
+  // of them plus the gather table, once
+  size_t blocks = 0;
+  for (const Forest::Op& op : f->forest.oplog()) blocks += op.refine ? 8 : 1;
+  const size_t nnew = f->forest.leaves().size();
+  const size_t blk_bytes = (size_t)stride * sizeof(double);
+  const size_t table_off = blocks * blk_bytes;
+  cudaError_t e = scratch_reserve(f, table_off + (nnew ? nnew : 1) * sizeof(double*));
   try {
+  double* next = (double*)f->scratch;
   for (const Forest::Op& op : f->forest.oplog()) {
     if (e != cudaSuccess) break;
     const NodeId& id = op.node;
     if (op.refine) {
-      double* ch = nullptr;
-      e = cudaMalloc(&ch, (size_t)8 * stride * sizeof(double));
-      if (e != cudaSuccess) break;
-      temps.push_back(ch);
-      e = cudaMemsetAsync(ch, 0, (size_t)8 * stride * sizeof(double), st);
+      double* ch = next;
+      next += 8 * stride;
+      e = cudaMemsetAsync(ch, 0, 8 * blk_bytes, st);
       if (e == cudaSuccess) e = launch_prolong(pool.at(id.packed()), ch, V, st);
       pool.erase(id.packed());
       for (int b = 0; b < 8; ++b)
         pool[id.child(b & 1, (b >> 1) & 1, (b >> 2) & 1).packed()] = ch + (long long)b * stride;
     } else {
-      double* pg = nullptr;
-      e = cudaMalloc(&pg, (size_t)stride * sizeof(double));
-      if (e != cudaSuccess) break;
-      temps.push_back(pg);
+      double* pg = next;
+      next += stride;
       const double* chp[8];
       for (int b = 0; b < 8; ++b) {
         const uint64_t c = id.child(b & 1, (b >> 1) & 1, (b >> 2) & 1).packed();
         chp[b] = pool.at(c);
         pool.erase(c);
       }
-      e = cudaMemsetAsync(pg, 0, (size_t)stride * sizeof(double), st);
+      e = cudaMemsetAsync(pg, 0, blk_bytes, st);
       if (e == cudaSuccess) e = launch_restrict(chp, pg, V, st);
       pool[id.packed()] = pg;
     }
@@ -514,20 +536,16 @@ int tmgpu_forest_regrid(tmgpu_forest* f, const uint64_t* refine, size_t nr, cons
     const auto& nl = f->forest.leaves();
     std::vector<const double*> src(nl.size());
     for (size_t s = 0; s < nl.size(); ++s) src[s] = pool.at(nl[s].packed());
-    const double** dsrc = nullptr;
-    e = cudaMalloc(&dsrc, (src.empty() ? 1 : src.size()) * sizeof(double*));
-    if (e == cudaSuccess && !src.empty())
+    const double** dsrc = (const double**)(f->scratch + table_off);
+    if (!src.empty())
       e = cudaMemcpy(dsrc, src.data(), src.size() * sizeof(double*), cudaMemcpyHostToDevice);
     if (e == cudaSuccess) e = launch_gather_blocks(dsrc, (long long)src.size(), f->arenas[f->cur], stride, st);
     if (e == cudaSuccess) e = cudaStreamSynchronize(st);
-    if (dsrc) cudaFree(dsrc);
   }
-  for (double* p : temps) cudaFree(p);
   cudaFree(old);
   if (rc != TMGPU_OK) return rc;
   return cuda_err(err, e, "tmgpu_forest_regrid");
   } catch (const std::exception& ex) {  // a bookkeeping bug, never expected
-    for (double* p : temps) cudaFree(p);
     return fail(err, TMGPU_ERR_AMR, std::string("regrid: ") + ex.what());
   }
 }
@@ -539,12 +557,11 @@ int tmgpu_forest_flag(tmgpu_forest* f, double theta, double rho_floor, int* flag
   if (err) std::memset(err, 0, sizeof(*err));
   if (int rc = ready(f, err)) return rc;
   const int V = f->forest.config().vars;
-  int* d = nullptr;
-  cudaError_t e = cudaMalloc(&d, (f->nslots ? f->nslots : 1) * sizeof(int));
+  cudaError_t e = scratch_reserve(f, (f->nslots ? f->nslots : 1) * sizeof(int));
+  int* d = (int*)f->scratch;
   if (e == cudaSuccess) e = launch_flag(f->arena(), (long long)V * 1728, f->nslots, theta, rho_floor, d, 0);
   if (e == cudaSuccess)
     e = cudaMemcpy(flags_host, d, f->nslots * sizeof(int), cudaMemcpyDeviceToHost);
-  if (d) cudaFree(d);
   return cuda_err(err, e, "tmgpu_forest_flag");
 }
 

@@ -52,6 +52,11 @@ struct GLv {
   const int* pgeo;  // cross-depth U entry -> row of the P2P geometry table
   double* unm;      // cross-depth U entry -> -(source mass), gathered per solve (amr_u_gather_kernel)
   long long nu;     // cross-depth U entries of this level
+  // leaf-mass indices (slot * 512 + cell, global slots) of the W/X entries
+  // whose source is a leaf cell (-1 otherwise) and of the U entries: with the
+  // leaf-mass array these replace the moment arrays' m of leaf cells (one GPU)
+  const int* mmi;
+  const int* pmi;
 };
 
 // P2P geometry of the 26 same-depth lattice offsets at unit spacing (depth 0):
@@ -138,8 +143,10 @@ __global__ void halo_mass_kernel(const GLv* __restrict__ Lv, const int* __restri
   }
 }
 
+// mass (one GPU, else null): leaf children's m from the leaf-mass array
+// (the same values P2M would store, read coalesced)
 __global__ void amr_m2m_kernel(const GLv* __restrict__ L, int l, const int* __restrict__ internal,
-                               long long n_int) {
+                               long long n_int, const double* __restrict__ mass = nullptr) {
   const GLv P = L[l], Ch = L[l + 1];
   const double hc = 1.0 / (double)(1LL << (l + 4));
   for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < n_int * 512;
@@ -152,7 +159,8 @@ __global__ void amr_m2m_kernel(const GLv* __restrict__ L, int l, const int* __re
     double o[10];
 #pragma unroll
     for (int q = 0; q < 10; ++q) o[q] = 0.0;
-    if (Ch.leaf_slot[cn] >= 0) {
+    const int lsl = Ch.leaf_slot[cn];
+    if (lsl >= 0) {
       // leaf child cells carry (m, +0, ..., +0): read only m. Dropping the +0
       // terms can only turn a +0 term into -0, and a sum started at +0 is the
       // same either way, so the result is tmo_grav_m2m's bit for bit.
@@ -161,7 +169,8 @@ __global__ void amr_m2m_kernel(const GLv* __restrict__ L, int l, const int* __re
           for (int a = 0; a < 2; ++a) {
             const double s[3] = {(a - 0.5) * hc, (b - 0.5) * hc, (cc - 0.5) * hc};
             const int ci = ((2 * I) & 7) + a, cj = ((2 * J) & 7) + b, ck = ((2 * K) & 7) + cc;
-            const double M = base[((ck * 8 + cj) * 8 + ci) * 10];
+            const int cc8 = (ck * 8 + cj) * 8 + ci;
+            const double M = mass ? mass[(long long)lsl * 512 + cc8] : base[cc8 * 10];
             o[0] += M;
 #pragma unroll
             for (int i = 0; i < 3; ++i) o[1 + i] += M * s[i];
@@ -403,9 +412,11 @@ __device__ __forceinline__ void m2l_patch(double* __restrict__ win, const double
   }
 }
 
+// mass (one GPU, else null): a leaf neighbour's window cells take m from the
+// leaf-mass array and zero-filled D, Q (its moments are (m, +0, ..., +0))
 __global__ void __launch_bounds__(kM2lThreads, 1) amr_m2l_fused_kernel(
     const GLv* __restrict__ Lv, const int2* __restrict__ work, const double* __restrict__ tab_all,
-    double* __restrict__ lloc, long long lo) {
+    double* __restrict__ lloc, long long lo, const double* __restrict__ mass) {
   extern __shared__ double sm[];
   double* win = sm;
   double* tabs = sm + kWinDoubles;
@@ -432,15 +443,21 @@ __global__ void __launch_bounds__(kM2lThreads, 1) amr_m2l_fused_kernel(
     ly -= 8 * oy, lz -= 8 * oz;
     const int* nbrow = nb27 + ((oz + 1) * 3 + (oy + 1)) * 3;
     const int nbs[3] = {nbrow[0], nbrow[1], nbrow[2]};
+    int lsl[3] = {-1, -1, -1};
+    if (mass)
+#pragma unroll
+      for (int q = 0; q < 3; ++q) lsl[q] = nbs[q] >= 0 ? L.leaf_slot[nbs[q]] : -1;
     double* dst = win + h * kWVar + ((wz & 1) * 2 + (wy & 1)) * kWSub + (wz >> 1) * kWPZ +
                   (wy >> 1) * kWPY;
     const long long rowoff = (long long)(lz * 8 + ly) * 8;
 #pragma unroll
     for (int wx = 0; wx < 12; ++wx) {
       const int ox = wx < 2 ? -1 : (wx > 9 ? 1 : 0), lx = wx - 2 - 8 * ox;
-      const int nb = nbs[ox + 1];
-      const double* src = L.mom + ((long long)(nb < 0 ? n : nb) * 512 + rowoff + lx) * 10 + h;
-      cp_async8(dst + wx, src, nb >= 0);
+      const int nb = nbs[ox + 1], ls = lsl[ox + 1];
+      if (ls >= 0)  // leaf neighbour (mass given): m, then +0s
+        cp_async8(dst + wx, mass + (long long)ls * 512 + rowoff + lx, h == 0);
+      else
+        cp_async8(dst + wx, L.mom + ((long long)(nb < 0 ? n : nb) * 512 + rowoff + lx) * 10 + h, nb >= 0);
     }
   }
   // neighbour patches that are internal (full moments): bit o of internal27
@@ -595,39 +612,51 @@ __device__ __forceinline__ void wx_mono(double nM, const double* __restrict__ e,
 
 template <int NOUT>
 __device__ __forceinline__ void wx_entries(const GLv* __restrict__ Lv, const long long* __restrict__ ment,
-                                           const int* __restrict__ mgeo, long long e0, long long e1,
+                                           const int* __restrict__ mgeo, const int* __restrict__ mmi,
+                                           const double* __restrict__ mass, long long e0, long long e1,
                                            const double* __restrict__ geo, double* acc) {
+  auto mom_of = [&](long long enc) { return Lv[enc >> 40].mom + (enc & ((1LL << 40) - 1)) * 10; };
+  auto apply = [&](long long e, int gi, double m0) {
+    if (gi < 0) {
+      wx_mono<NOUT>(-m0, geo + (long long)(~gi) * kTab, acc);
+    } else {
+      const double* pm = mom_of(__ldg(ment + e));
+      if constexpr (NOUT == 10) m2l_tab(pm, geo + (long long)gi * kTab, acc);
+      else m2l_tab4(pm, geo + (long long)gi * kTab, acc);
+    }
+  };
   long long e = e0;
-  for (; e + 3 < e1; e += 4) {  // four entries' first loads in flight, applied in order
+  if (mass) {  // leaf sources' m from the leaf-mass array (mmi >= 0 exactly when gi < 0)
+    for (; e + 3 < e1; e += 4) {  // four entries' loads in flight, applied in order
+      int gi[4], mi[4];
+      double m0[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) gi[u] = __ldg(mgeo + e + u), mi[u] = __ldg(mmi + e + u);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) m0[u] = mi[u] >= 0 ? __ldg(mass + mi[u]) : 0.0;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) apply(e + u, gi[u], m0[u]);
+    }
+    for (; e < e1; ++e) {
+      const int gi = __ldg(mgeo + e), mi = __ldg(mmi + e);
+      apply(e, gi, mi >= 0 ? __ldg(mass + mi) : 0.0);
+    }
+    return;
+  }
+  for (; e + 3 < e1; e += 4) {
     long long enc[4];
     int gi[4];
     double m0[4];
 #pragma unroll
     for (int u = 0; u < 4; ++u) enc[u] = __ldg(ment + e + u), gi[u] = __ldg(mgeo + e + u);
 #pragma unroll
-    for (int u = 0; u < 4; ++u) m0[u] = __ldg(Lv[enc[u] >> 40].mom + (enc[u] & ((1LL << 40) - 1)) * 10);
+    for (int u = 0; u < 4; ++u) m0[u] = __ldg(mom_of(enc[u]));
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      if (gi[u] < 0) {
-        wx_mono<NOUT>(-m0[u], geo + (long long)(~gi[u]) * kTab, acc);
-      } else {
-        const double* pm = Lv[enc[u] >> 40].mom + (enc[u] & ((1LL << 40) - 1)) * 10;
-        if constexpr (NOUT == 10) m2l_tab(pm, geo + (long long)gi[u] * kTab, acc);
-        else m2l_tab4(pm, geo + (long long)gi[u] * kTab, acc);
-      }
-    }
+    for (int u = 0; u < 4; ++u) apply(e + u, gi[u], m0[u]);
   }
   for (; e < e1; ++e) {
-    const long long enc = ment[e];
-    const double* mom = Lv[enc >> 40].mom + (enc & ((1LL << 40) - 1)) * 10;
-    const int gi = mgeo[e];
-    if (gi < 0) {
-      wx_mono<NOUT>(-mom[0], geo + (long long)(~gi) * kTab, acc);
-    } else if constexpr (NOUT == 10) {
-      m2l_tab(mom, geo + (long long)gi * kTab, acc);
-    } else {
-      m2l_tab4(mom, geo + (long long)gi * kTab, acc);
-    }
+    const int gi = __ldg(mgeo + e);
+    apply(e, gi, __ldg(mom_of(__ldg(ment + e))));
   }
 }
 
@@ -638,7 +667,8 @@ __device__ __forceinline__ void wx_entries(const GLv* __restrict__ Lv, const lon
 __global__ void __launch_bounds__(128, 4) amr_wx_kernel(const GLv* __restrict__ Lv, const int* __restrict__ tlev,
                                                         const long long* __restrict__ tflat, long long ntarget,
                                                         const double* __restrict__ geo,
-                                                        double* __restrict__ lloc, long long lo) {
+                                                        double* __restrict__ lloc, long long lo,
+                                                        const double* __restrict__ mass) {
   for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < ntarget;
        t += (long long)gridDim.x * blockDim.x) {
     const int l = tlev[t];
@@ -649,7 +679,7 @@ __global__ void __launch_bounds__(128, 4) amr_wx_kernel(const GLv* __restrict__ 
     if (leaf >= 0 && l > 0) {
       double* p = lloc + (long long)(leaf - lo) * 2048 + (flat & 511);
       double acc[4] = {p[0], p[512], p[1024], p[1536]};
-      wx_entries<4>(Lv, Lv[l].ment, Lv[l].mgeo, e0, e1, geo, acc);
+      wx_entries<4>(Lv, Lv[l].ment, Lv[l].mgeo, Lv[l].mmi, mass, e0, e1, geo, acc);
 #pragma unroll
       for (int q = 0; q < 4; ++q) p[q * 512] = acc[q];
     } else {
@@ -661,7 +691,7 @@ __global__ void __launch_bounds__(128, 4) amr_wx_kernel(const GLv* __restrict__ 
         acc[2 * h] = v.x;
         acc[2 * h + 1] = v.y;
       }
-      wx_entries<10>(Lv, Lv[l].ment, Lv[l].mgeo, e0, e1, geo, acc);
+      wx_entries<10>(Lv, Lv[l].ment, Lv[l].mgeo, Lv[l].mmi, mass, e0, e1, geo, acc);
 #pragma unroll
       for (int h = 0; h < 5; ++h)
         reinterpret_cast<double2*>(loc)[h] = make_double2(acc[2 * h], acc[2 * h + 1]);
@@ -761,12 +791,16 @@ __global__ void amr_l2l_kernel(const GLv* __restrict__ Lv, int l, long long nnod
 // -(source mass) of every cross-depth U entry, gathered in parallel over the
 // entries before L2P (whose per-target loop then reads them contiguously
 // instead of chasing entry -> moment); grid.y = level
-__global__ void amr_u_gather_kernel(const GLv* __restrict__ Lv) {
+__global__ void amr_u_gather_kernel(const GLv* __restrict__ Lv, const double* __restrict__ mass) {
   const GLv L = Lv[blockIdx.y];
   for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < L.nu;
        e += (long long)gridDim.x * blockDim.x) {
-    const long long enc = __ldg(L.pent + e);
-    L.unm[e] = -__ldg(Lv[enc >> 40].mom + (enc & ((1LL << 40) - 1)) * 10);
+    if (mass) {
+      L.unm[e] = -__ldg(mass + __ldg(L.pmi + e));
+    } else {
+      const long long enc = __ldg(L.pent + e);
+      L.unm[e] = -__ldg(Lv[enc >> 40].mom + (enc & ((1LL << 40) - 1)) * 10);
+    }
   }
 }
 
@@ -1138,7 +1172,7 @@ cudaError_t upload(const std::vector<T>& v, T** out) {
 // existing source, counted per neighbour-patch offset from the plan.
 // need: per-level node lists this GPU evaluates M2L for (nullptr = all);
 // [lo, hi): the canonical slots it evaluates L2P/P2P for.
-constexpr int kWorkCounts = 15;
+constexpr int kWorkCounts = 16;
 
 void count_work(const GravPlan& P, const std::vector<std::vector<int>>* need, long long lo,
                 long long hi, long long out[kWorkCounts]) {
@@ -1155,7 +1189,7 @@ void count_work(const GravPlan& P, const std::vector<std::vector<int>>* need, lo
           else if (dx || dy || dz) ++ptab[o];
         }
   }
-  long long v = 0, vk = 0, p = 0, wx = 0, u = 0, vleaf = 0, wxleaf = 0;
+  long long v = 0, vk = 0, p = 0, wx = 0, u = 0, vleaf = 0, wxleaf = 0, vmono = 0;
   long long vt[4] = {0, 0, 0, 0}, wt[4] = {0, 0, 0, 0};  // by (target internal?, source internal?)
   for (int l = 0; l < P.nlevels; ++l) {
     const GravLevel& L = P.lv[l];
@@ -1177,6 +1211,13 @@ void count_work(const GravPlan& P, const std::vector<std::vector<int>>* need, lo
       }
       v += vn;
       wx += wn;
+      // amr_m2l_mono_kernel's patches (leaf below the root, existing neighbours all leaves)
+      bool mono = l > 0 && L.leaf_slot[n] >= 0;
+      for (int o = 0; o < 27 && mono; ++o) {
+        const int nb = L.nbr[(size_t)n * 27 + o];
+        if (nb >= 0 && L.leaf_slot[nb] < 0) mono = false;
+      }
+      if (mono) vmono += vn;
       if (L.leaf_slot[n] >= 0) vleaf += vn, wxleaf += wn;  // L0, L_i only
     };
     if (need)
@@ -1211,14 +1252,17 @@ void count_work(const GravPlan& P, const std::vector<std::vector<int>>* need, lo
   out[5] = vleaf;
   out[6] = wxleaf;
   for (int q = 0; q < 4; ++q) out[7 + q] = vt[q], out[11 + q] = wt[q];
+  out[15] = vmono;
 }
 
 constexpr int kMaxLetPeers = 8;
 
 // per-phase device timing of solves (bench): events at the phase boundaries
 constexpr int kGravPhases = 6;  // up (P2M + owned M2M), let (moment exchange + top), m2l, l2l, l2p, am
+constexpr int kGravKernels = 3;  // the M2L kernels alone: mono, fused, W/X
 struct GravTimingRec {
   cudaEvent_t ev[kGravPhases + 1];
+  cudaEvent_t k[kGravKernels + 1];  // brackets of the M2L kernels (serialised when timing)
 };
 
 struct LetPeer {
@@ -1239,7 +1283,7 @@ struct GravAmrWork {
   long long work[kWorkCounts] = {};
   bool timing = false;
   std::vector<GravTimingRec> pending;
-  double phase_ms[kGravPhases] = {0, 0, 0, 0, 0, 0};
+  double phase_ms[kGravPhases + kGravKernels] = {};
   long long timed_solves = 0;
   std::vector<GLv> host_lv;
   std::vector<void*> allocs;
@@ -1266,6 +1310,7 @@ struct GravAmrWork {
   long long seg_max = 0;                   // largest rank segment (slots)
   // locally essential tree (grav_let_plan): device lists and buffers
   bool let = false;
+  bool root_leaf = false;  // a level-0 patch is a leaf (the dense top M2M reads its moments)
   std::vector<int*> let_owned, let_top;    // per level internal patch lists
   std::vector<long long> n_owned, n_top;
   int2* roots_all = nullptr;               // every rank's subtree roots, rank-major
@@ -1290,7 +1335,7 @@ struct GravAmrWork {
   long long* mono_slots = nullptr;  // amr_m2l_mono_kernel: leaf patches among leaf patches (slot)
   long long mono_ctas = 0;
   long long u_max = 0;  // most cross-depth U entries of a level
-  int* wx_tlev = nullptr;         // W/X kernel targets (level, flat), by entry count
+  int* wx_tlev = nullptr;         // W/X kernel targets (level, flat), in patch order
   long long* wx_tflat = nullptr;
   long long wx_targets = 0;
   double* wx_geo = nullptr;  // [distinct W/X separations][13]
@@ -1593,8 +1638,10 @@ extern "C" {
 
 void tmgpu_gravity_amr_destroy(tmgpu_gravity_amr* G) {
   if (!G) return;
-  for (auto& r : G->w.pending)
+  for (auto& r : G->w.pending) {
     for (auto& e : r.ev) cudaEventDestroy(e);
+    for (auto& e : r.k) cudaEventDestroy(e);
+  }
   if (G->w.ev_fork) cudaEventDestroy(G->w.ev_fork);
   if (G->w.ev_join) cudaEventDestroy(G->w.ev_join);
   if (G->w.side) cudaStreamDestroy(G->w.side);
@@ -1619,6 +1666,13 @@ tmgpu_gravity_amr* tmgpu_gravity_amr_create(const int* leaves, long long nleaves
   }
   const GravPlan& P = w.plan;
   count_work(P, nullptr, 0, nleaves, w.work);
+  if ((long long)nleaves * 512 > INT32_MAX) {
+    set_err(err, TMGPU_ERR_INVALID, "gravity_amr: more than 2^31 leaf cells");
+    delete G;
+    return nullptr;
+  }
+  w.root_leaf = false;
+  for (int ls : P.lv[0].leaf_slot) w.root_leaf |= ls >= 0;
   w.nslots = nleaves;
   w.hi = nleaves;
   while (w.P < nleaves) w.P <<= 1;
@@ -1667,7 +1721,22 @@ tmgpu_gravity_amr* tmgpu_gravity_amr_create(const int* leaves, long long nleaves
       e = upload(mg, &mgeo), track(mgeo);
     }
     if (e == cudaSuccess) e = upload(L.pgeo, &pgeo), track(pgeo);
+    int *mmi = nullptr, *pmi = nullptr;
+    if (e == cudaSuccess) {  // leaf-mass indices of leaf-cell W/X sources and of U sources
+      auto mass_index = [&](long long enc) -> int {
+        const GravLevel& S = P.lv[enc >> 40];
+        const long long flat = enc & ((1LL << 40) - 1);
+        const int ls = S.leaf_slot[(size_t)(flat >> 9)];
+        return ls >= 0 ? (int)((long long)ls * 512 + (flat & 511)) : -1;
+      };
+      std::vector<int> mi(L.ment.size()), pi(L.pent.size());
+      for (size_t q = 0; q < mi.size(); ++q) mi[q] = mass_index(L.ment[q]);
+      for (size_t q = 0; q < pi.size(); ++q) pi[q] = mass_index(L.pent[q]);
+      e = upload(mi, &mmi), track(mmi);
+      if (e == cudaSuccess) e = upload(pi, &pmi), track(pmi);
+    }
     if (e != cudaSuccess) break;
+    g.mmi = mmi, g.pmi = pmi;
     g.ijk = ijk, g.nbr = nbr, g.child = child, g.parent = parent, g.leaf_slot = slot;
     g.moff = moff, g.ment = ment, g.poff = poff, g.pent = pent, g.mgeo = mgeo, g.pgeo = pgeo;
     g.nu = (long long)L.pent.size();
@@ -1876,13 +1945,16 @@ int tmgpu_gravity_amr_solve(tmgpu_gravity_amr* G, const double* mass, double* ph
   const bool timed = w.timing && e == cudaSuccess;
   if (timed) {
     for (auto& ev : rec.ev) cudaEventCreate(&ev);
+    for (auto& ev : rec.k) cudaEventCreate(&ev);
     cudaEventRecord(rec.ev[0], st);
   }
   int rc = TMGPU_OK;
   // the mono M2L needs only the leaf masses (and, distributed, the halo
   // leaves' masses that come with the moment exchange): on one GPU it starts
   // now on its own stream and overlaps the whole upward pass
-  const bool mono_early = !w.let && w.mono_ctas > 0;
+  // (a timed solve runs the three M2L kernels one after another on `st`
+  // instead, each between its own events: their durations measured alone)
+  const bool mono_early = !w.let && w.mono_ctas > 0 && !timed;
   if (e == cudaSuccess && mono_early) {
     cudaEventRecord(w.ev_fork2, st);
     cudaStreamWaitEvent(w.side2, w.ev_fork2, 0);
@@ -1893,15 +1965,20 @@ int tmgpu_gravity_amr_solve(tmgpu_gravity_amr* G, const double* mass, double* ph
   }
   if (e == cudaSuccess && rc == TMGPU_OK) {
     long long launches = 0;
-    if (nloc)
+    // one GPU: leaf cells' m is read from the leaf-mass array wherever a
+    // leaf moment would be (M2M, the fused window, W/X, U), so P2M is skipped;
+    // distributed, leaf moments travel in the moment exchange and P2M stays
+    const double* lmass = (!w.let && !w.root_leaf) ? w.mass : nullptr;
+    if (nloc && !lmass) {
       amr_p2m_kernel<<<grid_for(nout), 128, 0, st>>>(w.mass, nloc, w.lo, w.slot_level, w.slot_node,
                                                      w.dev_lv);
-    ++launches;
+      ++launches;
+    }
     for (int l = P.nlevels - 2; l >= 0; --l) {  // own subtrees (all of the tree on one GPU)
       const long long ni = w.let ? w.n_owned[l] : (long long)P.lv[l].internal.size();
       if (!ni) continue;
       amr_m2m_kernel<<<grid_for(ni * 512), 128, 0, st>>>(w.dev_lv, l, w.let ? w.let_owned[l] : w.internal[l],
-                                                         ni);
+                                                         ni, lmass);
       ++launches;
     }
     if (timed) cudaEventRecord(rec.ev[1], st);
@@ -1965,24 +2042,34 @@ int tmgpu_gravity_amr_solve(tmgpu_gravity_amr* G, const double* mass, double* ph
       // the fused kernel (1 CTA/SM) first on the solve's stream, the mono kernel
       // (4 CTAs/SM, independent outputs) on a second stream: its CTAs take the
       // SMs the fused kernel's last waves leave idle; both join before W/X
+      if (timed) {
+        cudaEventRecord(rec.k[0], st);
+        if (w.mono_ctas)
+          amr_m2l_mono_kernel<<<(unsigned)w.mono_ctas, kM2lThreads, kMonoSmem, st>>>(
+              w.mono_slots, w.slot_level, w.mass, w.slot_nbs, w.tab, w.lloc, w.lo);
+        cudaEventRecord(rec.k[1], st);
+        launches += w.mono_ctas ? 1 : 0;
+      }
       if (w.m2l_ctas) {
         amr_m2l_fused_kernel<<<(unsigned)w.m2l_ctas, kM2lThreads, kM2lSmem, st>>>(w.dev_lv, w.m2l_work,
-                                                                                 w.tab, w.lloc, w.lo);
+                                                                                 w.tab, w.lloc, w.lo, lmass);
         ++launches;
       }
-      if (w.mono_ctas && !mono_early) {  // leaf patches among leaf patches: monopole sources
+      if (timed) cudaEventRecord(rec.k[2], st);
+      if (w.mono_ctas && !mono_early && !timed) {  // leaf patches among leaf patches: monopole sources
         cudaStreamWaitEvent(w.side2, w.ev_fork, 0);
         amr_m2l_mono_kernel<<<(unsigned)w.mono_ctas, kM2lThreads, kMonoSmem, w.side2>>>(
             w.mono_slots, w.slot_level, w.mass, w.slot_nbs, w.tab, w.lloc, w.lo);
         cudaEventRecord(w.ev_join2, w.side2);
         ++launches;
       }
-      if (w.mono_ctas) cudaStreamWaitEvent(st, w.ev_join2, 0);
+      if (w.mono_ctas && !timed) cudaStreamWaitEvent(st, w.ev_join2, 0);
       if (w.wx_targets) {
         amr_wx_kernel<<<grid_for(w.wx_targets), 128, 0, st>>>(w.dev_lv, w.wx_tlev, w.wx_tflat,
-                                                              w.wx_targets, w.wx_geo, w.lloc, w.lo);
+                                                              w.wx_targets, w.wx_geo, w.lloc, w.lo, lmass);
         ++launches;
       }
+      if (timed) cudaEventRecord(rec.k[3], st);
     }
     cudaStreamWaitEvent(st, w.ev_join, 0);
     if (timed) cudaEventRecord(rec.ev[3], st);
@@ -2002,7 +2089,7 @@ int tmgpu_gravity_amr_solve(tmgpu_gravity_amr* G, const double* mass, double* ph
       e = cudaMemsetAsync(w.part, 0, (size_t)w.P * 16 * sizeof(double), st);
     if (w.u_max) {  // U entries' source masses, gathered in parallel
       amr_u_gather_kernel<<<dim3((unsigned)std::min<long long>((w.u_max + 255) / 256, 1184), P.nlevels), 256, 0, st>>>(
-          w.dev_lv);
+          w.dev_lv, lmass);
       ++launches;
     }
     if (nloc)
@@ -2256,8 +2343,10 @@ int tmgpu_gravity_amr_set_timing(tmgpu_gravity_amr* G, int on) {
   GravAmrWork& w = G->w;
   w.timing = on != 0;
   if (on) {
-    for (auto& r : w.pending)
+    for (auto& r : w.pending) {
       for (auto& e : r.ev) cudaEventDestroy(e);
+      for (auto& e : r.k) cudaEventDestroy(e);
+    }
     w.pending.clear();
     for (double& x : w.phase_ms) x = 0.0;
     w.timed_solves = 0;
@@ -2275,12 +2364,18 @@ int tmgpu_gravity_amr_timing(tmgpu_gravity_amr* G, double* ms, long long* solves
       cudaEventElapsedTime(&t, r.ev[q], r.ev[q + 1]);
       w.phase_ms[q] += t;
     }
+    for (int q = 0; q < kGravKernels; ++q) {
+      float t = 0.f;
+      cudaEventElapsedTime(&t, r.k[q], r.k[q + 1]);
+      w.phase_ms[kGravPhases + q] += t;
+    }
     for (auto& e : r.ev) cudaEventDestroy(e);
+    for (auto& e : r.k) cudaEventDestroy(e);
     ++w.timed_solves;
   }
   w.pending.clear();
   if (ms)
-    for (int q = 0; q < kGravPhases; ++q) ms[q] = w.phase_ms[q];
+    for (int q = 0; q < kGravPhases + kGravKernels; ++q) ms[q] = w.phase_ms[q];
   if (solves) *solves = w.timed_solves;
   return TMGPU_OK;
 }

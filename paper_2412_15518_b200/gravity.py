@@ -271,22 +271,23 @@ class GravityAMR:
 
     def work(self):
         """Algorithmic work of one solve: dict of interaction counts."""
-        out = (C.c_longlong * 15)()
+        out = (C.c_longlong * 16)()
         lib.tmgpu_gravity_amr_work(self.h, out)
         kinds = ("ll", "li", "il", "ii")  # (target, source): l leaf, i internal
         return {"v_pairs": out[0], "wx_entries": out[1], "p2p_pairs": out[2],
                 "u_cross_entries": out[3], "v_pairs_evaluated": out[4], "v_pairs_leaf": out[5],
                 "wx_entries_leaf": out[6], **{"v_" + k: out[7 + q] for q, k in enumerate(kinds)},
-                **{"wx_" + k: out[11 + q] for q, k in enumerate(kinds)}}
+                **{"wx_" + k: out[11 + q] for q, k in enumerate(kinds)}, "v_mono": out[15]}
 
     def set_timing(self, on: bool) -> None:
         lib.tmgpu_gravity_amr_set_timing(self.h, int(on))
 
-    PHASES = ("up", "let", "m2l", "l2l", "l2p", "am")
+    PHASES = ("up", "let", "m2l", "l2l", "l2p", "am", "k_mono", "k_fused", "k_wx")
 
     def timing(self):
-        """(ms totals per phase, solves timed) since set_timing(True)."""
-        ms = (C.c_double * 6)()
+        """(ms totals per phase, solves timed) since set_timing(True). k_mono,
+        k_fused, k_wx: the M2L kernels alone (a timed solve serialises them)."""
+        ms = (C.c_double * 9)()
         n = C.c_longlong()
         _lib.check(lib.tmgpu_gravity_amr_timing(self.h, ms, C.byref(n)), TmgpuError())
         return dict(zip(self.PHASES, ms)), n.value
