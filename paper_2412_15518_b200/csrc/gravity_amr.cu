@@ -336,6 +336,13 @@ __device__ __forceinline__ void cp_async16(double* smem, const double* gmem) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem) : "memory");
 }
 
+// 16 bytes, zero-filled when !valid
+__device__ __forceinline__ void cp_async16z(double* smem, const double* gmem, bool valid) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa), "l"(gmem), "r"(valid ? 16 : 0)
+               : "memory");
+}
+
 __device__ __forceinline__ void cp_async8(double* smem, const double* gmem, bool valid) {
   const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(sa), "l"(gmem),
@@ -415,24 +422,32 @@ __device__ __forceinline__ void m2l_patch(double* __restrict__ win, const double
 // mass (one GPU, else null): a leaf neighbour's window cells take m from the
 // leaf-mass array and zero-filled D, Q (its moments are (m, +0, ..., +0))
 __global__ void __launch_bounds__(kM2lThreads, 1) amr_m2l_fused_kernel(
-    const GLv* __restrict__ Lv, const int2* __restrict__ work, const double* __restrict__ tab_all,
+    const GLv* __restrict__ Lv, const int2* __restrict__ work, const double* __restrict__ tabp_all,
     double* __restrict__ lloc, long long lo, const double* __restrict__ mass) {
   extern __shared__ double sm[];
+  __shared__ int s_nb[27], s_ls[27];
+  __shared__ unsigned s_int27;
   double* win = sm;
   double* tabs = sm + kWinDoubles;
   const int2 wk = work[blockIdx.x];
   const int l = wk.x, n = wk.y;
   const GLv L = Lv[l];
   const int* nb27 = L.nbr + (long long)n * 27;
-  // asynchronous fill (cp.async, 8-byte elements, zero-fill for missing
-  // patches and for the 27 near offsets of the level's geometry table)
-  const double* tab = tab_all + (long long)(l + 3) * kOff3 * kTab;
-  for (int q = threadIdx.x; q < kOff3 * kTab; q += kM2lThreads) {
-    const int o = q / kTab;
-    const int dx = o % kOff - 3, dy = (o / kOff) % kOff - 3, dz = o / (kOff * kOff) - 3;
-    const bool near = dx >= -1 && dx <= 1 && dy >= -1 && dy <= 1 && dz >= -1 && dz <= 1;
-    cp_async8(tabs + o * kTabP + (q - o * kTab), tab + q, !near);
+  // asynchronous fill (cp.async): the depth's geometry table, already in its
+  // shared-memory layout (tabp_all: 14-double rows, the 27 near rows zero)
+  const double* tabp = tabp_all + (long long)(l + 3) * kTabDoubles;
+  for (int q = threadIdx.x; q < kTabDoubles / 2; q += kM2lThreads) cp_async16(tabs + 2 * q, tabp + 2 * q);
+  // the 27 neighbour patches and their leaf slots, once; bit o of
+  // internal27: neighbour o exists and is internal (full moments)
+  if (threadIdx.x < 32) {
+    const int o = threadIdx.x;
+    const int nb = o < 27 ? nb27[o] : -1;
+    const int ls = nb >= 0 ? L.leaf_slot[nb] : -1;
+    const unsigned bits = __ballot_sync(0xffffffffu, nb >= 0 && ls < 0);
+    if (o < 27) s_nb[o] = nb, s_ls[o] = ls;
+    if (o == 0) s_int27 = bits;
   }
+  __syncthreads();
   // task = (window row (wy, wz), component), component fastest: a warp's
   // copies of one x position read ~3 consecutive cells' 80-byte moments
   for (int task = threadIdx.x; task < 1440; task += kM2lThreads) {
@@ -441,12 +456,12 @@ __global__ void __launch_bounds__(kM2lThreads, 1) amr_m2l_fused_kernel(
     int ly = wy - 2, lz = wz - 2;
     const int oy = ly < 0 ? -1 : (ly > 7 ? 1 : 0), oz = lz < 0 ? -1 : (lz > 7 ? 1 : 0);
     ly -= 8 * oy, lz -= 8 * oz;
-    const int* nbrow = nb27 + ((oz + 1) * 3 + (oy + 1)) * 3;
-    const int nbs[3] = {nbrow[0], nbrow[1], nbrow[2]};
+    const int r3 = ((oz + 1) * 3 + (oy + 1)) * 3;
+    const int nbs[3] = {s_nb[r3], s_nb[r3 + 1], s_nb[r3 + 2]};
     int lsl[3] = {-1, -1, -1};
     if (mass)
 #pragma unroll
-      for (int q = 0; q < 3; ++q) lsl[q] = nbs[q] >= 0 ? L.leaf_slot[nbs[q]] : -1;
+      for (int q = 0; q < 3; ++q) lsl[q] = s_ls[r3 + q];
     double* dst = win + h * kWVar + ((wz & 1) * 2 + (wy & 1)) * kWSub + (wz >> 1) * kWPZ +
                   (wy >> 1) * kWPY;
     const long long rowoff = (long long)(lz * 8 + ly) * 8;
@@ -460,12 +475,7 @@ __global__ void __launch_bounds__(kM2lThreads, 1) amr_m2l_fused_kernel(
         cp_async8(dst + wx, L.mom + ((long long)(nb < 0 ? n : nb) * 512 + rowoff + lx) * 10 + h, nb >= 0);
     }
   }
-  // neighbour patches that are internal (full moments): bit o of internal27
-  unsigned internal27 = 0;
-  for (int o = 0; o < 27; ++o) {
-    const int nb = nb27[o];
-    if (nb >= 0 && L.leaf_slot[nb] < 0) internal27 |= 1u << o;
-  }
+  const unsigned internal27 = s_int27;
   asm volatile("cp.async.wait_all;\n" ::: "memory");
   __syncthreads();
   const int leaf = L.leaf_slot[n];
@@ -525,26 +535,24 @@ __device__ __forceinline__ void mono_row(const double* __restrict__ src, const d
 
 __global__ void __launch_bounds__(kM2lThreads, 4) amr_m2l_mono_kernel(
     const long long* __restrict__ slots, const int* __restrict__ slot_level, const double* __restrict__ mass,
-    const int* __restrict__ slot_nbs, const double* __restrict__ tab_all, double* __restrict__ lloc,
+    const int* __restrict__ slot_nbs, const double* __restrict__ tab4p_all, double* __restrict__ lloc,
     long long lo) {
   extern __shared__ double sm[];
   double* win = sm;
   double* tabs = sm + kMonoWin;
   const long long s = slots[blockIdx.x];
   const int l = slot_level[s];
-  const double* tab = tab_all + (long long)(l + 3) * kOff3 * kTab;
-  for (int q = threadIdx.x; q < kOff3 * 4; q += kM2lThreads) {
-    const int o = q >> 2;
-    const int dx = o % kOff - 3, dy = (o / kOff) % kOff - 3, dz = o / (kOff * kOff) - 3;
-    const bool near = dx >= -1 && dx <= 1 && dy >= -1 && dy <= 1 && dz >= -1 && dz <= 1;
-    cp_async8(tabs + q, tab + (long long)o * kTab + (q & 3), !near);
-  }
-  const int* nb27 = slot_nbs + s * 27;
+  // the depth's monopole table (4 values per offset, near rows zero)
+  const double* tab4p = tab4p_all + (long long)(l + 3) * kOff3 * 4;
+  for (int q = threadIdx.x; q < kOff3 * 2; q += kM2lThreads) cp_async16(tabs + 2 * q, tab4p + 2 * q);
+  __shared__ int s_nb[27];
+  if (threadIdx.x < 27) s_nb[threadIdx.x] = slot_nbs[s * 27 + threadIdx.x];
+  __syncthreads();
   for (int t = threadIdx.x; t < 1728; t += kM2lThreads) {
-    const int wx = t % 12, wy = (t / 12) % 12, wz = t / 144;
+    const int row = t / 12, wx = t - 12 * row, wz = row / 12, wy = row - 12 * wz;
     const int ox = wx < 2 ? -1 : (wx > 9 ? 1 : 0), oy = wy < 2 ? -1 : (wy > 9 ? 1 : 0),
               oz = wz < 2 ? -1 : (wz > 9 ? 1 : 0);
-    const int nb = nb27[((oz + 1) * 3 + (oy + 1)) * 3 + ox + 1];
+    const int nb = s_nb[((oz + 1) * 3 + (oy + 1)) * 3 + ox + 1];
     const int lx = wx - 2 - 8 * ox, ly = wy - 2 - 8 * oy, lz = wz - 2 - 8 * oz;
     double* dst = win + ((wz & 1) * 2 + (wy & 1)) * kWSub + (wz >> 1) * kWPZ + (wy >> 1) * kWPY + wx;
     cp_async8(dst, mass + ((long long)(nb < 0 ? s : nb) * 512 + (lz * 8 + ly) * 8 + lx), nb >= 0);
@@ -660,6 +668,64 @@ __device__ __forceinline__ void wx_entries(const GLv* __restrict__ Lv, const lon
   }
 }
 
+// A leaf target's entries with the leaf-mass array (one GPU): eight entries'
+// loads in flight — index and geometry row, then the mass and the row's 4
+// monopole values (geo4, two 16-byte loads) — applied in order; the terms are
+// wx_mono<4>'s operations (an internal source's entry takes m2l_tab4).
+__device__ __forceinline__ void wx_leaf_entries(const GLv* __restrict__ Lv, const long long* __restrict__ ment,
+                                                const int* __restrict__ mgeo, const int* __restrict__ mmi,
+                                                const double* __restrict__ mass, long long e0, long long e1,
+                                                const double* __restrict__ geo, const double* __restrict__ geo4,
+                                                double* acc) {
+  constexpr int D = 8;
+  const double2* g2 = reinterpret_cast<const double2*>(geo4);
+  auto full = [&](long long e, int gi) {
+    const long long enc = __ldg(ment + e);
+    m2l_tab4(Lv[enc >> 40].mom + (enc & ((1LL << 40) - 1)) * 10, geo + (long long)gi * kTab, acc);
+  };
+  long long e = e0;
+  for (; e + D - 1 < e1; e += D) {
+    int gi[D], mi[D];
+#pragma unroll
+    for (int u = 0; u < D; ++u) gi[u] = __ldg(mgeo + e + u), mi[u] = __ldg(mmi + e + u);
+    double m0[D];
+    double2 ga[D], gb[D];
+#pragma unroll
+    for (int u = 0; u < D; ++u) {
+      const bool mono = gi[u] < 0;
+      const long long row = mono ? ~gi[u] : 0;
+      m0[u] = mono ? __ldg(mass + mi[u]) : 0.0;
+      ga[u] = __ldg(g2 + 2 * row);
+      gb[u] = __ldg(g2 + 2 * row + 1);
+    }
+#pragma unroll
+    for (int u = 0; u < D; ++u) {
+      if (gi[u] < 0) {
+        const double nM = -m0[u];
+        acc[0] = acc[0] + nM * ga[u].x;
+        acc[1] = fma(nM, ga[u].y, acc[1]);
+        acc[2] = fma(nM, gb[u].x, acc[2]);
+        acc[3] = fma(nM, gb[u].y, acc[3]);
+      } else {
+        full(e + u, gi[u]);
+      }
+    }
+  }
+  for (; e < e1; ++e) {
+    const int gi = __ldg(mgeo + e);
+    if (gi < 0) {
+      const double nM = -__ldg(mass + __ldg(mmi + e));
+      const double2 a = __ldg(g2 + 2 * (long long)~gi), b = __ldg(g2 + 2 * (long long)~gi + 1);
+      acc[0] = acc[0] + nM * a.x;
+      acc[1] = fma(nM, a.y, acc[1]);
+      acc[2] = fma(nM, b.x, acc[2]);
+      acc[3] = fma(nM, b.y, acc[3]);
+    } else {
+      full(e, gi);
+    }
+  }
+}
+
 // W/X pairs (AMR level jumps) after the V-list sums, in the list's sorted
 // order, one thread per target with entries (targets in patch order);
 // geometry from the plan's separation table (m2l_geom of each distinct R).
@@ -668,7 +734,8 @@ __global__ void __launch_bounds__(128, 4) amr_wx_kernel(const GLv* __restrict__ 
                                                         const long long* __restrict__ tflat, long long ntarget,
                                                         const double* __restrict__ geo,
                                                         double* __restrict__ lloc, long long lo,
-                                                        const double* __restrict__ mass) {
+                                                        const double* __restrict__ mass,
+                                                        const double* __restrict__ geo4) {
   for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < ntarget;
        t += (long long)gridDim.x * blockDim.x) {
     const int l = tlev[t];
@@ -679,7 +746,10 @@ __global__ void __launch_bounds__(128, 4) amr_wx_kernel(const GLv* __restrict__ 
     if (leaf >= 0 && l > 0) {
       double* p = lloc + (long long)(leaf - lo) * 2048 + (flat & 511);
       double acc[4] = {p[0], p[512], p[1024], p[1536]};
-      wx_entries<4>(Lv, Lv[l].ment, Lv[l].mgeo, Lv[l].mmi, mass, e0, e1, geo, acc);
+      if (mass)
+        wx_leaf_entries(Lv, Lv[l].ment, Lv[l].mgeo, Lv[l].mmi, mass, e0, e1, geo, geo4, acc);
+      else
+        wx_entries<4>(Lv, Lv[l].ment, Lv[l].mgeo, Lv[l].mmi, mass, e0, e1, geo, acc);
 #pragma unroll
       for (int q = 0; q < 4; ++q) p[q * 512] = acc[q];
     } else {
@@ -697,6 +767,22 @@ __global__ void __launch_bounds__(128, 4) amr_wx_kernel(const GLv* __restrict__ 
         reinterpret_cast<double2*>(loc)[h] = make_double2(acc[2 * h], acc[2 * h + 1]);
     }
   }
+}
+
+// The M2L geometry table in the kernels' shared-memory layouts, per depth:
+// tabp [343][14] (13 values + a zero pad) and tab4p [343][4] (the monopole
+// values), the 27 near offsets' rows zero
+__global__ void pad_tables_kernel(const double* __restrict__ tab, int D, double* __restrict__ tabp,
+                                  double* __restrict__ tab4p) {
+  const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (t >= (long long)(D + 1) * kOff3 * kTabP) return;
+  const long long row = t / kTabP;
+  const int q = (int)(t % kTabP), o = (int)(row % kOff3);
+  const int dx = o % kOff - 3, dy = (o / kOff) % kOff - 3, dz = o / (kOff * kOff) - 3;
+  const bool near = dx >= -1 && dx <= 1 && dy >= -1 && dy <= 1 && dz >= -1 && dz <= 1;
+  const double v = (near || q >= kTab) ? 0.0 : tab[row * kTab + q];
+  tabp[t] = v;
+  if (q < 4) tab4p[row * 4 + q] = v;
 }
 
 // P2P geometry of the 26 same-depth lattice offsets at every cell depth
@@ -813,10 +899,8 @@ __global__ void amr_u_gather_kernel(const GLv* __restrict__ Lv, const double* __
 // shared memory; neighbour masses come from the leaf-mass array (coalesced),
 // cross-depth U pairs from the plan's geometry table. Term order: 26 offsets
 // dz, dy, dx ascending, then the U pairs. With `part`, the slot's 16
-// angular-momentum sums follow (am_block_sums: the per-slot pair tree).
+// angular-momentum sums follow (am_block_sums2: the per-slot pair tree).
 __device__ __forceinline__ void cell_pos(const GLv* __restrict__ Lv, int l, int n, int c, double x[3]);
-__device__ __forceinline__ void am_block_sums(double m, const double x[3], double gx, double gy,
-                                              double gz, double* __restrict__ out16);
 __device__ __forceinline__ void am_block_sums2(double m0, const double x0[3], const double g0[3], double m1,
                                                const double x1[3], const double g1[3], double* __restrict__ out16);
 
@@ -834,8 +918,9 @@ __global__ void __launch_bounds__(kL2pThreads, 4) amr_l2p_kernel(const GLv* __re
                                                       double* __restrict__ part) {
   // everything the cell needs from memory is staged up front by cp.async, so
   // the loads overlap each other instead of forming per-thread chains:
-  //   mw   masses of the patch and its one-cell halo, [z 10][y 10][x pitch 24]
-  //        (pitch 24: the two rows of a half-warp fall in disjoint banks)
+  //   mw   masses of the patch and its one-cell halo, [z 10][y 10][x pitch 24],
+  //        x = -1..8 at offsets 1..10 (interior 16-byte aligned; pitch 24: the
+  //        two rows of a half-warp fall in disjoint banks)
   //   ll   the leaf's compact V + W/X locals [4][512]
   //   pl   the 4^3 parent cells above the patch, [cell][10] (the L2L input)
   __shared__ double w26[27][4];
@@ -858,14 +943,21 @@ __global__ void __launch_bounds__(kL2pThreads, 4) amr_l2p_kernel(const GLv* __re
     if (o == 0) valid27 = bit;
   }
   __syncthreads();
-  for (int t = threadIdx.x; t < 1000; t += blockDim.x) {
-    const int wx = t % 10, wy = (t / 10) % 10, wz = t / 100;
-    const int ox = wx < 1 ? -1 : (wx > 8 ? 1 : 0), oy = wy < 1 ? -1 : (wy > 8 ? 1 : 0),
-              oz = wz < 1 ? -1 : (wz > 8 ? 1 : 0);
+  // window rows (wy, wz) of x = -1..8 at offsets 1..10: the 8 interior x as
+  // four 16-byte copies from one neighbour row, the two halo cells as 8 bytes
+  for (int t = threadIdx.x; t < 600; t += blockDim.x) {
+    const bool interior = t < 400;
+    const int row = interior ? (t >> 2) : ((t - 400) >> 1), q = interior ? (t & 3) : ((t - 400) & 1);
+    const int wy = row % 10, wz = row / 10;
+    const int oy = wy < 1 ? -1 : (wy > 8 ? 1 : 0), oz = wz < 1 ? -1 : (wz > 8 ? 1 : 0);
+    const int ox = interior ? 0 : (q ? 1 : -1);
     const int nb = nbs[((oz + 1) * 3 + (oy + 1)) * 3 + ox + 1];
-    const int lx = wx - 1 - 8 * ox, ly = wy - 1 - 8 * oy, lz = wz - 1 - 8 * oz;
-    cp_async8(mw + (wz * 10 + wy) * 24 + wx, mass + ((long long)(nb < 0 ? s : nb) * 512 + (lz * 8 + ly) * 8 + lx),
-              nb >= 0);
+    const int ly = wy - 1 - 8 * oy, lz = wz - 1 - 8 * oz;
+    const double* src = mass + (long long)(nb < 0 ? s : nb) * 512 + (lz * 8 + ly) * 8;
+    if (interior)
+      cp_async16z(mw + row * 24 + 2 + 2 * q, src + 2 * q, nb >= 0);
+    else
+      cp_async8(mw + row * 24 + (q ? 10 : 1), src + (q ? 0 : 7), nb >= 0);
   }
   if (l > 0) {
     const double* src = lloc + ls * 2048;
@@ -883,9 +975,10 @@ __global__ void __launch_bounds__(kL2pThreads, 4) amr_l2p_kernel(const GLv* __re
   __syncthreads();
   // masses scaled by 2^d for the unit-spacing constant geometry (exact)
   const double sc1 = (double)(1LL << d);
-  for (int t = threadIdx.x; t < 1000; t += blockDim.x) {
-    double* m = mw + ((t / 100) * 10 + (t / 10) % 10) * 24 + t % 10;
-    *m = *m * sc1;
+  for (int t = threadIdx.x; t < 1200; t += blockDim.x) {  // the whole window (padding too)
+    double2* m = reinterpret_cast<double2*>(mw) + t;
+    const double2 v = *m;
+    *m = make_double2(v.x * sc1, v.y * sc1);
   }
   __syncthreads();
   const long long ncell = nslots * 512;
@@ -922,7 +1015,7 @@ __global__ void __launch_bounds__(kL2pThreads, 4) amr_l2p_kernel(const GLv* __re
                   oz = lz < 0 ? -1 : (lz > 7 ? 1 : 0);
         if (!((valid27 >> (((oz + 1) * 3 + (oy + 1)) * 3 + ox + 1)) & 1u)) continue;
         // -m 2^d and -m 2^2d against the unit geometry: p2p_geom's terms exactly
-        const double nm1 = -mw[((lz + 1) * 10 + (ly + 1)) * 24 + lx + 1], nm2 = nm1 * sc1;
+        const double nm1 = -mw[((lz + 1) * 10 + (ly + 1)) * 24 + lx + 2], nm2 = nm1 * sc1;
         const int o = ((dz + 1) * 3 + (dy + 1)) * 3 + dx + 1;
         p = fma(nm1, c_p2p_unit[o][0], p);
         gx = fma(nm2, c_p2p_unit[o][1], gx);
@@ -982,57 +1075,22 @@ __device__ __forceinline__ void cell_pos(const GLv* __restrict__ Lv, int l, int 
   x[2] = centre(8LL * L.ijk[3 * n + 2] + (c >> 6), d);
 }
 
-// one CTA (512 threads) = one slot: adjacent-pair tree over its 512 cells'
-// 16 values (warp shuffles, then one thread per value over the 16 warps)
-__device__ __forceinline__ void am_block_sums(double m, const double x[3], double gx, double gy,
-                                              double gz, double* __restrict__ out16) {
-  __shared__ double red[16][16];  // [warp][value]
-  const int c = threadIdx.x;
-  double v[16];
-  v[0] = m;
-  v[1] = m * x[0];
-  v[2] = m * x[1];
-  v[3] = m * x[2];
-  v[4] = m * gx;
-  v[5] = m * gy;
-  v[6] = m * gz;
-  v[7] = m * (x[1] * gz - x[2] * gy);
-  v[8] = m * (x[2] * gx - x[0] * gz);
-  v[9] = m * (x[0] * gy - x[1] * gx);
-  v[10] = v[1] * x[0];
-  v[11] = v[1] * x[1];
-  v[12] = v[1] * x[2];
-  v[13] = v[2] * x[1];
-  v[14] = v[2] * x[2];
-  v[15] = v[3] * x[2];
-  const int lane = c & 31, warp = c >> 5;
-#pragma unroll
-  for (int st = 1; st < 32; st <<= 1)
-#pragma unroll
-    for (int q = 0; q < 16; ++q) {
-      const double o = __shfl_down_sync(0xffffffffu, v[q], st);
-      if ((lane & (2 * st - 1)) == 0) v[q] = v[q] + o;
-    }
-  if (lane == 0)
-#pragma unroll
-    for (int q = 0; q < 16; ++q) red[warp][q] = v[q];
-  __syncthreads();
-  if (c < 16) {  // thread q: tree over the 16 warps for value q
-    double w[16];
-#pragma unroll
-    for (int a = 0; a < 16; ++a) w[a] = red[a][c];
-#pragma unroll
-    for (int st = 1; st < 16; st <<= 1)
-#pragma unroll
-      for (int a = 0; a < 16; a += 2 * st) w[a] = w[a] + w[a + st];
-    out16[c] = w[0];
-  }
+// The slot's 16 angular-momentum sums for 256 threads holding cells t and
+// t + 256: an adjacent-pair tree over the 512 cells in slot order (warp trees
+// over cells [32w, 32w + 32), then a tree over the 16 warp sums).
+// The warp tree is transposed: at level st the lane pair (l, l ^ st) holds the
+// same values for two adjacent subtrees; each lane keeps half of them and
+// receives the partner's half (8 + 4 + 2 + 1 shuffles, then one for the two
+// 16-lane halves) — every partial sum is the same (left subtree + right
+// subtree) as the plain tree's, and IEEE addition is commutative, so the sums
+// are bitwise the plain tree's with 16 shuffles instead of 80. Returns on
+// lanes 0..15 the warp sum of value am_lane_value(lane).
+__device__ __forceinline__ int am_lane_value(int lane) {
+  return ((lane & 1) << 3) | ((lane & 2) << 1) | ((lane & 4) >> 1) | ((lane & 8) >> 3);
 }
 
-// am_block_sums for 256 threads holding cells t and t + 256: the same
-// adjacent-pair tree (warp trees over cells [32w, 32w + 32), then the 16 warp
-// sums), the two halves' warp trees done one after the other
-__device__ __forceinline__ void am_warp_tree(double m, const double x[3], const double gg[3], double v[16]) {
+__device__ __forceinline__ double am_warp_tree(double m, const double x[3], const double gg[3]) {
+  double v[16];
   v[0] = m;
   v[1] = m * x[0];
   v[2] = m * x[1];
@@ -1049,29 +1107,39 @@ __device__ __forceinline__ void am_warp_tree(double m, const double x[3], const 
   v[13] = v[2] * x[1];
   v[14] = v[2] * x[2];
   v[15] = v[3] * x[2];
+  const unsigned full = 0xffffffffu;
   const int lane = threadIdx.x & 31;
+  double a[8], b[4], c[2];
+  const bool h1 = lane & 1, h2 = lane & 2, h4 = lane & 4, h8 = lane & 8;
 #pragma unroll
-  for (int st = 1; st < 32; st <<= 1)
+  for (int k = 0; k < 8; ++k) {
+    const double r = __shfl_xor_sync(full, h1 ? v[k] : v[8 + k], 1);
+    a[k] = (h1 ? v[8 + k] : v[k]) + r;
+  }
 #pragma unroll
-    for (int q = 0; q < 16; ++q) {
-      const double o = __shfl_down_sync(0xffffffffu, v[q], st);
-      if ((lane & (2 * st - 1)) == 0) v[q] = v[q] + o;
-    }
+  for (int k = 0; k < 4; ++k) {
+    const double r = __shfl_xor_sync(full, h2 ? a[k] : a[4 + k], 2);
+    b[k] = (h2 ? a[4 + k] : a[k]) + r;
+  }
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    const double r = __shfl_xor_sync(full, h4 ? b[k] : b[2 + k], 4);
+    c[k] = (h4 ? b[2 + k] : b[k]) + r;
+  }
+  const double d = (h8 ? c[1] : c[0]) + __shfl_xor_sync(full, h8 ? c[0] : c[1], 8);
+  return d + __shfl_xor_sync(full, d, 16);
 }
 
 __device__ __forceinline__ void am_block_sums2(double m0, const double x0[3], const double g0[3], double m1,
                                                const double x1[3], const double g1[3], double* __restrict__ out16) {
   __shared__ double red[16][16];  // [warp of 32 cells][value]
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  double v[16];
-  am_warp_tree(m0, x0, g0, v);
-  if (lane == 0)
-#pragma unroll
-    for (int q = 0; q < 16; ++q) red[warp][q] = v[q];
-  am_warp_tree(m1, x1, g1, v);
-  if (lane == 0)
-#pragma unroll
-    for (int q = 0; q < 16; ++q) red[warp + 8][q] = v[q];
+  const double s0 = am_warp_tree(m0, x0, g0);
+  const double s1 = am_warp_tree(m1, x1, g1);
+  if (lane < 16) {
+    red[warp][am_lane_value(lane)] = s0;
+    red[warp + 8][am_lane_value(lane)] = s1;
+  }
   __syncthreads();
   if (threadIdx.x < 16) {
     const int c = threadIdx.x;
@@ -1294,6 +1362,8 @@ struct GravAmrWork {
   double* dmom[3] = {nullptr, nullptr, nullptr};
   double* dloc[3] = {nullptr, nullptr, nullptr};
   double* tab = nullptr;
+  double* tabp = nullptr;   // tab in amr_m2l_fused_kernel's shared layout (pad_tables_kernel)
+  double* tab4p = nullptr;  // tab's monopole values in amr_m2l_mono_kernel's layout
   double* mass = nullptr;
   double* lloc = nullptr;   // [slot - lo][4][512] leaf locals L0, L_i (leaf patches only)
   double* p2p_tab = nullptr;  // [depth][27][4] same-depth P2P geometry
@@ -1339,6 +1409,7 @@ struct GravAmrWork {
   long long* wx_tflat = nullptr;
   long long wx_targets = 0;
   double* wx_geo = nullptr;  // [distinct W/X separations][13]
+  double* wx_geo4 = nullptr;  // the same rows' first 4 values (a leaf target's monopole term), 32-byte rows
   double* u_geo = nullptr;   // [distinct cross-depth U separations][4]
   cudaStream_t side = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
@@ -1802,6 +1873,13 @@ tmgpu_gravity_amr* tmgpu_gravity_amr_create(const int* leaves, long long nleaves
       g_launches.fetch_add(1, std::memory_order_relaxed);
       e = cudaDeviceSynchronize();
     }
+    if (e == cudaSuccess && kind == 0) {
+      e = cudaMalloc(&w.wx_geo4, (size_t)(ns ? ns : 1) * 4 * sizeof(double));
+      track(w.wx_geo4);
+      if (e == cudaSuccess && ns)
+        e = cudaMemcpy2D(w.wx_geo4, 4 * sizeof(double), w.wx_geo, kTab * sizeof(double), 4 * sizeof(double),
+                         (size_t)ns, cudaMemcpyDeviceToDevice);
+    }
     if (dsep) cudaFree(dsep);
   }
   if (e == cudaSuccess) e = cudaMalloc(&w.p2p_tab, (size_t)(Dmax + 1) * 27 * 4 * sizeof(double)), track(w.p2p_tab);
@@ -1811,7 +1889,15 @@ tmgpu_gravity_amr* tmgpu_gravity_amr_create(const int* leaves, long long nleaves
     e = cudaMemcpyToSymbol(c_p2p_unit, w.p2p_tab, 27 * 4 * sizeof(double), 0, cudaMemcpyDeviceToDevice);
     stencil_table_kernel<<<((Dmax + 1) * kOff3 + 127) / 128, 128>>>(w.tab, Dmax);
     g_launches.fetch_add(1, std::memory_order_relaxed);
-    e = cudaDeviceSynchronize();
+    e = cudaMalloc(&w.tabp, (size_t)(Dmax + 1) * kTabDoubles * sizeof(double));
+    track(w.tabp);
+    if (e == cudaSuccess) e = cudaMalloc(&w.tab4p, (size_t)(Dmax + 1) * kOff3 * 4 * sizeof(double)), track(w.tab4p);
+    if (e == cudaSuccess) {
+      pad_tables_kernel<<<(unsigned)(((long long)(Dmax + 1) * kTabDoubles + 255) / 256), 256>>>(w.tab, Dmax, w.tabp,
+                                                                                             w.tab4p);
+      g_launches.fetch_add(1, std::memory_order_relaxed);
+    }
+    if (e == cudaSuccess) e = cudaDeviceSynchronize();
   }
   if (e != cudaSuccess) {
     cuda_err(err, e, "tmgpu_gravity_amr_create");
@@ -1959,7 +2045,7 @@ int tmgpu_gravity_amr_solve(tmgpu_gravity_amr* G, const double* mass, double* ph
     cudaEventRecord(w.ev_fork2, st);
     cudaStreamWaitEvent(w.side2, w.ev_fork2, 0);
     amr_m2l_mono_kernel<<<(unsigned)w.mono_ctas, kM2lThreads, kMonoSmem, w.side2>>>(
-        w.mono_slots, w.slot_level, w.mass, w.slot_nbs, w.tab, w.lloc, w.lo);
+        w.mono_slots, w.slot_level, w.mass, w.slot_nbs, w.tab4p, w.lloc, w.lo);
     cudaEventRecord(w.ev_join2, w.side2);
     g_launches.fetch_add(1, std::memory_order_relaxed);
   }
@@ -2046,27 +2132,28 @@ int tmgpu_gravity_amr_solve(tmgpu_gravity_amr* G, const double* mass, double* ph
         cudaEventRecord(rec.k[0], st);
         if (w.mono_ctas)
           amr_m2l_mono_kernel<<<(unsigned)w.mono_ctas, kM2lThreads, kMonoSmem, st>>>(
-              w.mono_slots, w.slot_level, w.mass, w.slot_nbs, w.tab, w.lloc, w.lo);
+              w.mono_slots, w.slot_level, w.mass, w.slot_nbs, w.tab4p, w.lloc, w.lo);
         cudaEventRecord(rec.k[1], st);
         launches += w.mono_ctas ? 1 : 0;
       }
       if (w.m2l_ctas) {
         amr_m2l_fused_kernel<<<(unsigned)w.m2l_ctas, kM2lThreads, kM2lSmem, st>>>(w.dev_lv, w.m2l_work,
-                                                                                 w.tab, w.lloc, w.lo, lmass);
+                                                                                 w.tabp, w.lloc, w.lo, lmass);
         ++launches;
       }
       if (timed) cudaEventRecord(rec.k[2], st);
       if (w.mono_ctas && !mono_early && !timed) {  // leaf patches among leaf patches: monopole sources
         cudaStreamWaitEvent(w.side2, w.ev_fork, 0);
         amr_m2l_mono_kernel<<<(unsigned)w.mono_ctas, kM2lThreads, kMonoSmem, w.side2>>>(
-            w.mono_slots, w.slot_level, w.mass, w.slot_nbs, w.tab, w.lloc, w.lo);
+            w.mono_slots, w.slot_level, w.mass, w.slot_nbs, w.tab4p, w.lloc, w.lo);
         cudaEventRecord(w.ev_join2, w.side2);
         ++launches;
       }
       if (w.mono_ctas && !timed) cudaStreamWaitEvent(st, w.ev_join2, 0);
       if (w.wx_targets) {
         amr_wx_kernel<<<grid_for(w.wx_targets), 128, 0, st>>>(w.dev_lv, w.wx_tlev, w.wx_tflat,
-                                                              w.wx_targets, w.wx_geo, w.lloc, w.lo, lmass);
+                                                              w.wx_targets, w.wx_geo, w.lloc, w.lo, lmass,
+                                                              w.wx_geo4);
         ++launches;
       }
       if (timed) cudaEventRecord(rec.k[3], st);
