@@ -17,6 +17,15 @@
 
 using namespace tmgpu;
 
+constexpr int kGraphKey = 8;
+struct StepGraph {
+  uint64_t key[kGraphKey];
+  cudaGraphExec_t exec;
+  long long kernels;   // kernel nodes (the launch counter per replay)
+  int cur_after;       // arena parity after the step
+  uint64_t exchanges;  // ghost exchanges the step performs
+};
+
 struct tmgpu_forest {
   explicit tmgpu_forest(const ForestConfig& c) : forest(c) {}
   Forest forest;
@@ -110,6 +119,12 @@ struct tmgpu_forest {
   cudaEvent_t ev[8] = {};
   double t_cfl = 0, t_exchange = 0, t_stage = 0;
   long long timed_steps = 0, pending_timed = 0;
+  // CUDA graphs of the step (step_graph), dropped by graph_reset
+  std::vector<StepGraph> graphs;
+  cudaStream_t graph_stream = nullptr;
+  cudaEvent_t gev_in = nullptr, gev_out = nullptr;
+  bool graph_warm = false;  // one step ran outside a capture (kernel attributes set)
+  int graph_captures = 0;   // a caller varying dt every step stops capturing after 32
   int world() const { return comm_world(comm); }
   int rank() const { return comm_rank(comm); }
 };
@@ -162,7 +177,14 @@ void peer_close(tmgpu_forest* f, bool collective = false) {
   f->peer_seq = 0;
 }
 
+// Drop the cached step graphs (whatever a step enqueues is about to change).
+void graph_reset(tmgpu_forest* f) {
+  for (auto& g : f->graphs) cudaGraphExecDestroy(g.exec);
+  f->graphs.clear();
+}
+
 void free_dev(tmgpu_forest* f) {
+  graph_reset(f);
   peer_close(f);
   auto fr = [](void* p) {
     if (p) cudaFree(p);
@@ -434,6 +456,9 @@ void tmgpu_forest_destroy(tmgpu_forest* f) {
   free_dev(f);
   tmgpu_forest_set_reflux(f, 0, nullptr);
   if (f->scratch) cudaFree(f->scratch);
+  if (f->graph_stream) cudaStreamDestroy(f->graph_stream);
+  if (f->gev_in) cudaEventDestroy(f->gev_in);
+  if (f->gev_out) cudaEventDestroy(f->gev_out);
   if (f->ev_grav) cudaEventDestroy(f->ev_grav);
   if (f->ev_fork) cudaEventDestroy(f->ev_fork);
   if (f->side) cudaStreamDestroy(f->side);
@@ -637,6 +662,7 @@ int tmgpu_forest_scenario_fill(tmgpu_forest* f, int kind, uint64_t seed, double*
 int tmgpu_forest_distribute(tmgpu_forest* f, tmgpu_comm* comm, const int* owner, size_t n,
                             tmgpu_error* err) {
   if (err) std::memset(err, 0, sizeof(*err));
+  if (f) graph_reset(f);  // what a step enqueues changes
   if (n != f->forest.leaves().size())
     return fail(err, TMGPU_ERR_INVALID, "owner list does not match the leaf count");
   const int world = comm_world(comm);
@@ -779,6 +805,7 @@ int tmgpu_forest_max_wavespeed(tmgpu_forest* f, double gamma, double* per_leaf_h
 int tmgpu_forest_set_gravity(tmgpu_forest* f, const double* g, long long comp_stride,
                              tmgpu_error* err) {
   if (err) std::memset(err, 0, sizeof(*err));
+  if (f) graph_reset(f);  // what a step enqueues changes
   if (g && comp_stride < f->nslots * 512)
     return set_err(err, TMGPU_ERR_INVALID, "gravity: component stride below the local cell count");
   f->grav = g;
@@ -790,6 +817,7 @@ int tmgpu_forest_set_gravity_solver(tmgpu_forest* f, tmgpu_gravity_amr* G, int s
                                     int grav_flags, double* phi, double* g, double* g2,
                                     double* rho_tilde, long long comp_stride, tmgpu_error* err) {
   if (err) std::memset(err, 0, sizeof(*err));
+  if (f) graph_reset(f);  // what a step enqueues changes
   if (!f) return fail(err, TMGPU_ERR_INVALID, "null forest");
   if (!G) {
     f->gsolver = nullptr;
@@ -849,23 +877,16 @@ int tmgpu_forest_step(tmgpu_forest* f, double dt, double cfl, double gamma, int 
   return tmgpu_forest_step_io(f, nullptr, nullptr, dt, cfl, gamma, flags, stream, dt_used, err);
 }
 
-int tmgpu_forest_step_io(tmgpu_forest* f, const double* in_compact, double* out_compact, double dt,
-                         double cfl, double gamma, int flags, void* stream, double* dt_used,
-                         tmgpu_error* err) {
-  if (err) std::memset(err, 0, sizeof(*err));
-  if (int rc = ready(f, err)) return rc;
+namespace {
+// Everything one step enqueues on `st` (and the streams it forks), from the
+// first gravity solve to the output gather; host state it changes: f->cur,
+// f->exchanges. Captured whole into a CUDA graph by step_graph.
+int step_enqueue(tmgpu_forest* f, const double* in_compact, double* out_compact, double dt, double cfl,
+                 double gamma, int flags, cudaStream_t st, tmgpu_error* err) {
   const int V = f->forest.config().vars;
-  if (V != 5) return fail(err, TMGPU_ERR_INVALID, "the hydro step is Euler (vars 5)");
-  cudaStream_t st = as_stream(stream);
-  cudaError_t e = cudaSuccess;
   const int cadence = f->gsolver ? f->g_cadence : 0;
-  if (cadence == 6 && (flags & TMGPU_EXACT_GHOSTS))
-    return fail(err, TMGPU_ERR_INVALID, "the 6-solve gravity cadence needs the fused (ping-pong) step");
   const bool timed = f->timing;
-  if (timed) {
-    collect_timing(f);  // events are reused: fold the previous step in first
-    cudaEventRecord(f->ev[0], st);
-  }
+  cudaError_t e = cudaSuccess;
   if (cadence) {  // stage 1's solve on the step's initial state, overlapping the CFL and exchange
     const int rc = in_compact ? grav_solve(f, st, nullptr, in_compact, f->g_a, err, (long long)V * 512)
                               : grav_solve(f, st, f->arena(), nullptr, f->g_a, err);
@@ -1016,8 +1037,125 @@ int tmgpu_forest_step_io(tmgpu_forest* f, const double* in_compact, double* out_
   }
   if (e == cudaSuccess && out_compact && late_fix)
     e = interior_copy(f->arena(), out_compact, V, f->nslots, false, st);
-  if (timed && e == cudaSuccess) f->pending_timed = 1;
   if (e != cudaSuccess) return cuda_err(err, e, "tmgpu_forest_step");
+  return TMGPU_OK;
+}
+
+// The step as a CUDA graph (one GPU): captured once per distinct launch
+// (arena parity, input/output buffers, dt, cfl, gamma, flags) on the forest's
+// graph stream and replayed there, fenced to the caller's stream by events;
+// a replay applies the host-side effects the capture recorded (f->cur,
+// f->exchanges, the launch counter). Any setter that changes what a step
+// enqueues drops the cached graphs (graph_reset).
+int step_graph(tmgpu_forest* f, const double* in_compact, double* out_compact, double dt, double cfl,
+               double gamma, int flags, cudaStream_t st, tmgpu_error* err) {
+  auto bits = [](double x) {
+    uint64_t u;
+    std::memcpy(&u, &x, 8);
+    return u;
+  };
+  const uint64_t key[kGraphKey] = {(uint64_t)f->cur, (uint64_t)(uintptr_t)in_compact,
+                                   (uint64_t)(uintptr_t)out_compact, cfl > 0.0 ? 0 : bits(dt), bits(cfl), bits(gamma),
+                                   (uint64_t)(unsigned)flags, f->forest.topology_version()};
+  cudaError_t e = cudaSuccess;
+  if (!f->graph_stream) {
+    e = cudaStreamCreateWithFlags(&f->graph_stream, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&f->gev_in, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&f->gev_out, cudaEventDisableTiming);
+    if (e != cudaSuccess) return cuda_err(err, e, "tmgpu_forest_step: graph stream");
+  }
+  StepGraph* g = nullptr;
+  for (auto& x : f->graphs)
+    if (std::equal(key, key + kGraphKey, x.key)) g = &x;
+  if (!g) {
+    ++f->graph_captures;
+    const int cur0 = f->cur;
+    const uint64_t ex0 = f->exchanges, l0 = g_launches.load();
+    e = cudaStreamBeginCapture(f->graph_stream, cudaStreamCaptureModeThreadLocal);
+    if (e != cudaSuccess) return cuda_err(err, e, "tmgpu_forest_step: begin capture");
+    const int rc = step_enqueue(f, in_compact, out_compact, dt, cfl, gamma, flags, f->graph_stream, err);
+    cudaGraph_t graph = nullptr;
+    e = cudaStreamEndCapture(f->graph_stream, &graph);
+    StepGraph sg{};
+    std::copy(key, key + kGraphKey, sg.key);
+    sg.cur_after = f->cur;
+    sg.exchanges = f->exchanges - ex0;
+    f->cur = cur0;  // nothing ran yet
+    f->exchanges = ex0;
+    g_launches.fetch_sub(g_launches.load() - l0);  // counted per replay below
+    if (rc != TMGPU_OK || e != cudaSuccess) {
+      if (graph) cudaGraphDestroy(graph);
+      return rc != TMGPU_OK ? rc : cuda_err(err, e, "tmgpu_forest_step: end capture");
+    }
+    size_t n = 0;
+    e = cudaGraphGetNodes(graph, nullptr, &n);
+    std::vector<cudaGraphNode_t> nodes(n);
+    if (e == cudaSuccess && n) e = cudaGraphGetNodes(graph, nodes.data(), &n);
+    for (size_t q = 0; q < n && e == cudaSuccess; ++q) {
+      cudaGraphNodeType t;
+      e = cudaGraphNodeGetType(nodes[q], &t);
+      sg.kernels += t == cudaGraphNodeTypeKernel;
+    }
+    // each kernel node keeps the priority of the stream it was captured from
+    // (the gravity stream's high priority lets the up pass win over the early
+    // mono M2L, as in the stream path)
+    if (e == cudaSuccess) e = cudaGraphInstantiate(&sg.exec, graph, cudaGraphInstantiateFlagUseNodePriority);
+    cudaGraphDestroy(graph);
+    if (e != cudaSuccess) return cuda_err(err, e, "tmgpu_forest_step: graph instantiate");
+    if (f->graphs.size() >= 8) {  // bounded cache: drop the oldest
+      cudaGraphExecDestroy(f->graphs.front().exec);
+      f->graphs.erase(f->graphs.begin());
+    }
+    f->graphs.push_back(sg);
+    g = &f->graphs.back();
+  }
+  e = cudaEventRecord(f->gev_in, st);
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(f->graph_stream, f->gev_in, 0);
+  if (e == cudaSuccess) e = cudaGraphLaunch(g->exec, f->graph_stream);
+  if (e == cudaSuccess) e = cudaEventRecord(f->gev_out, f->graph_stream);
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(st, f->gev_out, 0);
+  if (e != cudaSuccess) return cuda_err(err, e, "tmgpu_forest_step: graph launch");
+  f->cur = g->cur_after;
+  f->exchanges += g->exchanges;
+  g_launches.fetch_add(g->kernels, std::memory_order_relaxed);
+  return TMGPU_OK;
+}
+}  // namespace
+
+int tmgpu_forest_step_io(tmgpu_forest* f, const double* in_compact, double* out_compact, double dt,
+                         double cfl, double gamma, int flags, void* stream, double* dt_used,
+                         tmgpu_error* err) {
+  if (err) std::memset(err, 0, sizeof(*err));
+  if (int rc = ready(f, err)) return rc;
+  const int V = f->forest.config().vars;
+  if (V != 5) return fail(err, TMGPU_ERR_INVALID, "the hydro step is Euler (vars 5)");
+  cudaStream_t st = as_stream(stream);
+  cudaError_t e = cudaSuccess;
+  const int cadence = f->gsolver ? f->g_cadence : 0;
+  if (cadence == 6 && (flags & TMGPU_EXACT_GHOSTS))
+    return fail(err, TMGPU_ERR_INVALID, "the 6-solve gravity cadence needs the fused (ping-pong) step");
+  const bool timed = f->timing;
+  if (timed) {
+    collect_timing(f);  // events are reused: fold the previous step in first
+    cudaEventRecord(f->ev[0], st);
+  }
+  // CUDA graph of the step on one GPU once the kernels have run (their
+  // one-time attribute setup is outside any capture): TMGPU_GRAPHS=0 disables
+  static const bool graphs_env = [] {
+    const char* v = std::getenv("TMGPU_GRAPHS");
+    return !(v && v[0] == '0');
+  }();
+  const bool use_graph = graphs_env && f->graph_warm && f->graph_captures < 32 && !timed && f->world() == 1 &&
+                         !f->peer &&
+                         (!f->gsolver || tmgpu_gravity_amr_graph_safe(f->gsolver)) &&
+                         (cadence || !f->grav_stream);
+  {
+    const int rc = use_graph ? step_graph(f, in_compact, out_compact, dt, cfl, gamma, flags, st, err)
+                             : step_enqueue(f, in_compact, out_compact, dt, cfl, gamma, flags, st, err);
+    if (rc != TMGPU_OK) return rc;
+  }
+  f->graph_warm = true;
+  if (timed) f->pending_timed = 1;
   if (flags & TMGPU_ASYNC) return TMGPU_OK;
   unsigned long long w = ~0ull;
   double dtv = dt;
@@ -1051,6 +1189,7 @@ int tmgpu_stream_wait(void* waiter, void* signaller) {
 // Re-call after tmgpu_forest_alloc (a new topology or distribution).
 int tmgpu_forest_set_peer(tmgpu_forest* f, int on, tmgpu_error* err) {
   if (err) std::memset(err, 0, sizeof(*err));
+  if (f) graph_reset(f);  // what a step enqueues changes
   if (int rc = ready(f, err)) return rc;
   peer_close(f, /*collective=*/true);
   if (!on) return TMGPU_OK;
@@ -1152,6 +1291,7 @@ int tmgpu_forest_set_peer(tmgpu_forest* f, int on, tmgpu_error* err) {
 // step): the step overlaps its CFL reduction and first exchange with it.
 int tmgpu_forest_set_gravity_stream(tmgpu_forest* f, void* stream, tmgpu_error* err) {
   if (err) std::memset(err, 0, sizeof(*err));
+  if (f) graph_reset(f);  // what a step enqueues changes
   if (!f) return fail(err, TMGPU_ERR_INVALID, "null forest");
   if (!f->ev_grav) {
     cudaError_t e = cudaEventCreateWithFlags(&f->ev_grav, cudaEventDisableTiming);
@@ -1165,6 +1305,7 @@ int tmgpu_forest_set_gravity_stream(tmgpu_forest* f, void* stream, tmgpu_error* 
 // SPEC.md:383-391 / flux_register.hpp; single GPU). on = 0 turns it off.
 int tmgpu_forest_set_reflux(tmgpu_forest* f, int on, tmgpu_error* err) {
   if (err) std::memset(err, 0, sizeof(*err));
+  if (f) graph_reset(f);  // what a step enqueues changes
   if (int rc = ready(f, err)) return rc;
   auto drop = [](int*& p) {
     if (p) cudaFree(p);
@@ -1279,6 +1420,7 @@ int tmgpu_forest_set_reflux(tmgpu_forest* f, int on, tmgpu_error* err) {
 // exchanges and the stage kernels.
 int tmgpu_forest_set_timing(tmgpu_forest* f, int on, tmgpu_error* err) {
   if (err) std::memset(err, 0, sizeof(*err));
+  if (f) graph_reset(f);  // what a step enqueues changes
   if (on && !f->ev[0])
     for (auto& e : f->ev) cudaEventCreate(&e);
   f->timing = on != 0;

@@ -2467,6 +2467,12 @@ int tmgpu_gravity_amr_timing(tmgpu_gravity_amr* G, double* ms, long long* solves
   return TMGPU_OK;
 }
 
+// Whether a solve enqueues the same work every call with no host-side state
+// (so a CUDA graph may capture it): not timing, not distributed.
+bool tmgpu_gravity_amr_graph_safe(const tmgpu_gravity_amr* G) {
+  return G && !G->w.timing && !G->w.let && !G->w.peer;
+}
+
 // Leaf-cell masses currently in the workspace ([slot][512], device pointer).
 const double* tmgpu_gravity_amr_mass_ptr(const tmgpu_gravity_amr* G) { return G ? G->w.mass : nullptr; }
 

@@ -7,6 +7,8 @@
 
 #include <mutex>
 
+#include <cstdlib>
+
 #include "stage_kernel.cuh"
 #include "tmgpu_internal.h"
 
@@ -40,7 +42,15 @@ cudaError_t launch_stage_t(const StageMaps& m, const StageLaunch& p, cudaStream_
   });
   if (attr_err != cudaSuccess) return attr_err;
   if (p.count <= 0) return cudaSuccess;
-  stage_kernel<V, FAST><<<p.count, kStageThreads, Lay<V>::kBytes, stream>>>(m.i, m.x, m.y, m.z, p);
+  static const int ahead = [] {  // two resident CTAs per SM: one wave ahead
+    if (const char* v = std::getenv("TMGPU_STAGE_PREFETCH")) return std::atoi(v);
+    int dev = 0, sms = 148;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    return 2 * sms;
+  }();
+  StageLaunch q = p;
+  q.prefetch_ahead = ahead;
+  stage_kernel<V, FAST><<<p.count, kStageThreads, Lay<V>::kBytes, stream>>>(m.i, m.x, m.y, m.z, q);
   g_launches.fetch_add(1, std::memory_order_relaxed);
   return cudaGetLastError();
 }

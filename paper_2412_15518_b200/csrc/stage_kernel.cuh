@@ -117,6 +117,19 @@ __device__ __forceinline__ void tma_load_5d(void* dst, const CUtensorMap* map, u
       : "memory");
 }
 
+__device__ __forceinline__ void tma_prefetch_5d(const CUtensorMap* map, int c0, int c1, int c2, int c3,
+                                                int c4) {
+  asm volatile("cp.async.bulk.prefetch.tensor.5d.L2.global.tile [%0, {%1, %2, %3, %4, %5}];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4)
+               : "memory");
+}
+
+__device__ __forceinline__ void bulk_prefetch(const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(reinterpret_cast<uint64_t>(src)), "r"(bytes)
+               : "memory");
+}
+
 __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes,
                                           uint64_t* bar) {
   asm volatile(
@@ -495,6 +508,28 @@ __global__ void __launch_bounds__(kStageThreads, 2)
       int c[3] = {kG, kG, kG};
       c[axis] = ca;
       tma_load_5d(sm + off[f], fm[axis], bar, c[0], c[1], c[2], 0, src);
+    }
+    // the same boxes of the CTA one resident wave ahead, into L2
+    if (p.prefetch_ahead > 0 && s + p.prefetch_ahead < p.count) {
+      const int sa = s + p.prefetch_ahead;
+      const int slot_a = p.index ? p.index[sa] : sa;
+      if (want_u0) bulk_prefetch(p.u0 + (long long)slot_a * p.u0_stride, V * kE3 * 8);
+      tma_prefetch_5d(&tm_i, 2, 2, 2, 0, slot_a);
+#pragma unroll
+      for (int f = 0; f < 6; ++f) {
+        const int axis = f >> 1, side = f & 1;
+        int src = slot_a, ca;
+        const int code = p.face_src ? p.face_src[(long long)slot_a * 6 + f] : (slot_a << 1);
+        if (code & 1) {
+          src = code >> 1;
+          ca = side ? kG : kE;
+        } else {
+          ca = side ? kG + kE : 0;
+        }
+        int c[3] = {kG, kG, kG};
+        c[axis] = ca;
+        tma_prefetch_5d(fm[axis], c[0], c[1], c[2], 0, src);
+      }
     }
   }
 

@@ -12,6 +12,10 @@
 
 #include "../../include/tmgpu.h"
 
+// gravity_amr.cu: may a CUDA graph capture this solver's solve (no host-side
+// state per call: not timing, not distributed)?
+extern "C" bool tmgpu_gravity_amr_graph_safe(const tmgpu_gravity_amr* G);
+
 namespace tmgpu {
 
 // Per-launch arguments of the aggregated stage kernel (stage_kernel.cuh).
@@ -61,6 +65,10 @@ struct StageLaunch {
   double* out_compact;
   unsigned long long* err;  // atomicMin of (slice << 32 | var-major interior index)
   int count;
+  // L2 prefetch distance in CTAs (set by launch_stage_t): CTA b also prefetches
+  // the boxes of CTA b + prefetch_ahead, which starts about one resident wave
+  // later, so its TMA loads hit L2 (0: off)
+  int prefetch_ahead;
 };
 
 // Number of kernels this library launched since load.

@@ -51,6 +51,19 @@ G.set_timing(False)
 print("phases ms/solve:", {k: round(v / ns, 4) for k, v in tot.items()})
 hd = HydroDriver(f)
 print(f"hydro step: {timed(lambda: hd.step(sync=False), reps):.3f} ms")
+import ctypes as C  # noqa: E402
+from paper_2412_15518_b200 import _lib  # noqa: E402
+L = _lib.lib
+L.tmgpu_forest_set_timing.argtypes = [C.c_void_p, C.c_int, C.c_void_p]
+L.tmgpu_forest_timing.argtypes = [C.c_void_p] + [C.POINTER(C.c_double)] * 3 + [C.POINTER(C.c_longlong)]
+L.tmgpu_forest_set_timing(f.h, 1, None)
+for _ in range(reps):
+    hd.step(sync=False)
+torch.cuda.synchronize()
+tc, te, ts, nst = C.c_double(), C.c_double(), C.c_double(), C.c_longlong()
+L.tmgpu_forest_timing(f.h, C.byref(tc), C.byref(te), C.byref(ts), C.byref(nst))
+L.tmgpu_forest_set_timing(f.h, 0, None)
+print(f"stage launch: {ts.value / (3 * max(nst.value, 1)):.4f} ms  exchange: {te.value / (3 * max(nst.value, 1)):.4f} ms")
 for sps in (1, 3, 6):
     gd = GravityHydroDriver(f, solves_per_step=sps)
     print(f"gravity+hydro step ({sps} solves): {timed(lambda: gd.step(sync=False), reps):.3f} ms")
