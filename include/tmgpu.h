@@ -43,6 +43,7 @@ typedef struct tmgpu_error {
 #define TMGPU_ASYNC 0x4      /* enqueue only; errors latched until tmgpu_forest_check */
 #define TMGPU_EXACT_GHOSTS 0x8 /* step: reference 3-pass full-shell exchange instead of one-round faces */
 #define TMGPU_OVERLAP 0x10   /* multi-GPU step: overlap the NCCL halo with the interior leaves' stage */
+#define TMGPU_NO_GRAPH 0x20  /* step: enqueue directly (one GPU replays the step as a cached CUDA graph) */
 #define TMGPU_GRAV_AM 0x100  /* gravity: angular-momentum correction (rigid-rotation field) */
 
 /* ---------------------------------------------------------------- hydro

@@ -26,6 +26,7 @@ TMGPU_ASYNC = 0x4
 TMGPU_EXACT_GHOSTS = 0x8
 TMGPU_GRAV_AM = 0x100
 TMGPU_OVERLAP = 0x10
+TMGPU_NO_GRAPH = 0x20
 
 
 class TmgpuError(C.Structure):

@@ -1145,7 +1145,7 @@ int tmgpu_forest_step_io(tmgpu_forest* f, const double* in_compact, double* out_
     const char* v = std::getenv("TMGPU_GRAPHS");
     return !(v && v[0] == '0');
   }();
-  const bool use_graph = graphs_env && f->graph_warm && f->graph_captures < 32 && !timed && f->world() == 1 &&
+  const bool use_graph = graphs_env && !(flags & TMGPU_NO_GRAPH) && f->graph_warm && f->graph_captures < 32 && !timed && f->world() == 1 &&
                          !f->peer &&
                          (!f->gsolver || tmgpu_gravity_amr_graph_safe(f->gsolver)) &&
                          (cadence || !f->grav_stream);

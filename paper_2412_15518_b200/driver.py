@@ -37,6 +37,7 @@ class HydroDriver:
         are exchanged after every stage (the same bits as one GPU)."""
         self.forest, self.gamma, self.cfl, self.fast = forest, gamma, cfl, fast
         self.exact_ghosts = exact_ghosts
+        self.graph = True  # one GPU: the step replays as a cached CUDA graph (False: direct enqueue)
         self.steps = 0
         self.reflux = reflux
         if reflux:
@@ -50,7 +51,8 @@ class HydroDriver:
         compact interiors [local][V][E^3] in device memory (tensors or None) —
         scattered / gathered inside the step's own passes (tmgpu_forest_step_io)."""
         flags = ((_lib.TMGPU_FAST if self.fast else 0) | (0 if sync else _lib.TMGPU_ASYNC) |
-                 (_lib.TMGPU_EXACT_GHOSTS if self.exact_ghosts else 0))
+                 (_lib.TMGPU_EXACT_GHOSTS if self.exact_ghosts else 0) |
+                 (0 if self.graph else _lib.TMGPU_NO_GRAPH))
         used = C.c_double(0.0)
         err = TmgpuError()
         din, dout = io if io is not None else (None, None)
