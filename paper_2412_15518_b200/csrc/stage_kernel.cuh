@@ -71,9 +71,12 @@ struct Lay {
   static constexpr int ZH = ZL + V * 128;
   static constexpr int kStaged = ZH + V * 128;  // = V*1408 doubles
   static constexpr int kAcc = kStaged;          // accumulator [V][64 rows][9] (acc_at)
-  static constexpr int kU0 = kAcc + V * kAccV;   // RK3 u0 block [V][E^3] (bulk-copied)
-  static constexpr int kDoubles = kU0 + V * kE3;
-  static constexpr int kBytes = kDoubles * 8 + 64;  // + mbarrier/scratch
+  // RK3 u0 block [V][E^3]: bulk-copied over the x and y face slabs (XL..YH,
+  // exactly V*512 doubles, contiguous) once the y pass has read them
+  static constexpr int kU0 = XL;
+  static_assert(YH + V * 128 - XL == V * kE3, "u0 fits the x/y face slabs");
+  static constexpr int kDoubles = kAcc + V * kAccV;
+  static constexpr int kBytes = kDoubles * 8 + 64;  // + mbarriers/scratch
   static constexpr uint32_t kTxBytes = (uint32_t)(V * 1408 * 8);
 };
 
@@ -167,6 +170,21 @@ __device__ __forceinline__ double div_rn(double a, double b, double y, bool b_ok
   const double q2 = fma(r, y, q);
   return (b_ok && exp_ok(a) && exp_ok(q2)) ? q2 : a / b;
 }
+// The same with a divisor of moderate magnitude: b and y = RN(1/b) in
+// [2^-60, 2^61) (b_narrow, checked once per divisor) and a in [2^-900, 2^900)
+// keep q, r and q2 in (2^-961, 2^961) — no over/underflow anywhere — so the
+// quotient's own range check is implied and dropped. Used for the gamma - 1
+// divisions (per launch) and the cons -> prim divisions by rho (per cell).
+__device__ __forceinline__ bool exp_narrow(double x) {
+  const unsigned e = ((unsigned)__double2hiint(x) >> 20) & 0x7ffu;
+  return (e - 963u) < 121u;
+}
+__device__ __forceinline__ double div_rn_n(double a, double b, double y, bool b_narrow) {
+  const double q = a * y;
+  const double r = fma(-q, b, a);
+  const double q2 = fma(r, y, q);
+  return (b_narrow && exp_ok(a)) ? q2 : a / b;
+}
 
 // euler.hpp:27-35
 __device__ __forceinline__ void recon(double um1, double u0, double up1, double up2, double& l,
@@ -187,9 +205,9 @@ __device__ __forceinline__ void rusanov(const double (&ql)[5], const double (&qr
   if constexpr (!FAST) {
     cl = sqrt(gamma * ql[4] / ql[0]);
     cr = sqrt(gamma * qr[4] / qr[0]);
-    el = div_rn(ql[4], gm1, inv_gm1, gm1_ok) +
+    el = div_rn_n(ql[4], gm1, inv_gm1, gm1_ok) +
          0.5 * ql[0] * (ql[1] * ql[1] + ql[2] * ql[2] + ql[3] * ql[3]);
-    er = div_rn(qr[4], gm1, inv_gm1, gm1_ok) +
+    er = div_rn_n(qr[4], gm1, inv_gm1, gm1_ok) +
          0.5 * qr[0] * (qr[1] * qr[1] + qr[2] * qr[2] + qr[3] * qr[3]);
   } else {
     cl = sqrt(gamma * ql[4] * __drcp_rn(ql[0]));
@@ -298,11 +316,14 @@ __device__ __forceinline__ int interior_index(int axis, int c0, int c1, int c2) 
 
 // One axis of the stage: fluxes of 3 faces per lane, boundary-face record,
 // then (after the barrier) the divergence update of the lane's cells.
+// After the y pass's barrier the x/y face slabs are dead: `u0_src` (when
+// non-null) is bulk-copied over them on `u0_bar`, in flight during the z pass.
 template <int V, int AXIS, bool FAST, bool EULER>
 __device__ __forceinline__ void axis_pass(const double* __restrict__ sm, double* __restrict__ acc,
                                           int tid, double gamma, double gm1, double inv_gm1,
                                           bool gm1_ok, double a_vel, double cdt,
-                                          double* faces_out) {
+                                          double* faces_out, const double* u0_src = nullptr,
+                                          uint64_t* u0_bar = nullptr) {
   int c1, c2, r, nb;
   const bool active = face_map<AXIS>(tid, c1, c2, r, nb);
   double F[3][V];
@@ -382,6 +403,12 @@ __device__ __forceinline__ void axis_pass(const double* __restrict__ sm, double*
     D[2][v] = nxt - F[2][v];
   }
   __syncthreads();  // previous axis' updates of every cell are complete
+  if (AXIS == 1 && u0_src && tid == 0) {
+    // the slabs' last generic reads are ordered before the async-proxy writes
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    mbar_expect_tx(u0_bar, (uint32_t)(V * kE3 * 8));
+    bulk_load(const_cast<double*>(sm) + Lay<V>::kU0, u0_src, V * kE3 * 8, u0_bar);
+  }
   if (active) {
     const int ncell = r == 2 ? 2 : 3;
 #pragma unroll
@@ -476,6 +503,8 @@ __global__ void __launch_bounds__(kStageThreads, 2)
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + L::kDoubles);
   unsigned int& s_hits = *reinterpret_cast<unsigned int*>(smem + L::kDoubles + 1);
   unsigned int& s_bad = *(reinterpret_cast<unsigned int*>(smem + L::kDoubles + 1) + 1);
+  uint64_t* bar_u0 = reinterpret_cast<uint64_t*>(smem + L::kDoubles + 2);
+  const bool want_u0 = p.u0 && p.rk_stage >= 2 && !p.defer;
 
   const int tid = threadIdx.x;
   const int s = blockIdx.x;
@@ -485,10 +514,8 @@ __global__ void __launch_bounds__(kStageThreads, 2)
     s_hits = 0;
     s_bad = 0xffffffffu;
     mbar_init(bar, 1);
-    const bool want_u0 = p.u0 && p.rk_stage >= 2 && !p.defer;
-    mbar_expect_tx(bar, L::kTxBytes + (want_u0 ? (uint32_t)(V * kE3 * 8) : 0u));
-    if (want_u0)  // u0 block rides the same barrier; consumed in the epilogue
-      bulk_load(smem + L::kU0, p.u0 + (long long)slot * p.u0_stride, V * kE3 * 8, bar);
+    mbar_init(bar_u0, 1);
+    mbar_expect_tx(bar, L::kTxBytes);
     tma_load_5d(sm + L::B0, &tm_i, bar, 2, 2, 2, 0, slot);
     // face f = 2*axis + side; own ghost layer or the same-level neighbour's
     // adjacent interior layers (ghost.cpp:40-68 same-slab, fused)
@@ -557,7 +584,7 @@ __global__ void __launch_bounds__(kStageThreads, 2)
   const double cdt = dt / dx;
   const double gm1 = gamma - 1.0;
   const double inv_gm1 = 1.0 / gm1;  // RN(1/(gamma-1)) for div_rn
-  const bool gm1_ok = exp_ok(gm1) && exp_ok(inv_gm1);
+  const bool gm1_ok = exp_narrow(gm1) && exp_narrow(inv_gm1);  // div_rn_n's divisor condition
 
   __syncthreads();  // barrier init visible
   mbar_wait(bar, 0);
@@ -593,10 +620,10 @@ __global__ void __launch_bounds__(kStageThreads, 2)
         double iu, iv, iw, ke, pr;
         if constexpr (!FAST) {
           const double yr = __drcp_rn(rho);  // RN(1/rho)
-          const bool rok = exp_ok(rho) && exp_ok(yr);
-          iu = div_rn(u[1], rho, yr, rok);
-          iv = div_rn(u[2], rho, yr, rok);
-          iw = div_rn(u[3], rho, yr, rok);
+          const bool rok = exp_narrow(rho) && exp_narrow(yr);
+          iu = div_rn_n(u[1], rho, yr, rok);
+          iv = div_rn_n(u[2], rho, yr, rok);
+          iw = div_rn_n(u[3], rho, yr, rok);
           ke = 0.5 * rho * (iu * iu + iv * iv + iw * iw);
           pr = stdmax_(gm1 * (u[4] - ke), kPressureFloor);
         } else {
@@ -619,13 +646,15 @@ __global__ void __launch_bounds__(kStageThreads, 2)
 
   // ---- phase 3: x, y, z passes
   double* faces_out = p.faces ? p.faces + (long long)slot * p.faces_stride : nullptr;
+  const double* u0_src = want_u0 ? p.u0 + (long long)slot * p.u0_stride : nullptr;
   if (V == 5 && euler) {
     axis_pass<V, 0, FAST, (V == 5)>(sm, acc, tid, gamma, gm1, inv_gm1, gm1_ok, 0.0, cdt, faces_out);
-    axis_pass<V, 1, FAST, (V == 5)>(sm, acc, tid, gamma, gm1, inv_gm1, gm1_ok, 0.0, cdt, faces_out);
+    axis_pass<V, 1, FAST, (V == 5)>(sm, acc, tid, gamma, gm1, inv_gm1, gm1_ok, 0.0, cdt, faces_out, u0_src,
+                                    bar_u0);
     axis_pass<V, 2, FAST, (V == 5)>(sm, acc, tid, gamma, gm1, inv_gm1, gm1_ok, 0.0, cdt, faces_out);
   } else {
     axis_pass<V, 0, FAST, false>(sm, acc, tid, gamma, gm1, inv_gm1, gm1_ok, ax, cdt, faces_out);
-    axis_pass<V, 1, FAST, false>(sm, acc, tid, gamma, gm1, inv_gm1, gm1_ok, ay, cdt, faces_out);
+    axis_pass<V, 1, FAST, false>(sm, acc, tid, gamma, gm1, inv_gm1, gm1_ok, ay, cdt, faces_out, u0_src, bar_u0);
     axis_pass<V, 2, FAST, false>(sm, acc, tid, gamma, gm1, inv_gm1, gm1_ok, az, cdt, faces_out);
   }
   __syncthreads();
@@ -641,7 +670,8 @@ __global__ void __launch_bounds__(kStageThreads, 2)
     return;
   }
   unsigned int hits = 0, bad = 0xffffffffu;
-  const double* u0p = (p.u0 && p.rk_stage >= 2) ? smem + L::kU0 : nullptr;
+  const double* u0p = want_u0 ? smem + L::kU0 : nullptr;
+  if (want_u0) mbar_wait(bar_u0, 0);
   for (int c = tid; c < kE3; c += kStageThreads) {
     double u[V];
 #pragma unroll
