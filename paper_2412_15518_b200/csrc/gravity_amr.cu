@@ -684,10 +684,14 @@ __device__ __forceinline__ void wx_leaf_entries(const GLv* __restrict__ Lv, cons
     m2l_tab4(Lv[enc >> 40].mom + (enc & ((1LL << 40) - 1)) * 10, geo + (long long)gi * kTab, acc);
   };
   long long e = e0;
-  for (; e + D - 1 < e1; e += D) {
-    int gi[D], mi[D];
+  // software pipeline: the next batch's indices load while this batch's
+  // masses and geometry rows are in flight (one round trip per batch)
+  int gi[D], mi[D];
+  if (e + D - 1 < e1) {
 #pragma unroll
     for (int u = 0; u < D; ++u) gi[u] = __ldg(mgeo + e + u), mi[u] = __ldg(mmi + e + u);
+  }
+  for (; e + D - 1 < e1; e += D) {
     double m0[D];
     double2 ga[D], gb[D];
 #pragma unroll
@@ -698,16 +702,23 @@ __device__ __forceinline__ void wx_leaf_entries(const GLv* __restrict__ Lv, cons
       ga[u] = __ldg(g2 + 2 * row);
       gb[u] = __ldg(g2 + 2 * row + 1);
     }
+    int gc[D];
+#pragma unroll
+    for (int u = 0; u < D; ++u) gc[u] = gi[u];
+    if (e + 2 * D - 1 < e1) {
+#pragma unroll
+      for (int u = 0; u < D; ++u) gi[u] = __ldg(mgeo + e + D + u), mi[u] = __ldg(mmi + e + D + u);
+    }
 #pragma unroll
     for (int u = 0; u < D; ++u) {
-      if (gi[u] < 0) {
+      if (gc[u] < 0) {
         const double nM = -m0[u];
         acc[0] = acc[0] + nM * ga[u].x;
         acc[1] = fma(nM, ga[u].y, acc[1]);
         acc[2] = fma(nM, gb[u].x, acc[2]);
         acc[3] = fma(nM, gb[u].y, acc[3]);
       } else {
-        full(e + u, gi[u]);
+        full(e + u, gc[u]);
       }
     }
   }
@@ -1408,6 +1419,7 @@ struct GravAmrWork {
   int* wx_tlev = nullptr;         // W/X kernel targets (level, flat), in patch order
   long long* wx_tflat = nullptr;
   long long wx_targets = 0;
+
   double* wx_geo = nullptr;  // [distinct W/X separations][13]
   double* wx_geo4 = nullptr;  // the same rows' first 4 values (a leaf target's monopole term), 32-byte rows
   double* u_geo = nullptr;   // [distinct cross-depth U separations][4]
@@ -1671,6 +1683,7 @@ static cudaError_t build_m2l_work(GravAmrWork& w, const std::vector<std::vector<
   w.mono_ctas = (long long)mono.size();
   drop(reinterpret_cast<void*&>(w.wx_tlev));
   drop(reinterpret_cast<void*&>(w.wx_tflat));
+
   w.m2l_ctas = (long long)wk.size();
   // targets with W/X entries among the M2L patches, in patch order (source locality)
   std::vector<std::pair<long long, std::pair<int, long long>>> tg;
@@ -1686,6 +1699,7 @@ static cudaError_t build_m2l_work(GravAmrWork& w, const std::vector<std::vector<
   std::vector<long long> tf(tg.size());
   for (size_t i = 0; i < tg.size(); ++i) tl[i] = tg[i].second.first, tf[i] = tg[i].second.second;
   w.wx_targets = (long long)tg.size();
+
   cudaError_t e = upload(wk, &w.m2l_work);
   if (w.m2l_work) w.allocs.push_back(w.m2l_work);
   if (e == cudaSuccess) e = upload(mono, &w.mono_slots);
@@ -2051,11 +2065,14 @@ int tmgpu_gravity_amr_solve(tmgpu_gravity_amr* G, const double* mass, double* ph
   }
   if (e == cudaSuccess && rc == TMGPU_OK) {
     long long launches = 0;
-    // one GPU: leaf cells' m is read from the leaf-mass array wherever a
-    // leaf moment would be (M2M, the fused window, W/X, U), so P2M is skipped;
-    // distributed, leaf moments travel in the moment exchange and P2M stays
-    const double* lmass = (!w.let && !w.root_leaf) ? w.mass : nullptr;
-    if (nloc && !lmass) {
+    // leaf cells' m is read from the leaf-mass array wherever a leaf moment
+    // would be: the owned-subtree M2M (owned leaves), and after the moment
+    // exchange the fused window, W/X and U (the masses of every other rank's
+    // leaf patch this rank reads arrive with it: halo_mass_kernel). One GPU
+    // skips P2M; distributed, leaf moments travel in the exchange (and the
+    // shared-top M2M reads them), so P2M stays
+    const double* lmass = !w.root_leaf ? w.mass : nullptr;
+    if (nloc && (w.let || !lmass)) {
       amr_p2m_kernel<<<grid_for(nout), 128, 0, st>>>(w.mass, nloc, w.lo, w.slot_level, w.slot_node,
                                                      w.dev_lv);
       ++launches;
