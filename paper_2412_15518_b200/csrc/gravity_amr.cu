@@ -179,9 +179,9 @@ __global__ void amr_m2m_kernel(const GLv* __restrict__ L, int l, const int* __re
 #pragma unroll
               for (int j = i; j < 3; ++j) o[4 + s2(i, j)] += M * s[i] * s[j];
           }
-      double* out = P.mom + ((long long)n * 512 + c) * 10;
+      double2* out = reinterpret_cast<double2*>(P.mom + ((long long)n * 512 + c) * 10);
 #pragma unroll
-      for (int q = 0; q < 10; ++q) out[q] = o[q];
+      for (int h = 0; h < 5; ++h) out[h] = make_double2(o[2 * h], o[2 * h + 1]);
       continue;
     }
     for (int cc = 0; cc < 2; ++cc)
@@ -189,7 +189,16 @@ __global__ void amr_m2m_kernel(const GLv* __restrict__ L, int l, const int* __re
         for (int a = 0; a < 2; ++a) {
           const double s[3] = {(a - 0.5) * hc, (b - 0.5) * hc, (cc - 0.5) * hc};
           const int ci = ((2 * I) & 7) + a, cj = ((2 * J) & 7) + b, ck = ((2 * K) & 7) + cc;
-          const double* ch = base + ((ck * 8 + cj) * 8 + ci) * 10;
+          double ch[10];  // the child's 80-byte record as five 16-byte loads
+          {
+            const double2* c2 = reinterpret_cast<const double2*>(base + ((ck * 8 + cj) * 8 + ci) * 10);
+#pragma unroll
+            for (int h = 0; h < 5; ++h) {
+              const double2 v = c2[h];
+              ch[2 * h] = v.x;
+              ch[2 * h + 1] = v.y;
+            }
+          }
           const double M = ch[0];
           o[0] += M;
 #pragma unroll
@@ -200,9 +209,9 @@ __global__ void amr_m2m_kernel(const GLv* __restrict__ L, int l, const int* __re
             for (int j = i; j < 3; ++j)
               o[4 + s2(i, j)] += ch[4 + s2(i, j)] + ch[1 + i] * s[j] + s[i] * ch[1 + j] + M * s[i] * s[j];
         }
-    double* out = P.mom + ((long long)n * 512 + c) * 10;
+    double2* out = reinterpret_cast<double2*>(P.mom + ((long long)n * 512 + c) * 10);
 #pragma unroll
-    for (int q = 0; q < 10; ++q) out[q] = o[q];
+    for (int h = 0; h < 5; ++h) out[h] = make_double2(o[2 * h], o[2 * h + 1]);
   }
 }
 
@@ -877,11 +886,17 @@ __global__ void amr_l2l_kernel(const GLv* __restrict__ Lv, int l, long long nnod
        tt += (long long)gridDim.x * blockDim.x) {
     const long long n = nodes[tt >> 9];
     const int c = (int)(tt & 511);
-    double s[3], sh[10];
-    l2l_shift<10>(l2l_parent(L, P, n, c, h, s), s, sh);
-    double* out = L.loc + (n * 512 + c) * 10;
+    double s[3], sh[10], lp[10], cur[10];
+    const double2* p2 = reinterpret_cast<const double2*>(l2l_parent(L, P, n, c, h, s));
+    double2* o2 = reinterpret_cast<double2*>(L.loc + (n * 512 + c) * 10);
 #pragma unroll
-    for (int q = 0; q < 10; ++q) out[q] = sh[q] + out[q];
+    for (int q = 0; q < 5; ++q) {  // 80-byte records as five 16-byte loads
+      const double2 a = p2[q], b = o2[q];
+      lp[2 * q] = a.x, lp[2 * q + 1] = a.y, cur[2 * q] = b.x, cur[2 * q + 1] = b.y;
+    }
+    l2l_shift<10>(lp, s, sh);
+#pragma unroll
+    for (int q = 0; q < 5; ++q) o2[q] = make_double2(sh[2 * q] + cur[2 * q], sh[2 * q + 1] + cur[2 * q + 1]);
   }
 }
 
@@ -1076,6 +1091,16 @@ __global__ void __launch_bounds__(kL2pThreads, 4) amr_l2p_kernel(const GLv* __re
   }
 }
 
+// The dense top's three M2M levels (4^3 <- level-0 patch, 2^3, 1) in one CTA
+__global__ void __launch_bounds__(128) top_m2m_kernel(const double* __restrict__ lv0, double* __restrict__ d2,
+                                                      double* __restrict__ d1, double* __restrict__ d0) {
+  if (threadIdx.x < 64) m2m_cell(lv0, d2, 4, 1.0 / 8.0, threadIdx.x);
+  __syncthreads();
+  if (threadIdx.x < 8) m2m_cell(d2, d1, 2, 1.0 / 4.0, threadIdx.x);
+  __syncthreads();
+  if (threadIdx.x == 0) m2m_cell(d1, d0, 1, 1.0 / 2.0, 0);
+}
+
 // ---- angular-momentum correction (tmo_grav_am_correct) ---------------------
 
 __device__ __forceinline__ void cell_pos(const GLv* __restrict__ Lv, int l, int n, int c, double x[3]) {
@@ -1168,8 +1193,14 @@ __device__ __forceinline__ void am_block_sums2(double m0, const double x0[3], co
 // adjacent-pair tree over n (power of two) entries of 16 sums: each CTA
 // reduces a chunk of min(n, 256) consecutive entries (the first levels of the
 // global tree) into out[blockIdx.x]
+__device__ __forceinline__ void am_solve(const double* __restrict__ S, double* __restrict__ rw);
+
+// rw (the last pass: one CTA over the whole remaining n): thread 0 solves
+// for the rigid-rotation field from the root sums (am_solve) instead of
+// storing them
 __global__ void __launch_bounds__(256) am_tree_pass_kernel(const double* __restrict__ in,
-                                                           double* __restrict__ out, long long n) {
+                                                           double* __restrict__ out, long long n,
+                                                           double* __restrict__ rw = nullptr) {
   __shared__ double v[256][17];
   const int chunk = n < 256 ? (int)n : 256;
   const long long base = (long long)blockIdx.x * chunk;
@@ -1184,13 +1215,15 @@ __global__ void __launch_bounds__(256) am_tree_pass_kernel(const double* __restr
       for (int q = 0; q < 16; ++q) v[t][q] = v[t][q] + v[t + st][q];
     __syncthreads();
   }
-  if (t < 16) out[(long long)blockIdx.x * 16 + t] = v[0][t];
+  if (rw) {
+    if (t == 0) am_solve(v[0], rw);
+  } else if (t < 16) {
+    out[(long long)blockIdx.x * 16 + t] = v[0][t];
+  }
 }
 
 // the 3x3 solve of tmo_grav_am_solve on the total sums S -> rw = (R, w, S)
-__global__ void am_solve_kernel(const double* __restrict__ part, double* __restrict__ rw) {
-  if (threadIdx.x != 0) return;
-  const double* S = part;
+__device__ __forceinline__ void am_solve(const double* __restrict__ S, double* __restrict__ rw) {
   double R[3], w[3];
   const double M = S[0];
   R[0] = S[1] / M;
@@ -1217,6 +1250,10 @@ __global__ void am_solve_kernel(const double* __restrict__ part, double* __restr
   }
   for (int q = 0; q < 3; ++q) rw[q] = R[q], rw[3 + q] = w[q];
   for (int q = 0; q < 16; ++q) rw[6 + q] = S[q];
+}
+
+__global__ void am_solve_kernel(const double* __restrict__ part, double* __restrict__ rw) {
+  if (threadIdx.x == 0) am_solve(part, rw);
 }
 
 __global__ void am_apply_kernel(const GLv* __restrict__ Lv, long long nslots, long long lo,
@@ -2055,9 +2092,16 @@ int tmgpu_gravity_amr_solve(tmgpu_gravity_amr* G, const double* mass, double* ph
   // (a timed solve runs the three M2L kernels one after another on `st`
   // instead, each between its own events: their durations measured alone)
   const bool mono_early = !w.let && w.mono_ctas > 0 && !timed;
+  // (one GPU) the U sources' masses are gathered there too, off the critical path
+  const bool u_side = mono_early && w.u_max && !w.root_leaf;
   if (e == cudaSuccess && mono_early) {
     cudaEventRecord(w.ev_fork2, st);
     cudaStreamWaitEvent(w.side2, w.ev_fork2, 0);
+    if (u_side) {
+      amr_u_gather_kernel<<<dim3((unsigned)std::min<long long>((w.u_max + 255) / 256, 1184), P.nlevels), 256, 0,
+                            w.side2>>>(w.dev_lv, w.mass);
+      g_launches.fetch_add(1, std::memory_order_relaxed);
+    }
     amr_m2l_mono_kernel<<<(unsigned)w.mono_ctas, kM2lThreads, kMonoSmem, w.side2>>>(
         w.mono_slots, w.slot_level, w.mass, w.slot_nbs, w.tab4p, w.lloc, w.lo);
     cudaEventRecord(w.ev_join2, w.side2);
@@ -2131,15 +2175,13 @@ int tmgpu_gravity_amr_solve(tmgpu_gravity_amr* G, const double* mass, double* ph
             w.dev_lv, w.halo_slots, w.n_halo_slots, w.slot_level, w.slot_node, w.mass);
       launches += 5;
     }
-    m2m_kernel<<<1, 128, 0, st>>>(w.host_lv[0].mom, w.dmom[2], 4, 1.0 / 8.0);
-    m2m_kernel<<<1, 128, 0, st>>>(w.dmom[2], w.dmom[1], 2, 1.0 / 4.0);
-    m2m_kernel<<<1, 128, 0, st>>>(w.dmom[1], w.dmom[0], 1, 1.0 / 2.0);
+    top_m2m_kernel<<<1, 128, 0, st>>>(w.host_lv[0].mom, w.dmom[2], w.dmom[1], w.dmom[0]);
     // the dense depth-2 M2L (one small CTA) overlaps the patch M2L on a side stream
     cudaEventRecord(w.ev_fork, st);
     cudaStreamWaitEvent(w.side, w.ev_fork, 0);
     m2l_kernel<<<1, 128, 0, w.side>>>(w.dmom[2], w.dloc[2], 4, w.tab + 2LL * kOff3 * kTab);
     cudaEventRecord(w.ev_join, w.side);
-    launches += 4;
+    launches += 2;
     if (timed) cudaEventRecord(rec.ev[2], st);
     {
       // the fused kernel (1 CTA/SM) first on the solve's stream, the mono kernel
@@ -2191,7 +2233,7 @@ int tmgpu_gravity_amr_solve(tmgpu_gravity_amr* G, const double* mass, double* ph
       e = cudaMemsetAsync(w.part + w.lo * 16, 0, (size_t)(w.hi - w.lo) * 16 * sizeof(double), st);
     else if (am)
       e = cudaMemsetAsync(w.part, 0, (size_t)w.P * 16 * sizeof(double), st);
-    if (w.u_max) {  // U entries' source masses, gathered in parallel
+    if (w.u_max && !u_side) {  // U entries' source masses, gathered in parallel
       amr_u_gather_kernel<<<dim3((unsigned)std::min<long long>((w.u_max + 255) / 256, 1184), P.nlevels), 256, 0, st>>>(
           w.dev_lv, lmass);
       ++launches;
@@ -2212,17 +2254,24 @@ int tmgpu_gravity_amr_solve(tmgpu_gravity_amr* G, const double* mass, double* ph
       }
       double* bufs[2] = {w.part, w.part2};
       int cur = 0;
+      bool solved = false;  // the last pass (one CTA) solves for the field
       for (long long n = w.P; n > 1;) {
         const long long chunk = n < 256 ? n : 256;
-        am_tree_pass_kernel<<<(unsigned)(n / chunk), 256, 0, st>>>(bufs[cur], bufs[cur ^ 1], n);
+        const bool last = n == chunk;
+        am_tree_pass_kernel<<<(unsigned)(n / chunk), 256, 0, st>>>(bufs[cur], bufs[cur ^ 1], n,
+                                                                   last ? w.part + w.P * 16 : nullptr);
+        solved |= last;
         n /= chunk;
         cur ^= 1;
         ++launches;
       }
-      am_solve_kernel<<<1, 32, 0, st>>>(bufs[cur], w.part + w.P * 16);
+      if (!solved) {
+        am_solve_kernel<<<1, 32, 0, st>>>(bufs[cur], w.part + w.P * 16);
+        ++launches;
+      }
       am_apply_kernel<<<grid_for(nout), 128, 0, st>>>(w.dev_lv, nloc, w.lo, w.slot_level, w.slot_node,
                                                       w.part + w.P * 16, dg);
-      launches += 3;
+      launches += 1;
     }
     if (w.peer) {  // every received patch and AM sum has been read
       let_done_kernel<<<1, 32, 0, st>>>(w.pt, w.peer_seq);

@@ -129,11 +129,10 @@ __device__ __forceinline__ void m2l_direct(const double* __restrict__ mom, doubl
   m2l_tab(mom, e, out);
 }
 
-__global__ void m2m_kernel(const double* __restrict__ child, double* __restrict__ parent, long long n,
-                           double hc) {
-  const long long n3 = n * n * n;
-  for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < n3;
-       p += (long long)gridDim.x * blockDim.x) {
+// M2M of dense cell p of an n^3 level from its 8 children (level 2n)
+__device__ __forceinline__ void m2m_cell(const double* __restrict__ child, double* __restrict__ parent,
+                                         long long n, double hc, long long p) {
+  {
     const long long I = p % n, J = (p / n) % n, K = p / (n * n);
     double o[10];
 #pragma unroll
@@ -157,6 +156,14 @@ __global__ void m2m_kernel(const double* __restrict__ child, double* __restrict_
 #pragma unroll
     for (int q = 0; q < 10; ++q) out[q] = o[q];
   }
+}
+
+__global__ void m2m_kernel(const double* __restrict__ child, double* __restrict__ parent, long long n,
+                           double hc) {
+  const long long n3 = n * n * n;
+  for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < n3;
+       p += (long long)gridDim.x * blockDim.x)
+    m2m_cell(child, parent, n, hc, p);
 }
 
 __global__ void __launch_bounds__(128) m2l_kernel(const double* __restrict__ mom,
