@@ -24,6 +24,7 @@
 //               tree (shuffles + shared memory), one-CTA tree over slots,
 //               3x3 solve, apply
 #include <algorithm>
+#include <type_traits>
 #include <cstdlib>
 #include <cstring>
 #include <string>
@@ -311,32 +312,44 @@ __device__ __forceinline__ void m2l_row_par(const double* __restrict__ src,
       }
       G[t][12] = trow[jj * kTabP + 12];
     }
+    // sources in x-groups sharing a neighbour patch (mi = 0 | 1..4 | 5):
+    // one branch per group, so a group's independent term chains share a
+    // basic block (the scheduler overlaps them); per target the sources still
+    // arrive in ascending mi
+    auto group = [&](auto lo_c, auto hi_c, bool f) {
+      constexpr int lo = decltype(lo_c)::value, hi = decltype(hi_c)::value;
+      if (f) {
 #pragma unroll
-    for (int mi = 0; mi < 6; ++mi) {
-      const int sx = pe + 2 * mi;
-      const int grp = sx < 2 ? 0 : (sx > 9 ? 2 : 1);
-      if (full[grp]) {
-        double m[10];
+        for (int mi = lo; mi <= hi; ++mi) {
+          const int sx = pe + 2 * mi;
+          double m[10];
 #pragma unroll
-        for (int q = 0; q < 10; ++q) m[q] = src[q * kWVar + sx];
+          for (int q = 0; q < 10; ++q) m[q] = src[q * kWVar + sx];
 #pragma unroll
-        for (int t = 0; t < 3; ++t) {
-          const int k = mi - t;
-          if (k < 0 || k > 3) continue;
-          if (NEAR && t == 1) continue;
-          m2l_term<NOUT>(m, G[t], acc[k]);
+          for (int t = 0; t < 3; ++t) {
+            const int k = mi - t;
+            if (k < 0 || k > 3) continue;
+            if (NEAR && t == 1) continue;
+            m2l_term<NOUT>(m, G[t], acc[k]);
+          }
         }
       } else {
-        const double nM = -src[sx];
 #pragma unroll
-        for (int t = 0; t < 3; ++t) {
-          const int k = mi - t;
-          if (k < 0 || k > 3) continue;
-          if (NEAR && t == 1) continue;
-          m2l_term_mono<NOUT>(nM, G[t], acc[k]);
+        for (int mi = lo; mi <= hi; ++mi) {
+          const double nM = -src[pe + 2 * mi];
+#pragma unroll
+          for (int t = 0; t < 3; ++t) {
+            const int k = mi - t;
+            if (k < 0 || k > 3) continue;
+            if (NEAR && t == 1) continue;
+            m2l_term_mono<NOUT>(nM, G[t], acc[k]);
+          }
         }
       }
-    }
+    };
+    group(std::integral_constant<int, 0>{}, std::integral_constant<int, 0>{}, full[0]);
+    group(std::integral_constant<int, 1>{}, std::integral_constant<int, 4>{}, full[1]);
+    group(std::integral_constant<int, 5>{}, std::integral_constant<int, 5>{}, full[2]);
   }
 }
 
