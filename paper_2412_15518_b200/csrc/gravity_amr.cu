@@ -1012,14 +1012,8 @@ __global__ void __launch_bounds__(kL2pThreads, 4) amr_l2p_kernel(const GLv* __re
   }
   asm volatile("cp.async.wait_all;\n" ::: "memory");
   __syncthreads();
-  // masses scaled by 2^d for the unit-spacing constant geometry (exact)
+  // masses scaled by 2^d at use for the unit-spacing constant geometry (exact)
   const double sc1 = (double)(1LL << d);
-  for (int t = threadIdx.x; t < 1200; t += blockDim.x) {  // the whole window (padding too)
-    double2* m = reinterpret_cast<double2*>(mw) + t;
-    const double2 v = *m;
-    *m = make_double2(v.x * sc1, v.y * sc1);
-  }
-  __syncthreads();
   const long long ncell = nslots * 512;
   double keep[2][3];  // the two cells' g for the angular-momentum sums
 #pragma unroll
@@ -1054,7 +1048,7 @@ __global__ void __launch_bounds__(kL2pThreads, 4) amr_l2p_kernel(const GLv* __re
                   oz = lz < 0 ? -1 : (lz > 7 ? 1 : 0);
         if (!((valid27 >> (((oz + 1) * 3 + (oy + 1)) * 3 + ox + 1)) & 1u)) continue;
         // -m 2^d and -m 2^2d against the unit geometry: p2p_geom's terms exactly
-        const double nm1 = -mw[((lz + 1) * 10 + (ly + 1)) * 24 + lx + 2], nm2 = nm1 * sc1;
+        const double nm1 = -(mw[((lz + 1) * 10 + (ly + 1)) * 24 + lx + 2] * sc1), nm2 = nm1 * sc1;
         const int o = ((dz + 1) * 3 + (dy + 1)) * 3 + dx + 1;
         p = fma(nm1, c_p2p_unit[o][0], p);
         gx = fma(nm2, c_p2p_unit[o][1], gx);
