@@ -1459,6 +1459,7 @@ struct GravAmrWork {
   long long m2l_ctas = 0;
   long long* mono_slots = nullptr;  // amr_m2l_mono_kernel: leaf patches among leaf patches (slot)
   long long mono_ctas = 0;
+  long long mono_local = 0;  // the first mono_local have only this rank's leaves as neighbours
   long long u_max = 0;  // most cross-depth U entries of a level
   int* wx_tlev = nullptr;         // W/X kernel targets (level, flat), in patch order
   long long* wx_tflat = nullptr;
@@ -1712,6 +1713,21 @@ static cudaError_t build_m2l_work(GravAmrWork& w, const std::vector<std::vector<
     else
       wk.push_back(x);
   }
+  // distributed: the mono patches whose neighbours are all this rank's own
+  // leaves first — they need only local masses and start with the solve,
+  // beside the upward pass and the moment exchange (w.mono_local of them)
+  auto local_mono = [&](long long slot) {
+    const GravLevel& L = w.plan.lv[w.plan.slot_level[(size_t)slot]];
+    const int n = w.plan.slot_node[(size_t)slot];
+    for (int o = 0; o < 27; ++o) {
+      const int nb = L.nbr[(size_t)n * 27 + o];
+      if (nb < 0) continue;
+      const long long ls = L.leaf_slot[(size_t)nb];
+      if (ls < w.lo || ls >= w.hi) return false;
+    }
+    return true;
+  };
+  w.mono_local = std::stable_partition(mono.begin(), mono.end(), local_mono) - mono.begin();
   // the heavier internal patches (all ten locals) first: the last waves are
   // then the lighter leaf patches, and the concurrent mono kernel fills the tail
   std::stable_partition(wk.begin(), wk.end(),
@@ -2099,8 +2115,17 @@ int tmgpu_gravity_amr_solve(tmgpu_gravity_amr* G, const double* mass, double* ph
   // (a timed solve runs the three M2L kernels one after another on `st`
   // instead, each between its own events: their durations measured alone)
   const bool mono_early = !w.let && w.mono_ctas > 0 && !timed;
+  // distributed: the mono patches with only local neighbours start now too
+  const long long mono_pre = (w.let && !timed && !w.root_leaf) ? w.mono_local : 0;
   // (one GPU) the U sources' masses are gathered there too, off the critical path
   const bool u_side = mono_early && w.u_max && !w.root_leaf;
+  if (e == cudaSuccess && mono_pre) {
+    cudaEventRecord(w.ev_fork2, st);
+    cudaStreamWaitEvent(w.side2, w.ev_fork2, 0);
+    amr_m2l_mono_kernel<<<(unsigned)mono_pre, kM2lThreads, kMonoSmem, w.side2>>>(
+        w.mono_slots, w.slot_level, w.mass, w.slot_nbs, w.tab4p, w.lloc, w.lo);
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+  }
   if (e == cudaSuccess && mono_early) {
     cudaEventRecord(w.ev_fork2, st);
     cudaStreamWaitEvent(w.side2, w.ev_fork2, 0);
@@ -2210,10 +2235,12 @@ int tmgpu_gravity_amr_solve(tmgpu_gravity_amr* G, const double* mass, double* ph
       if (timed) cudaEventRecord(rec.k[2], st);
       if (w.mono_ctas && !mono_early && !timed) {  // leaf patches among leaf patches: monopole sources
         cudaStreamWaitEvent(w.side2, w.ev_fork, 0);
-        amr_m2l_mono_kernel<<<(unsigned)w.mono_ctas, kM2lThreads, kMonoSmem, w.side2>>>(
-            w.mono_slots, w.slot_level, w.mass, w.slot_nbs, w.tab4p, w.lloc, w.lo);
+        if (w.mono_ctas > mono_pre) {  // (distributed: those not started at the solve's start)
+          amr_m2l_mono_kernel<<<(unsigned)(w.mono_ctas - mono_pre), kM2lThreads, kMonoSmem, w.side2>>>(
+              w.mono_slots + mono_pre, w.slot_level, w.mass, w.slot_nbs, w.tab4p, w.lloc, w.lo);
+          ++launches;
+        }
         cudaEventRecord(w.ev_join2, w.side2);
-        ++launches;
       }
       if (w.mono_ctas && !timed) cudaStreamWaitEvent(st, w.ev_join2, 0);
       if (w.wx_targets) {
