@@ -515,8 +515,10 @@ def run_ours(args, rank, world):
     for _ in range(2):
         pipe.step(pin_in, pin_out)
     a0.record(pipe.d2h)
+    h0 = time.perf_counter()
     for _ in range(k_e2e):
         pipe.step(pin_in, pin_out)
+    host_ms = (time.perf_counter() - h0) * 1e3 / k_e2e  # host time to enqueue one step (no sync)
     a1.record(pipe.d2h)
     pipe.synchronize()
     e2e_ms = a0.elapsed_time(a1) / k_e2e
@@ -576,7 +578,7 @@ def run_ours(args, rank, world):
                 if world > 1 else "single GPU"}),
             "e2e": {"value": cells / (e2e_ms * 1e-3), "unit": UNIT,
                     "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes,
-                    "ms_per_step": e2e_ms, "steps": k_e2e,
+                    "ms_per_step": e2e_ms, "steps": k_e2e, "host_enqueue_ms_per_step": host_ms,
                     "path": "paper_2412_15518_b200.driver.HostStepPipeline(" + type(drv).__name__ +
                             ").step(pinned in, pinned out): H2D -> tmgpu_forest_step_io (input scattered "
                             "in the step's first pass, output written by its last stage) -> D2H, copies "

@@ -1460,6 +1460,8 @@ struct GravAmrWork {
   long long* mono_slots = nullptr;  // amr_m2l_mono_kernel: leaf patches among leaf patches (slot)
   long long mono_ctas = 0;
   long long mono_local = 0;  // the first mono_local have only this rank's leaves as neighbours
+  long long m2l_local = 0;   // the first m2l_local fused patches read only this rank's subtrees
+  cudaEvent_t ev_up = nullptr, ev_fl = nullptr;  // owned upward pass done; local fused M2L done
   long long u_max = 0;  // most cross-depth U entries of a level
   int* wx_tlev = nullptr;         // W/X kernel targets (level, flat), in patch order
   long long* wx_tflat = nullptr;
@@ -1728,10 +1730,41 @@ static cudaError_t build_m2l_work(GravAmrWork& w, const std::vector<std::vector<
     return true;
   };
   w.mono_local = std::stable_partition(mono.begin(), mono.end(), local_mono) - mono.begin();
-  // the heavier internal patches (all ten locals) first: the last waves are
-  // then the lighter leaf patches, and the concurrent mono kernel fills the tail
-  std::stable_partition(wk.begin(), wk.end(),
-                        [&](const int2& x) { return w.plan.lv[x.x].leaf_slot[x.y] < 0 || x.x == 0; });
+  // distributed: the patches whose existing neighbours all lie in this rank's
+  // own subtrees first (their sources' moments come from the owned upward
+  // pass, their leaf sources' masses are local): they run beside the moment
+  // exchange (w.m2l_local of them). A patch is this rank's when every leaf of
+  // its subtree is (leaf slots are a Morton DFS, so subtrees are slot ranges)
+  std::vector<std::vector<char>> mine(w.plan.nlevels);
+  for (int l = w.plan.nlevels - 1; l >= 0; --l) {
+    const GravLevel& L = w.plan.lv[l];
+    mine[l].assign(L.n, 0);
+    for (int n = 0; n < L.n; ++n) {
+      if (L.leaf_slot[n] >= 0) {
+        mine[l][n] = L.leaf_slot[n] >= w.lo && L.leaf_slot[n] < w.hi;
+        continue;
+      }
+      bool all = true;
+      for (int c = 0; c < 8 && all; ++c) all = mine[l + 1][L.child[(size_t)n * 8 + c]] != 0;
+      mine[l][n] = all;
+    }
+  }
+  auto local_patch = [&](const int2& x) {
+    const GravLevel& L = w.plan.lv[x.x];
+    for (int o = 0; o < 27; ++o) {
+      const int nb = L.nbr[(size_t)x.y * 27 + o];
+      if (nb >= 0 && !mine[x.x][nb]) return false;
+    }
+    return true;
+  };
+  const auto split = need ? std::stable_partition(wk.begin(), wk.end(), local_patch) : wk.begin();
+  w.m2l_local = split - wk.begin();
+  // within each part the heavier internal patches (all ten locals) first: the
+  // last waves are then the lighter leaf patches, and the concurrent mono
+  // kernel fills the tail
+  auto internal_first = [&](const int2& x) { return w.plan.lv[x.x].leaf_slot[x.y] < 0 || x.x == 0; };
+  std::stable_partition(wk.begin(), split, internal_first);
+  std::stable_partition(split, wk.end(), internal_first);
   auto drop = [&w](void*& p) {
     if (!p) return;
     cudaFree(p);
@@ -1793,6 +1826,8 @@ void tmgpu_gravity_amr_destroy(tmgpu_gravity_amr* G) {
   if (G->w.side2) cudaStreamDestroy(G->w.side2);
   if (G->w.ev_join2) cudaEventDestroy(G->w.ev_join2);
   if (G->w.ev_fork2) cudaEventDestroy(G->w.ev_fork2);
+  if (G->w.ev_up) cudaEventDestroy(G->w.ev_up);
+  if (G->w.ev_fl) cudaEventDestroy(G->w.ev_fl);
   let_peer_close(G->w);
   for (void* p : G->w.allocs)
     if (p) cudaFree(p);
@@ -1933,6 +1968,8 @@ tmgpu_gravity_amr* tmgpu_gravity_amr_create(const int* leaves, long long nleaves
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&w.side2, cudaStreamNonBlocking);
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&w.ev_join2, cudaEventDisableTiming);
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&w.ev_fork2, cudaEventDisableTiming);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&w.ev_up, cudaEventDisableTiming);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&w.ev_fl, cudaEventDisableTiming);
 
   for (int kind = 0; kind < 2 && e == cudaSuccess; ++kind) {
     const std::vector<double>& sep = kind == 0 ? P.wx_sep : P.u_sep;
@@ -2160,6 +2197,17 @@ int tmgpu_gravity_amr_solve(tmgpu_gravity_amr* G, const double* mass, double* ph
                                                          ni, lmass);
       ++launches;
     }
+    // distributed: the fused M2L of patches that read only this rank's
+    // subtrees runs now on the side stream, beside the moment exchange
+    const long long m2l_pre = (w.let && !timed && !w.root_leaf) ? w.m2l_local : 0;
+    if (m2l_pre) {
+      cudaEventRecord(w.ev_up, st);
+      cudaStreamWaitEvent(w.side, w.ev_up, 0);
+      amr_m2l_fused_kernel<<<(unsigned)m2l_pre, kM2lThreads, kM2lSmem, w.side>>>(w.dev_lv, w.m2l_work, w.tabp,
+                                                                                w.lloc, w.lo, lmass);
+      cudaEventRecord(w.ev_fl, w.side);
+      ++launches;
+    }
     if (timed) cudaEventRecord(rec.ev[1], st);
     if (w.peer) {
       // roots to every peer and halo patches to their readers, straight into
@@ -2227,9 +2275,9 @@ int tmgpu_gravity_amr_solve(tmgpu_gravity_amr* G, const double* mass, double* ph
         cudaEventRecord(rec.k[1], st);
         launches += w.mono_ctas ? 1 : 0;
       }
-      if (w.m2l_ctas) {
-        amr_m2l_fused_kernel<<<(unsigned)w.m2l_ctas, kM2lThreads, kM2lSmem, st>>>(w.dev_lv, w.m2l_work,
-                                                                                 w.tabp, w.lloc, w.lo, lmass);
+      if (w.m2l_ctas > m2l_pre) {
+        amr_m2l_fused_kernel<<<(unsigned)(w.m2l_ctas - m2l_pre), kM2lThreads, kM2lSmem, st>>>(
+            w.dev_lv, w.m2l_work + m2l_pre, w.tabp, w.lloc, w.lo, lmass);
         ++launches;
       }
       if (timed) cudaEventRecord(rec.k[2], st);
@@ -2243,6 +2291,7 @@ int tmgpu_gravity_amr_solve(tmgpu_gravity_amr* G, const double* mass, double* ph
         cudaEventRecord(w.ev_join2, w.side2);
       }
       if (w.mono_ctas && !timed) cudaStreamWaitEvent(st, w.ev_join2, 0);
+      if (m2l_pre) cudaStreamWaitEvent(st, w.ev_fl, 0);  // W/X follows every V sum
       if (w.wx_targets) {
         amr_wx_kernel<<<grid_for(w.wx_targets), 128, 0, st>>>(w.dev_lv, w.wx_tlev, w.wx_tflat,
                                                               w.wx_targets, w.wx_geo, w.lloc, w.lo, lmass,
