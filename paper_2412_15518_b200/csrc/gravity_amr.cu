@@ -1098,6 +1098,46 @@ __global__ void __launch_bounds__(kL2pThreads, 4) amr_l2p_kernel(const GLv* __re
   }
 }
 
+// The dense depth-2 M2L (4^3 cells, every cell exists; m2l_kernel's loop
+// order and arithmetic) with the 64 cells' moments and the depth's geometry
+// table staged in shared memory; thread t < 64 sums target t's lower source
+// planes, thread t + 64 its upper ones (the specification's two partial sums),
+// added as o[0] + o[1]. One CTA.
+__global__ void __launch_bounds__(128) dense_m2l_staged_kernel(const double* __restrict__ mom,
+                                                               double* __restrict__ loc,
+                                                               const double* __restrict__ tab) {
+  __shared__ double s_mom[64 * 10];
+  __shared__ double s_tab[kOff3 * kTab];
+  __shared__ double s_up[64 * 10];
+  for (int q = threadIdx.x; q < 64 * 10; q += blockDim.x) s_mom[q] = mom[q];
+  for (int q = threadIdx.x; q < kOff3 * kTab; q += blockDim.x) s_tab[q] = tab[q];
+  __syncthreads();
+  const int t = threadIdx.x & 63, upper = threadIdx.x >> 6;
+  const int i = t & 3, j = (t >> 2) & 3, k = t >> 4;
+  double o[10];
+#pragma unroll
+  for (int q = 0; q < 10; ++q) o[q] = 0.0;
+  for (int dz = -2 - (k & 1); dz <= 3 - (k & 1); ++dz) {
+    if ((dz + (k & 1) >= 1) != (upper != 0)) continue;
+    for (int dy = -2 - (j & 1); dy <= 3 - (j & 1); ++dy)
+      for (int pe = 0; pe < 2; ++pe)  // even source x, then odd
+        for (int dx = -2 - (i & 1) + pe; dx <= 3 - (i & 1); dx += 2) {
+          if (dx >= -1 && dx <= 1 && dy >= -1 && dy <= 1 && dz >= -1 && dz <= 1) continue;
+          const int si = i + dx, sj = j + dy, sk = k + dz;
+          if (si < 0 || sj < 0 || sk < 0 || si >= 4 || sj >= 4 || sk >= 4) continue;
+          m2l_tab(s_mom + ((sk * 4 + sj) * 4 + si) * 10, s_tab + (((dz + 3) * kOff + (dy + 3)) * kOff + (dx + 3)) * kTab,
+                  o);
+        }
+  }
+  if (upper)
+#pragma unroll
+    for (int q = 0; q < 10; ++q) s_up[t * 10 + q] = o[q];
+  __syncthreads();
+  if (!upper)
+#pragma unroll
+    for (int q = 0; q < 10; ++q) loc[t * 10 + q] = o[q] + s_up[t * 10 + q];
+}
+
 // The dense top's three M2M levels (4^3 <- level-0 patch, 2^3, 1) in one CTA
 __global__ void __launch_bounds__(128) top_m2m_kernel(const double* __restrict__ lv0, double* __restrict__ d2,
                                                       double* __restrict__ d1, double* __restrict__ d0) {
@@ -2259,7 +2299,7 @@ int tmgpu_gravity_amr_solve(tmgpu_gravity_amr* G, const double* mass, double* ph
     // the dense depth-2 M2L (one small CTA) overlaps the patch M2L on a side stream
     cudaEventRecord(w.ev_fork, st);
     cudaStreamWaitEvent(w.side, w.ev_fork, 0);
-    m2l_kernel<<<1, 128, 0, w.side>>>(w.dmom[2], w.dloc[2], 4, w.tab + 2LL * kOff3 * kTab);
+    dense_m2l_staged_kernel<<<1, 128, 0, w.side>>>(w.dmom[2], w.dloc[2], w.tab + 2LL * kOff3 * kTab);
     cudaEventRecord(w.ev_join, w.side);
     launches += 2;
     if (timed) cudaEventRecord(rec.ev[2], st);
