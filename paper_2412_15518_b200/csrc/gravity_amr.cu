@@ -240,8 +240,15 @@ __global__ void amr_m2m_kernel(const GLv* __restrict__ L, int l, const int* __re
 // dz, dy, dx ascending, added; the W/X pairs follow in amr_wx_kernel —
 // tmo_grav_amr_solve's order, so the result is bitwise the oracle's.
 constexpr int kM2lThreads = 256;
-constexpr int kWPY = 13, kWPZ = 84, kWSub = 6 * kWPZ, kWVar = 4 * kWSub + 2;  // per var (+2: banks)
-constexpr int kWinDoubles = 10 * kWVar;                                   // 20,180
+constexpr int kWPY = 13, kWPZ = 84, kWSub = 6 * kWPZ;  // the mono kernel's mass window
+// The fused kernel's window: one 80-byte record (the 10 moments, as the global
+// AoS layout) per source cell, addressed in 16-byte chunks: rows of 12 records
+// at a pitch of 65 chunks (= 1 mod 8), 6 rows per z plane of a parity sub-grid
+// at 396 chunks (= 4 mod 8) — a warp's 16 distinct (Y, Z) sources then fill the
+// eight 16-byte bank groups exactly twice (conflict-free LDS.128), and the fill
+// copies 16-byte chunks.
+constexpr int kFRec = 5, kFPY = 65, kFPZ = 396, kFSub = 6 * kFPZ;  // chunks
+constexpr int kWinDoubles = 2 * 4 * kFSub;                          // 19,008
 constexpr int kTabP = 14;  // shared-memory table entry: 13 doubles + pad (16-byte rows)
 constexpr int kTabDoubles = kOff3 * kTabP;                                // 4,802
 constexpr size_t kM2lSmem = (size_t)(kWinDoubles + kTabDoubles) * sizeof(double);  // 199,856 B
@@ -293,7 +300,7 @@ __device__ __forceinline__ void m2l_term_mono(const double nM, const double (&e)
 // internal patch at x-offset -1, 0, +1 (warp votes; a warp whose sources in a
 // group are all leaf cells runs the monopole term for the group)
 template <bool NEAR, int NOUT>
-__device__ __forceinline__ void m2l_row_par(const double* __restrict__ src,
+__device__ __forceinline__ void m2l_row_par(const double2* __restrict__ src,
                                             const double* __restrict__ trow, double (&acc)[4][10],
                                             const bool (&full)[3]) {
 #pragma unroll
@@ -324,7 +331,11 @@ __device__ __forceinline__ void m2l_row_par(const double* __restrict__ src,
           const int sx = pe + 2 * mi;
           double m[10];
 #pragma unroll
-          for (int q = 0; q < 10; ++q) m[q] = src[q * kWVar + sx];
+          for (int q = 0; q < kFRec; ++q) {
+            const double2 v = src[sx * kFRec + q];
+            m[2 * q] = v.x;
+            m[2 * q + 1] = v.y;
+          }
 #pragma unroll
           for (int t = 0; t < 3; ++t) {
             const int k = mi - t;
@@ -336,7 +347,7 @@ __device__ __forceinline__ void m2l_row_par(const double* __restrict__ src,
       } else {
 #pragma unroll
         for (int mi = lo; mi <= hi; ++mi) {
-          const double nM = -src[pe + 2 * mi];
+          const double nM = -reinterpret_cast<const double*>(src + (pe + 2 * mi) * kFRec)[0];
 #pragma unroll
           for (int t = 0; t < 3; ++t) {
             const int k = mi - t;
@@ -356,6 +367,12 @@ __device__ __forceinline__ void m2l_row_par(const double* __restrict__ src,
 __device__ __forceinline__ void cp_async16(double* smem, const double* gmem) {
   const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem) : "memory");
+}
+
+// 16 bytes of which the first `bytes` (0, 8 or 16) are copied, the rest zero-filled
+__device__ __forceinline__ void cp_async16n(double* smem, const double* gmem, int bytes) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa), "l"(gmem), "r"(bytes) : "memory");
 }
 
 // 16 bytes, zero-filled when !valid
@@ -396,8 +413,8 @@ __device__ __forceinline__ void m2l_patch(double* __restrict__ win, const double
       const int dy = iy - 2 - b;
       const double* trow = tab_lane + ((dz + 3) * kOff + (dy + 3)) * kOff * kTabP;
       // source row: window y = 2Y + iy, z = 2Z + iz (parent-aligned, parity-free)
-      const double* src = win + ((iz & 1) * 2 + (iy & 1)) * kWSub + (Z + (iz >> 1)) * kWPZ +
-                          (Y + (iy >> 1)) * kWPY;
+      const double2* src = reinterpret_cast<const double2*>(win) + ((iz & 1) * 2 + (iy & 1)) * kFSub +
+                           (Z + (iz >> 1)) * kFPZ + (Y + (iy >> 1)) * kFPY;
       // this lane's source row lies in neighbour row (oy, oz); internal patches there?
       const int wy = 2 * Y + iy, wz = 2 * Z + iz;
       const int oy = wy < 2 ? 0 : (wy > 9 ? 2 : 1), oz = wz < 2 ? 0 : (wz > 9 ? 2 : 1);
@@ -471,9 +488,10 @@ __global__ void __launch_bounds__(kM2lThreads, 1) amr_m2l_fused_kernel(
   }
   __syncthreads();
   // task = (window row (wy, wz), component), component fastest: a warp's
-  // copies of one x position read ~3 consecutive cells' 80-byte moments
-  for (int task = threadIdx.x; task < 1440; task += kM2lThreads) {
-    const int h = task % 10, row = task / 10;
+  // copies of one x position read ~3 consecutive cells' 80-byte moments;
+  // h = the 16-byte chunk of the records
+  for (int task = threadIdx.x; task < 144 * kFRec; task += kM2lThreads) {
+    const int h = task % kFRec, row = task / kFRec;
     const int wy = row % 12, wz = row / 12;
     int ly = wy - 2, lz = wz - 2;
     const int oy = ly < 0 ? -1 : (ly > 7 ? 1 : 0), oz = lz < 0 ? -1 : (lz > 7 ? 1 : 0);
@@ -484,17 +502,21 @@ __global__ void __launch_bounds__(kM2lThreads, 1) amr_m2l_fused_kernel(
     if (mass)
 #pragma unroll
       for (int q = 0; q < 3; ++q) lsl[q] = s_ls[r3 + q];
-    double* dst = win + h * kWVar + ((wz & 1) * 2 + (wy & 1)) * kWSub + (wz >> 1) * kWPZ +
-                  (wy >> 1) * kWPY;
+    double* dst = win + 2 * (((wz & 1) * 2 + (wy & 1)) * kFSub + (wz >> 1) * kFPZ + (wy >> 1) * kFPY + h);
     const long long rowoff = (long long)(lz * 8 + ly) * 8;
 #pragma unroll
     for (int wx = 0; wx < 12; ++wx) {
       const int ox = wx < 2 ? -1 : (wx > 9 ? 1 : 0), lx = wx - 2 - 8 * ox;
       const int nb = nbs[ox + 1], ls = lsl[ox + 1];
-      if (ls >= 0)  // leaf neighbour (mass given): m, then +0s
-        cp_async8(dst + wx, mass + (long long)ls * 512 + rowoff + lx, h == 0);
-      else
-        cp_async8(dst + wx, L.mom + ((long long)(nb < 0 ? n : nb) * 512 + rowoff + lx) * 10 + h, nb >= 0);
+      double* d = dst + 2 * kFRec * wx;
+      if (ls >= 0 && h == 0) {  // leaf neighbour (mass given): chunk 0 = (m, +0) (the mass is 8-byte aligned)
+        cp_async8(d, mass + (long long)ls * 512 + rowoff + lx, true);
+        cp_async8(d + 1, mass, false);
+      } else if (ls >= 0 || nb < 0) {  // its other chunks, and missing patches: +0s
+        cp_async16n(d, L.mom, 0);
+      } else {
+        cp_async16n(d, L.mom + ((long long)nb * 512 + rowoff + lx) * 10 + 2 * h, 16);
+      }
     }
   }
   const unsigned internal27 = s_int27;
