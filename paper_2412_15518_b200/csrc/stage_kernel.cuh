@@ -39,7 +39,7 @@ namespace tmgpu {
 
 constexpr int kE = 8, kG = 2, kS = 12;
 constexpr int kE2 = 64, kE3 = 512;
-constexpr int kStageThreads = 224;  // 7 warps x 30 face lanes >= 64 pencils x 3 segments
+constexpr int kStageThreads = 256;  // 8 warps: the face passes use 7 (30 lanes x 7 >= 64 pencils x 3 segments), the cell phases all 8
 constexpr double kRhoFloor = 1e-10;       // euler.hpp:15
 constexpr double kPressureFloor = 1e-12;  // euler.hpp:16
 
