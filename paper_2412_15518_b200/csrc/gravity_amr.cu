@@ -996,6 +996,8 @@ __global__ void __launch_bounds__(kL2pThreads, 4) amr_l2p_kernel(const GLv* __re
   const GLv L = Lv[l];
   const int d = l + 3;
   const double h = 1.0 / (double)(1LL << d);
+  // the patch's cell-grid origin (8 ijk), for the angular-momentum sums' positions
+  const long long g0[3] = {8LL * L.ijk[3 * n], 8LL * L.ijk[3 * n + 1], 8LL * L.ijk[3 * n + 2]};
   if (threadIdx.x < 27) {  // the 27 neighbour slots, resolved once
     const int o = threadIdx.x;
     const int nb = slot_nbs[s * 27 + o];
@@ -1111,12 +1113,12 @@ __global__ void __launch_bounds__(kL2pThreads, 4) amr_l2p_kernel(const GLv* __re
   g[2 * ncell + t] = gz;
   keep[hc][0] = gx, keep[hc][1] = gy, keep[hc][2] = gz;
   }
-  if (part) {
-    double x0[3], x1[3];
-    const int c0 = threadIdx.x, c1 = threadIdx.x + kL2pThreads;
-    cell_pos(Lv, l, n, c0, x0);
-    cell_pos(Lv, l, n, c1, x1);
-    am_block_sums2(mass[s * 512 + c0], x0, keep[0], mass[s * 512 + c1], x1, keep[1], part + s * 16);
+  if (part) {  // the two cells' masses from the window, positions from the patch origin (cell_pos's values)
+    const int c0 = threadIdx.x, i = c0 & 7, j = (c0 >> 3) & 7, k = c0 >> 6;  // c1 = c0 + 256: k + 4
+    const double x0[3] = {centre(g0[0] + i, d), centre(g0[1] + j, d), centre(g0[2] + k, d)};
+    const double x1[3] = {x0[0], x0[1], centre(g0[2] + k + 4, d)};
+    const double m0 = mw[((k + 1) * 10 + (j + 1)) * 24 + i + 2], m1 = mw[((k + 5) * 10 + (j + 1)) * 24 + i + 2];
+    am_block_sums2(m0, x0, keep[0], m1, x1, keep[1], part + s * 16);
   }
 }
 
