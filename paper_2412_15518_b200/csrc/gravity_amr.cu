@@ -165,13 +165,22 @@ __global__ void amr_m2m_kernel(const GLv* __restrict__ L, int l, const int* __re
       // leaf child cells carry (m, +0, ..., +0): read only m. Dropping the +0
       // terms can only turn a +0 term into -0, and a sum started at +0 is the
       // same either way, so the result is tmo_grav_m2m's bit for bit.
+      // the 8 children's masses loaded together (one round trip), then summed in order
+      double Ms[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const int a = q & 1, b = (q >> 1) & 1, cc = q >> 2;
+        const int cc8 = ((((2 * K) & 7) + cc) * 8 + ((2 * J) & 7) + b) * 8 + ((2 * I) & 7) + a;
+        Ms[q] = mass ? mass[(long long)lsl * 512 + cc8] : base[cc8 * 10];
+      }
+#pragma unroll
       for (int cc = 0; cc < 2; ++cc)
+#pragma unroll
         for (int b = 0; b < 2; ++b)
+#pragma unroll
           for (int a = 0; a < 2; ++a) {
             const double s[3] = {(a - 0.5) * hc, (b - 0.5) * hc, (cc - 0.5) * hc};
-            const int ci = ((2 * I) & 7) + a, cj = ((2 * J) & 7) + b, ck = ((2 * K) & 7) + cc;
-            const int cc8 = (ck * 8 + cj) * 8 + ci;
-            const double M = mass ? mass[(long long)lsl * 512 + cc8] : base[cc8 * 10];
+            const double M = Ms[(cc * 2 + b) * 2 + a];
             o[0] += M;
 #pragma unroll
             for (int i = 0; i < 3; ++i) o[1 + i] += M * s[i];
@@ -185,20 +194,29 @@ __global__ void amr_m2m_kernel(const GLv* __restrict__ L, int l, const int* __re
       for (int h = 0; h < 5; ++h) out[h] = make_double2(o[2 * h], o[2 * h + 1]);
       continue;
     }
+    // the 8 children's 80-byte records (five 16-byte loads each) loaded
+    // together, then summed in order
+    double2 rec[8][5];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int a = q & 1, b = (q >> 1) & 1, cc = q >> 2;
+      const double2* c2 = reinterpret_cast<const double2*>(
+          base + (((((2 * K) & 7) + cc) * 8 + ((2 * J) & 7) + b) * 8 + ((2 * I) & 7) + a) * 10);
+#pragma unroll
+      for (int h = 0; h < 5; ++h) rec[q][h] = c2[h];
+    }
+#pragma unroll
     for (int cc = 0; cc < 2; ++cc)
+#pragma unroll
       for (int b = 0; b < 2; ++b)
+#pragma unroll
         for (int a = 0; a < 2; ++a) {
           const double s[3] = {(a - 0.5) * hc, (b - 0.5) * hc, (cc - 0.5) * hc};
-          const int ci = ((2 * I) & 7) + a, cj = ((2 * J) & 7) + b, ck = ((2 * K) & 7) + cc;
-          double ch[10];  // the child's 80-byte record as five 16-byte loads
-          {
-            const double2* c2 = reinterpret_cast<const double2*>(base + ((ck * 8 + cj) * 8 + ci) * 10);
+          double ch[10];
 #pragma unroll
-            for (int h = 0; h < 5; ++h) {
-              const double2 v = c2[h];
-              ch[2 * h] = v.x;
-              ch[2 * h + 1] = v.y;
-            }
+          for (int h = 0; h < 5; ++h) {
+            ch[2 * h] = rec[(cc * 2 + b) * 2 + a][h].x;
+            ch[2 * h + 1] = rec[(cc * 2 + b) * 2 + a][h].y;
           }
           const double M = ch[0];
           o[0] += M;
