@@ -156,3 +156,22 @@ def test_distributed_regrid_reflux_bitwise_equals_single_gpu(extra):
                        timeout=900)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     assert "BITWISE_OK" in r.stdout, r.stdout[-3000:]
+
+
+@pytest.mark.gpu
+def test_peer_wait_is_bounded_when_a_peer_stops():
+    """A rank whose peer stops stepping fails its next peer-memory step after
+    TMGPU_PEER_TIMEOUT_S instead of hanging (tests/mgpu_peer_timeout.py)."""
+    import torch
+
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs 2 GPUs (gpurun --gpus 2)")
+    script = os.path.join(ROOT, "tests", "mgpu_peer_timeout.py")
+    env = dict(os.environ, TMGPU_PEER_TIMEOUT_S="2", CUDA_VISIBLE_DEVICES="0,1")
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+                        "--master-addr", "127.0.0.1", "--master-port", "29539", script],
+                       capture_output=True, text=True, timeout=180, env=env)
+    assert "PEER_TIMEOUT_OK" in r.stdout, r.stdout[-3000:] + r.stderr[-3000:]
+    elapsed = float(r.stdout.split("PEER_TIMEOUT_OK")[1].split()[0])
+    assert elapsed < 15.0, r.stdout[-2000:]
+
