@@ -803,21 +803,27 @@ __device__ __forceinline__ void wx_leaf_entries(const GLv* __restrict__ Lv, cons
 // order, one thread per target with entries (targets in patch order);
 // geometry from the plan's separation table (m2l_geom of each distinct R).
 // Leaf-patch targets update their compact L0, L_i only.
-__global__ void __launch_bounds__(128, 4) amr_wx_kernel(const GLv* __restrict__ Lv, const int* __restrict__ tlev,
-                                                        const long long* __restrict__ tflat, long long ntarget,
+// A W/X target resolved with the plan: its entry range, and where its locals
+// live (leaf: the compact leaf locals at `off`; internal: level l's loc at
+// flat `off`) — one 32-byte load instead of a chain of dependent lookups.
+struct WxTarget {
+  long long e0, e1, off;
+  int level, leaf;
+};
+
+__global__ void __launch_bounds__(128, 4) amr_wx_kernel(const GLv* __restrict__ Lv,
+                                                        const WxTarget* __restrict__ targets, long long ntarget,
                                                         const double* __restrict__ geo,
-                                                        double* __restrict__ lloc, long long lo,
+                                                        double* __restrict__ lloc,
                                                         const double* __restrict__ mass,
                                                         const double* __restrict__ geo4) {
   for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < ntarget;
        t += (long long)gridDim.x * blockDim.x) {
-    const int l = tlev[t];
-    const long long flat = tflat[t];
-    const long long* moff = Lv[l].moff;
-    const long long e0 = moff[flat], e1 = moff[flat + 1];
-    const int leaf = Lv[l].leaf_slot[flat >> 9];
-    if (leaf >= 0 && l > 0) {
-      double* p = lloc + (long long)(leaf - lo) * 2048 + (flat & 511);
+    const WxTarget d = targets[t];
+    const int l = d.level;
+    const long long e0 = d.e0, e1 = d.e1, flat = d.off;
+    if (d.leaf) {
+      double* p = lloc + d.off;
       double acc[4] = {p[0], p[512], p[1024], p[1536]};
       if (mass)
         wx_leaf_entries(Lv, Lv[l].ment, Lv[l].mgeo, Lv[l].mmi, mass, e0, e1, geo, geo4, acc);
@@ -1545,8 +1551,7 @@ struct GravAmrWork {
   long long m2l_local = 0;   // the first m2l_local fused patches read only this rank's subtrees
   cudaEvent_t ev_up = nullptr, ev_fl = nullptr;  // owned upward pass done; local fused M2L done
   long long u_max = 0;  // most cross-depth U entries of a level
-  int* wx_tlev = nullptr;         // W/X kernel targets (level, flat), in patch order
-  long long* wx_tflat = nullptr;
+  WxTarget* wx_targets_dev = nullptr;  // W/X kernel targets, in patch order
   long long wx_targets = 0;
 
   double* wx_geo = nullptr;  // [distinct W/X separations][13]
@@ -1856,8 +1861,7 @@ static cudaError_t build_m2l_work(GravAmrWork& w, const std::vector<std::vector<
   drop(reinterpret_cast<void*&>(w.m2l_work));
   drop(reinterpret_cast<void*&>(w.mono_slots));
   w.mono_ctas = (long long)mono.size();
-  drop(reinterpret_cast<void*&>(w.wx_tlev));
-  drop(reinterpret_cast<void*&>(w.wx_tflat));
+  drop(reinterpret_cast<void*&>(w.wx_targets_dev));
 
   w.m2l_ctas = (long long)wk.size();
   // targets with W/X entries among the M2L patches, in patch order (source locality)
@@ -1870,19 +1874,24 @@ static cudaError_t build_m2l_work(GravAmrWork& w, const std::vector<std::vector<
       if (cnt) tg.push_back({-cnt, {x.x, f}});
     }
   }
-  std::vector<int> tl(tg.size());
-  std::vector<long long> tf(tg.size());
-  for (size_t i = 0; i < tg.size(); ++i) tl[i] = tg[i].second.first, tf[i] = tg[i].second.second;
+  std::vector<WxTarget> td(tg.size());
+  for (size_t i = 0; i < tg.size(); ++i) {
+    const int l = tg[i].second.first;
+    const long long f = tg[i].second.second;
+    const GravLevel& L = w.plan.lv[l];
+    const int leaf = L.leaf_slot[(size_t)(f >> 9)];
+    const bool lt = leaf >= 0 && l > 0;
+    td[i] = WxTarget{L.moff[(size_t)f], L.moff[(size_t)f + 1], lt ? (long long)(leaf - w.lo) * 2048 + (f & 511) : f,
+                     l, lt ? 1 : 0};
+  }
   w.wx_targets = (long long)tg.size();
 
   cudaError_t e = upload(wk, &w.m2l_work);
   if (w.m2l_work) w.allocs.push_back(w.m2l_work);
   if (e == cudaSuccess) e = upload(mono, &w.mono_slots);
   if (w.mono_slots) w.allocs.push_back(w.mono_slots);
-  if (e == cudaSuccess) e = upload(tl, &w.wx_tlev);
-  if (w.wx_tlev) w.allocs.push_back(w.wx_tlev);
-  if (e == cudaSuccess) e = upload(tf, &w.wx_tflat);
-  if (w.wx_tflat) w.allocs.push_back(w.wx_tflat);
+  if (e == cudaSuccess) e = upload(td, &w.wx_targets_dev);
+  if (w.wx_targets_dev) w.allocs.push_back(w.wx_targets_dev);
   return e;
 }
 
@@ -2375,9 +2384,8 @@ int tmgpu_gravity_amr_solve(tmgpu_gravity_amr* G, const double* mass, double* ph
       if (w.mono_ctas && !timed) cudaStreamWaitEvent(st, w.ev_join2, 0);
       if (m2l_pre) cudaStreamWaitEvent(st, w.ev_fl, 0);  // W/X follows every V sum
       if (w.wx_targets) {
-        amr_wx_kernel<<<grid_for(w.wx_targets), 128, 0, st>>>(w.dev_lv, w.wx_tlev, w.wx_tflat,
-                                                              w.wx_targets, w.wx_geo, w.lloc, w.lo, lmass,
-                                                              w.wx_geo4);
+        amr_wx_kernel<<<grid_for(w.wx_targets), 128, 0, st>>>(w.dev_lv, w.wx_targets_dev, w.wx_targets,
+                                                              w.wx_geo, w.lloc, lmass, w.wx_geo4);
         ++launches;
       }
       if (timed) cudaEventRecord(rec.k[3], st);
