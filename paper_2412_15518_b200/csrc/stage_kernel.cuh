@@ -75,7 +75,10 @@ struct Lay {
   // exactly V*512 doubles, contiguous) once the y pass has read them
   static constexpr int kU0 = XL;
   static_assert(YH + V * 128 - XL == V * kE3, "u0 fits the x/y face slabs");
-  static constexpr int kDoubles = kAcc + V * kAccV;
+  // the leaf's gravity field g[3][E^3] (Euler with gravity), bulk-copied at
+  // the start on its own mbarrier and read by the epilogue
+  static constexpr int kGv = kAcc + V * kAccV;
+  static constexpr int kDoubles = kGv + (V == 5 ? 3 * kE3 : 0);
   static constexpr int kBytes = kDoubles * 8 + 64;  // + mbarriers/scratch
   static constexpr uint32_t kTxBytes = (uint32_t)(V * 1408 * 8);
 };
@@ -431,14 +434,18 @@ __device__ __forceinline__ void axis_pass(const double* __restrict__ sm, double*
 // ------------------------------------------------------------------ epilogue
 // Gravity source (our spec): after the z update, before the
 // floors, with the stage input's primitives (oracle tmo_stage_subgrid_grav).
-__device__ __forceinline__ void grav_source(double (&u)[5], const StageLaunch& p, int slot, int c, double dt,
-                                            double rho, double iu, double iv, double iw) {
-  const double* gq = p.grav + (long long)slot * kE3 + c;
-  const double gx = gq[0], gy = gq[p.grav_stride], gz = gq[2 * p.grav_stride];
+__device__ __forceinline__ void grav_apply(double (&u)[5], double dt, double rho, double iu, double iv, double iw,
+                                           double gx, double gy, double gz) {
   u[1] = u[1] + dt * (rho * gx);
   u[2] = u[2] + dt * (rho * gy);
   u[3] = u[3] + dt * (rho * gz);
   u[4] = u[4] + dt * (rho * ((iu * gx + iv * gy) + iw * gz));
+}
+__device__ __forceinline__ void grav_source(double (&u)[5], const StageLaunch& p, int slot, int c, double dt,
+                                            double rho, double iu, double iv, double iw) {
+  const double* gq = p.grav + (long long)slot * kE3 + c;
+  const double gx = gq[0], gy = gq[p.grav_stride], gz = gq[2 * p.grav_stride];
+  grav_apply(u, dt, rho, iu, iv, iw, gx, gy, gz);
 }
 
 // stage.cpp:187-208 density and pressure floors; returns the floor hits
@@ -504,6 +511,8 @@ __global__ void __launch_bounds__(kStageThreads, 2)
   unsigned int& s_hits = *reinterpret_cast<unsigned int*>(smem + L::kDoubles + 1);
   unsigned int& s_bad = *(reinterpret_cast<unsigned int*>(smem + L::kDoubles + 1) + 1);
   uint64_t* bar_u0 = reinterpret_cast<uint64_t*>(smem + L::kDoubles + 2);
+  uint64_t* bar_g = reinterpret_cast<uint64_t*>(smem + L::kDoubles + 3);
+  const bool want_g = V == 5 && p.grav && !p.defer;
   const bool want_u0 = p.u0 && p.rk_stage >= 2 && !p.defer;
 
   const int tid = threadIdx.x;
@@ -515,6 +524,15 @@ __global__ void __launch_bounds__(kStageThreads, 2)
     s_bad = 0xffffffffu;
     mbar_init(bar, 1);
     mbar_init(bar_u0, 1);
+    if constexpr (V == 5) {
+      if (want_g) {  // g[3][E^3] of this leaf, needed only by the epilogue
+        mbar_init(bar_g, 1);
+        mbar_expect_tx(bar_g, 3 * kE3 * 8);
+#pragma unroll
+        for (int q = 0; q < 3; ++q)
+          bulk_load(smem + L::kGv + q * kE3, p.grav + q * p.grav_stride + (long long)slot * kE3, kE3 * 8, bar_g);
+      }
+    }
     mbar_expect_tx(bar, L::kTxBytes);
     tma_load_5d(sm + L::B0, &tm_i, bar, 2, 2, 2, 0, slot);
     // face f = 2*axis + side; own ghost layer or the same-level neighbour's
@@ -672,6 +690,7 @@ __global__ void __launch_bounds__(kStageThreads, 2)
   unsigned int hits = 0, bad = 0xffffffffu;
   const double* u0p = want_u0 ? smem + L::kU0 : nullptr;
   if (want_u0) mbar_wait(bar_u0, 0);
+  if (want_g) mbar_wait(bar_g, 0);
   for (int c = tid; c < kE3; c += kStageThreads) {
     double u[V];
 #pragma unroll
@@ -679,7 +698,8 @@ __global__ void __launch_bounds__(kStageThreads, 2)
     if constexpr (V == 5) {
       if (euler && p.grav) {  // gravity source with the stage input's primitives
         const double* pq = sm + L::B0 + (c >> 3) * 10 + (c & 7);
-        grav_source(u, p, slot, c, dt, pq[0], pq[640], pq[1280], pq[1920]);
+        const double* sg = smem + L::kGv + c;
+        grav_apply(u, dt, pq[0], pq[640], pq[1280], pq[1920], sg[0], sg[kE3], sg[2 * kE3]);
       }
       if (euler) hits += euler_floors<FAST>(u, gm1);
     }
