@@ -205,6 +205,10 @@ def time_reference(args, steps, warmup=0, budget_s=None):
     (oracle/gravity_amr_sparse.c: tabulated geometry, SIMD V lists, OpenMP;
     its topology plan built once, like the GPU's) at the same solves per step.
     Returns (median s/step, cores, mean phase seconds, steps timed, leaves, detail)."""
+    # torchrun sets OMP_NUM_THREADS=1 in every process of a multi-process launch;
+    # only rank 0 works here, so give the CPU path (its OpenMP FMM) all host
+    # cores before the oracle library starts its thread pool
+    os.environ["OMP_NUM_THREADS"] = str(os.cpu_count() or 1)
     from oracle import oracle as O
 
     ref = O.Ref()
