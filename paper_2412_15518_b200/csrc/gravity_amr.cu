@@ -1084,25 +1084,37 @@ __global__ void __launch_bounds__(kL2pThreads, 4) amr_l2p_kernel(const GLv* __re
     for (int q = 0; q < 4; ++q) loc4[q] = sh[q] + loc4[q];
   }
   double p = loc4[0], gx = -loc4[1], gy = -loc4[2], gz = -loc4[3];
+  // the 26 same-depth neighbours; a neighbour in a missing patch is skipped —
+  // a check needed only when some of the 27 patches is missing (valid27 is
+  // the same for the whole CTA, so the branch does not diverge)
+  auto p2p = [&](auto check_c) {
+    constexpr bool CHECK = decltype(check_c)::value;
 #pragma unroll
-  for (int dz = -1; dz <= 1; ++dz)
+    for (int dz = -1; dz <= 1; ++dz)
 #pragma unroll
-    for (int dy = -1; dy <= 1; ++dy)
+      for (int dy = -1; dy <= 1; ++dy)
 #pragma unroll
-      for (int dx = -1; dx <= 1; ++dx) {
-        if (!dx && !dy && !dz) continue;
-        const int lx = i + dx, ly = j + dy, lz = k + dz;
-        const int ox = lx < 0 ? -1 : (lx > 7 ? 1 : 0), oy = ly < 0 ? -1 : (ly > 7 ? 1 : 0),
-                  oz = lz < 0 ? -1 : (lz > 7 ? 1 : 0);
-        if (!((valid27 >> (((oz + 1) * 3 + (oy + 1)) * 3 + ox + 1)) & 1u)) continue;
-        // -m 2^d and -m 2^2d against the unit geometry: p2p_geom's terms exactly
-        const double nm1 = -(mw[((lz + 1) * 10 + (ly + 1)) * 24 + lx + 2] * sc1), nm2 = nm1 * sc1;
-        const int o = ((dz + 1) * 3 + (dy + 1)) * 3 + dx + 1;
-        p = fma(nm1, c_p2p_unit[o][0], p);
-        gx = fma(nm2, c_p2p_unit[o][1], gx);
-        gy = fma(nm2, c_p2p_unit[o][2], gy);
-        gz = fma(nm2, c_p2p_unit[o][3], gz);
-      }
+        for (int dx = -1; dx <= 1; ++dx) {
+          if (!dx && !dy && !dz) continue;
+          const int lx = i + dx, ly = j + dy, lz = k + dz;
+          if (CHECK) {
+            const int ox = lx < 0 ? -1 : (lx > 7 ? 1 : 0), oy = ly < 0 ? -1 : (ly > 7 ? 1 : 0),
+                      oz = lz < 0 ? -1 : (lz > 7 ? 1 : 0);
+            if (!((valid27 >> (((oz + 1) * 3 + (oy + 1)) * 3 + ox + 1)) & 1u)) continue;
+          }
+          // -m 2^d and -m 2^2d against the unit geometry: p2p_geom's terms exactly
+          const double nm1 = -(mw[((lz + 1) * 10 + (ly + 1)) * 24 + lx + 2] * sc1), nm2 = nm1 * sc1;
+          const int o = ((dz + 1) * 3 + (dy + 1)) * 3 + dx + 1;
+          p = fma(nm1, c_p2p_unit[o][0], p);
+          gx = fma(nm2, c_p2p_unit[o][1], gx);
+          gy = fma(nm2, c_p2p_unit[o][2], gy);
+          gz = fma(nm2, c_p2p_unit[o][3], gz);
+        }
+  };
+  if (valid27 == 0x7ffffffu)
+    p2p(std::integral_constant<bool, false>{});
+  else
+    p2p(std::integral_constant<bool, true>{});
   const long long e0 = L.poff[flat], e1 = L.poff[flat + 1];
   long long e = e0;
   for (; e + 3 < e1; e += 4) {  // cross-depth U pairs, sorted by source: 4 entries' loads in flight
