@@ -106,7 +106,6 @@ struct tmgpu_forest {
   // peer-memory exchange (tmgpu_forest_set_peer), valid for `peer_version`
   bool peer = false;
   uint64_t peer_version = ~0ull;
-  unsigned long long peer_seq = 0;
   PeerTab ptab{};
   unsigned long long* peer_flags = nullptr;
   PackItem* pack_peer = nullptr;
@@ -174,7 +173,6 @@ void peer_close(tmgpu_forest* f, bool collective = false) {
   f->ptab = PeerTab{};
   f->peer = false;
   f->peer_version = ~0ull;
-  f->peer_seq = 0;
 }
 
 // Drop the cached step graphs (whatever a step enqueues is about to change).
@@ -376,14 +374,17 @@ int exchange(tmgpu_forest* f, cudaStream_t st, ExchangeMode mode, std::string* w
         if (why) *why = "peer exchange: topology changed; call tmgpu_forest_set_peer again";
         return TMGPU_ERR_INVALID;
       }
-      const unsigned long long seq = ++f->peer_seq;
-      e = halo_pack_peer(f->arena(), prev, V, f->pack_peer, f->n_pack, f->slabs, f->ptab, seq, st);
+      // this round's sequence number lives in device memory (a captured step
+      // replays with a new one); every rank runs the same rounds
+      e = seq_bump(f->ptab.seqp, st);
+      if (e == cudaSuccess)
+        e = halo_pack_peer(f->arena(), prev, V, f->pack_peer, f->n_pack, f->slabs, f->ptab, st);
       // every face: one list whose faces all wait for the senders
       if (e == cudaSuccess)
         e = all ? halo_pull_peer(f->arena(), V, f->faces, f->pull_all, 0, f->n_pull_all, f->slabs,
-                                 f->ptab, seq, st)
+                                 f->ptab, st)
                 : halo_pull_peer(f->arena(), V, f->faces, f->pull_peer, f->n_pull_local,
-                                 f->n_pull_fused, f->slabs, f->ptab, seq, st);
+                                 f->n_pull_fused, f->slabs, f->ptab, st);
       if (e != cudaSuccess) {
         if (why) *why = std::string("peer ghost exchange: ") + cudaGetErrorString(e);
         return TMGPU_ERR_CUDA;
@@ -1217,8 +1218,9 @@ int tmgpu_forest_set_peer(tmgpu_forest* f, int on, tmgpu_error* err) {
       if (out[(size_t)q * kRec + kOk] != 1.0) return false;
     return true;
   };
-  e = cudaMalloc((void**)&f->peer_flags, (3 * world + 1) * sizeof(unsigned long long));
-  if (e == cudaSuccess) e = cudaMemset(f->peer_flags, 0, (3 * world + 1) * sizeof(unsigned long long));
+  // flag words [0, 3w] (PeerTab::mine) and this rank's sequence counter at [3w + 1]
+  e = cudaMalloc((void**)&f->peer_flags, (3 * world + 2) * sizeof(unsigned long long));
+  if (e == cudaSuccess) e = cudaMemset(f->peer_flags, 0, (3 * world + 2) * sizeof(unsigned long long));
   cudaIpcMemHandle_t hs{}, hf{};
   if (e == cudaSuccess) e = cudaIpcGetMemHandle(&hs, f->slabs);
   if (e == cudaSuccess) e = cudaIpcGetMemHandle(&hf, f->peer_flags);
@@ -1232,6 +1234,7 @@ int tmgpu_forest_set_peer(tmgpu_forest* f, int on, tmgpu_error* err) {
   PeerTab t{};
   t.spin_ns = peer_spin_ns();
   t.mine = f->peer_flags;
+  t.seqp = f->peer_flags + 3 * world + 1;
   t.me = me;
   t.world = world;
   for (int q = 0; q < world && ok && e == cudaSuccess; ++q) {
@@ -1283,7 +1286,6 @@ int tmgpu_forest_set_peer(tmgpu_forest* f, int on, tmgpu_error* err) {
   f->ptab = t;
   f->peer = true;
   f->peer_version = f->forest.topology_version();
-  f->peer_seq = 0;
   return TMGPU_OK;
 }
 

@@ -1492,6 +1492,7 @@ struct LetPeer {
   unsigned long long* flags[kMaxLetPeers];  // peers' flag words (IPC-mapped)
   double* part[kMaxLetPeers];               // peers' AM sum arrays (IPC-mapped)
   unsigned long long* mine;                 // this rank's flag words (GravAmrWork::pflags)
+  unsigned long long* seqp;                 // this rank's solve sequence number (pflags[4R])
   int n_push[kMaxLetPeers];                 // push CTAs per destination
   int me, world, nl;
   unsigned recv_mask;                       // ranks that store patches into this one
@@ -1576,7 +1577,6 @@ struct GravAmrWork {
   // peer-memory LET exchange (tmgpu_gravity_amr_set_peer): subtree roots and
   // halo patches stored straight into the peers' level moment arrays
   bool peer = false;
-  unsigned long long peer_seq = 0;
   LetPeer pt{};
   // [0,R) moment arrival, [R,2R) consumption, [2R,3R) push counters, [3R,4R) AM-sum arrival
   unsigned long long* pflags = nullptr;
@@ -1592,8 +1592,8 @@ struct GravAmrWork {
 // and the last CTA for a destination raises its arrival flag.
 __global__ void __launch_bounds__(256) let_push_kernel(const GLv* __restrict__ Lv,
                                                        const int4* __restrict__ items,
-                                                       double* const* __restrict__ peer_mom, LetPeer t,
-                                                       unsigned long long seq) {
+                                                       double* const* __restrict__ peer_mom, LetPeer t) {
+  const unsigned long long seq = *t.seqp;  // this solve's (let_bump_kernel ran before on the stream)
   const int4 it = items[blockIdx.x];
   const int q = it.z;
   if (threadIdx.x == 0) spin_geq(t.mine + t.world + q, seq - 1, t.spin_ns);
@@ -1613,7 +1613,8 @@ __global__ void __launch_bounds__(256) let_push_kernel(const GLv* __restrict__ L
   }
 }
 
-__global__ void let_wait_kernel(LetPeer t, unsigned long long seq) {
+__global__ void let_wait_kernel(LetPeer t) {
+  const unsigned long long seq = *t.seqp;
   if (threadIdx.x == 0)
     for (int s = 0; s < t.world; ++s)
       if (t.recv_mask >> s & 1u) spin_geq(t.mine + s, seq, t.spin_ns);
@@ -1621,7 +1622,8 @@ __global__ void let_wait_kernel(LetPeer t, unsigned long long seq) {
 
 // after the solve's last reader of received patches and AM sums: every rank
 // that stores into this one may store the next solve's
-__global__ void let_done_kernel(LetPeer t, unsigned long long seq) {
+__global__ void let_done_kernel(LetPeer t) {
+  const unsigned long long seq = *t.seqp;
   if (threadIdx.x == 0) {
     __threadfence_system();
     const unsigned from = t.recv_mask | t.am_mask;
@@ -1632,8 +1634,8 @@ __global__ void let_done_kernel(LetPeer t, unsigned long long seq) {
 
 // AM sums: this rank's slot segment of `part` to every peer (same offsets),
 // kAmPushCtas CTAs per destination; arrival flags at [3R + me].
-__global__ void __launch_bounds__(256) am_push_kernel(const double* __restrict__ part, LetPeer t,
-                                                      unsigned long long seq) {
+__global__ void __launch_bounds__(256) am_push_kernel(const double* __restrict__ part, LetPeer t) {
+  const unsigned long long seq = *t.seqp;
   int q = blockIdx.x / kAmPushCtas;
   q += q >= t.me;
   const int c = blockIdx.x % kAmPushCtas;
@@ -1654,7 +1656,11 @@ __global__ void __launch_bounds__(256) am_push_kernel(const double* __restrict__
   }
 }
 
-__global__ void am_wait_kernel(LetPeer t, unsigned long long seq) {
+// the next solve's sequence number (one thread, stream-ordered)
+__global__ void let_bump_kernel(unsigned long long* p) { *p += 1; }
+
+__global__ void am_wait_kernel(LetPeer t) {
+  const unsigned long long seq = *t.seqp;
   if (threadIdx.x == 0)
     for (int s = 0; s < t.world; ++s)
       if (t.am_mask >> s & 1u) spin_geq(t.mine + 3 * t.world + s, seq, t.spin_ns);
@@ -1680,7 +1686,6 @@ static void let_peer_close(GravAmrWork& w, bool collective = false) {
   w.n_push = 0;
   w.pt = LetPeer{};
   w.peer = false;
-  w.peer_seq = 0;
 }
 
 // Distributed: base[slot * per_slot ..] of every rank's slot range to every
@@ -2315,10 +2320,11 @@ int tmgpu_gravity_amr_solve(tmgpu_gravity_amr* G, const double* mass, double* ph
     if (w.peer) {
       // roots to every peer and halo patches to their readers, straight into
       // the peers' moment arrays; then the shared top as below
-      const unsigned long long seq = ++w.peer_seq;
+      let_bump_kernel<<<1, 1, 0, st>>>(w.pt.seqp);  // device-side: a captured solve replays
+      ++launches;
       if (w.n_push)
-        let_push_kernel<<<(unsigned)w.n_push, 256, 0, st>>>(w.dev_lv, w.push, w.peer_mom, w.pt, seq);
-      let_wait_kernel<<<1, 32, 0, st>>>(w.pt, seq);
+        let_push_kernel<<<(unsigned)w.n_push, 256, 0, st>>>(w.dev_lv, w.push, w.peer_mom, w.pt);
+      let_wait_kernel<<<1, 32, 0, st>>>(w.pt);
       launches += 2;
       for (int l = P.nlevels - 2; l >= 0; --l) {
         if (!w.n_top[l]) continue;
@@ -2431,8 +2437,8 @@ int tmgpu_gravity_amr_solve(tmgpu_gravity_amr* G, const double* mass, double* ph
     if (timed) cudaEventRecord(rec.ev[5], st);
     if (am) {  // the per-slot sums came with L2P
       if (w.peer && e == cudaSuccess) {  // identical global pair tree on every rank
-        am_push_kernel<<<(unsigned)((w.pt.world - 1) * kAmPushCtas), 256, 0, st>>>(w.part, w.pt, w.peer_seq);
-        am_wait_kernel<<<1, 32, 0, st>>>(w.pt, w.peer_seq);
+        am_push_kernel<<<(unsigned)((w.pt.world - 1) * kAmPushCtas), 256, 0, st>>>(w.part, w.pt);
+        am_wait_kernel<<<1, 32, 0, st>>>(w.pt);
         launches += 2;
       } else if (w.comm && e == cudaSuccess) {
         rc = allgather_slots(w, w.part, 16, st, &e, &why);
@@ -2459,7 +2465,7 @@ int tmgpu_gravity_amr_solve(tmgpu_gravity_amr* G, const double* mass, double* ph
       launches += 1;
     }
     if (w.peer) {  // every received patch and AM sum has been read
-      let_done_kernel<<<1, 32, 0, st>>>(w.pt, w.peer_seq);
+      let_done_kernel<<<1, 32, 0, st>>>(w.pt);
       ++launches;
     }
     g_launches.fetch_add(launches, std::memory_order_relaxed);
@@ -2586,8 +2592,9 @@ int tmgpu_gravity_amr_set_peer(tmgpu_gravity_amr* G, int on, tmgpu_error* err) {
       if (out[(size_t)q * rec_n + k_ok] != 1.0) return false;
     return true;
   };
-  e = cudaMalloc((void**)&w.pflags, 4 * R * sizeof(unsigned long long));
-  if (e == cudaSuccess) e = cudaMemset(w.pflags, 0, 4 * R * sizeof(unsigned long long));
+  // flag words [0, 4R) and this rank's sequence counter at [4R]
+  e = cudaMalloc((void**)&w.pflags, (4 * R + 1) * sizeof(unsigned long long));
+  if (e == cudaSuccess) e = cudaMemset(w.pflags, 0, (4 * R + 1) * sizeof(unsigned long long));
   cudaIpcMemHandle_t h{};
   if (e == cudaSuccess) e = cudaIpcGetMemHandle(&h, w.pflags);
   std::memcpy(&rec[0], &h, 64);
@@ -2601,6 +2608,7 @@ int tmgpu_gravity_amr_set_peer(tmgpu_gravity_amr* G, int on, tmgpu_error* err) {
   LetPeer t{};
   t.spin_ns = peer_spin_ns();
   t.mine = w.pflags;
+  t.seqp = w.pflags + 4 * R;
   t.me = me;
   t.world = R;
   t.nl = nl;

@@ -182,8 +182,8 @@ __global__ void __launch_bounds__(128) pull_kernel(double* __restrict__ arena, i
 __global__ void __launch_bounds__(128) pack_peer_kernel(const double* __restrict__ arena,
                                                         const double* __restrict__ prev, int V,
                                                         const PackItem* __restrict__ items,
-                                                        double* __restrict__ slabs, PeerTab t,
-                                                        unsigned long long seq) {
+                                                        double* __restrict__ slabs, PeerTab t) {
+  const unsigned long long seq = *t.seqp;  // this round's (seq_bump ran before on the stream)
   const PackItem it = items[blockIdx.x];
   const int q = it.pad[0] - 1;
   if (q < 0) {
@@ -212,8 +212,8 @@ __global__ void __launch_bounds__(128) pull_peer_kernel(double* __restrict__ are
                                                         const FaceSrc* __restrict__ faces,
                                                         const int2* __restrict__ items,
                                                         const double* __restrict__ slabs,
-                                                        PeerTab t, int n_local, int n_remote,
-                                                        unsigned long long seq) {
+                                                        PeerTab t, int n_local, int n_remote) {
+  const unsigned long long seq = *t.seqp;
   const bool remote = (int)blockIdx.x >= n_local;
   if (remote) {
     if (threadIdx.x == 0)
@@ -236,7 +236,15 @@ __global__ void __launch_bounds__(128) pull_peer_kernel(double* __restrict__ are
   }
 }
 
+__global__ void seq_bump_kernel(unsigned long long* p) { *p += 1; }
+
 }  // namespace
+
+cudaError_t seq_bump(unsigned long long* p, cudaStream_t st) {
+  seq_bump_kernel<<<1, 1, 0, st>>>(p);
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return cudaGetLastError();
+}
 
 cudaError_t halo_pack(const double* arena, const double* prev, int V, const PackItem* items,
                       int n_items, double* slabs, cudaStream_t st) {
@@ -255,20 +263,19 @@ cudaError_t halo_pull(double* arena, int V, const FaceSrc* faces, const int2* it
 }
 
 cudaError_t halo_pack_peer(const double* arena, const double* prev, int V, const PackItem* items,
-                           int n_items, double* slabs, const PeerTab& t, unsigned long long seq,
-                           cudaStream_t st) {
+                           int n_items, double* slabs, const PeerTab& t, cudaStream_t st) {
   if (n_items <= 0) return cudaSuccess;
-  pack_peer_kernel<<<n_items, 128, 0, st>>>(arena, prev, V, items, slabs, t, seq);
+  pack_peer_kernel<<<n_items, 128, 0, st>>>(arena, prev, V, items, slabs, t);
   g_launches.fetch_add(1, std::memory_order_relaxed);
   return cudaGetLastError();
 }
 
 cudaError_t halo_pull_peer(double* arena, int V, const FaceSrc* faces, const int2* items,
                            int n_local, int n_items, const double* slabs, const PeerTab& t,
-                           unsigned long long seq, cudaStream_t st) {
+                           cudaStream_t st) {
   if (n_items <= 0) return cudaSuccess;
   pull_peer_kernel<<<n_items, 128, 0, st>>>(arena, V, faces, items, slabs, t, n_local,
-                                            n_items - n_local, seq);
+                                            n_items - n_local);
   g_launches.fetch_add(1, std::memory_order_relaxed);
   return cudaGetLastError();
 }

@@ -57,14 +57,20 @@ struct PeerTab {
   int me, world;
   unsigned recv_mask;                     // peers this rank receives slabs from
   unsigned long long spin_ns;             // flag-wait limit (peer_spin_ns(); 0 = none)
+  // this rank's exchange sequence number in device memory ([3w + 1] of its
+  // flag words): bumped by seq_bump() at the start of every exchange and read
+  // by the exchange's kernels, so a captured step (CUDA graph) replays correctly
+  unsigned long long* seqp;
 };
 
+// *p += 1 on the stream (one thread): the next exchange round's sequence number
+cudaError_t seq_bump(unsigned long long* p, cudaStream_t st);
+
 cudaError_t halo_pack_peer(const double* arena, const double* prev, int V, const PackItem* items,
-                           int n_items, double* slabs, const PeerTab& t, unsigned long long seq,
-                           cudaStream_t st);
+                           int n_items, double* slabs, const PeerTab& t, cudaStream_t st);
 cudaError_t halo_pull_peer(double* arena, int V, const FaceSrc* faces, const int2* items,
                            int n_local, int n_items, const double* slabs, const PeerTab& t,
-                           unsigned long long seq, cudaStream_t st);
+                           cudaStream_t st);
 
 cudaError_t halo_pack(const double* arena, const double* prev, int V, const PackItem* items,
                       int n_items, double* slabs, cudaStream_t st);
