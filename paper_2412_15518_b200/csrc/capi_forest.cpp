@@ -1146,8 +1146,10 @@ int tmgpu_forest_step_io(tmgpu_forest* f, const double* in_compact, double* out_
     const char* v = std::getenv("TMGPU_GRAPHS");
     return !(v && v[0] == '0');
   }();
-  const bool use_graph = graphs_env && !(flags & TMGPU_NO_GRAPH) && f->graph_warm && f->graph_captures < 32 && !timed && f->world() == 1 &&
-                         !f->peer &&
+  // (distributed too: the peer protocols' sequence numbers live in device
+  // memory and NCCL calls are captured like kernels; every rank captures the
+  // same step)
+  const bool use_graph = graphs_env && !(flags & TMGPU_NO_GRAPH) && f->graph_warm && f->graph_captures < 32 && !timed &&
                          (!f->gsolver || tmgpu_gravity_amr_graph_safe(f->gsolver)) &&
                          (cadence || !f->grav_stream);
   {

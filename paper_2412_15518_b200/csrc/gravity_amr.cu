@@ -2727,9 +2727,10 @@ int tmgpu_gravity_amr_timing(tmgpu_gravity_amr* G, double* ms, long long* solves
 }
 
 // Whether a solve enqueues the same work every call with no host-side state
-// (so a CUDA graph may capture it): not timing, not distributed.
+// (so a CUDA graph may capture it): not timing (distributed solves qualify:
+// their peer sequence numbers are in device memory, their NCCL calls capture).
 bool tmgpu_gravity_amr_graph_safe(const tmgpu_gravity_amr* G) {
-  return G && !G->w.timing && !G->w.let && !G->w.peer;
+  return G && !G->w.timing;
 }
 
 // Leaf-cell masses currently in the workspace ([slot][512], device pointer).

@@ -13,7 +13,7 @@
 #include "../../include/tmgpu.h"
 
 // gravity_amr.cu: may a CUDA graph capture this solver's solve (no host-side
-// state per call: not timing, not distributed)?
+// state per call: not timing)?
 extern "C" bool tmgpu_gravity_amr_graph_safe(const tmgpu_gravity_amr* G);
 
 namespace tmgpu {
