@@ -17,7 +17,7 @@
 
 using namespace tmgpu;
 
-constexpr int kGraphKey = 8;
+constexpr int kGraphKey = 9;
 struct StepGraph {
   uint64_t key[kGraphKey];
   cudaGraphExec_t exec;
@@ -1057,7 +1057,8 @@ int step_graph(tmgpu_forest* f, const double* in_compact, double* out_compact, d
   };
   const uint64_t key[kGraphKey] = {(uint64_t)f->cur, (uint64_t)(uintptr_t)in_compact,
                                    (uint64_t)(uintptr_t)out_compact, cfl > 0.0 ? 0 : bits(dt), bits(cfl), bits(gamma),
-                                   (uint64_t)(unsigned)flags, f->forest.topology_version()};
+                                   (uint64_t)(unsigned)flags, f->forest.topology_version(),
+                                   tmgpu_gravity_amr_version(f->gsolver)};
   cudaError_t e = cudaSuccess;
   if (!f->graph_stream) {
     e = cudaStreamCreateWithFlags(&f->graph_stream, cudaStreamNonBlocking);

@@ -1536,6 +1536,7 @@ struct GravAmrWork {
   long long seg_max = 0;                   // largest rank segment (slots)
   // locally essential tree (grav_let_plan): device lists and buffers
   bool let = false;
+  unsigned long long version = 0;  // bumped by distribute / set_peer (a forest's cached step graph keys on it)
   bool root_leaf = false;  // a level-0 patch is a leaf (the dense top M2M reads its moments)
   std::vector<int*> let_owned, let_top;    // per level internal patch lists
   std::vector<long long> n_owned, n_top;
@@ -2505,6 +2506,7 @@ int tmgpu_gravity_amr_distribute(tmgpu_gravity_amr* G, tmgpu_comm* comm, const l
   if (err) std::memset(err, 0, sizeof(*err));
   if (!G || !comm || !slot_bounds) return set_err(err, TMGPU_ERR_INVALID, "gravity distribute: null argument");
   GravAmrWork& w = G->w;
+  ++w.version;
   const GravPlan& P = w.plan;
   const int R = comm_world(comm), me = comm_rank(comm);
   if (slot_bounds[0] != 0 || slot_bounds[R] != w.nslots)
@@ -2561,6 +2563,7 @@ int tmgpu_gravity_amr_set_peer(tmgpu_gravity_amr* G, int on, tmgpu_error* err) {
   if (err) std::memset(err, 0, sizeof(*err));
   if (!G) return set_err(err, TMGPU_ERR_INVALID, "null gravity solver");
   GravAmrWork& w = G->w;
+  ++w.version;
   let_peer_close(w, /*collective=*/true);
   if (!on) return TMGPU_OK;
   if (!w.let || !w.comm) return set_err(err, TMGPU_ERR_INVALID, "gravity peer exchange: call distribute first");
@@ -2732,6 +2735,8 @@ int tmgpu_gravity_amr_timing(tmgpu_gravity_amr* G, double* ms, long long* solves
 bool tmgpu_gravity_amr_graph_safe(const tmgpu_gravity_amr* G) {
   return G && !G->w.timing;
 }
+
+unsigned long long tmgpu_gravity_amr_version(const tmgpu_gravity_amr* G) { return G ? G->w.version : 0; }
 
 // Leaf-cell masses currently in the workspace ([slot][512], device pointer).
 const double* tmgpu_gravity_amr_mass_ptr(const tmgpu_gravity_amr* G) { return G ? G->w.mass : nullptr; }

@@ -15,6 +15,8 @@
 // gravity_amr.cu: may a CUDA graph capture this solver's solve (no host-side
 // state per call: not timing)?
 extern "C" bool tmgpu_gravity_amr_graph_safe(const tmgpu_gravity_amr* G);
+// ... and the solver's configuration version (distribute / set_peer bump it)
+extern "C" unsigned long long tmgpu_gravity_amr_version(const tmgpu_gravity_amr* G);
 
 namespace tmgpu {
 
