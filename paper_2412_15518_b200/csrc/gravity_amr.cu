@@ -1565,7 +1565,9 @@ struct GravAmrWork {
   long long m2l_local = 0;   // the first m2l_local fused patches read only this rank's subtrees
   cudaEvent_t ev_up = nullptr, ev_fl = nullptr;  // owned upward pass done; local fused M2L done
   long long u_max = 0;  // most cross-depth U entries of a level
-  WxTarget* wx_targets_dev = nullptr;  // W/X kernel targets, in patch order
+  WxTarget* wx_targets_dev = nullptr;  // W/X kernel targets: internal ones, then leaf ones, in patch order
+  long long wx_n_int = 0;              // the internal targets (their locals feed L2L)
+  cudaEvent_t ev_wx = nullptr, ev_wxl = nullptr;  // V sums done; leaf targets' W/X done
   long long wx_targets = 0;
 
   double* wx_geo = nullptr;  // [distinct W/X separations][13]
@@ -1902,7 +1904,11 @@ static cudaError_t build_m2l_work(GravAmrWork& w, const std::vector<std::vector<
     td[i] = WxTarget{L.moff[(size_t)f], L.moff[(size_t)f + 1], lt ? (long long)(leaf - w.lo) * 2048 + (f & 511) : f,
                      l, lt ? 1 : 0};
   }
+  // internal targets first (L2L reads their locals), then the leaf targets
+  // (only L2P reads theirs: their W/X runs beside the L2L chain)
+  std::stable_partition(td.begin(), td.end(), [](const WxTarget& t) { return !t.leaf; });
   w.wx_targets = (long long)tg.size();
+  w.wx_n_int = (long long)std::count_if(td.begin(), td.end(), [](const WxTarget& t) { return !t.leaf; });
 
   cudaError_t e = upload(wk, &w.m2l_work);
   if (w.m2l_work) w.allocs.push_back(w.m2l_work);
@@ -1937,6 +1943,8 @@ void tmgpu_gravity_amr_destroy(tmgpu_gravity_amr* G) {
   if (G->w.ev_fork2) cudaEventDestroy(G->w.ev_fork2);
   if (G->w.ev_up) cudaEventDestroy(G->w.ev_up);
   if (G->w.ev_fl) cudaEventDestroy(G->w.ev_fl);
+  if (G->w.ev_wx) cudaEventDestroy(G->w.ev_wx);
+  if (G->w.ev_wxl) cudaEventDestroy(G->w.ev_wxl);
   let_peer_close(G->w);
   for (void* p : G->w.allocs)
     if (p) cudaFree(p);
@@ -2079,6 +2087,8 @@ tmgpu_gravity_amr* tmgpu_gravity_amr_create(const int* leaves, long long nleaves
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&w.ev_fork2, cudaEventDisableTiming);
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&w.ev_up, cudaEventDisableTiming);
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&w.ev_fl, cudaEventDisableTiming);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&w.ev_wx, cudaEventDisableTiming);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&w.ev_wxl, cudaEventDisableTiming);
 
   for (int kind = 0; kind < 2 && e == cudaSuccess; ++kind) {
     const std::vector<double>& sep = kind == 0 ? P.wx_sep : P.u_sep;
@@ -2287,6 +2297,7 @@ int tmgpu_gravity_amr_solve(tmgpu_gravity_amr* G, const double* mass, double* ph
   }
   if (e == cudaSuccess && rc == TMGPU_OK) {
     long long launches = 0;
+    bool wx_beside = false;  // the leaf targets' W/X runs on the side stream (joined before L2P)
     // leaf cells' m is read from the leaf-mass array wherever a leaf moment
     // would be: the owned-subtree M2M (owned leaves), and after the moment
     // exchange the fused window, W/X and U (the masses of every other rank's
@@ -2402,9 +2413,20 @@ int tmgpu_gravity_amr_solve(tmgpu_gravity_amr* G, const double* mass, double* ph
       }
       if (w.mono_ctas && !timed) cudaStreamWaitEvent(st, w.ev_join2, 0);
       if (m2l_pre) cudaStreamWaitEvent(st, w.ev_fl, 0);  // W/X follows every V sum
-      if (w.wx_targets) {
-        amr_wx_kernel<<<grid_for(w.wx_targets), 128, 0, st>>>(w.dev_lv, w.wx_targets_dev, w.wx_targets,
-                                                              w.wx_geo, w.lloc, lmass, w.wx_geo4);
+      const long long nwx_leaf = w.wx_targets - w.wx_n_int;
+      wx_beside = !timed && nwx_leaf > 0;
+      if (wx_beside) {  // the leaf targets' W/X on the side stream, beside the L2L chain
+        cudaEventRecord(w.ev_wx, st);
+        cudaStreamWaitEvent(w.side2, w.ev_wx, 0);
+        amr_wx_kernel<<<grid_for(nwx_leaf), 128, 0, w.side2>>>(w.dev_lv, w.wx_targets_dev + w.wx_n_int, nwx_leaf,
+                                                                w.wx_geo, w.lloc, lmass, w.wx_geo4);
+        cudaEventRecord(w.ev_wxl, w.side2);
+        ++launches;
+      }
+      const long long nwx_st = wx_beside ? w.wx_n_int : w.wx_targets;
+      if (nwx_st) {
+        amr_wx_kernel<<<grid_for(nwx_st), 128, 0, st>>>(w.dev_lv, w.wx_targets_dev, nwx_st, w.wx_geo, w.lloc,
+                                                        lmass, w.wx_geo4);
         ++launches;
       }
       if (timed) cudaEventRecord(rec.k[3], st);
@@ -2430,6 +2452,7 @@ int tmgpu_gravity_amr_solve(tmgpu_gravity_amr* G, const double* mass, double* ph
           w.dev_lv, lmass);
       ++launches;
     }
+    if (wx_beside) cudaStreamWaitEvent(st, w.ev_wxl, 0);  // the leaf locals are complete
     if (nloc)
       amr_l2p_kernel<<<(unsigned)nloc, kL2pThreads, 0, st>>>(w.dev_lv, nloc, w.lo, w.slot_level, w.slot_node,
                                                      w.mass, w.u_geo, w.lloc, w.p2p_tab, w.slot_nbs, dphi, dg,
