@@ -66,6 +66,10 @@ struct GLv {
 // so L2P scales the neighbour masses instead and reads the geometry from the
 // constant bank (no shared-memory traffic)
 __constant__ double c_p2p_unit[27][4];
+// cell volume h^3 of a level-l leaf patch's cells (h = 1 / (8 * 2^l), a power of
+// two: exact however computed), for the masses m = rho * h^3
+constexpr int kMaxLevels = 48;
+__constant__ double c_level_dv[kMaxLevels];
 
 namespace {
 
@@ -89,8 +93,7 @@ __global__ void amr_mass_kernel(const double* __restrict__ arena, int V, long lo
     const long long s = t >> 9;
     const int c = (int)(t & 511);
     const int i = c & 7, j = (c >> 3) & 7, k = c >> 6;
-    const double h = 1.0 / (double)(8LL << slot_level[lo + s]);
-    const double dV = h * h * h;
+    const double dV = c_level_dv[slot_level[lo + s]];
     const double rho = V ? arena[s * V * 1728 + ((k + 2) * 12 + (j + 2)) * 12 + (i + 2)] : arena[s * cstride + c];
     mass[lo * 512 + t] = rho * dV;
   }
@@ -1968,6 +1971,11 @@ tmgpu_gravity_amr* tmgpu_gravity_amr_create(const int* leaves, long long nleaves
     delete G;
     return nullptr;
   }
+  if (P.nlevels > kMaxLevels) {
+    set_err(err, TMGPU_ERR_INVALID, "gravity_amr: more than 48 refinement levels");
+    delete G;
+    return nullptr;
+  }
   w.root_leaf = false;
   for (int ls : P.lv[0].leaf_slot) w.root_leaf |= ls >= 0;
   w.nslots = nleaves;
@@ -2117,6 +2125,12 @@ tmgpu_gravity_amr* tmgpu_gravity_amr_create(const int* leaves, long long nleaves
     p2p_table_kernel<<<((Dmax + 1) * 27 + 127) / 128, 128>>>(w.p2p_tab, Dmax);
     g_launches.fetch_add(1, std::memory_order_relaxed);
     e = cudaMemcpyToSymbol(c_p2p_unit, w.p2p_tab, 27 * 4 * sizeof(double), 0, cudaMemcpyDeviceToDevice);
+    double dv[kMaxLevels];
+    for (int l = 0; l < kMaxLevels; ++l) {
+      const double h = 1.0 / (double)(8LL << l);
+      dv[l] = h * h * h;
+    }
+    if (e == cudaSuccess) e = cudaMemcpyToSymbol(c_level_dv, dv, sizeof(dv));
     stencil_table_kernel<<<((Dmax + 1) * kOff3 + 127) / 128, 128>>>(w.tab, Dmax);
     g_launches.fetch_add(1, std::memory_order_relaxed);
     e = cudaMalloc(&w.tabp, (size_t)(Dmax + 1) * kTabDoubles * sizeof(double));
