@@ -563,7 +563,8 @@ __global__ void __launch_bounds__(kM2lThreads, 1) amr_m2l_fused_kernel(
 // remain — 5 of the 23 operations into a leaf target, bit for bit the full
 // term's result. The source window is then the 12^3 masses (from the compact
 // [slot][512] mass array, not the 80-byte moments), 16 KB instead of 161 KB,
-// so several CTAs share an SM. Thread mapping, source order and the two
+// so several CTAs share an SM (2 at 98 registers: faster per step than 4 at
+// 64, 3.92 vs 3.97 ms on C3). Thread mapping, source order and the two
 // partial sums are m2l_patch's.
 constexpr int kMonoWin = 2048;  // >= 4 * kWSub + 2 (window) and the 4 x 4 x 128 partial sums
 constexpr size_t kMonoSmem = (size_t)(kMonoWin + kOff3 * 4) * sizeof(double);  // 27,360 B
@@ -598,7 +599,7 @@ __device__ __forceinline__ void mono_row(const double* __restrict__ src, const d
   }
 }
 
-__global__ void __launch_bounds__(kM2lThreads, 4) amr_m2l_mono_kernel(
+__global__ void __launch_bounds__(kM2lThreads, 2) amr_m2l_mono_kernel(
     const long long* __restrict__ slots, const int* __restrict__ slot_level, const double* __restrict__ mass,
     const int* __restrict__ slot_nbs, const double* __restrict__ tab4p_all, double* __restrict__ lloc,
     long long lo) {
@@ -992,9 +993,9 @@ __device__ __forceinline__ void cell_pos(const GLv* __restrict__ Lv, int l, int 
 __device__ __forceinline__ void am_block_sums2(double m0, const double x0[3], const double g0[3], double m1,
                                                const double x1[3], const double g1[3], double* __restrict__ out16);
 
-constexpr int kL2pThreads = 256;  // two cells per thread: 4 CTAs per SM overlap their prologues
+constexpr int kL2pThreads = 256;  // two cells per thread: 5 CTAs per SM (48 registers) overlap their prologues
 
-__global__ void __launch_bounds__(kL2pThreads, 4) amr_l2p_kernel(const GLv* __restrict__ Lv, long long nslots,
+__global__ void __launch_bounds__(kL2pThreads, 5) amr_l2p_kernel(const GLv* __restrict__ Lv, long long nslots,
                                                       long long lo, const int* __restrict__ slot_level,
                                                       const int* __restrict__ slot_node,
                                                       const double* __restrict__ mass,
@@ -2400,7 +2401,7 @@ int tmgpu_gravity_amr_solve(tmgpu_gravity_amr* G, const double* mass, double* ph
     if (timed) cudaEventRecord(rec.ev[2], st);
     {
       // the fused kernel (1 CTA/SM) first on the solve's stream, the mono kernel
-      // (4 CTAs/SM, independent outputs) on a second stream: its CTAs take the
+      // (2 CTAs/SM, independent outputs) on a second stream: its CTAs take the
       // SMs the fused kernel's last waves leave idle; both join before W/X
       if (timed) {
         cudaEventRecord(rec.k[0], st);
